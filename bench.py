@@ -1,0 +1,335 @@
+"""Benchmark: batched generalized winding numbers on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
+
+One step = one pass of the hot path (cull -> intersect -> boundary ->
+reduce/re-shoot, plus the all-gather for N>1) over the rank's shard of the
+config's synthetic queries.  Default workload: config 2 (BASELINE.json
+configs[1]): closed 6-patch bicubic surface, 2^20 queries, fp64.
+
+Printed JSON (rank 0, one line):
+  value      queries/s over all ranks, queries resident in HBM, device-timed
+             (CUDA events, max over ranks), L2 flushed between steps
+  e2e        the same metric through the public API from pinned host memory
+             (H2D of the step's queries and D2H of w + status inside the timed
+             region)
+  roofline   K3 (the dominant kernel at config 2) algorithmic FP64 flops per
+             launch (device counters x per-stage flop constants, DESIGN.md
+             §Measurement) / its event-timed duration, vs the FP64 DFMA peak
+             measured live on this GPU
+  cpu_baseline  the CPU oracle port (oracle/, all host threads) on a bounded
+             sample of the same workload, rank 0 at N=1
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+# per-stage FP64 flop constants of K3 (FMA = 2 flops), counted from
+# csrc/gwn_intersect.cu
+FLOP_NODE = 454.0      # Krawczyk test: centre value, J(c), Y, 24 derivative bounds
+FLOP_SPLIT = 96.0      # de Casteljau halving of the 2 x 16 net (per split node)
+FLOP_NEWTON = 206.0    # Bernstein basis + value/partials of A,B + 2x2 solve
+FLOP_ROOT = 110.0      # C value/partials, normal, sign/tangency/grazing tests
+FLOP_SEGMENT = 40.0    # K4 per (query, net segment), shifted fan + complex product
+
+CONFIG_DESC = {
+    1: "config1: single open bicubic patch, 4096 queries U[-0.5,1.5]^3",
+    2: "config2: closed 6-patch bicubic cube-sphere, 2^20 queries U[-1.5,1.5]^3",
+    3: "config3: open 8x8 height-field sheet (64 patches), 2^22 queries (10% within 1e-3)",
+    4: "config4: 16 overlapping closed surfaces (1024 patches), 2^24 queries U[-3,3]^3",
+    5: "config5: 15876 patches (256 surfaces, 5% holes, 2% flipped duplicates), 2^26 queries",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--queries", type=int, default=0, help="override query count")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def mark(self):
+        return len(self.lines)
+
+    def stop(self, since: int = 0) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = [l.split(", ") for l in self.lines[since:] if l.count(",") >= 5] or \
+            [l.split(", ") for l in self.lines if l.count(",") >= 5]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[2:6]):
+                if v.strip().lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def cpu_baseline(spec, seconds: float) -> dict:
+    """Time the CPU oracle port (all host threads) on a bounded sample."""
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    n = 1024
+    q = spec.queries
+    O.scene_eval(spec.ctrl, q[:64])                     # warm caches / thread pool
+    while True:
+        t = time.perf_counter()
+        O.scene_eval(spec.ctrl, q[:n], qidx=np.arange(n), nthreads=cores)
+        dt = time.perf_counter() - t
+        if dt >= seconds / 4 or n >= len(q):
+            break
+        n = min(len(q), n * 4)
+    return {"value": n / dt, "unit": "queries/s", "cores": cores, "kind": "port",
+            "sample": f"first {n} queries of {CONFIG_DESC[spec.config].split(':')[0]} "
+                      f"({dt:.1f} s, oracle/gwn_oracle.c, {cores} threads)"}
+
+
+def run_reference(args, spec, rank, world):
+    """--impl reference: the CPU oracle port on the host cores (rank 0 only)."""
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    # bounded per-step sample: ~2 s of CPU work per step
+    n = 2048
+    while True:
+        t = time.perf_counter()
+        O.scene_eval(spec.ctrl, spec.queries[:n], qidx=np.arange(n), nthreads=cores)
+        dt = time.perf_counter() - t
+        if dt > 1.0 or n >= len(spec.queries):
+            break
+        n = min(len(spec.queries), n * 2)
+    for _ in range(args.warmup):
+        O.scene_eval(spec.ctrl, spec.queries[:n], qidx=np.arange(n), nthreads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.scene_eval(spec.ctrl, spec.queries[:n], qidx=np.arange(n), nthreads=cores)
+    el = time.perf_counter() - t0
+    v = n * args.steps / el
+    line = {
+        "impl": "reference", "metric": "winding-number queries/sec", "value": v,
+        "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8(d))",
+        "config": {"workload": CONFIG_DESC[spec.config], "n_patches": spec.n_patches,
+                   "queries": int(len(spec.queries)), "sample_per_step": n},
+        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
+                         "sample": f"first {n} queries per step, oracle/gwn_oracle.c"},
+        "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2408_04466_b200 import scenes
+    spec = scenes.make(args.config, args.queries or None)
+    if args.impl == "reference":
+        return run_reference(args, spec, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2408_04466_b200 as G
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_total = len(spec.queries)
+    from paper_2408_04466_b200.distributed import shard_bounds
+    s0, s1, per = shard_bounds(n_total, rank, world)
+    local_q = np.ascontiguousarray(spec.queries[s0:s1])
+    nq = len(local_q)
+    sc = G.Scene(spec.ctrl, device=local)
+    stream = torch.cuda.current_stream(dev)
+    q_dev = torch.from_numpy(local_q).to(dev)
+    w_dev = torch.empty(nq, dtype=torch.float64, device=dev)
+    st_dev = torch.empty(nq, dtype=torch.int8, device=dev)
+    q_pin = torch.from_numpy(local_q).pin_memory()
+    w_pin = torch.empty(nq, dtype=torch.float64).pin_memory()
+    st_pin = torch.empty(nq, dtype=torch.int8).pin_memory()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    w_all = torch.empty(per * world, dtype=torch.float64, device=dev)
+    st_all = torch.empty(per * world, dtype=torch.int8, device=dev)
+    w_pad = torch.zeros(per, dtype=torch.float64, device=dev)
+    st_pad = torch.zeros(per, dtype=torch.int8, device=dev)
+
+    def step_device():
+        G.winding_numbers(sc, q_dev, index_base=s0, out=(w_dev, st_dev),
+                          stream=stream.cuda_stream)
+        if world > 1:
+            w_pad[:nq].copy_(w_dev)
+            st_pad[:nq].copy_(st_dev)
+            dist.all_gather_into_tensor(w_all, w_pad)
+            dist.all_gather_into_tensor(st_all, st_pad)
+
+    def step_e2e():
+        G.winding_numbers(sc, q_pin, index_base=s0, out=(w_pin, st_pin),
+                          stream=stream.cuda_stream)
+        if world > 1:
+            w_pad[:nq].copy_(w_pin, non_blocking=True)
+            st_pad[:nq].copy_(st_pin, non_blocking=True)
+            dist.all_gather_into_tensor(w_all, w_pad)
+            dist.all_gather_into_tensor(st_all, st_pad)
+
+    def timed(fn, k):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(k)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        launches = 0
+        for a, b in evs:
+            flush.zero_()                      # L2 flush between steps (untimed)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            launches += int(sc.stats()["kernel_launches"])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = sum(a.elapsed_time(b) for a, b in evs)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), launches
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(max(3, args.warmup)):
+        step_device()
+    torch.cuda.synchronize()
+    mark = clocks.mark()
+    ms_dev, launches = timed(step_device, args.steps)
+    clock_info = clocks.stop(mark)
+    for _ in range(2):
+        step_e2e()
+    ms_e2e, _ = timed(step_e2e, args.steps)
+
+    # ---- roofline of the dominant kernel, measured live (events on `stream`)
+    sc.set_timing(True)
+    kk = 3
+    agg = {}
+    for _ in range(kk):
+        flush.zero_()
+        G.winding_numbers(sc, q_dev, index_base=s0, out=(w_dev, st_dev),
+                          stream=stream.cuda_stream)
+        for k, v in sc.stats().items():
+            agg[k] = agg.get(k, 0) + v
+    sc.set_timing(False)
+    stt = {k: v / kk for k, v in agg.items()}
+    k3_flops = (stt["nodes"] * (FLOP_NODE + 0.5 * FLOP_SPLIT) + stt["newton_iters"] * FLOP_NEWTON
+                + stt["roots"] * FLOP_ROOT)
+    k4_flops = stt["boundary_segments"] * FLOP_SEGMENT
+    peak_tf, _ = G.fp64_peak(local)
+    if k4_flops > k3_flops and stt["ms_boundary"] > 0:
+        kname, kflops, kms = "k_boundary (K4)", k4_flops, stt["ms_boundary"]
+    else:
+        kname, kflops, kms = "k_intersect (K3)", k3_flops, stt["ms_intersect"]
+    achieved = kflops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
+
+    value = n_total / (ms_dev * 1e-3 / args.steps)
+    e2e = n_total / (ms_e2e * 1e-3 / args.steps)
+    out = None
+    if rank == 0:
+        out = {
+            "metric": "winding-number queries/sec", "value": value, "unit": "queries/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": ms_dev / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generators, SURVEY.md §8(d); no public dataset)",
+            "config": {"workload": CONFIG_DESC[args.config], "n_patches": spec.n_patches,
+                       "queries": n_total, "queries_per_gpu": per,
+                       "net_boundary_segments": sc.n_net_segments,
+                       "parallelism": f"dp{world} (queries sharded, scene replicated, "
+                                      "one all-gather)",
+                       "l2": "flushed between steps (256 MiB write)"},
+            "nominal_pairs_per_s": value * spec.n_patches,
+            "candidate_pairs_per_s": stt["candidates"] / (ms_dev * 1e-3 / args.steps) * world,
+            "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": int(nq * 24),
+                    "d2h_bytes_per_step": int(nq * 9)},
+            "gpu_launches": launches,
+            "roofline": {"bound": "fp64", "kernel": kname, "achieved": achieved,
+                         "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tf if peak_tf else None, "traffic": None,
+                         "peak_source": "FP64 DFMA-chain microbenchmark run live on this GPU "
+                                        "(MEASURED_PEAKS.json has no FP64 entry)",
+                         "kernel_ms": kms, "kernel_share_of_step":
+                             kms / (ms_dev / args.steps) if ms_dev else None},
+            "stage_ms": {"cull": stt["ms_cull"], "intersect": stt["ms_intersect"],
+                         "boundary": stt["ms_boundary"], "finalize": stt["ms_other"]},
+            "counters": {k: stt[k] for k in ("candidates", "nodes", "newton_iters", "roots",
+                                             "boundary_segments", "retried", "rounds")},
+            "clocks": clock_info,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(spec, args.cpu_seconds)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

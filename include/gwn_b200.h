@@ -1,0 +1,150 @@
+/* include/gwn_b200.h -- C ABI of libgwn_b200.so (B200 / sm_100a).
+ *
+ * Batched generalized winding numbers of query points against bicubic
+ * Bezier patches (arXiv 2408.04466).  Plain pointers and sizes only; no
+ * torch types.  Each entry point replaces a reference interface:
+ *
+ *   gwn_scene_create   SPEC.md:355-365 `Scene` construction (patches +
+ *                      aggregated boundary loops, surfaces.py:611-626) and the
+ *                      per-patch `aabb()` of surfaces.py:562-564 / 636
+ *   gwn_eval           SPEC.md:371-380 engine.winding_number, batched; the
+ *                      per-query sum over patch.all_hits (surfaces.py:634-701)
+ *                      and the boundary term (_kernels.py:723-798), with the
+ *                      jitter/re-shoot policy of SPEC.md:320,373-375,427
+ *   gwn_all_hits       patch.all_hits(ray) (surfaces.py:587-589 protocol,
+ *                      body _multistart_ray_roots surfaces.py:634-701)
+ *   gwn_single_loop_batch
+ *                      _kernels.single_loop_batch (_kernels.py:801-823): the
+ *                      kernel dispatch layer's ray-reuse boundary kernel
+ *   gwn_last_error     error text; negative return codes map to the
+ *                      GwnError hierarchy (errors.py:9-90) in the wrapper
+ *
+ * Threading: a scene is immutable after creation; gwn_eval is
+ * reentrant on distinct streams (workspace comes from the stream-ordered
+ * allocator).  gwn_last_error is thread-local.
+ */
+#ifndef GWN_B200_H
+#define GWN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GWN_ABI_VERSION 1
+
+/* return codes (negative = error) */
+#define GWN_OK 0
+#define GWN_E_INVALID -1      /* bad argument            -> ValueError / SceneError */
+#define GWN_E_CUDA -2         /* CUDA runtime failure    -> GwnError */
+#define GWN_E_NODEVICE -3     /* no usable sm_100 device -> GwnError */
+#define GWN_E_OOM -4          /* device allocation       -> GwnError */
+
+/* per-query status (int8) written by gwn_eval */
+#define GWN_STATUS_OK 0
+#define GWN_STATUS_ON_SURFACE 1   /* OnSurface: jittered by jitter_scale*diag */
+#define GWN_STATUS_EXHAUSTED 2    /* SeedExhausted: re-shoot budget spent     */
+#define GWN_STATUS_DEGENERATE 3   /* DegenerateProjection: jittered           */
+
+/* gwn_eval flags */
+#define GWN_HOST_BUFFERS 1        /* queries / outputs are host pointers */
+
+/* Mirrors reference EpsilonConfig (config.py:15-38) + engine knobs. */
+typedef struct gwn_params {
+  double residual;          /* config.py:29  accepted |f(u,v)-O-tD|      1e-10 */
+  double dedup;             /* config.py:28  root merge distance         1e-9  */
+  double tangent;           /* config.py:25  tangent_parametric          1e-12 */
+  double edge_graze;        /* config.py:27  grazing distance            1e-10 */
+  double degenerate;        /* config.py:18  projection degeneracy       1e-12 */
+  double jitter_scale;      /* config.py:33  jitter, x scene diagonal    1e-7  */
+  double domain_tol;        /* surfaces.py:668 domain_contains tolerance 1e-9  */
+  double t_tol;             /* surfaces.py:670 t >= -t_tol               1e-12 */
+  double on_surface_t;      /* |t| of a hit that means "on the surface" 1e-9  */
+  double band_factor;       /* polyline/curve band safety factor         2.0   */
+  int32_t samples_per_edge; /* surfaces.py:611 boundary samples          200   */
+  int32_t max_rounds;       /* SPEC.md:320 ray re-shoot budget           32    */
+  int32_t max_jitters;      /* SPEC.md:375 jitter budget                 3     */
+  int32_t chunk_queries;    /* queries per internal chunk (0 = auto)           */
+  uint64_t dir_seed;        /* deterministic direction sequence seed           */
+} gwn_params;
+
+typedef struct gwn_scene gwn_scene;
+
+typedef struct gwn_scene_info {
+  int64_t n_patches;
+  int64_t n_net_edges;      /* boundary edge curves left after cancellation */
+  int64_t n_net_segments;   /* polyline segments the boundary term sums     */
+  double bbox_min[3];
+  double bbox_max[3];
+  double diag;
+  int32_t device;
+  int32_t sm_count;
+} gwn_scene_info;
+
+/* Device-side counters of the last gwn_eval on a scene (for the roofline
+ * and the divergence analysis). */
+typedef struct gwn_stats {
+  int64_t queries;
+  int64_t rounds;           /* direction rounds run (all chunks)           */
+  int64_t retried;          /* query re-evaluations beyond round 0         */
+  int64_t candidates;       /* (query, patch) pairs surviving the cull     */
+  int64_t nodes;            /* subdivision nodes tested in the intersector */
+  int64_t newton_iters;
+  int64_t roots;
+  int64_t boundary_segments;/* (query, net segment) pairs evaluated        */
+  int64_t kernel_launches;
+  double ms_cull, ms_intersect, ms_boundary, ms_other;  /* event timings, 0 if not timed */
+} gwn_stats;
+
+int gwn_abi_version(void);
+const char* gwn_last_error(void);
+void gwn_params_default(gwn_params* p);
+
+/* Copy n_patches bicubic control nets ((P,4,4,3) f64, i = u index) to
+ * `device`, build the net boundary and the round-0 patch hierarchy. */
+int gwn_scene_create(const double* ctrl, int64_t n_patches, const gwn_params* prm,
+                     int device, gwn_scene** out);
+int gwn_scene_destroy(gwn_scene* scene);
+int gwn_scene_info_get(const gwn_scene* scene, gwn_scene_info* out);
+
+/* w[i] = generalized winding number of queries[i] ((n,3) f64), status[i] as
+ * above.  `index_base` is the global id of queries[0] (jitter hash; keeps
+ * sharded results identical to unsharded).  stream = cudaStream_t or NULL. */
+int gwn_eval(gwn_scene* scene, const double* queries, int64_t n, int64_t index_base,
+             double* w_out, int8_t* status_out, int32_t flags, void* stream);
+
+/* Stats of the last gwn_eval on this scene; `timed` != 0 on the next eval
+ * records per-kernel CUDA-event times (adds event syncs). */
+int gwn_stats_get(const gwn_scene* scene, gwn_stats* out);
+int gwn_set_timing(gwn_scene* scene, int32_t timed);
+
+/* All hits of one ray with one patch of the scene (host buffers). Records:
+ * t, u, v, sign, tangency, grazing.  Returns count (may exceed cap: only cap
+ * written) or a negative error. */
+int gwn_all_hits(gwn_scene* scene, int64_t patch, const double origin[3],
+                 const double direction[3], double* t_out, double* uv_out,
+                 int32_t* sign_out, int8_t* tangency_out, int8_t* grazing_out,
+                 int32_t cap);
+
+/* _kernels.single_loop_batch on the GPU: closed loop (B,3), ray, cached hit
+ * ts/signs (H), query ts (K) -> w (K), ok (K).  Host buffers. */
+int gwn_single_loop_batch(const double* loop_pts, int64_t B, const double origin[3],
+                          const double direction[3], const double* hit_ts,
+                          const int64_t* hit_signs, int64_t H, const double* query_ts,
+                          int64_t K, double on_tol, double t_eps, double* w_out,
+                          int8_t* ok_out, int device);
+
+/* Host-side helpers shared with the oracle contract (no device needed). */
+void gwn_direction(uint64_t seed, int32_t round, double d[3]);
+void gwn_jitter_dir(uint64_t seed, int64_t qidx, int32_t attempt, double v[3]);
+int64_t gwn_net_boundary(const double* ctrl, int64_t n_patches, double* out_ctrl,
+                         int32_t* out_weight);
+
+/* FP64 peak microbenchmark (DFMA chains on every SM), TFLOP/s. */
+int gwn_fp64_peak(int device, double* tflops, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

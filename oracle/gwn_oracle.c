@@ -30,12 +30,12 @@
 /* ------------------------------------------------------------------------- */
 
 void or_params_default(or_params* p) {
-  p->residual = 1e-10;     /* config.py:31 */
-  p->dedup = 1e-9;         /* config.py:30 */
-  p->tangent = 1e-12;      /* config.py:26 */
-  p->edge_graze = 1e-10;   /* config.py:28 */
-  p->degenerate = 1e-12;   /* config.py:19 */
-  p->jitter_scale = 1e-7;  /* config.py:35 */
+  p->residual = 1e-10;     /* config.py:29 */
+  p->dedup = 1e-9;         /* config.py:28 */
+  p->tangent = 1e-12;      /* config.py:25 */
+  p->edge_graze = 1e-10;   /* config.py:27 */
+  p->degenerate = 1e-12;   /* config.py:18 */
+  p->jitter_scale = 1e-7;  /* config.py:33 */
   p->domain_tol = 1e-9;    /* surfaces.py:668 */
   p->t_tol = 1e-12;        /* surfaces.py:670 */
   p->on_surface_t = 1e-9;  /* SPEC.md:383 "within 1e-9 (else perturbed)" */
@@ -503,15 +503,23 @@ static inline double fan_segment(const double* xa, const double* xb, const doubl
     return 0.0;
   }
   for (int k = 0; k < 3; ++k) { a[k] /= la; b[k] /= lb; }
-  double cr[3];
-  cross3(a, b, cr);
-  double num = dot3(c, cr);
-  double ab = dot3(a, b);
-  double den = 1.0 + ab + dot3(b, c) + dot3(c, a);
+  /* van Oosterom-Strackee for the unit triangle (c, a, b), c = -d, in the
+   * exactly equivalent shifted form u = a - d, v = b - d:
+   *   1 + a.b + b.c + c.a = u.v,   c.(a x b) = -d.(u x v)
+   * which stays accurate when d points at the segment (u, v small). */
+  double d[3] = {-c[0], -c[1], -c[2]};
+  double u[3] = {a[0] - d[0], a[1] - d[1], a[2] - d[2]};
+  double v[3] = {b[0] - d[0], b[1] - d[1], b[2] - d[2]};
+  double uv[3];
+  cross3(u, v, uv);
+  double num = -dot3(d, uv);
+  double den = dot3(u, v);
   if (den < 0.0 && band_h > 0.0) {
     double seg[3] = {xb[0] - xa[0], xb[1] - xa[1], xb[2] - xa[2]};
     double dist = fmin(la, lb) - norm3(seg);
-    double s2 = (1.0 - ab) * (1.0 + ab);
+    double ab[3];
+    cross3(a, b, ab);
+    double s2 = dot3(ab, ab);
     if (dist <= 0.0) {
       *flags |= 2;
     } else {

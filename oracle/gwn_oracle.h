@@ -26,12 +26,12 @@ extern "C" {
  * engine knobs of SPEC.md:371-380,427 and the boundary sampling of
  * surfaces.py:611 (samples_per_edge). */
 typedef struct or_params {
-  double residual;        /* config.py:31  1e-10 */
-  double dedup;           /* config.py:30  1e-9  */
-  double tangent;         /* config.py:26  1e-12 (tangent_parametric) */
-  double edge_graze;      /* config.py:28  1e-10 */
-  double degenerate;      /* config.py:19  1e-12 */
-  double jitter_scale;    /* config.py:35  1e-7  */
+  double residual;        /* config.py:29  1e-10 */
+  double dedup;           /* config.py:28  1e-9  */
+  double tangent;         /* config.py:25  1e-12 (tangent_parametric) */
+  double edge_graze;      /* config.py:27  1e-10 */
+  double degenerate;      /* config.py:18  1e-12 */
+  double jitter_scale;    /* config.py:33  1e-7  */
   double domain_tol;      /* surfaces.py:668  1e-9 */
   double t_tol;           /* surfaces.py:670  1e-12 */
   double on_surface_t;    /* |t| of a hit below which the query is on the surface */

@@ -1,0 +1,224 @@
+// gwn_boundary.cu -- K4: per-query boundary term over the net boundary.
+//
+// The reference evaluates the boundary correction per query by projecting
+// the loop to the unit sphere, testing it for self-crossings, summing
+// Gauss-Bonnet turning angles and locating the ray direction relative to the
+// loop (_kernels.py:723-798); the generic case needs the SPEC arrangement
+// (SPEC.md:240-336).  Both equal the arrangement-free fan sum
+//     B(p, d) = (1/4pi) sum_e 2 atan2(c.(a^ x b^), 1 + a^.b^ + b^.c + c.a^),
+// c = -d, over the loop segments (a, b) (pinned against the
+// fixed single_loop_batch to 2.3e-13 by tests/test_oracle_golden.py).
+//
+// B200 formulation.  With unit vectors a^, b^ and d = -c the van Oosterom
+// terms are rewritten exactly in the shifted variables u = a^ - d, v = b^ - d:
+//     1 + a^.b^ + b^.c + c.a^ = u.v,     c.(a^ x b^) = -(d x u).v
+// which keeps full relative accuracy when d points at a segment (u, v small;
+// the plain form cancels catastrophically there -- measured 7e-9 drift on
+// config 5).  The per-segment atan2 is replaced by a running complex product
+// Z *= (u.v + i num) with an exact branch-cut counter from sign bits and a
+// power-of-two renormalisation every 8 segments; one atan2 per query.
+// Per vertex: 3 DADD, |r|^2, rsqrt, 3 DFMA for u, d x u; per segment: 2 dot
+// products + 4 for the complex product.  Boundary vertices (x,y,z) are
+// staged in shared-memory tiles and read as warp-wide broadcasts.
+#include "gwn_internal.h"
+
+namespace gwn {
+
+constexpr int kTileV = 2000;   // vertices per shared-memory tile (3 x 2000 x 8 B = 48 KB)
+constexpr int kBlockQ = 256;   // queries (threads) per block
+
+struct SegState {
+  double Zr, Zi;
+  int wraps;
+};
+
+__device__ __forceinline__ bool signbit_hi(double x) { return __double2hiint(x) < 0; }
+
+// multiply Z by (den + i num) with exact branch-cut bookkeeping
+__device__ __forceinline__ void cmul_track(SegState& s, double den, double num) {
+  double zr = s.Zr * den - s.Zi * num;
+  double zi = s.Zr * num + s.Zi * den;
+  bool a = signbit_hi(s.Zi), b = signbit_hi(num), c = signbit_hi(zi);
+  s.wraps += (!a && !b && c) ? 1 : 0;
+  s.wraps -= (a && b && !c) ? 1 : 0;
+  s.Zr = zr;
+  s.Zi = zi;
+}
+
+__device__ __forceinline__ void renorm(SegState& s) {
+  double m = fmax(fabs(s.Zr), fabs(s.Zi));
+  int e = ((__double2hiint(m) >> 20) & 0x7ff);
+  if (e == 0 || e == 0x7ff) return;  // zero/denormal/non-finite: degenerate, flagged elsewhere
+  double sc = __hiloint2double((2046 - e) << 20, 0);  // 2^(1023-e), exact
+  s.Zr *= sc;
+  s.Zi *= sc;
+}
+
+// Per-vertex quantities of the shifted fan formula.
+struct Vtx {
+  double ux, uy, uz;   // a^ - d
+  double gx, gy, gz;   // d x u
+  double rx, ry, rz;   // x - p (band test only)
+  double l;            // |x - p|
+  bool ok;
+};
+
+__device__ __forceinline__ Vtx make_vtx(double x, double y, double z, double px, double py,
+                                        double pz, double dx, double dy, double dz, double deg) {
+  Vtx v;
+  v.rx = x - px; v.ry = y - py; v.rz = z - pz;
+  const double l2 = v.rx * v.rx + v.ry * v.ry + v.rz * v.rz;
+  const double il = rsqrt(l2);
+  v.l = l2 * il;
+  v.ok = v.l >= deg;
+  v.ux = fma(v.rx, il, -dx);
+  v.uy = fma(v.ry, il, -dy);
+  v.uz = fma(v.rz, il, -dz);
+  v.gx = dy * v.uz - dz * v.uy;
+  v.gy = dz * v.ux - dx * v.uz;
+  v.gz = dx * v.uy - dy * v.ux;
+  return v;
+}
+
+// One segment (a, b): accumulate and run the (rare) band test.
+__device__ __forceinline__ void fan_segment(SegState& st, const Vtx& a, const Vtx& b, double dx,
+                                            double dy, double dz, double h, double band_factor,
+                                            int& flags) {
+  const double den = a.ux * b.ux + a.uy * b.uy + a.uz * b.uz;
+  const double num = -(a.gx * b.ux + a.gy * b.uy + a.gz * b.uz);
+  const bool ok = a.ok && b.ok;
+  if (den < 0.0 && ok && h > 0.0) {
+    // polyline/curve band: d within band_factor * h / dist of the arc
+    const double sgx = b.rx - a.rx, sgy = b.ry - a.ry, sgz = b.rz - a.rz;
+    const double L = sqrt(sgx * sgx + sgy * sgy + sgz * sgz);
+    const double dist = fmin(a.l, b.l) - L;
+    const double ax = a.ux + dx, ay = a.uy + dy, az = a.uz + dz;
+    const double bx = b.ux + dx, by = b.uy + dy, bz = b.uz + dz;
+    const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
+    const double s2 = cx * cx + cy * cy + cz * cz;
+    if (dist <= 0.0) {
+      flags |= FLAG_BAND;
+    } else {
+      const double th = band_factor * h / dist;
+      if (num * num <= th * th * s2) flags |= FLAG_BAND;
+    }
+  }
+  cmul_track(st, ok ? den : 1.0, ok ? num : 0.0);
+}
+
+__global__ void __launch_bounds__(kBlockQ)
+k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
+           const double* __restrict__ verts, int64_t V, int S,
+           const double* __restrict__ band_h, Frame f, DevParams prm,
+           double* __restrict__ bterm, int32_t* __restrict__ flag_acc,
+           unsigned long long* __restrict__ counters) {
+  __shared__ double sx[kTileV], sy[kTileV], sz[kTileV];
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = s < m;
+  const int32_t q = live ? (active ? active[s] : s) : 0;
+  const double px = live ? pos[3 * (int64_t)q] : 0.0;
+  const double py = live ? pos[3 * (int64_t)q + 1] : 0.0;
+  const double pz = live ? pos[3 * (int64_t)q + 2] : 0.0;
+  const double dx = f.d[0], dy = f.d[1], dz = f.d[2];
+  const double deg = prm.degenerate;
+  SegState st = {1.0, 0.0, 0};
+  int flags = 0;
+  Vtx va;
+  va.ok = false;
+  int nseg = 0;
+  for (int64_t t0 = 0; t0 < V; t0 += kTileV) {
+    const int nt = (int)min((int64_t)kTileV, V - t0);
+    __syncthreads();
+    for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+      int64_t g = t0 + k;
+      sx[k] = verts[g];
+      sy[k] = verts[V + g];
+      sz[k] = verts[2 * V + g];
+    }
+    __syncthreads();
+    int kin = (int)(t0 % S);  // index within its edge of the tile's first vertex
+    for (int k = 0; k < nt; ++k) {
+      Vtx vb = make_vtx(sx[k], sy[k], sz[k], px, py, pz, dx, dy, dz, deg);
+      if (!vb.ok) flags |= FLAG_DEGEN;
+      if (kin != 0) {  // segment (k-1, k) lies on one edge
+        const double h = (va.ok && vb.ok) ? __ldg(band_h + (t0 + k) / S) : 0.0;
+        fan_segment(st, va, vb, dx, dy, dz, h, prm.band_factor, flags);
+        ++nseg;
+        if ((nseg & 7) == 0) renorm(st);
+      }
+      va = vb;
+      if (++kin == S) kin = 0;
+    }
+  }
+  if (live) {
+    const double ang = atan2(st.Zi, st.Zr) + 6.283185307179586476925 * (double)st.wraps;
+    bterm[s] = ang * 0.15915494309189533576888;  // (2 ang) / (4 pi)
+    if (flags) atomicOr(&flag_acc[s], flags);
+  }
+  if (threadIdx.x == 0) {
+    int32_t nq = min((int32_t)blockDim.x, m - (int32_t)(blockIdx.x * blockDim.x));
+    int64_t segs = V - V / S;
+    atomicAdd(&counters[CNT_SEGMENTS], (unsigned long long)(segs * nq));
+  }
+}
+
+cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
+                            const int32_t* active, const double* pos, double* bterm,
+                            int32_t* flags, unsigned long long* counters, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  int64_t V = sc->n_edges * sc->S;
+  if (V == 0) return cudaMemsetAsync(bterm, 0, sizeof(double) * m, st);
+  k_boundary<<<(m + kBlockQ - 1) / kBlockQ, kBlockQ, 0, st>>>(
+      m, active, pos, sc->verts, V, sc->S, sc->band_h, rd.f, sc->dprm, bterm, flags, counters);
+  return cudaGetLastError();
+}
+
+// _kernels.single_loop_batch (_kernels.py:801-823) on the GPU: one closed loop,
+// queries p_k = o + t_k d on one ray, chi from the cached hits with t_h > t_k
+// (:778-788).  ok = 0 only for a hit clash |t_h - t_k| <= t_eps or a
+// degenerate projection; the fan formula needs no simple-loop restriction.
+__global__ void k_single_loop(const double* __restrict__ loop, int64_t B, double ox, double oy,
+                              double oz, double dx, double dy, double dz,
+                              const double* __restrict__ hit_ts,
+                              const int64_t* __restrict__ hit_signs, int64_t H,
+                              const double* __restrict__ qts, int64_t K, double t_eps,
+                              double deg, double* __restrict__ w, int8_t* __restrict__ ok) {
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const double t = qts[k];
+  const double px = ox + t * dx, py = oy + t * dy, pz = oz + t * dz;
+  long long chi = 0;
+  bool clash = false;
+  for (int64_t h = 0; h < H; ++h) {
+    if (fabs(hit_ts[h] - t) <= t_eps) clash = true;
+    if (hit_ts[h] > t) chi += hit_signs[h];
+  }
+  SegState st = {1.0, 0.0, 0};
+  bool bad = false;
+  Vtx va = make_vtx(loop[3 * (B - 1)], loop[3 * (B - 1) + 1], loop[3 * (B - 1) + 2], px, py, pz,
+                    dx, dy, dz, deg);
+  int flags = 0;
+  for (int64_t i = 0; i < B; ++i) {
+    Vtx vb = make_vtx(loop[3 * i], loop[3 * i + 1], loop[3 * i + 2], px, py, pz, dx, dy, dz, deg);
+    if (!va.ok || !vb.ok) bad = true;
+    fan_segment(st, va, vb, dx, dy, dz, 0.0, 0.0, flags);
+    if ((i & 7) == 7) renorm(st);
+    va = vb;
+  }
+  const double ang = atan2(st.Zi, st.Zr) + 6.283185307179586476925 * (double)st.wraps;
+  w[k] = (double)chi + ang * 0.15915494309189533576888;
+  ok[k] = (clash || bad) ? 0 : 1;
+}
+
+cudaError_t launch_single_loop(const double* loop, int64_t B, const double* o, const double* d,
+                               const double* hit_ts, const int64_t* hit_signs, int64_t H,
+                               const double* qts, int64_t K, double t_eps, double deg, double* w,
+                               int8_t* ok, cudaStream_t st) {
+  if (K <= 0) return cudaSuccess;
+  k_single_loop<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(loop, B, o[0], o[1], o[2], d[0],
+                                                             d[1], d[2], hit_ts, hit_signs, H,
+                                                             qts, K, t_eps, deg, w, ok);
+  return cudaGetLastError();
+}
+
+}  // namespace gwn

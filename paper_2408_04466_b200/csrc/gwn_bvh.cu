@@ -1,0 +1,229 @@
+// gwn_bvh.cu -- K1: per-direction patch projection and on-device 2-D LBVH.
+//
+// Every query of round r casts its ray along the same direction d_r, so the
+// ray-patch cull is a 2-D point query in the plane normal to d_r: a ray from
+// p hits patch k's control hull only if (p.e1, p.e2) lies in the projected
+// hull's box and the patch extends past p along d_r.  We therefore project
+// the control nets once per round (replacing the per-(ray,patch) Aabb work of
+// surfaces.py:636-639 / geometry.py:198-219) and build a Karras LBVH over the
+// projected boxes: 30-bit Morton codes, CUB radix sort, one thread per
+// internal node, bottom-up refit with atomic arrival counters.
+#include <cub/cub.cuh>
+
+#include "gwn_internal.h"
+
+namespace gwn {
+
+__global__ void k_project(const double* __restrict__ ctrl, int64_t P, Frame f,
+                          double* __restrict__ proj, double* __restrict__ leafbox,
+                          uint32_t* __restrict__ keys, int32_t* __restrict__ ids, double amin,
+                          double ainv, double bmin, double binv) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const double* X = ctrl + 48 * p;
+  double* out = proj + 48 * p;
+  double alo = INFINITY, ahi = -INFINITY, blo = INFINITY, bhi = -INFINITY, chi = -INFINITY,
+         mag = 0.0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    double x = X[3 * k], y = X[3 * k + 1], z = X[3 * k + 2];
+    double A = x * f.e1[0] + y * f.e1[1] + z * f.e1[2];
+    double B = x * f.e2[0] + y * f.e2[1] + z * f.e2[2];
+    double C = x * f.d[0] + y * f.d[1] + z * f.d[2];
+    out[k] = A;
+    out[16 + k] = B;
+    out[32 + k] = C;
+    alo = fmin(alo, A); ahi = fmax(ahi, A);
+    blo = fmin(blo, B); bhi = fmax(bhi, B);
+    chi = fmax(chi, C);
+    mag = fmax(mag, fmax(fabs(x), fmax(fabs(y), fabs(z))));
+  }
+  // conservative expansion: projection rounding plus the 1e-9 parametric
+  // acceptance band of surfaces.py:668 (roots just outside the domain)
+  double ext = fmax(ahi - alo, bhi - blo);
+  double eps = 1e-12 * (1.0 + mag) + 3e-9 * ext;
+  double* lb = leafbox + 5 * p;
+  lb[0] = alo - eps; lb[1] = ahi + eps; lb[2] = blo - eps; lb[3] = bhi + eps; lb[4] = chi + eps;
+  // Morton code of the box centre in the scene's projected bounds
+  double ca = (0.5 * (alo + ahi) - amin) * ainv, cb = (0.5 * (blo + bhi) - bmin) * binv;
+  uint32_t ia = (uint32_t)fmin(fmax(ca * 32767.0, 0.0), 32767.0);
+  uint32_t ib = (uint32_t)fmin(fmax(cb * 32767.0, 0.0), 32767.0);
+  uint32_t code = 0;
+  for (int bit = 0; bit < 15; ++bit)
+    code |= (((ia >> bit) & 1u) << (2 * bit)) | (((ib >> bit) & 1u) << (2 * bit + 1));
+  keys[p] = code;
+  ids[p] = (int32_t)p;
+}
+
+__device__ __forceinline__ int lbvh_delta(const uint32_t* keys, int n, int i, int j) {
+  if (j < 0 || j >= n) return -1;
+  uint32_t a = keys[i], b = keys[j];
+  if (a == b) return 32 + __clz((uint32_t)(i ^ j));
+  return __clz(a ^ b);
+}
+
+// Karras 2012: internal node i covers a key range; children are internal
+// nodes (>= 0) or leaves (~index in sorted order).
+__global__ void k_karras(const uint32_t* __restrict__ keys, int n, int32_t* __restrict__ left,
+                         int32_t* __restrict__ right, int32_t* __restrict__ parent_int,
+                         int32_t* __restrict__ parent_leaf) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  int d = (lbvh_delta(keys, n, i, i + 1) - lbvh_delta(keys, n, i, i - 1)) >= 0 ? 1 : -1;
+  int dmin = lbvh_delta(keys, n, i, i - d);
+  int lmax = 2;
+  while (lbvh_delta(keys, n, i, i + lmax * d) > dmin) lmax <<= 1;
+  int l = 0;
+  for (int t = lmax >> 1; t >= 1; t >>= 1)
+    if (lbvh_delta(keys, n, i, i + (l + t) * d) > dmin) l += t;
+  int j = i + l * d;
+  int dnode = lbvh_delta(keys, n, i, j);
+  int s = 0;
+  for (int t = (l + 1) >> 1;; t = (t + 1) >> 1) {
+    if (lbvh_delta(keys, n, i, i + (s + t) * d) > dnode) s += t;
+    if (t == 1) break;
+  }
+  int gamma = i + s * d + (d < 0 ? -1 : 0);
+  int lo = min(i, j), hi = max(i, j);
+  int L = (lo == gamma) ? ~gamma : gamma;
+  int R = (hi == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+  left[i] = L;
+  right[i] = R;
+  if (L >= 0) parent_int[L] = i; else parent_leaf[~L] = i;
+  if (R >= 0) parent_int[R] = i; else parent_leaf[~R] = i;
+}
+
+// Bottom-up refit: the second thread to reach a node writes both child boxes.
+__global__ void k_refit(int n, const int32_t* __restrict__ sorted_ids,
+                        const double* __restrict__ leafbox, const int32_t* __restrict__ left,
+                        const int32_t* __restrict__ right, const int32_t* __restrict__ parent_int,
+                        const int32_t* __restrict__ parent_leaf, int32_t* __restrict__ arrive,
+                        double* __restrict__ ibox, Node* __restrict__ nodes) {
+  int li = blockIdx.x * blockDim.x + threadIdx.x;
+  if (li >= n) return;
+  int node = parent_leaf[li];
+  while (node >= 0) {
+    __threadfence();
+    if (atomicAdd(&arrive[node], 1) == 0) return;  // first arrival: sibling not ready
+    __threadfence();
+    Node nd;
+    double u[5] = {INFINITY, -INFINITY, INFINITY, -INFINITY, -INFINITY};
+    for (int c = 0; c < 2; ++c) {
+      int ch = c == 0 ? left[node] : right[node];
+      const double* b;
+      if (ch < 0) {
+        b = leafbox + 5 * sorted_ids[~ch];
+        nd.child[c] = ~sorted_ids[~ch];  // leaf: ~patch id
+      } else {
+        b = ibox + 5 * ch;
+        nd.child[c] = ch;
+      }
+      double b0 = __ldcg(b), b1 = __ldcg(b + 1), b2 = __ldcg(b + 2), b3 = __ldcg(b + 3),
+             b4 = __ldcg(b + 4);
+      nd.alo[c] = b0; nd.ahi[c] = b1; nd.blo[c] = b2; nd.bhi[c] = b3; nd.cmax[c] = b4;
+      u[0] = fmin(u[0], b0); u[1] = fmax(u[1], b1); u[2] = fmin(u[2], b2);
+      u[3] = fmax(u[3], b3); u[4] = fmax(u[4], b4);
+    }
+    nodes[node] = nd;
+    for (int k = 0; k < 5; ++k) __stcg(ibox + 5 * node + k, u[k]);
+    node = parent_int[node];
+  }
+}
+
+void free_round(Round& rd) {
+  if (rd.proj) cudaFree(rd.proj);
+  if (rd.nodes) cudaFree(rd.nodes);
+  if (rd.leafbox) cudaFree(rd.leafbox);
+  rd = Round();
+}
+
+// Caller holds sc->mu.  Builds rounds[0..r] that are missing.
+cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+  while ((int)sc->rounds.size() <= r) {
+    int rr = (int)sc->rounds.size();
+    Round rd;
+    double d[3];
+    gwn_direction(sc->prm.dir_seed, rr, d);
+    make_frame(d, &rd.f);
+    const int64_t P = sc->P;
+    if (P > 0) {
+      // projected scene bounds from the 8 corners of the scene box
+      double amin = INFINITY, amax = -INFINITY, bmin = INFINITY, bmax = -INFINITY;
+      for (int c = 0; c < 8; ++c) {
+        double x = (c & 1) ? sc->bbox_max[0] : sc->bbox_min[0];
+        double y = (c & 2) ? sc->bbox_max[1] : sc->bbox_min[1];
+        double z = (c & 4) ? sc->bbox_max[2] : sc->bbox_min[2];
+        double A = x * rd.f.e1[0] + y * rd.f.e1[1] + z * rd.f.e1[2];
+        double B = x * rd.f.e2[0] + y * rd.f.e2[1] + z * rd.f.e2[2];
+        amin = fmin(amin, A); amax = fmax(amax, A);
+        bmin = fmin(bmin, B); bmax = fmax(bmax, B);
+      }
+      double ainv = amax > amin ? 1.0 / (amax - amin) : 0.0;
+      double binv = bmax > bmin ? 1.0 / (bmax - bmin) : 0.0;
+      uint32_t *keys = nullptr, *keys2 = nullptr;
+      int32_t *ids = nullptr, *ids2 = nullptr, *tmp = nullptr;
+      double* ibox = nullptr;
+      void* cub_tmp = nullptr;
+      size_t cub_bytes = 0;
+      const int n = (int)P;
+      const unsigned pb = (unsigned)((P + 127) / 128);
+#define RC(x)                     \
+  do {                            \
+    e = (x);                      \
+    if (e != cudaSuccess) goto out; \
+  } while (0)
+      RC(cudaMalloc(&rd.proj, sizeof(double) * 48 * P));
+      RC(cudaMalloc(&rd.leafbox, sizeof(double) * 5 * P));
+      RC(cudaMalloc(&keys, sizeof(uint32_t) * P));
+      RC(cudaMalloc(&keys2, sizeof(uint32_t) * P));
+      RC(cudaMalloc(&ids, sizeof(int32_t) * P));
+      RC(cudaMalloc(&ids2, sizeof(int32_t) * P));
+      k_project<<<pb, 128, 0, st>>>(sc->ctrl, P, rd.f, rd.proj, rd.leafbox, keys, ids, amin,
+                                    ainv, bmin, binv);
+      RC(cudaGetLastError());
+      if (P > 1) {
+        RC(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, keys, keys2, ids, ids2, n, 0, 30,
+                                           st));
+        RC(cudaMalloc(&cub_tmp, cub_bytes));
+        RC(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys, keys2, ids, ids2, n, 0, 30,
+                                           st));
+        RC(cudaMalloc(&rd.nodes, sizeof(Node) * (P - 1)));
+        RC(cudaMalloc(&tmp, sizeof(int32_t) * (5 * P)));
+        RC(cudaMalloc(&ibox, sizeof(double) * 5 * (P - 1)));
+        {
+          int32_t* left = tmp;
+          int32_t* right = tmp + P;
+          int32_t* parent_int = tmp + 2 * P;
+          int32_t* parent_leaf = tmp + 3 * P;
+          int32_t* arrive = tmp + 4 * P;
+          RC(cudaMemsetAsync(arrive, 0, sizeof(int32_t) * P, st));
+          RC(cudaMemsetAsync(parent_int, 0xff, sizeof(int32_t) * P, st));  // root parent = -1
+          k_karras<<<pb, 128, 0, st>>>(keys2, n, left, right, parent_int, parent_leaf);
+          RC(cudaGetLastError());
+          k_refit<<<pb, 128, 0, st>>>(n, ids2, rd.leafbox, left, right, parent_int, parent_leaf,
+                                      arrive, ibox, rd.nodes);
+          RC(cudaGetLastError());
+        }
+      }
+      RC(cudaStreamSynchronize(st));
+    out:
+      if (keys) cudaFree(keys);
+      if (keys2) cudaFree(keys2);
+      if (ids) cudaFree(ids);
+      if (ids2) cudaFree(ids2);
+      if (tmp) cudaFree(tmp);
+      if (ibox) cudaFree(ibox);
+      if (cub_tmp) cudaFree(cub_tmp);
+#undef RC
+      if (e != cudaSuccess) {
+        free_round(rd);
+        return e;
+      }
+    }
+    sc->rounds.push_back(rd);
+  }
+  return e;
+}
+
+}  // namespace gwn

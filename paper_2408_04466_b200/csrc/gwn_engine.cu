@@ -1,0 +1,404 @@
+// gwn_engine.cu -- the batched engine (SPEC.md:371-380 winding_number, for
+// many queries) and the C-ABI entry points that need device work.
+//
+// Per chunk of queries, per direction round r (all active queries of a round
+// share d_r, so the patch hierarchy of the round is shared):
+//   K2 cull count -> exclusive scan -> K2 fill   (candidate pairs by query)
+//   K3 intersect + segmented warp reduction       (chi, flags per query)
+//   K4 boundary term                              (B, flags per query)
+//   K5 finalize: w = chi + B, or jitter / re-shoot
+// Re-shot queries are compacted into the next round's active list.
+#include <cub/cub.cuh>
+
+#include <math.h>
+#include <string.h>
+
+#include "gwn_internal.h"
+
+namespace gwn {
+
+// K5: per active query decide done / jitter / re-shoot.
+__global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
+                           const int32_t* __restrict__ chi, const int32_t* __restrict__ flags,
+                           const double* __restrict__ bterm, int round, int max_rounds,
+                           int max_jitters, uint64_t seed, int64_t index_base, double jscale,
+                           const double* __restrict__ q0, double* __restrict__ pos,
+                           int8_t* __restrict__ jit, int8_t* __restrict__ jreason,
+                           double* __restrict__ w_out, int8_t* __restrict__ st_out,
+                           int32_t* __restrict__ next, int32_t* __restrict__ next_n) {
+  int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  bool push = false;
+  int32_t q = 0;
+  if (s < m) {
+    q = active ? active[s] : s;
+    int32_t f = flags[s];
+    double w = (double)chi[s] + bterm[s];
+    if (f & (FLAG_ONSURF | FLAG_DEGEN)) {
+      int reason = (f & FLAG_ONSURF) ? GWN_STATUS_ON_SURFACE : GWN_STATUS_DEGENERATE;
+      int j = jit[q];
+      if (j < max_jitters && round + 1 >= max_rounds) {
+        w_out[q] = w;  // jitter budget left but no round to use it (oracle eval_query)
+        st_out[q] = GWN_STATUS_EXHAUSTED;
+      } else if (j < max_jitters) {
+        ++j;
+        jit[q] = (int8_t)j;
+        jreason[q] = (int8_t)reason;
+        // deterministic jitter (same hash as gwn_jitter_dir / the oracle)
+        uint64_t st = seed ^ 0x5851F42D4C957F2Dull;
+        st ^= (uint64_t)(index_base + q) * 0x9E3779B97F4A7C15ull;
+        st ^= (uint64_t)(j + 1) * 0xC2B2AE3D27D4EB4Full;
+        double v[3];
+        for (int k = 0; k < 3; ++k) {
+          uint64_t z = (st += 0x9E3779B97F4A7C15ull);
+          z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+          z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+          z ^= z >> 31;
+          v[k] = __dadd_rn(__dmul_rn(2.0, __dmul_rn((double)(z >> 11), 1.0 / 9007199254740992.0)),
+                           -1.0);
+        }
+        double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(v[0], v[0]), __dmul_rn(v[1], v[1])),
+                                        __dmul_rn(v[2], v[2])));
+        if (n < 1e-3) {
+          v[0] = 1.0; v[1] = 0.0; v[2] = 0.0;
+        } else {
+          for (int k = 0; k < 3; ++k) v[k] = __ddiv_rn(v[k], n);
+        }
+        for (int k = 0; k < 3; ++k)
+          pos[3 * (int64_t)q + k] = __dadd_rn(q0[3 * (int64_t)q + k], __dmul_rn(jscale, v[k]));
+        push = true;
+      } else {
+        w_out[q] = w;
+        st_out[q] = (int8_t)reason;
+      }
+    } else if (f & (FLAG_RESHOOT | FLAG_BAND)) {
+      if (round + 1 < max_rounds) {
+        push = true;
+      } else {
+        w_out[q] = w;
+        st_out[q] = GWN_STATUS_EXHAUSTED;
+      }
+    } else {
+      w_out[q] = w;
+      st_out[q] = jit[q] ? jreason[q] : (int8_t)GWN_STATUS_OK;
+    }
+  }
+  // warp-aggregated compaction of the re-shot queries
+  unsigned mask = __ballot_sync(0xffffffffu, push);
+  if (mask) {
+    int lane = threadIdx.x & 31;
+    int leader = __ffs(mask) - 1;
+    int32_t base = 0;
+    if (lane == leader) base = atomicAdd(next_n, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (push) next[base + __popc(mask & ((1u << lane) - 1))] = q;
+  }
+}
+
+struct Workspace {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  cudaError_t err = cudaSuccess;
+  template <class T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    if (err != cudaSuccess) return nullptr;
+    err = cudaMallocAsync(&p, n * sizeof(T) + 16, st);
+    if (err == cudaSuccess) ptrs.push_back(p);
+    return (T*)p;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+    ptrs.clear();
+  }
+};
+
+}  // namespace gwn
+
+using namespace gwn;
+
+#define CKE(call)                                                              \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) {                                                   \
+      set_error("%s failed: %s", #call, cudaGetErrorString(e_));              \
+      rc = (e_ == cudaErrorMemoryAllocation) ? GWN_E_OOM : GWN_E_CUDA;         \
+      goto done;                                                               \
+    }                                                                          \
+  } while (0)
+
+static cudaError_t ensure_round(gwn_scene* sc, int r, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(sc->mu);
+  if ((int)sc->rounds.size() > r) return cudaSuccess;
+  return build_round(sc, r, st);
+}
+
+extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t index_base,
+                        double* w_out, int8_t* status_out, int32_t flags, void* stream) {
+  int rc = GWN_OK;
+  if (!sc || n < 0 || (n > 0 && (!queries || !w_out || !status_out))) {
+    set_error("gwn_eval: invalid arguments");
+    return GWN_E_INVALID;
+  }
+  if (n == 0) return GWN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace ws;
+  ws.st = st;
+  const bool host = (flags & GWN_HOST_BUFFERS) != 0;
+  const int64_t chunk_max = sc->prm.chunk_queries > 0 ? sc->prm.chunk_queries : (1ll << 22);
+  int64_t* h_scalar = nullptr;  // pinned: [0] pair total, [1] next count
+  const double* d_q = queries;
+  double* d_w = w_out;
+  int8_t* d_st = status_out;
+  gwn_stats stats;
+  memset(&stats, 0, sizeof stats);
+  stats.queries = n;
+  cudaEvent_t ev[8] = {};
+  int64_t launches = 0;
+  unsigned long long* d_cnt = nullptr;
+  unsigned long long h_cnt[CNT_N];
+  CKE(cudaSetDevice(sc->device));
+  CKE(cudaMallocHost(&h_scalar, 2 * sizeof(int64_t)));
+  d_cnt = ws.get<unsigned long long>(CNT_N);
+  CKE(ws.err);
+  CKE(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * CNT_N, st));
+  if (host) {
+    double* dq = ws.get<double>((size_t)(3 * n));
+    d_w = ws.get<double>((size_t)n);
+    d_st = ws.get<int8_t>((size_t)n);
+    CKE(ws.err);
+    CKE(cudaMemcpyAsync(dq, queries, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+    d_q = dq;
+  }
+  if (sc->timed)
+    for (auto& e : ev) CKE(cudaEventCreate(&e));
+  {
+    const int64_t cm = n < chunk_max ? n : chunk_max;
+    // per-chunk workspace (reused across chunks)
+    double* pos = ws.get<double>((size_t)(3 * cm));
+    int8_t* jit = ws.get<int8_t>((size_t)cm);
+    int8_t* jreason = ws.get<int8_t>((size_t)cm);
+    int32_t* act[2] = {ws.get<int32_t>((size_t)cm), ws.get<int32_t>((size_t)cm)};
+    int64_t* counts = ws.get<int64_t>((size_t)cm + 1);
+    int64_t* offs = ws.get<int64_t>((size_t)cm + 1);
+    double* qproj = ws.get<double>((size_t)(3 * cm));
+    int32_t* chi = ws.get<int32_t>((size_t)cm);
+    int32_t* fl = ws.get<int32_t>((size_t)cm);
+    double* bterm = ws.get<double>((size_t)cm);
+    int32_t* next_n = ws.get<int32_t>(1);
+    size_t scan_bytes = 0;
+    CKE(ws.err);
+    CKE(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts, offs, (int)cm + 1, st));
+    void* scan_tmp = ws.get<char>(scan_bytes);
+    int64_t pair_cap = 0;
+    int32_t* pair_slot = nullptr;
+    int32_t* pair_patch = nullptr;
+    CKE(ws.err);
+    for (int64_t c0 = 0; c0 < n; c0 += cm) {
+      const int32_t mc = (int32_t)((n - c0) < cm ? (n - c0) : cm);
+      const double* q0 = d_q + 3 * c0;
+      CKE(cudaMemcpyAsync(pos, q0, sizeof(double) * 3 * mc, cudaMemcpyDeviceToDevice, st));
+      CKE(cudaMemsetAsync(jit, 0, mc, st));
+      int32_t m = mc;
+      const int32_t* active = nullptr;
+      int cur = 0;
+      for (int r = 0; r < sc->prm.max_rounds && m > 0; ++r) {
+        CKE(ensure_round(sc, r, st));
+        const Round& rd = sc->rounds[r];
+        stats.rounds++;
+        if (r > 0) stats.retried += m;
+        if (sc->timed) CKE(cudaEventRecord(ev[0], st));
+        // ---- K2: cull (count, scan, fill)
+        int64_t npairs = 0;
+        if (sc->P > 0) {
+          CKE(launch_cull_count(sc, rd, m, active, pos, counts, qproj, st));
+          CKE(cudaMemsetAsync(counts + m, 0, sizeof(int64_t), st));
+          CKE(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, offs, m + 1, st));
+          CKE(cudaMemcpyAsync(h_scalar, offs + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+          CKE(cudaStreamSynchronize(st));
+          npairs = h_scalar[0];
+          if (npairs > pair_cap) {
+            if (pair_slot) cudaFreeAsync(pair_slot, st);
+            if (pair_patch) cudaFreeAsync(pair_patch, st);
+            pair_cap = npairs + npairs / 4 + 1024;
+            CKE(cudaMallocAsync(&pair_slot, sizeof(int32_t) * pair_cap, st));
+            CKE(cudaMallocAsync(&pair_patch, sizeof(int32_t) * pair_cap, st));
+          }
+          CKE(launch_cull_fill(sc, rd, m, active, pos, offs, pair_slot, pair_patch, st));
+          launches += 3;
+        }
+        stats.candidates += npairs;
+        if (sc->timed) CKE(cudaEventRecord(ev[1], st));
+        // ---- K3: intersect + segmented reduction
+        CKE(cudaMemsetAsync(chi, 0, sizeof(int32_t) * m, st));
+        CKE(cudaMemsetAsync(fl, 0, sizeof(int32_t) * m, st));
+        if (npairs > 0) {
+          CKE(launch_intersect(sc, rd, npairs, pair_slot, pair_patch, qproj, chi, fl, d_cnt, st));
+          ++launches;
+        }
+        if (sc->timed) CKE(cudaEventRecord(ev[2], st));
+        // ---- K4: boundary term
+        CKE(launch_boundary(sc, rd, m, active, pos, bterm, fl, d_cnt, st));
+        if (sc->n_edges > 0) ++launches;
+        if (sc->timed) CKE(cudaEventRecord(ev[3], st));
+        // ---- K5: finalize / compact re-shoots
+        CKE(cudaMemsetAsync(next_n, 0, sizeof(int32_t), st));
+        int32_t* nxt = act[cur];
+        k_finalize<<<(m + 127) / 128, 128, 0, st>>>(
+            m, active, chi, fl, bterm, r, sc->prm.max_rounds, sc->prm.max_jitters,
+            sc->prm.dir_seed, index_base + c0, sc->prm.jitter_scale * sc->diag, q0, pos, jit,
+            jreason, d_w + c0, d_st + c0, nxt, next_n);
+        CKE(cudaGetLastError());
+        ++launches;
+        CKE(cudaMemcpyAsync(h_scalar + 1, next_n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        if (sc->timed) CKE(cudaEventRecord(ev[4], st));
+        CKE(cudaStreamSynchronize(st));
+        if (sc->timed) {
+          float a = 0, b = 0, c = 0, d = 0;
+          cudaEventElapsedTime(&a, ev[0], ev[1]);
+          cudaEventElapsedTime(&b, ev[1], ev[2]);
+          cudaEventElapsedTime(&c, ev[2], ev[3]);
+          cudaEventElapsedTime(&d, ev[3], ev[4]);
+          stats.ms_cull += a;
+          stats.ms_intersect += b;
+          stats.ms_boundary += c;
+          stats.ms_other += d;
+        }
+        m = (int32_t)(*(int32_t*)(h_scalar + 1));
+        active = nxt;
+        cur ^= 1;
+      }
+    }
+    if (pair_slot) cudaFreeAsync(pair_slot, st);
+    if (pair_patch) cudaFreeAsync(pair_patch, st);
+  }
+  if (host) {
+    CKE(cudaMemcpyAsync(w_out, d_w, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CKE(cudaMemcpyAsync(status_out, d_st, n, cudaMemcpyDeviceToHost, st));
+  }
+  CKE(cudaMemcpyAsync(h_cnt, d_cnt, sizeof h_cnt, cudaMemcpyDeviceToHost, st));
+  CKE(cudaStreamSynchronize(st));
+  stats.nodes = (int64_t)h_cnt[CNT_NODES];
+  stats.newton_iters = (int64_t)h_cnt[CNT_NEWTON];
+  stats.roots = (int64_t)h_cnt[CNT_ROOTS];
+  stats.boundary_segments = (int64_t)h_cnt[CNT_SEGMENTS];
+  stats.kernel_launches = launches;
+  sc->stats = stats;
+done:
+  ws.release();
+  if (st) cudaStreamSynchronize(st);
+  else cudaDeviceSynchronize();
+  if (h_scalar) cudaFreeHost(h_scalar);
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  return rc;
+}
+
+extern "C" int gwn_all_hits(gwn_scene* sc, int64_t patch, const double origin[3],
+                            const double direction[3], double* t_out, double* uv_out,
+                            int32_t* sign_out, int8_t* tang_out, int8_t* graze_out, int32_t cap) {
+  int rc = GWN_OK;
+  double* d_out = nullptr;
+  int32_t* d_cnt = nullptr;
+  double* d_proj = nullptr;
+  int32_t cnt = 0;
+  double h[6 * 8];
+  Round rd;
+  if (!sc || patch < 0 || patch >= sc->P || !origin || !direction || cap < 0) {
+    set_error("gwn_all_hits: invalid arguments");
+    return GWN_E_INVALID;
+  }
+  {
+    double dd[3] = {direction[0], direction[1], direction[2]};
+    double l = sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]);
+    if (!(l > 0.0)) {
+      set_error("gwn_all_hits: zero direction");
+      return GWN_E_INVALID;
+    }
+    if (fabs(l - 1.0) > 1e-12)  // Ray normalisation rule, geometry.py:49-51
+      for (int k = 0; k < 3; ++k) dd[k] /= l;
+    make_frame(dd, &rd.f);
+  }
+  CKE(cudaSetDevice(sc->device));
+  {
+    // project just this patch on the host (48 dot products)
+    double X[48], P48[48];
+    CKE(cudaMemcpy(X, sc->ctrl + 48 * patch, sizeof X, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 16; ++k) {
+      P48[k] = X[3 * k] * rd.f.e1[0] + X[3 * k + 1] * rd.f.e1[1] + X[3 * k + 2] * rd.f.e1[2];
+      P48[16 + k] = X[3 * k] * rd.f.e2[0] + X[3 * k + 1] * rd.f.e2[1] + X[3 * k + 2] * rd.f.e2[2];
+      P48[32 + k] = X[3 * k] * rd.f.d[0] + X[3 * k + 1] * rd.f.d[1] + X[3 * k + 2] * rd.f.d[2];
+    }
+    CKE(cudaMalloc(&d_proj, sizeof P48));
+    CKE(cudaMemcpy(d_proj, P48, sizeof P48, cudaMemcpyHostToDevice));
+  }
+  CKE(cudaMalloc(&d_out, sizeof h));
+  CKE(cudaMalloc(&d_cnt, sizeof(int32_t)));
+  rd.proj = d_proj;
+  CKE(launch_all_hits(sc, rd, 0, origin, d_out, d_cnt, 8, 0));
+  CKE(cudaMemcpy(&cnt, d_cnt, sizeof cnt, cudaMemcpyDeviceToHost));
+  CKE(cudaMemcpy(h, d_out, sizeof h, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < cnt && k < cap && k < 8; ++k) {
+    if (t_out) t_out[k] = h[6 * k];
+    if (uv_out) {
+      uv_out[2 * k] = h[6 * k + 1];
+      uv_out[2 * k + 1] = h[6 * k + 2];
+    }
+    if (sign_out) sign_out[k] = (int32_t)h[6 * k + 3];
+    if (tang_out) tang_out[k] = (int8_t)h[6 * k + 4];
+    if (graze_out) graze_out[k] = (int8_t)h[6 * k + 5];
+  }
+  rc = cnt;
+done:
+  if (d_out) cudaFree(d_out);
+  if (d_cnt) cudaFree(d_cnt);
+  if (d_proj) cudaFree(d_proj);
+  return rc;
+}
+
+extern "C" int gwn_single_loop_batch(const double* loop, int64_t B, const double origin[3],
+                                     const double direction[3], const double* hit_ts,
+                                     const int64_t* hit_signs, int64_t H, const double* qts,
+                                     int64_t K, double on_tol, double t_eps, double* w_out,
+                                     int8_t* ok_out, int device) {
+  (void)on_tol;
+  int rc = GWN_OK;
+  double *d_loop = nullptr, *d_ht = nullptr, *d_q = nullptr, *d_w = nullptr;
+  int64_t* d_hs = nullptr;
+  int8_t* d_ok = nullptr;
+  double d[3];
+  if (!loop || B < 3 || !origin || !direction || H < 0 || K < 0 || (H && (!hit_ts || !hit_signs)) ||
+      (K && (!qts || !w_out || !ok_out))) {
+    set_error("gwn_single_loop_batch: invalid arguments (loop needs >= 3 points)");
+    return GWN_E_INVALID;
+  }
+  if (K == 0) return GWN_OK;
+  {
+    double l = sqrt(direction[0] * direction[0] + direction[1] * direction[1] +
+                    direction[2] * direction[2]);
+    for (int k = 0; k < 3; ++k) d[k] = fabs(l - 1.0) > 1e-12 ? direction[k] / l : direction[k];
+  }
+  CKE(cudaSetDevice(device));
+  CKE(cudaMalloc(&d_loop, sizeof(double) * 3 * B));
+  CKE(cudaMalloc(&d_ht, sizeof(double) * (H + 1)));
+  CKE(cudaMalloc(&d_hs, sizeof(int64_t) * (H + 1)));
+  CKE(cudaMalloc(&d_q, sizeof(double) * K));
+  CKE(cudaMalloc(&d_w, sizeof(double) * K));
+  CKE(cudaMalloc(&d_ok, K));
+  CKE(cudaMemcpy(d_loop, loop, sizeof(double) * 3 * B, cudaMemcpyHostToDevice));
+  if (H) {
+    CKE(cudaMemcpy(d_ht, hit_ts, sizeof(double) * H, cudaMemcpyHostToDevice));
+    CKE(cudaMemcpy(d_hs, hit_signs, sizeof(int64_t) * H, cudaMemcpyHostToDevice));
+  }
+  CKE(cudaMemcpy(d_q, qts, sizeof(double) * K, cudaMemcpyHostToDevice));
+  CKE(launch_single_loop(d_loop, B, origin, d, d_ht, d_hs, H, d_q, K, t_eps, 1e-12, d_w, d_ok, 0));
+  CKE(cudaMemcpy(w_out, d_w, sizeof(double) * K, cudaMemcpyDeviceToHost));
+  CKE(cudaMemcpy(ok_out, d_ok, K, cudaMemcpyDeviceToHost));
+done:
+  cudaFree(d_loop);
+  cudaFree(d_ht);
+  cudaFree(d_hs);
+  cudaFree(d_q);
+  cudaFree(d_w);
+  cudaFree(d_ok);
+  return rc;
+}

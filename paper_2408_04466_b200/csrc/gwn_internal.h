@@ -1,0 +1,118 @@
+// gwn_internal.h -- host/device shared definitions of libgwn_b200.so.
+//
+// Data layout in HBM:
+//   ctrl      (P,16,3) f64   original control nets, i = u index (row-major)
+//   proj[r]   (P,48)   f64   per direction round r: the 16 control points in
+//                            the ray frame (e1,e2,d): [A0..A15 | B0..B15 | C0..C15]
+//   nodes[r]  (P-1)    Node  2-D LBVH over the projected control hulls; each
+//                            internal node stores both children's boxes
+//   verts     (V,3)    f64   SoA x|y|z of the net boundary polylines, S per edge
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <vector>
+
+#include "../../include/gwn_b200.h"
+
+namespace gwn {
+
+// per-query flag bits accumulated over a round
+enum : int32_t {
+  FLAG_RESHOOT = 1,   // tangency / grazing / ambiguous root set -> new direction
+  FLAG_BAND = 2,      // ray within the polyline/curve band of a net segment
+  FLAG_ONSURF = 4,    // a hit with |t| <= on_surface_t -> jitter
+  FLAG_DEGEN = 8,     // query on a boundary vertex -> jitter
+};
+
+// device counters (index into a u64 array)
+enum : int {
+  CNT_CANDIDATES = 0,
+  CNT_NODES = 1,
+  CNT_NEWTON = 2,
+  CNT_ROOTS = 3,
+  CNT_SEGMENTS = 4,
+  CNT_N = 8,
+};
+
+struct Frame {
+  double e1[3], e2[3], d[3];
+};
+
+struct DevParams {
+  double residual, dedup, tangent, edge_graze, degenerate;
+  double domain_tol, t_tol, on_surface_t, band_factor;
+};
+
+// 2-D LBVH node in the ray frame.  Child c's box: a in [alo,ahi], b in
+// [blo,bhi], patch extent along d up to cmax.  child >= 0: internal node,
+// child < 0: leaf patch ~child.
+struct alignas(16) Node {
+  double alo[2], ahi[2], blo[2], bhi[2], cmax[2];
+  int32_t child[2];
+};
+
+struct Round {
+  Frame f;
+  double* proj = nullptr;     // (P,48)
+  Node* nodes = nullptr;      // (P-1)
+  double* leafbox = nullptr;  // (P,5) when P == 1 (root is a leaf)
+};
+
+}  // namespace gwn
+
+struct gwn_scene {
+  gwn_params prm;
+  gwn::DevParams dprm;
+  int device = 0;
+  int sm_count = 0;
+  int64_t P = 0;
+  double bbox_min[3], bbox_max[3], diag = 0.0;
+  double* ctrl = nullptr;       // device (P,48)
+  // net boundary
+  int64_t n_edges = 0;          // after expanding multiplicities
+  int32_t S = 0;
+  double* verts = nullptr;      // (3,V) SoA, V = n_edges*S
+  double* band_h = nullptr;     // (n_edges)
+  // per-round caches
+  std::mutex mu;
+  std::vector<gwn::Round> rounds;
+  // last-eval stats
+  gwn_stats stats;
+  int timed = 0;
+};
+
+namespace gwn {
+
+// launchers (stream-ordered); defined in the .cu files
+cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st);            // gwn_bvh.cu
+void free_round(Round& rd);
+cudaError_t launch_cull_count(const gwn_scene* sc, const Round& rd, int32_t m,
+                              const int32_t* active, const double* pos, int64_t* counts,
+                              double* qproj, cudaStream_t st);             // gwn_cull.cu
+cudaError_t launch_cull_fill(const gwn_scene* sc, const Round& rd, int32_t m,
+                             const int32_t* active, const double* pos, const int64_t* offs,
+                             int32_t* pair_slot, int32_t* pair_patch, cudaStream_t st);
+cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, int64_t npairs,
+                             const int32_t* pair_slot, const int32_t* pair_patch,
+                             const double* qproj, int32_t* chi, int32_t* flags,
+                             unsigned long long* counters, cudaStream_t st);  // gwn_intersect.cu
+cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
+                            const int32_t* active, const double* pos, double* bterm,
+                            int32_t* flags, unsigned long long* counters,
+                            cudaStream_t st);                                 // gwn_boundary.cu
+cudaError_t launch_all_hits(const gwn_scene* sc, const Round& rd, int64_t patch,
+                            const double* o, double* out, int32_t* count, int32_t cap,
+                            cudaStream_t st);
+cudaError_t launch_single_loop(const double* loop, int64_t B, const double* o, const double* d,
+                               const double* hit_ts, const int64_t* hit_signs, int64_t H,
+                               const double* qts, int64_t K, double t_eps, double deg, double* w,
+                               int8_t* ok, cudaStream_t st);
+
+// host helpers (gwn_scene.cu)
+void make_frame(const double d[3], Frame* f);
+void set_error(const char* fmt, ...);
+
+}  // namespace gwn

@@ -1,0 +1,239 @@
+"""Top-level engine: the SPEC ``engine`` API on the B200 kernels.
+
+Reference surface (the drop-in boundary):
+  * ``Scene`` -- SPEC.md:355-365 (patches + aggregated oriented boundary)
+  * ``winding_number(scene, p)`` -- SPEC.md:371-380
+  * ``winding_numbers_along_ray(scene, r, ts)`` -- SPEC.md:381-389
+  * ``combine(a, b, op)`` -- SPEC.md:409-416
+plus the batched call every other path funnels into,
+``winding_numbers(scene, queries)``, which is one ``gwn_eval`` of
+libgwn_b200.so.  Accepts numpy arrays (host buffers; the library does the
+copies) or torch tensors (CUDA tensors stay on the device; CPU tensors,
+ideally pinned, are copied inside the call).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import warnings
+from typing import Iterable
+
+import numpy as np
+
+from . import _lib
+from . import config as cfg
+from .config import DEFAULT_EPS, EpsilonConfig
+from .errors import STATUS_ERRORS, STATUS_OK, GridMismatch, SceneError, SeedExhausted
+from .geometry import Aabb, Ray
+
+
+def _as_ctrl(patches) -> np.ndarray:
+    if isinstance(patches, np.ndarray):
+        ctrl = patches
+    else:
+        lst = list(patches)
+        if lst and hasattr(lst[0], "control"):
+            ctrl = np.stack([np.asarray(p.control, dtype=np.float64) for p in lst]) if lst else \
+                np.zeros((0, 4, 4, 3))
+        else:
+            ctrl = np.asarray(lst, dtype=np.float64).reshape(-1, 4, 4, 3)
+    ctrl = np.ascontiguousarray(ctrl, dtype=np.float64)
+    if ctrl.ndim != 4 or ctrl.shape[1:] != (4, 4, 3):
+        raise SceneError(f"expected (P,4,4,3) bicubic control nets, got {ctrl.shape}")
+    if not np.all(np.isfinite(ctrl)):
+        raise SceneError("control points must be finite")
+    return ctrl
+
+
+class Scene:
+    """Immutable device-resident scene (SPEC.md:216 concurrency model).
+
+    ``patches``: a list of :class:`BicubicPatch` (or anything with a
+    ``control`` (4,4,3) array) or a ``(P,4,4,3)`` array.
+    """
+
+    def __init__(self, patches, eps: EpsilonConfig = DEFAULT_EPS,
+                 samples_per_edge: int = 200, device: int | None = None,
+                 max_rounds: int = cfg.MAX_ROUNDS, max_jitters: int = cfg.MAX_JITTERS,
+                 dir_seed: int = cfg.DIR_SEED, chunk_queries: int = 0):
+        if samples_per_edge < 2:
+            raise ValueError("need at least 2 samples per edge")
+        self.ctrl = _as_ctrl(patches)
+        self.eps = eps
+        self.samples_per_edge = samples_per_edge
+        if device is None:
+            device = _current_device()
+        self.device = device
+        p = _lib.default_params()
+        p.residual = eps.residual
+        p.dedup = eps.dedup
+        p.tangent = eps.tangent_parametric
+        p.edge_graze = eps.edge_graze
+        p.degenerate = eps.degenerate
+        p.jitter_scale = eps.jitter_scale
+        p.samples_per_edge = samples_per_edge
+        p.max_rounds = max_rounds
+        p.max_jitters = max_jitters
+        p.dir_seed = dir_seed
+        p.chunk_queries = chunk_queries
+        self.params = p
+        h = C.c_void_p()
+        dp = C.POINTER(C.c_double)
+        _lib.check(_lib.lib().gwn_scene_create(self.ctrl.ctypes.data_as(dp), len(self.ctrl),
+                                               C.byref(p), device, C.byref(h)),
+                   "gwn_scene_create")
+        self.handle = h
+        info = _lib.SceneInfo()
+        _lib.check(_lib.lib().gwn_scene_info_get(h, C.byref(info)), "gwn_scene_info_get")
+        self.info = info
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().gwn_scene_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self.handle = None
+
+    @property
+    def n_patches(self) -> int:
+        return int(self.info.n_patches)
+
+    @property
+    def n_net_segments(self) -> int:
+        return int(self.info.n_net_segments)
+
+    @property
+    def diag(self) -> float:
+        return float(self.info.diag)
+
+    def aabb(self) -> Aabb:
+        return Aabb(np.array(self.info.bbox_min[:]), np.array(self.info.bbox_max[:]))
+
+    def stats(self) -> dict:
+        s = _lib.Stats()
+        _lib.check(_lib.lib().gwn_stats_get(self.handle, C.byref(s)), "gwn_stats_get")
+        return s.as_dict()
+
+    def set_timing(self, on: bool) -> None:
+        _lib.check(_lib.lib().gwn_set_timing(self.handle, int(bool(on))), "gwn_set_timing")
+
+
+def _current_device() -> int:
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:  # pragma: no cover
+        pass
+    return 0
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def winding_numbers(scene: Scene, queries, *, index_base: int = 0, stream=None,
+                    out=None, return_status: bool = True):
+    """Generalized winding numbers of many query points (one ``gwn_eval``).
+
+    Returns ``(w, status)``; ``status`` codes: 0 ok, 1 on-surface (jittered),
+    2 re-shoot budget exhausted, 3 degenerate projection (jittered).
+    """
+    L = _lib.lib()
+    if _is_torch(queries):
+        import torch
+        q = queries
+        if q.dtype != torch.float64 or q.dim() != 2 or q.shape[1] != 3:
+            raise ValueError("queries must be an (n,3) float64 tensor")
+        q = q.contiguous()
+        n = q.shape[0]
+        if out is not None:
+            w, st = out
+        else:
+            w = torch.empty(n, dtype=torch.float64, device=q.device)
+            st = torch.empty(n, dtype=torch.int8, device=q.device)
+        flags = 0 if q.is_cuda else _lib.GWN_HOST_BUFFERS
+        if q.is_cuda and (not w.is_cuda or not st.is_cuda):
+            raise ValueError("device queries need device outputs")
+        if stream is None and q.is_cuda:
+            stream = torch.cuda.current_stream(q.device).cuda_stream
+        _lib.check(L.gwn_eval(scene.handle, C.c_void_p(q.data_ptr()), n, index_base,
+                              C.c_void_p(w.data_ptr()), C.c_void_p(st.data_ptr()), flags,
+                              C.c_void_p(stream or 0)), "gwn_eval")
+        return (w, st) if return_status else w
+    q = np.ascontiguousarray(queries, dtype=np.float64)
+    if q.ndim != 2 or q.shape[1] != 3:
+        raise ValueError("queries must have shape (n, 3)")
+    n = q.shape[0]
+    w = np.empty(n, np.float64)
+    st = np.empty(n, np.int8)
+    _lib.check(L.gwn_eval(scene.handle, C.c_void_p(q.ctypes.data), n, index_base,
+                          C.c_void_p(w.ctypes.data), C.c_void_p(st.ctypes.data),
+                          _lib.GWN_HOST_BUFFERS, C.c_void_p(stream or 0)), "gwn_eval")
+    return (w, st) if return_status else w
+
+
+def winding_number(scene: Scene, p) -> float:
+    """w(p).  On-surface / degenerate queries are jittered
+    by ``jitter_scale * diag`` (at most 3 times) with a warning; an exhausted
+    re-shoot budget raises :class:`SeedExhausted`."""
+    w, st = winding_numbers(scene, np.asarray(p, dtype=np.float64).reshape(1, 3))
+    code = int(st[0])
+    if code == 2:
+        raise SeedExhausted(f"every ray from {p} was tangent / grazing")
+    if code != STATUS_OK:
+        warnings.warn(f"query {p}: {STATUS_ERRORS[code].__name__}; evaluated at a jittered point")
+    return float(w[0])
+
+
+def winding_numbers_along_ray(scene: Scene, r: Ray, ts: Iterable[float]) -> list[float]:
+    """w at r.origin + t r.direction for sorted ts."""
+    ts = np.asarray(list(ts), dtype=np.float64)
+    if ts.size == 0:
+        return []
+    if np.any(np.diff(ts) < 0):
+        raise ValueError("ts must be sorted ascending")
+    pts = r.origin[None, :] + ts[:, None] * r.direction[None, :]
+    w, _ = winding_numbers(scene, pts)
+    return [float(x) for x in w]
+
+
+def combine(field_a, field_b, op: str):
+    """Boolean combination of winding-number fields."""
+    a, b = np.asarray(field_a), np.asarray(field_b)
+    if a.shape != b.shape:
+        raise GridMismatch(f"grid shapes differ: {a.shape} vs {b.shape}")
+    if op == "union":
+        return a + b
+    if op == "intersection":
+        return a * b
+    raise ValueError(f"unknown op {op!r}")
+
+
+def direction(seed: int, rnd: int) -> np.ndarray:
+    """Direction of re-shoot round ``rnd`` (host helper, same as the oracle)."""
+    d = np.empty(3)
+    _lib.lib().gwn_direction(seed, rnd, d.ctypes.data_as(C.POINTER(C.c_double)))
+    return d
+
+
+def net_boundary(ctrl) -> tuple[np.ndarray, np.ndarray]:
+    """Net boundary edge curves after exact cancellation: ((E,4,3), weights)."""
+    ctrl = _as_ctrl(ctrl)
+    L = _lib.lib()
+    dp = C.POINTER(C.c_double)
+    n = L.gwn_net_boundary(ctrl.ctypes.data_as(dp), len(ctrl), None, None)
+    ec = np.empty((max(n, 1), 4, 3))
+    w = np.empty(max(n, 1), np.int32)
+    L.gwn_net_boundary(ctrl.ctypes.data_as(dp), len(ctrl), ec.ctypes.data_as(dp),
+                       w.ctypes.data_as(C.POINTER(C.c_int32)))
+    return ec[:n], w[:n]
+
+
+def fp64_peak(device: int = 0) -> tuple[float, float]:
+    """Measured FP64 DFMA peak (TFLOP/s, ms) of ``device``."""
+    tf, ms = C.c_double(), C.c_double()
+    _lib.check(_lib.lib().gwn_fp64_peak(device, C.byref(tf), C.byref(ms)), "gwn_fp64_peak")
+    return tf.value, ms.value
