@@ -232,7 +232,7 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
         CKE(cudaMemsetAsync(chi, 0, sizeof(int32_t) * m, st));
         CKE(cudaMemsetAsync(fl, 0, sizeof(int32_t) * m, st));
         if (npairs > 0) {
-          CKE(launch_intersect(sc, rd, npairs, pair_slot, pair_patch, qproj, chi, fl, d_cnt, st));
+          CKE(launch_intersect(sc, rd, npairs, pair_slot, pair_patch, qproj, chi, fl, m, d_cnt, st));
           ++launches;
         }
         if (sc->timed) CKE(cudaEventRecord(ev[2], st));

@@ -97,8 +97,8 @@ cudaError_t launch_cull_fill(const gwn_scene* sc, const Round& rd, int32_t m,
                              int32_t* pair_slot, int32_t* pair_patch, cudaStream_t st);
 cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, int64_t npairs,
                              const int32_t* pair_slot, const int32_t* pair_patch,
-                             const double* qproj, int32_t* chi, int32_t* flags,
-                             unsigned long long* counters, cudaStream_t st);  // gwn_intersect.cu
+                             const double* qproj, int32_t* chi, int32_t* flags, int32_t m,
+                             unsigned long long* counters, cudaStream_t st);  // gwn_wavefront.cu
 cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             const int32_t* active, const double* pos, double* bterm,
                             int32_t* flags, unsigned long long* counters,

@@ -17,15 +17,12 @@
 // d.n with n = f_u x f_v, tangency |d.n^| <= 1e-12, grazing if the domain
 // boundary distance < 1e-10.  Per-pair chi and flags are combined per query
 // with a segmented warp-shuffle reduction (K5) before one atomic per segment.
-#include "gwn_internal.h"
+#include "gwn_patch.cuh"
 
 namespace gwn {
 
-constexpr int kMaxLevel = 44;
-constexpr int kNodeBudget = 4096;
 constexpr int kMaxRoots = 8;
 constexpr int kStackNets = 24;
-constexpr int kNewtonMax = 16;
 
 struct PairOut {
   int32_t chi;
@@ -34,134 +31,6 @@ struct PairOut {
   int32_t newton;
   int32_t roots;
 };
-
-__device__ __forceinline__ void bern3(double t, double b[4], double db[4]) {
-  double s = 1.0 - t;
-  b[0] = s * s * s;
-  b[1] = 3.0 * t * s * s;
-  b[2] = 3.0 * t * t * s;
-  b[3] = t * t * t;
-  db[0] = -3.0 * s * s;
-  db[1] = 3.0 * s * (s - 2.0 * t);
-  db[2] = 3.0 * t * (2.0 * s - t);
-  db[3] = 3.0 * t * t;
-}
-
-// value and partials of one projected coordinate net X (16) at (u,v)
-__device__ __forceinline__ void eval_coord(const double* __restrict__ X, const double bu[4],
-                                           const double dbu[4], const double bv[4],
-                                           const double dbv[4], double& f, double& fu,
-                                           double& fv) {
-  double r[4], rv[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    r[i] = bv[0] * X[4 * i] + bv[1] * X[4 * i + 1] + bv[2] * X[4 * i + 2] + bv[3] * X[4 * i + 3];
-    rv[i] = dbv[0] * X[4 * i] + dbv[1] * X[4 * i + 1] + dbv[2] * X[4 * i + 2] +
-            dbv[3] * X[4 * i + 3];
-  }
-  f = bu[0] * r[0] + bu[1] * r[1] + bu[2] * r[2] + bu[3] * r[3];
-  fu = dbu[0] * r[0] + dbu[1] * r[1] + dbu[2] * r[2] + dbu[3] * r[3];
-  fv = bu[0] * rv[0] + bu[1] * rv[1] + bu[2] * rv[2] + bu[3] * rv[3];
-}
-
-// de Casteljau halving of 4 values: (p0..p3) -> left in p, right in q
-__device__ __forceinline__ void half4(double& p0, double& p1, double& p2, double& p3, double& q0,
-                                      double& q1, double& q2, double& q3) {
-  double a01 = 0.5 * (p0 + p1), a12 = 0.5 * (p1 + p2), a23 = 0.5 * (p2 + p3);
-  double b0 = 0.5 * (a01 + a12), b1 = 0.5 * (a12 + a23);
-  double c = 0.5 * (b0 + b1);
-  q3 = p3; q2 = a23; q1 = b1; q0 = c;
-  p1 = a01; p2 = b0; p3 = c;
-}
-
-// Split net (a,b) along u (dir 0) or v (dir 1); left half stays in (a,b),
-// right half is written to (ra, rb).
-__device__ __forceinline__ void split_net(double* a, double* b, double* ra, double* rb, int dir) {
-#pragma unroll
-  for (int l = 0; l < 4; ++l) {
-    int i0 = dir == 0 ? l : 4 * l;
-    int st = dir == 0 ? 4 : 1;
-    half4(a[i0], a[i0 + st], a[i0 + 2 * st], a[i0 + 3 * st], ra[i0], ra[i0 + st],
-          ra[i0 + 2 * st], ra[i0 + 3 * st]);
-    half4(b[i0], b[i0 + st], b[i0 + 2 * st], b[i0 + 3 * st], rb[i0], rb[i0 + st],
-          rb[i0 + 2 * st], rb[i0 + 3 * st]);
-  }
-}
-
-__device__ __forceinline__ bool box_has_origin(const double* a, const double* b, double eps) {
-  double amin = a[0], amax = a[0], bmin = b[0], bmax = b[0];
-#pragma unroll
-  for (int k = 1; k < 16; ++k) {
-    amin = fmin(amin, a[k]); amax = fmax(amax, a[k]);
-    bmin = fmin(bmin, b[k]); bmax = fmax(bmax, b[k]);
-  }
-  return amin <= eps && amax >= -eps && bmin <= eps && bmax >= -eps;
-}
-
-// Krawczyk test on the node net (local coords s in [0,1]^2).
-// Returns 0 exclude, 1 unique root (s0,s1 = Newton-predicted root), 2 split.
-// xlo/xhi: exclusion box in local coords (domain-tolerance expansion).
-__device__ __forceinline__ int krawczyk(const double* a, const double* b, double xlo_u,
-                                        double xhi_u, double xlo_v, double xhi_v, double& s0,
-                                        double& s1) {
-  const double w3[4] = {0.125, 0.375, 0.375, 0.125};
-  const double w2[3] = {0.25, 0.5, 0.25};
-  double ga = 0.0, gb = 0.0, Jua = 0.0, Jub = 0.0, Jva = 0.0, Jvb = 0.0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      double w = w3[i] * w3[j];
-      ga += w * a[4 * i + j];
-      gb += w * b[4 * i + j];
-      if (i < 3) {
-        double wu = w2[i] * w3[j];
-        Jua += wu * (a[4 * (i + 1) + j] - a[4 * i + j]);
-        Jub += wu * (b[4 * (i + 1) + j] - b[4 * i + j]);
-      }
-      if (j < 3) {
-        double wv = w3[i] * w2[j];
-        Jva += wv * (a[4 * i + j + 1] - a[4 * i + j]);
-        Jvb += wv * (b[4 * i + j + 1] - b[4 * i + j]);
-      }
-    }
-  }
-  // derivative nets are 3 x differences; fold the 3 into Y
-  double det = Jua * Jvb - Jva * Jub;
-  if (!(fabs(det) > 1e-300) || !isfinite(det)) return 2;
-  double id = 1.0 / det;
-  double Y00 = Jvb * id, Y01 = -Jva * id, Y10 = -Jub * id, Y11 = Jua * id;  // (J/3)^-1
-  double d0 = (Y00 * ga + Y01 * gb) * (1.0 / 3.0);
-  double d1 = (Y10 * ga + Y11 * gb) * (1.0 / 3.0);
-  double e11 = 0.0, e21 = 0.0, e12 = 0.0, e22 = 0.0;
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      double qa = a[4 * (i + 1) + j] - a[4 * i + j], qb = b[4 * (i + 1) + j] - b[4 * i + j];
-      e11 = fmax(e11, fabs(Y00 * qa + Y01 * qb - 1.0));
-      e21 = fmax(e21, fabs(Y10 * qa + Y11 * qb));
-    }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      double qa = a[4 * i + j + 1] - a[4 * i + j], qb = b[4 * i + j + 1] - b[4 * i + j];
-      e12 = fmax(e12, fabs(Y00 * qa + Y01 * qb));
-      e22 = fmax(e22, fabs(Y10 * qa + Y11 * qb - 1.0));
-    }
-  // rounding + 1e-7 box expansion margins
-  const double rad = 0.5 + 1e-7;
-  double r0 = (e11 + e12) * rad * (1.0 + 1e-9) + 1e-12;
-  double r1 = (e21 + e22) * rad * (1.0 + 1e-9) + 1e-12;
-  s0 = 0.5 - d0;
-  s1 = 0.5 - d1;
-  if (!isfinite(s0) || !isfinite(s1)) return 2;
-  if (s0 + r0 < xlo_u || s0 - r0 > xhi_u || s1 + r1 < xlo_v || s1 - r1 > xhi_v) return 0;
-  if (s0 - r0 > -1e-7 && s0 + r0 < 1.0 + 1e-7 && s1 - r1 > -1e-7 && s1 + r1 < 1.0 + 1e-7)
-    return 1;
-  return 2;
-}
 
 template <bool kRecord>
 struct RootAcc {
@@ -182,78 +51,31 @@ struct RootAcc<true> {
   int32_t newton;
 };
 
-// Newton on the whole patch from (u,v); on acceptance record the root.
+// Newton on the whole patch from (u,v); on acceptance record the root with
+// the reference's 1e-9 dedup (surfaces.py:672-674).
 template <bool kRecord>
 __device__ void newton_root(const double* __restrict__ P48, double qa, double qb, double qc,
                             double u, double v, const DevParams& prm, RootAcc<kRecord>& acc) {
-  double bu[4], dbu[4], bv[4], dbv[4];
-  double A, Au, Av, B, Bu, Bv;
-  bool conv = false;
-  for (int it = 0; it < kNewtonMax; ++it) {
-    bern3(u, bu, dbu);
-    bern3(v, bv, dbv);
-    eval_coord(P48, bu, dbu, bv, dbv, A, Au, Av);
-    eval_coord(P48 + 16, bu, dbu, bv, dbv, B, Bu, Bv);
-    A -= qa;
-    B -= qb;
-    acc.newton++;
-    double det = Au * Bv - Av * Bu;
-    if (!(fabs(det) > 0.0)) break;
-    double id = 1.0 / det;
-    double du = (Bv * A - Av * B) * id, dv = (Au * B - Bu * A) * id;
-    if (!isfinite(du) || !isfinite(dv)) break;
-    if (fabs(du) <= 2e-16 * fmax(1.0, fabs(u)) && fabs(dv) <= 2e-16 * fmax(1.0, fabs(v))) {
-      conv = true;
-      break;
-    }
-    u -= du;
-    v -= dv;
-    if (fabs(u) > 8.0 || fabs(v) > 8.0) break;  // left the patch neighbourhood
-  }
-  if (!conv) {
-    // final evaluation at the last iterate (xtol-style stop, surfaces.py:662)
-    bern3(u, bu, dbu);
-    bern3(v, bv, dbv);
-    eval_coord(P48, bu, dbu, bv, dbv, A, Au, Av);
-    eval_coord(P48 + 16, bu, dbu, bv, dbv, B, Bu, Bv);
-    A -= qa;
-    B -= qb;
-  }
-  if (!(sqrt(A * A + B * B) <= prm.residual)) return;                 // surfaces.py:665
-  const double tol = prm.domain_tol;                                  // surfaces.py:668
-  if (!(u >= -tol && u <= 1.0 + tol && v >= -tol && v <= 1.0 + tol)) return;
-  double C, Cu, Cv;
-  eval_coord(P48 + 32, bu, dbu, bv, dbv, C, Cu, Cv);
-  double t = C - qc;
-  if (t < -prm.t_tol) return;                                         // surfaces.py:670
-  for (int k = 0; k < acc.n; ++k)                                     // surfaces.py:672-674
-    if (fabs(acc.t[k] - t) < prm.dedup) return;
+  RootResult r = newton_solve(P48, qa, qb, qc, u, v, prm);
+  acc.newton += r.iters;
+  if (r.status != ROOT_ACCEPTED) return;
+  for (int k = 0; k < acc.n; ++k)
+    if (fabs(acc.t[k] - r.t) < prm.dedup) return;
   if (acc.n >= kMaxRoots) {
     acc.flags |= FLAG_RESHOOT;
     return;
   }
   const int k = acc.n++;
-  acc.t[k] = t;
-  // record (surfaces.py:681-697) in the right-handed ray frame: d = (0,0,1)
-  double nx = Bu * Cv - Cu * Bv, ny = Cu * Av - Au * Cv, nz = Au * Bv - Bu * Av;
-  double nn = sqrt(nx * nx + ny * ny + nz * nz);
-  int32_t sign = 1, tang = 1, graze = 1;
-  if (!(nn < prm.degenerate)) {                                       // surfaces.py:684-687
-    double dd = nz / nn;
-    sign = dd > 0.0 ? 1 : -1;                                         // surfaces.py:695
-    tang = fabs(dd) <= prm.tangent;                                   // :696 tangency
-    double bd = fmin(fmin(u, 1.0 - u), fmin(v, 1.0 - v));
-    graze = bd < prm.edge_graze;                                      // :697 grazing
-  }
-  acc.chi += sign;
-  if (tang || graze) acc.flags |= FLAG_RESHOOT;
-  if (fabs(t) <= prm.on_surface_t) acc.flags |= FLAG_ONSURF;
+  acc.t[k] = r.t;
+  acc.chi += r.sign;
+  if (r.tang || r.graze) acc.flags |= FLAG_RESHOOT;
+  if (r.onsurf) acc.flags |= FLAG_ONSURF;
   if constexpr (kRecord) {
-    acc.u[k] = u;
-    acc.v[k] = v;
-    acc.sign[k] = sign;
-    acc.tang[k] = tang;
-    acc.graze[k] = graze;
+    acc.u[k] = r.u;
+    acc.v[k] = r.v;
+    acc.sign[k] = r.sign;
+    acc.tang[k] = r.tang;
+    acc.graze[k] = r.graze;
   }
 }
 
@@ -391,18 +213,7 @@ k_intersect(int64_t npairs, const int32_t* __restrict__ pair_slot,
   // query slot (pairs are grouped by slot), one atomic per segment.
   const int lane = threadIdx.x & 31;
   int32_t chi = r.chi, fl = r.flags;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int32_t s_up = __shfl_up_sync(0xffffffffu, slot, o);
-    int32_t c_up = __shfl_up_sync(0xffffffffu, chi, o);
-    int32_t f_up = __shfl_up_sync(0xffffffffu, fl, o);
-    if (lane >= o && s_up == slot) {
-      chi += c_up;
-      fl |= f_up;
-    }
-  }
-  int32_t s_next = __shfl_down_sync(0xffffffffu, slot, 1);
-  bool tail = (lane == 31) || (s_next != slot);
+  const bool tail = seg_reduce(slot, chi, fl);
   if (slot >= 0 && tail) {
     if (chi) atomicAdd(&chi_acc[slot], chi);
     if (fl) atomicOr(&flag_acc[slot], fl);
@@ -412,7 +223,7 @@ k_intersect(int64_t npairs, const int32_t* __restrict__ pair_slot,
   warp_add_u64(&counters[CNT_ROOTS], (unsigned long long)r.roots);
 }
 
-cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, int64_t npairs,
+cudaError_t launch_intersect_dfs(const gwn_scene* sc, const Round& rd, int64_t npairs,
                              const int32_t* pair_slot, const int32_t* pair_patch,
                              const double* qproj, int32_t* chi, int32_t* flags,
                              unsigned long long* counters, cudaStream_t st) {

@@ -1,0 +1,255 @@
+// gwn_patch.cuh -- device helpers for projected bicubic nets (K3).
+//
+// A node net is the (a, b) pair of 4x4 ray-frame coordinates of a sub-patch
+// minus the query's projection, index 4*i+j with i the u index.
+#pragma once
+
+#include "gwn_internal.h"
+
+namespace gwn {
+
+constexpr int kMaxLevel = 44;
+constexpr int kNodeBudget = 4096;
+constexpr int kNewtonMax = 16;
+
+__device__ __forceinline__ void bern3(double t, double b[4], double db[4]) {
+  double s = 1.0 - t;
+  b[0] = s * s * s;
+  b[1] = 3.0 * t * s * s;
+  b[2] = 3.0 * t * t * s;
+  b[3] = t * t * t;
+  db[0] = -3.0 * s * s;
+  db[1] = 3.0 * s * (s - 2.0 * t);
+  db[2] = 3.0 * t * (2.0 * s - t);
+  db[3] = 3.0 * t * t;
+}
+
+// value and partials of one projected coordinate net X (16) at (u,v)
+__device__ __forceinline__ void eval_coord(const double* __restrict__ X, const double bu[4],
+                                           const double dbu[4], const double bv[4],
+                                           const double dbv[4], double& f, double& fu,
+                                           double& fv) {
+  double r[4], rv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    r[i] = bv[0] * X[4 * i] + bv[1] * X[4 * i + 1] + bv[2] * X[4 * i + 2] + bv[3] * X[4 * i + 3];
+    rv[i] = dbv[0] * X[4 * i] + dbv[1] * X[4 * i + 1] + dbv[2] * X[4 * i + 2] +
+            dbv[3] * X[4 * i + 3];
+  }
+  f = bu[0] * r[0] + bu[1] * r[1] + bu[2] * r[2] + bu[3] * r[3];
+  fu = dbu[0] * r[0] + dbu[1] * r[1] + dbu[2] * r[2] + dbu[3] * r[3];
+  fv = bu[0] * rv[0] + bu[1] * rv[1] + bu[2] * rv[2] + bu[3] * rv[3];
+}
+
+// de Casteljau halving of 4 values: (p0..p3) -> left in p, right in q
+__device__ __forceinline__ void half4(double& p0, double& p1, double& p2, double& p3, double& q0,
+                                      double& q1, double& q2, double& q3) {
+  double a01 = 0.5 * (p0 + p1), a12 = 0.5 * (p1 + p2), a23 = 0.5 * (p2 + p3);
+  double b0 = 0.5 * (a01 + a12), b1 = 0.5 * (a12 + a23);
+  double c = 0.5 * (b0 + b1);
+  q3 = p3; q2 = a23; q1 = b1; q0 = c;
+  p1 = a01; p2 = b0; p3 = c;
+}
+
+// Split net (a,b) along u (dir 0) or v (dir 1); left half stays in (a,b),
+// right half is written to (ra, rb).
+__device__ __forceinline__ void split_net(double* a, double* b, double* ra, double* rb, int dir) {
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    int i0 = dir == 0 ? l : 4 * l;
+    int st = dir == 0 ? 4 : 1;
+    half4(a[i0], a[i0 + st], a[i0 + 2 * st], a[i0 + 3 * st], ra[i0], ra[i0 + st],
+          ra[i0 + 2 * st], ra[i0 + 3 * st]);
+    half4(b[i0], b[i0 + st], b[i0 + 2 * st], b[i0 + 3 * st], rb[i0], rb[i0 + st],
+          rb[i0 + 2 * st], rb[i0 + 3 * st]);
+  }
+}
+
+__device__ __forceinline__ bool box_has_origin(const double* a, const double* b, double eps) {
+  double amin = a[0], amax = a[0], bmin = b[0], bmax = b[0];
+#pragma unroll
+  for (int k = 1; k < 16; ++k) {
+    amin = fmin(amin, a[k]); amax = fmax(amax, a[k]);
+    bmin = fmin(bmin, b[k]); bmax = fmax(bmax, b[k]);
+  }
+  return amin <= eps && amax >= -eps && bmin <= eps && bmax >= -eps;
+}
+
+// Krawczyk test on the node net (local coords s in [0,1]^2).
+// Returns 0 exclude, 1 unique root (s0,s1 = Newton-predicted root), 2 split.
+// xlo/xhi: exclusion box in local coords (domain-tolerance expansion).
+__device__ __forceinline__ int krawczyk(const double* a, const double* b, double xlo_u,
+                                        double xhi_u, double xlo_v, double xhi_v, double& s0,
+                                        double& s1) {
+  const double w3[4] = {0.125, 0.375, 0.375, 0.125};
+  const double w2[3] = {0.25, 0.5, 0.25};
+  double ga = 0.0, gb = 0.0, Jua = 0.0, Jub = 0.0, Jva = 0.0, Jvb = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double w = w3[i] * w3[j];
+      ga += w * a[4 * i + j];
+      gb += w * b[4 * i + j];
+      if (i < 3) {
+        double wu = w2[i] * w3[j];
+        Jua += wu * (a[4 * (i + 1) + j] - a[4 * i + j]);
+        Jub += wu * (b[4 * (i + 1) + j] - b[4 * i + j]);
+      }
+      if (j < 3) {
+        double wv = w3[i] * w2[j];
+        Jva += wv * (a[4 * i + j + 1] - a[4 * i + j]);
+        Jvb += wv * (b[4 * i + j + 1] - b[4 * i + j]);
+      }
+    }
+  }
+  // derivative nets are 3 x differences; fold the 3 into Y
+  double det = Jua * Jvb - Jva * Jub;
+  if (!(fabs(det) > 1e-300) || !isfinite(det)) return 2;
+  double id = 1.0 / det;
+  double Y00 = Jvb * id, Y01 = -Jva * id, Y10 = -Jub * id, Y11 = Jua * id;  // (J/3)^-1
+  double d0 = (Y00 * ga + Y01 * gb) * (1.0 / 3.0);
+  double d1 = (Y10 * ga + Y11 * gb) * (1.0 / 3.0);
+  double e11 = 0.0, e21 = 0.0, e12 = 0.0, e22 = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double qa = a[4 * (i + 1) + j] - a[4 * i + j], qb = b[4 * (i + 1) + j] - b[4 * i + j];
+      e11 = fmax(e11, fabs(Y00 * qa + Y01 * qb - 1.0));
+      e21 = fmax(e21, fabs(Y10 * qa + Y11 * qb));
+    }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double qa = a[4 * i + j + 1] - a[4 * i + j], qb = b[4 * i + j + 1] - b[4 * i + j];
+      e12 = fmax(e12, fabs(Y00 * qa + Y01 * qb));
+      e22 = fmax(e22, fabs(Y10 * qa + Y11 * qb - 1.0));
+    }
+  // rounding + 1e-7 box expansion margins
+  const double rad = 0.5 + 1e-7;
+  double r0 = (e11 + e12) * rad * (1.0 + 1e-9) + 1e-12;
+  double r1 = (e21 + e22) * rad * (1.0 + 1e-9) + 1e-12;
+  s0 = 0.5 - d0;
+  s1 = 0.5 - d1;
+  if (!isfinite(s0) || !isfinite(s1)) return 2;
+  if (s0 + r0 < xlo_u || s0 - r0 > xhi_u || s1 + r1 < xlo_v || s1 - r1 > xhi_v) return 0;
+  if (s0 - r0 > -1e-7 && s0 + r0 < 1.0 + 1e-7 && s1 - r1 > -1e-7 && s1 + r1 < 1.0 + 1e-7)
+    return 1;
+  return 2;
+}
+
+
+// Segmented warp-shuffle reduction keyed by `key` (K5): sums `v` and ORs `f`
+// over each maximal run of equal keys among adjacent lanes; returns true on the
+// lane that ends its run (that lane holds the run totals).  Works for any key
+// order: runs are delimited by head flags, not by key equality at a distance.
+__device__ __forceinline__ bool seg_reduce(int32_t key, int32_t& v, int32_t& f) {
+  const int lane = threadIdx.x & 31;
+  const int32_t kprev = __shfl_up_sync(0xffffffffu, key, 1);
+  int start = (lane == 0 || kprev != key) ? lane : 0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {  // max-scan of run heads -> run start lane
+    int s = __shfl_up_sync(0xffffffffu, start, o);
+    if (lane >= o) start = max(start, s);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t vu = __shfl_up_sync(0xffffffffu, v, o);
+    int32_t fu = __shfl_up_sync(0xffffffffu, f, o);
+    if (lane - o >= start) {
+      v += vu;
+      f |= fu;
+    }
+  }
+  const int32_t knext = __shfl_down_sync(0xffffffffu, key, 1);
+  return lane == 31 || knext != key;
+}
+
+// Outcome of a Newton solve started inside a node (surfaces.py:664-700 rules).
+enum : int { ROOT_ACCEPTED = 0, ROOT_REJECTED = 1, ROOT_DIVERGED = 2 };
+
+struct RootResult {
+  int status;
+  double u, v, t;
+  int32_t sign, tang, graze, onsurf;
+  int32_t iters;
+};
+
+// Newton on the whole patch from (u, v); residual / domain / t acceptance of
+// surfaces.py:665-670, record fields of surfaces.py:681-697 in the
+// right-handed ray frame (d = (0,0,1)).
+__device__ __forceinline__ RootResult newton_solve(const double* __restrict__ P48, double qa,
+                                                   double qb, double qc, double u, double v,
+                                                   const DevParams& prm) {
+  RootResult r;
+  r.iters = 0;
+  double bu[4], dbu[4], bv[4], dbv[4];
+  double A, Au, Av, B, Bu, Bv;
+  bool conv = false;
+  for (int it = 0; it < kNewtonMax; ++it) {
+    bern3(u, bu, dbu);
+    bern3(v, bv, dbv);
+    eval_coord(P48, bu, dbu, bv, dbv, A, Au, Av);
+    eval_coord(P48 + 16, bu, dbu, bv, dbv, B, Bu, Bv);
+    A -= qa;
+    B -= qb;
+    r.iters++;
+    double det = Au * Bv - Av * Bu;
+    if (!(fabs(det) > 0.0)) break;
+    double id = 1.0 / det;
+    double du = (Bv * A - Av * B) * id, dv = (Au * B - Bu * A) * id;
+    if (!isfinite(du) || !isfinite(dv)) break;
+    if (fabs(du) <= 2e-16 * fmax(1.0, fabs(u)) && fabs(dv) <= 2e-16 * fmax(1.0, fabs(v))) {
+      conv = true;
+      break;
+    }
+    u -= du;
+    v -= dv;
+    if (fabs(u) > 8.0 || fabs(v) > 8.0) break;  // left the patch neighbourhood
+  }
+  if (!conv) {
+    bern3(u, bu, dbu);
+    bern3(v, bv, dbv);
+    eval_coord(P48, bu, dbu, bv, dbv, A, Au, Av);
+    eval_coord(P48 + 16, bu, dbu, bv, dbv, B, Bu, Bv);
+    A -= qa;
+    B -= qb;
+  }
+  r.u = u;
+  r.v = v;
+  r.t = 0.0;
+  r.sign = 0; r.tang = 0; r.graze = 0; r.onsurf = 0;
+  if (!(sqrt(A * A + B * B) <= prm.residual)) {                        // surfaces.py:665
+    r.status = ROOT_DIVERGED;
+    return r;
+  }
+  const double tol = prm.domain_tol;                                   // surfaces.py:668
+  if (!(u >= -tol && u <= 1.0 + tol && v >= -tol && v <= 1.0 + tol)) {
+    r.status = ROOT_REJECTED;
+    return r;
+  }
+  double C, Cu, Cv;
+  eval_coord(P48 + 32, bu, dbu, bv, dbv, C, Cu, Cv);
+  r.t = C - qc;
+  if (r.t < -prm.t_tol) {                                              // surfaces.py:670
+    r.status = ROOT_REJECTED;
+    return r;
+  }
+  double nx = Bu * Cv - Cu * Bv, ny = Cu * Av - Au * Cv, nz = Au * Bv - Bu * Av;
+  double nn = sqrt(nx * nx + ny * ny + nz * nz);
+  r.sign = 1; r.tang = 1; r.graze = 1;
+  if (!(nn < prm.degenerate)) {                                        // surfaces.py:684-687
+    double dd = nz / nn;
+    r.sign = dd > 0.0 ? 1 : -1;                                        // surfaces.py:695
+    r.tang = fabs(dd) <= prm.tangent;                                  // :696 tangency
+    double bd = fmin(fmin(u, 1.0 - u), fmin(v, 1.0 - v));
+    r.graze = bd < prm.edge_graze;                                     // :697 grazing
+  }
+  r.onsurf = fabs(r.t) <= prm.on_surface_t;
+  r.status = ROOT_ACCEPTED;
+  return r;
+}
+
+}  // namespace gwn

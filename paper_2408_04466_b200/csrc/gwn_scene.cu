@@ -257,6 +257,14 @@ extern "C" int gwn_scene_create(const double* ctrl, int64_t P, const gwn_params*
     return GWN_E_NODEVICE;
   }
   sc->sm_count = prop.multiProcessorCount;
+  {
+    // keep stream-ordered workspace cached across evals (default threshold 0
+    // would unmap it at every synchronisation)
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   // scene box (Aabb.of_points over every control point, geometry.py:70-73)
   for (int k = 0; k < 3; ++k) {
     sc->bbox_min[k] = P ? INFINITY : 0.0;
