@@ -58,7 +58,6 @@ __device__ __forceinline__ void renorm(SegState& s) {
 struct Vtx {
   double ux, uy, uz;   // a^ - d
   double gx, gy, gz;   // d x u
-  double rx, ry, rz;   // x - p (band test only)
   double l;            // |x - p|
   bool ok;
 };
@@ -66,46 +65,50 @@ struct Vtx {
 __device__ __forceinline__ Vtx make_vtx(double x, double y, double z, double px, double py,
                                         double pz, double dx, double dy, double dz, double deg) {
   Vtx v;
-  v.rx = x - px; v.ry = y - py; v.rz = z - pz;
-  const double l2 = v.rx * v.rx + v.ry * v.ry + v.rz * v.rz;
+  const double rx = x - px, ry = y - py, rz = z - pz;
+  const double l2 = rx * rx + ry * ry + rz * rz;
   const double il = rsqrt(l2);
   v.l = l2 * il;
   v.ok = v.l >= deg;
-  v.ux = fma(v.rx, il, -dx);
-  v.uy = fma(v.ry, il, -dy);
-  v.uz = fma(v.rz, il, -dz);
+  v.ux = fma(rx, il, -dx);
+  v.uy = fma(ry, il, -dy);
+  v.uz = fma(rz, il, -dz);
   v.gx = dy * v.uz - dz * v.uy;
   v.gy = dz * v.ux - dx * v.uz;
   v.gz = dx * v.uy - dy * v.ux;
   return v;
 }
 
-// One segment (a, b): accumulate and run the (rare) band test.
+// polyline/curve band test (rare path, den < 0): d within band_factor*h/dist
+// of the arc (a, b).  Raw offsets are recovered as (u + d) * l.
+__device__ __forceinline__ bool band_hit(const Vtx& a, const Vtx& b, double num, double dx,
+                                      double dy, double dz, double h, double band_factor) {
+  const double ax = a.ux + dx, ay = a.uy + dy, az = a.uz + dz;
+  const double bx = b.ux + dx, by = b.uy + dy, bz = b.uz + dz;
+  const double sgx = bx * b.l - ax * a.l, sgy = by * b.l - ay * a.l, sgz = bz * b.l - az * a.l;
+  const double L = sqrt(sgx * sgx + sgy * sgy + sgz * sgz);
+  const double dist = fmin(a.l, b.l) - L;
+  if (dist <= 0.0) return true;
+  const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
+  const double s2 = cx * cx + cy * cy + cz * cz;
+  const double th = band_factor * h / dist;
+  return num * num <= th * th * s2;
+}
+
+// One segment (a, b): accumulate; the band test runs only when den < 0.
 __device__ __forceinline__ void fan_segment(SegState& st, const Vtx& a, const Vtx& b, double dx,
-                                            double dy, double dz, double h, double band_factor,
-                                            int& flags) {
+                                            double dy, double dz, const double* band_h,
+                                            int64_t e, double band_factor, int& flags) {
   const double den = a.ux * b.ux + a.uy * b.uy + a.uz * b.uz;
   const double num = -(a.gx * b.ux + a.gy * b.uy + a.gz * b.uz);
   const bool ok = a.ok && b.ok;
-  if (den < 0.0 && ok && h > 0.0) {
-    // polyline/curve band: d within band_factor * h / dist of the arc
-    const double sgx = b.rx - a.rx, sgy = b.ry - a.ry, sgz = b.rz - a.rz;
-    const double L = sqrt(sgx * sgx + sgy * sgy + sgz * sgz);
-    const double dist = fmin(a.l, b.l) - L;
-    const double ax = a.ux + dx, ay = a.uy + dy, az = a.uz + dz;
-    const double bx = b.ux + dx, by = b.uy + dy, bz = b.uz + dz;
-    const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
-    const double s2 = cx * cx + cy * cy + cz * cz;
-    if (dist <= 0.0) {
-      flags |= FLAG_BAND;
-    } else {
-      const double th = band_factor * h / dist;
-      if (num * num <= th * th * s2) flags |= FLAG_BAND;
-    }
+  if (den < 0.0 && ok && band_h) {
+    if (band_hit(a, b, num, dx, dy, dz, __ldg(band_h + e), band_factor)) flags |= FLAG_BAND;
   }
   cmul_track(st, ok ? den : 1.0, ok ? num : 0.0);
 }
 
+template <int QPT>
 __global__ void __launch_bounds__(kBlockQ)
 k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
            const double* __restrict__ verts, int64_t V, int S,
@@ -113,50 +116,67 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
            double* __restrict__ bterm, int32_t* __restrict__ flag_acc,
            unsigned long long* __restrict__ counters) {
   __shared__ double sx[kTileV], sy[kTileV], sz[kTileV];
-  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = s < m;
-  const int32_t q = live ? (active ? active[s] : s) : 0;
-  const double px = live ? pos[3 * (int64_t)q] : 0.0;
-  const double py = live ? pos[3 * (int64_t)q + 1] : 0.0;
-  const double pz = live ? pos[3 * (int64_t)q + 2] : 0.0;
   const double dx = f.d[0], dy = f.d[1], dz = f.d[2];
   const double deg = prm.degenerate;
-  SegState st = {1.0, 0.0, 0};
-  int flags = 0;
-  Vtx va;
-  va.ok = false;
+  int32_t slot[QPT];
+  double px[QPT], py[QPT], pz[QPT];
+  SegState st[QPT];
+  int flags[QPT];
+  Vtx va[QPT];
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) {
+    slot[j] = blockIdx.x * (blockDim.x * QPT) + j * blockDim.x + threadIdx.x;
+    const bool live = slot[j] < m;
+    const int32_t q = live ? (active ? active[slot[j]] : slot[j]) : 0;
+    px[j] = live ? pos[3 * (int64_t)q] : 0.0;
+    py[j] = live ? pos[3 * (int64_t)q + 1] : 0.0;
+    pz[j] = live ? pos[3 * (int64_t)q + 2] : 0.0;
+    st[j] = SegState{1.0, 0.0, 0};
+    flags[j] = 0;
+    va[j].ok = false;
+  }
   int nseg = 0;
   for (int64_t t0 = 0; t0 < V; t0 += kTileV) {
     const int nt = (int)min((int64_t)kTileV, V - t0);
     __syncthreads();
     for (int k = threadIdx.x; k < nt; k += blockDim.x) {
-      int64_t g = t0 + k;
+      const int64_t g = t0 + k;
       sx[k] = verts[g];
       sy[k] = verts[V + g];
       sz[k] = verts[2 * V + g];
     }
     __syncthreads();
-    int kin = (int)(t0 % S);  // index within its edge of the tile's first vertex
+    int64_t e = t0 / S;               // edge of the tile's first vertex
+    int kin = (int)(t0 - e * S);      // its index within that edge
     for (int k = 0; k < nt; ++k) {
-      Vtx vb = make_vtx(sx[k], sy[k], sz[k], px, py, pz, dx, dy, dz, deg);
-      if (!vb.ok) flags |= FLAG_DEGEN;
-      if (kin != 0) {  // segment (k-1, k) lies on one edge
-        const double h = (va.ok && vb.ok) ? __ldg(band_h + (t0 + k) / S) : 0.0;
-        fan_segment(st, va, vb, dx, dy, dz, h, prm.band_factor, flags);
-        ++nseg;
-        if ((nseg & 7) == 0) renorm(st);
+      const double x = sx[k], y = sy[k], z = sz[k];
+#pragma unroll
+      for (int j = 0; j < QPT; ++j) {
+        const Vtx vb = make_vtx(x, y, z, px[j], py[j], pz[j], dx, dy, dz, deg);
+        if (!vb.ok) flags[j] |= FLAG_DEGEN;
+        if (kin != 0) fan_segment(st[j], va[j], vb, dx, dy, dz, band_h, e, prm.band_factor, flags[j]);
+        va[j] = vb;
       }
-      va = vb;
-      if (++kin == S) kin = 0;
+      if (kin != 0 && (++nseg & 7) == 0) {
+#pragma unroll
+        for (int j = 0; j < QPT; ++j) renorm(st[j]);
+      }
+      if (++kin == S) {
+        kin = 0;
+        ++e;
+      }
     }
   }
-  if (live) {
-    const double ang = atan2(st.Zi, st.Zr) + 6.283185307179586476925 * (double)st.wraps;
-    bterm[s] = ang * 0.15915494309189533576888;  // (2 ang) / (4 pi)
-    if (flags) atomicOr(&flag_acc[s], flags);
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) {
+    if (slot[j] < m) {
+      const double ang = atan2(st[j].Zi, st[j].Zr) + 6.283185307179586476925 * (double)st[j].wraps;
+      bterm[slot[j]] = ang * 0.15915494309189533576888;  // (2 ang) / (4 pi)
+      if (flags[j]) atomicOr(&flag_acc[slot[j]], flags[j]);
+    }
   }
   if (threadIdx.x == 0) {
-    int32_t nq = min((int32_t)blockDim.x, m - (int32_t)(blockIdx.x * blockDim.x));
+    int32_t nq = min((int32_t)(blockDim.x * QPT), m - (int32_t)(blockIdx.x * blockDim.x * QPT));
     int64_t segs = V - V / S;
     atomicAdd(&counters[CNT_SEGMENTS], (unsigned long long)(segs * nq));
   }
@@ -168,7 +188,8 @@ cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
   if (m <= 0) return cudaSuccess;
   int64_t V = sc->n_edges * sc->S;
   if (V == 0) return cudaMemsetAsync(bterm, 0, sizeof(double) * m, st);
-  k_boundary<<<(m + kBlockQ - 1) / kBlockQ, kBlockQ, 0, st>>>(
+  constexpr int QPT = 2;
+  k_boundary<QPT><<<(m + kBlockQ * QPT - 1) / (kBlockQ * QPT), kBlockQ, 0, st>>>(
       m, active, pos, sc->verts, V, sc->S, sc->band_h, rd.f, sc->dprm, bterm, flags, counters);
   return cudaGetLastError();
 }
@@ -201,7 +222,7 @@ __global__ void k_single_loop(const double* __restrict__ loop, int64_t B, double
   for (int64_t i = 0; i < B; ++i) {
     Vtx vb = make_vtx(loop[3 * i], loop[3 * i + 1], loop[3 * i + 2], px, py, pz, dx, dy, dz, deg);
     if (!va.ok || !vb.ok) bad = true;
-    fan_segment(st, va, vb, dx, dy, dz, 0.0, 0.0, flags);
+    fan_segment(st, va, vb, dx, dy, dz, nullptr, 0, 0.0, flags);
     if ((i & 7) == 7) renorm(st);
     va = vb;
   }

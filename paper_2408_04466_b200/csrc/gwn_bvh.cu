@@ -2,57 +2,131 @@
 //
 // Every query of round r casts its ray along the same direction d_r, so the
 // ray-patch cull is a 2-D point query in the plane normal to d_r: a ray from
-// p hits patch k's control hull only if (p.e1, p.e2) lies in the projected
-// hull's box and the patch extends past p along d_r.  We therefore project
-// the control nets once per round (replacing the per-(ray,patch) Aabb work of
-// surfaces.py:636-639 / geometry.py:198-219) and build a Karras LBVH over the
-// projected boxes: 30-bit Morton codes, CUB radix sort, one thread per
-// internal node, bottom-up refit with atomic arrival counters.
+// p can hit a piece of patch only if (p.e1, p.e2) lies in the piece's
+// projected control box and the piece extends past p along d_r.  Per round we
+// (1) project the control nets into the ray frame (replacing the
+// per-(ray,patch) Aabb work of surfaces.py:636-639 / geometry.py:198-219),
+// (2) cut every patch into adaptive leaf sub-patches carrying the
+// query-independent Krawczyk data, and (3) build a Karras LBVH
+// over the leaves' projected boxes: 30-bit Morton codes, CUB radix sort, one
+// thread per internal node, bottom-up refit with atomic arrival counters.
 #include <cub/cub.cuh>
 
-#include "gwn_internal.h"
+#include "gwn_patch.cuh"
 
 namespace gwn {
 
 __global__ void k_project(const double* __restrict__ ctrl, int64_t P, Frame f,
-                          double* __restrict__ proj, double* __restrict__ leafbox,
-                          uint32_t* __restrict__ keys, int32_t* __restrict__ ids, double amin,
-                          double ainv, double bmin, double binv) {
+                          double* __restrict__ proj) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   const double* X = ctrl + 48 * p;
   double* out = proj + 48 * p;
-  double alo = INFINITY, ahi = -INFINITY, blo = INFINITY, bhi = -INFINITY, chi = -INFINITY,
-         mag = 0.0;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     double x = X[3 * k], y = X[3 * k + 1], z = X[3 * k + 2];
-    double A = x * f.e1[0] + y * f.e1[1] + z * f.e1[2];
-    double B = x * f.e2[0] + y * f.e2[1] + z * f.e2[2];
-    double C = x * f.d[0] + y * f.d[1] + z * f.d[2];
-    out[k] = A;
-    out[16 + k] = B;
-    out[32 + k] = C;
-    alo = fmin(alo, A); ahi = fmax(ahi, A);
-    blo = fmin(blo, B); bhi = fmax(bhi, B);
-    chi = fmax(chi, C);
-    mag = fmax(mag, fmax(fabs(x), fmax(fabs(y), fabs(z))));
+    out[k] = x * f.e1[0] + y * f.e1[1] + z * f.e1[2];
+    out[16 + k] = x * f.e2[0] + y * f.e2[1] + z * f.e2[2];
+    out[32 + k] = x * f.d[0] + y * f.d[1] + z * f.d[2];
   }
-  // conservative expansion: projection rounding plus the 1e-9 parametric
-  // acceptance band of surfaces.py:668 (roots just outside the domain)
-  double ext = fmax(ahi - alo, bhi - blo);
-  double eps = 1e-12 * (1.0 + mag) + 3e-9 * ext;
-  double* lb = leafbox + 5 * p;
-  lb[0] = alo - eps; lb[1] = ahi + eps; lb[2] = blo - eps; lb[3] = bhi + eps; lb[4] = chi + eps;
-  // Morton code of the box centre in the scene's projected bounds
-  double ca = (0.5 * (alo + ahi) - amin) * ainv, cb = (0.5 * (blo + bhi) - bmin) * binv;
-  uint32_t ia = (uint32_t)fmin(fmax(ca * 32767.0, 0.0), 32767.0);
-  uint32_t ib = (uint32_t)fmin(fmax(cb * 32767.0, 0.0), 32767.0);
-  uint32_t code = 0;
-  for (int bit = 0; bit < 15; ++bit)
-    code |= (((ia >> bit) & 1u) << (2 * bit)) | (((ib >> bit) & 1u) << (2 * bit + 1));
-  keys[p] = code;
-  ids[p] = (int32_t)p;
+}
+
+// Adaptive leaf sub-patches of every patch for this direction: depth-first
+// subdivision (u/v alternating, as in K3) until the Krawczyk radii over the
+// leaf box expanded by kLeafM on each side are below kLeafRmax (every root in
+// the leaf then certifies from the precomputed data alone), or kLeafMaxLevel.
+// kFill = false: count leaves per patch; true: write LeafRec, the leaf's
+// control-box (cull primitive) and its Morton key.
+template <bool kFill>
+__global__ void k_leaves(int64_t P, const double* __restrict__ proj,
+                         const int64_t* __restrict__ offs, int64_t* __restrict__ counts,
+                         LeafRec* __restrict__ leaves, double* __restrict__ leafbox,
+                         uint32_t* __restrict__ keys, int32_t* __restrict__ ids, double amin,
+                         double ainv, double bmin, double binv) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const double* P48 = proj + 48 * p;
+  double mag = 0.0, alo = INFINITY, ahi = -INFINITY, blo = INFINITY, bhi = -INFINITY;
+  for (int k = 0; k < 16; ++k) {
+    const double A = P48[k], B = P48[16 + k], C = P48[32 + k];
+    mag = fmax(mag, fmax(fabs(A), fmax(fabs(B), fabs(C))));
+    alo = fmin(alo, A); ahi = fmax(ahi, A); blo = fmin(blo, B); bhi = fmax(bhi, B);
+  }
+  // conservative expansion: rounding + the 1e-9 parametric acceptance band of
+  // surfaces.py:668 (roots just outside the domain)
+  const double eps = 1e-12 * (1.0 + mag) + 3e-9 * fmax(ahi - alo, bhi - blo);
+  uint64_t stack[2 * kLeafMaxLevel + 4];
+  int top = 0;
+  stack[top++] = 0;  // root code
+  int64_t n = 0;
+  const int64_t o = kFill ? offs[p] : 0;
+  while (top > 0) {
+    const uint64_t code = stack[--top];
+    const int L = code_level(code);
+    const double wu = code_wu(L), wv = code_wv(L);
+    const double u0 = (double)code_iu(code) * wu, v0 = (double)code_iv(code) * wv;
+    double a[16], b[16];
+    for (int k = 0; k < 16; ++k) {
+      a[k] = P48[k];
+      b[k] = P48[16 + k];
+    }
+    extract_net(a, u0 - kLeafM * wu, u0 + (1.0 + kLeafM) * wu, v0 - kLeafM * wv,
+                v0 + (1.0 + kLeafM) * wv);
+    extract_net(b, u0 - kLeafM * wu, u0 + (1.0 + kLeafM) * wu, v0 - kLeafM * wv,
+                v0 + (1.0 + kLeafM) * wv);
+    const KrawPre kp = kraw_pre(a, b);
+    const bool leaf = (kp.ok && kp.R0 < kLeafRmax && kp.R1 < kLeafRmax) || L >= kLeafMaxLevel;
+    if (!leaf) {
+      const uint64_t iu = code_iu(code), iv = code_iv(code);
+      if ((L & 1) == 0) {
+        stack[top++] = make_code(L + 1, 2 * iu + 1, iv);
+        stack[top++] = make_code(L + 1, 2 * iu, iv);
+      } else {
+        stack[top++] = make_code(L + 1, iu, 2 * iv + 1);
+        stack[top++] = make_code(L + 1, iu, 2 * iv);
+      }
+      continue;
+    }
+    if (kFill) {
+      const int64_t li = o + n;
+      LeafRec r;
+      r.Ga = kp.Ga; r.Gb = kp.Gb;
+      r.Y00 = kp.Y00; r.Y01 = kp.Y01; r.Y10 = kp.Y10; r.Y11 = kp.Y11;
+      r.R0 = kp.R0; r.R1 = kp.R1;
+      r.code = code;
+      r.patch = (int32_t)p;
+      r.ok = kp.ok;
+      leaves[li] = r;
+      // the leaf's own control box (convex hull of the piece over D)
+      double c[16];
+      for (int k = 0; k < 16; ++k) {
+        a[k] = P48[k];
+        b[k] = P48[16 + k];
+        c[k] = P48[32 + k];
+      }
+      extract_net(a, u0, u0 + wu, v0, v0 + wv);
+      extract_net(b, u0, u0 + wu, v0, v0 + wv);
+      extract_net(c, u0, u0 + wu, v0, v0 + wv);
+      double la = INFINITY, ha = -INFINITY, lb = INFINITY, hb = -INFINITY, hc = -INFINITY;
+      for (int k = 0; k < 16; ++k) {
+        la = fmin(la, a[k]); ha = fmax(ha, a[k]);
+        lb = fmin(lb, b[k]); hb = fmax(hb, b[k]);
+        hc = fmax(hc, c[k]);
+      }
+      double* lbx = leafbox + 5 * li;
+      lbx[0] = la - eps; lbx[1] = ha + eps; lbx[2] = lb - eps; lbx[3] = hb + eps; lbx[4] = hc + eps;
+      const double ca = (0.5 * (la + ha) - amin) * ainv, cb = (0.5 * (lb + hb) - bmin) * binv;
+      const uint32_t ia = (uint32_t)fmin(fmax(ca * 32767.0, 0.0), 32767.0);
+      const uint32_t ib = (uint32_t)fmin(fmax(cb * 32767.0, 0.0), 32767.0);
+      uint32_t key = 0;
+      for (int bit = 0; bit < 15; ++bit)
+        key |= (((ia >> bit) & 1u) << (2 * bit)) | (((ib >> bit) & 1u) << (2 * bit + 1));
+      keys[li] = key;
+      ids[li] = (int32_t)li;
+    }
+    ++n;
+  }
+  if (!kFill) counts[p] = n;
 }
 
 __device__ __forceinline__ int lbvh_delta(const uint32_t* keys, int n, int i, int j) {
@@ -134,6 +208,7 @@ void free_round(Round& rd) {
   if (rd.proj) cudaFree(rd.proj);
   if (rd.nodes) cudaFree(rd.nodes);
   if (rd.leafbox) cudaFree(rd.leafbox);
+  if (rd.leaves) cudaFree(rd.leaves);
   rd = Round();
 }
 
@@ -163,10 +238,13 @@ cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st) {
       double binv = bmax > bmin ? 1.0 / (bmax - bmin) : 0.0;
       uint32_t *keys = nullptr, *keys2 = nullptr;
       int32_t *ids = nullptr, *ids2 = nullptr, *tmp = nullptr;
+      int64_t *lcount = nullptr, *loffs = nullptr;
       double* ibox = nullptr;
       void* cub_tmp = nullptr;
       size_t cub_bytes = 0;
-      const int n = (int)P;
+      int64_t nl = 0;
+      int n = 0;
+      unsigned lb = 0;
       const unsigned pb = (unsigned)((P + 127) / 128);
 #define RC(x)                     \
   do {                            \
@@ -174,34 +252,59 @@ cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st) {
     if (e != cudaSuccess) goto out; \
   } while (0)
       RC(cudaMalloc(&rd.proj, sizeof(double) * 48 * P));
-      RC(cudaMalloc(&rd.leafbox, sizeof(double) * 5 * P));
-      RC(cudaMalloc(&keys, sizeof(uint32_t) * P));
-      RC(cudaMalloc(&keys2, sizeof(uint32_t) * P));
-      RC(cudaMalloc(&ids, sizeof(int32_t) * P));
-      RC(cudaMalloc(&ids2, sizeof(int32_t) * P));
-      k_project<<<pb, 128, 0, st>>>(sc->ctrl, P, rd.f, rd.proj, rd.leafbox, keys, ids, amin,
-                                    ainv, bmin, binv);
+      k_project<<<pb, 128, 0, st>>>(sc->ctrl, P, rd.f, rd.proj);
       RC(cudaGetLastError());
-      if (P > 1) {
+      // leaves: count, scan, fill
+      RC(cudaMalloc(&lcount, sizeof(int64_t) * (P + 1)));
+      RC(cudaMalloc(&loffs, sizeof(int64_t) * (P + 1)));
+      RC(cudaMemsetAsync(lcount + P, 0, sizeof(int64_t), st));
+      k_leaves<false><<<(unsigned)((P + 63) / 64), 64, 0, st>>>(
+          P, rd.proj, nullptr, lcount, nullptr, nullptr, nullptr, nullptr, amin, ainv, bmin, binv);
+      RC(cudaGetLastError());
+      RC(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, lcount, loffs, (int)P + 1, st));
+      RC(cudaMalloc(&cub_tmp, cub_bytes));
+      RC(cub::DeviceScan::ExclusiveSum(cub_tmp, cub_bytes, lcount, loffs, (int)P + 1, st));
+      RC(cudaMemcpyAsync(&nl, loffs + P, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      RC(cudaStreamSynchronize(st));
+      cudaFree(cub_tmp);
+      cub_tmp = nullptr;
+      cub_bytes = 0;
+      if (nl <= 0 || nl > (1ll << 30)) {
+        e = cudaErrorInvalidValue;
+        goto out;
+      }
+      rd.n_leaves = nl;
+      n = (int)nl;
+      lb = (unsigned)((nl + 127) / 128);
+      RC(cudaMalloc(&rd.leaves, sizeof(LeafRec) * nl));
+      RC(cudaMalloc(&rd.leafbox, sizeof(double) * 5 * nl));
+      RC(cudaMalloc(&keys, sizeof(uint32_t) * nl));
+      RC(cudaMalloc(&keys2, sizeof(uint32_t) * nl));
+      RC(cudaMalloc(&ids, sizeof(int32_t) * nl));
+      RC(cudaMalloc(&ids2, sizeof(int32_t) * nl));
+      k_leaves<true><<<(unsigned)((P + 63) / 64), 64, 0, st>>>(
+          P, rd.proj, loffs, nullptr, rd.leaves, rd.leafbox, keys, ids, amin, ainv, bmin, binv);
+      RC(cudaGetLastError());
+      if (nl > 1) {
         RC(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, keys, keys2, ids, ids2, n, 0, 30,
                                            st));
         RC(cudaMalloc(&cub_tmp, cub_bytes));
         RC(cub::DeviceRadixSort::SortPairs(cub_tmp, cub_bytes, keys, keys2, ids, ids2, n, 0, 30,
                                            st));
-        RC(cudaMalloc(&rd.nodes, sizeof(Node) * (P - 1)));
-        RC(cudaMalloc(&tmp, sizeof(int32_t) * (5 * P)));
-        RC(cudaMalloc(&ibox, sizeof(double) * 5 * (P - 1)));
+        RC(cudaMalloc(&rd.nodes, sizeof(Node) * (nl - 1)));
+        RC(cudaMalloc(&tmp, sizeof(int32_t) * (5 * nl)));
+        RC(cudaMalloc(&ibox, sizeof(double) * 5 * (nl - 1)));
         {
           int32_t* left = tmp;
-          int32_t* right = tmp + P;
-          int32_t* parent_int = tmp + 2 * P;
-          int32_t* parent_leaf = tmp + 3 * P;
-          int32_t* arrive = tmp + 4 * P;
-          RC(cudaMemsetAsync(arrive, 0, sizeof(int32_t) * P, st));
-          RC(cudaMemsetAsync(parent_int, 0xff, sizeof(int32_t) * P, st));  // root parent = -1
-          k_karras<<<pb, 128, 0, st>>>(keys2, n, left, right, parent_int, parent_leaf);
+          int32_t* right = tmp + nl;
+          int32_t* parent_int = tmp + 2 * nl;
+          int32_t* parent_leaf = tmp + 3 * nl;
+          int32_t* arrive = tmp + 4 * nl;
+          RC(cudaMemsetAsync(arrive, 0, sizeof(int32_t) * nl, st));
+          RC(cudaMemsetAsync(parent_int, 0xff, sizeof(int32_t) * nl, st));  // root parent = -1
+          k_karras<<<lb, 128, 0, st>>>(keys2, n, left, right, parent_int, parent_leaf);
           RC(cudaGetLastError());
-          k_refit<<<pb, 128, 0, st>>>(n, ids2, rd.leafbox, left, right, parent_int, parent_leaf,
+          k_refit<<<lb, 128, 0, st>>>(n, ids2, rd.leafbox, left, right, parent_int, parent_leaf,
                                       arrive, ibox, rd.nodes);
           RC(cudaGetLastError());
         }
@@ -215,6 +318,8 @@ cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st) {
       if (tmp) cudaFree(tmp);
       if (ibox) cudaFree(ibox);
       if (cub_tmp) cudaFree(cub_tmp);
+      if (lcount) cudaFree(lcount);
+      if (loffs) cudaFree(loffs);
 #undef RC
       if (e != cudaSuccess) {
         free_round(rd);

@@ -3,10 +3,11 @@
 //
 // Replaces the reference's per-(ray, patch) `patch.aabb()` + ray_aabb_clip
 // (surfaces.py:636-639, geometry.py:198-219): with every ray of the round
-// parallel to d, a patch can be hit only if the query's projection
-// (p.e1, p.e2) lies in the patch's projected hull box and the patch reaches
+// parallel to d, a leaf sub-patch can be hit only if the query's projection
+// (p.e1, p.e2) lies in the leaf's projected control box and the leaf reaches
 // past p along d (cmax >= p.d).  Two passes with the same deterministic
-// traversal: count, (scan), fill -> pairs grouped by query slot.
+// traversal: count, (scan), fill -> (query slot, leaf) candidates grouped by
+// query slot.
 #include "gwn_internal.h"
 
 namespace gwn {
@@ -103,7 +104,7 @@ cudaError_t launch_cull_count(const gwn_scene* sc, const Round& rd, int32_t m,
                               const int32_t* active, const double* pos, int64_t* counts,
                               double* qproj, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
-  k_cull_count<<<(m + 127) / 128, 128, 0, st>>>(rd.nodes, rd.leafbox, sc->P, rd.f, m, active,
+  k_cull_count<<<(m + 127) / 128, 128, 0, st>>>(rd.nodes, rd.leafbox, rd.n_leaves, rd.f, m, active,
                                                 pos, counts, qproj);
   return cudaGetLastError();
 }
@@ -112,7 +113,7 @@ cudaError_t launch_cull_fill(const gwn_scene* sc, const Round& rd, int32_t m,
                              const int32_t* active, const double* pos, const int64_t* offs,
                              int32_t* pair_slot, int32_t* pair_patch, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
-  k_cull_fill<<<(m + 127) / 128, 128, 0, st>>>(rd.nodes, rd.leafbox, sc->P, rd.f, m, active, pos,
+  k_cull_fill<<<(m + 127) / 128, 128, 0, st>>>(rd.nodes, rd.leafbox, rd.n_leaves, rd.f, m, active, pos,
                                                offs, pair_slot, pair_patch);
   return cudaGetLastError();
 }

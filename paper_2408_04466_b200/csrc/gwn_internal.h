@@ -54,11 +54,15 @@ struct alignas(16) Node {
   int32_t child[2];
 };
 
+struct LeafRec;
+
 struct Round {
   Frame f;
-  double* proj = nullptr;     // (P,48)
-  Node* nodes = nullptr;      // (P-1)
-  double* leafbox = nullptr;  // (P,5) when P == 1 (root is a leaf)
+  double* proj = nullptr;      // (P,48)
+  int64_t n_leaves = 0;
+  LeafRec* leaves = nullptr;   // (n_leaves) adaptive leaf sub-patches
+  double* leafbox = nullptr;   // (n_leaves,5) cull boxes: a lo/hi, b lo/hi, c max
+  Node* nodes = nullptr;       // (n_leaves-1) LBVH over the leaf boxes
 };
 
 }  // namespace gwn

@@ -211,7 +211,6 @@ k_intersect(int64_t npairs, const int32_t* __restrict__ pair_slot,
   __syncwarp();
   // K5 part 1: segmented warp-shuffle reduction of (chi, flags) keyed by the
   // query slot (pairs are grouped by slot), one atomic per segment.
-  const int lane = threadIdx.x & 31;
   int32_t chi = r.chi, fl = r.flags;
   const bool tail = seg_reduce(slot, chi, fl);
   if (slot >= 0 && tail) {

@@ -75,14 +75,24 @@ __device__ __forceinline__ bool box_has_origin(const double* a, const double* b,
   return amin <= eps && amax >= -eps && bmin <= eps && bmax >= -eps;
 }
 
-// Krawczyk test on the node net (local coords s in [0,1]^2).
-// Returns 0 exclude, 1 unique root (s0,s1 = Newton-predicted root), 2 split.
-// xlo/xhi: exclusion box in local coords (domain-tolerance expansion).
-__device__ __forceinline__ int krawczyk(const double* a, const double* b, double xlo_u,
-                                        double xhi_u, double xlo_v, double xhi_v, double& s0,
-                                        double& s1) {
+// Query-independent part of the Krawczyk operator of a node net (local
+// coords t in [0,1]^2, centre 1/2):
+//   G  = value at the centre, Ys = J(c)^-1 (Newton step = Ys g),
+//   R  = radius of (I - J(c)^-1 J(D))(D - c) from the Bernstein hulls of the
+//        derivative nets.
+// For parallel rays only g(c) = G - q depends on the query, so G, Ys, R of a
+// sub-patch can be computed once per direction.
+struct KrawPre {
+  double Ga, Gb;
+  double Y00, Y01, Y10, Y11;
+  double R0, R1;
+  bool ok;
+};
+
+__device__ __forceinline__ KrawPre kraw_pre(const double* a, const double* b) {
   const double w3[4] = {0.125, 0.375, 0.375, 0.125};
   const double w2[3] = {0.25, 0.5, 0.25};
+  KrawPre k;
   double ga = 0.0, gb = 0.0, Jua = 0.0, Jub = 0.0, Jva = 0.0, Jvb = 0.0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -103,13 +113,19 @@ __device__ __forceinline__ int krawczyk(const double* a, const double* b, double
       }
     }
   }
-  // derivative nets are 3 x differences; fold the 3 into Y
-  double det = Jua * Jvb - Jva * Jub;
-  if (!(fabs(det) > 1e-300) || !isfinite(det)) return 2;
-  double id = 1.0 / det;
-  double Y00 = Jvb * id, Y01 = -Jva * id, Y10 = -Jub * id, Y11 = Jua * id;  // (J/3)^-1
-  double d0 = (Y00 * ga + Y01 * gb) * (1.0 / 3.0);
-  double d1 = (Y10 * ga + Y11 * gb) * (1.0 / 3.0);
+  k.Ga = ga;
+  k.Gb = gb;
+  // derivative nets are 3 x differences: J(c) = 3 Jd, Y = Jd^-1 bounds the
+  // preconditioned derivative hull, Ys = Y / 3 is the Newton step matrix
+  const double det = Jua * Jvb - Jva * Jub;
+  k.ok = fabs(det) > 1e-300 && isfinite(det);
+  if (!k.ok) {
+    k.Y00 = k.Y01 = k.Y10 = k.Y11 = 0.0;
+    k.R0 = k.R1 = INFINITY;
+    return k;
+  }
+  const double id = 1.0 / det;
+  const double Y00 = Jvb * id, Y01 = -Jva * id, Y10 = -Jub * id, Y11 = Jua * id;
   double e11 = 0.0, e21 = 0.0, e12 = 0.0, e22 = 0.0;
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -129,17 +145,90 @@ __device__ __forceinline__ int krawczyk(const double* a, const double* b, double
     }
   // rounding + 1e-7 box expansion margins
   const double rad = 0.5 + 1e-7;
-  double r0 = (e11 + e12) * rad * (1.0 + 1e-9) + 1e-12;
-  double r1 = (e21 + e22) * rad * (1.0 + 1e-9) + 1e-12;
-  s0 = 0.5 - d0;
-  s1 = 0.5 - d1;
+  k.R0 = (e11 + e12) * rad * (1.0 + 1e-9) + 1e-12;
+  k.R1 = (e21 + e22) * rad * (1.0 + 1e-9) + 1e-12;
+  k.Y00 = Y00 * (1.0 / 3.0);
+  k.Y01 = Y01 * (1.0 / 3.0);
+  k.Y10 = Y10 * (1.0 / 3.0);
+  k.Y11 = Y11 * (1.0 / 3.0);
+  return k;
+}
+
+// Query part: g = G - q at the centre -> predicted root t* = 1/2 - Ys g and
+// K = t* +- R.  Returns 0 exclude (K misses the exclusion box [xlo, xhi]),
+// 1 unique root in the certification box [clo, chi], 2 undecided.
+__device__ __forceinline__ int kraw_query(const KrawPre& k, double ga, double gb, double xlo_u,
+                                          double xhi_u, double xlo_v, double xhi_v, double clo,
+                                          double chi, double& s0, double& s1) {
+  if (!k.ok) return 2;
+  s0 = 0.5 - (k.Y00 * ga + k.Y01 * gb);
+  s1 = 0.5 - (k.Y10 * ga + k.Y11 * gb);
   if (!isfinite(s0) || !isfinite(s1)) return 2;
+  const double r0 = k.R0, r1 = k.R1;
   if (s0 + r0 < xlo_u || s0 - r0 > xhi_u || s1 + r1 < xlo_v || s1 - r1 > xhi_v) return 0;
-  if (s0 - r0 > -1e-7 && s0 + r0 < 1.0 + 1e-7 && s1 - r1 > -1e-7 && s1 + r1 < 1.0 + 1e-7)
-    return 1;
+  if (s0 - r0 > clo && s0 + r0 < chi && s1 - r1 > clo && s1 + r1 < chi) return 1;
   return 2;
 }
 
+// Krawczyk test on a query-shifted node net (local coords s in [0,1]^2).
+// Returns 0 exclude, 1 unique root (s0,s1 = Newton-predicted root), 2 split.
+// xlo/xhi: exclusion box in local coords (domain-tolerance expansion).
+__device__ __forceinline__ int krawczyk(const double* a, const double* b, double xlo_u,
+                                        double xhi_u, double xlo_v, double xhi_v, double& s0,
+                                        double& s1) {
+  const KrawPre k = kraw_pre(a, b);
+  return kraw_query(k, k.Ga, k.Gb, xlo_u, xhi_u, xlo_v, xhi_v, -1e-7, 1.0 + 1e-7, s0, s1);
+}
+
+// Blossom extraction of the cubic piece over [x0, x1] (general de Casteljau):
+// new control points f(x0,x0,x0), f(x0,x0,x1), f(x0,x1,x1), f(x1,x1,x1).
+__device__ __forceinline__ void extract4(double& p0, double& p1, double& p2, double& p3,
+                                         double x0, double x1) {
+  // stages with x0: l = (p01, p12, p23)(x0), m = (l01, l12)(x0)
+  const double a01 = fma(x0, p1 - p0, p0), a12 = fma(x0, p2 - p1, p1), a23 = fma(x0, p3 - p2, p2);
+  const double b0 = fma(x0, a12 - a01, a01), b1 = fma(x0, a23 - a12, a12);
+  const double c01 = fma(x1, p1 - p0, p0), c12 = fma(x1, p2 - p1, p1), c23 = fma(x1, p3 - p2, p2);
+  const double d0 = fma(x1, c12 - c01, c01), d1 = fma(x1, c23 - c12, c12);
+  const double q0 = fma(x0, b1 - b0, b0);   // f(x0,x0,x0)
+  const double q1 = fma(x1, b1 - b0, b0);   // f(x0,x0,x1)
+  const double q2 = fma(x0, d1 - d0, d0);   // f(x1,x1,x0)
+  const double q3 = fma(x1, d1 - d0, d0);   // f(x1,x1,x1)
+  p0 = q0; p1 = q1; p2 = q2; p3 = q3;
+}
+
+// extract the sub-net over [u0,u1] x [v0,v1] of a 16-value net, in place
+__device__ __forceinline__ void extract_net(double* x, double u0, double u1, double v0,
+                                            double v1) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) extract4(x[j], x[4 + j], x[8 + j], x[12 + j], u0, u1);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) extract4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3], v0, v1);
+}
+
+// Precomputed leaf sub-patch of a round (K1): the Krawczyk data over the
+// leaf box D expanded by kLeafM on every side (D'), so that every root in D
+// certifies from the leaf itself when R0, R1 < kLeafRmax.
+constexpr double kLeafM = 0.5;
+constexpr double kLeafRmax = 0.12;
+constexpr int kLeafMaxLevel = 12;
+
+struct alignas(16) LeafRec {
+  double Ga, Gb;
+  double Y00, Y01, Y10, Y11;
+  double R0, R1;
+  uint64_t code;   // level:6 | iu:29 | iv:29 in the patch's subdivision tree
+  int32_t patch;
+  int32_t ok;
+};
+
+__device__ __forceinline__ uint64_t make_code(int level, uint64_t iu, uint64_t iv) {
+  return ((uint64_t)level << 58) | (iu << 29) | iv;
+}
+__device__ __forceinline__ int code_level(uint64_t c) { return (int)(c >> 58); }
+__device__ __forceinline__ uint64_t code_iu(uint64_t c) { return (c >> 29) & ((1ull << 29) - 1); }
+__device__ __forceinline__ uint64_t code_iv(uint64_t c) { return c & ((1ull << 29) - 1); }
+__device__ __forceinline__ double code_wu(int level) { return ldexp(1.0, -((level + 1) >> 1)); }
+__device__ __forceinline__ double code_wv(int level) { return ldexp(1.0, -(level >> 1)); }
 
 // Segmented warp-shuffle reduction keyed by `key` (K5): sums `v` and ORs `f`
 // over each maximal run of equal keys among adjacent lanes; returns true on the

@@ -28,17 +28,11 @@ struct NodeItem {
 
 struct NewtonItem {
   int32_t pair;
-  int32_t kind;   // 0: certified, 1: level cap
+  int32_t kind;   // 0: certified node, 1: level cap, 2: certified leaf (expanded box)
   uint64_t code;
   double u, v;
 };
 
-__device__ __forceinline__ uint64_t make_code(int level, uint64_t iu, uint64_t iv) {
-  return ((uint64_t)level << 58) | (iu << 29) | iv;
-}
-__device__ __forceinline__ int code_level(uint64_t c) { return (int)(c >> 58); }
-__device__ __forceinline__ uint64_t code_iu(uint64_t c) { return (c >> 29) & ((1ull << 29) - 1); }
-__device__ __forceinline__ uint64_t code_iv(uint64_t c) { return c & ((1ull << 29) - 1); }
 
 struct RootNet {
   double a[16], b[16];
@@ -149,7 +143,7 @@ __device__ __forceinline__ void warp_sum_u64(unsigned long long* dst, unsigned l
 
 struct WaveArgs {
   const int32_t* pair_slot;
-  const int32_t* pair_patch;
+  int32_t* pair_patch;
   const double* qproj;
   const double* proj;
   DevParams prm;
@@ -163,69 +157,119 @@ struct WaveArgs {
   unsigned long long n_cap;
 };
 
-// One subdivision level.  Level 0: items are the pairs themselves.
+// K3 pass 0: one thread per (query, leaf) candidate.  The leaf's Krawczyk
+// data are query-independent (K1), so the test is ~20 flops: exclude,
+// certified (-> Newton item) or undecided (-> node wavefront from the leaf).
 __global__ void __launch_bounds__(128)
-k3_level(int level, int64_t npairs, const NodeItem* __restrict__ in,
-         const unsigned long long* __restrict__ in_count, NodeItem* __restrict__ out,
-         unsigned long long* __restrict__ out_count, unsigned long long out_cap, WaveArgs w) {
-  const int64_t n = level == 0 ? npairs : (int64_t)*in_count;
+k3_candidates(int64_t npairs, const int32_t* __restrict__ pair_leaf,
+              const LeafRec* __restrict__ leaves, NodeItem* __restrict__ out,
+              unsigned long long* __restrict__ out_count, unsigned long long out_cap, WaveArgs w) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long tested = 0;
+  // leaf box D inside the expanded certification box D' (local coords t)
+  const double span = 1.0 + 2.0 * kLeafM;
+  const double tl = kLeafM / span, th = (1.0 + kLeafM) / span;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < npairs; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool wantN = false, wantF = false;
+    int32_t pair = (int32_t)i;
+    uint64_t code = 0;
+    double nu_ = 0.0, nv_ = 0.0;
+    if (i < npairs) {
+      const LeafRec L = leaves[pair_leaf[i]];
+      w.pair_patch[i] = L.patch;
+      code = L.code;
+      const int32_t slot = w.pair_slot[i];
+      const double qa = w.qproj[3 * (int64_t)slot], qb = w.qproj[3 * (int64_t)slot + 1];
+      ++tested;
+      const int lev = code_level(code);
+      const double wu = code_wu(lev), wv = code_wv(lev);
+      const double u0 = (double)code_iu(code) * wu, v0 = (double)code_iv(code) * wv;
+      const double tol = w.prm.domain_tol;
+      const double xlo_u = tl - (u0 == 0.0 ? tol / (wu * span) : 0.0);
+      const double xhi_u = th + (u0 + wu == 1.0 ? tol / (wu * span) : 0.0);
+      const double xlo_v = tl - (v0 == 0.0 ? tol / (wv * span) : 0.0);
+      const double xhi_v = th + (v0 + wv == 1.0 ? tol / (wv * span) : 0.0);
+      KrawPre k;
+      k.Ga = L.Ga; k.Gb = L.Gb;
+      k.Y00 = L.Y00; k.Y01 = L.Y01; k.Y10 = L.Y10; k.Y11 = L.Y11;
+      k.R0 = L.R0; k.R1 = L.R1;
+      k.ok = L.ok != 0;
+      double s0, s1;
+      const int kr = kraw_query(k, L.Ga - qa, L.Gb - qb, xlo_u, xhi_u, xlo_v, xhi_v, -1e-7,
+                                1.0 + 1e-7, s0, s1);
+      if (kr == 1) {
+        wantN = true;
+        nu_ = u0 - kLeafM * wu + s0 * span * wu;
+        nv_ = v0 - kLeafM * wv + s1 * span * wv;
+      } else if (kr == 2) {
+        wantF = true;
+      }
+    }
+    long long k = warp_push(wantF, out_count, out_cap, w.overflow);
+    if (k >= 0) out[k] = NodeItem{pair, 0, code};
+    k = warp_push(wantN, w.n_count, w.n_cap, w.overflow);
+    if (k >= 0) w.nq[k] = NewtonItem{pair, 2, code, nu_, nv_};
+  }
+  warp_sum_u64(&w.counters[CNT_NODES], tested);
+}
+
+// One wavefront pass over undecided nodes (each item carries its own level).
+__global__ void __launch_bounds__(128)
+k3_level(const NodeItem* __restrict__ in, const unsigned long long* __restrict__ in_count,
+         NodeItem* __restrict__ out, unsigned long long* __restrict__ out_count,
+         unsigned long long out_cap, WaveArgs w) {
+  const int64_t n = (int64_t)*in_count;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   unsigned long long nodes = 0;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
-    bool live = i < n;
+    const bool live = i < n;
     int32_t pair = 0;
     uint64_t code = 0;
     if (live) {
-      if (level == 0) {
-        pair = (int32_t)i;
-      } else {
-        NodeItem it = in[i];
-        pair = it.pair;
-        code = it.code;
-      }
+      NodeItem it = in[i];
+      pair = it.pair;
+      code = it.code;
     }
+    const int level = code_level(code);
+    const uint64_t iu = code_iu(code), iv = code_iv(code);
     bool wantL = false, wantR = false, wantN = false;
     int kind = 0;
     double nu_ = 0.0, nv_ = 0.0;
-    uint64_t iu = code_iu(code), iv = code_iv(code);
     if (live) {
       const int32_t slot = w.pair_slot[pair];
       const double* P48 = w.proj + 48 * (int64_t)w.pair_patch[pair];
       const double qa = w.qproj[3 * (int64_t)slot], qb = w.qproj[3 * (int64_t)slot + 1];
       RootNet rn;
       load_root(P48, qa, qb, w.prm, rn);
-      bool go = level > 0 || box_has_origin(rn.a, rn.b, rn.eps_box);
-      if (go) {
-        ++nodes;
-        rebuild(rn.a, rn.b, level, iu, iv);
-        const double wu = ldexp(1.0, -((level + 1) >> 1));
-        const double wv = ldexp(1.0, -(level >> 1));
-        const double u0 = (double)iu * wu, v0 = (double)iv * wv;
-        const double tol = w.prm.domain_tol;
-        const double xlo_u = u0 == 0.0 ? -tol / wu : 0.0;
-        const double xhi_u = u0 + wu == 1.0 ? 1.0 + tol / wu : 1.0;
-        const double xlo_v = v0 == 0.0 ? -tol / wv : 0.0;
-        const double xhi_v = v0 + wv == 1.0 ? 1.0 + tol / wv : 1.0;
-        double s0, s1;
-        const int kr = krawczyk(rn.a, rn.b, xlo_u, xhi_u, xlo_v, xhi_v, s0, s1);
-        if (kr == 1) {
+      ++nodes;
+      rebuild(rn.a, rn.b, level, iu, iv);
+      const double wu = code_wu(level), wv = code_wv(level);
+      const double u0 = (double)iu * wu, v0 = (double)iv * wv;
+      const double tol = w.prm.domain_tol;
+      const double xlo_u = u0 == 0.0 ? -tol / wu : 0.0;
+      const double xhi_u = u0 + wu == 1.0 ? 1.0 + tol / wu : 1.0;
+      const double xlo_v = v0 == 0.0 ? -tol / wv : 0.0;
+      const double xhi_v = v0 + wv == 1.0 ? 1.0 + tol / wv : 1.0;
+      double s0, s1;
+      const int kr = krawczyk(rn.a, rn.b, xlo_u, xhi_u, xlo_v, xhi_v, s0, s1);
+      if (kr == 1) {
+        wantN = true;
+        nu_ = u0 + s0 * wu;
+        nv_ = v0 + s1 * wv;
+      } else if (kr == 2) {
+        if (level >= kMaxLevel) {
           wantN = true;
-          nu_ = u0 + s0 * wu;
-          nv_ = v0 + s1 * wv;
-        } else if (kr == 2) {
-          if (level >= kMaxLevel) {
-            wantN = true;
-            kind = 1;
-            nu_ = u0 + 0.5 * wu;
-            nv_ = v0 + 0.5 * wv;
-          } else {
-            child_boxes(rn.a, rn.b, level & 1, rn.eps_box, wantL, wantR);
-            const int add = (int)wantL + (int)wantR;
-            if (add && atomicAdd(&w.pair_nodes[pair], add) + add > kNodeBudget) {
-              atomicOr(&w.flags[slot], FLAG_RESHOOT);  // tangent-like explosion: re-shoot
-              wantL = wantR = false;
-            }
+          kind = 1;
+          nu_ = u0 + 0.5 * wu;
+          nv_ = v0 + 0.5 * wv;
+        } else {
+          child_boxes(rn.a, rn.b, level & 1, rn.eps_box, wantL, wantR);
+          const int add = (int)wantL + (int)wantR;
+          if (add && atomicAdd(&w.pair_nodes[pair], add) + add > kNodeBudget) {
+            atomicOr(&w.flags[slot], FLAG_RESHOOT);  // tangent-like explosion: re-shoot
+            wantL = wantR = false;
           }
         }
       }
@@ -248,7 +292,6 @@ k3_level(int level, int64_t npairs, const NodeItem* __restrict__ in,
 __global__ void __launch_bounds__(128) k3_newton(WaveArgs w) {
   const int64_t n = (int64_t)*w.n_count;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int lane = threadIdx.x & 31;
   unsigned long long iters = 0, roots = 0;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
@@ -267,7 +310,7 @@ __global__ void __launch_bounds__(128) k3_newton(WaveArgs w) {
       const double u1 = u0 + wu, v1 = v0 + wv;
       const double tol = w.prm.domain_tol;
       if (r.status == ROOT_DIVERGED) {
-        if (it.kind == 0) fl |= FLAG_RESHOOT;  // certified root not reached: re-shoot
+        if (it.kind != 1) fl |= FLAG_RESHOOT;  // certified root not reached: re-shoot
       } else {
         // half-open ownership box (domain edges own the tolerance band)
         const double lo_u = u0 == 0.0 ? -tol : u0, hi_u = u1 == 1.0 ? 1.0 + tol : u1;
@@ -281,10 +324,12 @@ __global__ void __launch_bounds__(128) k3_newton(WaveArgs w) {
             if (r.tang || r.graze) fl |= FLAG_RESHOOT;
             if (r.onsurf) fl |= FLAG_ONSURF;
           }
-        } else if (it.kind == 0) {
-          // certified: the unique root lies in the 1e-7-expanded box; farther
-          // away means Newton left the certified basin
-          const double mu = 2e-7 * wu, mv = 2e-7 * wv;
+        } else if (it.kind != 1) {
+          // certified: the unique root lies in the certification box (node
+          // +1e-7, or the kLeafM-expanded leaf box); farther away means Newton
+          // left the certified basin
+          const double ex = it.kind == 2 ? kLeafM + 1e-6 : 2e-7;
+          const double mu = ex * wu, mv = ex * wv;
           if (r.u < u0 - mu || r.u > u1 + mu || r.v < v0 - mv || r.v > v1 + mv)
             fl |= FLAG_RESHOOT;
         } else {
@@ -318,26 +363,27 @@ static int grid_for(const void* fn, int sm_count) {
 // size; queue overflow (never seen in practice) clears the accumulators of
 // the m active queries and retries with doubled capacity.
 cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, int64_t npairs,
-                             const int32_t* pair_slot, const int32_t* pair_patch,
+                             const int32_t* pair_slot, const int32_t* pair_leaf,
                              const double* qproj, int32_t* chi, int32_t* flags, int32_t m,
                              unsigned long long* counters, cudaStream_t st) {
   if (npairs <= 0) return cudaSuccess;
-  static thread_local int g_level = 0, g_newton = 0, g_dev = -1;
+  static thread_local int g_cand = 0, g_level = 0, g_newton = 0, g_dev = -1;
   static thread_local unsigned long long* h = nullptr;
   if (g_dev != sc->device) {
+    g_cand = grid_for((const void*)k3_candidates, sc->sm_count);
     g_level = grid_for((const void*)k3_level, sc->sm_count);
     g_newton = grid_for((const void*)k3_newton, sc->sm_count);
     g_dev = sc->device;
   }
   cudaError_t e = cudaSuccess;
   if (!h && (e = cudaMallocHost(&h, sizeof(unsigned long long) * 4)) != cudaSuccess) return e;
-  unsigned long long cap = (unsigned long long)(npairs * 2 + 4096);
-  unsigned long long ncap = (unsigned long long)(npairs * 2 + 4096);
+  unsigned long long cap = (unsigned long long)(npairs + 4096);
+  unsigned long long ncap = (unsigned long long)(npairs + 4096);
   for (int attempt = 0; attempt < 8; ++attempt) {
     NodeItem *qa = nullptr, *qb = nullptr;
     NewtonItem* nq = nullptr;
-    unsigned long long* cnt = nullptr;  // [0],[1] level queues, [2] newton, [3] overflow
-    int32_t* pn = nullptr;
+    unsigned long long* cnt = nullptr;  // [0],[1] node queues, [2] newton, [3] overflow
+    int32_t *pn = nullptr, *pp = nullptr;
     bool overflow = false;
 #define WC(x)                       \
   do {                              \
@@ -349,25 +395,30 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, int64_t npair
     WC(cudaMallocAsync(&nq, sizeof(NewtonItem) * ncap, st));
     WC(cudaMallocAsync(&cnt, sizeof(unsigned long long) * 4, st));
     WC(cudaMallocAsync(&pn, sizeof(int32_t) * npairs, st));
+    WC(cudaMallocAsync(&pp, sizeof(int32_t) * npairs, st));
     WC(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 4, st));
     WC(cudaMemsetAsync(pn, 0, sizeof(int32_t) * npairs, st));
     {
-      WaveArgs w{pair_slot, pair_patch, qproj, rd.proj, sc->dprm, chi, flags, pn,
+      WaveArgs w{pair_slot, pp, qproj, rd.proj, sc->dprm, chi, flags, pn,
                  counters, (int*)(cnt + 3), nq, cnt + 2, ncap};
       NodeItem* bufs[2] = {qa, qb};
-      int level = 0;
-      bool more = true;
-      while (more && level <= kMaxLevel) {
-        for (int k = 0; k < 4 && level <= kMaxLevel; ++k, ++level) {
-          unsigned long long* out_c = cnt + ((level + 1) & 1);
+      k3_candidates<<<g_cand, 128, 0, st>>>(npairs, pair_leaf, rd.leaves, qa, cnt, cap, w);
+      WC(cudaGetLastError());
+      WC(cudaMemcpyAsync(h, cnt, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
+      WC(cudaStreamSynchronize(st));
+      bool more = h[0] > 0 && !h[3];
+      int pass = 0;
+      while (more && pass <= kMaxLevel) {
+        for (int k = 0; k < 4 && pass <= kMaxLevel; ++k, ++pass) {
+          unsigned long long* out_c = cnt + ((pass + 1) & 1);
           WC(cudaMemsetAsync(out_c, 0, sizeof(unsigned long long), st));
-          k3_level<<<g_level, 128, 0, st>>>(level, npairs, bufs[level & 1], cnt + (level & 1),
-                                            bufs[(level + 1) & 1], out_c, cap, w);
+          k3_level<<<g_level, 128, 0, st>>>(bufs[pass & 1], cnt + (pass & 1),
+                                            bufs[(pass + 1) & 1], out_c, cap, w);
           WC(cudaGetLastError());
         }
         WC(cudaMemcpyAsync(h, cnt, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, st));
         WC(cudaStreamSynchronize(st));
-        more = h[level & 1] > 0 && !h[3];
+        more = h[pass & 1] > 0 && !h[3];
       }
       overflow = h[3] != 0;
       if (!overflow) {
@@ -381,6 +432,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, int64_t npair
     if (nq) cudaFreeAsync(nq, st);
     if (cnt) cudaFreeAsync(cnt, st);
     if (pn) cudaFreeAsync(pn, st);
+    if (pp) cudaFreeAsync(pp, st);
 #undef WC
     if (e != cudaSuccess) return e;
     if (!overflow) return cudaSuccess;
