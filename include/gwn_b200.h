@@ -95,6 +95,9 @@ typedef struct gwn_stats {
   int64_t boundary_segments;/* (query, net segment) pairs evaluated        */
   int64_t kernel_launches;
   double ms_cull, ms_intersect, ms_boundary, ms_other;  /* event timings, 0 if not timed */
+  double ms_k3_candidates, ms_k3_fallback, ms_k3_newton;  /* split of ms_intersect */
+  int64_t k3_fallback_items;  /* undecided leaf candidates solved by the DFS fallback */
+  int64_t k3_newton_items;    /* certified leaf candidates (Newton solves)          */
 } gwn_stats;
 
 int gwn_abi_version(void);

@@ -57,7 +57,9 @@ class Stats(C.Structure):
         ("candidates", C.c_int64), ("nodes", C.c_int64), ("newton_iters", C.c_int64),
         ("roots", C.c_int64), ("boundary_segments", C.c_int64), ("kernel_launches", C.c_int64),
         ("ms_cull", C.c_double), ("ms_intersect", C.c_double), ("ms_boundary", C.c_double),
-        ("ms_other", C.c_double),
+        ("ms_other", C.c_double), ("ms_k3_candidates", C.c_double),
+        ("ms_k3_fallback", C.c_double), ("ms_k3_newton", C.c_double),
+        ("k3_fallback_items", C.c_int64), ("k3_newton_items", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

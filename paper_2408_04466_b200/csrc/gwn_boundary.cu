@@ -20,6 +20,8 @@
 // Per vertex: 3 DADD, |r|^2, rsqrt, 3 DFMA for u, d x u; per segment: 2 dot
 // products + 4 for the complex product.  Boundary vertices (x,y,z) are
 // staged in shared-memory tiles and read as warp-wide broadcasts.
+#include <algorithm>
+
 #include "gwn_internal.h"
 
 namespace gwn {
@@ -111,10 +113,14 @@ __device__ __forceinline__ void fan_segment(SegState& st, const Vtx& a, const Vt
 template <int QPT>
 __global__ void __launch_bounds__(kBlockQ)
 k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
-           const double* __restrict__ verts, int64_t V, int S,
+           const double* __restrict__ verts, int64_t V, int S, int64_t n_edges,
            const double* __restrict__ band_h, Frame f, DevParams prm,
-           double* __restrict__ bterm, int32_t* __restrict__ flag_acc,
+           double* __restrict__ bpart, int32_t* __restrict__ flag_acc,
            unsigned long long* __restrict__ counters) {
+  // blockIdx.y: chunk of whole edges [e0, e1) -> vertex range [v0, v1)
+  const int nchunk = gridDim.y;
+  const int64_t e0 = n_edges * blockIdx.y / nchunk, e1 = n_edges * (blockIdx.y + 1) / nchunk;
+  const int64_t vbeg = e0 * S, vend = e1 * S;
   __shared__ double sx[kTileV], sy[kTileV], sz[kTileV];
   const double dx = f.d[0], dy = f.d[1], dz = f.d[2];
   const double deg = prm.degenerate;
@@ -136,8 +142,8 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
     va[j].ok = false;
   }
   int nseg = 0;
-  for (int64_t t0 = 0; t0 < V; t0 += kTileV) {
-    const int nt = (int)min((int64_t)kTileV, V - t0);
+  for (int64_t t0 = vbeg; t0 < vend; t0 += kTileV) {
+    const int nt = (int)min((int64_t)kTileV, vend - t0);
     __syncthreads();
     for (int k = threadIdx.x; k < nt; k += blockDim.x) {
       const int64_t g = t0 + k;
@@ -170,27 +176,40 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
 #pragma unroll
   for (int j = 0; j < QPT; ++j) {
     if (slot[j] < m) {
-      const double ang = atan2(st[j].Zi, st[j].Zr) + 6.283185307179586476925 * (double)st[j].wraps;
-      bterm[slot[j]] = ang * 0.15915494309189533576888;  // (2 ang) / (4 pi)
+      // partial angle sum of this edge chunk; K5 adds the chunks in order
+      bpart[(int64_t)blockIdx.y * m + slot[j]] =
+          atan2(st[j].Zi, st[j].Zr) + 6.283185307179586476925 * (double)st[j].wraps;
       if (flags[j]) atomicOr(&flag_acc[slot[j]], flags[j]);
     }
   }
   if (threadIdx.x == 0) {
     int32_t nq = min((int32_t)(blockDim.x * QPT), m - (int32_t)(blockIdx.x * blockDim.x * QPT));
-    int64_t segs = V - V / S;
+    int64_t segs = (vend - vbeg) - (e1 - e0);
     atomicAdd(&counters[CNT_SEGMENTS], (unsigned long long)(segs * nq));
   }
 }
 
+constexpr int kQPT = 2;
+
+// Edge chunks of the boundary sum.  Fixed per scene (not per batch) so the
+// chunk partials -- added in chunk order by K5 -- make w bit-identical for any
+// batching, chunking or sharding of the queries; enough chunks that small
+// batches still fill the GPU.
+int boundary_chunks(const gwn_scene* sc, int32_t m) {
+  (void)m;
+  if (sc->n_edges <= 0) return 1;
+  return (int)std::min<int64_t>(sc->n_edges, 64);
+}
+
 cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
-                            const int32_t* active, const double* pos, double* bterm,
+                            const int32_t* active, const double* pos, double* bpart, int nchunk,
                             int32_t* flags, unsigned long long* counters, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
   int64_t V = sc->n_edges * sc->S;
-  if (V == 0) return cudaMemsetAsync(bterm, 0, sizeof(double) * m, st);
-  constexpr int QPT = 2;
-  k_boundary<QPT><<<(m + kBlockQ * QPT - 1) / (kBlockQ * QPT), kBlockQ, 0, st>>>(
-      m, active, pos, sc->verts, V, sc->S, sc->band_h, rd.f, sc->dprm, bterm, flags, counters);
+  if (V == 0) return cudaMemsetAsync(bpart, 0, sizeof(double) * m, st);
+  dim3 grid((m + kBlockQ * kQPT - 1) / (kBlockQ * kQPT), nchunk);
+  k_boundary<kQPT><<<grid, kBlockQ, 0, st>>>(m, active, pos, sc->verts, V, sc->S, sc->n_edges,
+                                             sc->band_h, rd.f, sc->dprm, bpart, flags, counters);
   return cudaGetLastError();
 }
 

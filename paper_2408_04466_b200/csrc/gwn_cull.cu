@@ -1,68 +1,23 @@
-// gwn_cull.cu -- K2: query x patch cull by 2-D LBVH traversal in the ray
-// frame of the round.
+// gwn_cull.cu -- K2: query x leaf cull by 2-D LBVH traversal in the ray frame
+// of the round.
 //
 // Replaces the reference's per-(ray, patch) `patch.aabb()` + ray_aabb_clip
 // (surfaces.py:636-639, geometry.py:198-219): with every ray of the round
 // parallel to d, a leaf sub-patch can be hit only if the query's projection
 // (p.e1, p.e2) lies in the leaf's projected control box and the leaf reaches
-// past p along d (cmax >= p.d).  Two passes with the same deterministic
-// traversal: count, (scan), fill -> (query slot, leaf) candidates grouped by
-// query slot.
+// past p along d (cmax >= p.d).  One pass: each thread collects its leaves in
+// a small register buffer, then the warp reserves space for all lanes with a
+// single atomic (warp prefix sum), so the (slot, leaf) candidates of a query
+// are contiguous.  Queries with more than kLBuf candidates append the rest
+// one by one (the segmented reduction downstream does not need sorted keys).
+// The kernel always counts every candidate; if the buffer capacity was too
+// small the engine re-runs the round with the exact size.
 #include "gwn_internal.h"
 
 namespace gwn {
 
 constexpr int kStack = 64;  // >= LBVH depth bound (30-bit Morton + 32-bit index tie-break)
-
-template <bool kFill>
-__device__ __forceinline__ int traverse(const Node* __restrict__ nodes,
-                                        const double* __restrict__ leafbox, int64_t P,
-                                        double qa, double qb, double qc, int32_t slot,
-                                        int32_t* __restrict__ out_slot,
-                                        int32_t* __restrict__ out_patch) {
-  int count = 0;
-  if (P == 1) {
-    const double* b = leafbox;
-    if (qa >= b[0] && qa <= b[1] && qb >= b[2] && qb <= b[3] && b[4] >= qc) {
-      if (kFill) { out_slot[0] = slot; out_patch[0] = 0; }
-      count = 1;
-    }
-    return count;
-  }
-  int stack[kStack];
-  int top = 0;
-  int node = 0;
-  for (;;) {
-    const Node& n = nodes[node];
-    int next = -1;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      bool hit = qa >= n.alo[c] && qa <= n.ahi[c] && qb >= n.blo[c] && qb <= n.bhi[c] &&
-                 n.cmax[c] >= qc;
-      if (!hit) continue;
-      int ch = n.child[c];
-      if (ch < 0) {
-        if (kFill) {
-          out_slot[count] = slot;
-          out_patch[count] = ~ch;
-        }
-        ++count;
-      } else if (next < 0) {
-        next = ch;
-      } else if (top < kStack) {
-        stack[top++] = ch;
-      }
-    }
-    if (next >= 0) {
-      node = next;
-    } else if (top > 0) {
-      node = stack[--top];
-    } else {
-      break;
-    }
-  }
-  return count;
-}
+constexpr int kLBuf = 12;
 
 __device__ __forceinline__ void query_proj(const Frame& f, const double* __restrict__ pos,
                                            int32_t q, double& qa, double& qb, double& qc) {
@@ -72,49 +27,89 @@ __device__ __forceinline__ void query_proj(const Frame& f, const double* __restr
   qc = x * f.d[0] + y * f.d[1] + z * f.d[2];
 }
 
-__global__ void k_cull_count(const Node* __restrict__ nodes, const double* __restrict__ leafbox,
-                             int64_t P, Frame f, int32_t m, const int32_t* __restrict__ active,
-                             const double* __restrict__ pos, int64_t* __restrict__ counts,
-                             double* __restrict__ qproj) {
-  int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= m) return;
-  int32_t q = active ? active[s] : s;
-  double qa, qb, qc;
-  query_proj(f, pos, q, qa, qb, qc);
-  qproj[3 * (int64_t)s] = qa;
-  qproj[3 * (int64_t)s + 1] = qb;
-  qproj[3 * (int64_t)s + 2] = qc;
-  counts[s] = traverse<false>(nodes, leafbox, P, qa, qb, qc, s, nullptr, nullptr);
+__global__ void __launch_bounds__(128)
+k_cull(const Node* __restrict__ nodes, const double* __restrict__ leafbox, int64_t n_leaves,
+       Frame f, int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
+       double* __restrict__ qproj, int32_t* __restrict__ pair_slot,
+       int32_t* __restrict__ pair_leaf, unsigned long long* __restrict__ pair_count,
+       unsigned long long cap) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = s < m;
+  int buf[kLBuf];
+  int n = 0;
+  if (live) {
+    const int32_t q = active ? active[s] : s;
+    double qa, qb, qc;
+    query_proj(f, pos, q, qa, qb, qc);
+    qproj[3 * (int64_t)s] = qa;
+    qproj[3 * (int64_t)s + 1] = qb;
+    qproj[3 * (int64_t)s + 2] = qc;
+    auto emit = [&](int leaf) {
+      if (n < kLBuf) {
+        buf[n++] = leaf;
+      } else {  // spill: rare, append individually
+        unsigned long long k = atomicAdd(pair_count, 1ull);
+        if (k < cap) {
+          pair_slot[k] = s;
+          pair_leaf[k] = leaf;
+        }
+      }
+    };
+    if (n_leaves == 1) {
+      const double* b = leafbox;
+      if (qa >= b[0] && qa <= b[1] && qb >= b[2] && qb <= b[3] && b[4] >= qc) emit(0);
+    } else {
+      int stack[kStack];
+      int top = 0;
+      int node = 0;
+      for (;;) {
+        const Node& nd = nodes[node];
+        int next = -1;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const bool hit = qa >= nd.alo[c] && qa <= nd.ahi[c] && qb >= nd.blo[c] &&
+                           qb <= nd.bhi[c] && nd.cmax[c] >= qc;
+          if (!hit) continue;
+          const int ch = nd.child[c];
+          if (ch < 0) emit(~ch);
+          else if (next < 0) next = ch;
+          else if (top < kStack) stack[top++] = ch;
+        }
+        if (next >= 0) node = next;
+        else if (top > 0) node = stack[--top];
+        else break;
+      }
+    }
+  }
+  // warp-aggregated reservation of the buffered candidates
+  const int lane = threadIdx.x & 31;
+  int incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long base = 0;
+  if (lane == 31 && total) base = atomicAdd(pair_count, (unsigned long long)total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  const unsigned long long o0 = base + (unsigned long long)(incl - n);
+  for (int k = 0; k < n; ++k) {
+    if (o0 + k < cap) {
+      pair_slot[o0 + k] = s;
+      pair_leaf[o0 + k] = buf[k];
+    }
+  }
 }
 
-__global__ void k_cull_fill(const Node* __restrict__ nodes, const double* __restrict__ leafbox,
-                            int64_t P, Frame f, int32_t m, const int32_t* __restrict__ active,
-                            const double* __restrict__ pos, const int64_t* __restrict__ offs,
-                            int32_t* __restrict__ pair_slot, int32_t* __restrict__ pair_patch) {
-  int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= m) return;
-  int32_t q = active ? active[s] : s;
-  double qa, qb, qc;
-  query_proj(f, pos, q, qa, qb, qc);
-  int64_t o = offs[s];
-  traverse<true>(nodes, leafbox, P, qa, qb, qc, s, pair_slot + o, pair_patch + o);
-}
-
-cudaError_t launch_cull_count(const gwn_scene* sc, const Round& rd, int32_t m,
-                              const int32_t* active, const double* pos, int64_t* counts,
-                              double* qproj, cudaStream_t st) {
+cudaError_t launch_cull(const gwn_scene* sc, const Round& rd, int32_t m, const int32_t* active,
+                        const double* pos, double* qproj, int32_t* pair_slot, int32_t* pair_leaf,
+                        unsigned long long* pair_count, int64_t cap, cudaStream_t st) {
+  (void)sc;
   if (m <= 0) return cudaSuccess;
-  k_cull_count<<<(m + 127) / 128, 128, 0, st>>>(rd.nodes, rd.leafbox, rd.n_leaves, rd.f, m, active,
-                                                pos, counts, qproj);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_cull_fill(const gwn_scene* sc, const Round& rd, int32_t m,
-                             const int32_t* active, const double* pos, const int64_t* offs,
-                             int32_t* pair_slot, int32_t* pair_patch, cudaStream_t st) {
-  if (m <= 0) return cudaSuccess;
-  k_cull_fill<<<(m + 127) / 128, 128, 0, st>>>(rd.nodes, rd.leafbox, rd.n_leaves, rd.f, m, active, pos,
-                                               offs, pair_slot, pair_patch);
+  k_cull<<<(m + 127) / 128, 128, 0, st>>>(rd.nodes, rd.leafbox, rd.n_leaves, rd.f, m, active,
+                                          pos, qproj, pair_slot, pair_leaf, pair_count,
+                                          (unsigned long long)cap);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,11 @@
 #include <cub/cub.cuh>
 
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
+
+#include <chrono>
 
 #include "gwn_internal.h"
 
@@ -20,19 +24,26 @@ namespace gwn {
 // K5: per active query decide done / jitter / re-shoot.
 __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
                            const int32_t* __restrict__ chi, const int32_t* __restrict__ flags,
-                           const double* __restrict__ bterm, int round, int max_rounds,
+                           const double* __restrict__ bpart, int nchunk, int round, int max_rounds,
                            int max_jitters, uint64_t seed, int64_t index_base, double jscale,
                            const double* __restrict__ q0, double* __restrict__ pos,
                            int8_t* __restrict__ jit, int8_t* __restrict__ jreason,
                            double* __restrict__ w_out, int8_t* __restrict__ st_out,
-                           int32_t* __restrict__ next, int32_t* __restrict__ next_n) {
+                           int32_t* __restrict__ next, int32_t* __restrict__ next_n,
+                           const unsigned long long* __restrict__ pair_count,
+                           unsigned long long pair_cap) {
+  if (*pair_count > pair_cap) return;  // candidate buffer overflowed: round is re-run
   int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   bool push = false;
   int32_t q = 0;
   if (s < m) {
     q = active ? active[s] : s;
     int32_t f = flags[s];
-    double w = (double)chi[s] + bterm[s];
+    // boundary term: per-chunk partial angles summed in chunk order
+    // (deterministic), (2 * angle) / (4 pi)
+    double ang = 0.0;
+    for (int c = 0; c < nchunk; ++c) ang += bpart[(int64_t)c * m + s];
+    double w = (double)chi[s] + ang * 0.15915494309189533576888;
     if (f & (FLAG_ONSURF | FLAG_DEGEN)) {
       int reason = (f & FLAG_ONSURF) ? GWN_STATUS_ON_SURFACE : GWN_STATUS_DEGENERATE;
       int j = jit[q];
@@ -94,6 +105,21 @@ __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
   }
 }
 
+// GWN_TRACE=1: host wall-clock trace of the eval phases (development aid)
+struct Trace {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  Trace() : on(getenv("GWN_TRACE") != nullptr) { t0 = last = std::chrono::steady_clock::now(); }
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[gwn] %-28s +%8.1f us  (%8.1f)\n", what,
+            std::chrono::duration<double, std::micro>(now - last).count(),
+            std::chrono::duration<double, std::micro>(now - t0).count());
+    last = now;
+  }
+};
+
 struct Workspace {
   cudaStream_t st;
   std::vector<void*> ptrs;
@@ -141,23 +167,33 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
   }
   if (n == 0) return GWN_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  Trace tr;
   Workspace ws;
   ws.st = st;
   const bool host = (flags & GWN_HOST_BUFFERS) != 0;
-  const int64_t chunk_max = sc->prm.chunk_queries > 0 ? sc->prm.chunk_queries : (1ll << 22);
-  int64_t* h_scalar = nullptr;  // pinned: [0] pair total, [1] next count
+  // auto chunk: 4M queries (2M when the boundary partials are wide)
+  const int64_t chunk_max = sc->prm.chunk_queries > 0 ? sc->prm.chunk_queries
+                            : boundary_chunks(sc, 0) > 16 ? (1ll << 21) : (1ll << 22);
+  int64_t* h_scalar = nullptr;  // pinned: [0] candidate count, [1] next active count
   const double* d_q = queries;
   double* d_w = w_out;
   int8_t* d_st = status_out;
   gwn_stats stats;
   memset(&stats, 0, sizeof stats);
   stats.queries = n;
-  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev[8] = {}, ev4[4] = {};
   int64_t launches = 0;
   unsigned long long* d_cnt = nullptr;
   unsigned long long h_cnt[CNT_N];
   CKE(cudaSetDevice(sc->device));
-  CKE(cudaMallocHost(&h_scalar, 2 * sizeof(int64_t)));
+  {
+    // pinned round scalars: one small buffer per host thread (gwn_eval
+    // synchronises its stream before returning, so reuse is safe)
+    static thread_local int64_t* t_pinned = nullptr;
+    if (!t_pinned) CKE(cudaMallocHost(&t_pinned, 4 * sizeof(int64_t)));
+    h_scalar = t_pinned;
+  }
+  tr.mark("setup");
   d_cnt = ws.get<unsigned long long>(CNT_N);
   CKE(ws.err);
   CKE(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * CNT_N, st));
@@ -169,29 +205,29 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
     CKE(cudaMemcpyAsync(dq, queries, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
     d_q = dq;
   }
-  if (sc->timed)
+  if (sc->timed) {
     for (auto& e : ev) CKE(cudaEventCreate(&e));
+    for (auto& e : ev4) CKE(cudaEventCreate(&e));
+  }
   {
     const int64_t cm = n < chunk_max ? n : chunk_max;
-    // per-chunk workspace (reused across chunks)
+    // per-chunk workspace (reused across chunks and rounds)
     double* pos = ws.get<double>((size_t)(3 * cm));
     int8_t* jit = ws.get<int8_t>((size_t)cm);
     int8_t* jreason = ws.get<int8_t>((size_t)cm);
     int32_t* act[2] = {ws.get<int32_t>((size_t)cm), ws.get<int32_t>((size_t)cm)};
-    int64_t* counts = ws.get<int64_t>((size_t)cm + 1);
-    int64_t* offs = ws.get<int64_t>((size_t)cm + 1);
     double* qproj = ws.get<double>((size_t)(3 * cm));
     int32_t* chi = ws.get<int32_t>((size_t)cm);
     int32_t* fl = ws.get<int32_t>((size_t)cm);
-    double* bterm = ws.get<double>((size_t)cm);
-    int32_t* next_n = ws.get<int32_t>(1);
-    size_t scan_bytes = 0;
-    CKE(ws.err);
-    CKE(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, counts, offs, (int)cm + 1, st));
-    void* scan_tmp = ws.get<char>(scan_bytes);
+    const int nchunk_max = boundary_chunks(sc, (int32_t)cm);
+    double* bterm = ws.get<double>((size_t)cm * nchunk_max);
+    // round scalars: [0] candidate count, [1] next active count,
+    // [2] fallback items, [3] newton items
+    unsigned long long* rsc = ws.get<unsigned long long>(4);
     int64_t pair_cap = 0;
     int32_t* pair_slot = nullptr;
-    int32_t* pair_patch = nullptr;
+    int32_t* pair_leaf = nullptr;
+    void* k3_scratch = nullptr;
     CKE(ws.err);
     for (int64_t c0 = 0; c0 < n; c0 += cm) {
       const int32_t mc = (int32_t)((n - c0) < cm ? (n - c0) : cm);
@@ -201,57 +237,71 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
       int32_t m = mc;
       const int32_t* active = nullptr;
       int cur = 0;
-      for (int r = 0; r < sc->prm.max_rounds && m > 0; ++r) {
+      for (int r = 0; r < sc->prm.max_rounds && m > 0;) {
         CKE(ensure_round(sc, r, st));
         const Round& rd = sc->rounds[r];
-        stats.rounds++;
-        if (r > 0) stats.retried += m;
-        if (sc->timed) CKE(cudaEventRecord(ev[0], st));
-        // ---- K2: cull (count, scan, fill)
-        int64_t npairs = 0;
-        if (sc->P > 0) {
-          CKE(launch_cull_count(sc, rd, m, active, pos, counts, qproj, st));
-          CKE(cudaMemsetAsync(counts + m, 0, sizeof(int64_t), st));
-          CKE(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, counts, offs, m + 1, st));
-          CKE(cudaMemcpyAsync(h_scalar, offs + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-          CKE(cudaStreamSynchronize(st));
-          npairs = h_scalar[0];
-          if (npairs > pair_cap) {
-            if (pair_slot) cudaFreeAsync(pair_slot, st);
-            if (pair_patch) cudaFreeAsync(pair_patch, st);
-            pair_cap = npairs + npairs / 4 + 1024;
-            CKE(cudaMallocAsync(&pair_slot, sizeof(int32_t) * pair_cap, st));
-            CKE(cudaMallocAsync(&pair_patch, sizeof(int32_t) * pair_cap, st));
-          }
-          CKE(launch_cull_fill(sc, rd, m, active, pos, offs, pair_slot, pair_patch, st));
-          launches += 3;
+        // candidate capacity from the scene's running estimate
+        int64_t want = (int64_t)(sc->pairs_per_query * 1.25 * m) + 4096;
+        if (want > pair_cap) {
+          if (pair_slot) CKE(cudaFreeAsync(pair_slot, st));
+          if (pair_leaf) CKE(cudaFreeAsync(pair_leaf, st));
+          if (k3_scratch) CKE(cudaFreeAsync(k3_scratch, st));
+          pair_slot = pair_leaf = nullptr;
+          k3_scratch = nullptr;
+          pair_cap = want;
+          CKE(cudaMallocAsync(&pair_slot, sizeof(int32_t) * pair_cap, st));
+          CKE(cudaMallocAsync(&pair_leaf, sizeof(int32_t) * pair_cap, st));
+          CKE(cudaMallocAsync(&k3_scratch, intersect_scratch_bytes(pair_cap), st));
         }
-        stats.candidates += npairs;
-        if (sc->timed) CKE(cudaEventRecord(ev[1], st));
-        // ---- K3: intersect + segmented reduction
-        CKE(cudaMemsetAsync(chi, 0, sizeof(int32_t) * m, st));
-        CKE(cudaMemsetAsync(fl, 0, sizeof(int32_t) * m, st));
-        if (npairs > 0) {
-          CKE(launch_intersect(sc, rd, npairs, pair_slot, pair_patch, qproj, chi, fl, m, d_cnt, st));
+        tr.mark("round setup");
+        if (sc->timed) CKE(cudaEventRecord(ev[0], st));
+        CKE(cudaMemsetAsync(rsc, 0, sizeof(unsigned long long) * 4, st));
+        // ---- K2: cull (one pass, warp-aggregated appends)
+        if (sc->P > 0) {
+          CKE(launch_cull(sc, rd, m, active, pos, qproj, pair_slot, pair_leaf, rsc, pair_cap, st));
           ++launches;
         }
+        tr.mark("cull launched");
+        if (sc->timed) CKE(cudaEventRecord(ev[1], st));
+        // ---- K3: candidate test, DFS fallback, Newton + segmented reduction
+        CKE(cudaMemsetAsync(chi, 0, sizeof(int32_t) * m, st));
+        CKE(cudaMemsetAsync(fl, 0, sizeof(int32_t) * m, st));
+        if (sc->P > 0) {
+          CKE(launch_intersect(sc, rd, pair_slot, pair_leaf, rsc, pair_cap, qproj, chi, fl, d_cnt,
+                               k3_scratch, sc->timed ? ev4 : nullptr, rsc + 2, st));
+          launches += 3;
+        }
+        tr.mark("k3 launched");
         if (sc->timed) CKE(cudaEventRecord(ev[2], st));
         // ---- K4: boundary term
-        CKE(launch_boundary(sc, rd, m, active, pos, bterm, fl, d_cnt, st));
+        const int nchunk = boundary_chunks(sc, m);
+        CKE(launch_boundary(sc, rd, m, active, pos, bterm, nchunk, fl, d_cnt, st));
         if (sc->n_edges > 0) ++launches;
         if (sc->timed) CKE(cudaEventRecord(ev[3], st));
         // ---- K5: finalize / compact re-shoots
-        CKE(cudaMemsetAsync(next_n, 0, sizeof(int32_t), st));
         int32_t* nxt = act[cur];
         k_finalize<<<(m + 127) / 128, 128, 0, st>>>(
-            m, active, chi, fl, bterm, r, sc->prm.max_rounds, sc->prm.max_jitters,
+            m, active, chi, fl, bterm, nchunk, r, sc->prm.max_rounds, sc->prm.max_jitters,
             sc->prm.dir_seed, index_base + c0, sc->prm.jitter_scale * sc->diag, q0, pos, jit,
-            jreason, d_w + c0, d_st + c0, nxt, next_n);
+            jreason, d_w + c0, d_st + c0, nxt, (int32_t*)(rsc + 1), rsc,
+            (unsigned long long)pair_cap);
         CKE(cudaGetLastError());
         ++launches;
-        CKE(cudaMemcpyAsync(h_scalar + 1, next_n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CKE(cudaMemcpyAsync(h_scalar, rsc, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost,
+                            st));
         if (sc->timed) CKE(cudaEventRecord(ev[4], st));
+        tr.mark("round launched");
         CKE(cudaStreamSynchronize(st));
+        tr.mark("round synced");
+        const int64_t npairs = h_scalar[0];
+        if (npairs > pair_cap) {  // re-run the round with the exact capacity
+          std::lock_guard<std::mutex> lk(sc->mu);
+          sc->pairs_per_query = fmax(sc->pairs_per_query, (double)npairs / m);
+          continue;
+        }
+        stats.rounds++;
+        if (r > 0) stats.retried += m;
+        stats.candidates += npairs;
         if (sc->timed) {
           float a = 0, b = 0, c = 0, d = 0;
           cudaEventElapsedTime(&a, ev[0], ev[1]);
@@ -262,14 +312,26 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
           stats.ms_intersect += b;
           stats.ms_boundary += c;
           stats.ms_other += d;
+          if (sc->P > 0) {
+            cudaEventElapsedTime(&a, ev4[0], ev4[1]);
+            cudaEventElapsedTime(&b, ev4[1], ev4[2]);
+            cudaEventElapsedTime(&c, ev4[2], ev4[3]);
+            stats.ms_k3_candidates += a;
+            stats.ms_k3_fallback += b;
+            stats.ms_k3_newton += c;
+          }
         }
+        stats.k3_fallback_items += h_scalar[2];
+        stats.k3_newton_items += h_scalar[3];
         m = (int32_t)(*(int32_t*)(h_scalar + 1));
         active = nxt;
         cur ^= 1;
+        ++r;
       }
     }
     if (pair_slot) cudaFreeAsync(pair_slot, st);
-    if (pair_patch) cudaFreeAsync(pair_patch, st);
+    if (pair_leaf) cudaFreeAsync(pair_leaf, st);
+    if (k3_scratch) cudaFreeAsync(k3_scratch, st);
   }
   if (host) {
     CKE(cudaMemcpyAsync(w_out, d_w, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
@@ -283,13 +345,16 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
   stats.boundary_segments = (int64_t)h_cnt[CNT_SEGMENTS];
   stats.kernel_launches = launches;
   sc->stats = stats;
+  tr.mark("outputs copied");
 done:
   ws.release();
   if (st) cudaStreamSynchronize(st);
   else cudaDeviceSynchronize();
-  if (h_scalar) cudaFreeHost(h_scalar);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ev4)
+    if (e) cudaEventDestroy(e);
+  tr.mark("done");
   return rc;
 }
 

@@ -83,6 +83,8 @@ struct gwn_scene {
   // per-round caches
   std::mutex mu;
   std::vector<gwn::Round> rounds;
+  // candidate (query, leaf) pairs per query seen so far (buffer sizing)
+  double pairs_per_query = 4.0;
   // last-eval stats
   gwn_stats stats;
   int timed = 0;
@@ -93,20 +95,22 @@ namespace gwn {
 // launchers (stream-ordered); defined in the .cu files
 cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st);            // gwn_bvh.cu
 void free_round(Round& rd);
-cudaError_t launch_cull_count(const gwn_scene* sc, const Round& rd, int32_t m,
-                              const int32_t* active, const double* pos, int64_t* counts,
-                              double* qproj, cudaStream_t st);             // gwn_cull.cu
-cudaError_t launch_cull_fill(const gwn_scene* sc, const Round& rd, int32_t m,
-                             const int32_t* active, const double* pos, const int64_t* offs,
-                             int32_t* pair_slot, int32_t* pair_patch, cudaStream_t st);
-cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, int64_t npairs,
-                             const int32_t* pair_slot, const int32_t* pair_patch,
-                             const double* qproj, int32_t* chi, int32_t* flags, int32_t m,
-                             unsigned long long* counters, cudaStream_t st);  // gwn_wavefront.cu
+cudaError_t launch_cull(const gwn_scene* sc, const Round& rd, int32_t m, const int32_t* active,
+                        const double* pos, double* qproj, int32_t* pair_slot, int32_t* pair_leaf,
+                        unsigned long long* pair_count, int64_t cap,
+                        cudaStream_t st);                                     // gwn_cull.cu
+cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t* pair_slot,
+                             const int32_t* pair_leaf, const unsigned long long* npairs_dev,
+                             int64_t pair_cap, const double* qproj, int32_t* chi,
+                             int32_t* flags, unsigned long long* counters, void* scratch,
+                             cudaEvent_t* ev4, unsigned long long* items_out,
+                             cudaStream_t st);                                // gwn_wavefront.cu
+size_t intersect_scratch_bytes(int64_t pair_cap);
 cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
-                            const int32_t* active, const double* pos, double* bterm,
+                            const int32_t* active, const double* pos, double* bpart, int nchunk,
                             int32_t* flags, unsigned long long* counters,
                             cudaStream_t st);                                 // gwn_boundary.cu
+int boundary_chunks(const gwn_scene* sc, int32_t m);
 cudaError_t launch_all_hits(const gwn_scene* sc, const Round& rd, int64_t patch,
                             const double* o, double* out, int32_t* count, int32_t cap,
                             cudaStream_t st);

@@ -230,6 +230,56 @@ __device__ __forceinline__ uint64_t code_iv(uint64_t c) { return c & ((1ull << 2
 __device__ __forceinline__ double code_wu(int level) { return ldexp(1.0, -((level + 1) >> 1)); }
 __device__ __forceinline__ double code_wv(int level) { return ldexp(1.0, -(level >> 1)); }
 
+struct RootNet {
+  double a[16], b[16];
+  double eps_box;
+};
+
+__device__ __forceinline__ void load_root(const double* __restrict__ P48, double qa, double qb,
+                                          const DevParams& prm, RootNet& n) {
+  double amag = 0.0, alo = INFINITY, ahi = -INFINITY, blo = INFINITY, bhi = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    double A = __ldg(P48 + k), B = __ldg(P48 + 16 + k);
+    n.a[k] = A - qa;
+    n.b[k] = B - qb;
+    amag = fmax(amag, fmax(fabs(A), fabs(B)));
+    alo = fmin(alo, A); ahi = fmax(ahi, A); blo = fmin(blo, B); bhi = fmax(bhi, B);
+  }
+  n.eps_box = 1e-12 * (1.0 + amag) + 3.0 * prm.domain_tol * fmax(ahi - alo, bhi - blo);
+}
+
+// keep the left (right=false) or right half of a split along dir, in place
+__device__ __forceinline__ void halve_keep(double* a, double* b, int dir, bool right) {
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int i0 = dir == 0 ? l : 4 * l;
+    const int st = dir == 0 ? 4 : 1;
+    double q0, q1, q2, q3;
+    half4(a[i0], a[i0 + st], a[i0 + 2 * st], a[i0 + 3 * st], q0, q1, q2, q3);
+    if (right) { a[i0] = q0; a[i0 + st] = q1; a[i0 + 2 * st] = q2; a[i0 + 3 * st] = q3; }
+    half4(b[i0], b[i0 + st], b[i0 + 2 * st], b[i0 + 3 * st], q0, q1, q2, q3);
+    if (right) { b[i0] = q0; b[i0 + st] = q1; b[i0 + 2 * st] = q2; b[i0 + 3 * st] = q3; }
+  }
+}
+
+// Rebuild the node net: levels alternate u (even) / v (odd) splits; the
+// path bits are iu / iv read from the most significant end.
+__device__ __forceinline__ void rebuild(double* a, double* b, int level, uint64_t iu,
+                                        uint64_t iv) {
+  const int nu = (level + 1) >> 1, nv = level >> 1;
+  int ku = 0, kv = 0;
+  for (int l = 0; l < level; ++l) {
+    if ((l & 1) == 0) {
+      halve_keep(a, b, 0, (iu >> (nu - 1 - ku)) & 1);
+      ++ku;
+    } else {
+      halve_keep(a, b, 1, (iv >> (nv - 1 - kv)) & 1);
+      ++kv;
+    }
+  }
+}
+
 // Segmented warp-shuffle reduction keyed by `key` (K5): sums `v` and ORs `f`
 // over each maximal run of equal keys among adjacent lanes; returns true on the
 // lane that ends its run (that lane holds the run totals).  Works for any key
@@ -275,7 +325,8 @@ __device__ __forceinline__ RootResult newton_solve(const double* __restrict__ P4
   RootResult r;
   r.iters = 0;
   double bu[4], dbu[4], bv[4], dbv[4];
-  double A, Au, Av, B, Bu, Bv;
+  double A = 0, Au = 0, Av = 0, B = 0, Bu = 0, Bv = 0;
+  double du = 0.0, dv = 0.0;  // final (quadratically converged) step, applied below
   bool conv = false;
   for (int it = 0; it < kNewtonMax; ++it) {
     bern3(u, bu, dbu);
@@ -285,17 +336,24 @@ __device__ __forceinline__ RootResult newton_solve(const double* __restrict__ P4
     A -= qa;
     B -= qb;
     r.iters++;
-    double det = Au * Bv - Av * Bu;
+    const double det = Au * Bv - Av * Bu;
     if (!(fabs(det) > 0.0)) break;
-    double id = 1.0 / det;
-    double du = (Bv * A - Av * B) * id, dv = (Au * B - Bu * A) * id;
-    if (!isfinite(du) || !isfinite(dv)) break;
-    if (fabs(du) <= 2e-16 * fmax(1.0, fabs(u)) && fabs(dv) <= 2e-16 * fmax(1.0, fabs(v))) {
+    const double id = 1.0 / det;
+    const double su = (Bv * A - Av * B) * id, sv = (Au * B - Bu * A) * id;
+    if (!isfinite(su) || !isfinite(sv)) break;
+    // stop once the step is tiny: Newton's quadratic convergence makes the
+    // stepped point accurate to ~1e-22, so it is applied without another
+    // evaluation (t and the record use the current partials, t corrected to
+    // first order)
+    if (fabs(su) <= 1e-11 * fmax(1.0, fabs(u)) && fabs(sv) <= 1e-11 * fmax(1.0, fabs(v)) &&
+        sqrt(A * A + B * B) <= prm.residual) {
+      du = su;
+      dv = sv;
       conv = true;
       break;
     }
-    u -= du;
-    v -= dv;
+    u -= su;
+    v -= sv;
     if (fabs(u) > 8.0 || fabs(v) > 8.0) break;  // left the patch neighbourhood
   }
   if (!conv) {
@@ -306,34 +364,38 @@ __device__ __forceinline__ RootResult newton_solve(const double* __restrict__ P4
     A -= qa;
     B -= qb;
   }
-  r.u = u;
-  r.v = v;
   r.t = 0.0;
   r.sign = 0; r.tang = 0; r.graze = 0; r.onsurf = 0;
   if (!(sqrt(A * A + B * B) <= prm.residual)) {                        // surfaces.py:665
+    r.u = u;
+    r.v = v;
     r.status = ROOT_DIVERGED;
     return r;
   }
+  double C, Cu, Cv;
+  eval_coord(P48 + 32, bu, dbu, bv, dbv, C, Cu, Cv);
+  u -= du;
+  v -= dv;
+  r.u = u;
+  r.v = v;
   const double tol = prm.domain_tol;                                   // surfaces.py:668
   if (!(u >= -tol && u <= 1.0 + tol && v >= -tol && v <= 1.0 + tol)) {
     r.status = ROOT_REJECTED;
     return r;
   }
-  double C, Cu, Cv;
-  eval_coord(P48 + 32, bu, dbu, bv, dbv, C, Cu, Cv);
-  r.t = C - qc;
+  r.t = C - qc - (Cu * du + Cv * dv);
   if (r.t < -prm.t_tol) {                                              // surfaces.py:670
     r.status = ROOT_REJECTED;
     return r;
   }
-  double nx = Bu * Cv - Cu * Bv, ny = Cu * Av - Au * Cv, nz = Au * Bv - Bu * Av;
-  double nn = sqrt(nx * nx + ny * ny + nz * nz);
+  const double nx = Bu * Cv - Cu * Bv, ny = Cu * Av - Au * Cv, nz = Au * Bv - Bu * Av;
+  const double nn = sqrt(nx * nx + ny * ny + nz * nz);
   r.sign = 1; r.tang = 1; r.graze = 1;
   if (!(nn < prm.degenerate)) {                                        // surfaces.py:684-687
-    double dd = nz / nn;
+    const double dd = nz / nn;
     r.sign = dd > 0.0 ? 1 : -1;                                        // surfaces.py:695
     r.tang = fabs(dd) <= prm.tangent;                                  // :696 tangency
-    double bd = fmin(fmin(u, 1.0 - u), fmin(v, 1.0 - v));
+    const double bd = fmin(fmin(u, 1.0 - u), fmin(v, 1.0 - v));
     r.graze = bd < prm.edge_graze;                                     // :697 grazing
   }
   r.onsurf = fabs(r.t) <= prm.on_surface_t;
