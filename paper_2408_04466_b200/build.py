@@ -30,6 +30,7 @@ def needs_build() -> bool:
         return True
     t = os.path.getmtime(LIB)
     deps = sources() + glob.glob(os.path.join(HERE, "csrc", "*.h")) + \
+        glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + \
         [os.path.join(REPO, "include", "gwn_b200.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 

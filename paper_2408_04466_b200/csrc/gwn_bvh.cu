@@ -96,7 +96,6 @@ __global__ void k_leaves(int64_t P, const double* __restrict__ proj,
       r.code = code;
       r.patch = (int32_t)p;
       r.ok = kp.ok;
-      leaves[li] = r;
       // the leaf's own control box (convex hull of the piece over D)
       double c[16];
       for (int k = 0; k < 16; ++k) {
@@ -113,6 +112,8 @@ __global__ void k_leaves(int64_t P, const double* __restrict__ proj,
         lb = fmin(lb, b[k]); hb = fmax(hb, b[k]);
         hc = fmax(hc, c[k]);
       }
+      hull_axes(a, b, eps + 1e-15 * (fabs(la) + fabs(ha) + fabs(lb) + fabs(hb)), r);
+      leaves[li] = r;
       double* lbx = leafbox + 5 * li;
       lbx[0] = la - eps; lbx[1] = ha + eps; lbx[2] = lb - eps; lbx[3] = hb + eps; lbx[4] = hc + eps;
       const double ca = (0.5 * (la + ha) - amin) * ainv, cb = (0.5 * (lb + hb) - bmin) * binv;
@@ -204,6 +205,34 @@ __global__ void k_refit(int n, const int32_t* __restrict__ sorted_ids,
   }
 }
 
+// 30-bit Morton key of each query's projection (p.e1, p.e2): sorting the
+// round-0 queries by it makes warps traverse the LBVH and touch the leaf
+// records coherently.
+__global__ void k_query_keys(int32_t m, const double* __restrict__ pos, Frame f, double amin,
+                             double ainv, double bmin, double binv, uint32_t* __restrict__ keys,
+                             int32_t* __restrict__ ids) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  const double x = pos[3 * (int64_t)s], y = pos[3 * (int64_t)s + 1], z = pos[3 * (int64_t)s + 2];
+  const double a = x * f.e1[0] + y * f.e1[1] + z * f.e1[2];
+  const double b = x * f.e2[0] + y * f.e2[1] + z * f.e2[2];
+  const uint32_t ia = (uint32_t)fmin(fmax((a - amin) * ainv * 32767.0, 0.0), 32767.0);
+  const uint32_t ib = (uint32_t)fmin(fmax((b - bmin) * binv * 32767.0, 0.0), 32767.0);
+  uint32_t key = 0;
+  for (int bit = 0; bit < 15; ++bit)
+    key |= (((ia >> bit) & 1u) << (2 * bit)) | (((ib >> bit) & 1u) << (2 * bit + 1));
+  keys[s] = key;
+  ids[s] = s;
+}
+
+cudaError_t launch_query_keys(const Round& rd, int32_t m, const double* pos, uint32_t* keys,
+                              int32_t* ids, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  k_query_keys<<<(m + 255) / 256, 256, 0, st>>>(m, pos, rd.f, rd.amin, rd.ainv, rd.bmin, rd.binv,
+                                                keys, ids);
+  return cudaGetLastError();
+}
+
 void free_round(Round& rd) {
   if (rd.proj) cudaFree(rd.proj);
   if (rd.nodes) cudaFree(rd.nodes);
@@ -236,6 +265,10 @@ cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st) {
       }
       double ainv = amax > amin ? 1.0 / (amax - amin) : 0.0;
       double binv = bmax > bmin ? 1.0 / (bmax - bmin) : 0.0;
+      rd.amin = amin;
+      rd.ainv = ainv;
+      rd.bmin = bmin;
+      rd.binv = binv;
       uint32_t *keys = nullptr, *keys2 = nullptr;
       int32_t *ids = nullptr, *ids2 = nullptr, *tmp = nullptr;
       int64_t *lcount = nullptr, *loffs = nullptr;

@@ -224,6 +224,17 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
     // round scalars: [0] candidate count, [1] next active count,
     // [2] fallback items, [3] newton items
     unsigned long long* rsc = ws.get<unsigned long long>(4);
+    // round-0 spatial sort of the queries (Morton order in the ray frame)
+    const bool sort_q = sc->P > 0 && cm >= 65536;
+    uint32_t* qkeys = sort_q ? ws.get<uint32_t>((size_t)cm * 2) : nullptr;
+    int32_t* qids = sort_q ? ws.get<int32_t>((size_t)cm) : nullptr;
+    size_t sort_bytes = 0;
+    void* sort_tmp = nullptr;
+    if (sort_q) {
+      CKE(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, qkeys, qkeys + cm, qids, qids,
+                                          (int)cm, 0, 30, st));
+      sort_tmp = ws.get<char>(sort_bytes);
+    }
     int64_t pair_cap = 0;
     int32_t* pair_slot = nullptr;
     int32_t* pair_leaf = nullptr;
@@ -237,6 +248,15 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
       int32_t m = mc;
       const int32_t* active = nullptr;
       int cur = 0;
+      if (sort_q) {
+        CKE(ensure_round(sc, 0, st));
+        CKE(launch_query_keys(sc->rounds[0], mc, pos, qkeys, qids, st));
+        size_t sb = sort_bytes;
+        CKE(cub::DeviceRadixSort::SortPairs(sort_tmp, sb, qkeys, qkeys + cm, qids, act[1], mc, 0,
+                                            30, st));
+        active = act[1];  // round 0 writes its re-shoot list into act[0]
+        ++launches;
+      }
       for (int r = 0; r < sc->prm.max_rounds && m > 0;) {
         CKE(ensure_round(sc, r, st));
         const Round& rd = sc->rounds[r];
@@ -343,6 +363,9 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
   stats.newton_iters = (int64_t)h_cnt[CNT_NEWTON];
   stats.roots = (int64_t)h_cnt[CNT_ROOTS];
   stats.boundary_segments = (int64_t)h_cnt[CNT_SEGMENTS];
+  if (getenv("GWN_TRACE"))
+    fprintf(stderr, "[gwn] fallback: max nodes/item %llu, items > 16 nodes %llu\n",
+            h_cnt[CNT_MAXNODES], h_cnt[CNT_BIGITEMS]);
   stats.kernel_launches = launches;
   sc->stats = stats;
   tr.mark("outputs copied");

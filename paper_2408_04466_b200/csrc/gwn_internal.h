@@ -34,6 +34,8 @@ enum : int {
   CNT_NEWTON = 2,
   CNT_ROOTS = 3,
   CNT_SEGMENTS = 4,
+  CNT_MAXNODES = 5,  // max DFS nodes of one fallback item (diagnostic)
+  CNT_BIGITEMS = 6,  // fallback items with > 16 nodes (diagnostic)
   CNT_N = 8,
 };
 
@@ -63,6 +65,7 @@ struct Round {
   LeafRec* leaves = nullptr;   // (n_leaves) adaptive leaf sub-patches
   double* leafbox = nullptr;   // (n_leaves,5) cull boxes: a lo/hi, b lo/hi, c max
   Node* nodes = nullptr;       // (n_leaves-1) LBVH over the leaf boxes
+  double amin = 0, ainv = 0, bmin = 0, binv = 0;  // projected scene box (Morton keys)
 };
 
 }  // namespace gwn
@@ -106,6 +109,8 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
                              cudaEvent_t* ev4, unsigned long long* items_out,
                              cudaStream_t st);                                // gwn_wavefront.cu
 size_t intersect_scratch_bytes(int64_t pair_cap);
+cudaError_t launch_query_keys(const Round& rd, int32_t m, const double* pos, uint32_t* keys,
+                              int32_t* ids, cudaStream_t st);                 // gwn_bvh.cu
 cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             const int32_t* active, const double* pos, double* bpart, int nchunk,
                             int32_t* flags, unsigned long long* counters,

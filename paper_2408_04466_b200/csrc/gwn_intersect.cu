@@ -30,7 +30,7 @@ __global__ void k_all_hits(const double* __restrict__ P48, Frame f, double ox, d
   double qb = ox * f.e2[0] + oy * f.e2[1] + oz * f.e2[2];
   double qc = ox * f.d[0] + oy * f.d[1] + oz * f.d[2];
   RootAcc<true> acc;
-  solve_pair(P48, qa, qb, qc, prm, 0, acc);
+  solve_pair(P48, qa, qb, qc, prm, 0, kMaxLevel, acc);
   // insertion sort by t
   int idx[kMaxRoots];
   for (int k = 0; k < acc.n; ++k) idx[k] = k;

@@ -154,6 +154,46 @@ __device__ __forceinline__ KrawPre kraw_pre(const double* a, const double* b) {
   return k;
 }
 
+// Separating-axis test of the point q against the convex hull of a node net
+// along the normals of its two centre tangent directions (u and v partials,
+// difference form).  Returns false if q is provably outside the hull.
+__device__ __forceinline__ bool hull_sat(const double* a, const double* b, double qa, double qb,
+                                         double eps) {
+  const double w3[4] = {0.125, 0.375, 0.375, 0.125};
+  const double w2[3] = {0.25, 0.5, 0.25};
+  double ua = 0.0, ub = 0.0, va = 0.0, vb = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (i < 3) {
+        ua += w2[i] * w3[j] * (a[4 * (i + 1) + j] - a[4 * i + j]);
+        ub += w2[i] * w3[j] * (b[4 * (i + 1) + j] - b[4 * i + j]);
+      }
+      if (j < 3) {
+        va += w3[i] * w2[j] * (a[4 * i + j + 1] - a[4 * i + j]);
+        vb += w3[i] * w2[j] * (b[4 * i + j + 1] - b[4 * i + j]);
+      }
+    }
+#pragma unroll
+  for (int ax = 0; ax < 2; ++ax) {
+    double na = ax == 0 ? -ub : -vb, nb = ax == 0 ? ua : va;
+    const double nl = sqrt(na * na + nb * nb);
+    if (!(nl > 0.0)) continue;
+    na /= nl;
+    nb /= nl;
+    double lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const double s = na * (a[k] - qa) + nb * (b[k] - qb);
+      lo = fmin(lo, s);
+      hi = fmax(hi, s);
+    }
+    if (lo > 2.0 * eps || hi < -2.0 * eps) return false;
+  }
+  return true;
+}
+
 // Query part: g = G - q at the centre -> predicted root t* = 1/2 - Ys g and
 // K = t* +- R.  Returns 0 exclude (K misses the exclusion box [xlo, xhi]),
 // 1 unique root in the certification box [clo, chi], 2 undecided.
@@ -216,10 +256,56 @@ struct alignas(16) LeafRec {
   double Ga, Gb;
   double Y00, Y01, Y10, Y11;
   double R0, R1;
+  // two separating axes of the leaf's control hull (normals of its centre
+  // tangents) with the hull's extent along each: q outside -> no root
+  double n1a, n1b, lo1, hi1;
+  double n2a, n2b, lo2, hi2;
   uint64_t code;   // level:6 | iu:29 | iv:29 in the patch's subdivision tree
   int32_t patch;
   int32_t ok;
 };
+
+// Query-independent separating axes of a (raw) net: unit normals of the
+// centre u/v tangents and the net's extent along them (hull_sat below).
+__device__ __forceinline__ void hull_axes(const double* a, const double* b, double eps,
+                                          LeafRec& r) {
+  const double w3[4] = {0.125, 0.375, 0.375, 0.125};
+  const double w2[3] = {0.25, 0.5, 0.25};
+  double ua = 0.0, ub = 0.0, va = 0.0, vb = 0.0;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      if (i < 3) {
+        ua += w2[i] * w3[j] * (a[4 * (i + 1) + j] - a[4 * i + j]);
+        ub += w2[i] * w3[j] * (b[4 * (i + 1) + j] - b[4 * i + j]);
+      }
+      if (j < 3) {
+        va += w3[i] * w2[j] * (a[4 * i + j + 1] - a[4 * i + j]);
+        vb += w3[i] * w2[j] * (b[4 * i + j + 1] - b[4 * i + j]);
+      }
+    }
+  for (int ax = 0; ax < 2; ++ax) {
+    double na = ax == 0 ? -ub : -vb, nb = ax == 0 ? ua : va;
+    const double nl = sqrt(na * na + nb * nb);
+    double lo = -INFINITY, hi = INFINITY;
+    if (nl > 0.0) {
+      na /= nl;
+      nb /= nl;
+      lo = INFINITY;
+      hi = -INFINITY;
+      for (int k = 0; k < 16; ++k) {
+        const double s = na * a[k] + nb * b[k];
+        lo = fmin(lo, s);
+        hi = fmax(hi, s);
+      }
+      lo -= 2.0 * eps;
+      hi += 2.0 * eps;
+    } else {
+      na = nb = 0.0;
+    }
+    if (ax == 0) { r.n1a = na; r.n1b = nb; r.lo1 = lo; r.hi1 = hi; }
+    else { r.n2a = na; r.n2b = nb; r.lo2 = lo; r.hi2 = hi; }
+  }
+}
 
 __device__ __forceinline__ uint64_t make_code(int level, uint64_t iu, uint64_t iv) {
   return ((uint64_t)level << 58) | (iu << 29) | iv;

@@ -118,8 +118,12 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev,
       k.R0 = L.R0; k.R1 = L.R1;
       k.ok = L.ok != 0;
       double s0, s1;
-      const int kr = kraw_query(k, L.Ga - qa, L.Gb - qb, xlo_u, xhi_u, xlo_v, xhi_v, -1e-7,
-                                1.0 + 1e-7, s0, s1);
+      int kr = kraw_query(k, L.Ga - qa, L.Gb - qb, xlo_u, xhi_u, xlo_v, xhi_v, -1e-7,
+                          1.0 + 1e-7, s0, s1);
+      if (kr == 2) {  // separating axes of the leaf hull (rigorous exclusion)
+        const double p1 = L.n1a * qa + L.n1b * qb, p2 = L.n2a * qa + L.n2b * qb;
+        if (p1 < L.lo1 || p1 > L.hi1 || p2 < L.lo2 || p2 > L.hi2) kr = 0;
+      }
       if (kr == 1) {
         wantN = true;
         nu_ = u0 - kLeafM * wu + s0 * span * wu;
@@ -136,39 +140,100 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev,
   warp_sum_u64(&w.counters[CNT_NODES], tested);
 }
 
-// Undecided leaves (rare): per-thread depth-first Krawczyk subdivision below
-// the leaf, roots owned by the leaf box (gwn_dfs.cuh).
+// Undecided leaves (rare; rays near a silhouette fold of the projection):
+// one item per warp, breadth-first below the leaf; the lanes test the item's
+// frontier nodes in parallel (node_test, gwn_dfs.cuh), so the critical path
+// is depth x node latency rather than node count x node latency.  Roots
+// count only in the node that owns them; undecidable nodes kDfsDepth levels
+// below the leaf flag the query for a new direction.
+constexpr int kFrontier = 128;
+
 __global__ void __launch_bounds__(128)
 k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restrict__ in_count,
             WaveArgs w) {
+  __shared__ uint64_t fr[4][2][kFrontier];
   const int64_t n = (int64_t)*in_count;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  unsigned long long nodes = 0, iters = 0, roots = 0;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    int32_t slot = -1, chi = 0, fl = 0;
-    if (i < n) {
-      const NodeItem it = in[i];
-      slot = w.pair_slot[it.pair];
-      const double* P48 = w.proj + 48 * (int64_t)w.pair_patch[it.pair];
-      const double* q = w.qproj + 3 * (int64_t)slot;
-      RootAcc<false> acc;
-      const PairOut r = solve_pair(P48, q[0], q[1], q[2], w.prm, it.code, acc);
-      chi = r.chi;
-      fl = r.flags;
-      nodes += r.nodes;
-      iters += r.newton;
-      roots += r.roots;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long nodes = 0, iters = 0, roots = 0, maxn = 0;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    const NodeItem it = in[i];
+    const int32_t slot = w.pair_slot[it.pair];
+    const double* q = w.qproj + 3 * (int64_t)slot;
+    const NodeCtx ctx = node_ctx(w.proj + 48 * (int64_t)w.pair_patch[it.pair], q[0], q[1], q[2],
+                                 w.prm);
+    const int max_level = min(code_level(it.code) + kDfsDepth, kMaxLevel);
+    int cur = 0, ncur = 1, item_nodes = 0;
+    int32_t chi = 0, fl = 0;
+    if (lane == 0) fr[wib][0][0] = it.code;
+    __syncwarp();
+    while (ncur > 0) {
+      int nnext = 0;
+      for (int base = 0; base < ncur; base += 32) {
+        const int k = base + lane;
+        int o = NODE_EXCLUDED;
+        uint64_t code = 0;
+        if (k < ncur) {
+          code = fr[wib][cur][k];
+          RootResult r;
+          bool owned = false;
+          o = node_test(ctx, code, max_level, w.prm, r, owned);
+          if (o == NODE_AMBIGUOUS) {
+            fl |= FLAG_RESHOOT;
+          } else if (o == NODE_ROOT) {
+            iters += r.iters;
+            if (r.status == ROOT_ACCEPTED && owned) {
+              ++roots;
+              chi += r.sign;
+              if (r.tang || r.graze) fl |= FLAG_RESHOOT;
+              if (r.onsurf) fl |= FLAG_ONSURF;
+            }
+          }
+        }
+        // warp-aggregated append of the children of split nodes
+        const bool sp = o == NODE_SPLIT;
+        const unsigned mask = __ballot_sync(0xffffffffu, sp);
+        if (sp) {
+          const int pos = nnext + 2 * __popc(mask & ((1u << lane) - 1));
+          uint64_t c0, c1;
+          child_codes(code, c0, c1);
+          if (pos + 1 < kFrontier) {
+            fr[wib][cur ^ 1][pos] = c0;
+            fr[wib][cur ^ 1][pos + 1] = c1;
+          } else {
+            fl |= FLAG_RESHOOT;  // frontier overflow: give up on this direction
+          }
+        }
+        nnext = min(nnext + 2 * __popc(mask), kFrontier);
+        item_nodes += min(32, ncur - base);
+      }
+      __syncwarp();
+      cur ^= 1;
+      ncur = nnext;
+      if (item_nodes > kDfsBudget) {
+        fl |= FLAG_RESHOOT;
+        break;
+      }
     }
-    const bool tail = seg_reduce(slot, chi, fl);
-    if (slot >= 0 && tail) {
+    nodes += lane == 0 ? item_nodes : 0;
+    maxn = max(maxn, (unsigned long long)item_nodes);
+    // reduce the item's lanes (all lanes hold the same slot)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      chi += __shfl_down_sync(0xffffffffu, chi, off);
+      fl |= __shfl_down_sync(0xffffffffu, fl, off);
+    }
+    if (lane == 0) {
       if (chi) atomicAdd(&w.chi[slot], chi);
       if (fl) atomicOr(&w.flags[slot], fl);
     }
+    __syncwarp();
   }
   warp_sum_u64(&w.counters[CNT_NODES], nodes);
   warp_sum_u64(&w.counters[CNT_NEWTON], iters);
   warp_sum_u64(&w.counters[CNT_ROOTS], roots);
+  if (lane == 0 && maxn) atomicMax(&w.counters[CNT_MAXNODES], maxn);
 }
 
 // Newton pass over the certified / level-cap nodes + ownership + K5 part 1.
