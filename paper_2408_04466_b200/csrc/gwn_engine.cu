@@ -181,7 +181,7 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
   gwn_stats stats;
   memset(&stats, 0, sizeof stats);
   stats.queries = n;
-  cudaEvent_t ev[8] = {}, ev4[4] = {};
+  cudaEvent_t ev[8] = {}, ev4[5] = {};
   int64_t launches = 0;
   unsigned long long* d_cnt = nullptr;
   unsigned long long h_cnt[CNT_N];
@@ -232,7 +232,7 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
     void* sort_tmp = nullptr;
     if (sort_q) {
       CKE(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, qkeys, qkeys + cm, qids, qids,
-                                          (int)cm, 0, 30, st));
+                                          (int)cm, 14, 30, st));
       sort_tmp = ws.get<char>(sort_bytes);
     }
     int64_t pair_cap = 0;
@@ -252,7 +252,8 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
         CKE(ensure_round(sc, 0, st));
         CKE(launch_query_keys(sc->rounds[0], mc, pos, qkeys, qids, st));
         size_t sb = sort_bytes;
-        CKE(cub::DeviceRadixSort::SortPairs(sort_tmp, sb, qkeys, qkeys + cm, qids, act[1], mc, 0,
+        // top 16 Morton bits (256 x 256 cells): two radix passes
+        CKE(cub::DeviceRadixSort::SortPairs(sort_tmp, sb, qkeys, qkeys + cm, qids, act[1], mc, 14,
                                             30, st));
         active = act[1];  // round 0 writes its re-shoot list into act[0]
         ++launches;
@@ -286,9 +287,10 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
         // ---- K3: candidate test, DFS fallback, Newton + segmented reduction
         CKE(cudaMemsetAsync(chi, 0, sizeof(int32_t) * m, st));
         CKE(cudaMemsetAsync(fl, 0, sizeof(int32_t) * m, st));
+        cudaEvent_t join = nullptr;
         if (sc->P > 0) {
           CKE(launch_intersect(sc, rd, pair_slot, pair_leaf, rsc, pair_cap, qproj, chi, fl, d_cnt,
-                               k3_scratch, sc->timed ? ev4 : nullptr, rsc + 2, st));
+                               k3_scratch, sc->timed ? ev4 : nullptr, rsc + 2, &join, st));
           launches += 3;
         }
         tr.mark("k3 launched");
@@ -298,7 +300,8 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
         CKE(launch_boundary(sc, rd, m, active, pos, bterm, nchunk, fl, d_cnt, st));
         if (sc->n_edges > 0) ++launches;
         if (sc->timed) CKE(cudaEventRecord(ev[3], st));
-        // ---- K5: finalize / compact re-shoots
+        // ---- K5: finalize / compact re-shoots (after the K3 side stream)
+        if (join) CKE(cudaStreamWaitEvent(st, join, 0));
         int32_t* nxt = act[cur];
         k_finalize<<<(m + 127) / 128, 128, 0, st>>>(
             m, active, chi, fl, bterm, nchunk, r, sc->prm.max_rounds, sc->prm.max_jitters,
@@ -333,9 +336,9 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
           stats.ms_boundary += c;
           stats.ms_other += d;
           if (sc->P > 0) {
-            cudaEventElapsedTime(&a, ev4[0], ev4[1]);
+            cudaEventElapsedTime(&a, ev4[0], ev4[4]);
             cudaEventElapsedTime(&b, ev4[1], ev4[2]);
-            cudaEventElapsedTime(&c, ev4[2], ev4[3]);
+            cudaEventElapsedTime(&c, ev4[4], ev4[3]);
             stats.ms_k3_candidates += a;
             stats.ms_k3_fallback += b;
             stats.ms_k3_newton += c;

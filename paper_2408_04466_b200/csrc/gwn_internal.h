@@ -106,7 +106,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
                              const int32_t* pair_leaf, const unsigned long long* npairs_dev,
                              int64_t pair_cap, const double* qproj, int32_t* chi,
                              int32_t* flags, unsigned long long* counters, void* scratch,
-                             cudaEvent_t* ev4, unsigned long long* items_out,
+                             cudaEvent_t* ev4, unsigned long long* items_out, cudaEvent_t* join,
                              cudaStream_t st);                                // gwn_wavefront.cu
 size_t intersect_scratch_bytes(int64_t pair_cap);
 cudaError_t launch_query_keys(const Round& rd, int32_t m, const double* pos, uint32_t* keys,

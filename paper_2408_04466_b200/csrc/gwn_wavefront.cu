@@ -314,7 +314,8 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
                              const int32_t* pair_leaf, const unsigned long long* npairs_dev,
                              int64_t pair_cap, const double* qproj, int32_t* chi,
                              int32_t* flags, unsigned long long* counters, void* scratch,
-                             cudaEvent_t* ev4, unsigned long long* items_out, cudaStream_t st) {
+                             cudaEvent_t* ev4, unsigned long long* items_out, cudaEvent_t* join,
+                             cudaStream_t st) {
   static thread_local int g_cand = 0, g_fb = 0, g_newton = 0, g_dev = -1;
   if (g_dev != sc->device) {
     g_cand = grid_for((const void*)k3_candidates, sc->sm_count);
@@ -340,10 +341,25 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
   k3_candidates<<<g_cand, 128, 0, st>>>(npairs_dev, pair_leaf, rd.leaves, fq, cnt,
                                         (unsigned long long)pair_cap, w);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (ev4) cudaEventRecord(ev4[1], st);
-  k3_fallback<<<g_fb, 128, 0, st>>>(fq, cnt, w);
+  // The fallback (few, latency-bound items) runs on a side stream,
+  // concurrently with the Newton pass and K4; the engine joins it (`join`)
+  // before K5 reads the accumulators.
+  static thread_local cudaStream_t side = nullptr;
+  static thread_local cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  if (!side) {
+    if ((e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
+  if ((e = cudaEventRecord(fork_ev, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(side, fork_ev, 0)) != cudaSuccess) return e;
+  if (ev4) cudaEventRecord(ev4[1], side);
+  k3_fallback<<<g_fb, 128, 0, side>>>(fq, cnt, w);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (ev4) cudaEventRecord(ev4[2], st);
+  if (ev4) cudaEventRecord(ev4[2], side);
+  if ((e = cudaEventRecord(join_ev, side)) != cudaSuccess) return e;
+  *join = join_ev;
+  if (ev4) cudaEventRecord(ev4[4], st);
   k3_newton<<<g_newton, 128, 0, st>>>(w);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev4) cudaEventRecord(ev4[3], st);
