@@ -56,40 +56,52 @@ __device__ __forceinline__ void renorm(SegState& s) {
   s.Zi *= sc;
 }
 
-// Per-vertex quantities of the shifted fan formula.
-struct Vtx {
-  double ux, uy, uz;   // a^ - d
-  double gx, gy, gz;   // d x u
-  double l;            // |x - p|
-  bool ok;
+// Full-precision reciprocal square root: MUFU.RSQ64H seed + two Newton steps
+// (no special-value path; l2 > 0 is guaranteed unless the query sits on a
+// vertex, which the degenerate test flags anyway).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = x * y;
+  double e = fma(-h, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  h = x * y;
+  e = fma(-h, y, 1.0);
+  return fma(0.5 * y, e, y);
+}
+
+// Per-vertex quantities of the shifted fan formula in the round's ray frame
+// (e1, e2, d): d = (0,0,1), so u = r/|r| - d = (rx il, ry il, rz il - 1).
+struct VtxF {
+  double ux, uy, uz;   // a^ - d in frame coordinates
+  double il;           // 1 / |x - p|
 };
 
-__device__ __forceinline__ Vtx make_vtx(double x, double y, double z, double px, double py,
-                                        double pz, double dx, double dy, double dz, double deg) {
-  Vtx v;
-  const double rx = x - px, ry = y - py, rz = z - pz;
+__device__ __forceinline__ VtxF make_vtxf(double X, double Y, double Zc, double qa, double qb,
+                                          double qc, int& flags) {
+  VtxF v;
+  const double rx = X - qa, ry = Y - qb, rz = Zc - qc;
   const double l2 = rx * rx + ry * ry + rz * rz;
-  const double il = rsqrt(l2);
-  v.l = l2 * il;
-  v.ok = v.l >= deg;
-  v.ux = fma(rx, il, -dx);
-  v.uy = fma(ry, il, -dy);
-  v.uz = fma(rz, il, -dz);
-  v.gx = dy * v.uz - dz * v.uy;
-  v.gy = dz * v.ux - dx * v.uz;
-  v.gz = dx * v.uy - dy * v.ux;
+  // degenerate projection |x - p| < 1e-12 (_kernels.py:541-542), integer
+  // compare on the IEEE pattern of l2 (monotone for l2 >= 0): 1e-24 = deg^2
+  if (__double_as_longlong(l2) < 0x3AF357C299A88EA7LL) flags |= FLAG_DEGEN;
+  v.il = rsqrt_nr(l2);
+  v.ux = rx * v.il;
+  v.uy = ry * v.il;
+  v.uz = fma(rz, v.il, -1.0);
   return v;
 }
 
 // polyline/curve band test (rare path, den < 0): d within band_factor*h/dist
-// of the arc (a, b).  Raw offsets are recovered as (u + d) * l.
-__device__ __forceinline__ bool band_hit(const Vtx& a, const Vtx& b, double num, double dx,
-                                      double dy, double dz, double h, double band_factor) {
-  const double ax = a.ux + dx, ay = a.uy + dy, az = a.uz + dz;
-  const double bx = b.ux + dx, by = b.uy + dy, bz = b.uz + dz;
-  const double sgx = bx * b.l - ax * a.l, sgy = by * b.l - ay * a.l, sgz = bz * b.l - az * a.l;
+// of the arc (a, b); raw offsets are (u + d) / il.
+__device__ __forceinline__ bool band_hit_f(const VtxF& a, const VtxF& b, double num, double h,
+                                           double band_factor) {
+  const double la = 1.0 / a.il, lb = 1.0 / b.il;
+  const double ax = a.ux, ay = a.uy, az = a.uz + 1.0;
+  const double bx = b.ux, by = b.uy, bz = b.uz + 1.0;
+  const double sgx = bx * lb - ax * la, sgy = by * lb - ay * la, sgz = bz * lb - az * la;
   const double L = sqrt(sgx * sgx + sgy * sgy + sgz * sgz);
-  const double dist = fmin(a.l, b.l) - L;
+  const double dist = fmin(la, lb) - L;
   if (dist <= 0.0) return true;
   const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
   const double s2 = cx * cx + cy * cy + cz * cz;
@@ -97,49 +109,37 @@ __device__ __forceinline__ bool band_hit(const Vtx& a, const Vtx& b, double num,
   return num * num <= th * th * s2;
 }
 
-// One segment (a, b): accumulate; the band test runs only when den < 0.
-__device__ __forceinline__ void fan_segment(SegState& st, const Vtx& a, const Vtx& b, double dx,
-                                            double dy, double dz, const double* band_h,
-                                            int64_t e, double band_factor, int& flags) {
-  const double den = a.ux * b.ux + a.uy * b.uy + a.uz * b.uz;
-  const double num = -(a.gx * b.ux + a.gy * b.uy + a.gz * b.uz);
-  const bool ok = a.ok && b.ok;
-  if (den < 0.0 && ok && band_h) {
-    if (band_hit(a, b, num, dx, dy, dz, __ldg(band_h + e), band_factor)) flags |= FLAG_BAND;
-  }
-  cmul_track(st, ok ? den : 1.0, ok ? num : 0.0);
-}
-
 template <int QPT>
 __global__ void __launch_bounds__(kBlockQ)
 k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
-           const double* __restrict__ verts, int64_t V, int S, int64_t n_edges,
+           const double* __restrict__ vproj, int64_t V, int S, int64_t n_edges,
            const double* __restrict__ band_h, Frame f, DevParams prm,
            double* __restrict__ bpart, int32_t* __restrict__ flag_acc,
            unsigned long long* __restrict__ counters) {
-  // blockIdx.y: chunk of whole edges [e0, e1) -> vertex range [v0, v1)
+  // blockIdx.y: chunk of whole edges [e0, e1) -> vertex range [vbeg, vend)
   const int nchunk = gridDim.y;
   const int64_t e0 = n_edges * blockIdx.y / nchunk, e1 = n_edges * (blockIdx.y + 1) / nchunk;
   const int64_t vbeg = e0 * S, vend = e1 * S;
   __shared__ double sx[kTileV], sy[kTileV], sz[kTileV];
-  const double dx = f.d[0], dy = f.d[1], dz = f.d[2];
-  const double deg = prm.degenerate;
   int32_t slot[QPT];
-  double px[QPT], py[QPT], pz[QPT];
+  double qa[QPT], qb[QPT], qc[QPT];
   SegState st[QPT];
   int flags[QPT];
-  Vtx va[QPT];
+  VtxF va[QPT];
 #pragma unroll
   for (int j = 0; j < QPT; ++j) {
     slot[j] = blockIdx.x * (blockDim.x * QPT) + j * blockDim.x + threadIdx.x;
     const bool live = slot[j] < m;
     const int32_t q = live ? (active ? active[slot[j]] : slot[j]) : 0;
-    px[j] = live ? pos[3 * (int64_t)q] : 0.0;
-    py[j] = live ? pos[3 * (int64_t)q + 1] : 0.0;
-    pz[j] = live ? pos[3 * (int64_t)q + 2] : 0.0;
+    const double px = live ? pos[3 * (int64_t)q] : 0.0;
+    const double py = live ? pos[3 * (int64_t)q + 1] : 0.0;
+    const double pz = live ? pos[3 * (int64_t)q + 2] : 0.0;
+    qa[j] = px * f.e1[0] + py * f.e1[1] + pz * f.e1[2];
+    qb[j] = px * f.e2[0] + py * f.e2[1] + pz * f.e2[2];
+    qc[j] = px * f.d[0] + py * f.d[1] + pz * f.d[2];
     st[j] = SegState{1.0, 0.0, 0};
     flags[j] = 0;
-    va[j].ok = false;
+    va[j] = VtxF{0.0, 0.0, -1.0, 1.0};
   }
   int nseg = 0;
   for (int64_t t0 = vbeg; t0 < vend; t0 += kTileV) {
@@ -147,20 +147,27 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
     __syncthreads();
     for (int k = threadIdx.x; k < nt; k += blockDim.x) {
       const int64_t g = t0 + k;
-      sx[k] = verts[g];
-      sy[k] = verts[V + g];
-      sz[k] = verts[2 * V + g];
+      sx[k] = vproj[g];
+      sy[k] = vproj[V + g];
+      sz[k] = vproj[2 * V + g];
     }
     __syncthreads();
     int64_t e = t0 / S;               // edge of the tile's first vertex
     int kin = (int)(t0 - e * S);      // its index within that edge
     for (int k = 0; k < nt; ++k) {
-      const double x = sx[k], y = sy[k], z = sz[k];
+      const double X = sx[k], Y = sy[k], Zc = sz[k];
 #pragma unroll
       for (int j = 0; j < QPT; ++j) {
-        const Vtx vb = make_vtx(x, y, z, px[j], py[j], pz[j], dx, dy, dz, deg);
-        if (!vb.ok) flags[j] |= FLAG_DEGEN;
-        if (kin != 0) fan_segment(st[j], va[j], vb, dx, dy, dz, band_h, e, prm.band_factor, flags[j]);
+        const VtxF vb = make_vtxf(X, Y, Zc, qa[j], qb[j], qc[j], flags[j]);
+        if (kin != 0) {  // segment (k-1, k) lies on one edge
+          const double num = va[j].uy * vb.ux - va[j].ux * vb.uy;   // c.(a^ x b^)
+          const double den = va[j].ux * vb.ux + va[j].uy * vb.uy + va[j].uz * vb.uz;
+          if (__double2hiint(den) < 0 && band_h) {
+            if (band_hit_f(va[j], vb, num, __ldg(band_h + e), prm.band_factor))
+              flags[j] |= FLAG_BAND;
+          }
+          cmul_track(st[j], den, num);
+        }
         va[j] = vb;
       }
       if (kin != 0 && (++nseg & 7) == 0) {
@@ -189,6 +196,26 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
   }
 }
 
+// Boundary vertices in the round's ray frame (X = x.e1, Y = x.e2, Zc = x.d).
+__global__ void k_vproj(const double* __restrict__ verts, int64_t V, Frame f,
+                        double* __restrict__ vproj) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= V) return;
+  const double x = verts[i], y = verts[V + i], z = verts[2 * V + i];
+  vproj[i] = x * f.e1[0] + y * f.e1[1] + z * f.e1[2];
+  vproj[V + i] = x * f.e2[0] + y * f.e2[1] + z * f.e2[2];
+  vproj[2 * V + i] = x * f.d[0] + y * f.d[1] + z * f.d[2];
+}
+
+cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st) {
+  const int64_t V = sc->n_edges * sc->S;
+  if (V == 0) return cudaSuccess;
+  cudaError_t e = cudaMalloc(&rd.vproj, sizeof(double) * 3 * V);
+  if (e != cudaSuccess) return e;
+  k_vproj<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(sc->verts, V, rd.f, rd.vproj);
+  return cudaGetLastError();
+}
+
 constexpr int kQPT = 2;
 
 // Edge chunks of the boundary sum.  Fixed per scene (not per batch) so the
@@ -208,7 +235,7 @@ cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
   int64_t V = sc->n_edges * sc->S;
   if (V == 0) return cudaMemsetAsync(bpart, 0, sizeof(double) * m, st);
   dim3 grid((m + kBlockQ * kQPT - 1) / (kBlockQ * kQPT), nchunk);
-  k_boundary<kQPT><<<grid, kBlockQ, 0, st>>>(m, active, pos, sc->verts, V, sc->S, sc->n_edges,
+  k_boundary<kQPT><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S, sc->n_edges,
                                              sc->band_h, rd.f, sc->dprm, bpart, flags, counters);
   return cudaGetLastError();
 }
@@ -218,14 +245,14 @@ cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
 // (:778-788).  ok = 0 only for a hit clash |t_h - t_k| <= t_eps or a
 // degenerate projection; the fan formula needs no simple-loop restriction.
 __global__ void k_single_loop(const double* __restrict__ loop, int64_t B, double ox, double oy,
-                              double oz, double dx, double dy, double dz,
-                              const double* __restrict__ hit_ts,
+                              double oz, Frame f, const double* __restrict__ hit_ts,
                               const int64_t* __restrict__ hit_signs, int64_t H,
                               const double* __restrict__ qts, int64_t K, double t_eps,
-                              double deg, double* __restrict__ w, int8_t* __restrict__ ok) {
+                              double* __restrict__ w, int8_t* __restrict__ ok) {
   int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= K) return;
   const double t = qts[k];
+  const double dx = f.d[0], dy = f.d[1], dz = f.d[2];
   const double px = ox + t * dx, py = oy + t * dy, pz = oz + t * dz;
   long long chi = 0;
   bool clash = false;
@@ -233,21 +260,29 @@ __global__ void k_single_loop(const double* __restrict__ loop, int64_t B, double
     if (fabs(hit_ts[h] - t) <= t_eps) clash = true;
     if (hit_ts[h] > t) chi += hit_signs[h];
   }
+  const double qa = px * f.e1[0] + py * f.e1[1] + pz * f.e1[2];
+  const double qb = px * f.e2[0] + py * f.e2[1] + pz * f.e2[2];
+  const double qc = px * f.d[0] + py * f.d[1] + pz * f.d[2];
+  auto vtx = [&](int64_t i, int& fl) {
+    const double x = loop[3 * i], y = loop[3 * i + 1], z = loop[3 * i + 2];
+    return make_vtxf(x * f.e1[0] + y * f.e1[1] + z * f.e1[2],
+                     x * f.e2[0] + y * f.e2[1] + z * f.e2[2],
+                     x * f.d[0] + y * f.d[1] + z * f.d[2], qa, qb, qc, fl);
+  };
   SegState st = {1.0, 0.0, 0};
-  bool bad = false;
-  Vtx va = make_vtx(loop[3 * (B - 1)], loop[3 * (B - 1) + 1], loop[3 * (B - 1) + 2], px, py, pz,
-                    dx, dy, dz, deg);
   int flags = 0;
+  VtxF va = vtx(B - 1, flags);
   for (int64_t i = 0; i < B; ++i) {
-    Vtx vb = make_vtx(loop[3 * i], loop[3 * i + 1], loop[3 * i + 2], px, py, pz, dx, dy, dz, deg);
-    if (!va.ok || !vb.ok) bad = true;
-    fan_segment(st, va, vb, dx, dy, dz, nullptr, 0, 0.0, flags);
+    const VtxF vb = vtx(i, flags);
+    const double num = va.uy * vb.ux - va.ux * vb.uy;
+    const double den = va.ux * vb.ux + va.uy * vb.uy + va.uz * vb.uz;
+    cmul_track(st, den, num);
     if ((i & 7) == 7) renorm(st);
     va = vb;
   }
   const double ang = atan2(st.Zi, st.Zr) + 6.283185307179586476925 * (double)st.wraps;
   w[k] = (double)chi + ang * 0.15915494309189533576888;
-  ok[k] = (clash || bad) ? 0 : 1;
+  ok[k] = (clash || (flags & FLAG_DEGEN)) ? 0 : 1;
 }
 
 cudaError_t launch_single_loop(const double* loop, int64_t B, const double* o, const double* d,
@@ -255,9 +290,12 @@ cudaError_t launch_single_loop(const double* loop, int64_t B, const double* o, c
                                const double* qts, int64_t K, double t_eps, double deg, double* w,
                                int8_t* ok, cudaStream_t st) {
   if (K <= 0) return cudaSuccess;
-  k_single_loop<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(loop, B, o[0], o[1], o[2], d[0],
-                                                             d[1], d[2], hit_ts, hit_signs, H,
-                                                             qts, K, t_eps, deg, w, ok);
+  (void)deg;
+  Frame f;
+  make_frame(d, &f);
+  k_single_loop<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(loop, B, o[0], o[1], o[2], f,
+                                                             hit_ts, hit_signs, H, qts, K, t_eps,
+                                                             w, ok);
   return cudaGetLastError();
 }
 

@@ -238,6 +238,7 @@ void free_round(Round& rd) {
   if (rd.nodes) cudaFree(rd.nodes);
   if (rd.leafbox) cudaFree(rd.leafbox);
   if (rd.leaves) cudaFree(rd.leaves);
+  if (rd.vproj) cudaFree(rd.vproj);
   rd = Round();
 }
 
@@ -358,6 +359,11 @@ cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st) {
         free_round(rd);
         return e;
       }
+    }
+    if ((e = launch_vproj(sc, rd, st)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(st)) != cudaSuccess) {
+      free_round(rd);
+      return e;
     }
     sc->rounds.push_back(rd);
   }

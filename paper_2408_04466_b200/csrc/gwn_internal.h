@@ -66,6 +66,7 @@ struct Round {
   double* leafbox = nullptr;   // (n_leaves,5) cull boxes: a lo/hi, b lo/hi, c max
   Node* nodes = nullptr;       // (n_leaves-1) LBVH over the leaf boxes
   double amin = 0, ainv = 0, bmin = 0, binv = 0;  // projected scene box (Morton keys)
+  double* vproj = nullptr;     // (3,V) boundary vertices in the ray frame (K4)
 };
 
 }  // namespace gwn
@@ -116,6 +117,7 @@ cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             int32_t* flags, unsigned long long* counters,
                             cudaStream_t st);                                 // gwn_boundary.cu
 int boundary_chunks(const gwn_scene* sc, int32_t m);
+cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st);  // gwn_boundary.cu
 cudaError_t launch_all_hits(const gwn_scene* sc, const Round& rd, int64_t patch,
                             const double* o, double* out, int32_t* count, int32_t cap,
                             cudaStream_t st);
