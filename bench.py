@@ -41,8 +41,8 @@ sys.path.insert(0, HERE)
 FLOP_NEWTON = 234.0    # K3 Newton iteration: 2 Bernstein bases, value + partials
                        # of A and B (2 x 88), 2x2 solve
 FLOP_ROOT = 110.0      # K3 accepted root: C value/partials, normal, record tests
-FLOP_SEGMENT = 49.0    # K4 per (query, net segment): vertex (3 sub, |r|^2, rsqrt,
-                       # u = r/|r| - d, d x u) + den, num, complex product
+FLOP_SEGMENT = 34.0    # K4 per (query, net segment) in the ray frame: vertex (3 sub, |r|^2 5,
+                       # rsqrt seed + Halley 8, u 4) + num 3, den 5, complex product 6
 
 CONFIG_DESC = {
     1: "config1: single open bicubic patch, 4096 queries U[-0.5,1.5]^3",

@@ -147,6 +147,9 @@ int64_t gwn_net_boundary(const double* ctrl, int64_t n_patches, double* out_ctrl
 /* FP64 peak microbenchmark (DFMA chains on every SM), TFLOP/s. */
 int gwn_fp64_peak(int device, double* tflops, double* ms);
 
+/* Max ulp error of K4's reciprocal square root over a log-uniform sweep. */
+int gwn_selftest_rsqrt(int device, int64_t n, uint64_t* max_ulp);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,7 +29,7 @@ EXPORTS = (
     "gwn_abi_version", "gwn_last_error", "gwn_params_default", "gwn_scene_create",
     "gwn_scene_destroy", "gwn_scene_info_get", "gwn_eval", "gwn_stats_get", "gwn_set_timing",
     "gwn_all_hits", "gwn_single_loop_batch", "gwn_direction", "gwn_jitter_dir",
-    "gwn_net_boundary", "gwn_fp64_peak",
+    "gwn_net_boundary", "gwn_fp64_peak", "gwn_selftest_rsqrt",
 )
 
 
@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
         L.gwn_net_boundary.argtypes = [dp, C.c_int64, dp, C.POINTER(C.c_int32)]
         L.gwn_net_boundary.restype = C.c_int64
         L.gwn_fp64_peak.argtypes = [C.c_int, dp, dp]
+        L.gwn_selftest_rsqrt.argtypes = [C.c_int, C.c_int64, C.POINTER(C.c_uint64)]
         _lib = L
     return _lib
 

@@ -38,11 +38,13 @@ __device__ __forceinline__ bool signbit_hi(double x) { return __double2hiint(x) 
 
 // multiply Z by (den + i num) with exact branch-cut bookkeeping
 __device__ __forceinline__ void cmul_track(SegState& s, double den, double num) {
-  double zr = s.Zr * den - s.Zi * num;
-  double zi = s.Zr * num + s.Zi * den;
-  bool a = signbit_hi(s.Zi), b = signbit_hi(num), c = signbit_hi(zi);
-  s.wraps += (!a && !b && c) ? 1 : 0;
-  s.wraps -= (a && b && !c) ? 1 : 0;
+  const double zr = s.Zr * den - s.Zi * num;
+  const double zi = s.Zr * num + s.Zi * den;
+  // arg(Z) + arg(z) crossed +pi (both upper half-planes, result lower) or
+  // -pi (both lower, result upper); sign bits of the high words
+  const unsigned a = (unsigned)__double2hiint(s.Zi), b = (unsigned)__double2hiint(num),
+                 c = (unsigned)__double2hiint(zi);
+  s.wraps += (int)((~a & ~b & c) >> 31) - (int)((a & b & ~c) >> 31);
   s.Zr = zr;
   s.Zi = zi;
 }
@@ -56,18 +58,17 @@ __device__ __forceinline__ void renorm(SegState& s) {
   s.Zi *= sc;
 }
 
-// Full-precision reciprocal square root: MUFU.RSQ64H seed + two Newton steps
-// (no special-value path; l2 > 0 is guaranteed unless the query sits on a
-// vertex, which the degenerate test flags anyway).
+// Full-precision reciprocal square root: MUFU.RSQ64H seed (~2^-22) + one
+// Halley step y(1 + e/2 + 3e^2/8), e = 1 - x y^2 (cubic convergence); no
+// special-value path (x > 0 unless the query sits on a vertex, which the
+// degenerate test flags).  Accuracy checked by gwn_selftest_rsqrt.
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double h = x * y;
-  double e = fma(-h, y, 1.0);
-  y = fma(0.5 * y, e, y);
-  h = x * y;
-  e = fma(-h, y, 1.0);
-  return fma(0.5 * y, e, y);
+  const double h = x * y;
+  const double e = fma(-h, y, 1.0);
+  const double p = fma(0.375, e, 0.5);
+  return fma(y * e, p, y);
 }
 
 // Per-vertex quantities of the shifted fan formula in the round's ray frame
@@ -77,14 +78,16 @@ struct VtxF {
   double il;           // 1 / |x - p|
 };
 
+// degenerate projection |x - p| < 1e-12 (_kernels.py:541-542): the high word
+// of l2 >= 0 is monotone in l2; hi(1e-24) = 0x3AF357C2
+constexpr int kDegHi = 0x3AF357C2;
+
 __device__ __forceinline__ VtxF make_vtxf(double X, double Y, double Zc, double qa, double qb,
-                                          double qc, int& flags) {
+                                          double qc, int& minhi) {
   VtxF v;
   const double rx = X - qa, ry = Y - qb, rz = Zc - qc;
   const double l2 = rx * rx + ry * ry + rz * rz;
-  // degenerate projection |x - p| < 1e-12 (_kernels.py:541-542), integer
-  // compare on the IEEE pattern of l2 (monotone for l2 >= 0): 1e-24 = deg^2
-  if (__double_as_longlong(l2) < 0x3AF357C299A88EA7LL) flags |= FLAG_DEGEN;
+  minhi = min(minhi, __double2hiint(l2));
   v.il = rsqrt_nr(l2);
   v.ux = rx * v.il;
   v.uy = ry * v.il;
@@ -110,7 +113,7 @@ __device__ __forceinline__ bool band_hit_f(const VtxF& a, const VtxF& b, double 
 }
 
 template <int QPT>
-__global__ void __launch_bounds__(kBlockQ)
+__global__ void __launch_bounds__(kBlockQ, 3)
 k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
            const double* __restrict__ vproj, int64_t V, int S, int64_t n_edges,
            const double* __restrict__ band_h, Frame f, DevParams prm,
@@ -141,6 +144,19 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
     flags[j] = 0;
     va[j] = VtxF{0.0, 0.0, -1.0, 1.0};
   }
+  int minhi[QPT];
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) minhi[j] = 0x7fffffff;
+  // one segment (A -> B) of query j
+  auto seg = [&](int j, const VtxF& A, const VtxF& B, int64_t e) {
+    const double num = A.uy * B.ux - A.ux * B.uy;   // c.(a^ x b^)
+    const double den = A.ux * B.ux + A.uy * B.uy + A.uz * B.uz;
+    if (__double2hiint(den) < 0 && band_h) {
+      if (band_hit_f(A, B, num, __ldg(band_h + e), prm.band_factor)) flags[j] |= FLAG_BAND;
+    }
+    cmul_track(st[j], den, num);
+  };
+  VtxF vb[QPT];
   int nseg = 0;
   for (int64_t t0 = vbeg; t0 < vend; t0 += kTileV) {
     const int nt = (int)min((int64_t)kTileV, vend - t0);
@@ -154,21 +170,50 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
     __syncthreads();
     int64_t e = t0 / S;               // edge of the tile's first vertex
     int kin = (int)(t0 - e * S);      // its index within that edge
-    for (int k = 0; k < nt; ++k) {
+    // unrolled by two vertices with the carried vertex alternating between
+    // va and vb, so no per-vertex register copies
+    int k = 0;
+    for (; k + 1 < nt; k += 2) {
+      {
+        const double X = sx[k], Y = sy[k], Zc = sz[k];
+#pragma unroll
+        for (int j = 0; j < QPT; ++j) {
+          vb[j] = make_vtxf(X, Y, Zc, qa[j], qb[j], qc[j], minhi[j]);
+          if (kin != 0) seg(j, va[j], vb[j], e);
+        }
+        if (kin != 0 && (++nseg & 7) == 0) {
+#pragma unroll
+          for (int j = 0; j < QPT; ++j) renorm(st[j]);
+        }
+        if (++kin == S) {
+          kin = 0;
+          ++e;
+        }
+      }
+      {
+        const double X = sx[k + 1], Y = sy[k + 1], Zc = sz[k + 1];
+#pragma unroll
+        for (int j = 0; j < QPT; ++j) {
+          va[j] = make_vtxf(X, Y, Zc, qa[j], qb[j], qc[j], minhi[j]);
+          if (kin != 0) seg(j, vb[j], va[j], e);
+        }
+        if (kin != 0 && (++nseg & 7) == 0) {
+#pragma unroll
+          for (int j = 0; j < QPT; ++j) renorm(st[j]);
+        }
+        if (++kin == S) {
+          kin = 0;
+          ++e;
+        }
+      }
+    }
+    if (k < nt) {  // odd tile length
       const double X = sx[k], Y = sy[k], Zc = sz[k];
 #pragma unroll
       for (int j = 0; j < QPT; ++j) {
-        const VtxF vb = make_vtxf(X, Y, Zc, qa[j], qb[j], qc[j], flags[j]);
-        if (kin != 0) {  // segment (k-1, k) lies on one edge
-          const double num = va[j].uy * vb.ux - va[j].ux * vb.uy;   // c.(a^ x b^)
-          const double den = va[j].ux * vb.ux + va[j].uy * vb.uy + va[j].uz * vb.uz;
-          if (__double2hiint(den) < 0 && band_h) {
-            if (band_hit_f(va[j], vb, num, __ldg(band_h + e), prm.band_factor))
-              flags[j] |= FLAG_BAND;
-          }
-          cmul_track(st[j], den, num);
-        }
-        va[j] = vb;
+        vb[j] = make_vtxf(X, Y, Zc, qa[j], qb[j], qc[j], minhi[j]);
+        if (kin != 0) seg(j, va[j], vb[j], e);
+        va[j] = vb[j];
       }
       if (kin != 0 && (++nseg & 7) == 0) {
 #pragma unroll
@@ -180,6 +225,9 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
       }
     }
   }
+#pragma unroll
+  for (int j = 0; j < QPT; ++j)
+    if (minhi[j] < kDegHi) flags[j] |= FLAG_DEGEN;
 #pragma unroll
   for (int j = 0; j < QPT; ++j) {
     if (slot[j] < m) {
@@ -194,6 +242,29 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
     int64_t segs = (vend - vbeg) - (e1 - e0);
     atomicAdd(&counters[CNT_SEGMENTS], (unsigned long long)(segs * nq));
   }
+}
+
+// Accuracy of rsqrt_nr against the correctly rounded 1/sqrt on a log-uniform
+// sweep of [1e-20, 1e20] (gwn_selftest_rsqrt).
+__global__ void k_rsqrt_selftest(int64_t n, unsigned long long* max_ulp) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = exp10(-20.0 + 40.0 * ((double)i + 0.5) / (double)n);
+  const double ref = __drcp_rn(__dsqrt_rn(x));
+  const double got = rsqrt_nr(x);
+  const long long d = __double_as_longlong(got) - __double_as_longlong(ref);
+  atomicMax(max_ulp, (unsigned long long)(d < 0 ? -d : d));
+}
+
+cudaError_t selftest_rsqrt(int64_t n, unsigned long long* max_ulp_host) {
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(unsigned long long));
+  if (e != cudaSuccess) return e;
+  cudaMemset(d, 0, sizeof(unsigned long long));
+  k_rsqrt_selftest<<<(unsigned)((n + 255) / 256), 256>>>(n, d);
+  e = cudaMemcpy(max_ulp_host, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e;
 }
 
 // Boundary vertices in the round's ray frame (X = x.e1, Y = x.e2, Zc = x.d).
@@ -263,17 +334,17 @@ __global__ void k_single_loop(const double* __restrict__ loop, int64_t B, double
   const double qa = px * f.e1[0] + py * f.e1[1] + pz * f.e1[2];
   const double qb = px * f.e2[0] + py * f.e2[1] + pz * f.e2[2];
   const double qc = px * f.d[0] + py * f.d[1] + pz * f.d[2];
-  auto vtx = [&](int64_t i, int& fl) {
+  auto vtx = [&](int64_t i, int& mh) {
     const double x = loop[3 * i], y = loop[3 * i + 1], z = loop[3 * i + 2];
     return make_vtxf(x * f.e1[0] + y * f.e1[1] + z * f.e1[2],
                      x * f.e2[0] + y * f.e2[1] + z * f.e2[2],
-                     x * f.d[0] + y * f.d[1] + z * f.d[2], qa, qb, qc, fl);
+                     x * f.d[0] + y * f.d[1] + z * f.d[2], qa, qb, qc, mh);
   };
   SegState st = {1.0, 0.0, 0};
-  int flags = 0;
-  VtxF va = vtx(B - 1, flags);
+  int minhi = 0x7fffffff;
+  VtxF va = vtx(B - 1, minhi);
   for (int64_t i = 0; i < B; ++i) {
-    const VtxF vb = vtx(i, flags);
+    const VtxF vb = vtx(i, minhi);
     const double num = va.uy * vb.ux - va.ux * vb.uy;
     const double den = va.ux * vb.ux + va.uy * vb.uy + va.uz * vb.uz;
     cmul_track(st, den, num);
@@ -282,7 +353,7 @@ __global__ void k_single_loop(const double* __restrict__ loop, int64_t B, double
   }
   const double ang = atan2(st.Zi, st.Zr) + 6.283185307179586476925 * (double)st.wraps;
   w[k] = (double)chi + ang * 0.15915494309189533576888;
-  ok[k] = (clash || (flags & FLAG_DEGEN)) ? 0 : 1;
+  ok[k] = (clash || minhi < kDegHi) ? 0 : 1;
 }
 
 cudaError_t launch_single_loop(const double* loop, int64_t B, const double* o, const double* d,

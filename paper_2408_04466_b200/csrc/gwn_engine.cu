@@ -493,3 +493,17 @@ done:
   cudaFree(d_ok);
   return rc;
 }
+
+extern "C" int gwn_selftest_rsqrt(int device, int64_t n, uint64_t* max_ulp) {
+  int rc = GWN_OK;
+  unsigned long long m = 0;
+  if (!max_ulp || n <= 0) {
+    set_error("gwn_selftest_rsqrt: invalid arguments");
+    return GWN_E_INVALID;
+  }
+  CKE(cudaSetDevice(device));
+  CKE(selftest_rsqrt(n, &m));
+  *max_ulp = m;
+done:
+  return rc;
+}

@@ -118,6 +118,7 @@ cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             cudaStream_t st);                                 // gwn_boundary.cu
 int boundary_chunks(const gwn_scene* sc, int32_t m);
 cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st);  // gwn_boundary.cu
+cudaError_t selftest_rsqrt(int64_t n, unsigned long long* max_ulp_host);
 cudaError_t launch_all_hits(const gwn_scene* sc, const Round& rd, int64_t patch,
                             const double* o, double* out, int32_t* count, int32_t cap,
                             cudaStream_t st);

@@ -179,3 +179,11 @@ def test_single_loop_batch_matches_fixed_reference(golden_dir):
 def test_fp64_peak_measures():
     tf, ms = G.fp64_peak(0)
     assert 10.0 < tf < 60.0, tf
+
+
+def test_k4_rsqrt_full_precision():
+    import ctypes as C
+    from paper_2408_04466_b200 import _lib
+    u = C.c_uint64()
+    _lib.check(_lib.lib().gwn_selftest_rsqrt(0, 1 << 20, C.byref(u)), "gwn_selftest_rsqrt")
+    assert u.value <= 2, u.value
