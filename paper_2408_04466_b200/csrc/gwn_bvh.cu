@@ -12,6 +12,10 @@
 // thread per internal node, bottom-up refit with atomic arrival counters.
 #include <cub/cub.cuh>
 
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
 #include "gwn_patch.cuh"
 
 namespace gwn {
@@ -205,32 +209,222 @@ __global__ void k_refit(int n, const int32_t* __restrict__ sorted_ids,
   }
 }
 
-// 30-bit Morton key of each query's projection (p.e1, p.e2): sorting the
-// round-0 queries by it makes warps traverse the LBVH and touch the leaf
-// records coherently.
-__global__ void k_query_keys(int32_t m, const double* __restrict__ pos, Frame f, double amin,
-                             double ainv, double bmin, double binv, uint32_t* __restrict__ keys,
-                             int32_t* __restrict__ ids) {
-  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= m) return;
+// Round-0 spatial ordering of the queries: a counting sort into the 256
+// cells of a 16 x 16 Morton grid over the projected scene box (~4K queries
+// per cell at 1M queries, so every warp stays inside one cell).  Warps then
+// traverse the LBVH and touch leaf records coherently.  The order inside a
+// cell depends on atomic timing, which no result depends on (all reductions
+// are keyed by query slot).
+constexpr int kBuckets = 256;
+
+__device__ __forceinline__ int query_bucket(const double* __restrict__ pos, int32_t s,
+                                            const Frame& f, double amin, double ainv,
+                                            double bmin, double binv) {
   const double x = pos[3 * (int64_t)s], y = pos[3 * (int64_t)s + 1], z = pos[3 * (int64_t)s + 2];
   const double a = x * f.e1[0] + y * f.e1[1] + z * f.e1[2];
   const double b = x * f.e2[0] + y * f.e2[1] + z * f.e2[2];
-  const uint32_t ia = (uint32_t)fmin(fmax((a - amin) * ainv * 32767.0, 0.0), 32767.0);
-  const uint32_t ib = (uint32_t)fmin(fmax((b - bmin) * binv * 32767.0, 0.0), 32767.0);
+  const uint32_t ia = (uint32_t)fmin(fmax((a - amin) * ainv * 16.0, 0.0), 15.0);
+  const uint32_t ib = (uint32_t)fmin(fmax((b - bmin) * binv * 16.0, 0.0), 15.0);
   uint32_t key = 0;
-  for (int bit = 0; bit < 15; ++bit)
+  for (int bit = 0; bit < 4; ++bit)
     key |= (((ia >> bit) & 1u) << (2 * bit)) | (((ib >> bit) & 1u) << (2 * bit + 1));
-  keys[s] = key;
-  ids[s] = s;
+  return (int)key;
 }
 
-cudaError_t launch_query_keys(const Round& rd, int32_t m, const double* pos, uint32_t* keys,
-                              int32_t* ids, cudaStream_t st) {
+__global__ void __launch_bounds__(256)
+k_bucket_count(int32_t m, const double* __restrict__ pos, Frame f, double amin, double ainv,
+               double bmin, double binv, uint16_t* __restrict__ keys,
+               int32_t* __restrict__ hist) {
+  __shared__ int32_t h[kBuckets];
+  for (int k = threadIdx.x; k < kBuckets; k += blockDim.x) h[k] = 0;
+  __syncthreads();
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < m) {
+    const int key = query_bucket(pos, s, f, amin, ainv, bmin, binv);
+    keys[s] = (uint16_t)key;
+    atomicAdd(&h[key], 1);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kBuckets; k += blockDim.x)
+    if (h[k]) atomicAdd(&hist[k], h[k]);
+}
+
+// exclusive scan of the kBuckets counts (one block), cursors zeroed
+__global__ void __launch_bounds__(kBuckets) k_bucket_scan(int32_t* __restrict__ hist,
+                                                          int32_t* __restrict__ cursor) {
+  __shared__ int32_t part[kBuckets];
+  const int t = threadIdx.x;
+  const int32_t v = hist[t];
+  part[t] = v;
+  __syncthreads();
+  for (int o = 1; o < kBuckets; o <<= 1) {
+    const int32_t add = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += add;
+    __syncthreads();
+  }
+  hist[t] = part[t] - v;
+  cursor[t] = 0;
+}
+
+__global__ void __launch_bounds__(256)
+k_bucket_scatter(int32_t m, const uint16_t* __restrict__ keys, const int32_t* __restrict__ offs,
+                 int32_t* __restrict__ cursor, int32_t* __restrict__ perm) {
+  __shared__ int32_t cnt[kBuckets];
+  __shared__ int32_t base[kBuckets];
+  for (int k = threadIdx.x; k < kBuckets; k += blockDim.x) cnt[k] = 0;
+  __syncthreads();
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  int key = 0, local = 0;
+  if (s < m) {
+    key = keys[s];
+    local = atomicAdd(&cnt[key], 1);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kBuckets; k += blockDim.x)
+    if (cnt[k]) base[k] = atomicAdd(&cursor[k], cnt[k]);
+  __syncthreads();
+  if (s < m) perm[offs[key] + base[key] + local] = s;
+}
+
+cudaError_t launch_query_order(const Round& rd, int32_t m, const double* pos, void* scratch,
+                               int32_t* perm, cudaStream_t st) {
   if (m <= 0) return cudaSuccess;
-  k_query_keys<<<(m + 255) / 256, 256, 0, st>>>(m, pos, rd.f, rd.amin, rd.ainv, rd.bmin, rd.binv,
-                                                keys, ids);
+  int32_t* hist = (int32_t*)scratch;
+  int32_t* cursor = hist + kBuckets;
+  uint16_t* keys = (uint16_t*)(cursor + kBuckets);
+  cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(int32_t) * kBuckets, st);
+  if (e != cudaSuccess) return e;
+  const unsigned g = (unsigned)((m + 255) / 256);
+  k_bucket_count<<<g, 256, 0, st>>>(m, pos, rd.f, rd.amin, rd.ainv, rd.bmin, rd.binv, keys, hist);
+  k_bucket_scan<<<1, kBuckets, 0, st>>>(hist, cursor);
+  k_bucket_scatter<<<g, 256, 0, st>>>(m, keys, hist, cursor, perm);
   return cudaGetLastError();
+}
+
+size_t query_order_scratch_bytes(int32_t m) {
+  return sizeof(int32_t) * 2 * kBuckets + sizeof(uint16_t) * ((size_t)m + 8);
+}
+
+// ---- uniform grid over the leaf boxes ------------------------------------
+
+__global__ void k_leaf_extent_sum(const double* __restrict__ leafbox, int64_t n,
+                                  double* __restrict__ acc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double w = 0.0, h = 0.0;
+  if (i < n) {
+    w = leafbox[5 * i + 1] - leafbox[5 * i];
+    h = leafbox[5 * i + 3] - leafbox[5 * i + 2];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    w += __shfl_down_sync(0xffffffffu, w, o);
+    h += __shfl_down_sync(0xffffffffu, h, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(acc, w);
+    atomicAdd(acc + 1, h);
+  }
+}
+
+__device__ __forceinline__ void leaf_cells(const double* b, double gx0, double gy0, double gia,
+                                           double gib, int ga, int gb, int& i0, int& i1, int& j0,
+                                           int& j1) {
+  i0 = max(0, min(ga - 1, (int)floor((b[0] - gx0) * gia)));
+  i1 = max(0, min(ga - 1, (int)floor((b[1] - gx0) * gia)));
+  j0 = max(0, min(gb - 1, (int)floor((b[2] - gy0) * gib)));
+  j1 = max(0, min(gb - 1, (int)floor((b[3] - gy0) * gib)));
+}
+
+template <bool kFill>
+__global__ void k_grid_bin(const double* __restrict__ leafbox, int64_t n, double gx0, double gy0,
+                           double gia, double gib, int ga, int gb, int32_t* __restrict__ cnt,
+                           const int32_t* __restrict__ offs, int32_t* __restrict__ cells) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int i0, i1, j0, j1;
+  leaf_cells(leafbox + 5 * i, gx0, gy0, gia, gib, ga, gb, i0, i1, j0, j1);
+  for (int j = j0; j <= j1; ++j)
+    for (int ii = i0; ii <= i1; ++ii) {
+      const int c = j * ga + ii;
+      const int k = atomicAdd(&cnt[c], 1);
+      if (kFill) cells[offs[c] + k] = (int32_t)i;
+    }
+}
+
+// Build the grid if it stays compact: cell ~ half the mean leaf box extent.
+static cudaError_t build_grid(Round& rd, double amin, double amax, double bmin, double bmax,
+                              cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+  const int64_t n = rd.n_leaves;
+  double* acc = nullptr;
+  int32_t* cnt = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  double h[2] = {0, 0};
+  const char* mode = getenv("GWN_CULL");
+  if (mode && !strcmp(mode, "bvh")) return cudaSuccess;
+#define GC(x)                       \
+  do {                              \
+    e = (x);                        \
+    if (e != cudaSuccess) goto out; \
+  } while (0)
+  GC(cudaMalloc(&acc, 2 * sizeof(double)));
+  GC(cudaMemsetAsync(acc, 0, 2 * sizeof(double), st));
+  k_leaf_extent_sum<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rd.leafbox, n, acc);
+  GC(cudaMemcpyAsync(h, acc, sizeof h, cudaMemcpyDeviceToHost, st));
+  GC(cudaStreamSynchronize(st));
+  {
+    // wider than any leaf-box expansion (<= 1e-12 (1 + mag) + 3e-9 patch extent)
+    const double margin = 1e-8 * (1.0 + fabs(amin) + fabs(amax) + fabs(bmin) + fabs(bmax));
+    const double x0 = amin - margin, x1 = amax + margin, y0 = bmin - margin, y1 = bmax + margin;
+    const double cw = fmax(0.5 * h[0] / (double)n, (x1 - x0) / 4096.0);
+    const double ch = fmax(0.5 * h[1] / (double)n, (y1 - y0) / 4096.0);
+    const int ga = (int)fmin(4096.0, fmax(1.0, ceil((x1 - x0) / cw)));
+    const int gb = (int)fmin(4096.0, fmax(1.0, ceil((y1 - y0) / ch)));
+    const int64_t ncell = (int64_t)ga * gb;
+    if (ncell > (1ll << 24)) goto out;
+    rd.ga = ga;
+    rd.gb = gb;
+    rd.gx0 = x0;
+    rd.gy0 = y0;
+    rd.gia = ga / (x1 - x0);
+    rd.gib = gb / (y1 - y0);
+    GC(cudaMalloc(&cnt, sizeof(int32_t) * (ncell + 1)));
+    GC(cudaMalloc(&rd.cell_offs, sizeof(int32_t) * (ncell + 1)));
+    GC(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (ncell + 1), st));
+    k_grid_bin<false><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+        rd.leafbox, n, rd.gx0, rd.gy0, rd.gia, rd.gib, ga, gb, cnt, nullptr, nullptr);
+    GC(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, rd.cell_offs, (int)(ncell + 1), st));
+    GC(cudaMalloc(&tmp, tb));
+    GC(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, rd.cell_offs, (int)(ncell + 1), st));
+    int32_t total = 0;
+    GC(cudaMemcpyAsync(&total, rd.cell_offs + ncell, sizeof total, cudaMemcpyDeviceToHost, st));
+    GC(cudaStreamSynchronize(st));
+    // compact enough?  (else keep the LBVH)
+    if (total > 64 * n + 4096 && !(mode && !strcmp(mode, "grid"))) {
+      cudaFree(rd.cell_offs);
+      rd.cell_offs = nullptr;
+      goto out;
+    }
+    rd.grid_entries = total;
+    GC(cudaMalloc(&rd.cell_leaves, sizeof(int32_t) * ((size_t)total + 1)));
+    GC(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (ncell + 1), st));
+    k_grid_bin<true><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+        rd.leafbox, n, rd.gx0, rd.gy0, rd.gia, rd.gib, ga, gb, cnt, rd.cell_offs, rd.cell_leaves);
+    GC(cudaGetLastError());
+    GC(cudaStreamSynchronize(st));
+    rd.use_grid = true;
+    if (getenv("GWN_TRACE"))
+      fprintf(stderr, "[gwn] round grid %d x %d, %d entries for %lld leaves\n", ga, gb, total,
+              (long long)n);
+  }
+out:
+#undef GC
+  if (acc) cudaFree(acc);
+  if (cnt) cudaFree(cnt);
+  if (tmp) cudaFree(tmp);
+  return e;
 }
 
 void free_round(Round& rd) {
@@ -239,6 +433,8 @@ void free_round(Round& rd) {
   if (rd.leafbox) cudaFree(rd.leafbox);
   if (rd.leaves) cudaFree(rd.leaves);
   if (rd.vproj) cudaFree(rd.vproj);
+  if (rd.cell_offs) cudaFree(rd.cell_offs);
+  if (rd.cell_leaves) cudaFree(rd.cell_leaves);
   rd = Round();
 }
 
@@ -344,6 +540,7 @@ cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st) {
         }
       }
       RC(cudaStreamSynchronize(st));
+      RC(build_grid(rd, amin, amax, bmin, bmax, st));
     out:
       if (keys) cudaFree(keys);
       if (keys2) cudaFree(keys2);

@@ -27,9 +27,16 @@ __device__ __forceinline__ void query_proj(const Frame& f, const double* __restr
   qc = x * f.d[0] + y * f.d[1] + z * f.d[2];
 }
 
+struct GridView {
+  const int32_t* offs;
+  const int32_t* leaves;
+  int32_t na, nb;
+  double x0, y0, ia, ib;
+};
+
 __global__ void __launch_bounds__(128)
 k_cull(const Node* __restrict__ nodes, const double* __restrict__ leafbox, int64_t n_leaves,
-       Frame f, int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
+       GridView grid, Frame f, int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
        double* __restrict__ qproj, int32_t* __restrict__ pair_slot,
        int32_t* __restrict__ pair_leaf, unsigned long long* __restrict__ pair_count,
        unsigned long long cap) {
@@ -55,7 +62,21 @@ k_cull(const Node* __restrict__ nodes, const double* __restrict__ leafbox, int64
         }
       }
     };
-    if (n_leaves == 1) {
+    if (grid.offs) {
+      // uniform grid: one cell, a short list of leaf boxes
+      const double fa = (qa - grid.x0) * grid.ia, fb = (qb - grid.y0) * grid.ib;
+      if (fa >= 0.0 && fb >= 0.0 && fa < (double)grid.na && fb < (double)grid.nb) {
+        const int c = (int)fb * grid.na + (int)fa;
+        const int k1 = __ldg(grid.offs + c + 1);
+        for (int k = __ldg(grid.offs + c); k < k1; ++k) {
+          const int leaf = __ldg(grid.leaves + k);
+          const double* b = leafbox + 5 * (int64_t)leaf;
+          if (qa >= __ldg(b) && qa <= __ldg(b + 1) && qb >= __ldg(b + 2) && qb <= __ldg(b + 3) &&
+              __ldg(b + 4) >= qc)
+            emit(leaf);
+        }
+      }
+    } else if (n_leaves == 1) {
       const double* b = leafbox;
       if (qa >= b[0] && qa <= b[1] && qb >= b[2] && qb <= b[3] && b[4] >= qc) emit(0);
     } else {
@@ -107,7 +128,9 @@ cudaError_t launch_cull(const gwn_scene* sc, const Round& rd, int32_t m, const i
                         unsigned long long* pair_count, int64_t cap, cudaStream_t st) {
   (void)sc;
   if (m <= 0) return cudaSuccess;
-  k_cull<<<(m + 127) / 128, 128, 0, st>>>(rd.nodes, rd.leafbox, rd.n_leaves, rd.f, m, active,
+  GridView g{rd.use_grid ? rd.cell_offs : nullptr, rd.cell_leaves, rd.ga, rd.gb,
+              rd.gx0, rd.gy0, rd.gia, rd.gib};
+  k_cull<<<(m + 127) / 128, 128, 0, st>>>(rd.nodes, rd.leafbox, rd.n_leaves, g, rd.f, m, active,
                                           pos, qproj, pair_slot, pair_leaf, pair_count,
                                           (unsigned long long)cap);
   return cudaGetLastError();

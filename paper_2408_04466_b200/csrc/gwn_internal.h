@@ -67,6 +67,14 @@ struct Round {
   Node* nodes = nullptr;       // (n_leaves-1) LBVH over the leaf boxes
   double amin = 0, ainv = 0, bmin = 0, binv = 0;  // projected scene box (Morton keys)
   double* vproj = nullptr;     // (3,V) boundary vertices in the ray frame (K4)
+  // uniform grid over the leaf boxes (K2 point location); used when its
+  // cells stay short, else the LBVH
+  bool use_grid = false;
+  int32_t ga = 0, gb = 0;      // cells along a, b
+  double gx0 = 0, gy0 = 0, gia = 0, gib = 0;  // origin and inverse cell size
+  int32_t* cell_offs = nullptr;    // (ga*gb+1) exclusive offsets
+  int32_t* cell_leaves = nullptr;  // leaf ids per cell
+  int64_t grid_entries = 0;
 };
 
 }  // namespace gwn
@@ -110,8 +118,9 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
                              cudaEvent_t* ev4, unsigned long long* items_out, cudaEvent_t* join,
                              cudaStream_t st);                                // gwn_wavefront.cu
 size_t intersect_scratch_bytes(int64_t pair_cap);
-cudaError_t launch_query_keys(const Round& rd, int32_t m, const double* pos, uint32_t* keys,
-                              int32_t* ids, cudaStream_t st);                 // gwn_bvh.cu
+cudaError_t launch_query_order(const Round& rd, int32_t m, const double* pos, void* scratch,
+                               int32_t* perm, cudaStream_t st);               // gwn_bvh.cu
+size_t query_order_scratch_bytes(int32_t m);
 cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             const int32_t* active, const double* pos, double* bpart, int nchunk,
                             int32_t* flags, unsigned long long* counters,

@@ -26,11 +26,16 @@ struct NodeItem {
   uint64_t code;  // level:6 | iu:29 | iv:29
 };
 
-struct NewtonItem {
-  int32_t pair;
-  int32_t kind;   // 0: certified node, 1: level cap, 2: certified leaf (expanded box)
+// Self-contained Newton work item (one coalesced 64-byte load): the query
+// slot, the patch, the leaf code for ownership, the certified start and the
+// query's ray-frame projection.
+struct alignas(16) NewtonItem {
+  int32_t slot;
+  int32_t patch;
   uint64_t code;
   double u, v;
+  double qa, qb, qc;
+  double pad;
 };
 
 
@@ -94,15 +99,18 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev,
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < npairs; base += stride) {
     const int64_t i = base + threadIdx.x;
     bool wantN = false, wantF = false;
-    int32_t pair = (int32_t)i;
+    int32_t pair = (int32_t)i, slot = 0, patch = 0;
     uint64_t code = 0;
-    double nu_ = 0.0, nv_ = 0.0;
+    double nu_ = 0.0, nv_ = 0.0, qa = 0.0, qb = 0.0, qc = 0.0;
     if (i < npairs) {
       const LeafRec L = leaves[pair_leaf[i]];
       w.pair_patch[i] = L.patch;
+      patch = L.patch;
       code = L.code;
-      const int32_t slot = w.pair_slot[i];
-      const double qa = w.qproj[3 * (int64_t)slot], qb = w.qproj[3 * (int64_t)slot + 1];
+      slot = w.pair_slot[i];
+      qa = w.qproj[3 * (int64_t)slot];
+      qb = w.qproj[3 * (int64_t)slot + 1];
+      qc = w.qproj[3 * (int64_t)slot + 2];
       ++tested;
       const int lev = code_level(code);
       const double wu = code_wu(lev), wv = code_wv(lev);
@@ -135,7 +143,7 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev,
     long long k = warp_push(wantF, out_count, out_cap, w.overflow);
     if (k >= 0) out[k] = NodeItem{pair, 0, code};
     k = warp_push(wantN, w.n_count, w.n_cap, w.overflow);
-    if (k >= 0) w.nq[k] = NewtonItem{pair, 2, code, nu_, nv_};
+    if (k >= 0) w.nq[k] = NewtonItem{slot, patch, code, nu_, nv_, qa, qb, qc, 0.0};
   }
   warp_sum_u64(&w.counters[CNT_NODES], tested);
 }
@@ -236,56 +244,45 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
   if (lane == 0 && maxn) atomicMax(&w.counters[CNT_MAXNODES], maxn);
 }
 
-// Newton pass over the certified / level-cap nodes + ownership + K5 part 1.
+// Newton pass over the certified leaves + ownership + K5 part 1.
 __global__ void __launch_bounds__(128) k3_newton(WaveArgs w) {
   const int64_t n = (int64_t)*w.n_count;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   unsigned long long iters = 0, roots = 0;
+  const double span = 1.0 + 2.0 * kLeafM;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
     int32_t slot = -1, chi = 0, fl = 0;
     if (i < n) {
       const NewtonItem it = w.nq[i];
-      slot = w.pair_slot[it.pair];
-      const double* P48 = w.proj + 48 * (int64_t)w.pair_patch[it.pair];
-      const double* q = w.qproj + 3 * (int64_t)slot;
-      RootResult r = newton_solve(P48, q[0], q[1], q[2], it.u, it.v, w.prm);
+      slot = it.slot;
+      const double* P48 = w.proj + 48 * (int64_t)it.patch;
+      RootResult r = newton_solve(P48, it.qa, it.qb, it.qc, it.u, it.v, w.prm);
       iters += r.iters;
       const int level = code_level(it.code);
-      const double wu = ldexp(1.0, -((level + 1) >> 1));
-      const double wv = ldexp(1.0, -(level >> 1));
+      const double wu = code_wu(level), wv = code_wv(level);
       const double u0 = (double)code_iu(it.code) * wu, v0 = (double)code_iv(it.code) * wv;
       const double u1 = u0 + wu, v1 = v0 + wv;
       const double tol = w.prm.domain_tol;
-      if (r.status == ROOT_DIVERGED) {
-        if (it.kind != 1) fl |= FLAG_RESHOOT;  // certified root not reached: re-shoot
-      } else {
+      // the unique root lies in the certification box (leaf box expanded by
+      // kLeafM); landing farther away means Newton left the certified basin
+      const double ex = kLeafM + 1e-6;
+      const bool in_cert = r.u >= u0 - ex * wu && r.u <= u1 + ex * wu && r.v >= v0 - ex * wv &&
+                           r.v <= v1 + ex * wv;
+      (void)span;
+      if (r.status == ROOT_DIVERGED || !in_cert) {
+        fl |= FLAG_RESHOOT;  // certified root not reached: re-shoot
+      } else if (r.status == ROOT_ACCEPTED) {
         // half-open ownership box (domain edges own the tolerance band)
         const double lo_u = u0 == 0.0 ? -tol : u0, hi_u = u1 == 1.0 ? 1.0 + tol : u1;
         const double lo_v = v0 == 0.0 ? -tol : v0, hi_v = v1 == 1.0 ? 1.0 + tol : v1;
         const bool own = r.u >= lo_u && (r.u < hi_u || (u1 == 1.0 && r.u <= hi_u)) &&
                          r.v >= lo_v && (r.v < hi_v || (v1 == 1.0 && r.v <= hi_v));
         if (own) {
-          if (r.status == ROOT_ACCEPTED) {
-            ++roots;
-            chi = r.sign;
-            if (r.tang || r.graze) fl |= FLAG_RESHOOT;
-            if (r.onsurf) fl |= FLAG_ONSURF;
-          }
-        } else if (it.kind != 1) {
-          // certified: the unique root lies in the certification box (node
-          // +1e-7, or the kLeafM-expanded leaf box); farther away means Newton
-          // left the certified basin
-          const double ex = it.kind == 2 ? kLeafM + 1e-6 : 2e-7;
-          const double mu = ex * wu, mv = ex * wv;
-          if (r.u < u0 - mu || r.u > u1 + mu || r.v < v0 - mv || r.v > v1 + mv)
-            fl |= FLAG_RESHOOT;
-        } else {
-          // level cap: a root well outside this tiny node belongs elsewhere
-          if (r.status == ROOT_ACCEPTED && fabs(r.u - 0.5 * (u0 + u1)) < 2.0 * wu &&
-              fabs(r.v - 0.5 * (v0 + v1)) < 2.0 * wv) {
-            // a neighbour owns it
-          }
+          ++roots;
+          chi = r.sign;
+          if (r.tang || r.graze) fl |= FLAG_RESHOOT;
+          if (r.onsurf) fl |= FLAG_ONSURF;
         }
       }
     }
@@ -351,14 +348,21 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
     if ((e = cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming)) != cudaSuccess) return e;
   }
-  if ((e = cudaEventRecord(fork_ev, st)) != cudaSuccess) return e;
-  if ((e = cudaStreamWaitEvent(side, fork_ev, 0)) != cudaSuccess) return e;
-  if (ev4) cudaEventRecord(ev4[1], side);
-  k3_fallback<<<g_fb, 128, 0, side>>>(fq, cnt, w);
+  // In timing mode (ev4) everything runs on `st` so each kernel's events
+  // measure it alone.
+  cudaStream_t fs = ev4 ? st : side;
+  if (!ev4) {
+    if ((e = cudaEventRecord(fork_ev, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(side, fork_ev, 0)) != cudaSuccess) return e;
+  }
+  if (ev4) cudaEventRecord(ev4[1], fs);
+  k3_fallback<<<g_fb, 128, 0, fs>>>(fq, cnt, w);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (ev4) cudaEventRecord(ev4[2], side);
-  if ((e = cudaEventRecord(join_ev, side)) != cudaSuccess) return e;
-  *join = join_ev;
+  if (ev4) cudaEventRecord(ev4[2], fs);
+  if (!ev4) {
+    if ((e = cudaEventRecord(join_ev, side)) != cudaSuccess) return e;
+    *join = join_ev;
+  }
   if (ev4) cudaEventRecord(ev4[4], st);
   k3_newton<<<g_newton, 128, 0, st>>>(w);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
