@@ -148,54 +148,87 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev,
   warp_sum_u64(&w.counters[CNT_NODES], tested);
 }
 
-// Undecided leaves (rare; rays near a silhouette fold of the projection):
-// one item per warp, breadth-first below the leaf; the lanes test the item's
-// frontier nodes in parallel (node_test, gwn_dfs.cuh), so the critical path
-// is depth x node latency rather than node count x node latency.  Roots
-// count only in the node that owns them; undecidable nodes kDfsDepth levels
-// below the leaf flag the query for a new direction.
-constexpr int kFrontier = 128;
+// Undecided leaves (rays near a silhouette fold of the projection):
+// breadth-first below the leaf with a frontier shared by a batch of items per
+// warp; the lanes test frontier nodes of any item in parallel (node_test,
+// gwn_dfs.cuh).  Items per warp = ceil(items / warps), at most 32: few items
+// stay spread over the GPU, many items keep every lane busy.  Roots count only
+// in the node that owns them; undecidable nodes kDfsDepth levels below the
+// leaf flag the query for a new direction.
+constexpr int kFrontier = 512;
+constexpr int kFbWarps = 4;  // warps per block
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(32 * kFbWarps)
 k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restrict__ in_count,
             WaveArgs w) {
-  __shared__ uint64_t fr[4][2][kFrontier];
+  __shared__ uint64_t fr[kFbWarps][2][kFrontier];
+  __shared__ uint8_t fi[kFbWarps][2][kFrontier];
+  __shared__ double iq[kFbWarps][32][4];  // qa, qb, qc, eps_box
+  __shared__ int32_t islot[kFbWarps][32], ipatch[kFbWarps][32], imax[kFbWarps][32];
+  __shared__ int32_t ichi[kFbWarps][32], ifl[kFbWarps][32], inodes[kFbWarps][32];
   const int64_t n = (int64_t)*in_count;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wb = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long nodes = 0, iters = 0, roots = 0, maxn = 0;
-  for (int64_t i = warp; i < n; i += nwarps) {
-    const NodeItem it = in[i];
-    const int32_t slot = w.pair_slot[it.pair];
-    const double* q = w.qproj + 3 * (int64_t)slot;
-    const NodeCtx ctx = node_ctx(w.proj + 48 * (int64_t)w.pair_patch[it.pair], q[0], q[1], q[2],
-                                 w.prm);
-    const int max_level = min(code_level(it.code) + kDfsDepth, kMaxLevel);
-    int cur = 0, ncur = 1, item_nodes = 0;
-    int32_t chi = 0, fl = 0;
-    if (lane == 0) fr[wib][0][0] = it.code;
+  const long long want = (long long)((n + nwarps - 1) / nwarps);
+  const int ipw = (int)(want < 1 ? 1 : want > 32 ? 32 : want);
+  unsigned long long nodes = 0, iters = 0, roots = 0;
+  for (int64_t b0 = warp * ipw; b0 < n; b0 += nwarps * ipw) {
+    const int nb = (int)min((int64_t)ipw, n - b0);
+    if (lane < nb) {
+      const NodeItem it = in[b0 + lane];
+      const int32_t slot = w.pair_slot[it.pair];
+      const int32_t patch = w.pair_patch[it.pair];
+      const double* q = w.qproj + 3 * (int64_t)slot;
+      const NodeCtx c = node_ctx(w.proj + 48 * (int64_t)patch, q[0], q[1], q[2], w.prm);
+      iq[wb][lane][0] = c.qa;
+      iq[wb][lane][1] = c.qb;
+      iq[wb][lane][2] = c.qc;
+      iq[wb][lane][3] = c.eps_box;
+      islot[wb][lane] = slot;
+      ipatch[wb][lane] = patch;
+      imax[wb][lane] = min(code_level(it.code) + kDfsDepth, kMaxLevel);
+      ichi[wb][lane] = 0;
+      ifl[wb][lane] = 0;
+      inodes[wb][lane] = 0;
+      fr[wb][0][lane] = it.code;
+      fi[wb][0][lane] = (uint8_t)lane;
+    }
     __syncwarp();
+    int cur = 0, ncur = nb;
     while (ncur > 0) {
       int nnext = 0;
       for (int base = 0; base < ncur; base += 32) {
         const int k = base + lane;
-        int o = NODE_EXCLUDED;
+        int o = NODE_EXCLUDED, item = 0;
         uint64_t code = 0;
         if (k < ncur) {
-          code = fr[wib][cur][k];
+          code = fr[wb][cur][k];
+          item = fi[wb][cur][k];
+          NodeCtx c;
+          c.P48 = w.proj + 48 * (int64_t)ipatch[wb][item];
+          c.qa = iq[wb][item][0];
+          c.qb = iq[wb][item][1];
+          c.qc = iq[wb][item][2];
+          c.eps_box = iq[wb][item][3];
           RootResult r;
           bool owned = false;
-          o = node_test(ctx, code, max_level, w.prm, r, owned);
+          o = node_test(c, code, imax[wb][item], w.prm, r, owned);
+          ++nodes;
+          if (atomicAdd(&inodes[wb][item], 1) >= kDfsBudget) {
+            o = NODE_AMBIGUOUS;  // budget: give up on this direction
+          }
           if (o == NODE_AMBIGUOUS) {
-            fl |= FLAG_RESHOOT;
+            atomicOr(&ifl[wb][item], FLAG_RESHOOT);
           } else if (o == NODE_ROOT) {
             iters += r.iters;
             if (r.status == ROOT_ACCEPTED && owned) {
               ++roots;
-              chi += r.sign;
-              if (r.tang || r.graze) fl |= FLAG_RESHOOT;
-              if (r.onsurf) fl |= FLAG_ONSURF;
+              atomicAdd(&ichi[wb][item], r.sign);
+              int f = 0;
+              if (r.tang || r.graze) f |= FLAG_RESHOOT;
+              if (r.onsurf) f |= FLAG_ONSURF;
+              if (f) atomicOr(&ifl[wb][item], f);
             }
           }
         }
@@ -204,44 +237,34 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
         const unsigned mask = __ballot_sync(0xffffffffu, sp);
         if (sp) {
           const int pos = nnext + 2 * __popc(mask & ((1u << lane) - 1));
-          uint64_t c0, c1;
-          child_codes(code, c0, c1);
           if (pos + 1 < kFrontier) {
-            fr[wib][cur ^ 1][pos] = c0;
-            fr[wib][cur ^ 1][pos + 1] = c1;
+            uint64_t c0, c1;
+            child_codes(code, c0, c1);
+            fr[wb][cur ^ 1][pos] = c0;
+            fr[wb][cur ^ 1][pos + 1] = c1;
+            fi[wb][cur ^ 1][pos] = (uint8_t)item;
+            fi[wb][cur ^ 1][pos + 1] = (uint8_t)item;
           } else {
-            fl |= FLAG_RESHOOT;  // frontier overflow: give up on this direction
+            atomicOr(&ifl[wb][item], FLAG_RESHOOT);  // frontier overflow
           }
         }
         nnext = min(nnext + 2 * __popc(mask), kFrontier);
-        item_nodes += min(32, ncur - base);
       }
       __syncwarp();
       cur ^= 1;
       ncur = nnext;
-      if (item_nodes > kDfsBudget) {
-        fl |= FLAG_RESHOOT;
-        break;
-      }
     }
-    nodes += lane == 0 ? item_nodes : 0;
-    maxn = max(maxn, (unsigned long long)item_nodes);
-    // reduce the item's lanes (all lanes hold the same slot)
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      chi += __shfl_down_sync(0xffffffffu, chi, off);
-      fl |= __shfl_down_sync(0xffffffffu, fl, off);
-    }
-    if (lane == 0) {
-      if (chi) atomicAdd(&w.chi[slot], chi);
-      if (fl) atomicOr(&w.flags[slot], fl);
+    __syncwarp();
+    if (lane < nb) {
+      const int32_t slot = islot[wb][lane];
+      if (ichi[wb][lane]) atomicAdd(&w.chi[slot], ichi[wb][lane]);
+      if (ifl[wb][lane]) atomicOr(&w.flags[slot], ifl[wb][lane]);
     }
     __syncwarp();
   }
   warp_sum_u64(&w.counters[CNT_NODES], nodes);
   warp_sum_u64(&w.counters[CNT_NEWTON], iters);
   warp_sum_u64(&w.counters[CNT_ROOTS], roots);
-  if (lane == 0 && maxn) atomicMax(&w.counters[CNT_MAXNODES], maxn);
 }
 
 // Newton pass over the certified leaves + ownership + K5 part 1.
@@ -297,9 +320,9 @@ __global__ void __launch_bounds__(128) k3_newton(WaveArgs w) {
   warp_sum_u64(&w.counters[CNT_ROOTS], roots);
 }
 
-static int grid_for(const void* fn, int sm_count) {
+static int grid_for(const void* fn, int sm_count, int block = 128) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 128, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, 0);
   if (per_sm < 1) per_sm = 1;
   return sm_count * per_sm;
 }
@@ -316,7 +339,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
   static thread_local int g_cand = 0, g_fb = 0, g_newton = 0, g_dev = -1;
   if (g_dev != sc->device) {
     g_cand = grid_for((const void*)k3_candidates, sc->sm_count);
-    g_fb = grid_for((const void*)k3_fallback, sc->sm_count);
+    g_fb = grid_for((const void*)k3_fallback, sc->sm_count, 32 * kFbWarps);
     g_newton = grid_for((const void*)k3_newton, sc->sm_count);
     g_dev = sc->device;
   }
@@ -356,7 +379,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
     if ((e = cudaStreamWaitEvent(side, fork_ev, 0)) != cudaSuccess) return e;
   }
   if (ev4) cudaEventRecord(ev4[1], fs);
-  k3_fallback<<<g_fb, 128, 0, fs>>>(fq, cnt, w);
+  k3_fallback<<<g_fb, 32 * kFbWarps, 0, fs>>>(fq, cnt, w);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev4) cudaEventRecord(ev4[2], fs);
   if (!ev4) {
