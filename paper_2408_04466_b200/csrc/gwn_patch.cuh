@@ -249,7 +249,7 @@ __device__ __forceinline__ void extract_net(double* x, double u0, double u1, dou
 // leaf box D expanded by kLeafM on every side (D'), so that every root in D
 // certifies from the leaf itself when R0, R1 < kLeafRmax.
 constexpr double kLeafM = 0.5;
-constexpr double kLeafRmax = 0.12;
+constexpr double kLeafRmax = 0.24;
 constexpr int kLeafMaxLevel = 12;
 
 struct alignas(16) LeafRec {
