@@ -187,3 +187,64 @@ def test_k4_rsqrt_full_precision():
     u = C.c_uint64()
     _lib.check(_lib.lib().gwn_selftest_rsqrt(0, 1 << 20, C.byref(u)), "gwn_selftest_rsqrt")
     assert u.value <= 2, u.value
+
+
+# ---------------------------------------------------------------------------
+# edge cases the reference's degeneracy rules cover (errors.py)
+# ---------------------------------------------------------------------------
+
+def _edge_compare(ctrl, queries, tol=1e-9, min_ok=0.99, **kw):
+    sc = G.Scene(ctrl, **kw)
+    w, st = G.winding_numbers(sc, queries)
+    prm = O.params(samples_per_edge=kw.get("samples_per_edge", 200))
+    wo, so, _, _ = O.scene_eval(ctrl, queries, prm=prm)
+    both = (st == 0) & (so == 0)
+    assert both.mean() >= min_ok, (np.unique(st, return_counts=True),
+                                   np.unique(so, return_counts=True))
+    assert np.abs(w - wo)[both].max() <= tol
+    return w, st
+
+
+def test_collapsed_edge_patch():
+    # triangle-like bicubic: the v=0 edge collapses to a point (singular Jacobian)
+    rng = np.random.default_rng(11)
+    ctrl = np.array([[(i / 3, j / 3, 0.3 * np.sin(i + 2 * j)) for j in range(4)]
+                     for i in range(4)])
+    ctrl[:, 0] = ctrl[0, 0]
+    q = rng.uniform(-0.5, 1.5, (2000, 3))
+    _edge_compare(ctrl[None], q)
+
+
+def test_flat_patch_and_far_translation():
+    rng = np.random.default_rng(12)
+    flat = np.array([[(i / 3, j / 3, 0.0) for j in range(4)] for i in range(4)])[None]
+    q = rng.uniform(-0.5, 1.5, (2000, 3))
+    w, _ = _edge_compare(flat, q)
+    # exact solid-angle check against the unit square formula away from it
+    s1 = scenes.make(1, 2000)
+    t = np.array([1234.5, -987.25, 512.0])
+    _edge_compare(s1.ctrl + t, s1.queries + t, tol=1e-8)
+
+
+def test_single_query_and_outside_box():
+    s = scenes.make(2, 8)
+    sc = G.Scene(s.ctrl)
+    w, st = G.winding_numbers(sc, np.array([[0.01, 0.02, 0.03]]))
+    assert st[0] == 0 and w[0] == 1.0
+    far = np.array([[50.0, 0.1, 0.2], [-30.0, 40.0, 10.0], [0.0, 0.0, 99.0]])
+    w, st = G.winding_numbers(sc, far)
+    assert np.all(st == 0) and np.all(w == 0.0)
+
+
+def test_odd_batch_sizes_equal_full_batch():
+    s, sc = _scene(1)
+    w, st = G.winding_numbers(sc, s.queries)
+    for a, b in ((0, 1), (1, 33), (33, 161), (161, 4096)):
+        wp, sp = G.winding_numbers(sc, s.queries[a:b], index_base=a)
+        assert np.array_equal(wp, w[a:b]) and np.array_equal(sp, st[a:b])
+
+
+def test_samples_per_edge_parity():
+    s = scenes.make(1, 1000)
+    for S in (2, 50, 1900):
+        _edge_compare(s.ctrl, s.queries, samples_per_edge=S)
