@@ -144,22 +144,31 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
     flags[j] = 0;
     va[j] = VtxF{0.0, 0.0, -1.0, 1.0};
   }
-  int minhi[QPT];
+  int minhi[QPT], neg[QPT];
 #pragma unroll
-  for (int j = 0; j < QPT; ++j) minhi[j] = 0x7fffffff;
-  // one segment (A -> B) of query j
-  auto seg = [&](int j, const VtxF& A, const VtxF& B, int64_t e) {
+  for (int j = 0; j < QPT; ++j) {
+    minhi[j] = 0x7fffffff;
+    neg[j] = 0;
+  }
+  // hot path of one segment (A -> B): only the complex product; the sign of
+  // den is OR-ed into neg so the rare band test runs after the tile
+  auto seg = [&](int j, const VtxF& A, const VtxF& B) {
     const double num = A.uy * B.ux - A.ux * B.uy;   // c.(a^ x b^)
     const double den = A.ux * B.ux + A.uy * B.uy + A.uz * B.uz;
-    if (__double2hiint(den) < 0 && band_h) {
-      if (band_hit_f(A, B, num, __ldg(band_h + e), prm.band_factor)) flags[j] |= FLAG_BAND;
-    }
+    neg[j] |= __double2hiint(den);
     cmul_track(st[j], den, num);
   };
+  __shared__ double prev_x[3];  // vertex carried into the current tile
   VtxF vb[QPT];
   int nseg = 0;
   for (int64_t t0 = vbeg; t0 < vend; t0 += kTileV) {
     const int nt = (int)min((int64_t)kTileV, vend - t0);
+    __syncthreads();
+    if (threadIdx.x == 0 && t0 > vbeg) {
+      prev_x[0] = sx[kTileV - 1];
+      prev_x[1] = sy[kTileV - 1];
+      prev_x[2] = sz[kTileV - 1];
+    }
     __syncthreads();
     for (int k = threadIdx.x; k < nt; k += blockDim.x) {
       const int64_t g = t0 + k;
@@ -168,8 +177,9 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
       sz[k] = vproj[2 * V + g];
     }
     __syncthreads();
-    int64_t e = t0 / S;               // edge of the tile's first vertex
-    int kin = (int)(t0 - e * S);      // its index within that edge
+    const int64_t e_t0 = t0 / S;                // edge of the tile's first vertex
+    const int kin_t0 = (int)(t0 - e_t0 * S);    // its index within that edge
+    int kin = kin_t0;
     // unrolled by two vertices with the carried vertex alternating between
     // va and vb, so no per-vertex register copies
     int k = 0;
@@ -179,32 +189,26 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
 #pragma unroll
         for (int j = 0; j < QPT; ++j) {
           vb[j] = make_vtxf(X, Y, Zc, qa[j], qb[j], qc[j], minhi[j]);
-          if (kin != 0) seg(j, va[j], vb[j], e);
+          if (kin != 0) seg(j, va[j], vb[j]);
         }
         if (kin != 0 && (++nseg & 7) == 0) {
 #pragma unroll
           for (int j = 0; j < QPT; ++j) renorm(st[j]);
         }
-        if (++kin == S) {
-          kin = 0;
-          ++e;
-        }
+        if (++kin == S) kin = 0;
       }
       {
         const double X = sx[k + 1], Y = sy[k + 1], Zc = sz[k + 1];
 #pragma unroll
         for (int j = 0; j < QPT; ++j) {
           va[j] = make_vtxf(X, Y, Zc, qa[j], qb[j], qc[j], minhi[j]);
-          if (kin != 0) seg(j, vb[j], va[j], e);
+          if (kin != 0) seg(j, vb[j], va[j]);
         }
         if (kin != 0 && (++nseg & 7) == 0) {
 #pragma unroll
           for (int j = 0; j < QPT; ++j) renorm(st[j]);
         }
-        if (++kin == S) {
-          kin = 0;
-          ++e;
-        }
+        if (++kin == S) kin = 0;
       }
     }
     if (k < nt) {  // odd tile length
@@ -212,16 +216,44 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
 #pragma unroll
       for (int j = 0; j < QPT; ++j) {
         vb[j] = make_vtxf(X, Y, Zc, qa[j], qb[j], qc[j], minhi[j]);
-        if (kin != 0) seg(j, va[j], vb[j], e);
+        if (kin != 0) seg(j, va[j], vb[j]);
         va[j] = vb[j];
       }
       if (kin != 0 && (++nseg & 7) == 0) {
 #pragma unroll
         for (int j = 0; j < QPT; ++j) renorm(st[j]);
       }
-      if (++kin == S) {
-        kin = 0;
-        ++e;
+      if (++kin == S) kin = 0;
+    }
+    // rare: some segment of this tile had den < 0 -> polyline/curve band test
+    // for the queries concerned, re-walking the tile
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) any |= neg[j] < 0;
+    if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+      for (int j = 0; j < QPT; ++j) {
+        if (neg[j] >= 0) continue;
+        int mh = 0x7fffffff;
+        int kk = kin_t0;
+        int64_t e = e_t0;
+        VtxF A = VtxF{0.0, 0.0, -1.0, 1.0};
+        if (kk != 0) A = make_vtxf(prev_x[0], prev_x[1], prev_x[2], qa[j], qb[j], qc[j], mh);
+        for (int i = 0; i < nt; ++i) {
+          const VtxF B = make_vtxf(sx[i], sy[i], sz[i], qa[j], qb[j], qc[j], mh);
+          if (kk != 0) {
+            const double num = A.uy * B.ux - A.ux * B.uy;
+            const double den = A.ux * B.ux + A.uy * B.uy + A.uz * B.uz;
+            if (den < 0.0 && band_hit_f(A, B, num, __ldg(band_h + e), prm.band_factor))
+              flags[j] |= FLAG_BAND;
+          }
+          A = B;
+          if (++kk == S) {
+            kk = 0;
+            ++e;
+          }
+        }
+        neg[j] = 0;
       }
     }
   }
