@@ -113,7 +113,7 @@ __device__ __forceinline__ bool band_hit_f(const VtxF& a, const VtxF& b, double 
 }
 
 template <int QPT>
-__global__ void __launch_bounds__(kBlockQ, 3)
+__global__ void __launch_bounds__(kBlockQ, 2)
 k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
            const double* __restrict__ vproj, int64_t V, int S, int64_t n_edges,
            const double* __restrict__ band_h, Frame f, DevParams prm,
