@@ -13,6 +13,9 @@
  *                      jitter/re-shoot policy of SPEC.md:320,373-375,427
  *   gwn_all_hits       patch.all_hits(ray) (surfaces.py:587-589 protocol,
  *                      body _multistart_ray_roots surfaces.py:634-701)
+ *   gwn_eval_rays      SPEC.md:381-407 winding_numbers_along_ray / slice /
+ *                      voxelize: one intersection pass per ray, reused by
+ *                      every point on it (ray reuse)
  *   gwn_single_loop_batch
  *                      _kernels.single_loop_batch (_kernels.py:801-823): the
  *                      kernel dispatch layer's ray-reuse boundary kernel
@@ -120,6 +123,20 @@ int gwn_eval(gwn_scene* scene, const double* queries, int64_t n, int64_t index_b
 /* Stats of the last gwn_eval on this scene; `timed` != 0 on the next eval
  * records per-kernel CUDA-event times (adds event syncs). */
 int gwn_stats_get(const gwn_scene* scene, gwn_stats* out);
+
+/* Ray reuse (SPEC.md:381-407 winding_numbers_along_ray / slice / voxelize;
+ * PAPER.md:305-307): R parallel rays o_r + t d, sharing `direction`; ray r
+ * carries the sorted parameters ts[offs[r] .. offs[r+1]) (offs has R+1
+ * entries, offs[0] = 0).  One intersection pass per RAY; each point takes
+ * chi from the cached hits beyond it plus its own boundary term.  Points on
+ * rays with a tangent / grazing hit, clashing with a hit, degenerate or in
+ * the band are re-evaluated by the per-point engine (same status codes as
+ * gwn_eval; jitter keyed by the point's global index).  *rays_cast (may be
+ * NULL) receives the number of intersection rays cast (= R). */
+int gwn_eval_rays(gwn_scene* scene, const double* origins, int64_t R,
+                  const double direction[3], const double* ts, const int64_t* offs,
+                  double* w_out, int8_t* status_out, int32_t flags, void* stream,
+                  int64_t* rays_cast);
 int gwn_set_timing(gwn_scene* scene, int32_t timed);
 
 /* All hits of one ray with one patch of the scene (host buffers). Records:

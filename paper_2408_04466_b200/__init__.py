@@ -7,7 +7,8 @@ patch protocol, running on hand-written sm_100a kernels in libgwn_b200.so.
 
 from .config import DEFAULT_EPS, EpsilonConfig
 from .engine import (Scene, combine, direction, fp64_peak, net_boundary, winding_number,
-                     winding_numbers, winding_numbers_along_ray)
+                     winding_numbers, winding_numbers_along_ray, winding_numbers_rays,
+                     slice, voxelize)
 from .errors import GwnError
 from .geometry import Aabb, Ray
 from .surfaces import BicubicPatch, BoundaryLoop, IntersectionRecord, patch_boundary
@@ -15,6 +16,7 @@ from .surfaces import BicubicPatch, BoundaryLoop, IntersectionRecord, patch_boun
 __all__ = [
     "DEFAULT_EPS", "EpsilonConfig", "Scene", "combine", "direction", "fp64_peak",
     "net_boundary", "winding_number", "winding_numbers", "winding_numbers_along_ray",
+    "winding_numbers_rays", "slice", "voxelize",
     "GwnError", "Aabb", "Ray", "BicubicPatch", "BoundaryLoop", "IntersectionRecord",
     "patch_boundary",
 ]

@@ -29,7 +29,7 @@ EXPORTS = (
     "gwn_abi_version", "gwn_last_error", "gwn_params_default", "gwn_scene_create",
     "gwn_scene_destroy", "gwn_scene_info_get", "gwn_eval", "gwn_stats_get", "gwn_set_timing",
     "gwn_all_hits", "gwn_single_loop_batch", "gwn_direction", "gwn_jitter_dir",
-    "gwn_net_boundary", "gwn_fp64_peak", "gwn_selftest_rsqrt",
+    "gwn_net_boundary", "gwn_fp64_peak", "gwn_selftest_rsqrt", "gwn_eval_rays",
 )
 
 
@@ -95,6 +95,8 @@ def lib() -> C.CDLL:
         L.gwn_scene_destroy.argtypes = [vp]
         L.gwn_scene_info_get.argtypes = [vp, C.POINTER(SceneInfo)]
         L.gwn_eval.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, vp, C.c_int32, vp]
+        L.gwn_eval_rays.argtypes = [vp, vp, C.c_int64, dp, vp, vp, vp, vp, C.c_int32, vp,
+                                    C.POINTER(C.c_int64)]
         L.gwn_stats_get.argtypes = [vp, C.POINTER(Stats)]
         L.gwn_set_timing.argtypes = [vp, C.c_int32]
         L.gwn_all_hits.argtypes = [vp, C.c_int64, dp, dp, dp, dp, C.POINTER(C.c_int32),

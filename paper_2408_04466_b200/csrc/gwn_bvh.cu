@@ -438,15 +438,12 @@ void free_round(Round& rd) {
   rd = Round();
 }
 
-// Caller holds sc->mu.  Builds rounds[0..r] that are missing.
-cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st) {
+// Build the per-direction structures (projection, leaves, cull grid/LBVH,
+// boundary vertices in the ray frame) for unit direction d.
+cudaError_t build_round_dir(gwn_scene* sc, const double d[3], Round& rd, cudaStream_t st) {
   cudaError_t e = cudaSuccess;
-  while ((int)sc->rounds.size() <= r) {
-    int rr = (int)sc->rounds.size();
-    Round rd;
-    double d[3];
-    gwn_direction(sc->prm.dir_seed, rr, d);
-    make_frame(d, &rd.f);
+  make_frame(d, &rd.f);
+  {
     const int64_t P = sc->P;
     if (P > 0) {
       // projected scene bounds from the 8 corners of the scene box
@@ -562,9 +559,21 @@ cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st) {
       free_round(rd);
       return e;
     }
-    sc->rounds.push_back(rd);
   }
   return e;
+}
+
+// Caller holds sc->mu.  Builds rounds[0..r] that are missing.
+cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st) {
+  while ((int)sc->rounds.size() <= r) {
+    double d[3];
+    gwn_direction(sc->prm.dir_seed, (int32_t)sc->rounds.size(), d);
+    Round rd;
+    cudaError_t e = build_round_dir(sc, d, rd, st);
+    if (e != cudaSuccess) return e;
+    sc->rounds.push_back(rd);
+  }
+  return cudaSuccess;
 }
 
 }  // namespace gwn

@@ -25,7 +25,8 @@ namespace gwn {
 __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
                            const int32_t* __restrict__ chi, const int32_t* __restrict__ flags,
                            const double* __restrict__ bpart, int nchunk, int round, int max_rounds,
-                           int max_jitters, uint64_t seed, int64_t index_base, double jscale,
+                           int max_jitters, uint64_t seed, int64_t index_base,
+                           const int64_t* __restrict__ qidx, double jscale,
                            const double* __restrict__ q0, double* __restrict__ pos,
                            int8_t* __restrict__ jit, int8_t* __restrict__ jreason,
                            double* __restrict__ w_out, int8_t* __restrict__ st_out,
@@ -56,7 +57,7 @@ __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
         jreason[q] = (int8_t)reason;
         // deterministic jitter (same hash as gwn_jitter_dir / the oracle)
         uint64_t st = seed ^ 0x5851F42D4C957F2Dull;
-        st ^= (uint64_t)(index_base + q) * 0x9E3779B97F4A7C15ull;
+        st ^= (uint64_t)(qidx ? qidx[q] : index_base + q) * 0x9E3779B97F4A7C15ull;
         st ^= (uint64_t)(j + 1) * 0xC2B2AE3D27D4EB4Full;
         double v[3];
         for (int k = 0; k < 3; ++k) {
@@ -158,8 +159,9 @@ static cudaError_t ensure_round(gwn_scene* sc, int r, cudaStream_t st) {
   return build_round(sc, r, st);
 }
 
-extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t index_base,
-                        double* w_out, int8_t* status_out, int32_t flags, void* stream) {
+static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t index_base,
+                     const int64_t* qidx, double* w_out, int8_t* status_out, int32_t flags,
+                     void* stream) {
   int rc = GWN_OK;
   if (!sc || n < 0 || (n > 0 && (!queries || !w_out || !status_out))) {
     set_error("gwn_eval: invalid arguments");
@@ -280,7 +282,8 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
         cudaEvent_t join = nullptr;
         if (sc->P > 0) {
           CKE(launch_intersect(sc, rd, pair_slot, pair_leaf, rsc, pair_cap, qproj, chi, fl, d_cnt,
-                               k3_scratch, sc->timed ? ev4 : nullptr, rsc + 2, &join, st));
+                               k3_scratch, sc->timed ? ev4 : nullptr, rsc + 2, &join, nullptr,
+                               st));
           launches += 3;
         }
         tr.mark("k3 launched");
@@ -295,7 +298,8 @@ extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t
         int32_t* nxt = act[cur];
         k_finalize<<<(m + 127) / 128, 128, 0, st>>>(
             m, active, chi, fl, bterm, nchunk, r, sc->prm.max_rounds, sc->prm.max_jitters,
-            sc->prm.dir_seed, index_base + c0, sc->prm.jitter_scale * sc->diag, q0, pos, jit,
+            sc->prm.dir_seed, index_base + c0, qidx ? qidx + c0 : nullptr,
+            sc->prm.jitter_scale * sc->diag, q0, pos, jit,
             jreason, d_w + c0, d_st + c0, nxt, (int32_t*)(rsc + 1), rsc,
             (unsigned long long)pair_cap);
         CKE(cudaGetLastError());
@@ -373,6 +377,21 @@ done:
   tr.mark("done");
   return rc;
 }
+
+extern "C" int gwn_eval(gwn_scene* sc, const double* queries, int64_t n, int64_t index_base,
+                        double* w_out, int8_t* status_out, int32_t flags, void* stream) {
+  return eval_core(sc, queries, n, index_base, nullptr, w_out, status_out, flags, stream);
+}
+
+namespace gwn {
+int eval_impl(gwn_scene* sc, const double* d_q, int64_t n, int64_t index_base,
+              const int64_t* qidx, double* d_w, int8_t* d_st, cudaStream_t st,
+              gwn_stats& stats) {
+  const int rc = eval_core(sc, d_q, n, index_base, qidx, d_w, d_st, 0, st);
+  stats = sc->stats;
+  return rc;
+}
+}  // namespace gwn
 
 extern "C" int gwn_all_hits(gwn_scene* sc, int64_t patch, const double origin[3],
                             const double direction[3], double* t_out, double* uv_out,

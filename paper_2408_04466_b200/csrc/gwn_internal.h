@@ -12,7 +12,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <array>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "../../include/gwn_b200.h"
@@ -41,6 +43,19 @@ enum : int {
 
 struct Frame {
   double e1[3], e2[3], d[3];
+};
+
+// one ray-patch root in record mode (ray reuse): slot, sign, t
+struct HitRec {
+  int32_t slot;
+  int32_t sign;
+  double t;
+};
+
+struct RecordSink {
+  HitRec* rec;
+  unsigned long long* count;
+  unsigned long long cap;
 };
 
 struct DevParams {
@@ -97,6 +112,8 @@ struct gwn_scene {
   std::vector<gwn::Round> rounds;
   // candidate (query, leaf) pairs per query seen so far (buffer sizing)
   double pairs_per_query = 4.0;
+  // rounds for explicit ray directions (ray reuse), keyed by direction
+  std::vector<std::pair<std::array<double, 3>, gwn::Round>> dir_rounds;
   // last-eval stats
   gwn_stats stats;
   int timed = 0;
@@ -106,6 +123,7 @@ namespace gwn {
 
 // launchers (stream-ordered); defined in the .cu files
 cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st);            // gwn_bvh.cu
+cudaError_t build_round_dir(gwn_scene* sc, const double d[3], Round& rd, cudaStream_t st);
 void free_round(Round& rd);
 cudaError_t launch_cull(const gwn_scene* sc, const Round& rd, int32_t m, const int32_t* active,
                         const double* pos, double* qproj, int32_t* pair_slot, int32_t* pair_leaf,
@@ -116,7 +134,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
                              int64_t pair_cap, const double* qproj, int32_t* chi,
                              int32_t* flags, unsigned long long* counters, void* scratch,
                              cudaEvent_t* ev4, unsigned long long* items_out, cudaEvent_t* join,
-                             cudaStream_t st);                                // gwn_wavefront.cu
+                             const RecordSink* rec, cudaStream_t st);         // gwn_wavefront.cu
 size_t intersect_scratch_bytes(int64_t pair_cap);
 cudaError_t launch_query_order(const Round& rd, int32_t m, const double* pos, void* scratch,
                                int32_t* perm, cudaStream_t st);               // gwn_bvh.cu
@@ -135,6 +153,11 @@ cudaError_t launch_single_loop(const double* loop, int64_t B, const double* o, c
                                const double* hit_ts, const int64_t* hit_signs, int64_t H,
                                const double* qts, int64_t K, double t_eps, double deg, double* w,
                                int8_t* ok, cudaStream_t st);
+
+// the engine body shared by gwn_eval and the ray-reuse fallback (gwn_engine.cu):
+// device buffers; qidx (nullable, device) gives the global id of each query
+int eval_impl(gwn_scene* sc, const double* d_q, int64_t n, int64_t index_base,
+              const int64_t* qidx, double* d_w, int8_t* d_st, cudaStream_t st, gwn_stats& stats);
 
 // host helpers (gwn_scene.cu)
 void make_frame(const double d[3], Frame* f);

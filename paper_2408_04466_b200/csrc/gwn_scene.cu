@@ -346,6 +346,7 @@ extern "C" int gwn_scene_destroy(gwn_scene* sc) {
   if (!sc) return GWN_OK;
   cudaSetDevice(sc->device);
   for (auto& r : sc->rounds) free_round(r);
+  for (auto& r : sc->dir_rounds) free_round(r.second);
   if (sc->ctrl) cudaFree(sc->ctrl);
   if (sc->verts) cudaFree(sc->verts);
   if (sc->band_h) cudaFree(sc->band_h);

@@ -72,7 +72,9 @@ struct WaveArgs {
   DevParams prm;
   int32_t* chi;
   int32_t* flags;
-  int32_t* pair_nodes;  // unused (DFS fallback has its own per-pair budget)
+  HitRec* rec;          // record mode (ray reuse): every owned root, else nullptr
+  unsigned long long* rec_count;
+  unsigned long long rec_cap;
   unsigned long long* counters;
   int* overflow;
   NewtonItem* nq;
@@ -228,6 +230,11 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
               int f = 0;
               if (r.tang || r.graze) f |= FLAG_RESHOOT;
               if (r.onsurf) f |= FLAG_ONSURF;
+              if (w.rec) {
+                const unsigned long long kk = atomicAdd(w.rec_count, 1ull);
+                if (kk < w.rec_cap) w.rec[kk] = HitRec{islot[wb][item], r.sign, r.t};
+                else f |= FLAG_RESHOOT;
+              }
               if (f) atomicOr(&ifl[wb][item], f);
             }
           }
@@ -306,6 +313,11 @@ __global__ void __launch_bounds__(128) k3_newton(WaveArgs w) {
           chi = r.sign;
           if (r.tang || r.graze) fl |= FLAG_RESHOOT;
           if (r.onsurf) fl |= FLAG_ONSURF;
+          if (w.rec) {
+            const unsigned long long k = atomicAdd(w.rec_count, 1ull);
+            if (k < w.rec_cap) w.rec[k] = HitRec{slot, r.sign, r.t};
+            else atomicOr(&w.flags[slot], FLAG_RESHOOT);
+          }
         }
       }
     }
@@ -335,7 +347,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
                              int64_t pair_cap, const double* qproj, int32_t* chi,
                              int32_t* flags, unsigned long long* counters, void* scratch,
                              cudaEvent_t* ev4, unsigned long long* items_out, cudaEvent_t* join,
-                             cudaStream_t st) {
+                             const RecordSink* rec, cudaStream_t st) {
   static thread_local int g_cand = 0, g_fb = 0, g_newton = 0, g_dev = -1;
   if (g_dev != sc->device) {
     g_cand = grid_for((const void*)k3_candidates, sc->sm_count);
@@ -355,7 +367,8 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
   unsigned long long* cnt = (unsigned long long*)p;  // [0] fallback, [1] newton, [2] ovf
   cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 4, st);
   if (e != cudaSuccess) return e;
-  WaveArgs w{pair_slot, pp, qproj, rd.proj, sc->dprm, chi, flags, nullptr,
+  WaveArgs w{pair_slot, pp, qproj, rd.proj, sc->dprm, chi, flags,
+             rec ? rec->rec : nullptr, rec ? rec->count : nullptr, rec ? rec->cap : 0ull,
              counters, (int*)(cnt + 2), nq, cnt + 1, (unsigned long long)pair_cap};
   if (ev4) cudaEventRecord(ev4[0], st);
   k3_candidates<<<g_cand, 128, 0, st>>>(npairs_dev, pair_leaf, rd.leaves, fq, cnt,

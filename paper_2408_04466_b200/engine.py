@@ -188,16 +188,118 @@ def winding_number(scene: Scene, p) -> float:
     return float(w[0])
 
 
+def winding_numbers_rays(scene: Scene, origins, direction, ts, offs, *, stream=None,
+                         return_rays: bool = False):
+    """Ray reuse (``gwn_eval_rays``): points ``origins[r] + ts[k] * direction``
+    for k in ``[offs[r], offs[r+1])``, one intersection pass per ray r.
+
+    ``ts`` must be ascending within each ray.  Returns ``(w, status)`` over
+    the flattened points (plus the number of rays cast if ``return_rays``).
+    Host (numpy) buffers; the library does the copies.
+    """
+    o = np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(ts, dtype=np.float64).reshape(-1)
+    f = np.ascontiguousarray(offs, dtype=np.int64).reshape(-1)
+    R = o.shape[0]
+    if f.shape[0] != R + 1 or f[0] != 0 or f[-1] != t.shape[0] or np.any(np.diff(f) < 0):
+        raise ValueError("offs must have R+1 non-decreasing entries from 0 to len(ts)")
+    for r in range(R) if R <= 4096 else ():
+        if np.any(np.diff(t[f[r]:f[r + 1]]) < 0):
+            raise ValueError("ts must be sorted ascending on every ray")
+    if R > 4096:
+        seg = np.repeat(np.arange(R), np.diff(f))
+        bad = (np.diff(t) < 0) & (seg[1:] == seg[:-1])
+        if np.any(bad):
+            raise ValueError("ts must be sorted ascending on every ray")
+    d = np.ascontiguousarray(direction, dtype=np.float64).reshape(3)
+    n = t.shape[0]
+    w = np.empty(n, np.float64)
+    st = np.empty(n, np.int8)
+    cast = C.c_int64(0)
+    if R > 0:
+        _lib.check(_lib.lib().gwn_eval_rays(
+            scene.handle, C.c_void_p(o.ctypes.data), R, d.ctypes.data_as(C.POINTER(C.c_double)),
+            C.c_void_p(t.ctypes.data), C.c_void_p(f.ctypes.data), C.c_void_p(w.ctypes.data),
+            C.c_void_p(st.ctypes.data), _lib.GWN_HOST_BUFFERS, C.c_void_p(stream or 0),
+            C.byref(cast)), "gwn_eval_rays")
+    scene.rays_cast = int(cast.value)
+    return (w, st, int(cast.value)) if return_rays else (w, st)
+
+
 def winding_numbers_along_ray(scene: Scene, r: Ray, ts: Iterable[float]) -> list[float]:
-    """w at r.origin + t r.direction for sorted ts."""
+    """w at r.origin + t r.direction for sorted ts: one
+    intersection pass for the ray, chi of every point from the cached hits
+    beyond it (``gwn_eval_rays``)."""
     ts = np.asarray(list(ts), dtype=np.float64)
     if ts.size == 0:
         return []
     if np.any(np.diff(ts) < 0):
         raise ValueError("ts must be sorted ascending")
-    pts = r.origin[None, :] + ts[:, None] * r.direction[None, :]
-    w, _ = winding_numbers(scene, pts)
+    w, _ = winding_numbers_rays(scene, np.asarray(r.origin, np.float64)[None, :],
+                                np.asarray(r.direction, np.float64), ts,
+                                np.array([0, ts.size], np.int64))
     return [float(x) for x in w]
+
+
+def slice(scene: Scene, origin, u_axis, v_axis, width: int, height: int) -> np.ndarray:
+    """Winding numbers at the W x H pixel centres of the plane patch
+    ``origin + a u_axis + b v_axis``, a, b in [0,1].
+
+    Pixel (j, i) (row j along v, column i along u) is at
+    ``origin + (i+0.5)/W u_axis + (j+0.5)/H v_axis``.  The pixels are grouped
+    into min(W, H) collinear families along the longer axis, one ray each
+    (PAPER.md:305-307); ``scene.rays_cast`` records the count.  Returns an
+    (H, W) array.
+    """
+    W, H = int(width), int(height)
+    if W < 1 or H < 1:
+        raise ValueError("W, H must be >= 1")
+    o = np.asarray(origin, np.float64).reshape(3)
+    u = np.asarray(u_axis, np.float64).reshape(3)
+    v = np.asarray(v_axis, np.float64).reshape(3)
+    along_u = W >= H
+    a, b = (u, v) if along_u else (v, u)
+    na, nb = (W, H) if along_u else (H, W)
+    la = float(np.linalg.norm(a))
+    if not la > 0:
+        raise ValueError("degenerate slice axes")
+    d = a / la
+    fb = (np.arange(nb) + 0.5) / nb
+    origins = o[None, :] + fb[:, None] * b[None, :]
+    ts = np.tile((np.arange(na) + 0.5) / na * la, nb)
+    offs = np.arange(nb + 1, dtype=np.int64) * na
+    w, _ = winding_numbers_rays(scene, origins, d, ts, offs)
+    img = w.reshape(nb, na)
+    return img if along_u else img.T.copy()
+
+
+def voxelize(scene: Scene, n: int, box_min=None, box_max=None, threshold: float = 0.5):
+    """Winding numbers and occupancy at the n^3 voxel centres of
+    [box_min, box_max] (default: the scene AABB) with n^2 rays along +x
+    (occupied iff w >= threshold, PAPER §7).
+
+    Returns ``(occupancy bool (n,n,n), w (n,n,n))`` indexed [ix, iy, iz];
+    ``scene.rays_cast`` == n^2.
+    """
+    n = int(n)
+    if n < 1:
+        raise ValueError("N must be >= 1")
+    if box_min is None or box_max is None:
+        bb = scene.aabb()
+        box_min = bb.min_corner if box_min is None else box_min
+        box_max = bb.max_corner if box_max is None else box_max
+    lo = np.asarray(box_min, np.float64).reshape(3)
+    hi = np.asarray(box_max, np.float64).reshape(3)
+    c = (np.arange(n) + 0.5) / n
+    ys = lo[1] + c * (hi[1] - lo[1])
+    zs = lo[2] + c * (hi[2] - lo[2])
+    Y, Z = np.meshgrid(ys, zs, indexing="ij")  # ray (iy, iz)
+    origins = np.stack([np.full(n * n, lo[0]), Y.ravel(), Z.ravel()], axis=1)
+    ts = np.tile(c * (hi[0] - lo[0]), n * n)
+    offs = np.arange(n * n + 1, dtype=np.int64) * n
+    w, _ = winding_numbers_rays(scene, origins, np.array([1.0, 0.0, 0.0]), ts, offs)
+    w = w.reshape(n, n, n).transpose(2, 0, 1).copy()  # (iy, iz, ix) -> (ix, iy, iz)
+    return w >= threshold, w
 
 
 def combine(field_a, field_b, op: str):
