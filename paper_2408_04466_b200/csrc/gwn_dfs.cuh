@@ -65,10 +65,10 @@ __device__ __forceinline__ OwnBox own_box_of(uint64_t code, double tol) {
   const double u0 = (double)code_iu(code) * wu, v0 = (double)code_iv(code) * wv;
   const double u1 = u0 + wu, v1 = v0 + wv;
   OwnBox o;
-  o.lo_u = u0 == 0.0 ? -tol : u0;
-  o.hi_u = u1 == 1.0 ? 1.0 + tol : u1;
-  o.lo_v = v0 == 0.0 ? -tol : v0;
-  o.hi_v = v1 == 1.0 ? 1.0 + tol : v1;
+  o.lo_u = own_lo(u0, tol);
+  o.hi_u = own_hi(u1, tol);
+  o.lo_v = own_lo(v0, tol);
+  o.hi_v = own_hi(v1, tol);
   o.closed_u = u1 == 1.0;
   o.closed_v = v1 == 1.0;
   return o;

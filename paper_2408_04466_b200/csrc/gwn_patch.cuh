@@ -250,6 +250,20 @@ __device__ __forceinline__ void extract_net(double* x, double u0, double u1, dou
 // certifies from the leaf itself when R0, R1 < kLeafRmax.
 constexpr double kLeafM = 0.5;
 constexpr double kLeafRmax = 0.24;
+
+// Ownership cut of an interior split line x (a dyadic value, computed exactly
+// by both neighbouring boxes): x + kOwnShift.  Two leaves solve a root on
+// their shared split line independently, so their Newton results straddle x
+// by an ulp either way; shifting the cut off the dyadic lattice keeps roots
+// of structured inputs (voxel grids, slices: dyadic coordinates on a linear
+// patch) away from it, so exactly one neighbour owns every root.
+constexpr double kOwnShift = 3.14159265358979e-11;
+__device__ __forceinline__ double own_lo(double x, double tol) {
+  return x == 0.0 ? -tol : x + kOwnShift;
+}
+__device__ __forceinline__ double own_hi(double x, double tol) {
+  return x == 1.0 ? 1.0 + tol : x + kOwnShift;
+}
 constexpr int kLeafMaxLevel = 12;
 
 struct alignas(16) LeafRec {

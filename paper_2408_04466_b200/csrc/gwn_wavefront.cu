@@ -304,8 +304,8 @@ __global__ void __launch_bounds__(128) k3_newton(WaveArgs w) {
         fl |= FLAG_RESHOOT;  // certified root not reached: re-shoot
       } else if (r.status == ROOT_ACCEPTED) {
         // half-open ownership box (domain edges own the tolerance band)
-        const double lo_u = u0 == 0.0 ? -tol : u0, hi_u = u1 == 1.0 ? 1.0 + tol : u1;
-        const double lo_v = v0 == 0.0 ? -tol : v0, hi_v = v1 == 1.0 ? 1.0 + tol : v1;
+        const double lo_u = own_lo(u0, tol), hi_u = own_hi(u1, tol);
+        const double lo_v = own_lo(v0, tol), hi_v = own_hi(v1, tol);
         const bool own = r.u >= lo_u && (r.u < hi_u || (u1 == 1.0 && r.u <= hi_u)) &&
                          r.v >= lo_v && (r.v < hi_v || (v1 == 1.0 && r.v <= hi_v));
         if (own) {

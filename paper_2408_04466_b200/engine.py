@@ -189,41 +189,78 @@ def winding_number(scene: Scene, p) -> float:
 
 
 def winding_numbers_rays(scene: Scene, origins, direction, ts, offs, *, stream=None,
-                         return_rays: bool = False):
+                         return_rays: bool = False, check: bool = True):
     """Ray reuse (``gwn_eval_rays``): points ``origins[r] + ts[k] * direction``
     for k in ``[offs[r], offs[r+1])``, one intersection pass per ray r.
 
     ``ts`` must be ascending within each ray.  Returns ``(w, status)`` over
     the flattened points (plus the number of rays cast if ``return_rays``).
-    Host (numpy) buffers; the library does the copies.
+    numpy inputs are host buffers (the library does the copies); CUDA torch
+    tensors stay on the device and run on the current torch stream.
     """
-    o = np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)
-    t = np.ascontiguousarray(ts, dtype=np.float64).reshape(-1)
-    f = np.ascontiguousarray(offs, dtype=np.int64).reshape(-1)
-    R = o.shape[0]
-    if f.shape[0] != R + 1 or f[0] != 0 or f[-1] != t.shape[0] or np.any(np.diff(f) < 0):
-        raise ValueError("offs must have R+1 non-decreasing entries from 0 to len(ts)")
-    for r in range(R) if R <= 4096 else ():
-        if np.any(np.diff(t[f[r]:f[r + 1]]) < 0):
-            raise ValueError("ts must be sorted ascending on every ray")
-    if R > 4096:
-        seg = np.repeat(np.arange(R), np.diff(f))
-        bad = (np.diff(t) < 0) & (seg[1:] == seg[:-1])
-        if np.any(bad):
-            raise ValueError("ts must be sorted ascending on every ray")
+    L = _lib.lib()
     d = np.ascontiguousarray(direction, dtype=np.float64).reshape(3)
-    n = t.shape[0]
-    w = np.empty(n, np.float64)
-    st = np.empty(n, np.int8)
     cast = C.c_int64(0)
-    if R > 0:
-        _lib.check(_lib.lib().gwn_eval_rays(
-            scene.handle, C.c_void_p(o.ctypes.data), R, d.ctypes.data_as(C.POINTER(C.c_double)),
-            C.c_void_p(t.ctypes.data), C.c_void_p(f.ctypes.data), C.c_void_p(w.ctypes.data),
-            C.c_void_p(st.ctypes.data), _lib.GWN_HOST_BUFFERS, C.c_void_p(stream or 0),
-            C.byref(cast)), "gwn_eval_rays")
+    if _is_torch(ts):
+        import torch
+        o = origins.to(torch.float64).contiguous().reshape(-1, 3)
+        t = ts.to(torch.float64).contiguous().reshape(-1)
+        f = offs.to(torch.int64).contiguous().reshape(-1)
+        R = o.shape[0]
+        if f.shape[0] != R + 1:
+            raise ValueError("offs must have R+1 entries")
+        dev = t.is_cuda
+        if dev != o.is_cuda or dev != f.is_cuda:
+            raise ValueError("origins, ts and offs must be on the same device")
+        if check:
+            fc = f.cpu().numpy() if dev else f.numpy()
+            if fc[0] != 0 or fc[-1] != t.shape[0] or np.any(np.diff(fc) < 0):
+                raise ValueError("offs must be non-decreasing from 0 to len(ts)")
+            seg = torch.repeat_interleave(torch.arange(R, device=t.device), f.diff())
+            if bool(((t.diff() < 0) & (seg[1:] == seg[:-1])).any()):
+                raise ValueError("ts must be sorted ascending on every ray")
+        n = t.shape[0]
+        w = torch.empty(n, dtype=torch.float64, device=t.device)
+        st = torch.empty(n, dtype=torch.int8, device=t.device)
+        if stream is None and dev:
+            stream = torch.cuda.current_stream(t.device).cuda_stream
+        if R > 0:
+            _lib.check(L.gwn_eval_rays(
+                scene.handle, C.c_void_p(o.data_ptr()), R, d.ctypes.data_as(C.POINTER(C.c_double)),
+                C.c_void_p(t.data_ptr()), C.c_void_p(f.data_ptr()), C.c_void_p(w.data_ptr()),
+                C.c_void_p(st.data_ptr()), 0 if dev else _lib.GWN_HOST_BUFFERS,
+                C.c_void_p(stream or 0), C.byref(cast)), "gwn_eval_rays")
+    else:
+        o = np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)
+        t = np.ascontiguousarray(ts, dtype=np.float64).reshape(-1)
+        f = np.ascontiguousarray(offs, dtype=np.int64).reshape(-1)
+        R = o.shape[0]
+        if f.shape[0] != R + 1 or f[0] != 0 or f[-1] != t.shape[0] or np.any(np.diff(f) < 0):
+            raise ValueError("offs must have R+1 non-decreasing entries from 0 to len(ts)")
+        if check:
+            seg = np.repeat(np.arange(R), np.diff(f))
+            if np.any((np.diff(t) < 0) & (seg[1:] == seg[:-1])):
+                raise ValueError("ts must be sorted ascending on every ray")
+        n = t.shape[0]
+        w = np.empty(n, np.float64)
+        st = np.empty(n, np.int8)
+        if R > 0:
+            _lib.check(L.gwn_eval_rays(
+                scene.handle, C.c_void_p(o.ctypes.data), R,
+                d.ctypes.data_as(C.POINTER(C.c_double)), C.c_void_p(t.ctypes.data),
+                C.c_void_p(f.ctypes.data), C.c_void_p(w.ctypes.data), C.c_void_p(st.ctypes.data),
+                _lib.GWN_HOST_BUFFERS, C.c_void_p(stream or 0), C.byref(cast)), "gwn_eval_rays")
     scene.rays_cast = int(cast.value)
     return (w, st, int(cast.value)) if return_rays else (w, st)
+
+
+def _device_torch():
+    """torch if a CUDA device is usable (grid generation on the device), else None."""
+    try:
+        import torch
+        return torch if torch.cuda.is_available() else None
+    except Exception:  # pragma: no cover
+        return None
 
 
 def winding_numbers_along_ray(scene: Scene, r: Ray, ts: Iterable[float]) -> list[float]:
@@ -264,12 +301,22 @@ def slice(scene: Scene, origin, u_axis, v_axis, width: int, height: int) -> np.n
     if not la > 0:
         raise ValueError("degenerate slice axes")
     d = a / la
-    fb = (np.arange(nb) + 0.5) / nb
-    origins = o[None, :] + fb[:, None] * b[None, :]
-    ts = np.tile((np.arange(na) + 0.5) / na * la, nb)
-    offs = np.arange(nb + 1, dtype=np.int64) * na
-    w, _ = winding_numbers_rays(scene, origins, d, ts, offs)
-    img = w.reshape(nb, na)
+    T = _device_torch()
+    if T is not None:
+        dev = T.device("cuda", scene.device)
+        fb = (T.arange(nb, dtype=T.float64, device=dev) + 0.5) / nb
+        origins = T.from_numpy(o).to(dev)[None, :] + fb[:, None] * T.from_numpy(b).to(dev)[None, :]
+        ts = ((T.arange(na, dtype=T.float64, device=dev) + 0.5) / na * la).repeat(nb)
+        offs = T.arange(nb + 1, dtype=T.int64, device=dev) * na
+        w, _ = winding_numbers_rays(scene, origins, d, ts, offs, check=False)
+        img = w.reshape(nb, na).cpu().numpy()
+    else:
+        fb = (np.arange(nb) + 0.5) / nb
+        origins = o[None, :] + fb[:, None] * b[None, :]
+        ts = np.tile((np.arange(na) + 0.5) / na * la, nb)
+        offs = np.arange(nb + 1, dtype=np.int64) * na
+        w, _ = winding_numbers_rays(scene, origins, d, ts, offs, check=False)
+        img = w.reshape(nb, na)
     return img if along_u else img.T.copy()
 
 
@@ -290,15 +337,30 @@ def voxelize(scene: Scene, n: int, box_min=None, box_max=None, threshold: float 
         box_max = bb.max_corner if box_max is None else box_max
     lo = np.asarray(box_min, np.float64).reshape(3)
     hi = np.asarray(box_max, np.float64).reshape(3)
-    c = (np.arange(n) + 0.5) / n
-    ys = lo[1] + c * (hi[1] - lo[1])
-    zs = lo[2] + c * (hi[2] - lo[2])
-    Y, Z = np.meshgrid(ys, zs, indexing="ij")  # ray (iy, iz)
-    origins = np.stack([np.full(n * n, lo[0]), Y.ravel(), Z.ravel()], axis=1)
-    ts = np.tile(c * (hi[0] - lo[0]), n * n)
-    offs = np.arange(n * n + 1, dtype=np.int64) * n
-    w, _ = winding_numbers_rays(scene, origins, np.array([1.0, 0.0, 0.0]), ts, offs)
-    w = w.reshape(n, n, n).transpose(2, 0, 1).copy()  # (iy, iz, ix) -> (ix, iy, iz)
+    T = _device_torch()
+    if T is not None:  # grid generated and transposed on the device
+        dev = T.device("cuda", scene.device)
+        c = (T.arange(n, dtype=T.float64, device=dev) + 0.5) / n
+        ys = float(lo[1]) + c * float(hi[1] - lo[1])
+        zs = float(lo[2]) + c * float(hi[2] - lo[2])
+        Y, Z = T.meshgrid(ys, zs, indexing="ij")  # ray (iy, iz)
+        origins = T.stack([T.full_like(Y, float(lo[0])), Y, Z], dim=-1).reshape(-1, 3)
+        ts = (c * float(hi[0] - lo[0])).repeat(n * n)
+        offs = T.arange(n * n + 1, dtype=T.int64, device=dev) * n
+        w, _ = winding_numbers_rays(scene, origins, np.array([1.0, 0.0, 0.0]), ts, offs,
+                                    check=False)
+        w = w.reshape(n, n, n).permute(2, 0, 1).contiguous().cpu().numpy()
+    else:
+        c = (np.arange(n) + 0.5) / n
+        ys = lo[1] + c * (hi[1] - lo[1])
+        zs = lo[2] + c * (hi[2] - lo[2])
+        Y, Z = np.meshgrid(ys, zs, indexing="ij")
+        origins = np.stack([np.full(n * n, lo[0]), Y.ravel(), Z.ravel()], axis=1)
+        ts = np.tile(c * (hi[0] - lo[0]), n * n)
+        offs = np.arange(n * n + 1, dtype=np.int64) * n
+        w, _ = winding_numbers_rays(scene, origins, np.array([1.0, 0.0, 0.0]), ts, offs,
+                                    check=False)
+        w = w.reshape(n, n, n).transpose(2, 0, 1).copy()  # (iy, iz, ix) -> (ix, iy, iz)
     return w >= threshold, w
 
 

@@ -27,6 +27,31 @@ def main():
         pts = np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1)
         G.voxelize(sc, n)
         G.winding_numbers(sc, pts)
+        import torch
+        dev = torch.device("cuda")
+        cc = (torch.arange(n, dtype=torch.float64, device=dev) + 0.5) / n
+        Yd, Zd = torch.meshgrid(torch.as_tensor(ax[1], device=dev), torch.as_tensor(ax[2], device=dev),
+                                indexing="ij")
+        org = torch.stack([torch.full_like(Yd, bb.min_corner[0]), Yd, Zd], -1).reshape(-1, 3)
+        tsd = (cc * (bb.max_corner[0] - bb.min_corner[0])).repeat(n * n)
+        offd = torch.arange(n * n + 1, dtype=torch.int64, device=dev) * n
+        qd = torch.from_numpy(pts).to(dev)
+        for _ in range(2):
+            G.winding_numbers_rays(sc, org, [1.0, 0, 0], tsd, offd, check=False)
+            G.winding_numbers(sc, qd)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(3):
+            G.winding_numbers_rays(sc, org, [1.0, 0, 0], tsd, offd, check=False)
+        torch.cuda.synchronize()
+        trd = (time.perf_counter() - t) / 3
+        t = time.perf_counter()
+        for _ in range(3):
+            G.winding_numbers(sc, qd)
+        torch.cuda.synchronize()
+        tpd = (time.perf_counter() - t) / 3
+        print(f"  device-resident: rays {trd*1e3:.2f} ms ({n**3/trd/1e6:.1f} Mpts/s) vs per-point "
+              f"{tpd*1e3:.2f} ms ({n**3/tpd/1e6:.1f} Mpts/s) -> {tpd/trd:.2f}x", flush=True)
         reps = 3
         t = time.perf_counter()
         for _ in range(reps):
