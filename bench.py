@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--queries", type=int, default=0, help="override query count")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ray-reuse", action="store_true",
+                    help="skip the SURVEY §8(f1) ray-reuse side measurement")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -175,6 +177,48 @@ def run_reference(args, spec, rank, world):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def ray_reuse(G, torch, sc, dev, stream, n=256, k=5):
+    """voxel centres of the scene AABB at n^3 through
+    gwn_eval_rays (n^2 rays along +x) against gwn_eval of the same points,
+    both device-resident, CUDA events on `stream`."""
+    bb = sc.aabb()
+    lo, hi = bb.min_corner, bb.max_corner
+    c = (torch.arange(n, dtype=torch.float64, device=dev) + 0.5) / n
+    ax = [float(lo[i]) + c * float(hi[i] - lo[i]) for i in range(3)]
+    Y, Z = torch.meshgrid(ax[1], ax[2], indexing="ij")
+    org = torch.stack([torch.full_like(Y, float(lo[0])), Y, Z], -1).reshape(-1, 3)
+    ts = (c * float(hi[0] - lo[0])).repeat(n * n)
+    offs = torch.arange(n * n + 1, dtype=torch.int64, device=dev) * n
+    pts = org.repeat_interleave(n, 0)
+    pts[:, 0] += ts
+    w_pp = torch.empty(n ** 3, dtype=torch.float64, device=dev)
+    st_pp = torch.empty(n ** 3, dtype=torch.int8, device=dev)
+
+    def t_of(fn):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / k
+
+    res = {}
+    ms_r = t_of(lambda: res.update(r=G.winding_numbers_rays(
+        sc, org, [1.0, 0.0, 0.0], ts, offs, stream=stream.cuda_stream, check=False)))
+    ms_p = t_of(lambda: G.winding_numbers(sc, pts, out=(w_pp, st_pp), stream=stream.cuda_stream))
+    w_r, st_r = res["r"]
+    ok = (st_r == 0) & (st_pp == 0)
+    diff = float((w_r - w_pp).abs()[ok].max()) if bool(ok.any()) else 0.0
+    return {"workload": f"voxelize scene AABB at {n}^3 = {n ** 3} voxel centres, {n * n} rays "
+                        "along +x (SPEC.md:398-407)",
+            "value": n ** 3 / (ms_r * 1e-3), "unit": "points/s", "ms": ms_r,
+            "rays_cast": sc.rays_cast, "per_point_value": n ** 3 / (ms_p * 1e-3),
+            "per_point_ms": ms_p, "speedup": ms_p / ms_r, "max_abs_diff_vs_per_point": diff}
 
 
 def main():
@@ -325,6 +369,8 @@ def main():
                                              "boundary_segments", "retried", "rounds")},
             "clocks": clock_info,
         }
+        if world == 1 and not args.no_ray_reuse:
+            out["ray_reuse"] = ray_reuse(G, torch, sc, dev, stream)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(spec, args.cpu_seconds)
         print(json.dumps(out), flush=True)

@@ -12,6 +12,8 @@
 // thread per internal node, bottom-up refit with atomic arrival counters.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -41,25 +43,93 @@ __global__ void k_project(const double* __restrict__ ctrl, int64_t P, Frame f,
 // the leaf then certifies from the precomputed data alone), or kLeafMaxLevel.
 // kFill = false: count leaves per patch; true: write LeafRec, the leaf's
 // control-box (cull primitive) and its Morton key.
-template <bool kFill>
-__global__ void k_leaves(int64_t P, const double* __restrict__ proj,
-                         const int64_t* __restrict__ offs, int64_t* __restrict__ counts,
-                         LeafRec* __restrict__ leaves, double* __restrict__ leafbox,
-                         uint32_t* __restrict__ keys, int32_t* __restrict__ ids, double amin,
-                         double ainv, double bmin, double binv) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= P) return;
-  const double* P48 = proj + 48 * p;
+// leaf depth cap (GWN_LEAF_MAXLEVEL overrides, for experiments)
+static int leaf_max_level() {
+  static int v = [] {
+    const char* e = getenv("GWN_LEAF_MAXLEVEL");
+    int x = e ? atoi(e) : kLeafMaxLevel;
+    return x < 1 ? 1 : x > kLeafLevelCap ? kLeafLevelCap : x;
+  }();
+  return v;
+}
+
+// Conservative box expansion of patch P48 (rounding + the 1e-9 parametric
+// acceptance band of surfaces.py:668: roots just outside the domain).
+__device__ __forceinline__ double patch_eps(const double* __restrict__ P48) {
   double mag = 0.0, alo = INFINITY, ahi = -INFINITY, blo = INFINITY, bhi = -INFINITY;
   for (int k = 0; k < 16; ++k) {
     const double A = P48[k], B = P48[16 + k], C = P48[32 + k];
     mag = fmax(mag, fmax(fabs(A), fmax(fabs(B), fabs(C))));
     alo = fmin(alo, A); ahi = fmax(ahi, A); blo = fmin(blo, B); bhi = fmax(bhi, B);
   }
-  // conservative expansion: rounding + the 1e-9 parametric acceptance band of
-  // surfaces.py:668 (roots just outside the domain)
-  const double eps = 1e-12 * (1.0 + mag) + 3e-9 * fmax(ahi - alo, bhi - blo);
-  uint64_t stack[2 * kLeafMaxLevel + 4];
+  return 1e-12 * (1.0 + mag) + 3e-9 * fmax(ahi - alo, bhi - blo);
+}
+
+// Krawczyk data of the piece `code` over its box expanded by kLeafM.
+__device__ __forceinline__ KrawPre piece_kraw(const double* __restrict__ P48, uint64_t code) {
+  const int L = code_level(code);
+  const double wu = code_wu(L), wv = code_wv(L);
+  const double u0 = (double)code_iu(code) * wu, v0 = (double)code_iv(code) * wv;
+  double a[16], b[16];
+  for (int k = 0; k < 16; ++k) {
+    a[k] = P48[k];
+    b[k] = P48[16 + k];
+  }
+  extract_net(a, u0 - kLeafM * wu, u0 + (1.0 + kLeafM) * wu, v0 - kLeafM * wv,
+              v0 + (1.0 + kLeafM) * wv);
+  extract_net(b, u0 - kLeafM * wu, u0 + (1.0 + kLeafM) * wu, v0 - kLeafM * wv,
+              v0 + (1.0 + kLeafM) * wv);
+  return kraw_pre(a, b);
+}
+
+__device__ __forceinline__ bool kraw_certifies(const KrawPre& kp) {
+  return kp.ok && kp.R0 < kLeafRmax && kp.R1 < kLeafRmax;
+}
+
+// Leaf record (Krawczyk data, separating axes) and cull box (a lo/hi, b lo/hi,
+// c max) of the piece `code` of patch p.
+__device__ void make_leaf(const double* __restrict__ P48, int32_t p, uint64_t code,
+                          const KrawPre& kp, double eps, LeafRec& r, double box[5]) {
+  const int L = code_level(code);
+  const double wu = code_wu(L), wv = code_wv(L);
+  const double u0 = (double)code_iu(code) * wu, v0 = (double)code_iv(code) * wv;
+  r.Ga = kp.Ga; r.Gb = kp.Gb;
+  r.Y00 = kp.Y00; r.Y01 = kp.Y01; r.Y10 = kp.Y10; r.Y11 = kp.Y11;
+  r.R0 = kp.R0; r.R1 = kp.R1;
+  r.code = code;
+  r.patch = p;
+  r.ok = kp.ok;
+  // the piece's own control box (convex hull of the piece over D)
+  double a[16], b[16], c[16];
+  for (int k = 0; k < 16; ++k) {
+    a[k] = P48[k];
+    b[k] = P48[16 + k];
+    c[k] = P48[32 + k];
+  }
+  extract_net(a, u0, u0 + wu, v0, v0 + wv);
+  extract_net(b, u0, u0 + wu, v0, v0 + wv);
+  extract_net(c, u0, u0 + wu, v0, v0 + wv);
+  double la = INFINITY, ha = -INFINITY, lb = INFINITY, hb = -INFINITY, hc = -INFINITY;
+  for (int k = 0; k < 16; ++k) {
+    la = fmin(la, a[k]); ha = fmax(ha, a[k]);
+    lb = fmin(lb, b[k]); hb = fmax(hb, b[k]);
+    hc = fmax(hc, c[k]);
+  }
+  hull_axes(a, b, eps + 1e-15 * (fabs(la) + fabs(ha) + fabs(lb) + fabs(hb)), r);
+  box[0] = la - eps; box[1] = ha + eps; box[2] = lb - eps; box[3] = hb + eps; box[4] = hc + eps;
+}
+
+template <bool kFill>
+__global__ void k_leaves(int64_t P, const double* __restrict__ proj,
+                         const int64_t* __restrict__ offs, int64_t* __restrict__ counts,
+                         LeafRec* __restrict__ leaves, double* __restrict__ leafbox,
+                         uint32_t* __restrict__ keys, int32_t* __restrict__ ids, double amin,
+                         double ainv, double bmin, double binv, int max_level) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const double* P48 = proj + 48 * p;
+  const double eps = patch_eps(P48);
+  uint64_t stack[2 * kLeafLevelCap + 4];
   int top = 0;
   stack[top++] = 0;  // root code
   int64_t n = 0;
@@ -67,19 +137,8 @@ __global__ void k_leaves(int64_t P, const double* __restrict__ proj,
   while (top > 0) {
     const uint64_t code = stack[--top];
     const int L = code_level(code);
-    const double wu = code_wu(L), wv = code_wv(L);
-    const double u0 = (double)code_iu(code) * wu, v0 = (double)code_iv(code) * wv;
-    double a[16], b[16];
-    for (int k = 0; k < 16; ++k) {
-      a[k] = P48[k];
-      b[k] = P48[16 + k];
-    }
-    extract_net(a, u0 - kLeafM * wu, u0 + (1.0 + kLeafM) * wu, v0 - kLeafM * wv,
-                v0 + (1.0 + kLeafM) * wv);
-    extract_net(b, u0 - kLeafM * wu, u0 + (1.0 + kLeafM) * wu, v0 - kLeafM * wv,
-                v0 + (1.0 + kLeafM) * wv);
-    const KrawPre kp = kraw_pre(a, b);
-    const bool leaf = (kp.ok && kp.R0 < kLeafRmax && kp.R1 < kLeafRmax) || L >= kLeafMaxLevel;
+    const KrawPre kp = piece_kraw(P48, code);
+    const bool leaf = kraw_certifies(kp) || L >= max_level;
     if (!leaf) {
       const uint64_t iu = code_iu(code), iv = code_iv(code);
       if ((L & 1) == 0) {
@@ -94,32 +153,10 @@ __global__ void k_leaves(int64_t P, const double* __restrict__ proj,
     if (kFill) {
       const int64_t li = o + n;
       LeafRec r;
-      r.Ga = kp.Ga; r.Gb = kp.Gb;
-      r.Y00 = kp.Y00; r.Y01 = kp.Y01; r.Y10 = kp.Y10; r.Y11 = kp.Y11;
-      r.R0 = kp.R0; r.R1 = kp.R1;
-      r.code = code;
-      r.patch = (int32_t)p;
-      r.ok = kp.ok;
-      // the leaf's own control box (convex hull of the piece over D)
-      double c[16];
-      for (int k = 0; k < 16; ++k) {
-        a[k] = P48[k];
-        b[k] = P48[16 + k];
-        c[k] = P48[32 + k];
-      }
-      extract_net(a, u0, u0 + wu, v0, v0 + wv);
-      extract_net(b, u0, u0 + wu, v0, v0 + wv);
-      extract_net(c, u0, u0 + wu, v0, v0 + wv);
-      double la = INFINITY, ha = -INFINITY, lb = INFINITY, hb = -INFINITY, hc = -INFINITY;
-      for (int k = 0; k < 16; ++k) {
-        la = fmin(la, a[k]); ha = fmax(ha, a[k]);
-        lb = fmin(lb, b[k]); hb = fmax(hb, b[k]);
-        hc = fmax(hc, c[k]);
-      }
-      hull_axes(a, b, eps + 1e-15 * (fabs(la) + fabs(ha) + fabs(lb) + fabs(hb)), r);
-      leaves[li] = r;
       double* lbx = leafbox + 5 * li;
-      lbx[0] = la - eps; lbx[1] = ha + eps; lbx[2] = lb - eps; lbx[3] = hb + eps; lbx[4] = hc + eps;
+      make_leaf(P48, (int32_t)p, code, kp, eps, r, lbx);
+      leaves[li] = r;
+      const double la = lbx[0], ha = lbx[1], lb = lbx[2], hb = lbx[3];
       const double ca = (0.5 * (la + ha) - amin) * ainv, cb = (0.5 * (lb + hb) - bmin) * binv;
       const uint32_t ia = (uint32_t)fmin(fmax(ca * 32767.0, 0.0), 32767.0);
       const uint32_t ib = (uint32_t)fmin(fmax(cb * 32767.0, 0.0), 32767.0);
@@ -132,6 +169,86 @@ __global__ void k_leaves(int64_t P, const double* __restrict__ proj,
     ++n;
   }
   if (!kFill) counts[p] = n;
+}
+
+// Fold trees (query-independent, once per round).  A leaf that did not
+// certify at the leaf depth cap sits on a silhouette fold of the projection.
+// Its subtree is refined further, to sub_level, with the same criterion, and
+// stored in depth-first preorder with skip counts: node k's subtree is
+// [k, k + skip[k]), a leaf has skip 1.  Every node keeps its control box and
+// separating axes (LeafRec + box), so a query near the fold walks the tree
+// stacklessly with cheap exclusion tests instead of re-deriving each node's
+// net (node_test), and only the uncertified sub-leaves on the fold itself
+// still need the per-query subdivision fallback.
+// kFill = false: count tree nodes per leaf; true: write them.
+template <bool kFill>
+__global__ void k_foldtree(int64_t n_leaves, const LeafRec* __restrict__ leaves,
+                           const double* __restrict__ proj, int sub_level,
+                           const int64_t* __restrict__ offs, int64_t* __restrict__ counts,
+                           LeafRec* __restrict__ sub, double* __restrict__ subbox,
+                           int32_t* __restrict__ subskip) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_leaves) return;
+  const LeafRec L = leaves[i];
+  const int32_t p = L.patch;
+  int64_t n = 0;
+  const int64_t o = kFill ? offs[i] : 0;
+  const bool cert = L.ok && L.R0 < kLeafRmax && L.R1 < kLeafRmax;
+  if (!cert && code_level(L.code) < sub_level) {
+    const double* P48 = proj + 48 * (int64_t)p;
+    const double eps = patch_eps(P48);
+    uint64_t stack[2 * kLeafLevelCap + 4];
+    int64_t open_idx[kLeafLevelCap + 2];
+    int open_top[kLeafLevelCap + 2];
+    int top = 0, otop = 0;
+    {
+      uint64_t c0, c1;
+      const int lv = code_level(L.code);
+      const uint64_t iu = code_iu(L.code), iv = code_iv(L.code);
+      if ((lv & 1) == 0) {
+        c0 = make_code(lv + 1, 2 * iu, iv);
+        c1 = make_code(lv + 1, 2 * iu + 1, iv);
+      } else {
+        c0 = make_code(lv + 1, iu, 2 * iv);
+        c1 = make_code(lv + 1, iu, 2 * iv + 1);
+      }
+      stack[top++] = c1;
+      stack[top++] = c0;
+    }
+    for (;;) {
+      // close the internal nodes whose subtrees are complete
+      while (otop > 0 && top <= open_top[otop - 1]) {
+        --otop;
+        if (kFill) subskip[o + open_idx[otop]] = (int32_t)(n - open_idx[otop]);
+      }
+      if (top == 0) break;
+      const uint64_t code = stack[--top];
+      const int lv = code_level(code);
+      const KrawPre kp = piece_kraw(P48, code);
+      const bool leaf = kraw_certifies(kp) || lv >= sub_level;
+      if (kFill) {
+        LeafRec r;
+        make_leaf(P48, p, code, kp, eps, r, subbox + 5 * (o + n));
+        sub[o + n] = r;
+        if (leaf) subskip[o + n] = 1;
+      }
+      if (!leaf) {
+        open_idx[otop] = n;
+        open_top[otop] = top;
+        ++otop;
+        const uint64_t iu = code_iu(code), iv = code_iv(code);
+        if ((lv & 1) == 0) {
+          stack[top++] = make_code(lv + 1, 2 * iu + 1, iv);
+          stack[top++] = make_code(lv + 1, 2 * iu, iv);
+        } else {
+          stack[top++] = make_code(lv + 1, iu, 2 * iv + 1);
+          stack[top++] = make_code(lv + 1, iu, 2 * iv);
+        }
+      }
+      ++n;
+    }
+  }
+  if (!kFill) counts[i] = n;
 }
 
 __device__ __forceinline__ int lbvh_delta(const uint32_t* keys, int n, int i, int j) {
@@ -427,7 +544,70 @@ out:
   return e;
 }
 
+// Fold trees of the round's uncertified leaves (k_foldtree): the deepest
+// sub_level <= kSubLevelMax whose node count stays within the budget
+// (GWN_SUB_LEVEL overrides; 0 disables).
+static cudaError_t build_subleaves(Round& rd, cudaStream_t st) {
+  const char* env = getenv("GWN_SUB_LEVEL");
+  int level = env ? atoi(env) : kSubLevelMax;
+  if (level > kLeafLevelCap) level = kLeafLevelCap;
+  const int64_t n = rd.n_leaves;
+  if (level <= leaf_max_level() || n <= 0) return cudaSuccess;
+  const int64_t budget = std::max<int64_t>(4 * n, 1ll << 20);
+  cudaError_t e = cudaSuccess;
+  int64_t *cnt = nullptr, *offs = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  int64_t total = 0;
+  const unsigned g = (unsigned)((n + 127) / 128);
+#define SC(x)                       \
+  do {                              \
+    e = (x);                        \
+    if (e != cudaSuccess) goto out; \
+  } while (0)
+  SC(cudaMalloc(&cnt, sizeof(int64_t) * (n + 1)));
+  SC(cudaMalloc(&offs, sizeof(int64_t) * (n + 1)));
+  SC(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, offs, (int)(n + 1), st));
+  SC(cudaMalloc(&tmp, tb));
+  for (;; level -= 2) {
+    if (level <= leaf_max_level()) goto out;  // nothing fits: keep the plain fallback
+    SC(cudaMemsetAsync(cnt + n, 0, sizeof(int64_t), st));
+    k_foldtree<false><<<g, 128, 0, st>>>(n, rd.leaves, rd.proj, level, nullptr, cnt, nullptr,
+                                         nullptr, nullptr);
+    SC(cudaGetLastError());
+    SC(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, offs, (int)(n + 1), st));
+    SC(cudaMemcpyAsync(&total, offs + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SC(cudaStreamSynchronize(st));
+    if (total <= budget) break;
+  }
+  if (total > 0) {
+    SC(cudaMalloc(&rd.sub, sizeof(LeafRec) * total));
+    SC(cudaMalloc(&rd.subbox, sizeof(double) * 5 * total));
+    SC(cudaMalloc(&rd.subskip, sizeof(int32_t) * total));
+    k_foldtree<true><<<g, 128, 0, st>>>(n, rd.leaves, rd.proj, level, offs, nullptr, rd.sub,
+                                        rd.subbox, rd.subskip);
+    SC(cudaGetLastError());
+    rd.sub_offs = offs;
+    offs = nullptr;
+    rd.n_sub = total;
+    rd.sub_level = level;
+    SC(cudaStreamSynchronize(st));
+  }
+  if (getenv("GWN_TRACE"))
+    fprintf(stderr, "[gwn] fold trees: %lld nodes to level %d\n", (long long)total, level);
+out:
+#undef SC
+  if (cnt) cudaFree(cnt);
+  if (offs) cudaFree(offs);
+  if (tmp) cudaFree(tmp);
+  return e;
+}
+
 void free_round(Round& rd) {
+  if (rd.sub) cudaFree(rd.sub);
+  if (rd.subbox) cudaFree(rd.subbox);
+  if (rd.subskip) cudaFree(rd.subskip);
+  if (rd.sub_offs) cudaFree(rd.sub_offs);
   if (rd.proj) cudaFree(rd.proj);
   if (rd.nodes) cudaFree(rd.nodes);
   if (rd.leafbox) cudaFree(rd.leafbox);
@@ -486,7 +666,7 @@ cudaError_t build_round_dir(gwn_scene* sc, const double d[3], Round& rd, cudaStr
       RC(cudaMalloc(&loffs, sizeof(int64_t) * (P + 1)));
       RC(cudaMemsetAsync(lcount + P, 0, sizeof(int64_t), st));
       k_leaves<false><<<(unsigned)((P + 63) / 64), 64, 0, st>>>(
-          P, rd.proj, nullptr, lcount, nullptr, nullptr, nullptr, nullptr, amin, ainv, bmin, binv);
+          P, rd.proj, nullptr, lcount, nullptr, nullptr, nullptr, nullptr, amin, ainv, bmin, binv, leaf_max_level());
       RC(cudaGetLastError());
       RC(cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, lcount, loffs, (int)P + 1, st));
       RC(cudaMalloc(&cub_tmp, cub_bytes));
@@ -510,7 +690,7 @@ cudaError_t build_round_dir(gwn_scene* sc, const double d[3], Round& rd, cudaStr
       RC(cudaMalloc(&ids, sizeof(int32_t) * nl));
       RC(cudaMalloc(&ids2, sizeof(int32_t) * nl));
       k_leaves<true><<<(unsigned)((P + 63) / 64), 64, 0, st>>>(
-          P, rd.proj, loffs, nullptr, rd.leaves, rd.leafbox, keys, ids, amin, ainv, bmin, binv);
+          P, rd.proj, loffs, nullptr, rd.leaves, rd.leafbox, keys, ids, amin, ainv, bmin, binv, leaf_max_level());
       RC(cudaGetLastError());
       if (nl > 1) {
         RC(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, keys, keys2, ids, ids2, n, 0, 30,
@@ -538,6 +718,7 @@ cudaError_t build_round_dir(gwn_scene* sc, const double d[3], Round& rd, cudaStr
       }
       RC(cudaStreamSynchronize(st));
       RC(build_grid(rd, amin, amax, bmin, bmax, st));
+      RC(build_subleaves(rd, st));
     out:
       if (keys) cudaFree(keys);
       if (keys2) cudaFree(keys2);

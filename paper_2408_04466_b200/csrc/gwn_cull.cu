@@ -39,12 +39,15 @@ k_cull(const Node* __restrict__ nodes, const double* __restrict__ leafbox, int64
        GridView grid, Frame f, int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
        double* __restrict__ qproj, int32_t* __restrict__ pair_slot,
        int32_t* __restrict__ pair_leaf, unsigned long long* __restrict__ pair_count,
-       unsigned long long cap) {
+       unsigned long long cap, CullZero z) {
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = s < m;
   int buf[kLBuf];
   int n = 0;
   if (live) {
+    // the round's per-slot accumulators start at zero (K3/K4 run after K2)
+    if (z.chi) z.chi[s] = 0;
+    if (z.flags) z.flags[s] = 0;
     const int32_t q = active ? active[s] : s;
     double qa, qb, qc;
     query_proj(f, pos, q, qa, qb, qc);
@@ -125,14 +128,15 @@ k_cull(const Node* __restrict__ nodes, const double* __restrict__ leafbox, int64
 
 cudaError_t launch_cull(const gwn_scene* sc, const Round& rd, int32_t m, const int32_t* active,
                         const double* pos, double* qproj, int32_t* pair_slot, int32_t* pair_leaf,
-                        unsigned long long* pair_count, int64_t cap, cudaStream_t st) {
+                        unsigned long long* pair_count, int64_t cap, cudaStream_t st,
+                        CullZero z) {
   (void)sc;
   if (m <= 0) return cudaSuccess;
   GridView g{rd.use_grid ? rd.cell_offs : nullptr, rd.cell_leaves, rd.ga, rd.gb,
               rd.gx0, rd.gy0, rd.gia, rd.gib};
   k_cull<<<(m + 127) / 128, 128, 0, st>>>(rd.nodes, rd.leafbox, rd.n_leaves, g, rd.f, m, active,
                                           pos, qproj, pair_slot, pair_leaf, pair_count,
-                                          (unsigned long long)cap);
+                                          (unsigned long long)cap, z);
   return cudaGetLastError();
 }
 

@@ -47,7 +47,7 @@ __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
     double w = (double)chi[s] + ang * 0.15915494309189533576888;
     if (f & (FLAG_ONSURF | FLAG_DEGEN)) {
       int reason = (f & FLAG_ONSURF) ? GWN_STATUS_ON_SURFACE : GWN_STATUS_DEGENERATE;
-      int j = jit[q];
+      int j = round > 0 ? jit[q] : 0;  // round 0: jit / pos not yet initialised
       if (j < max_jitters && round + 1 >= max_rounds) {
         w_out[q] = w;  // jitter budget left but no round to use it (oracle eval_query)
         st_out[q] = GWN_STATUS_EXHAUSTED;
@@ -85,13 +85,17 @@ __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
     } else if (f & (FLAG_RESHOOT | FLAG_BAND)) {
       if (round + 1 < max_rounds) {
         push = true;
+        if (round == 0) {  // next round reads pos / jit of the queries it gets
+          jit[q] = 0;
+          for (int k = 0; k < 3; ++k) pos[3 * (int64_t)q + k] = q0[3 * (int64_t)q + k];
+        }
       } else {
         w_out[q] = w;
         st_out[q] = GWN_STATUS_EXHAUSTED;
       }
     } else {
       w_out[q] = w;
-      st_out[q] = jit[q] ? jreason[q] : (int8_t)GWN_STATUS_OK;
+      st_out[q] = (round > 0 && jit[q]) ? jreason[q] : (int8_t)GWN_STATUS_OK;
     }
   }
   // warp-aggregated compaction of the re-shot queries
@@ -107,6 +111,8 @@ __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
 }
 
 // GWN_TRACE=1: host wall-clock trace of the eval phases (development aid)
+thread_local GpuTimeline* g_tl = nullptr;
+
 struct Trace {
   bool on;
   std::chrono::steady_clock::time_point t0, last;
@@ -170,13 +176,18 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   if (n == 0) return GWN_OK;
   cudaStream_t st = (cudaStream_t)stream;
   Trace tr;
+  GpuTimeline tl;
   Workspace ws;
   ws.st = st;
   const bool host = (flags & GWN_HOST_BUFFERS) != 0;
   // auto chunk: 4M queries (2M when the boundary partials are wide)
   const int64_t chunk_max = sc->prm.chunk_queries > 0 ? sc->prm.chunk_queries
                             : boundary_chunks(sc, 0) > 16 ? (1ll << 21) : (1ll << 22);
-  int64_t* h_scalar = nullptr;  // pinned: [0] candidate count, [1] next active count
+  // device scalar block, copied to pinned host memory once per round:
+  // [0, CNT_N) eval counters, CNT_N + [0] candidate count, [1] next active
+  // count, [4] fallback items, [5] Newton items, [6] overflow, [7] Newton work
+  constexpr int kBlk = CNT_N + 8;
+  int64_t* h_scalar = nullptr;
   const double* d_q = queries;
   double* d_w = w_out;
   int8_t* d_st = status_out;
@@ -192,13 +203,14 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     // pinned round scalars: one small buffer per host thread (gwn_eval
     // synchronises its stream before returning, so reuse is safe)
     static thread_local int64_t* t_pinned = nullptr;
-    if (!t_pinned) CKE(cudaMallocHost(&t_pinned, 4 * sizeof(int64_t)));
+    if (!t_pinned) CKE(cudaMallocHost(&t_pinned, kBlk * sizeof(int64_t)));
     h_scalar = t_pinned;
   }
+  g_tl = getenv("GWN_TIMELINE") ? &tl : nullptr;
+  tl_mark(st, "start");
   tr.mark("setup");
-  d_cnt = ws.get<unsigned long long>(CNT_N);
+  d_cnt = ws.get<unsigned long long>(kBlk);
   CKE(ws.err);
-  CKE(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * CNT_N, st));
   if (host) {
     double* dq = ws.get<double>((size_t)(3 * n));
     d_w = ws.get<double>((size_t)n);
@@ -223,9 +235,9 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     int32_t* fl = ws.get<int32_t>((size_t)cm);
     const int nchunk_max = boundary_chunks(sc, (int32_t)cm);
     double* bterm = ws.get<double>((size_t)cm * nchunk_max);
-    // round scalars: [0] candidate count, [1] next active count,
-    // [2] fallback items, [3] newton items
-    unsigned long long* rsc = ws.get<unsigned long long>(4);
+    unsigned long long* rsc = d_cnt + CNT_N;  // round scalars (see kBlk)
+    unsigned long long* k3cnt = rsc + 4;
+    bool cnt_zeroed = false;
     // round-0 spatial ordering of the queries (64 x 64 Morton cells)
     // (measured on config 2: the ordering costs what it saves in the cull, so
     // it is opt-in; the grid cull does not need coherent queries)
@@ -239,14 +251,14 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     for (int64_t c0 = 0; c0 < n; c0 += cm) {
       const int32_t mc = (int32_t)((n - c0) < cm ? (n - c0) : cm);
       const double* q0 = d_q + 3 * c0;
-      CKE(cudaMemcpyAsync(pos, q0, sizeof(double) * 3 * mc, cudaMemcpyDeviceToDevice, st));
-      CKE(cudaMemsetAsync(jit, 0, mc, st));
+      // round 0 reads the queries in place; k_finalize fills pos / jit for
+      // the queries it passes on to the next round
       int32_t m = mc;
       const int32_t* active = nullptr;
       int cur = 0;
       if (sort_q) {
         CKE(ensure_round(sc, 0, st));
-        CKE(launch_query_order(sc->rounds[0], mc, pos, order_tmp, act[1], st));
+        CKE(launch_query_order(sc->rounds[0], mc, q0, order_tmp, act[1], st));
         active = act[1];  // round 0 writes its re-shoot list into act[0]
         launches += 3;
       }
@@ -267,34 +279,54 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
           CKE(cudaMallocAsync(&k3_scratch, intersect_scratch_bytes(pair_cap), st));
         }
         tr.mark("round setup");
+        tl_mark(st, "round setup done");
         if (sc->timed) CKE(cudaEventRecord(ev[0], st));
-        CKE(cudaMemsetAsync(rsc, 0, sizeof(unsigned long long) * 4, st));
+        const double* rpos = r == 0 ? q0 : pos;
+        if (!cnt_zeroed) {  // eval counters + round scalars, one memset
+          CKE(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * kBlk, st));
+          cnt_zeroed = true;
+        } else {
+          CKE(cudaMemsetAsync(rsc, 0, sizeof(unsigned long long) * 8, st));
+        }
         // ---- K2: cull (one pass, warp-aggregated appends)
         if (sc->P > 0) {
-          CKE(launch_cull(sc, rd, m, active, pos, qproj, pair_slot, pair_leaf, rsc, pair_cap, st));
+          CullZero z;
+          z.chi = chi;
+          z.flags = fl;
+          CKE(launch_cull(sc, rd, m, active, rpos, qproj, pair_slot, pair_leaf, rsc, pair_cap, st,
+                          z));
           ++launches;
         }
         tr.mark("cull launched");
+        tl_mark(st, "cull done");
         if (sc->timed) CKE(cudaEventRecord(ev[1], st));
         // ---- K3: candidate test, DFS fallback, Newton + segmented reduction
-        CKE(cudaMemsetAsync(chi, 0, sizeof(int32_t) * m, st));
-        CKE(cudaMemsetAsync(fl, 0, sizeof(int32_t) * m, st));
+        if (sc->P == 0) {  // no cull kernel to zero the accumulators
+          CKE(cudaMemsetAsync(chi, 0, sizeof(int32_t) * m, st));
+          CKE(cudaMemsetAsync(fl, 0, sizeof(int32_t) * m, st));
+        }
         cudaEvent_t join = nullptr;
         if (sc->P > 0) {
           CKE(launch_intersect(sc, rd, pair_slot, pair_leaf, rsc, pair_cap, qproj, chi, fl, d_cnt,
-                               k3_scratch, sc->timed ? ev4 : nullptr, rsc + 2, &join, nullptr,
+                               k3_scratch, k3cnt, sc->timed ? ev4 : nullptr, k3cnt, &join, nullptr,
                                st));
           launches += 3;
         }
         tr.mark("k3 launched");
+        tl_mark(st, "k3 main done");
         if (sc->timed) CKE(cudaEventRecord(ev[2], st));
         // ---- K4: boundary term
-        const int nchunk = boundary_chunks(sc, m);
-        CKE(launch_boundary(sc, rd, m, active, pos, bterm, nchunk, fl, d_cnt, st));
-        if (sc->n_edges > 0) ++launches;
+        // (closed scenes: no net boundary, B = 0, nothing to launch)
+        const int nchunk = sc->n_edges > 0 ? boundary_chunks(sc, m) : 0;
+        if (nchunk > 0) {
+          CKE(launch_boundary(sc, rd, m, active, rpos, bterm, nchunk, fl, d_cnt, st));
+          ++launches;
+        }
         if (sc->timed) CKE(cudaEventRecord(ev[3], st));
         // ---- K5: finalize / compact re-shoots (after the K3 side stream)
+        tl_mark(st, "k4 done");
         if (join) CKE(cudaStreamWaitEvent(st, join, 0));
+        tl_mark(st, "joined");
         int32_t* nxt = act[cur];
         k_finalize<<<(m + 127) / 128, 128, 0, st>>>(
             m, active, chi, fl, bterm, nchunk, r, sc->prm.max_rounds, sc->prm.max_jitters,
@@ -304,13 +336,14 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
             (unsigned long long)pair_cap);
         CKE(cudaGetLastError());
         ++launches;
-        CKE(cudaMemcpyAsync(h_scalar, rsc, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost,
-                            st));
+        CKE(cudaMemcpyAsync(h_scalar, d_cnt, sizeof(unsigned long long) * kBlk,
+                            cudaMemcpyDeviceToHost, st));
         if (sc->timed) CKE(cudaEventRecord(ev[4], st));
+        tl_mark(st, "finalize+d2h done");
         tr.mark("round launched");
         CKE(cudaStreamSynchronize(st));
         tr.mark("round synced");
-        const int64_t npairs = h_scalar[0];
+        const int64_t npairs = h_scalar[CNT_N];
         if (npairs > pair_cap) {  // re-run the round with the exact capacity
           std::lock_guard<std::mutex> lk(sc->mu);
           sc->pairs_per_query = fmax(sc->pairs_per_query, (double)npairs / m);
@@ -338,9 +371,9 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
             stats.ms_k3_newton += c;
           }
         }
-        stats.k3_fallback_items += h_scalar[2];
-        stats.k3_newton_items += h_scalar[3];
-        m = (int32_t)(*(int32_t*)(h_scalar + 1));
+        stats.k3_fallback_items += h_scalar[CNT_N + 4];
+        stats.k3_newton_items += h_scalar[CNT_N + 5];
+        m = (int32_t)(*(int32_t*)(h_scalar + CNT_N + 1));
         active = nxt;
         cur ^= 1;
         ++r;
@@ -354,17 +387,19 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     CKE(cudaMemcpyAsync(w_out, d_w, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     CKE(cudaMemcpyAsync(status_out, d_st, n, cudaMemcpyDeviceToHost, st));
   }
-  CKE(cudaMemcpyAsync(h_cnt, d_cnt, sizeof h_cnt, cudaMemcpyDeviceToHost, st));
-  CKE(cudaStreamSynchronize(st));
+  // eval counters: from the last round's scalar copy (no extra round trip)
+  for (int k = 0; k < CNT_N; ++k) h_cnt[k] = (unsigned long long)h_scalar[k];
+  if (host) CKE(cudaStreamSynchronize(st));
   stats.nodes = (int64_t)h_cnt[CNT_NODES];
   stats.newton_iters = (int64_t)h_cnt[CNT_NEWTON];
   stats.roots = (int64_t)h_cnt[CNT_ROOTS];
   stats.boundary_segments = (int64_t)h_cnt[CNT_SEGMENTS];
   if (getenv("GWN_TRACE"))
-    fprintf(stderr, "[gwn] fallback: max nodes/item %llu, items > 16 nodes %llu\n",
-            h_cnt[CNT_MAXNODES], h_cnt[CNT_BIGITEMS]);
+    fprintf(stderr, "[gwn] fallback: max nodes/item %llu, items > 16 nodes %llu, max levels %llu\n",
+            h_cnt[CNT_MAXNODES], h_cnt[CNT_BIGITEMS], h_cnt[CNT_MAXLEVELS]);
   stats.kernel_launches = launches;
   sc->stats = stats;
+  tl_mark(st, "outputs copied");
   tr.mark("outputs copied");
 done:
   ws.release();
@@ -375,6 +410,11 @@ done:
   for (auto& e : ev4)
     if (e) cudaEventDestroy(e);
   tr.mark("done");
+  if (g_tl) {
+    cudaDeviceSynchronize();
+    g_tl->dump();
+    g_tl = nullptr;
+  }
   return rc;
 }
 

@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stdio.h>
 #include <stdint.h>
 
 #include <array>
@@ -38,6 +39,7 @@ enum : int {
   CNT_SEGMENTS = 4,
   CNT_MAXNODES = 5,  // max DFS nodes of one fallback item (diagnostic)
   CNT_BIGITEMS = 6,  // fallback items with > 16 nodes (diagnostic)
+  CNT_MAXLEVELS = 7, // deepest fallback BFS, in levels (diagnostic)
   CNT_N = 8,
 };
 
@@ -90,6 +92,15 @@ struct Round {
   int32_t* cell_offs = nullptr;    // (ga*gb+1) exclusive offsets
   int32_t* cell_leaves = nullptr;  // leaf ids per cell
   int64_t grid_entries = 0;
+  // fold trees of the uncertified leaves (k_foldtree): the tree of leaf i
+  // is nodes [sub_offs[i], sub_offs[i+1]) in preorder, node k's subtree is
+  // [k, k + subskip[k]) (1 = leaf); boxes as leafbox
+  LeafRec* sub = nullptr;
+  double* subbox = nullptr;
+  int32_t* subskip = nullptr;
+  int64_t* sub_offs = nullptr;  // (n_leaves+1), null when no leaf needed it
+  int64_t n_sub = 0;
+  int sub_level = 0;
 };
 
 }  // namespace gwn
@@ -121,6 +132,40 @@ struct gwn_scene {
 
 namespace gwn {
 
+// GPU-side timeline (GWN_TIMELINE=1, development aid): timing events
+// recorded between the ops of one eval on whichever stream runs them;
+// recording an event does not order the streams.
+struct GpuTimeline {
+  cudaEvent_t ev[48];
+  const char* name[48];
+  int n = 0;
+  void mark(cudaStream_t s, const char* nm) {
+    if (n >= 48 || cudaEventCreate(&ev[n]) != cudaSuccess) return;
+    cudaEventRecord(ev[n], s);
+    name[n++] = nm;
+  }
+  void dump() {
+    for (int k = 0; k < n; ++k) {
+      float ms = 0.f;
+      const cudaError_t e = cudaEventElapsedTime(&ms, ev[0], ev[k]);
+      fprintf(stderr, "[gwn-tl] %-26s %9.1f us %s\n", name[k], ms * 1e3f,
+              e == cudaSuccess ? "" : cudaGetErrorString(e));
+    }
+    for (int k = 0; k < n; ++k) cudaEventDestroy(ev[k]);
+    n = 0;
+  }
+};
+extern thread_local GpuTimeline* g_tl;
+inline void tl_mark(cudaStream_t s, const char* nm) {
+  if (g_tl) g_tl->mark(s, nm);
+}
+
+// per-slot accumulators the cull kernel zeroes for its round (nullable)
+struct CullZero {
+  int32_t* chi = nullptr;
+  int32_t* flags = nullptr;
+};
+
 // launchers (stream-ordered); defined in the .cu files
 cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st);            // gwn_bvh.cu
 cudaError_t build_round_dir(gwn_scene* sc, const double d[3], Round& rd, cudaStream_t st);
@@ -128,13 +173,17 @@ void free_round(Round& rd);
 cudaError_t launch_cull(const gwn_scene* sc, const Round& rd, int32_t m, const int32_t* active,
                         const double* pos, double* qproj, int32_t* pair_slot, int32_t* pair_leaf,
                         unsigned long long* pair_count, int64_t cap,
-                        cudaStream_t st);                                     // gwn_cull.cu
+                        cudaStream_t st,
+                        CullZero z = CullZero{});                                     // gwn_cull.cu
 cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t* pair_slot,
                              const int32_t* pair_leaf, const unsigned long long* npairs_dev,
                              int64_t pair_cap, const double* qproj, int32_t* chi,
                              int32_t* flags, unsigned long long* counters, void* scratch,
-                             cudaEvent_t* ev4, unsigned long long* items_out, cudaEvent_t* join,
+                             unsigned long long* k3cnt, cudaEvent_t* ev4,
+                             unsigned long long* items_out, cudaEvent_t* join,
                              const RecordSink* rec, cudaStream_t st);         // gwn_wavefront.cu
+// k3cnt: 4 zeroed device counters per round ([0] fallback items, [1] Newton
+// items, [2] overflow, [3] Newton work); items_out may alias k3cnt
 size_t intersect_scratch_bytes(int64_t pair_cap);
 cudaError_t launch_query_order(const Round& rd, int32_t m, const double* pos, void* scratch,
                                int32_t* perm, cudaStream_t st);               // gwn_bvh.cu

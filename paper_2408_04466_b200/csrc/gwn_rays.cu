@@ -232,10 +232,10 @@ extern "C" int gwn_eval_rays(gwn_scene* sc, const double* origins, int64_t R,
       double* qproj = dalloc<double>(bufs, 3 * R, st, ae);
       int32_t* rchi = dalloc<int32_t>(bufs, R, st, ae);
       int32_t* rfl = dalloc<int32_t>(bufs, R, st, ae);
-      unsigned long long* cnt = dalloc<unsigned long long>(bufs, CNT_N + 8, st, ae);
+      unsigned long long* cnt = dalloc<unsigned long long>(bufs, CNT_N + 12, st, ae);
       CKR(ae);
-      unsigned long long* rsc = cnt + CNT_N;  // [0] candidates, [2..3] K3 items, [4] records
-      CKR(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (CNT_N + 8), st));
+      unsigned long long* rsc = cnt + CNT_N;  // [0] candidates, [4] records, [8..11] K3 counters
+      CKR(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (CNT_N + 12), st));
       k_ray_starts<<<(unsigned)((R + 127) / 128), 128, 0, st>>>(
           R, d_org, d_ts, d_offs, rd->f, 1e-6 * (1.0 + sc->diag), rpos, rt0);
       CKR(cudaGetLastError());
@@ -251,14 +251,14 @@ extern "C" int gwn_eval_rays(gwn_scene* sc, const double* origins, int64_t R,
         const int64_t rcap = 2 * pair_cap + 1024;
         rec = dalloc<HitRec>(bufs, rcap, st, ae);
         CKR(ae);
-        CKR(cudaMemsetAsync(rsc, 0, sizeof(unsigned long long) * 8, st));
+        CKR(cudaMemsetAsync(rsc, 0, sizeof(unsigned long long) * 12, st));
         CKR(cudaMemsetAsync(rchi, 0, sizeof(int32_t) * R, st));
         CKR(cudaMemsetAsync(rfl, 0, sizeof(int32_t) * R, st));
         CKR(launch_cull(sc, *rd, m, nullptr, rpos, qproj, ps, pl, rsc, pair_cap, st));
         RecordSink sink{rec, rsc + 4, (unsigned long long)rcap};
         cudaEvent_t join = nullptr;
         CKR(launch_intersect(sc, *rd, ps, pl, rsc, pair_cap, qproj, rchi, rfl, cnt, scratch,
-                             nullptr, rsc + 2, &join, &sink, st));
+                             rsc + 8, nullptr, rsc + 8, &join, &sink, st));
         if (join) CKR(cudaStreamWaitEvent(st, join, 0));
         unsigned long long h[8];
         CKR(cudaMemcpyAsync(h, rsc, sizeof h, cudaMemcpyDeviceToHost, st));
@@ -314,8 +314,9 @@ extern "C" int gwn_eval_rays(gwn_scene* sc, const double* origins, int64_t R,
         k_ray_points<<<g, 128, 0, st>>>(p0, np, R, d_org, d_ts, d_offs, rd->f, hoff, ht, hs, rfl,
                                         sc->dprm.on_surface_t, pos, chi, qfl);
         CKR(cudaGetLastError());
-        CKR(launch_boundary(sc, *rd, (int32_t)np, nullptr, pos, bpart, nch, qfl, cnt, st));
-        k_ray_finalize<<<g, 128, 0, st>>>(np, chi, qfl, bpart, sc->n_edges > 0 ? nch : 1,
+        if (sc->n_edges > 0)
+          CKR(launch_boundary(sc, *rd, (int32_t)np, nullptr, pos, bpart, nch, qfl, cnt, st));
+        k_ray_finalize<<<g, 128, 0, st>>>(np, chi, qfl, bpart, sc->n_edges > 0 ? nch : 0,
                                           d_w + p0, d_st + p0, fb, nfb, p0);
         CKR(cudaGetLastError());
       }

@@ -22,7 +22,7 @@ namespace gwn {
 
 struct NodeItem {
   int32_t pair;
-  int32_t pad;
+  int32_t leaf;   // round leaf index (its fold tree, if any)
   uint64_t code;  // level:6 | iu:29 | iv:29
 };
 
@@ -80,7 +80,89 @@ struct WaveArgs {
   NewtonItem* nq;
   unsigned long long* n_count;
   unsigned long long n_cap;
+  unsigned long long* n_work;  // Newton work counter (dynamic fetch), zeroed per round
+  // fold trees of the round (Round::sub*), sub_offs null when there are none
+  const int64_t* sub_offs;
+  const LeafRec* sub;
+  const double* subbox;
+  const int32_t* subskip;
+  int32_t sub_level;
 };
+
+// Newton solve of a certified (leaf or fold sub-leaf) candidate + ownership:
+// adds the owned root's sign to chi and its flags to fl.
+__device__ __forceinline__ void newton_accept(const WaveArgs& w, int32_t slot, int32_t patch,
+                                              uint64_t code, double u, double v, double qa,
+                                              double qb, double qc, int32_t& chi, int32_t& fl,
+                                              unsigned long long& iters,
+                                              unsigned long long& roots) {
+  const double* P48 = w.proj + 48 * (int64_t)patch;
+  RootResult r = newton_solve(P48, qa, qb, qc, u, v, w.prm);
+  iters += r.iters;
+  const int level = code_level(code);
+  const double wu = code_wu(level), wv = code_wv(level);
+  const double u0 = (double)code_iu(code) * wu, v0 = (double)code_iv(code) * wv;
+  const double u1 = u0 + wu, v1 = v0 + wv;
+  const double tol = w.prm.domain_tol;
+  // the unique root lies in the certification box (leaf box expanded by
+  // kLeafM); landing farther away means Newton left the certified basin
+  const double ex = kLeafM + 1e-6;
+  const bool in_cert = r.u >= u0 - ex * wu && r.u <= u1 + ex * wu && r.v >= v0 - ex * wv &&
+                       r.v <= v1 + ex * wv;
+  if (r.status == ROOT_DIVERGED || !in_cert) {
+    fl |= FLAG_RESHOOT;  // certified root not reached: re-shoot
+  } else if (r.status == ROOT_ACCEPTED) {
+    // half-open ownership box (domain edges own the tolerance band)
+    const double lo_u = own_lo(u0, tol), hi_u = own_hi(u1, tol);
+    const double lo_v = own_lo(v0, tol), hi_v = own_hi(v1, tol);
+    const bool own = r.u >= lo_u && (r.u < hi_u || (u1 == 1.0 && r.u <= hi_u)) &&
+                     r.v >= lo_v && (r.v < hi_v || (v1 == 1.0 && r.v <= hi_v));
+    if (own) {
+      ++roots;
+      chi += r.sign;
+      if (r.tang || r.graze) fl |= FLAG_RESHOOT;
+      if (r.onsurf) fl |= FLAG_ONSURF;
+      if (w.rec) {
+        const unsigned long long k = atomicAdd(w.rec_count, 1ull);
+        if (k < w.rec_cap) w.rec[k] = HitRec{slot, r.sign, r.t};
+        else fl |= FLAG_RESHOOT;
+      }
+    }
+  }
+}
+
+// Candidate test of query (qa, qb) against a leaf / sub-leaf record:
+// 0 exclude, 1 certified root (Newton start nu, nv), 2 undecided.
+__device__ __forceinline__ int leaf_test(const LeafRec& L, double qa, double qb,
+                                         const DevParams& prm, double& nu, double& nv) {
+  const double span = 1.0 + 2.0 * kLeafM;
+  const double tl = kLeafM / span, th = (1.0 + kLeafM) / span;
+  const int lev = code_level(L.code);
+  const double wu = code_wu(lev), wv = code_wv(lev);
+  const double u0 = (double)code_iu(L.code) * wu, v0 = (double)code_iv(L.code) * wv;
+  const double tol = prm.domain_tol;
+  const double xlo_u = tl - (u0 == 0.0 ? tol / (wu * span) : 0.0);
+  const double xhi_u = th + (u0 + wu == 1.0 ? tol / (wu * span) : 0.0);
+  const double xlo_v = tl - (v0 == 0.0 ? tol / (wv * span) : 0.0);
+  const double xhi_v = th + (v0 + wv == 1.0 ? tol / (wv * span) : 0.0);
+  KrawPre k;
+  k.Ga = L.Ga; k.Gb = L.Gb;
+  k.Y00 = L.Y00; k.Y01 = L.Y01; k.Y10 = L.Y10; k.Y11 = L.Y11;
+  k.R0 = L.R0; k.R1 = L.R1;
+  k.ok = L.ok != 0;
+  double s0, s1;
+  int kr = kraw_query(k, L.Ga - qa, L.Gb - qb, xlo_u, xhi_u, xlo_v, xhi_v, -1e-7, 1.0 + 1e-7,
+                      s0, s1);
+  if (kr == 2) {  // separating axes of the leaf hull (rigorous exclusion)
+    const double p1 = L.n1a * qa + L.n1b * qb, p2 = L.n2a * qa + L.n2b * qb;
+    if (p1 < L.lo1 || p1 > L.hi1 || p2 < L.lo2 || p2 > L.hi2) kr = 0;
+  }
+  if (kr == 1) {
+    nu = u0 - kLeafM * wu + s0 * span * wu;
+    nv = v0 - kLeafM * wv + s1 * span * wv;
+  }
+  return kr;
+}
 
 // K3 pass 0: one thread per (query, leaf) candidate.  The leaf's Krawczyk
 // data are query-independent (K1), so the test is ~20 flops: exclude,
@@ -95,9 +177,6 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev,
   const int64_t npairs = (int64_t)min(*npairs_dev, out_cap);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   unsigned long long tested = 0;
-  // leaf box D inside the expanded certification box D' (local coords t)
-  const double span = 1.0 + 2.0 * kLeafM;
-  const double tl = kLeafM / span, th = (1.0 + kLeafM) / span;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < npairs; base += stride) {
     const int64_t i = base + threadIdx.x;
     bool wantN = false, wantF = false;
@@ -114,36 +193,15 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev,
       qb = w.qproj[3 * (int64_t)slot + 1];
       qc = w.qproj[3 * (int64_t)slot + 2];
       ++tested;
-      const int lev = code_level(code);
-      const double wu = code_wu(lev), wv = code_wv(lev);
-      const double u0 = (double)code_iu(code) * wu, v0 = (double)code_iv(code) * wv;
-      const double tol = w.prm.domain_tol;
-      const double xlo_u = tl - (u0 == 0.0 ? tol / (wu * span) : 0.0);
-      const double xhi_u = th + (u0 + wu == 1.0 ? tol / (wu * span) : 0.0);
-      const double xlo_v = tl - (v0 == 0.0 ? tol / (wv * span) : 0.0);
-      const double xhi_v = th + (v0 + wv == 1.0 ? tol / (wv * span) : 0.0);
-      KrawPre k;
-      k.Ga = L.Ga; k.Gb = L.Gb;
-      k.Y00 = L.Y00; k.Y01 = L.Y01; k.Y10 = L.Y10; k.Y11 = L.Y11;
-      k.R0 = L.R0; k.R1 = L.R1;
-      k.ok = L.ok != 0;
-      double s0, s1;
-      int kr = kraw_query(k, L.Ga - qa, L.Gb - qb, xlo_u, xhi_u, xlo_v, xhi_v, -1e-7,
-                          1.0 + 1e-7, s0, s1);
-      if (kr == 2) {  // separating axes of the leaf hull (rigorous exclusion)
-        const double p1 = L.n1a * qa + L.n1b * qb, p2 = L.n2a * qa + L.n2b * qb;
-        if (p1 < L.lo1 || p1 > L.hi1 || p2 < L.lo2 || p2 > L.hi2) kr = 0;
-      }
+      const int kr = leaf_test(L, qa, qb, w.prm, nu_, nv_);
       if (kr == 1) {
         wantN = true;
-        nu_ = u0 - kLeafM * wu + s0 * span * wu;
-        nv_ = v0 - kLeafM * wv + s1 * span * wv;
       } else if (kr == 2) {
         wantF = true;
       }
     }
     long long k = warp_push(wantF, out_count, out_cap, w.overflow);
-    if (k >= 0) out[k] = NodeItem{pair, 0, code};
+    if (k >= 0) out[k] = NodeItem{pair, wantF ? pair_leaf[i] : 0, code};
     k = warp_push(wantN, w.n_count, w.n_cap, w.overflow);
     if (k >= 0) w.nq[k] = NewtonItem{slot, patch, code, nu_, nv_, qa, qb, qc, 0.0};
   }
@@ -152,13 +210,18 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev,
 
 // Undecided leaves (rays near a silhouette fold of the projection):
 // breadth-first below the leaf with a frontier shared by a batch of items per
-// warp; the lanes test frontier nodes of any item in parallel (node_test,
-// gwn_dfs.cuh).  Items per warp = ceil(items / warps), at most 32: few items
-// stay spread over the GPU, many items keep every lane busy.  Roots count only
-// in the node that owns them; undecidable nodes kDfsDepth levels below the
-// leaf flag the query for a new direction.
+// warp; the lanes test frontier entries of any item in parallel.  Items per
+// warp = ceil(items / warps), at most 32: few items stay spread over the
+// GPU, many items keep every lane busy.  A frontier entry is either
+//   * a node of the leaf's precomputed fold tree (K1, k_foldtree): box and
+//     separating-axis test from stored data, certified sub-leaves solved by
+//     Newton in place, the fold's own sub-leaves handed on as codes; or
+//   * a subdivision code: node_test (gwn_dfs.cuh) derives the node's net.
+// Roots count only in the node that owns them; undecidable nodes below the
+// depth cap flag the query for a new direction.
 constexpr int kFrontier = 512;
 constexpr int kFbWarps = 4;  // warps per block
+constexpr uint8_t kTreeTag = 0x80;  // fi tag: entry is a fold-tree node index
 
 __global__ void __launch_bounds__(32 * kFbWarps)
 k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restrict__ in_count,
@@ -168,7 +231,8 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
   __shared__ double iq[kFbWarps][32][4];  // qa, qb, qc, eps_box
   __shared__ int32_t islot[kFbWarps][32], ipatch[kFbWarps][32], imax[kFbWarps][32];
   __shared__ int32_t ichi[kFbWarps][32], ifl[kFbWarps][32], inodes[kFbWarps][32];
-  const int64_t n = (int64_t)*in_count;
+  __shared__ int32_t s_n0[kFbWarps];  // initial frontier size
+  const int64_t n = (int64_t)min(*in_count, w.n_cap);  // pushes past capacity were dropped
   const int lane = threadIdx.x & 31, wb = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -177,6 +241,8 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
   unsigned long long nodes = 0, iters = 0, roots = 0;
   for (int64_t b0 = warp * ipw; b0 < n; b0 += nwarps * ipw) {
     const int nb = (int)min((int64_t)ipw, n - b0);
+    if (lane == 0) s_n0[wb] = 0;
+    __syncwarp();
     if (lane < nb) {
       const NodeItem it = in[b0 + lane];
       const int32_t slot = w.pair_slot[it.pair];
@@ -189,73 +255,127 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
       iq[wb][lane][3] = c.eps_box;
       islot[wb][lane] = slot;
       ipatch[wb][lane] = patch;
-      imax[wb][lane] = min(code_level(it.code) + kDfsDepth, kMaxLevel);
+      imax[wb][lane] = min(max(code_level(it.code) + kDfsDepth, w.sub_level + 4), kMaxLevel);
       ichi[wb][lane] = 0;
       ifl[wb][lane] = 0;
       inodes[wb][lane] = 0;
-      fr[wb][0][lane] = it.code;
-      fi[wb][0][lane] = (uint8_t)lane;
+      const int64_t t0 = w.sub_offs ? w.sub_offs[it.leaf] : 0;
+      const int64_t t1 = w.sub_offs ? w.sub_offs[it.leaf + 1] : 0;
+      if (t1 > t0) {  // the two subtrees of the leaf's fold tree
+        const int64_t t0b = t0 + w.subskip[t0];
+        const int pos = atomicAdd(&s_n0[wb], t0b < t1 ? 2 : 1);  // <= 64 <= kFrontier
+        fr[wb][0][pos] = (uint64_t)t0;
+        fi[wb][0][pos] = (uint8_t)(lane | kTreeTag);
+        if (t0b < t1) {
+          fr[wb][0][pos + 1] = (uint64_t)t0b;
+          fi[wb][0][pos + 1] = (uint8_t)(lane | kTreeTag);
+        }
+      } else {
+        const int pos = atomicAdd(&s_n0[wb], 1);
+        fr[wb][0][pos] = it.code;
+        fi[wb][0][pos] = (uint8_t)lane;
+      }
     }
     __syncwarp();
-    int cur = 0, ncur = nb;
+    int cur = 0, ncur = s_n0[wb], levels = 0;
     while (ncur > 0) {
+      ++levels;
       int nnext = 0;
       for (int base = 0; base < ncur; base += 32) {
         const int k = base + lane;
-        int o = NODE_EXCLUDED, item = 0;
-        uint64_t code = 0;
+        int nout = 0, item = 0;
+        uint8_t otag = 0;
+        uint64_t out0 = 0, out1 = 0;
         if (k < ncur) {
-          code = fr[wb][cur][k];
-          item = fi[wb][cur][k];
-          NodeCtx c;
-          c.P48 = w.proj + 48 * (int64_t)ipatch[wb][item];
-          c.qa = iq[wb][item][0];
-          c.qb = iq[wb][item][1];
-          c.qc = iq[wb][item][2];
-          c.eps_box = iq[wb][item][3];
-          RootResult r;
-          bool owned = false;
-          o = node_test(c, code, imax[wb][item], w.prm, r, owned);
+          const uint64_t e = fr[wb][cur][k];
+          const uint8_t tg = fi[wb][cur][k];
+          item = tg & 0x7f;
+          const double qa = iq[wb][item][0], qb = iq[wb][item][1], qc = iq[wb][item][2];
           ++nodes;
-          if (atomicAdd(&inodes[wb][item], 1) >= kDfsBudget) {
-            o = NODE_AMBIGUOUS;  // budget: give up on this direction
-          }
-          if (o == NODE_AMBIGUOUS) {
-            atomicOr(&ifl[wb][item], FLAG_RESHOOT);
-          } else if (o == NODE_ROOT) {
-            iters += r.iters;
-            if (r.status == ROOT_ACCEPTED && owned) {
-              ++roots;
-              atomicAdd(&ichi[wb][item], r.sign);
-              int f = 0;
-              if (r.tang || r.graze) f |= FLAG_RESHOOT;
-              if (r.onsurf) f |= FLAG_ONSURF;
-              if (w.rec) {
-                const unsigned long long kk = atomicAdd(w.rec_count, 1ull);
-                if (kk < w.rec_cap) w.rec[kk] = HitRec{islot[wb][item], r.sign, r.t};
-                else f |= FLAG_RESHOOT;
+          if (tg & kTreeTag) {
+            // precomputed fold-tree node
+            const int64_t t = (int64_t)e;
+            const double* bx = w.subbox + 5 * t;
+            const int32_t sk = w.subskip[t];
+            if (qa >= bx[0] && qa <= bx[1] && qb >= bx[2] && qb <= bx[3] && bx[4] >= qc) {
+              const LeafRec S = w.sub[t];
+              if (sk == 1) {
+                double su = 0.0, sv = 0.0;
+                const int kr = leaf_test(S, qa, qb, w.prm, su, sv);
+                if (kr == 1) {
+                  int32_t cchi = 0, cfl = 0;
+                  newton_accept(w, islot[wb][item], ipatch[wb][item], S.code, su, sv, qa, qb, qc,
+                                cchi, cfl, iters, roots);
+                  if (cchi) atomicAdd(&ichi[wb][item], cchi);
+                  if (cfl) atomicOr(&ifl[wb][item], cfl);
+                } else if (kr == 2) {  // on the fold itself: subdivide from here
+                  nout = 1;
+                  out0 = S.code;
+                }
+              } else {
+                const double p1 = S.n1a * qa + S.n1b * qb, p2 = S.n2a * qa + S.n2b * qb;
+                if (!(p1 < S.lo1 || p1 > S.hi1 || p2 < S.lo2 || p2 > S.hi2)) {
+                  nout = 2;
+                  otag = kTreeTag;
+                  out0 = (uint64_t)(t + 1);
+                  out1 = (uint64_t)(t + 1 + w.subskip[t + 1]);
+                }
               }
-              if (f) atomicOr(&ifl[wb][item], f);
+            }
+          } else {
+            NodeCtx c;
+            c.P48 = w.proj + 48 * (int64_t)ipatch[wb][item];
+            c.qa = qa;
+            c.qb = qb;
+            c.qc = qc;
+            c.eps_box = iq[wb][item][3];
+            RootResult r;
+            bool owned = false;
+            int o = node_test(c, e, imax[wb][item], w.prm, r, owned);
+            if (atomicAdd(&inodes[wb][item], 1) >= kDfsBudget) {
+              o = NODE_AMBIGUOUS;  // budget: give up on this direction
+            }
+            if (o == NODE_AMBIGUOUS) {
+              atomicOr(&ifl[wb][item], FLAG_RESHOOT);
+            } else if (o == NODE_ROOT) {
+              iters += r.iters;
+              if (r.status == ROOT_ACCEPTED && owned) {
+                ++roots;
+                atomicAdd(&ichi[wb][item], r.sign);
+                int f = 0;
+                if (r.tang || r.graze) f |= FLAG_RESHOOT;
+                if (r.onsurf) f |= FLAG_ONSURF;
+                if (w.rec) {
+                  const unsigned long long kk = atomicAdd(w.rec_count, 1ull);
+                  if (kk < w.rec_cap) w.rec[kk] = HitRec{islot[wb][item], r.sign, r.t};
+                  else f |= FLAG_RESHOOT;
+                }
+                if (f) atomicOr(&ifl[wb][item], f);
+              }
+            } else if (o == NODE_SPLIT) {
+              nout = 2;
+              child_codes(e, out0, out1);
             }
           }
         }
-        // warp-aggregated append of the children of split nodes
-        const bool sp = o == NODE_SPLIT;
-        const unsigned mask = __ballot_sync(0xffffffffu, sp);
-        if (sp) {
-          const int pos = nnext + 2 * __popc(mask & ((1u << lane) - 1));
-          if (pos + 1 < kFrontier) {
-            uint64_t c0, c1;
-            child_codes(code, c0, c1);
-            fr[wb][cur ^ 1][pos] = c0;
-            fr[wb][cur ^ 1][pos + 1] = c1;
-            fi[wb][cur ^ 1][pos] = (uint8_t)item;
-            fi[wb][cur ^ 1][pos + 1] = (uint8_t)item;
+        // warp-aggregated append of 0, 1 or 2 entries per lane
+        const unsigned b1 = __ballot_sync(0xffffffffu, nout >= 1);
+        const unsigned b2 = __ballot_sync(0xffffffffu, nout == 2);
+        if (nout) {
+          const unsigned lt = (1u << lane) - 1;
+          const int pos = nnext + __popc(b1 & lt) + __popc(b2 & lt);
+          if (pos + nout <= kFrontier) {
+            fr[wb][cur ^ 1][pos] = out0;
+            fi[wb][cur ^ 1][pos] = (uint8_t)(item | otag);
+            if (nout == 2) {
+              fr[wb][cur ^ 1][pos + 1] = out1;
+              fi[wb][cur ^ 1][pos + 1] = (uint8_t)(item | otag);
+            }
           } else {
             atomicOr(&ifl[wb][item], FLAG_RESHOOT);  // frontier overflow
           }
         }
-        nnext = min(nnext + 2 * __popc(mask), kFrontier);
+        nnext = min(nnext + __popc(b1) + __popc(b2), kFrontier);
       }
       __syncwarp();
       cur ^= 1;
@@ -266,6 +386,11 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
       const int32_t slot = islot[wb][lane];
       if (ichi[wb][lane]) atomicAdd(&w.chi[slot], ichi[wb][lane]);
       if (ifl[wb][lane]) atomicOr(&w.flags[slot], ifl[wb][lane]);
+      // diagnostics: largest item, items beyond 16 nodes
+      const int nn = inodes[wb][lane];
+      atomicMax(&w.counters[CNT_MAXNODES], (unsigned long long)nn);
+      if (nn > 16) atomicAdd(&w.counters[CNT_BIGITEMS], 1ull);
+      if (lane == 0) atomicMax(&w.counters[CNT_MAXLEVELS], (unsigned long long)levels);
     }
     __syncwarp();
   }
@@ -276,50 +401,24 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
 
 // Newton pass over the certified leaves + ownership + K5 part 1.
 __global__ void __launch_bounds__(128) k3_newton(WaveArgs w) {
-  const int64_t n = (int64_t)*w.n_count;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n = (int64_t)min(*w.n_count, w.n_cap);
   unsigned long long iters = 0, roots = 0;
-  const double span = 1.0 + 2.0 * kLeafM;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  // dynamic fetch, 32 items per warp: blocks that start late (the fallback
+  // kernel holds part of every SM) find the queue drained instead of owning
+  // a fixed share of it
+  for (;;) {
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(w.n_work, 32ull);
+    const int64_t base = (int64_t)__shfl_sync(0xffffffffu, b, 0);
+    if (base >= n) break;
+    const int64_t i = base + lane;
     int32_t slot = -1, chi = 0, fl = 0;
     if (i < n) {
       const NewtonItem it = w.nq[i];
       slot = it.slot;
-      const double* P48 = w.proj + 48 * (int64_t)it.patch;
-      RootResult r = newton_solve(P48, it.qa, it.qb, it.qc, it.u, it.v, w.prm);
-      iters += r.iters;
-      const int level = code_level(it.code);
-      const double wu = code_wu(level), wv = code_wv(level);
-      const double u0 = (double)code_iu(it.code) * wu, v0 = (double)code_iv(it.code) * wv;
-      const double u1 = u0 + wu, v1 = v0 + wv;
-      const double tol = w.prm.domain_tol;
-      // the unique root lies in the certification box (leaf box expanded by
-      // kLeafM); landing farther away means Newton left the certified basin
-      const double ex = kLeafM + 1e-6;
-      const bool in_cert = r.u >= u0 - ex * wu && r.u <= u1 + ex * wu && r.v >= v0 - ex * wv &&
-                           r.v <= v1 + ex * wv;
-      (void)span;
-      if (r.status == ROOT_DIVERGED || !in_cert) {
-        fl |= FLAG_RESHOOT;  // certified root not reached: re-shoot
-      } else if (r.status == ROOT_ACCEPTED) {
-        // half-open ownership box (domain edges own the tolerance band)
-        const double lo_u = own_lo(u0, tol), hi_u = own_hi(u1, tol);
-        const double lo_v = own_lo(v0, tol), hi_v = own_hi(v1, tol);
-        const bool own = r.u >= lo_u && (r.u < hi_u || (u1 == 1.0 && r.u <= hi_u)) &&
-                         r.v >= lo_v && (r.v < hi_v || (v1 == 1.0 && r.v <= hi_v));
-        if (own) {
-          ++roots;
-          chi = r.sign;
-          if (r.tang || r.graze) fl |= FLAG_RESHOOT;
-          if (r.onsurf) fl |= FLAG_ONSURF;
-          if (w.rec) {
-            const unsigned long long k = atomicAdd(w.rec_count, 1ull);
-            if (k < w.rec_cap) w.rec[k] = HitRec{slot, r.sign, r.t};
-            else atomicOr(&w.flags[slot], FLAG_RESHOOT);
-          }
-        }
-      }
+      newton_accept(w, it.slot, it.patch, it.code, it.u, it.v, it.qa, it.qb, it.qc, chi, fl,
+                    iters, roots);
     }
     // segmented warp-shuffle reduction keyed by query slot, one atomic per run
     const bool tail = seg_reduce(slot, chi, fl);
@@ -346,31 +445,41 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
                              const int32_t* pair_leaf, const unsigned long long* npairs_dev,
                              int64_t pair_cap, const double* qproj, int32_t* chi,
                              int32_t* flags, unsigned long long* counters, void* scratch,
-                             cudaEvent_t* ev4, unsigned long long* items_out, cudaEvent_t* join,
+                             unsigned long long* k3cnt, cudaEvent_t* ev4,
+                             unsigned long long* items_out, cudaEvent_t* join,
                              const RecordSink* rec, cudaStream_t st) {
   static thread_local int g_cand = 0, g_fb = 0, g_newton = 0, g_dev = -1;
   if (g_dev != sc->device) {
     g_cand = grid_for((const void*)k3_candidates, sc->sm_count);
-    g_fb = grid_for((const void*)k3_fallback, sc->sm_count, 32 * kFbWarps);
-    g_newton = grid_for((const void*)k3_newton, sc->sm_count);
+    // the fallback holds few, long-lived warps: one block per SM leaves room
+    // for the concurrent Newton pass (GWN_FB_BPS overrides, for experiments)
+    const char* e_bps = getenv("GWN_FB_BPS");
+    const int bps = e_bps ? atoi(e_bps) : 1;
+    g_fb = bps > 0 ? sc->sm_count * bps : grid_for((const void*)k3_fallback, sc->sm_count, 32 * kFbWarps);
+    // Newton leaves one SM slot per block of the concurrent fallback kernel
+    // (GWN_NEWTON_BPS overrides, for experiments; 0 = full occupancy)
+    const char* e_nb = getenv("GWN_NEWTON_BPS");
+    const int nbps = e_nb ? atoi(e_nb) : 2;
+    const int full = grid_for((const void*)k3_newton, sc->sm_count);
+    g_newton = nbps > 0 && sc->sm_count * nbps < full ? sc->sm_count * nbps : full;
     g_dev = sc->device;
   }
   // scratch layout (intersect_scratch_bytes): fallback queue, Newton queue,
-  // pair -> patch, 4 counters
+  // pair -> patch (the round counters come in k3cnt)
   char* p = (char*)scratch;
   NodeItem* fq = (NodeItem*)p;
   p += sizeof(NodeItem) * pair_cap;
   NewtonItem* nq = (NewtonItem*)p;
   p += sizeof(NewtonItem) * pair_cap;
   int32_t* pp = (int32_t*)p;
-  p += sizeof(int32_t) * ((pair_cap + 3) & ~3ll);
-  unsigned long long* cnt = (unsigned long long*)p;  // [0] fallback, [1] newton, [2] ovf
-  cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * 4, st);
-  if (e != cudaSuccess) return e;
+  unsigned long long* cnt = k3cnt;  // [0] fallback, [1] newton, [2] ovf, [3] newton work
+  cudaError_t e = cudaSuccess;
   WaveArgs w{pair_slot, pp, qproj, rd.proj, sc->dprm, chi, flags,
              rec ? rec->rec : nullptr, rec ? rec->count : nullptr, rec ? rec->cap : 0ull,
-             counters, (int*)(cnt + 2), nq, cnt + 1, (unsigned long long)pair_cap};
+             counters, (int*)(cnt + 2), nq, cnt + 1, (unsigned long long)pair_cap, cnt + 3,
+             rd.sub_offs, rd.sub, rd.subbox, rd.subskip, rd.sub_level};
   if (ev4) cudaEventRecord(ev4[0], st);
+  tl_mark(st, "k3 start");
   k3_candidates<<<g_cand, 128, 0, st>>>(npairs_dev, pair_leaf, rd.leaves, fq, cnt,
                                         (unsigned long long)pair_cap, w);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -380,7 +489,14 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
   static thread_local cudaStream_t side = nullptr;
   static thread_local cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   if (!side) {
-    if ((e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    // high priority: the fallback's blocks are dispatched ahead of the Newton
+    // pass's, so its long dependent chains start first (GWN_FB_PRIO=0: off)
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    const char* e_pr = getenv("GWN_FB_PRIO");
+    const int prio = (e_pr && atoi(e_pr) == 0) ? lo_prio : hi_prio;
+    if ((e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, prio)) != cudaSuccess)
+      return e;
     if ((e = cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming)) != cudaSuccess) return e;
   }
@@ -392,7 +508,9 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
     if ((e = cudaStreamWaitEvent(side, fork_ev, 0)) != cudaSuccess) return e;
   }
   if (ev4) cudaEventRecord(ev4[1], fs);
+  tl_mark(fs, "fb start");
   k3_fallback<<<g_fb, 32 * kFbWarps, 0, fs>>>(fq, cnt, w);
+  tl_mark(fs, "fb done");
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev4) cudaEventRecord(ev4[2], fs);
   if (!ev4) {
@@ -400,10 +518,12 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
     *join = join_ev;
   }
   if (ev4) cudaEventRecord(ev4[4], st);
+  tl_mark(st, "newton start");
   k3_newton<<<g_newton, 128, 0, st>>>(w);
+  tl_mark(st, "newton done");
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev4) cudaEventRecord(ev4[3], st);
-  if (items_out)  // [0] fallback items, [1] newton items
+  if (items_out && items_out != cnt)  // [0] fallback items, [1] newton items
     e = cudaMemcpyAsync(items_out, cnt, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToDevice,
                         st);
   return e;
@@ -411,7 +531,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
 
 size_t intersect_scratch_bytes(int64_t pair_cap) {
   return sizeof(NodeItem) * pair_cap + sizeof(NewtonItem) * pair_cap +
-         sizeof(int32_t) * ((pair_cap + 3) & ~3ll) + sizeof(unsigned long long) * 4;
+         sizeof(int32_t) * ((pair_cap + 3) & ~3ll);
 }
 
 }  // namespace gwn

@@ -23,6 +23,7 @@ for arg in sys.argv[1:] or ["2"]:
     stt = sc.stats()
     print(f"cfg{cfg} Q={len(q)} P={sc.n_patches} segs={sc.n_net_segments}: {dt*1e3:.3f} ms/eval "
           f"({len(q)/dt/1e6:.1f} Mq/s) stages cull={stt['ms_cull']:.3f} int={stt['ms_intersect']:.3f} "
-          f"bnd={stt['ms_boundary']:.3f} fin={stt['ms_other']:.3f} | cand={stt['candidates']} "
+          f"bnd={stt['ms_boundary']:.3f} fin={stt['ms_other']:.3f} [k3 cand={stt['ms_k3_candidates']:.3f} "
+          f"fb={stt['ms_k3_fallback']:.3f} ({stt['k3_fallback_items']} items) newton={stt['ms_k3_newton']:.3f}] | cand={stt['candidates']} "
           f"nodes={stt['nodes']} newton={stt['newton_iters']} roots={stt['roots']} retried={stt['retried']} "
           f"status={np.unique(st.cpu().numpy(), return_counts=True)}", flush=True)
