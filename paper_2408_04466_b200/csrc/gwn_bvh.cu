@@ -456,16 +456,26 @@ __device__ __forceinline__ void leaf_cells(const double* b, double gx0, double g
 template <bool kFill>
 __global__ void k_grid_bin(const double* __restrict__ leafbox, int64_t n, double gx0, double gy0,
                            double gia, double gib, int ga, int gb, int32_t* __restrict__ cnt,
-                           const int32_t* __restrict__ offs, int32_t* __restrict__ cells) {
+                           const int32_t* __restrict__ offs, CellEnt* __restrict__ cells) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const double* b = leafbox + 5 * i;
   int i0, i1, j0, j1;
-  leaf_cells(leafbox + 5 * i, gx0, gy0, gia, gib, ga, gb, i0, i1, j0, j1);
+  leaf_cells(b, gx0, gy0, gia, gib, ga, gb, i0, i1, j0, j1);
+  CellEnt ent;
+  if (kFill) {  // rounded outward: the float test is a superset of the double one
+    ent.alo = __double2float_rd(b[0]);
+    ent.ahi = __double2float_ru(b[1]);
+    ent.blo = __double2float_rd(b[2]);
+    ent.bhi = __double2float_ru(b[3]);
+    ent.cmax = __double2float_ru(b[4]);
+    ent.leaf = (int32_t)i;
+  }
   for (int j = j0; j <= j1; ++j)
     for (int ii = i0; ii <= i1; ++ii) {
       const int c = j * ga + ii;
       const int k = atomicAdd(&cnt[c], 1);
-      if (kFill) cells[offs[c] + k] = (int32_t)i;
+      if (kFill) cells[offs[c] + k] = ent;
     }
 }
 
@@ -525,10 +535,10 @@ static cudaError_t build_grid(Round& rd, double amin, double amax, double bmin, 
       goto out;
     }
     rd.grid_entries = total;
-    GC(cudaMalloc(&rd.cell_leaves, sizeof(int32_t) * ((size_t)total + 1)));
+    GC(cudaMalloc(&rd.cell_ent, sizeof(CellEnt) * ((size_t)total + 1)));
     GC(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (ncell + 1), st));
     k_grid_bin<true><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
-        rd.leafbox, n, rd.gx0, rd.gy0, rd.gia, rd.gib, ga, gb, cnt, rd.cell_offs, rd.cell_leaves);
+        rd.leafbox, n, rd.gx0, rd.gy0, rd.gia, rd.gib, ga, gb, cnt, rd.cell_offs, rd.cell_ent);
     GC(cudaGetLastError());
     GC(cudaStreamSynchronize(st));
     rd.use_grid = true;
@@ -614,7 +624,7 @@ void free_round(Round& rd) {
   if (rd.leaves) cudaFree(rd.leaves);
   if (rd.vproj) cudaFree(rd.vproj);
   if (rd.cell_offs) cudaFree(rd.cell_offs);
-  if (rd.cell_leaves) cudaFree(rd.cell_leaves);
+  if (rd.cell_ent) cudaFree(rd.cell_ent);
   rd = Round();
 }
 

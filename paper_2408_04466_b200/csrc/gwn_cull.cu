@@ -1,18 +1,22 @@
-// gwn_cull.cu -- K2: query x leaf cull by 2-D LBVH traversal in the ray frame
-// of the round.
+// gwn_cull.cu -- K2: query x leaf cull in the ray frame of the round.
 //
 // Replaces the reference's per-(ray, patch) `patch.aabb()` + ray_aabb_clip
 // (surfaces.py:636-639, geometry.py:198-219): with every ray of the round
 // parallel to d, a leaf sub-patch can be hit only if the query's projection
 // (p.e1, p.e2) lies in the leaf's projected control box and the leaf reaches
-// past p along d (cmax >= p.d).  One pass: each thread collects its leaves in
-// a small register buffer, then the warp reserves space for all lanes with a
-// single atomic (warp prefix sum), so the (slot, leaf) candidates of a query
-// are contiguous.  Queries with more than kLBuf candidates append the rest
-// one by one (the segmented reduction downstream does not need sorted keys).
-// The kernel always counts every candidate; if the buffer capacity was too
-// small the engine re-runs the round with the exact size.
-#include "gwn_internal.h"
+// past p along d (cmax >= p.d).  Point location is a uniform grid of packed
+// float boxes (rounded outward, so the float test keeps every true
+// candidate), or the LBVH when the grid would not stay compact.
+//
+// One pass: each thread collects its leaves in a small register buffer, then
+// the warp reserves space for all lanes with a single atomic (warp prefix
+// sum), so the (slot, leaf) candidates of a query are contiguous; queries
+// with more than kLBuf candidates append the rest one by one.  The kernel
+// counts every candidate; if the round's capacity was too small the engine
+// re-runs the round with the exact size.  (Fusing the candidate test into
+// this kernel was measured slower: its registers cut the occupancy the
+// latency-bound cell walk needs.)
+#include "gwn_k3.cuh"
 
 namespace gwn {
 
@@ -29,27 +33,27 @@ __device__ __forceinline__ void query_proj(const Frame& f, const double* __restr
 
 struct GridView {
   const int32_t* offs;
-  const int32_t* leaves;
+  const CellEnt* ent;
   int32_t na, nb;
   double x0, y0, ia, ib;
 };
 
 __global__ void __launch_bounds__(128)
 k_cull(const Node* __restrict__ nodes, const double* __restrict__ leafbox, int64_t n_leaves,
-       GridView grid, Frame f, int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
-       double* __restrict__ qproj, int32_t* __restrict__ pair_slot,
-       int32_t* __restrict__ pair_leaf, unsigned long long* __restrict__ pair_count,
+       GridView grid, Frame f, int32_t m, const int32_t* __restrict__ active,
+       const double* __restrict__ pos, double* __restrict__ qproj,
+       int2* __restrict__ pairs, unsigned long long* __restrict__ pair_count,
        unsigned long long cap, CullZero z) {
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = s < m;
   int buf[kLBuf];
   int n = 0;
+  double qa = 0.0, qb = 0.0, qc = 0.0;
   if (live) {
     // the round's per-slot accumulators start at zero (K3/K4 run after K2)
     if (z.chi) z.chi[s] = 0;
     if (z.flags) z.flags[s] = 0;
     const int32_t q = active ? active[s] : s;
-    double qa, qb, qc;
     query_proj(f, pos, q, qa, qb, qc);
     qproj[3 * (int64_t)s] = qa;
     qproj[3 * (int64_t)s + 1] = qb;
@@ -58,25 +62,24 @@ k_cull(const Node* __restrict__ nodes, const double* __restrict__ leafbox, int64
       if (n < kLBuf) {
         buf[n++] = leaf;
       } else {  // spill: rare, append individually
-        unsigned long long k = atomicAdd(pair_count, 1ull);
-        if (k < cap) {
-          pair_slot[k] = s;
-          pair_leaf[k] = leaf;
-        }
+        const unsigned long long k = atomicAdd(pair_count, 1ull);
+        if (k < cap) pairs[k] = make_int2(s, leaf);
       }
     };
     if (grid.offs) {
-      // uniform grid: one cell, a short list of leaf boxes
+      // uniform grid: one cell, a short list of packed float boxes
       const double fa = (qa - grid.x0) * grid.ia, fb = (qb - grid.y0) * grid.ib;
       if (fa >= 0.0 && fb >= 0.0 && fa < (double)grid.na && fb < (double)grid.nb) {
         const int c = (int)fb * grid.na + (int)fa;
         const int k1 = __ldg(grid.offs + c + 1);
+        // float compares on the rounded query are a superset of the double
+        // test: qa >= lo implies fl(qa) >= fl(lo) >= lo rounded down
+        const float fqa = (float)qa, fqb = (float)qb, fqc = (float)qc;
         for (int k = __ldg(grid.offs + c); k < k1; ++k) {
-          const int leaf = __ldg(grid.leaves + k);
-          const double* b = leafbox + 5 * (int64_t)leaf;
-          if (qa >= __ldg(b) && qa <= __ldg(b + 1) && qb >= __ldg(b + 2) && qb <= __ldg(b + 3) &&
-              __ldg(b + 4) >= qc)
-            emit(leaf);
+          const float2* e = reinterpret_cast<const float2*>(grid.ent + k);
+          const float2 e0 = __ldg(e), e1 = __ldg(e + 1), e2 = __ldg(e + 2);
+          if (fqa >= e0.x && fqa <= e0.y && fqb >= e1.x && fqb <= e1.y && e2.x >= fqc)
+            emit(__float_as_int(e2.y));
         }
       }
     } else if (n_leaves == 1) {
@@ -118,24 +121,21 @@ k_cull(const Node* __restrict__ nodes, const double* __restrict__ leafbox, int64
   if (lane == 31 && total) base = atomicAdd(pair_count, (unsigned long long)total);
   base = __shfl_sync(0xffffffffu, base, 31);
   const unsigned long long o0 = base + (unsigned long long)(incl - n);
-  for (int k = 0; k < n; ++k) {
-    if (o0 + k < cap) {
-      pair_slot[o0 + k] = s;
-      pair_leaf[o0 + k] = buf[k];
-    }
-  }
+  for (int k = 0; k < n; ++k)
+    if (o0 + k < cap) pairs[o0 + k] = make_int2(s, buf[k]);
 }
 
 cudaError_t launch_cull(const gwn_scene* sc, const Round& rd, int32_t m, const int32_t* active,
-                        const double* pos, double* qproj, int32_t* pair_slot, int32_t* pair_leaf,
-                        unsigned long long* pair_count, int64_t cap, cudaStream_t st,
-                        CullZero z) {
+                        const double* pos, double* qproj, unsigned long long* pair_count,
+                        int64_t cap, CullZero z, const K3Queues& Q, unsigned long long* counters,
+                        cudaStream_t st) {
   (void)sc;
+  (void)counters;
   if (m <= 0) return cudaSuccess;
-  GridView g{rd.use_grid ? rd.cell_offs : nullptr, rd.cell_leaves, rd.ga, rd.gb,
-              rd.gx0, rd.gy0, rd.gia, rd.gib};
+  GridView g{rd.use_grid ? rd.cell_offs : nullptr, rd.cell_ent, rd.ga, rd.gb,
+             rd.gx0, rd.gy0, rd.gia, rd.gib};
   k_cull<<<(m + 127) / 128, 128, 0, st>>>(rd.nodes, rd.leafbox, rd.n_leaves, g, rd.f, m, active,
-                                          pos, qproj, pair_slot, pair_leaf, pair_count,
+                                          pos, qproj, Q.pairs, pair_count,
                                           (unsigned long long)cap, z);
   return cudaGetLastError();
 }

@@ -18,6 +18,7 @@
 #include <chrono>
 
 #include "gwn_internal.h"
+#include "gwn_k3.cuh"
 
 namespace gwn {
 
@@ -244,9 +245,7 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     const bool sort_q = sc->P > 0 && cm >= 65536 && getenv("GWN_QUERY_ORDER");
     void* order_tmp = sort_q ? ws.get<char>(query_order_scratch_bytes((int32_t)cm)) : nullptr;
     int64_t pair_cap = 0;
-    int32_t* pair_slot = nullptr;
-    int32_t* pair_leaf = nullptr;
-    void* k3_scratch = nullptr;
+    void* k3_scratch = nullptr;  // K3 queues (fallback + Newton items)
     CKE(ws.err);
     for (int64_t c0 = 0; c0 < n; c0 += cm) {
       const int32_t mc = (int32_t)((n - c0) < cm ? (n - c0) : cm);
@@ -268,16 +267,12 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         // candidate capacity from the scene's running estimate
         int64_t want = (int64_t)(sc->pairs_per_query * 1.25 * m) + 4096;
         if (want > pair_cap) {
-          if (pair_slot) CKE(cudaFreeAsync(pair_slot, st));
-          if (pair_leaf) CKE(cudaFreeAsync(pair_leaf, st));
           if (k3_scratch) CKE(cudaFreeAsync(k3_scratch, st));
-          pair_slot = pair_leaf = nullptr;
           k3_scratch = nullptr;
           pair_cap = want;
-          CKE(cudaMallocAsync(&pair_slot, sizeof(int32_t) * pair_cap, st));
-          CKE(cudaMallocAsync(&pair_leaf, sizeof(int32_t) * pair_cap, st));
           CKE(cudaMallocAsync(&k3_scratch, intersect_scratch_bytes(pair_cap), st));
         }
+        const K3Queues Q = k3_queues(k3_scratch, pair_cap, k3cnt);
         tr.mark("round setup");
         tl_mark(st, "round setup done");
         if (sc->timed) CKE(cudaEventRecord(ev[0], st));
@@ -288,13 +283,12 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         } else {
           CKE(cudaMemsetAsync(rsc, 0, sizeof(unsigned long long) * 8, st));
         }
-        // ---- K2: cull (one pass, warp-aggregated appends)
+        // ---- K2: cull -> (query, leaf) candidates
         if (sc->P > 0) {
           CullZero z;
           z.chi = chi;
           z.flags = fl;
-          CKE(launch_cull(sc, rd, m, active, rpos, qproj, pair_slot, pair_leaf, rsc, pair_cap, st,
-                          z));
+          CKE(launch_cull(sc, rd, m, active, rpos, qproj, rsc, pair_cap, z, Q, d_cnt, st));
           ++launches;
         }
         tr.mark("cull launched");
@@ -307,9 +301,8 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         }
         cudaEvent_t join = nullptr;
         if (sc->P > 0) {
-          CKE(launch_intersect(sc, rd, pair_slot, pair_leaf, rsc, pair_cap, qproj, chi, fl, d_cnt,
-                               k3_scratch, k3cnt, sc->timed ? ev4 : nullptr, k3cnt, &join, nullptr,
-                               st));
+          CKE(launch_intersect(sc, rd, Q, rsc, qproj, chi, fl, d_cnt, k3cnt + 3,
+                               sc->timed ? ev4 : nullptr, &join, nullptr, st));
           launches += 3;
         }
         tr.mark("k3 launched");
@@ -379,8 +372,6 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         ++r;
       }
     }
-    if (pair_slot) cudaFreeAsync(pair_slot, st);
-    if (pair_leaf) cudaFreeAsync(pair_leaf, st);
     if (k3_scratch) cudaFreeAsync(k3_scratch, st);
   }
   if (host) {

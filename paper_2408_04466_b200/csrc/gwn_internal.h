@@ -75,6 +75,12 @@ struct alignas(16) Node {
 
 struct LeafRec;
 
+// packed uniform-grid entry: a leaf's cull box rounded outward to float
+struct CellEnt {
+  float alo, ahi, blo, bhi, cmax;
+  int32_t leaf;
+};
+
 struct Round {
   Frame f;
   double* proj = nullptr;      // (P,48)
@@ -90,7 +96,7 @@ struct Round {
   int32_t ga = 0, gb = 0;      // cells along a, b
   double gx0 = 0, gy0 = 0, gia = 0, gib = 0;  // origin and inverse cell size
   int32_t* cell_offs = nullptr;    // (ga*gb+1) exclusive offsets
-  int32_t* cell_leaves = nullptr;  // leaf ids per cell
+  CellEnt* cell_ent = nullptr;     // packed leaf boxes per cell
   int64_t grid_entries = 0;
   // fold trees of the uncertified leaves (k_foldtree): the tree of leaf i
   // is nodes [sub_offs[i], sub_offs[i+1]) in preorder, node k's subtree is
@@ -160,6 +166,8 @@ inline void tl_mark(cudaStream_t s, const char* nm) {
   if (g_tl) g_tl->mark(s, nm);
 }
 
+struct K3Queues;  // gwn_k3.cuh
+
 // per-slot accumulators the cull kernel zeroes for its round (nullable)
 struct CullZero {
   int32_t* chi = nullptr;
@@ -171,19 +179,19 @@ cudaError_t build_round(gwn_scene* sc, int r, cudaStream_t st);            // gw
 cudaError_t build_round_dir(gwn_scene* sc, const double d[3], Round& rd, cudaStream_t st);
 void free_round(Round& rd);
 cudaError_t launch_cull(const gwn_scene* sc, const Round& rd, int32_t m, const int32_t* active,
-                        const double* pos, double* qproj, int32_t* pair_slot, int32_t* pair_leaf,
-                        unsigned long long* pair_count, int64_t cap,
-                        cudaStream_t st,
-                        CullZero z = CullZero{});                                     // gwn_cull.cu
-cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t* pair_slot,
-                             const int32_t* pair_leaf, const unsigned long long* npairs_dev,
-                             int64_t pair_cap, const double* qproj, int32_t* chi,
-                             int32_t* flags, unsigned long long* counters, void* scratch,
-                             unsigned long long* k3cnt, cudaEvent_t* ev4,
-                             unsigned long long* items_out, cudaEvent_t* join,
-                             const RecordSink* rec, cudaStream_t st);         // gwn_wavefront.cu
-// k3cnt: 4 zeroed device counters per round ([0] fallback items, [1] Newton
-// items, [2] overflow, [3] Newton work); items_out may alias k3cnt
+                        const double* pos, double* qproj, unsigned long long* pair_count,
+                        int64_t cap, CullZero z, const K3Queues& Q, unsigned long long* counters,
+                        cudaStream_t st);  // gwn_cull.cu: K2 -> Q.pairs                                     // gwn_cull.cu
+cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queues& Q,
+                             const unsigned long long* npairs_dev, const double* qproj,
+                             int32_t* chi, int32_t* flags, unsigned long long* counters,
+                             unsigned long long* newton_work, cudaEvent_t* ev4,
+                             cudaEvent_t* join, const RecordSink* rec,
+                             cudaStream_t st);  // gwn_wavefront.cu: candidates, fallback, Newton
+// K3 queues in `scratch` (intersect_scratch_bytes(cap)); k3cnt: 4 zeroed
+// device counters per round ([0] fallback items, [1] Newton items,
+// [2] overflow, [3] Newton work)
+K3Queues k3_queues(void* scratch, int64_t cap, unsigned long long* k3cnt);
 size_t intersect_scratch_bytes(int64_t pair_cap);
 cudaError_t launch_query_order(const Round& rd, int32_t m, const double* pos, void* scratch,
                                int32_t* perm, cudaStream_t st);               // gwn_bvh.cu

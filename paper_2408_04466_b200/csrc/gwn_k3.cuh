@@ -1,0 +1,101 @@
+// gwn_k3.cuh -- K3 work items and the per-candidate leaf test, shared by
+// the fused cull (gwn_cull.cu, K2 + K3 pass 0) and the K3 passes
+// (gwn_wavefront.cu).
+#pragma once
+
+#include "gwn_dfs.cuh"
+
+namespace gwn {
+
+struct NodeItem {
+  int32_t slot;   // query slot of the round
+  int32_t leaf;   // round leaf index (patch, fold tree)
+  uint64_t code;  // level:6 | iu:29 | iv:29
+};
+
+// Self-contained Newton work item (one coalesced 64-byte load): the query
+// slot, the patch, the leaf code for ownership, the certified start and the
+// query's ray-frame projection.
+struct alignas(16) NewtonItem {
+  int32_t slot;
+  int32_t patch;
+  uint64_t code;
+  double u, v;
+  double qa, qb, qc;
+  double pad;
+};
+
+
+// warp-aggregated append: returns the slot or -1 if over capacity
+__device__ __forceinline__ long long warp_push(bool want, unsigned long long* counter,
+                                               unsigned long long cap, int* overflow) {
+  unsigned mask = __ballot_sync(0xffffffffu, want);
+  if (!mask) return -1;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(mask) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (!want) return -1;
+  unsigned long long idx = base + __popc(mask & ((1u << lane) - 1));
+  if (idx >= cap) {
+    *overflow = 1;
+    return -1;
+  }
+  return (long long)idx;
+}
+
+__device__ __forceinline__ void warp_sum_u64(unsigned long long* dst, unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+// Candidate test of query (qa, qb) against a leaf / sub-leaf record:
+// 0 exclude, 1 certified root (Newton start nu, nv), 2 undecided.
+__device__ __forceinline__ int leaf_test(const LeafRec& L, double qa, double qb,
+                                         const DevParams& prm, double& nu, double& nv) {
+  const double span = 1.0 + 2.0 * kLeafM;
+  const double tl = kLeafM / span, th = (1.0 + kLeafM) / span;
+  const int lev = code_level(L.code);
+  const double wu = code_wu(lev), wv = code_wv(lev);
+  const double u0 = (double)code_iu(L.code) * wu, v0 = (double)code_iv(L.code) * wv;
+  const double tol = prm.domain_tol;
+  const double xlo_u = tl - (u0 == 0.0 ? tol / (wu * span) : 0.0);
+  const double xhi_u = th + (u0 + wu == 1.0 ? tol / (wu * span) : 0.0);
+  const double xlo_v = tl - (v0 == 0.0 ? tol / (wv * span) : 0.0);
+  const double xhi_v = th + (v0 + wv == 1.0 ? tol / (wv * span) : 0.0);
+  KrawPre k;
+  k.Ga = L.Ga; k.Gb = L.Gb;
+  k.Y00 = L.Y00; k.Y01 = L.Y01; k.Y10 = L.Y10; k.Y11 = L.Y11;
+  k.R0 = L.R0; k.R1 = L.R1;
+  k.ok = L.ok != 0;
+  double s0, s1;
+  int kr = kraw_query(k, L.Ga - qa, L.Gb - qb, xlo_u, xhi_u, xlo_v, xhi_v, -1e-7, 1.0 + 1e-7,
+                      s0, s1);
+  if (kr == 2) {  // separating axes of the leaf hull (rigorous exclusion)
+    const double p1 = L.n1a * qa + L.n1b * qb, p2 = L.n2a * qa + L.n2b * qb;
+    if (p1 < L.lo1 || p1 > L.hi1 || p2 < L.lo2 || p2 > L.hi2) kr = 0;
+  }
+  if (kr == 1) {
+    nu = u0 - kLeafM * wu + s0 * span * wu;
+    nv = v0 - kLeafM * wv + s1 * span * wv;
+  }
+  return kr;
+}
+
+// K3 queues: the cull's (query, leaf) candidates; after the candidate test
+// the undecided ones for the subdivision fallback, certified ones for the
+// Newton pass.  Each candidate yields at most one item, so every queue has
+// cap = the candidate capacity of the round.
+struct K3Queues {
+  int2* pairs;  // (query slot, leaf) candidates from the cull
+  NodeItem* fq;
+  unsigned long long* f_count;
+  NewtonItem* nq;
+  unsigned long long* n_count;
+  unsigned long long cap;
+  int* overflow;
+};
+
+}  // namespace gwn

@@ -21,6 +21,7 @@
 #include <string.h>
 
 #include "gwn_internal.h"
+#include "gwn_k3.cuh"
 
 namespace gwn {
 
@@ -245,20 +246,20 @@ extern "C" int gwn_eval_rays(gwn_scene* sc, const double* origins, int64_t R,
       HitRec* rec = nullptr;
       for (;;) {
         std::vector<void*> rb;
-        int32_t* ps = dalloc<int32_t>(rb, pair_cap, st, ae);
-        int32_t* pl = dalloc<int32_t>(rb, pair_cap, st, ae);
         void* scratch = dalloc<char>(rb, intersect_scratch_bytes(pair_cap), st, ae);
         const int64_t rcap = 2 * pair_cap + 1024;
         rec = dalloc<HitRec>(bufs, rcap, st, ae);
         CKR(ae);
         CKR(cudaMemsetAsync(rsc, 0, sizeof(unsigned long long) * 12, st));
-        CKR(cudaMemsetAsync(rchi, 0, sizeof(int32_t) * R, st));
-        CKR(cudaMemsetAsync(rfl, 0, sizeof(int32_t) * R, st));
-        CKR(launch_cull(sc, *rd, m, nullptr, rpos, qproj, ps, pl, rsc, pair_cap, st));
+        const K3Queues Q = k3_queues(scratch, pair_cap, rsc + 8);
+        CullZero z;
+        z.chi = rchi;
+        z.flags = rfl;
+        CKR(launch_cull(sc, *rd, m, nullptr, rpos, qproj, rsc, pair_cap, z, Q, cnt, st));
         RecordSink sink{rec, rsc + 4, (unsigned long long)rcap};
         cudaEvent_t join = nullptr;
-        CKR(launch_intersect(sc, *rd, ps, pl, rsc, pair_cap, qproj, rchi, rfl, cnt, scratch,
-                             rsc + 8, nullptr, rsc + 8, &join, &sink, st));
+        CKR(launch_intersect(sc, *rd, Q, rsc, qproj, rchi, rfl, cnt, rsc + 11, nullptr, &join,
+                             &sink, st));
         if (join) CKR(cudaStreamWaitEvent(st, join, 0));
         unsigned long long h[8];
         CKR(cudaMemcpyAsync(h, rsc, sizeof h, cudaMemcpyDeviceToHost, st));

@@ -16,57 +16,12 @@
 // the node whose half-open parameter box contains it (the domain edge nodes
 // own the surfaces.py:668 tolerance band).  Per-query chi / flags are then
 // reduced with a segmented warp-shuffle reduction keyed by query slot.
-#include "gwn_dfs.cuh"
+#include "gwn_k3.cuh"
 
 namespace gwn {
 
-struct NodeItem {
-  int32_t pair;
-  int32_t leaf;   // round leaf index (its fold tree, if any)
-  uint64_t code;  // level:6 | iu:29 | iv:29
-};
-
-// Self-contained Newton work item (one coalesced 64-byte load): the query
-// slot, the patch, the leaf code for ownership, the certified start and the
-// query's ray-frame projection.
-struct alignas(16) NewtonItem {
-  int32_t slot;
-  int32_t patch;
-  uint64_t code;
-  double u, v;
-  double qa, qb, qc;
-  double pad;
-};
-
-
-// warp-aggregated append: returns the slot or -1 if over capacity
-__device__ __forceinline__ long long warp_push(bool want, unsigned long long* counter,
-                                               unsigned long long cap, int* overflow) {
-  unsigned mask = __ballot_sync(0xffffffffu, want);
-  if (!mask) return -1;
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(mask) - 1;
-  unsigned long long base = 0;
-  if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(mask));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (!want) return -1;
-  unsigned long long idx = base + __popc(mask & ((1u << lane) - 1));
-  if (idx >= cap) {
-    *overflow = 1;
-    return -1;
-  }
-  return (long long)idx;
-}
-
-__device__ __forceinline__ void warp_sum_u64(unsigned long long* dst, unsigned long long v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
-}
-
 struct WaveArgs {
-  const int32_t* pair_slot;
-  int32_t* pair_patch;
+  const LeafRec* leaves;  // round leaves (patch of a fallback item)
   const double* qproj;
   const double* proj;
   DevParams prm;
@@ -131,79 +86,41 @@ __device__ __forceinline__ void newton_accept(const WaveArgs& w, int32_t slot, i
   }
 }
 
-// Candidate test of query (qa, qb) against a leaf / sub-leaf record:
-// 0 exclude, 1 certified root (Newton start nu, nv), 2 undecided.
-__device__ __forceinline__ int leaf_test(const LeafRec& L, double qa, double qb,
-                                         const DevParams& prm, double& nu, double& nv) {
-  const double span = 1.0 + 2.0 * kLeafM;
-  const double tl = kLeafM / span, th = (1.0 + kLeafM) / span;
-  const int lev = code_level(L.code);
-  const double wu = code_wu(lev), wv = code_wv(lev);
-  const double u0 = (double)code_iu(L.code) * wu, v0 = (double)code_iv(L.code) * wv;
-  const double tol = prm.domain_tol;
-  const double xlo_u = tl - (u0 == 0.0 ? tol / (wu * span) : 0.0);
-  const double xhi_u = th + (u0 + wu == 1.0 ? tol / (wu * span) : 0.0);
-  const double xlo_v = tl - (v0 == 0.0 ? tol / (wv * span) : 0.0);
-  const double xhi_v = th + (v0 + wv == 1.0 ? tol / (wv * span) : 0.0);
-  KrawPre k;
-  k.Ga = L.Ga; k.Gb = L.Gb;
-  k.Y00 = L.Y00; k.Y01 = L.Y01; k.Y10 = L.Y10; k.Y11 = L.Y11;
-  k.R0 = L.R0; k.R1 = L.R1;
-  k.ok = L.ok != 0;
-  double s0, s1;
-  int kr = kraw_query(k, L.Ga - qa, L.Gb - qb, xlo_u, xhi_u, xlo_v, xhi_v, -1e-7, 1.0 + 1e-7,
-                      s0, s1);
-  if (kr == 2) {  // separating axes of the leaf hull (rigorous exclusion)
-    const double p1 = L.n1a * qa + L.n1b * qb, p2 = L.n2a * qa + L.n2b * qb;
-    if (p1 < L.lo1 || p1 > L.hi1 || p2 < L.lo2 || p2 > L.hi2) kr = 0;
-  }
-  if (kr == 1) {
-    nu = u0 - kLeafM * wu + s0 * span * wu;
-    nv = v0 - kLeafM * wv + s1 * span * wv;
-  }
-  return kr;
-}
-
 // K3 pass 0: one thread per (query, leaf) candidate.  The leaf's Krawczyk
-// data are query-independent (K1), so the test is ~20 flops: exclude,
-// certified (-> Newton item) or undecided (-> node wavefront from the leaf).
+// data are query-independent (K1), so the test is ~40 flops: exclude,
+// certified (-> Newton item) or undecided (-> fallback item).
 __global__ void __launch_bounds__(128)
-k3_candidates(const unsigned long long* __restrict__ npairs_dev,
-              const int32_t* __restrict__ pair_leaf,
-              const LeafRec* __restrict__ leaves, NodeItem* __restrict__ out,
-              unsigned long long* __restrict__ out_count, unsigned long long out_cap, WaveArgs w) {
+k3_candidates(const unsigned long long* __restrict__ npairs_dev, K3Queues Q, WaveArgs w) {
   // on capacity overflow the engine discards and re-runs the round; never
   // read past the buffers
-  const int64_t npairs = (int64_t)min(*npairs_dev, out_cap);
+  const int64_t npairs = (int64_t)min(*npairs_dev, Q.cap);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   unsigned long long tested = 0;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < npairs; base += stride) {
     const int64_t i = base + threadIdx.x;
     bool wantN = false, wantF = false;
-    int32_t pair = (int32_t)i, slot = 0, patch = 0;
+    int32_t slot = 0, patch = 0, leaf = 0;
     uint64_t code = 0;
     double nu_ = 0.0, nv_ = 0.0, qa = 0.0, qb = 0.0, qc = 0.0;
     if (i < npairs) {
-      const LeafRec L = leaves[pair_leaf[i]];
-      w.pair_patch[i] = L.patch;
+      const int2 pr = Q.pairs[i];
+      slot = pr.x;
+      leaf = pr.y;
+      const LeafRec L = w.leaves[leaf];
       patch = L.patch;
       code = L.code;
-      slot = w.pair_slot[i];
       qa = w.qproj[3 * (int64_t)slot];
       qb = w.qproj[3 * (int64_t)slot + 1];
       qc = w.qproj[3 * (int64_t)slot + 2];
       ++tested;
       const int kr = leaf_test(L, qa, qb, w.prm, nu_, nv_);
-      if (kr == 1) {
-        wantN = true;
-      } else if (kr == 2) {
-        wantF = true;
-      }
+      wantN = kr == 1;
+      wantF = kr == 2;
     }
-    long long k = warp_push(wantF, out_count, out_cap, w.overflow);
-    if (k >= 0) out[k] = NodeItem{pair, wantF ? pair_leaf[i] : 0, code};
-    k = warp_push(wantN, w.n_count, w.n_cap, w.overflow);
-    if (k >= 0) w.nq[k] = NewtonItem{slot, patch, code, nu_, nv_, qa, qb, qc, 0.0};
+    long long k = warp_push(wantF, Q.f_count, Q.cap, Q.overflow);
+    if (k >= 0) Q.fq[k] = NodeItem{slot, leaf, code};
+    k = warp_push(wantN, Q.n_count, Q.cap, Q.overflow);
+    if (k >= 0) Q.nq[k] = NewtonItem{slot, patch, code, nu_, nv_, qa, qb, qc, 0.0};
   }
   warp_sum_u64(&w.counters[CNT_NODES], tested);
 }
@@ -245,8 +162,8 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
     __syncwarp();
     if (lane < nb) {
       const NodeItem it = in[b0 + lane];
-      const int32_t slot = w.pair_slot[it.pair];
-      const int32_t patch = w.pair_patch[it.pair];
+      const int32_t slot = it.slot;
+      const int32_t patch = w.leaves[it.leaf].patch;
       const double* q = w.qproj + 3 * (int64_t)slot;
       const NodeCtx c = node_ctx(w.proj + 48 * (int64_t)patch, q[0], q[1], q[2], w.prm);
       iq[wb][lane][0] = c.qa;
@@ -438,16 +355,14 @@ static int grid_for(const void* fn, int sm_count, int block = 128) {
   return sm_count * per_sm;
 }
 
-// K3 driver: three stream-ordered launches, no host synchronisation (each
-// kernel reads its item count from device memory; every queue is sized by
-// the candidate count so none can overflow).
-cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t* pair_slot,
-                             const int32_t* pair_leaf, const unsigned long long* npairs_dev,
-                             int64_t pair_cap, const double* qproj, int32_t* chi,
-                             int32_t* flags, unsigned long long* counters, void* scratch,
-                             unsigned long long* k3cnt, cudaEvent_t* ev4,
-                             unsigned long long* items_out, cudaEvent_t* join,
-                             const RecordSink* rec, cudaStream_t st) {
+// K3 driver: candidate tests, then the fallback on a side stream
+// concurrently with the Newton pass; every kernel reads its queue length
+// from device memory -- no host synchronisation.
+cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queues& Q,
+                             const unsigned long long* npairs_dev, const double* qproj,
+                             int32_t* chi, int32_t* flags, unsigned long long* counters,
+                             unsigned long long* newton_work, cudaEvent_t* ev4,
+                             cudaEvent_t* join, const RecordSink* rec, cudaStream_t st) {
   static thread_local int g_cand = 0, g_fb = 0, g_newton = 0, g_dev = -1;
   if (g_dev != sc->device) {
     g_cand = grid_for((const void*)k3_candidates, sc->sm_count);
@@ -464,24 +379,14 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
     g_newton = nbps > 0 && sc->sm_count * nbps < full ? sc->sm_count * nbps : full;
     g_dev = sc->device;
   }
-  // scratch layout (intersect_scratch_bytes): fallback queue, Newton queue,
-  // pair -> patch (the round counters come in k3cnt)
-  char* p = (char*)scratch;
-  NodeItem* fq = (NodeItem*)p;
-  p += sizeof(NodeItem) * pair_cap;
-  NewtonItem* nq = (NewtonItem*)p;
-  p += sizeof(NewtonItem) * pair_cap;
-  int32_t* pp = (int32_t*)p;
-  unsigned long long* cnt = k3cnt;  // [0] fallback, [1] newton, [2] ovf, [3] newton work
   cudaError_t e = cudaSuccess;
-  WaveArgs w{pair_slot, pp, qproj, rd.proj, sc->dprm, chi, flags,
+  WaveArgs w{rd.leaves, qproj, rd.proj, sc->dprm, chi, flags,
              rec ? rec->rec : nullptr, rec ? rec->count : nullptr, rec ? rec->cap : 0ull,
-             counters, (int*)(cnt + 2), nq, cnt + 1, (unsigned long long)pair_cap, cnt + 3,
+             counters, Q.overflow, Q.nq, Q.n_count, Q.cap, newton_work,
              rd.sub_offs, rd.sub, rd.subbox, rd.subskip, rd.sub_level};
   if (ev4) cudaEventRecord(ev4[0], st);
   tl_mark(st, "k3 start");
-  k3_candidates<<<g_cand, 128, 0, st>>>(npairs_dev, pair_leaf, rd.leaves, fq, cnt,
-                                        (unsigned long long)pair_cap, w);
+  k3_candidates<<<g_cand, 128, 0, st>>>(npairs_dev, Q, w);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // The fallback (few, latency-bound items) runs on a side stream,
   // concurrently with the Newton pass and K4; the engine joins it (`join`)
@@ -509,7 +414,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
   }
   if (ev4) cudaEventRecord(ev4[1], fs);
   tl_mark(fs, "fb start");
-  k3_fallback<<<g_fb, 32 * kFbWarps, 0, fs>>>(fq, cnt, w);
+  k3_fallback<<<g_fb, 32 * kFbWarps, 0, fs>>>(Q.fq, Q.f_count, w);
   tl_mark(fs, "fb done");
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev4) cudaEventRecord(ev4[2], fs);
@@ -523,15 +428,27 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const int32_t
   tl_mark(st, "newton done");
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev4) cudaEventRecord(ev4[3], st);
-  if (items_out && items_out != cnt)  // [0] fallback items, [1] newton items
-    e = cudaMemcpyAsync(items_out, cnt, sizeof(unsigned long long) * 2, cudaMemcpyDeviceToDevice,
-                        st);
   return e;
 }
 
+K3Queues k3_queues(void* scratch, int64_t cap, unsigned long long* k3cnt) {
+  char* p = (char*)scratch;
+  K3Queues q;
+  auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };  // keep every queue aligned
+  q.pairs = (int2*)p;
+  p += up(sizeof(int2) * cap);
+  q.fq = (NodeItem*)p;
+  p += up(sizeof(NodeItem) * cap);
+  q.nq = (NewtonItem*)p;
+  q.f_count = k3cnt;
+  q.n_count = k3cnt + 1;
+  q.overflow = (int*)(k3cnt + 2);
+  q.cap = (unsigned long long)cap;
+  return q;
+}
+
 size_t intersect_scratch_bytes(int64_t pair_cap) {
-  return sizeof(NodeItem) * pair_cap + sizeof(NewtonItem) * pair_cap +
-         sizeof(int32_t) * ((pair_cap + 3) & ~3ll);
+  return (sizeof(int2) + sizeof(NodeItem) + sizeof(NewtonItem)) * pair_cap + 512;
 }
 
 }  // namespace gwn
