@@ -16,6 +16,9 @@ from . import errors as E
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgwn_b200.so")
+# development aid: A/B builds from build.py --variant (build/variants/, git-ignored)
+if os.environ.get("GWN_B200_LIB"):
+    LIB_PATH = os.environ["GWN_B200_LIB"]
 
 GWN_OK = 0
 GWN_E_INVALID = -1

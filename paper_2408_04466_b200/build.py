@@ -51,5 +51,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Development aid: the library with extra -D flags into build/variants/
+    (selected at import with GWN_B200_LIB=<path>); not used by the product."""
+    out = os.path.join(REPO, "build", "variants", f"libgwn_b200_{name}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(REPO, "include"),
+           "-o", out, *sources()]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"nvcc failed building variant {name}")
+    return out
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

@@ -317,7 +317,10 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
 }
 
 // Newton pass over the certified leaves + ownership + K5 part 1.
-__global__ void __launch_bounds__(128) k3_newton(WaveArgs w) {
+#ifndef GWN_NEWTON_MINB
+#define GWN_NEWTON_MINB 1
+#endif
+__global__ void __launch_bounds__(128, GWN_NEWTON_MINB) k3_newton(WaveArgs w) {
   const int64_t n = (int64_t)min(*w.n_count, w.n_cap);
   unsigned long long iters = 0, roots = 0;
   const int lane = threadIdx.x & 31;
@@ -366,15 +369,15 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
   static thread_local int g_cand = 0, g_fb = 0, g_newton = 0, g_dev = -1;
   if (g_dev != sc->device) {
     g_cand = grid_for((const void*)k3_candidates, sc->sm_count);
-    // the fallback holds few, long-lived warps: one block per SM leaves room
-    // for the concurrent Newton pass (GWN_FB_BPS overrides, for experiments)
+    // fallback: 3 blocks per SM spread its few, long-lived items thinly
+    // (measured on config 2 against 1, 2, 4, 6, 8; GWN_FB_BPS overrides)
     const char* e_bps = getenv("GWN_FB_BPS");
-    const int bps = e_bps ? atoi(e_bps) : 1;
+    const int bps = e_bps ? atoi(e_bps) : 3;
     g_fb = bps > 0 ? sc->sm_count * bps : grid_for((const void*)k3_fallback, sc->sm_count, 32 * kFbWarps);
-    // Newton leaves one SM slot per block of the concurrent fallback kernel
-    // (GWN_NEWTON_BPS overrides, for experiments; 0 = full occupancy)
+    // Newton at full occupancy: its dynamic fetch drains the queue, then the
+    // fallback blocks take the SMs (GWN_NEWTON_BPS > 0 caps blocks per SM)
     const char* e_nb = getenv("GWN_NEWTON_BPS");
-    const int nbps = e_nb ? atoi(e_nb) : 2;
+    const int nbps = e_nb ? atoi(e_nb) : 0;
     const int full = grid_for((const void*)k3_newton, sc->sm_count);
     g_newton = nbps > 0 && sc->sm_count * nbps < full ? sc->sm_count * nbps : full;
     g_dev = sc->device;
