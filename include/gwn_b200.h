@@ -16,6 +16,10 @@
  *   gwn_eval_rays      SPEC.md:381-407 winding_numbers_along_ray / slice /
  *                      voxelize: one intersection pass per ray, reused by
  *                      every point on it (ray reuse)
+ *   gwn_solid_angle_many, gwn_ray_tris_hits, gwn_arc_crossings
+ *                      the rest of the kernel dispatch layer
+ *                      (_kernels.py:170, :366, :443, :466): mesh solid
+ *                      angles, ray/mesh all-hits, great-circle arc crossings
  *   gwn_single_loop_batch
  *                      _kernels.single_loop_batch (_kernels.py:801-823): the
  *                      kernel dispatch layer's ray-reuse boundary kernel
@@ -154,6 +158,62 @@ int gwn_single_loop_batch(const double* loop_pts, int64_t B, const double origin
                           const int64_t* hit_signs, int64_t H, const double* query_ts,
                           int64_t K, double on_tol, double t_eps, double* w_out,
                           int8_t* ok_out, int device);
+
+/* ---- the rest of the kernel dispatch layer (pkg/src/gwn/_kernels.py) ----
+ * Host buffers in and out; numpy-twin semantics (the numba kernels share the
+ * broken _cross helper, _kernels.py:45). */
+
+/* solid_angle_many / solid_angle_sum (_kernels.py:443-475): for each point
+ * P[k] the signed solid angle sum_f 2 atan2(num, den) of the triangles
+ * (V (nV,3) f64, T (nT,3) int64) -- NOT divided by 4 pi -- and
+ * on_surface[k] = 1 when P[k] is on (or numerically on) the surface; those
+ * triangles are left out of the sum (:405-411). */
+int gwn_solid_angle_many(const double* V, int64_t nV, const int64_t* T, int64_t nT,
+                         const double* P, int64_t nP, double guard, double* out,
+                         int8_t* on_surface, int device);
+
+/* The reference's Bvh (surfaces.py:74-163, build_bvh): node arrays and the
+ * per-triangle Moller-Trumbore data, all host pointers, C-contiguous. */
+typedef struct gwn_tri_bvh {
+  const double* node_min;     /* (N,3) */
+  const double* node_max;     /* (N,3) */
+  const int64_t* node_left;   /* (N) -1 for leaves */
+  const int64_t* node_right;  /* (N) */
+  const int64_t* node_start;  /* (N) */
+  const int64_t* node_count;  /* (N) */
+  const int64_t* tri_order;   /* (F) */
+  int64_t n_nodes;
+  const double* V0;           /* (F,3) */
+  const double* E1;           /* (F,3) */
+  const double* E2;           /* (F,3) */
+  const double* NN;           /* (F) |e1 x e2| */
+  const double* NH;           /* (F,3) unit normals */
+  const double* C;            /* (F,3) centroids */
+  const double* R2;           /* (F) squared circumradii about the centroid */
+  int64_t n_tris;
+} gwn_tri_bvh;
+
+/* bvh_ray_all_hits (_kernels.py:366-381) for R rays at once: hits of ray r
+ * are [offs[r], offs[r+1]) (offs has R+1 entries, always written), in the
+ * numpy twin's order (regular hits by triangle, then parallel contacts by
+ * triangle; _kernels.py:312-363).  Returns the total hit count; the hit
+ * arrays are written only when total <= cap (call again with cap = total
+ * otherwise).  Negative on error. */
+int64_t gwn_ray_tris_hits(const gwn_tri_bvh* bvh, const double* origins, const double* dirs,
+                          int64_t R, double t_lo, double t_hi, double tang_eps,
+                          double plane_tol, int64_t* offs, double* ts, int64_t* tris,
+                          double* dotdn, double* us, double* vs, int64_t cap, int device);
+
+/* arc_crossings (_kernels.py:170-190, numpy twin :119-167): transversal
+ * crossings between great-circle arcs i < j (chain neighbours skipped),
+ * sorted by (i, j) with the +d crossing before -d; coplanar pairs sorted by
+ * (i, j) into cop_i/cop_j (*n_cop).  Returns the crossing count; outputs
+ * are written only when both counts are <= cap.  Negative on error. */
+int64_t gwn_arc_crossings(const double* S, const double* E, const double* P, const double* L,
+                          const int64_t* prev_idx, const int64_t* next_idx, int64_t B,
+                          double on_tol, double cop_tol, int64_t* pair_i, int64_t* pair_j,
+                          double* points, int64_t* cop_i, int64_t* cop_j, int64_t* n_cop,
+                          int64_t cap, int device);
 
 /* Host-side helpers shared with the oracle contract (no device needed). */
 void gwn_direction(uint64_t seed, int32_t round, double d[3]);

@@ -12,11 +12,12 @@ from .engine import (Scene, combine, direction, fp64_peak, net_boundary, winding
 from .errors import GwnError
 from .geometry import Aabb, Ray
 from .surfaces import BicubicPatch, BoundaryLoop, IntersectionRecord, patch_boundary
+from .mesh import build_bvh, intersect_ray_mesh, mesh_winding_numbers
 
 __all__ = [
     "DEFAULT_EPS", "EpsilonConfig", "Scene", "combine", "direction", "fp64_peak",
     "net_boundary", "winding_number", "winding_numbers", "winding_numbers_along_ray",
     "winding_numbers_rays", "slice", "voxelize",
     "GwnError", "Aabb", "Ray", "BicubicPatch", "BoundaryLoop", "IntersectionRecord",
-    "patch_boundary",
+    "patch_boundary", "build_bvh", "intersect_ray_mesh", "mesh_winding_numbers",
 ]

@@ -33,6 +33,7 @@ EXPORTS = (
     "gwn_scene_destroy", "gwn_scene_info_get", "gwn_eval", "gwn_stats_get", "gwn_set_timing",
     "gwn_all_hits", "gwn_single_loop_batch", "gwn_direction", "gwn_jitter_dir",
     "gwn_net_boundary", "gwn_fp64_peak", "gwn_selftest_rsqrt", "gwn_eval_rays",
+    "gwn_solid_angle_many", "gwn_ray_tris_hits", "gwn_arc_crossings",
 )
 
 
@@ -44,6 +45,17 @@ class GwnParams(C.Structure):
         ("band_factor", C.c_double), ("samples_per_edge", C.c_int32), ("max_rounds", C.c_int32),
         ("max_jitters", C.c_int32), ("chunk_queries", C.c_int32), ("dir_seed", C.c_uint64),
     ]
+
+
+class TriBvh(C.Structure):
+    """gwn_tri_bvh (include/gwn_b200.h): the reference's Bvh arrays."""
+    _fields_ = [("node_min", C.c_void_p), ("node_max", C.c_void_p),
+                ("node_left", C.c_void_p), ("node_right", C.c_void_p),
+                ("node_start", C.c_void_p), ("node_count", C.c_void_p),
+                ("tri_order", C.c_void_p), ("n_nodes", C.c_int64),
+                ("V0", C.c_void_p), ("E1", C.c_void_p), ("E2", C.c_void_p),
+                ("NN", C.c_void_p), ("NH", C.c_void_p), ("C", C.c_void_p),
+                ("R2", C.c_void_p), ("n_tris", C.c_int64)]
 
 
 class SceneInfo(C.Structure):
@@ -113,6 +125,16 @@ def lib() -> C.CDLL:
         L.gwn_net_boundary.restype = C.c_int64
         L.gwn_fp64_peak.argtypes = [C.c_int, dp, dp]
         L.gwn_selftest_rsqrt.argtypes = [C.c_int, C.c_int64, C.POINTER(C.c_uint64)]
+        ip = C.POINTER(C.c_int64)
+        L.gwn_solid_angle_many.argtypes = [dp, C.c_int64, ip, C.c_int64, dp, C.c_int64,
+                                           C.c_double, dp, C.POINTER(C.c_int8), C.c_int]
+        L.gwn_ray_tris_hits.argtypes = [C.POINTER(TriBvh), dp, dp, C.c_int64, C.c_double,
+                                        C.c_double, C.c_double, C.c_double, ip, dp, ip, dp,
+                                        dp, dp, C.c_int64, C.c_int]
+        L.gwn_ray_tris_hits.restype = C.c_int64
+        L.gwn_arc_crossings.argtypes = [dp, dp, dp, dp, ip, ip, C.c_int64, C.c_double,
+                                        C.c_double, ip, ip, dp, ip, ip, ip, C.c_int64, C.c_int]
+        L.gwn_arc_crossings.restype = C.c_int64
         _lib = L
     return _lib
 

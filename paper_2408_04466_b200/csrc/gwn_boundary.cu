@@ -22,54 +22,12 @@
 // staged in shared-memory tiles and read as warp-wide broadcasts.
 #include <algorithm>
 
-#include "gwn_internal.h"
+#include "gwn_fan.cuh"
 
 namespace gwn {
 
 constexpr int kTileV = 2000;   // vertices per shared-memory tile (3 x 2000 x 8 B = 48 KB)
 constexpr int kBlockQ = 256;   // queries (threads) per block
-
-struct SegState {
-  double Zr, Zi;
-  int wraps;
-};
-
-__device__ __forceinline__ bool signbit_hi(double x) { return __double2hiint(x) < 0; }
-
-// multiply Z by (den + i num) with exact branch-cut bookkeeping
-__device__ __forceinline__ void cmul_track(SegState& s, double den, double num) {
-  const double zr = s.Zr * den - s.Zi * num;
-  const double zi = s.Zr * num + s.Zi * den;
-  // arg(Z) + arg(z) crossed +pi (both upper half-planes, result lower) or
-  // -pi (both lower, result upper); sign bits of the high words
-  const unsigned a = (unsigned)__double2hiint(s.Zi), b = (unsigned)__double2hiint(num),
-                 c = (unsigned)__double2hiint(zi);
-  s.wraps += (int)((~a & ~b & c) >> 31) - (int)((a & b & ~c) >> 31);
-  s.Zr = zr;
-  s.Zi = zi;
-}
-
-__device__ __forceinline__ void renorm(SegState& s) {
-  double m = fmax(fabs(s.Zr), fabs(s.Zi));
-  int e = ((__double2hiint(m) >> 20) & 0x7ff);
-  if (e == 0 || e == 0x7ff) return;  // zero/denormal/non-finite: degenerate, flagged elsewhere
-  double sc = __hiloint2double((2046 - e) << 20, 0);  // 2^(1023-e), exact
-  s.Zr *= sc;
-  s.Zi *= sc;
-}
-
-// Full-precision reciprocal square root: MUFU.RSQ64H seed (~2^-22) + one
-// Halley step y(1 + e/2 + 3e^2/8), e = 1 - x y^2 (cubic convergence); no
-// special-value path (x > 0 unless the query sits on a vertex, which the
-// degenerate test flags).  Accuracy checked by gwn_selftest_rsqrt.
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double h = x * y;
-  const double e = fma(-h, y, 1.0);
-  const double p = fma(0.375, e, 0.5);
-  return fma(y * e, p, y);
-}
 
 // Per-vertex quantities of the shifted fan formula in the round's ray frame
 // (e1, e2, d): d = (0,0,1), so u = r/|r| - d = (rx il, ry il, rz il - 1).
