@@ -239,6 +239,24 @@ def config5(n_queries: int | None = None) -> SceneSpec:
     return SceneSpec(5, ctrl, queries, closed=False, meta=meta)
 
 
+def unit_cube(lo=(0.0, 0.0, 0.0), size: float = 1.0) -> np.ndarray:
+    """An axis-aligned cube as 6 flat bicubic patches, outward (f_u x f_v)
+    orientation -- the SPEC examples' watertight cube."""
+    faces = [  # (corner, a, b) with a x b outward
+        ((0, 0, 0), (0, 0, 1), (0, 1, 0)), ((1, 0, 0), (0, 1, 0), (0, 0, 1)),
+        ((0, 0, 0), (1, 0, 0), (0, 0, 1)), ((0, 1, 0), (0, 0, 1), (1, 0, 0)),
+        ((0, 0, 0), (0, 1, 0), (1, 0, 0)), ((0, 0, 1), (1, 0, 0), (0, 1, 0)),
+    ]
+    lo = np.asarray(lo, np.float64)
+    ctrl = np.empty((6, 4, 4, 3))
+    for k, (c, a, b) in enumerate(faces):
+        c, a, b = (np.asarray(x, np.float64) for x in (c, a, b))
+        for i in range(4):
+            for j in range(4):
+                ctrl[k, i, j] = lo + size * (c + (i / 3.0) * a + (j / 3.0) * b)
+    return ctrl
+
+
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
 
 

@@ -23,19 +23,7 @@ TOL = 1e-9  # SPEC.md:385 "results equal pointwise winding_number within 1e-9"
 
 
 def unit_cube() -> np.ndarray:
-    """[0,1]^3 as 6 flat bicubic patches, outward (f_u x f_v) orientation."""
-    faces = [  # (corner, a, b) with a x b outward
-        ((0, 0, 0), (0, 0, 1), (0, 1, 0)), ((1, 0, 0), (0, 1, 0), (0, 0, 1)),
-        ((0, 0, 0), (1, 0, 0), (0, 0, 1)), ((0, 1, 0), (0, 0, 1), (1, 0, 0)),
-        ((0, 0, 0), (0, 1, 0), (1, 0, 0)), ((0, 0, 1), (1, 0, 0), (0, 1, 0)),
-    ]
-    ctrl = np.empty((6, 4, 4, 3))
-    for k, (c, a, b) in enumerate(faces):
-        c, a, b = (np.asarray(x, np.float64) for x in (c, a, b))
-        for i in range(4):
-            for j in range(4):
-                ctrl[k, i, j] = c + (i / 3.0) * a + (j / 3.0) * b
-    return ctrl
+    return scenes.unit_cube()
 
 
 def _random_rays(rng, lo, hi, R, K):
