@@ -20,6 +20,8 @@
 // Per vertex: 3 DADD, |r|^2, rsqrt, 3 DFMA for u, d x u; per segment: 2 dot
 // products + 4 for the complex product.  Boundary vertices (x,y,z) are
 // staged in shared-memory tiles and read as warp-wide broadcasts.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "gwn_fan.cuh"
@@ -234,6 +236,144 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
   }
 }
 
+// Edge-aligned K4 (S <= kTileV): a tile holds whole edges, so every edge's
+// S-1 segments run as blocks of 8 with no per-vertex edge bookkeeping
+// (vertex index mod S, the first-vertex branch, the renorm counter); the
+// vertex carried between segments alternates between two registers.  Same
+// segment order and the same power-of-two renormalisations (exact scalings)
+// as k_boundary, so the partial sums are bit-identical to it.
+template <int QPT>
+__global__ void __launch_bounds__(kBlockQ, 2)
+k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
+             const double* __restrict__ vproj, int64_t V, int S, int64_t n_edges,
+             const double* __restrict__ band_h, Frame f, DevParams prm,
+             double* __restrict__ bpart, int32_t* __restrict__ flag_acc,
+             unsigned long long* __restrict__ counters) {
+  const int nchunk = gridDim.y;
+  const int64_t e0 = n_edges * blockIdx.y / nchunk, e1 = n_edges * (blockIdx.y + 1) / nchunk;
+  const int ept = kTileV / S;  // whole edges per tile
+  __shared__ double sx[kTileV], sy[kTileV], sz[kTileV];
+  int32_t slot[QPT];
+  double qa[QPT], qb[QPT], qc[QPT];
+  SegState st[QPT];
+  int flags[QPT], minhi[QPT], neg[QPT];
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) {
+    slot[j] = blockIdx.x * (blockDim.x * QPT) + j * blockDim.x + threadIdx.x;
+    const bool live = slot[j] < m;
+    const int32_t q = live ? (active ? active[slot[j]] : slot[j]) : 0;
+    const double px = live ? pos[3 * (int64_t)q] : 0.0;
+    const double py = live ? pos[3 * (int64_t)q + 1] : 0.0;
+    const double pz = live ? pos[3 * (int64_t)q + 2] : 0.0;
+    qa[j] = px * f.e1[0] + py * f.e1[1] + pz * f.e1[2];
+    qb[j] = px * f.e2[0] + py * f.e2[1] + pz * f.e2[2];
+    qc[j] = px * f.d[0] + py * f.d[1] + pz * f.d[2];
+    st[j] = SegState{1.0, 0.0, 0};
+    flags[j] = 0;
+    minhi[j] = 0x7fffffff;
+    neg[j] = 0;
+  }
+  VtxF va[QPT], vb[QPT];
+  for (int64_t te = e0; te < e1; te += ept) {
+    const int ne = (int)min((int64_t)ept, e1 - te);
+    const int nt = ne * S;
+    const int64_t t0 = te * S;
+    __syncthreads();
+    for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+      const int64_t g = t0 + k;
+      sx[k] = vproj[g];
+      sy[k] = vproj[V + g];
+      sz[k] = vproj[2 * V + g];
+    }
+    __syncthreads();
+    for (int e = 0; e < ne; ++e) {
+      const int b = e * S;
+#pragma unroll
+      for (int j = 0; j < QPT; ++j)
+        va[j] = make_vtxf(sx[b], sy[b], sz[b], qa[j], qb[j], qc[j], minhi[j]);
+      int k = b + 1;
+      const int kend = b + S;
+      // blocks of 8 segments: va -> vb -> va ..., renorm after each block
+      for (; k + 8 <= kend; k += 8) {
+#pragma unroll
+        for (int h = 0; h < 8; h += 2) {
+#pragma unroll
+          for (int j = 0; j < QPT; ++j) {
+            vb[j] = make_vtxf(sx[k + h], sy[k + h], sz[k + h], qa[j], qb[j], qc[j], minhi[j]);
+            const double num = va[j].uy * vb[j].ux - va[j].ux * vb[j].uy;
+            const double den = va[j].ux * vb[j].ux + va[j].uy * vb[j].uy + va[j].uz * vb[j].uz;
+            neg[j] |= __double2hiint(den);
+            cmul_track(st[j], den, num);
+          }
+#pragma unroll
+          for (int j = 0; j < QPT; ++j) {
+            va[j] = make_vtxf(sx[k + h + 1], sy[k + h + 1], sz[k + h + 1], qa[j], qb[j], qc[j],
+                              minhi[j]);
+            const double num = vb[j].uy * va[j].ux - vb[j].ux * va[j].uy;
+            const double den = vb[j].ux * va[j].ux + vb[j].uy * va[j].uy + vb[j].uz * va[j].uz;
+            neg[j] |= __double2hiint(den);
+            cmul_track(st[j], den, num);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < QPT; ++j) renorm(st[j]);
+      }
+      for (; k < kend; ++k) {
+#pragma unroll
+        for (int j = 0; j < QPT; ++j) {
+          vb[j] = make_vtxf(sx[k], sy[k], sz[k], qa[j], qb[j], qc[j], minhi[j]);
+          const double num = va[j].uy * vb[j].ux - va[j].ux * vb[j].uy;
+          const double den = va[j].ux * vb[j].ux + va[j].uy * vb[j].uy + va[j].uz * vb[j].uz;
+          neg[j] |= __double2hiint(den);
+          cmul_track(st[j], den, num);
+          va[j] = vb[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < QPT; ++j) renorm(st[j]);
+    }
+    // rare: some segment of this tile had den < 0 -> polyline/curve band test
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) any |= neg[j] < 0;
+    if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+      for (int j = 0; j < QPT; ++j) {
+        if (neg[j] >= 0) continue;
+        int mh = 0x7fffffff;
+        for (int e = 0; e < ne; ++e) {
+          const int b = e * S;
+          const double h = __ldg(band_h + te + e);
+          VtxF A = make_vtxf(sx[b], sy[b], sz[b], qa[j], qb[j], qc[j], mh);
+          for (int i = b + 1; i < b + S; ++i) {
+            const VtxF B = make_vtxf(sx[i], sy[i], sz[i], qa[j], qb[j], qc[j], mh);
+            const double num = A.uy * B.ux - A.ux * B.uy;
+            const double den = A.ux * B.ux + A.uy * B.uy + A.uz * B.uz;
+            if (den < 0.0 && band_hit_f(A, B, num, h, prm.band_factor)) flags[j] |= FLAG_BAND;
+            A = B;
+          }
+        }
+        neg[j] = 0;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < QPT; ++j)
+    if (minhi[j] < kDegHi) flags[j] |= FLAG_DEGEN;
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) {
+    if (slot[j] < m) {
+      bpart[(int64_t)blockIdx.y * m + slot[j]] = seg_angle(st[j]);
+      if (flags[j]) atomicOr(&flag_acc[slot[j]], flags[j]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    int32_t nq = min((int32_t)(blockDim.x * QPT), m - (int32_t)(blockIdx.x * blockDim.x * QPT));
+    const int64_t segs = (e1 - e0) * (int64_t)(S - 1);
+    atomicAdd(&counters[CNT_SEGMENTS], (unsigned long long)(segs * nq));
+  }
+}
+
 // Accuracy of rsqrt_nr against the correctly rounded 1/sqrt on a log-uniform
 // sweep of [1e-20, 1e20] (gwn_selftest_rsqrt).
 __global__ void k_rsqrt_selftest(int64_t n, unsigned long long* max_ulp) {
@@ -296,8 +436,15 @@ cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
   int64_t V = sc->n_edges * sc->S;
   if (V == 0) return cudaMemsetAsync(bpart, 0, sizeof(double) * m, st);
   dim3 grid((m + kBlockQ * kQPT - 1) / (kBlockQ * kQPT), nchunk);
-  k_boundary<kQPT><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S, sc->n_edges,
-                                             sc->band_h, rd.f, sc->dprm, bpart, flags, counters);
+  static const bool generic = getenv("GWN_K4_GENERIC") != nullptr;  // A/B switch
+  if (sc->S <= kTileV && !generic)
+    k_boundary_e<kQPT><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S, sc->n_edges,
+                                                 sc->band_h, rd.f, sc->dprm, bpart, flags,
+                                                 counters);
+  else
+    k_boundary<kQPT><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S, sc->n_edges,
+                                               sc->band_h, rd.f, sc->dprm, bpart, flags,
+                                               counters);
   return cudaGetLastError();
 }
 
