@@ -242,8 +242,11 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
 // vertex carried between segments alternates between two registers.  Same
 // segment order and the same power-of-two renormalisations (exact scalings)
 // as k_boundary, so the partial sums are bit-identical to it.
+#ifndef GWN_K4_MINB
+#define GWN_K4_MINB 2
+#endif
 template <int QPT>
-__global__ void __launch_bounds__(kBlockQ, 2)
+__global__ void __launch_bounds__(kBlockQ, GWN_K4_MINB)
 k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
              const double* __restrict__ vproj, int64_t V, int S, int64_t n_edges,
              const double* __restrict__ band_h, Frame f, DevParams prm,
@@ -417,7 +420,10 @@ cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-constexpr int kQPT = 2;
+#ifndef GWN_K4_QPT
+#define GWN_K4_QPT 2
+#endif
+constexpr int kQPT = GWN_K4_QPT;
 
 // Edge chunks of the boundary sum.  Fixed per scene (not per batch) so the
 // chunk partials -- added in chunk order by K5 -- make w bit-identical for any

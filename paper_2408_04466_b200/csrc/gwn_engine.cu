@@ -22,6 +22,76 @@
 
 namespace gwn {
 
+// w = chi + (sum of the chunk partial angles) / 2 pi, rounded the same way in
+// every finalize path (explicit roundings: no FMA contraction choices)
+__device__ __forceinline__ double w_of(int32_t chi, double ang) {
+  return __dadd_rn((double)chi, __dmul_rn(ang, 0.15915494309189533576888));
+}
+
+// K5 for one query slot s (query q): done / jitter / re-shoot; returns true
+// when q goes to the next round.
+__device__ __forceinline__ bool finalize_one(
+    int32_t s, int32_t q, int32_t m, int32_t f, double w, int round, int max_rounds,
+    int max_jitters, uint64_t seed, int64_t index_base, const int64_t* __restrict__ qidx,
+    double jscale, const double* __restrict__ q0, double* __restrict__ pos,
+    int8_t* __restrict__ jit, int8_t* __restrict__ jreason, double* __restrict__ w_out,
+    int8_t* __restrict__ st_out) {
+  bool push = false;
+  if (f & (FLAG_ONSURF | FLAG_DEGEN)) {
+    int reason = (f & FLAG_ONSURF) ? GWN_STATUS_ON_SURFACE : GWN_STATUS_DEGENERATE;
+    int j = round > 0 ? jit[q] : 0;  // round 0: jit / pos not yet initialised
+    if (j < max_jitters && round + 1 >= max_rounds) {
+      w_out[q] = w;  // jitter budget left but no round to use it (oracle eval_query)
+      st_out[q] = GWN_STATUS_EXHAUSTED;
+    } else if (j < max_jitters) {
+      ++j;
+      jit[q] = (int8_t)j;
+      jreason[q] = (int8_t)reason;
+      // deterministic jitter (same hash as gwn_jitter_dir / the oracle)
+      uint64_t st = seed ^ 0x5851F42D4C957F2Dull;
+      st ^= (uint64_t)(qidx ? qidx[q] : index_base + q) * 0x9E3779B97F4A7C15ull;
+      st ^= (uint64_t)(j + 1) * 0xC2B2AE3D27D4EB4Full;
+      double v[3];
+      for (int k = 0; k < 3; ++k) {
+        uint64_t z = (st += 0x9E3779B97F4A7C15ull);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        v[k] = __dadd_rn(__dmul_rn(2.0, __dmul_rn((double)(z >> 11), 1.0 / 9007199254740992.0)),
+                         -1.0);
+      }
+      double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(v[0], v[0]), __dmul_rn(v[1], v[1])),
+                                      __dmul_rn(v[2], v[2])));
+      if (n < 1e-3) {
+        v[0] = 1.0; v[1] = 0.0; v[2] = 0.0;
+      } else {
+        for (int k = 0; k < 3; ++k) v[k] = __ddiv_rn(v[k], n);
+      }
+      for (int k = 0; k < 3; ++k)
+        pos[3 * (int64_t)q + k] = __dadd_rn(q0[3 * (int64_t)q + k], __dmul_rn(jscale, v[k]));
+      push = true;
+    } else {
+      w_out[q] = w;
+      st_out[q] = (int8_t)reason;
+    }
+  } else if (f & (FLAG_RESHOOT | FLAG_BAND)) {
+    if (round + 1 < max_rounds) {
+      push = true;
+      if (round == 0) {  // next round reads pos / jit of the queries it gets
+        jit[q] = 0;
+        for (int k = 0; k < 3; ++k) pos[3 * (int64_t)q + k] = q0[3 * (int64_t)q + k];
+      }
+    } else {
+      w_out[q] = w;
+      st_out[q] = GWN_STATUS_EXHAUSTED;
+    }
+  } else {
+    w_out[q] = w;
+    st_out[q] = (round > 0 && jit[q]) ? jreason[q] : (int8_t)GWN_STATUS_OK;
+  }
+  return push;
+}
+
 // K5: per active query decide done / jitter / re-shoot.
 __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
                            const int32_t* __restrict__ chi, const int32_t* __restrict__ flags,
@@ -40,64 +110,14 @@ __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
   int32_t q = 0;
   if (s < m) {
     q = active ? active[s] : s;
-    int32_t f = flags[s];
+    const int32_t f = flags[s];
     // boundary term: per-chunk partial angles summed in chunk order
     // (deterministic), (2 * angle) / (4 pi)
     double ang = 0.0;
-    for (int c = 0; c < nchunk; ++c) ang += bpart[(int64_t)c * m + s];
-    double w = (double)chi[s] + ang * 0.15915494309189533576888;
-    if (f & (FLAG_ONSURF | FLAG_DEGEN)) {
-      int reason = (f & FLAG_ONSURF) ? GWN_STATUS_ON_SURFACE : GWN_STATUS_DEGENERATE;
-      int j = round > 0 ? jit[q] : 0;  // round 0: jit / pos not yet initialised
-      if (j < max_jitters && round + 1 >= max_rounds) {
-        w_out[q] = w;  // jitter budget left but no round to use it (oracle eval_query)
-        st_out[q] = GWN_STATUS_EXHAUSTED;
-      } else if (j < max_jitters) {
-        ++j;
-        jit[q] = (int8_t)j;
-        jreason[q] = (int8_t)reason;
-        // deterministic jitter (same hash as gwn_jitter_dir / the oracle)
-        uint64_t st = seed ^ 0x5851F42D4C957F2Dull;
-        st ^= (uint64_t)(qidx ? qidx[q] : index_base + q) * 0x9E3779B97F4A7C15ull;
-        st ^= (uint64_t)(j + 1) * 0xC2B2AE3D27D4EB4Full;
-        double v[3];
-        for (int k = 0; k < 3; ++k) {
-          uint64_t z = (st += 0x9E3779B97F4A7C15ull);
-          z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-          z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-          z ^= z >> 31;
-          v[k] = __dadd_rn(__dmul_rn(2.0, __dmul_rn((double)(z >> 11), 1.0 / 9007199254740992.0)),
-                           -1.0);
-        }
-        double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(v[0], v[0]), __dmul_rn(v[1], v[1])),
-                                        __dmul_rn(v[2], v[2])));
-        if (n < 1e-3) {
-          v[0] = 1.0; v[1] = 0.0; v[2] = 0.0;
-        } else {
-          for (int k = 0; k < 3; ++k) v[k] = __ddiv_rn(v[k], n);
-        }
-        for (int k = 0; k < 3; ++k)
-          pos[3 * (int64_t)q + k] = __dadd_rn(q0[3 * (int64_t)q + k], __dmul_rn(jscale, v[k]));
-        push = true;
-      } else {
-        w_out[q] = w;
-        st_out[q] = (int8_t)reason;
-      }
-    } else if (f & (FLAG_RESHOOT | FLAG_BAND)) {
-      if (round + 1 < max_rounds) {
-        push = true;
-        if (round == 0) {  // next round reads pos / jit of the queries it gets
-          jit[q] = 0;
-          for (int k = 0; k < 3; ++k) pos[3 * (int64_t)q + k] = q0[3 * (int64_t)q + k];
-        }
-      } else {
-        w_out[q] = w;
-        st_out[q] = GWN_STATUS_EXHAUSTED;
-      }
-    } else {
-      w_out[q] = w;
-      st_out[q] = (round > 0 && jit[q]) ? jreason[q] : (int8_t)GWN_STATUS_OK;
-    }
+    for (int c = 0; c < nchunk; ++c) ang = __dadd_rn(ang, bpart[(int64_t)c * m + s]);
+    const double w = w_of(chi[s], ang);
+    push = finalize_one(s, q, m, f, w, round, max_rounds, max_jitters, seed, index_base, qidx,
+                        jscale, q0, pos, jit, jreason, w_out, st_out);
   }
   // warp-aggregated compaction of the re-shot queries
   unsigned mask = __ballot_sync(0xffffffffu, push);
@@ -108,6 +128,66 @@ __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
     if (lane == leader) base = atomicAdd(next_n, __popc(mask));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (push) next[base + __popc(mask & ((1u << lane) - 1))] = q;
+  }
+}
+
+// K5, round 0 with the identity slot map (the common case): four queries per
+// thread with 16-byte loads of chi / flags / partials and 16- and 4-byte
+// stores of w / status; flagged queries (rare) take finalize_one and a plain
+// atomic append.
+__global__ void k_finalize4(int32_t m, const int32_t* __restrict__ chi,
+                            const int32_t* __restrict__ flags, const double* __restrict__ bpart,
+                            int nchunk, int max_rounds, int max_jitters, uint64_t seed,
+                            int64_t index_base, const int64_t* __restrict__ qidx, double jscale,
+                            const double* __restrict__ q0, double* __restrict__ pos,
+                            int8_t* __restrict__ jit, int8_t* __restrict__ jreason,
+                            double* __restrict__ w_out, int8_t* __restrict__ st_out,
+                            int32_t* __restrict__ next, int32_t* __restrict__ next_n,
+                            const unsigned long long* __restrict__ pair_count,
+                            unsigned long long pair_cap) {
+  if (*pair_count > pair_cap) return;
+  const int32_t s0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (s0 >= m) return;
+  if (s0 + 4 > m) {  // ragged tail: scalar
+    for (int32_t s = s0; s < m; ++s) {
+      double ang = 0.0;
+      for (int c = 0; c < nchunk; ++c) ang = __dadd_rn(ang, bpart[(int64_t)c * m + s]);
+      const double w = w_of(chi[s], ang);
+      if (finalize_one(s, s, m, flags[s], w, 0, max_rounds, max_jitters, seed, index_base, qidx,
+                       jscale, q0, pos, jit, jreason, w_out, st_out))
+        next[atomicAdd(next_n, 1)] = s;
+    }
+    return;
+  }
+  const int4 c4 = *reinterpret_cast<const int4*>(chi + s0);
+  const int4 f4 = *reinterpret_cast<const int4*>(flags + s0);
+  double ang[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int c = 0; c < nchunk; ++c) {
+    const double* b = bpart + (int64_t)c * m + s0;
+    if ((m & 1) == 0) {
+      const double2 x = *reinterpret_cast<const double2*>(b);
+      const double2 y = *reinterpret_cast<const double2*>(b + 2);
+      ang[0] = __dadd_rn(ang[0], x.x); ang[1] = __dadd_rn(ang[1], x.y);
+      ang[2] = __dadd_rn(ang[2], y.x); ang[3] = __dadd_rn(ang[3], y.y);
+    } else {
+      for (int k = 0; k < 4; ++k) ang[k] = __dadd_rn(ang[k], b[k]);
+    }
+  }
+  const int cc[4] = {c4.x, c4.y, c4.z, c4.w};
+  const int ff[4] = {f4.x, f4.y, f4.z, f4.w};
+  double w[4];
+  for (int k = 0; k < 4; ++k) w[k] = w_of(cc[k], ang[k]);
+  if ((ff[0] | ff[1] | ff[2] | ff[3]) == 0) {
+    *reinterpret_cast<double2*>(w_out + s0) = make_double2(w[0], w[1]);
+    *reinterpret_cast<double2*>(w_out + s0 + 2) = make_double2(w[2], w[3]);
+    *reinterpret_cast<int32_t*>(st_out + s0) = 0;  // 4 x GWN_STATUS_OK
+    return;
+  }
+  for (int k = 0; k < 4; ++k) {
+    const int32_t s = s0 + k;
+    if (finalize_one(s, s, m, ff[k], w[k], 0, max_rounds, max_jitters, seed, index_base, qidx,
+                     jscale, q0, pos, jit, jreason, w_out, st_out))
+      next[atomicAdd(next_n, 1)] = s;
   }
 }
 
@@ -321,12 +401,23 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         if (join) CKE(cudaStreamWaitEvent(st, join, 0));
         tl_mark(st, "joined");
         int32_t* nxt = act[cur];
-        k_finalize<<<(m + 127) / 128, 128, 0, st>>>(
-            m, active, chi, fl, bterm, nchunk, r, sc->prm.max_rounds, sc->prm.max_jitters,
-            sc->prm.dir_seed, index_base + c0, qidx ? qidx + c0 : nullptr,
-            sc->prm.jitter_scale * sc->diag, q0, pos, jit,
-            jreason, d_w + c0, d_st + c0, nxt, (int32_t*)(rsc + 1), rsc,
-            (unsigned long long)pair_cap);
+        const bool vec4 = r == 0 && !active && ((uintptr_t)(d_w + c0) & 15) == 0 &&
+                          ((uintptr_t)(d_st + c0) & 3) == 0;
+        if (vec4) {
+          const int32_t nth = (m + 3) / 4;
+          k_finalize4<<<(nth + 127) / 128, 128, 0, st>>>(
+              m, chi, fl, bterm, nchunk, sc->prm.max_rounds, sc->prm.max_jitters,
+              sc->prm.dir_seed, index_base + c0, qidx ? qidx + c0 : nullptr,
+              sc->prm.jitter_scale * sc->diag, q0, pos, jit, jreason, d_w + c0, d_st + c0, nxt,
+              (int32_t*)(rsc + 1), rsc, (unsigned long long)pair_cap);
+        } else {
+          k_finalize<<<(m + 127) / 128, 128, 0, st>>>(
+              m, active, chi, fl, bterm, nchunk, r, sc->prm.max_rounds, sc->prm.max_jitters,
+              sc->prm.dir_seed, index_base + c0, qidx ? qidx + c0 : nullptr,
+              sc->prm.jitter_scale * sc->diag, q0, pos, jit,
+              jreason, d_w + c0, d_st + c0, nxt, (int32_t*)(rsc + 1), rsc,
+              (unsigned long long)pair_cap);
+        }
         CKE(cudaGetLastError());
         ++launches;
         CKE(cudaMemcpyAsync(h_scalar, d_cnt, sizeof(unsigned long long) * kBlk,

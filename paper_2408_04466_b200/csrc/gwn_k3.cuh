@@ -84,6 +84,50 @@ __device__ __forceinline__ int leaf_test(const LeafRec& L, double qa, double qb,
   return kr;
 }
 
+// leaf_test reading the record through a pointer, in two steps: the
+// Krawczyk data (64 B) and code/patch/ok (16 B) first, the separating axes
+// (64 B) only for the undecided candidates -- most are settled by the first
+// step, which halves the record traffic of K3 pass 0.
+__device__ __forceinline__ int leaf_test_lazy(const LeafRec* __restrict__ Lp, double qa,
+                                              double qb, const DevParams& prm, double& nu,
+                                              double& nv, int32_t& patch, uint64_t& code) {
+  const double2* p = reinterpret_cast<const double2*>(Lp);
+  const double2 g = __ldg(p), y0 = __ldg(p + 1), y1 = __ldg(p + 2), r = __ldg(p + 3);
+  const double2 tail = __ldg(p + 8);
+  code = (uint64_t)__double_as_longlong(tail.x);
+  const long long po = __double_as_longlong(tail.y);
+  patch = (int32_t)(po & 0xffffffffll);
+  const int32_t ok = (int32_t)(po >> 32);
+  const double span = 1.0 + 2.0 * kLeafM;
+  const double tl = kLeafM / span, th = (1.0 + kLeafM) / span;
+  const int lev = code_level(code);
+  const double wu = code_wu(lev), wv = code_wv(lev);
+  const double u0 = (double)code_iu(code) * wu, v0 = (double)code_iv(code) * wv;
+  const double tol = prm.domain_tol;
+  const double xlo_u = tl - (u0 == 0.0 ? tol / (wu * span) : 0.0);
+  const double xhi_u = th + (u0 + wu == 1.0 ? tol / (wu * span) : 0.0);
+  const double xlo_v = tl - (v0 == 0.0 ? tol / (wv * span) : 0.0);
+  const double xhi_v = th + (v0 + wv == 1.0 ? tol / (wv * span) : 0.0);
+  KrawPre k;
+  k.Ga = g.x; k.Gb = g.y;
+  k.Y00 = y0.x; k.Y01 = y0.y; k.Y10 = y1.x; k.Y11 = y1.y;
+  k.R0 = r.x; k.R1 = r.y;
+  k.ok = ok != 0;
+  double s0, s1;
+  int kr = kraw_query(k, g.x - qa, g.y - qb, xlo_u, xhi_u, xlo_v, xhi_v, -1e-7, 1.0 + 1e-7,
+                      s0, s1);
+  if (kr == 2) {  // separating axes of the leaf hull (rigorous exclusion)
+    const double2 a0 = __ldg(p + 4), a1 = __ldg(p + 5), a2 = __ldg(p + 6), a3 = __ldg(p + 7);
+    const double p1 = a0.x * qa + a0.y * qb, p2 = a2.x * qa + a2.y * qb;
+    if (p1 < a1.x || p1 > a1.y || p2 < a3.x || p2 > a3.y) kr = 0;
+  }
+  if (kr == 1) {
+    nu = u0 - kLeafM * wu + s0 * span * wu;
+    nv = v0 - kLeafM * wv + s1 * span * wv;
+  }
+  return kr;
+}
+
 // K3 queues: the cull's (query, leaf) candidates; after the candidate test
 // the undecided ones for the subdivision fallback, certified ones for the
 // Newton pass.  Each candidate yields at most one item, so every queue has

@@ -4,6 +4,8 @@
 // minus the query's projection, index 4*i+j with i the u index.
 #pragma once
 
+#include <stddef.h>
+
 #include "gwn_internal.h"
 
 namespace gwn {
@@ -280,6 +282,10 @@ struct alignas(16) LeafRec {
   int32_t patch;
   int32_t ok;
 };
+// leaf_test_lazy (gwn_k3.cuh) reads the record as 9 double2 words
+static_assert(sizeof(LeafRec) == 144 && offsetof(LeafRec, code) == 128 &&
+                  offsetof(LeafRec, patch) == 136 && offsetof(LeafRec, ok) == 140,
+              "LeafRec layout");
 
 // Query-independent separating axes of a (raw) net: unit normals of the
 // centre u/v tangents and the net's extent along them (hull_sat below).

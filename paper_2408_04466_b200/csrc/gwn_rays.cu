@@ -94,8 +94,8 @@ __global__ void k_ray_finalize(int64_t np, const int32_t* __restrict__ chi,
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= np) return;
   double ang = 0.0;
-  for (int c = 0; c < nchunk; ++c) ang += bpart[(int64_t)c * np + i];
-  w[i] = (double)chi[i] + ang * 0.15915494309189533576888;
+  for (int c = 0; c < nchunk; ++c) ang = __dadd_rn(ang, bpart[(int64_t)c * np + i]);
+  w[i] = __dadd_rn((double)chi[i], __dmul_rn(ang, 0.15915494309189533576888));
   stt[i] = GWN_STATUS_OK;
   if (qfl[i]) {  // per-point engine (new direction / jitter)
     const unsigned long long k = atomicAdd(nfb, 1ull);

@@ -106,14 +106,11 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev, K3Queues Q, Wav
       const int2 pr = Q.pairs[i];
       slot = pr.x;
       leaf = pr.y;
-      const LeafRec L = w.leaves[leaf];
-      patch = L.patch;
-      code = L.code;
       qa = w.qproj[3 * (int64_t)slot];
       qb = w.qproj[3 * (int64_t)slot + 1];
       qc = w.qproj[3 * (int64_t)slot + 2];
       ++tested;
-      const int kr = leaf_test(L, qa, qb, w.prm, nu_, nv_);
+      const int kr = leaf_test_lazy(w.leaves + leaf, qa, qb, w.prm, nu_, nv_, patch, code);
       wantN = kr == 1;
       wantF = kr == 2;
     }
