@@ -593,7 +593,8 @@ static cudaError_t build_subleaves(Round& rd, cudaStream_t st) {
   if (total > 0) {
     SC(cudaMalloc(&rd.sub, sizeof(LeafRec) * total));
     SC(cudaMalloc(&rd.subbox, sizeof(double) * 5 * total));
-    SC(cudaMalloc(&rd.subskip, sizeof(int32_t) * total));
+    SC(cudaMalloc(&rd.subskip, sizeof(int32_t) * (total + 1)));  // +1: read-ahead pad
+    SC(cudaMemsetAsync(rd.subskip + total, 0, sizeof(int32_t), st));
     k_foldtree<true><<<g, 128, 0, st>>>(n, rd.leaves, rd.proj, level, offs, nullptr, rd.sub,
                                         rd.subbox, rd.subskip);
     SC(cudaGetLastError());

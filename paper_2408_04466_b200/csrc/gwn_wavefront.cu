@@ -209,10 +209,14 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
           if (tg & kTreeTag) {
             // precomputed fold-tree node
             const int64_t t = (int64_t)e;
+            // every load of the node up front (one memory round trip per
+            // level): box, skips of the node and of its first child, record
             const double* bx = w.subbox + 5 * t;
-            const int32_t sk = w.subskip[t];
-            if (qa >= bx[0] && qa <= bx[1] && qb >= bx[2] && qb <= bx[3] && bx[4] >= qc) {
-              const LeafRec S = w.sub[t];
+            const int32_t sk = __ldg(w.subskip + t), sk1 = __ldg(w.subskip + t + 1);
+            const double b0 = __ldg(bx), b1 = __ldg(bx + 1), b2 = __ldg(bx + 2),
+                         b3 = __ldg(bx + 3), b4 = __ldg(bx + 4);
+            const LeafRec S = w.sub[t];
+            if (qa >= b0 && qa <= b1 && qb >= b2 && qb <= b3 && b4 >= qc) {
               if (sk == 1) {
                 double su = 0.0, sv = 0.0;
                 const int kr = leaf_test(S, qa, qb, w.prm, su, sv);
@@ -232,7 +236,7 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
                   nout = 2;
                   otag = kTreeTag;
                   out0 = (uint64_t)(t + 1);
-                  out1 = (uint64_t)(t + 1 + w.subskip[t + 1]);
+                  out1 = (uint64_t)(t + 1 + sk1);
                 }
               }
             }
