@@ -15,7 +15,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <chrono>
+#include <vector>
 
 #include "gwn_internal.h"
 #include "gwn_k3.cuh"
@@ -277,6 +279,11 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   stats.queries = n;
   cudaEvent_t ev[8] = {}, ev4[5] = {};
   int64_t launches = 0;
+  // host buffers, large batches: chunks pipelined against the copies
+  // (H2D of chunk k+1 and D2H of chunk k-1 overlap chunk k's rounds)
+  const bool pipe = host && n >= (1ll << 18) && !sc->timed;
+  static thread_local cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  std::vector<cudaEvent_t> pev;  // per chunk: [2k] input copied, [2k+1] chunk done
   unsigned long long* d_cnt = nullptr;
   unsigned long long h_cnt[CNT_N];
   CKE(cudaSetDevice(sc->device));
@@ -297,7 +304,8 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     d_w = ws.get<double>((size_t)n);
     d_st = ws.get<int8_t>((size_t)n);
     CKE(ws.err);
-    CKE(cudaMemcpyAsync(dq, queries, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+    if (!pipe)
+      CKE(cudaMemcpyAsync(dq, queries, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
     d_q = dq;
   }
   if (sc->timed) {
@@ -305,7 +313,24 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     for (auto& e : ev4) CKE(cudaEventCreate(&e));
   }
   {
-    const int64_t cm = n < chunk_max ? n : chunk_max;
+    int64_t cm = n < chunk_max ? n : chunk_max;
+    if (pipe) {
+      static const int64_t parts = [] {  // GWN_PIPE_CHUNKS overrides (experiments)
+        const char* e = getenv("GWN_PIPE_CHUNKS");
+        const long long v = e ? atoll(e) : 4;
+        return (int64_t)(v < 1 ? 1 : v);
+      }();
+      const int64_t pc =
+          (std::max<int64_t>(1ll << 16, (n + parts - 1) / parts) + 1023) & ~1023ll;
+      cm = std::min(cm, pc);
+      if (!cs_in) {
+        CKE(cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking));
+        CKE(cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking));
+      }
+      const int64_t nch = (n + cm - 1) / cm;
+      pev.assign((size_t)(2 * nch), nullptr);
+      for (auto& e : pev) CKE(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     // per-chunk workspace (reused across chunks and rounds)
     double* pos = ws.get<double>((size_t)(3 * cm));
     int8_t* jit = ws.get<int8_t>((size_t)cm);
@@ -330,6 +355,19 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     for (int64_t c0 = 0; c0 < n; c0 += cm) {
       const int32_t mc = (int32_t)((n - c0) < cm ? (n - c0) : cm);
       const double* q0 = d_q + 3 * c0;
+      const int64_t ci = c0 / cm;
+      if (pipe) {
+        auto h2d = [&](int64_t k) -> cudaError_t {
+          const int64_t a = k * cm, b = std::min(n, a + cm);
+          cudaError_t e = cudaMemcpyAsync((double*)d_q + 3 * a, queries + 3 * a,
+                                          sizeof(double) * 3 * (b - a), cudaMemcpyHostToDevice,
+                                          cs_in);
+          return e != cudaSuccess ? e : cudaEventRecord(pev[2 * k], cs_in);
+        };
+        if (ci == 0) CKE(h2d(0));
+        if (c0 + cm < n) CKE(h2d(ci + 1));
+        CKE(cudaStreamWaitEvent(st, pev[2 * ci], 0));
+      }
       // round 0 reads the queries in place; k_finalize fills pos / jit for
       // the queries it passes on to the next round
       int32_t m = mc;
@@ -462,13 +500,21 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         cur ^= 1;
         ++r;
       }
+      if (pipe) {  // this chunk's outputs back while the next chunk runs
+        CKE(cudaEventRecord(pev[2 * ci + 1], st));
+        CKE(cudaStreamWaitEvent(cs_out, pev[2 * ci + 1], 0));
+        CKE(cudaMemcpyAsync(w_out + c0, d_w + c0, sizeof(double) * mc, cudaMemcpyDeviceToHost,
+                            cs_out));
+        CKE(cudaMemcpyAsync(status_out + c0, d_st + c0, mc, cudaMemcpyDeviceToHost, cs_out));
+      }
     }
     if (k3_scratch) cudaFreeAsync(k3_scratch, st);
   }
-  if (host) {
+  if (host && !pipe) {
     CKE(cudaMemcpyAsync(w_out, d_w, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     CKE(cudaMemcpyAsync(status_out, d_st, n, cudaMemcpyDeviceToHost, st));
   }
+  if (pipe) CKE(cudaStreamSynchronize(cs_out));
   // eval counters: from the last round's scalar copy (no extra round trip)
   for (int k = 0; k < CNT_N; ++k) h_cnt[k] = (unsigned long long)h_scalar[k];
   if (host) CKE(cudaStreamSynchronize(st));
@@ -484,6 +530,12 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   tl_mark(st, "outputs copied");
   tr.mark("outputs copied");
 done:
+  if (pipe && cs_in) {  // no copy may outlive the workspace
+    cudaStreamSynchronize(cs_in);
+    cudaStreamSynchronize(cs_out);
+  }
+  for (auto& e : pev)
+    if (e) cudaEventDestroy(e);
   ws.release();
   if (st) cudaStreamSynchronize(st);
   else cudaDeviceSynchronize();
