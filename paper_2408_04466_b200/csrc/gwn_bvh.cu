@@ -183,7 +183,7 @@ __global__ void k_leaves(int64_t P, const double* __restrict__ proj,
 // kFill = false: count tree nodes per leaf; true: write them.
 template <bool kFill>
 __global__ void k_foldtree(int64_t n_leaves, const LeafRec* __restrict__ leaves,
-                           const double* __restrict__ proj, int sub_level,
+                           const double* __restrict__ proj, int sub_level, double tree_r,
                            const int64_t* __restrict__ offs, int64_t* __restrict__ counts,
                            LeafRec* __restrict__ sub, double* __restrict__ subbox,
                            int32_t* __restrict__ subskip) {
@@ -194,7 +194,12 @@ __global__ void k_foldtree(int64_t n_leaves, const LeafRec* __restrict__ leaves,
   int64_t n = 0;
   const int64_t o = kFill ? offs[i] : 0;
   const bool cert = L.ok && L.R0 < kLeafRmax && L.R1 < kLeafRmax;
-  if (!cert && code_level(L.code) < sub_level) {
+  // certified leaves with large radii get a full two-level tree: a query whose
+  // predicted root sits near the leaf border (K = t* +- R leaves the
+  // certification box) is then settled by stored children, not node_test
+  const bool wide = cert && fmax(L.R0, L.R1) >= tree_r;
+  const int lim = wide ? code_level(L.code) + 2 : sub_level;
+  if ((!cert || wide) && code_level(L.code) < lim) {
     const double* P48 = proj + 48 * (int64_t)p;
     const double eps = patch_eps(P48);
     uint64_t stack[2 * kLeafLevelCap + 4];
@@ -225,7 +230,10 @@ __global__ void k_foldtree(int64_t n_leaves, const LeafRec* __restrict__ leaves,
       const uint64_t code = stack[--top];
       const int lv = code_level(code);
       const KrawPre kp = piece_kraw(P48, code);
-      const bool leaf = kraw_certifies(kp) || lv >= sub_level;
+      // fold trees: a certified node still splits while its radii are wide
+      // (so border queries settle in stored nodes), to the depth cap
+      const bool leaf = wide ? lv >= lim
+                             : ((kraw_certifies(kp) && fmax(kp.R0, kp.R1) < tree_r) || lv >= lim);
       if (kFill) {
         LeafRec r;
         make_leaf(P48, p, code, kp, eps, r, subbox + 5 * (o + n));
@@ -554,16 +562,46 @@ out:
   return e;
 }
 
+// Grandchild lists of the fold trees: for an internal node t with children
+// c0 = t+1 and c1 = t+1+skip[t+1], each child contributes itself if it is a
+// leaf, else its two children -- the fallback walks every other level only
+// (half the dependent memory round trips) and never skips a leaf.
+__global__ void k_foldtree_gc(int64_t total, const int32_t* __restrict__ skip,
+                              int4* __restrict__ gc) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  int4 g = make_int4(-1, -1, -1, -1);
+  if (skip[t] > 1) {
+    const int64_t c[2] = {t + 1, t + 1 + skip[t + 1]};
+    int out[4] = {-1, -1, -1, -1};
+    int n = 0;
+    for (int k = 0; k < 2; ++k) {
+      if (skip[c[k]] == 1) {
+        out[n++] = (int)(c[k] - t);
+      } else {
+        out[n++] = (int)(c[k] + 1 - t);
+        out[n++] = (int)(c[k] + 1 + skip[c[k] + 1] - t);
+      }
+    }
+    g = make_int4(out[0], out[1], out[2], out[3]);
+  }
+  gc[t] = g;
+}
+
 // Fold trees of the round's uncertified leaves (k_foldtree): the deepest
 // sub_level <= kSubLevelMax whose node count stays within the budget
 // (GWN_SUB_LEVEL overrides; 0 disables).
 static cudaError_t build_subleaves(Round& rd, cudaStream_t st) {
   const char* env = getenv("GWN_SUB_LEVEL");
   int level = env ? atoi(env) : kSubLevelMax;
-  if (level > kLeafLevelCap) level = kLeafLevelCap;
+  if (level > kLeafLevelCap) level = kLeafLevelCap;  // (kLeafLevelCap bounds the stacks)
   const int64_t n = rd.n_leaves;
   if (level <= leaf_max_level() || n <= 0) return cudaSuccess;
-  const int64_t budget = std::max<int64_t>(4 * n, 1ll << 20);
+  const char* env_b = getenv("GWN_TREE_BUDGET");  // node budget (experiments)
+  const int64_t budget = env_b ? atoll(env_b) : std::max<int64_t>(4 * n, 1ll << 20);
+  const int level0 = level;
+  const char* env_r = getenv("GWN_TREE_R");  // certified-leaf tree threshold (experiments)
+  double tree_r = env_r ? atof(env_r) : kTreeR;
   cudaError_t e = cudaSuccess;
   int64_t *cnt = nullptr, *offs = nullptr;
   void* tmp = nullptr;
@@ -580,10 +618,17 @@ static cudaError_t build_subleaves(Round& rd, cudaStream_t st) {
   SC(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, offs, (int)(n + 1), st));
   SC(cudaMalloc(&tmp, tb));
   for (;; level -= 2) {
-    if (level <= leaf_max_level()) goto out;  // nothing fits: keep the plain fallback
+    if (level <= leaf_max_level()) {
+      if (tree_r < 1.0) {  // drop the certified-leaf trees, retry the fold trees alone
+        tree_r = INFINITY;
+        level = level0 + 2;
+        continue;
+      }
+      goto out;  // nothing fits: keep the plain fallback
+    }
     SC(cudaMemsetAsync(cnt + n, 0, sizeof(int64_t), st));
-    k_foldtree<false><<<g, 128, 0, st>>>(n, rd.leaves, rd.proj, level, nullptr, cnt, nullptr,
-                                         nullptr, nullptr);
+    k_foldtree<false><<<g, 128, 0, st>>>(n, rd.leaves, rd.proj, level, tree_r, nullptr, cnt,
+                                         nullptr, nullptr, nullptr);
     SC(cudaGetLastError());
     SC(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, offs, (int)(n + 1), st));
     SC(cudaMemcpyAsync(&total, offs + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -595,8 +640,11 @@ static cudaError_t build_subleaves(Round& rd, cudaStream_t st) {
     SC(cudaMalloc(&rd.subbox, sizeof(double) * 5 * total));
     SC(cudaMalloc(&rd.subskip, sizeof(int32_t) * (total + 1)));  // +1: read-ahead pad
     SC(cudaMemsetAsync(rd.subskip + total, 0, sizeof(int32_t), st));
-    k_foldtree<true><<<g, 128, 0, st>>>(n, rd.leaves, rd.proj, level, offs, nullptr, rd.sub,
-                                        rd.subbox, rd.subskip);
+    k_foldtree<true><<<g, 128, 0, st>>>(n, rd.leaves, rd.proj, level, tree_r, offs, nullptr,
+                                        rd.sub, rd.subbox, rd.subskip);
+    SC(cudaGetLastError());
+    SC(cudaMalloc(&rd.subgc, sizeof(int4) * total));
+    k_foldtree_gc<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(total, rd.subskip, rd.subgc);
     SC(cudaGetLastError());
     rd.sub_offs = offs;
     offs = nullptr;
@@ -605,7 +653,8 @@ static cudaError_t build_subleaves(Round& rd, cudaStream_t st) {
     SC(cudaStreamSynchronize(st));
   }
   if (getenv("GWN_TRACE"))
-    fprintf(stderr, "[gwn] fold trees: %lld nodes to level %d\n", (long long)total, level);
+    fprintf(stderr, "[gwn] fold trees: %lld nodes to level %d (certified-leaf trees R >= %g)\n",
+            (long long)total, level, tree_r);
 out:
 #undef SC
   if (cnt) cudaFree(cnt);
@@ -618,6 +667,7 @@ void free_round(Round& rd) {
   if (rd.sub) cudaFree(rd.sub);
   if (rd.subbox) cudaFree(rd.subbox);
   if (rd.subskip) cudaFree(rd.subskip);
+  if (rd.subgc) cudaFree(rd.subgc);
   if (rd.sub_offs) cudaFree(rd.sub_offs);
   if (rd.proj) cudaFree(rd.proj);
   if (rd.nodes) cudaFree(rd.nodes);

@@ -523,8 +523,8 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   stats.roots = (int64_t)h_cnt[CNT_ROOTS];
   stats.boundary_segments = (int64_t)h_cnt[CNT_SEGMENTS];
   if (getenv("GWN_TRACE"))
-    fprintf(stderr, "[gwn] fallback: max nodes/item %llu, items > 16 nodes %llu, max levels %llu\n",
-            h_cnt[CNT_MAXNODES], h_cnt[CNT_BIGITEMS], h_cnt[CNT_MAXLEVELS]);
+    fprintf(stderr, "[gwn] fallback: max nodes/item %llu, slowest batch: %llu cycles tree %llu code %llu items %llu, max levels %llu\n",
+            h_cnt[CNT_MAXNODES], h_cnt[CNT_BIGITEMS] >> 24, (h_cnt[CNT_BIGITEMS] >> 16) & 255, (h_cnt[CNT_BIGITEMS] >> 8) & 255, h_cnt[CNT_BIGITEMS] & 255, h_cnt[CNT_MAXLEVELS]);
   stats.kernel_launches = launches;
   sc->stats = stats;
   tl_mark(st, "outputs copied");

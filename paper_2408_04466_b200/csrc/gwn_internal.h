@@ -104,6 +104,7 @@ struct Round {
   LeafRec* sub = nullptr;
   double* subbox = nullptr;
   int32_t* subskip = nullptr;
+  int4* subgc = nullptr;        // grandchild offsets (k_foldtree_gc), -1 = none
   int64_t* sub_offs = nullptr;  // (n_leaves+1), null when no leaf needed it
   int64_t n_sub = 0;
   int sub_level = 0;

@@ -267,8 +267,9 @@ __device__ __forceinline__ double own_hi(double x, double tol) {
   return x == 1.0 ? 1.0 + tol : x + kOwnShift;
 }
 constexpr int kLeafMaxLevel = 12;
-constexpr int kLeafLevelCap = 24;  // stack bound of the leaf builder
+constexpr int kLeafLevelCap = 30;  // stack bound of the leaf builder
 constexpr int kSubLevelMax = 24;   // fold-tree depth (budget permitting)
+constexpr double kTreeR = 0.06;    // tree nodes split while certified but max(R) >= this
 
 struct alignas(16) LeafRec {
   double Ga, Gb;

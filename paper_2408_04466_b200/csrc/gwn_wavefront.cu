@@ -41,6 +41,7 @@ struct WaveArgs {
   const LeafRec* sub;
   const double* subbox;
   const int32_t* subskip;
+  const int4* subgc;
   int32_t sub_level;
 };
 
@@ -192,14 +193,24 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
     }
     __syncwarp();
     int cur = 0, ncur = s_n0[wb], levels = 0;
+    const long long tclk0 = clock64();
+    int tree_lv = 0, code_lv = 0, newton_calls = 0;
     while (ncur > 0) {
       ++levels;
+      {
+        bool hc = false, ht = false;
+        for (int k = lane; k < ncur; k += 32) {
+          if (fi[wb][cur][k] & kTreeTag) ht = true; else hc = true;
+        }
+        if (__any_sync(0xffffffffu, hc)) ++code_lv;
+        if (__any_sync(0xffffffffu, ht)) ++tree_lv;
+      }
       int nnext = 0;
       for (int base = 0; base < ncur; base += 32) {
         const int k = base + lane;
         int nout = 0, item = 0;
         uint8_t otag = 0;
-        uint64_t out0 = 0, out1 = 0;
+        uint64_t out0 = 0, out1 = 0, out2 = 0, out3 = 0;
         if (k < ncur) {
           const uint64_t e = fr[wb][cur][k];
           const uint8_t tg = fi[wb][cur][k];
@@ -212,7 +223,8 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
             // every load of the node up front (one memory round trip per
             // level): box, skips of the node and of its first child, record
             const double* bx = w.subbox + 5 * t;
-            const int32_t sk = __ldg(w.subskip + t), sk1 = __ldg(w.subskip + t + 1);
+            const int32_t sk = __ldg(w.subskip + t);
+            const int4 gc = w.subgc[t];
             const double b0 = __ldg(bx), b1 = __ldg(bx + 1), b2 = __ldg(bx + 2),
                          b3 = __ldg(bx + 3), b4 = __ldg(bx + 4);
             const LeafRec S = w.sub[t];
@@ -233,10 +245,13 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
               } else {
                 const double p1 = S.n1a * qa + S.n1b * qb, p2 = S.n2a * qa + S.n2b * qb;
                 if (!(p1 < S.lo1 || p1 > S.hi1 || p2 < S.lo2 || p2 > S.hi2)) {
-                  nout = 2;
+                  // grandchildren (a leaf child stands for itself)
                   otag = kTreeTag;
-                  out0 = (uint64_t)(t + 1);
-                  out1 = (uint64_t)(t + 1 + sk1);
+                  nout = 2 + (gc.z >= 0) + (gc.w >= 0);
+                  out0 = (uint64_t)(t + gc.x);
+                  out1 = (uint64_t)(t + gc.y);
+                  out2 = (uint64_t)(t + gc.z);
+                  out3 = (uint64_t)(t + gc.w);
                 }
               }
             }
@@ -276,24 +291,27 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
             }
           }
         }
-        // warp-aggregated append of 0, 1 or 2 entries per lane
-        const unsigned b1 = __ballot_sync(0xffffffffu, nout >= 1);
-        const unsigned b2 = __ballot_sync(0xffffffffu, nout == 2);
+        // warp-aggregated append of 0..4 entries per lane (inclusive scan)
+        int incl = nout;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
         if (nout) {
-          const unsigned lt = (1u << lane) - 1;
-          const int pos = nnext + __popc(b1 & lt) + __popc(b2 & lt);
+          const int pos = nnext + incl - nout;
           if (pos + nout <= kFrontier) {
-            fr[wb][cur ^ 1][pos] = out0;
-            fi[wb][cur ^ 1][pos] = (uint8_t)(item | otag);
-            if (nout == 2) {
-              fr[wb][cur ^ 1][pos + 1] = out1;
-              fi[wb][cur ^ 1][pos + 1] = (uint8_t)(item | otag);
+            const uint64_t outs[4] = {out0, out1, out2, out3};
+            for (int q = 0; q < nout; ++q) {
+              fr[wb][cur ^ 1][pos + q] = outs[q];
+              fi[wb][cur ^ 1][pos + q] = (uint8_t)(item | otag);
             }
           } else {
             atomicOr(&ifl[wb][item], FLAG_RESHOOT);  // frontier overflow
           }
         }
-        nnext = min(nnext + __popc(b1) + __popc(b2), kFrontier);
+        nnext = min(nnext + tot, kFrontier);
       }
       __syncwarp();
       cur ^= 1;
@@ -307,8 +325,16 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
       // diagnostics: largest item, items beyond 16 nodes
       const int nn = inodes[wb][lane];
       atomicMax(&w.counters[CNT_MAXNODES], (unsigned long long)nn);
-      if (nn > 16) atomicAdd(&w.counters[CNT_BIGITEMS], 1ull);
+      (void)nn;
       if (lane == 0) atomicMax(&w.counters[CNT_MAXLEVELS], (unsigned long long)levels);
+      if (lane == 0) {
+        const long long dt = clock64() - tclk0;
+        // debug: slowest warp batch: cycles | tree levels | code levels | items
+        const unsigned long long key = ((unsigned long long)(dt > 0 ? dt : 0) << 24) |
+                                       ((unsigned long long)tree_lv << 16) |
+                                       ((unsigned long long)code_lv << 8) | (unsigned long long)nb;
+        atomicMax(&w.counters[CNT_BIGITEMS], key);
+      }
     }
     __syncwarp();
   }
@@ -387,7 +413,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
   WaveArgs w{rd.leaves, qproj, rd.proj, sc->dprm, chi, flags,
              rec ? rec->rec : nullptr, rec ? rec->count : nullptr, rec ? rec->cap : 0ull,
              counters, Q.overflow, Q.nq, Q.n_count, Q.cap, newton_work,
-             rd.sub_offs, rd.sub, rd.subbox, rd.subskip, rd.sub_level};
+             rd.sub_offs, rd.sub, rd.subbox, rd.subskip, rd.subgc, rd.sub_level};
   if (ev4) cudaEventRecord(ev4[0], st);
   tl_mark(st, "k3 start");
   k3_candidates<<<g_cand, 128, 0, st>>>(npairs_dev, Q, w);
