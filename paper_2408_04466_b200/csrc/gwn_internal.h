@@ -38,7 +38,7 @@ enum : int {
   CNT_ROOTS = 3,
   CNT_SEGMENTS = 4,
   CNT_MAXNODES = 5,  // max DFS nodes of one fallback item (diagnostic)
-  CNT_BIGITEMS = 6,  // fallback items with > 16 nodes (diagnostic)
+  CNT_BIGITEMS = 6,  // slowest fallback warp: cycles<<24 | tree levels<<16 | code levels<<8 | items
   CNT_MAXLEVELS = 7, // deepest fallback BFS, in levels (diagnostic)
   CNT_N = 8,
 };
