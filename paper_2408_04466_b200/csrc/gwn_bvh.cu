@@ -551,8 +551,8 @@ static cudaError_t build_grid(Round& rd, double amin, double amax, double bmin, 
     GC(cudaStreamSynchronize(st));
     rd.use_grid = true;
     if (getenv("GWN_TRACE"))
-      fprintf(stderr, "[gwn] round grid %d x %d, %d entries for %lld leaves\n", ga, gb, total,
-              (long long)n);
+      fprintf(stderr, "[gwn] round grid %d x %d, %d entries for %lld leaves (%.2f per cell)\n",
+              ga, gb, total, (long long)n, (double)total / ((double)ga * gb));
   }
 out:
 #undef GC
