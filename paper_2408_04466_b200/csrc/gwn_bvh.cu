@@ -617,23 +617,47 @@ static cudaError_t build_subleaves(Round& rd, cudaStream_t st) {
   SC(cudaMalloc(&offs, sizeof(int64_t) * (n + 1)));
   SC(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, offs, (int)(n + 1), st));
   SC(cudaMalloc(&tmp, tb));
-  for (;; level -= 2) {
-    if (level <= leaf_max_level()) {
-      if (tree_r < 1.0) {  // drop the certified-leaf trees, retry the fold trees alone
-        tree_r = INFINITY;
-        level = level0 + 2;
-        continue;
+  {
+    // ascending search: the deepest level (and, first, with the wide
+    // certified-node splitting) whose node count fits the budget; each
+    // deeper count costs ~4x the previous, so the search costs ~1.3 counts
+    auto count = [&](int lv, double tr, int64_t& tot) -> cudaError_t {
+      cudaError_t ce = cudaMemsetAsync(cnt + n, 0, sizeof(int64_t), st);
+      if (ce != cudaSuccess) return ce;
+      k_foldtree<false><<<g, 128, 0, st>>>(n, rd.leaves, rd.proj, lv, tr, nullptr, cnt, nullptr,
+                                           nullptr, nullptr);
+      if ((ce = cudaGetLastError()) != cudaSuccess) return ce;
+      if ((ce = cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, offs, (int)(n + 1), st)) != cudaSuccess)
+        return ce;
+      if ((ce = cudaMemcpyAsync(&tot, offs + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st)) !=
+          cudaSuccess)
+        return ce;
+      return cudaStreamSynchronize(st);
+    };
+    int best = -1;
+    bool last_is_best = false;
+    const double trs[2] = {tree_r, INFINITY};
+    for (int pass = 0; pass < 2 && best < 0; ++pass) {
+      if (pass == 1 && !(trs[0] < 1.0)) break;
+      int64_t t2 = 0, t1 = 0;  // the two previous counts (growth estimate)
+      for (int lv = leaf_max_level() + 2; lv <= level0; lv += 2) {
+        // skip a count whose geometric estimate is far over the budget
+        if (t2 > 0 && t1 > 0 && (double)t1 * ((double)t1 / (double)t2) > 1.5 * (double)budget)
+          break;
+        int64_t tot = 0;
+        SC(count(lv, trs[pass], tot));
+        last_is_best = tot <= budget;
+        if (!last_is_best) break;
+        best = lv;
+        tree_r = trs[pass];
+        total = tot;
+        t2 = t1;
+        t1 = tot;
       }
-      goto out;  // nothing fits: keep the plain fallback
     }
-    SC(cudaMemsetAsync(cnt + n, 0, sizeof(int64_t), st));
-    k_foldtree<false><<<g, 128, 0, st>>>(n, rd.leaves, rd.proj, level, tree_r, nullptr, cnt,
-                                         nullptr, nullptr, nullptr);
-    SC(cudaGetLastError());
-    SC(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, offs, (int)(n + 1), st));
-    SC(cudaMemcpyAsync(&total, offs + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC(cudaStreamSynchronize(st));
-    if (total <= budget) break;
+    if (best < 0) goto out;  // nothing fits: keep the plain fallback
+    level = best;
+    if (!last_is_best) SC(count(level, tree_r, total));
   }
   if (total > 0) {
     SC(cudaMalloc(&rd.sub, sizeof(LeafRec) * total));
