@@ -94,8 +94,27 @@ __device__ __forceinline__ bool finalize_one(
   return push;
 }
 
+// Last block of a K5 launch: copy the round's scalar block (eval counters
+// and round scalars) into mapped pinned host memory -- the host's one round
+// trip per round reads it after the stream sync, no D2H copy op.
+__device__ __forceinline__ void publish_scalars(unsigned long long* __restrict__ done,
+                                                const unsigned long long* __restrict__ blk,
+                                                unsigned long long* __restrict__ host, int nblk) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long prev = atomicAdd(done, 1ull);
+    if (prev == (unsigned long long)gridDim.x - 1) {
+      __threadfence();
+      for (int k = 0; k < nblk; ++k)
+        host[k] = *(volatile const unsigned long long*)(blk + k);
+      __threadfence_system();
+    }
+  }
+}
+
 // K5: per active query decide done / jitter / re-shoot.
-__global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
+__device__ __forceinline__ void finalize_body(int32_t m, const int32_t* __restrict__ active,
                            const int32_t* __restrict__ chi, const int32_t* __restrict__ flags,
                            const double* __restrict__ bpart, int nchunk, int round, int max_rounds,
                            int max_jitters, uint64_t seed, int64_t index_base,
@@ -106,11 +125,11 @@ __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
                            int32_t* __restrict__ next, int32_t* __restrict__ next_n,
                            const unsigned long long* __restrict__ pair_count,
                            unsigned long long pair_cap) {
-  if (*pair_count > pair_cap) return;  // candidate buffer overflowed: round is re-run
   int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   bool push = false;
   int32_t q = 0;
-  if (s < m) {
+  // candidate buffer overflowed: the round is re-run (nothing written)
+  if (s < m && *pair_count <= pair_cap) {
     q = active ? active[s] : s;
     const int32_t f = flags[s];
     // boundary term: per-chunk partial angles summed in chunk order
@@ -133,11 +152,29 @@ __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
   }
 }
 
+__global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
+                           const int32_t* __restrict__ chi, const int32_t* __restrict__ flags,
+                           const double* __restrict__ bpart, int nchunk, int round, int max_rounds,
+                           int max_jitters, uint64_t seed, int64_t index_base,
+                           const int64_t* __restrict__ qidx, double jscale,
+                           const double* __restrict__ q0, double* __restrict__ pos,
+                           int8_t* __restrict__ jit, int8_t* __restrict__ jreason,
+                           double* __restrict__ w_out, int8_t* __restrict__ st_out,
+                           int32_t* __restrict__ next, int32_t* __restrict__ next_n,
+                           const unsigned long long* __restrict__ pair_count,
+                           unsigned long long pair_cap, unsigned long long* done,
+                           const unsigned long long* blk, unsigned long long* host, int nblk) {
+  finalize_body(m, active, chi, flags, bpart, nchunk, round, max_rounds, max_jitters, seed,
+                index_base, qidx, jscale, q0, pos, jit, jreason, w_out, st_out, next, next_n,
+                pair_count, pair_cap);
+  publish_scalars(done, blk, host, nblk);
+}
+
 // K5, round 0 with the identity slot map (the common case): four queries per
 // thread with 16-byte loads of chi / flags / partials and 16- and 4-byte
 // stores of w / status; flagged queries (rare) take finalize_one and a plain
 // atomic append.
-__global__ void k_finalize4(int32_t m, const int32_t* __restrict__ chi,
+__device__ __forceinline__ void finalize4_body(int32_t m, const int32_t* __restrict__ chi,
                             const int32_t* __restrict__ flags, const double* __restrict__ bpart,
                             int nchunk, int max_rounds, int max_jitters, uint64_t seed,
                             int64_t index_base, const int64_t* __restrict__ qidx, double jscale,
@@ -147,7 +184,7 @@ __global__ void k_finalize4(int32_t m, const int32_t* __restrict__ chi,
                             int32_t* __restrict__ next, int32_t* __restrict__ next_n,
                             const unsigned long long* __restrict__ pair_count,
                             unsigned long long pair_cap) {
-  if (*pair_count > pair_cap) return;
+  if (*pair_count > pair_cap) return;  // the round is re-run
   const int32_t s0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   if (s0 >= m) return;
   if (s0 + 4 > m) {  // ragged tail: scalar
@@ -191,6 +228,23 @@ __global__ void k_finalize4(int32_t m, const int32_t* __restrict__ chi,
                      jscale, q0, pos, jit, jreason, w_out, st_out))
       next[atomicAdd(next_n, 1)] = s;
   }
+}
+
+__global__ void k_finalize4(int32_t m, const int32_t* __restrict__ chi,
+                            const int32_t* __restrict__ flags, const double* __restrict__ bpart,
+                            int nchunk, int max_rounds, int max_jitters, uint64_t seed,
+                            int64_t index_base, const int64_t* __restrict__ qidx, double jscale,
+                            const double* __restrict__ q0, double* __restrict__ pos,
+                            int8_t* __restrict__ jit, int8_t* __restrict__ jreason,
+                            double* __restrict__ w_out, int8_t* __restrict__ st_out,
+                            int32_t* __restrict__ next, int32_t* __restrict__ next_n,
+                            const unsigned long long* __restrict__ pair_count,
+                            unsigned long long pair_cap, unsigned long long* done,
+                            const unsigned long long* blk, unsigned long long* host, int nblk) {
+  finalize4_body(m, chi, flags, bpart, nchunk, max_rounds, max_jitters, seed, index_base, qidx,
+                 jscale, q0, pos, jit, jreason, w_out, st_out, next, next_n, pair_count,
+                 pair_cap);
+  publish_scalars(done, blk, host, nblk);
 }
 
 // GWN_TRACE=1: host wall-clock trace of the eval phases (development aid)
@@ -266,11 +320,14 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   // auto chunk: 4M queries (2M when the boundary partials are wide)
   const int64_t chunk_max = sc->prm.chunk_queries > 0 ? sc->prm.chunk_queries
                             : boundary_chunks(sc, 0) > 16 ? (1ll << 21) : (1ll << 22);
-  // device scalar block, copied to pinned host memory once per round:
+  // device scalar block, published to mapped pinned memory once per round
+  // by K5's last block:
   // [0, CNT_N) eval counters, CNT_N + [0] candidate count, [1] next active
-  // count, [4] fallback items, [5] Newton items, [6] overflow, [7] Newton work
+  // count, [2] K5 blocks done, [4] fallback items, [5] Newton items, [6] overflow,
+  // [7] Newton work
   constexpr int kBlk = CNT_N + 8;
   int64_t* h_scalar = nullptr;
+  unsigned long long* h_map = nullptr;  // device view of h_scalar (mapped)
   const double* d_q = queries;
   double* d_w = w_out;
   int8_t* d_st = status_out;
@@ -291,8 +348,13 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     // pinned round scalars: one small buffer per host thread (gwn_eval
     // synchronises its stream before returning, so reuse is safe)
     static thread_local int64_t* t_pinned = nullptr;
-    if (!t_pinned) CKE(cudaMallocHost(&t_pinned, kBlk * sizeof(int64_t)));
+    static thread_local unsigned long long* t_map = nullptr;
+    if (!t_pinned) {
+      CKE(cudaHostAlloc(&t_pinned, kBlk * sizeof(int64_t), cudaHostAllocMapped));
+      CKE(cudaHostGetDevicePointer((void**)&t_map, t_pinned, 0));
+    }
     h_scalar = t_pinned;
+    h_map = t_map;
   }
   g_tl = getenv("GWN_TIMELINE") ? &tl : nullptr;
   tl_mark(st, "start");
@@ -447,19 +509,18 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
               m, chi, fl, bterm, nchunk, sc->prm.max_rounds, sc->prm.max_jitters,
               sc->prm.dir_seed, index_base + c0, qidx ? qidx + c0 : nullptr,
               sc->prm.jitter_scale * sc->diag, q0, pos, jit, jreason, d_w + c0, d_st + c0, nxt,
-              (int32_t*)(rsc + 1), rsc, (unsigned long long)pair_cap);
+              (int32_t*)(rsc + 1), rsc, (unsigned long long)pair_cap, rsc + 2, d_cnt, h_map, kBlk);
         } else {
           k_finalize<<<(m + 127) / 128, 128, 0, st>>>(
               m, active, chi, fl, bterm, nchunk, r, sc->prm.max_rounds, sc->prm.max_jitters,
               sc->prm.dir_seed, index_base + c0, qidx ? qidx + c0 : nullptr,
               sc->prm.jitter_scale * sc->diag, q0, pos, jit,
               jreason, d_w + c0, d_st + c0, nxt, (int32_t*)(rsc + 1), rsc,
-              (unsigned long long)pair_cap);
+              (unsigned long long)pair_cap, rsc + 2, d_cnt, h_map, kBlk);
         }
         CKE(cudaGetLastError());
         ++launches;
-        CKE(cudaMemcpyAsync(h_scalar, d_cnt, sizeof(unsigned long long) * kBlk,
-                            cudaMemcpyDeviceToHost, st));
+        // (K5's last block publishes the scalar block into h_scalar: mapped)
         if (sc->timed) CKE(cudaEventRecord(ev[4], st));
         tl_mark(st, "finalize+d2h done");
         tr.mark("round launched");
