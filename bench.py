@@ -179,6 +179,32 @@ def run_reference(args, spec, rank, world):
     return 0
 
 
+def boundary_roofline(G, torch, dev, stream, peak_tf, nq=1 << 20, k=3):
+    """K4 (the open-scene kernel) on config 3's scene, 2^20 queries: algorithmic
+    FP64 flops (device segment counter x FLOP_SEGMENT) over its CUDA-event
+    time, best of k -- a side measurement: the bench workload (config 2) is
+    closed and has no net boundary."""
+    from paper_2408_04466_b200 import scenes
+    s = scenes.make(3, nq)
+    sc = G.Scene(s.ctrl)
+    q = torch.from_numpy(s.queries).to(dev)
+    G.winding_numbers(sc, q, stream=stream.cuda_stream)
+    sc.set_timing(True)
+    best, segs = float("inf"), 0
+    for _ in range(k):
+        G.winding_numbers(sc, q, stream=stream.cuda_stream)
+        st = sc.stats()
+        if st["ms_boundary"] < best:
+            best, segs = st["ms_boundary"], st["boundary_segments"]
+    sc.set_timing(False)
+    ach = segs * FLOP_SEGMENT / (best * 1e-3) / 1e12
+    return {"workload": f"config3 scene (64 patches, {sc.n_net_segments} net segments), "
+                        f"{nq} queries", "kernel": "k_boundary_e (K4 fan term)",
+            "bound": "fp64", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": ach / peak_tf if peak_tf else None, "kernel_ms": best,
+            "segment_pairs": segs}
+
+
 def ray_reuse(G, torch, sc, dev, stream, n=256, k=5):
     """voxel centres of the scene AABB at n^3 through
     gwn_eval_rays (n^2 rays along +x) against gwn_eval of the same points,
@@ -377,6 +403,8 @@ def main():
         }
         if world == 1 and not args.no_ray_reuse:
             out["ray_reuse"] = ray_reuse(G, torch, sc, dev, stream)
+        if world == 1 and not args.no_ray_reuse:
+            out["roofline_open_scene"] = boundary_roofline(G, torch, dev, stream, peak_tf)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(spec, args.cpu_seconds)
         print(json.dumps(out), flush=True)
