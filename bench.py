@@ -59,7 +59,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--queries", type=int, default=0, help="override query count")
+    ap.add_argument("--queries", type=int, default=0,
+                    help="override the per-GPU query count (weak scaling) / total (strong)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every GPU evaluates the config's query count (total grows "
+                         "with N); strong: the config's queries are split over the GPUs")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ray-reuse", action="store_true",
@@ -166,7 +170,8 @@ def run_reference(args, spec, rank, world):
     line = {
         "impl": "reference", "metric": "winding-number queries/sec", "value": v,
         "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+        "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY.md §8(d))",
         "config": {"workload": CONFIG_DESC[spec.config], "n_patches": spec.n_patches,
                    "queries": int(len(spec.queries)), "sample_per_step": n},
@@ -259,7 +264,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     from paper_2408_04466_b200 import scenes
-    spec = scenes.make(args.config, args.queries or None)
+    base = args.queries or scenes.FULL_QUERIES[args.config]
+    # weak scaling: N x the per-GPU count from the same seeded generator
+    total = base * world if args.scaling == "weak" else base
+    spec = scenes.make(args.config, total)
     if args.impl == "reference":
         return run_reference(args, spec, rank, world)
 
@@ -372,7 +380,8 @@ def main():
         out = {
             "metric": "winding-number queries/sec", "value": value, "unit": "queries/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
-            "ms_per_step": ms_dev / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_dev / args.steps, "higher_is_better": True,
+            "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, SURVEY.md §8(d); no public dataset)",
             "config": {"workload": CONFIG_DESC[args.config], "n_patches": spec.n_patches,
