@@ -296,10 +296,16 @@ using namespace gwn;
     }                                                                          \
   } while (0)
 
-static cudaError_t ensure_round(gwn_scene* sc, int r, cudaStream_t st) {
+// Round r of the scene (built on first use); the pointer stays valid for
+// the scene's lifetime (deque), taken under the scene mutex.
+static cudaError_t ensure_round(gwn_scene* sc, int r, cudaStream_t st, const Round** out) {
   std::lock_guard<std::mutex> lk(sc->mu);
-  if ((int)sc->rounds.size() > r) return cudaSuccess;
-  return build_round(sc, r, st);
+  if ((int)sc->rounds.size() <= r) {
+    const cudaError_t e = build_round(sc, r, st);
+    if (e != cudaSuccess) return e;
+  }
+  *out = &sc->rounds[r];
+  return cudaSuccess;
 }
 
 static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t index_base,
@@ -436,14 +442,16 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
       const int32_t* active = nullptr;
       int cur = 0;
       if (sort_q) {
-        CKE(ensure_round(sc, 0, st));
-        CKE(launch_query_order(sc->rounds[0], mc, q0, order_tmp, act[1], st));
+        const Round* r0 = nullptr;
+        CKE(ensure_round(sc, 0, st, &r0));
+        CKE(launch_query_order(*r0, mc, q0, order_tmp, act[1], st));
         active = act[1];  // round 0 writes its re-shoot list into act[0]
         launches += 3;
       }
       for (int r = 0; r < sc->prm.max_rounds && m > 0;) {
-        CKE(ensure_round(sc, r, st));
-        const Round& rd = sc->rounds[r];
+        const Round* rdp = nullptr;
+        CKE(ensure_round(sc, r, st, &rdp));
+        const Round& rd = *rdp;
         // candidate capacity from the scene's running estimate
         int64_t want = (int64_t)(sc->pairs_per_query * 1.25 * m) + 4096;
         if (want > pair_cap) {
@@ -587,7 +595,10 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     fprintf(stderr, "[gwn] fallback: max nodes/item %llu, slowest batch: %llu cycles tree %llu code %llu items %llu, max levels %llu\n",
             h_cnt[CNT_MAXNODES], h_cnt[CNT_BIGITEMS] >> 24, (h_cnt[CNT_BIGITEMS] >> 16) & 255, (h_cnt[CNT_BIGITEMS] >> 8) & 255, h_cnt[CNT_BIGITEMS] & 255, h_cnt[CNT_MAXLEVELS]);
   stats.kernel_launches = launches;
-  sc->stats = stats;
+  {
+    std::lock_guard<std::mutex> lk(sc->mu);
+    sc->stats = stats;
+  }
   tl_mark(st, "outputs copied");
   tr.mark("outputs copied");
 done:

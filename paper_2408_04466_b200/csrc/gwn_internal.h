@@ -16,6 +16,7 @@
 #include <array>
 #include <mutex>
 #include <utility>
+#include <deque>
 #include <vector>
 
 #include "../../include/gwn_b200.h"
@@ -127,11 +128,13 @@ struct gwn_scene {
   double* band_h = nullptr;     // (n_edges)
   // per-round caches
   std::mutex mu;
-  std::vector<gwn::Round> rounds;
+  // deques: push_back never moves existing rounds, so a Round* taken under
+  // `mu` stays valid while other threads add rounds
+  std::deque<gwn::Round> rounds;
   // candidate (query, leaf) pairs per query seen so far (buffer sizing)
   double pairs_per_query = 4.0;
   // rounds for explicit ray directions (ray reuse), keyed by direction
-  std::vector<std::pair<std::array<double, 3>, gwn::Round>> dir_rounds;
+  std::deque<std::pair<std::array<double, 3>, gwn::Round>> dir_rounds;
   // last-eval stats
   gwn_stats stats;
   int timed = 0;

@@ -142,8 +142,15 @@ using namespace gwn;
     }                                                                          \
   } while (0)
 
-static cudaError_t dir_round(gwn_scene* sc, const double d[3], Round** out, cudaStream_t st) {
+// Round for an explicit ray direction: cached per scene (up to kDirCache
+// directions, never evicted, so a cached Round* stays valid for the scene's
+// lifetime); past the cache the call builds a private round (*owned) that it
+// frees when done.
+constexpr size_t kDirCache = 8;
+static cudaError_t dir_round(gwn_scene* sc, const double d[3], Round** out, Round* owned,
+                             bool* is_owned, cudaStream_t st) {
   std::lock_guard<std::mutex> lk(sc->mu);
+  *is_owned = false;
   for (auto& kv : sc->dir_rounds)
     if (kv.first[0] == d[0] && kv.first[1] == d[1] && kv.first[2] == d[2]) {
       *out = &kv.second;
@@ -152,9 +159,11 @@ static cudaError_t dir_round(gwn_scene* sc, const double d[3], Round** out, cuda
   Round rd;
   cudaError_t e = build_round_dir(sc, d, rd, st);
   if (e != cudaSuccess) return e;
-  if (sc->dir_rounds.size() >= 8) {  // small LRU-less cache: drop the oldest
-    free_round(sc->dir_rounds.front().second);
-    sc->dir_rounds.erase(sc->dir_rounds.begin());
+  if (sc->dir_rounds.size() >= kDirCache) {
+    *owned = rd;
+    *is_owned = true;
+    *out = owned;
+    return cudaSuccess;
   }
   sc->dir_rounds.push_back({{d[0], d[1], d[2]}, rd});
   *out = &sc->dir_rounds.back().second;
@@ -182,6 +191,8 @@ extern "C" int gwn_eval_rays(gwn_scene* sc, const double* origins, int64_t R,
   int64_t nq = 0;
   double d[3];
   Round* rd = nullptr;
+  Round rd_owned;
+  bool rd_is_owned = false;
   gwn_stats stats;
   memset(&stats, 0, sizeof stats);
   if (!sc || R < 0 || !direction || (R > 0 && (!origins || !ts || !offs || !w_out || !status_out))) {
@@ -226,7 +237,7 @@ extern "C" int gwn_eval_rays(gwn_scene* sc, const double* origins, int64_t R,
       CKR(cudaStreamSynchronize(st));
     }
     if (nq > 0) {
-      CKR(dir_round(sc, d, &rd, st));
+      CKR(dir_round(sc, d, &rd, &rd_owned, &rd_is_owned, st));
       const int32_t m = (int32_t)R;
       double* rpos = dalloc<double>(bufs, 3 * R, st, ae);
       double* rt0 = dalloc<double>(bufs, R, st, ae);
@@ -354,12 +365,16 @@ extern "C" int gwn_eval_rays(gwn_scene* sc, const double* origins, int64_t R,
       stats.newton_iters = (int64_t)hc[CNT_NEWTON];
       stats.roots = (int64_t)hc[CNT_ROOTS];
       stats.boundary_segments = (int64_t)hc[CNT_SEGMENTS];
-      sc->stats = stats;
+      {
+    std::lock_guard<std::mutex> lk(sc->mu);
+    sc->stats = stats;
+  }
       if (rays_cast) *rays_cast = R;
     }
   }
 done:
   for (void* p : bufs) cudaFreeAsync(p, st);
   cudaStreamSynchronize(st);
+  if (rd_is_owned) free_round(rd_owned);
   return rc;
 }

@@ -377,6 +377,7 @@ extern "C" int gwn_stats_get(const gwn_scene* sc, gwn_stats* out) {
     set_error("gwn_stats_get: null argument");
     return GWN_E_INVALID;
   }
+  std::lock_guard<std::mutex> lk(const_cast<gwn_scene*>(sc)->mu);
   *out = sc->stats;
   return GWN_OK;
 }

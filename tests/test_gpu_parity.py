@@ -248,3 +248,29 @@ def test_samples_per_edge_parity():
     s = scenes.make(1, 1000)
     for S in (2, 50, 1900):
         _edge_compare(s.ctrl, s.queries, samples_per_edge=S)
+
+
+def test_concurrent_evals_on_distinct_streams():
+    """gwn_eval is reentrant on distinct streams (include/gwn_b200.h): two host
+    threads on one scene, including a re-shoot round built concurrently."""
+    import threading
+    s, sc = _scene(3)
+    ref_w, ref_st = G.winding_numbers(sc, s.queries)
+    out = {}
+
+    def run(k):
+        st = torch.cuda.Stream()
+        q = torch.from_numpy(s.queries).cuda()
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                w, t = G.winding_numbers(sc, q)
+            st.synchronize()
+            out[k] = (w.cpu().numpy(), t.cpu().numpy())
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for k in range(2):
+        assert np.array_equal(out[k][0], ref_w) and np.array_equal(out[k][1], ref_st)
