@@ -36,11 +36,14 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
-# Algorithmic FP64 flops per unit of work (FMA = 2), counted from the kernel
-# source:
-FLOP_NEWTON = 234.0    # K3 Newton iteration: 2 Bernstein bases, value + partials
-                       # of A and B (2 x 88), 2x2 solve
-FLOP_ROOT = 110.0      # K3 accepted root: C value/partials, normal, record tests
+# Algorithmic FP64 flops per unit of work (FMA = 2).  K3: SURVEY.md §8(d)'s
+# per-unit figures for the reference algorithm's work units (a Newton
+# iteration evaluates the map and its partials in the Bernstein basis and
+# solves the 2x2 system; an accepted root adds C, the normal and the record
+# tests).  The kernel's Horner form of the same iteration executes fewer
+# (142), so achieved counts work done, not instructions issued.
+FLOP_NEWTON = 220.0    # K3 Newton iteration (220 per N_newton)
+FLOP_ROOT = 200.0      # K3 accepted root (200 per N_root)
 FLOP_SEGMENT = 34.0    # K4 per (query, net segment) in the ray frame: vertex (3 sub, |r|^2 5,
                        # rsqrt seed + Halley 8, u 4) + num 3, den 5, complex product 6
 

@@ -22,19 +22,46 @@
 
 namespace gwn {
 
+// cubic Bernstein coefficients -> power basis (p(t) = c0 + c1 t + c2 t^2 + c3 t^3)
+__device__ __forceinline__ void bern_to_pow(double& p0, double& p1, double& p2, double& p3) {
+  const double c1 = 3.0 * (p1 - p0);
+  const double c2 = 3.0 * (p0 - 2.0 * p1 + p2);
+  const double c3 = (p3 - p0) + 3.0 * (p1 - p2);
+  p1 = c1;
+  p2 = c2;
+  p3 = c3;
+}
+
+// Projected control nets of every patch in the round's frame (Bernstein, K1
+// and the fallback) and the same nets in the tensor power basis, index
+// 4*i+j = coefficient of u^i v^j (K3 Newton evaluates them by Horner).
 __global__ void k_project(const double* __restrict__ ctrl, int64_t P, Frame f,
-                          double* __restrict__ proj) {
+                          double* __restrict__ proj, double* __restrict__ powc) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   const double* X = ctrl + 48 * p;
   double* out = proj + 48 * p;
+  double net[48];
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     double x = X[3 * k], y = X[3 * k + 1], z = X[3 * k + 2];
-    out[k] = x * f.e1[0] + y * f.e1[1] + z * f.e1[2];
-    out[16 + k] = x * f.e2[0] + y * f.e2[1] + z * f.e2[2];
-    out[32 + k] = x * f.d[0] + y * f.d[1] + z * f.d[2];
+    net[k] = x * f.e1[0] + y * f.e1[1] + z * f.e1[2];
+    net[16 + k] = x * f.e2[0] + y * f.e2[1] + z * f.e2[2];
+    net[32 + k] = x * f.d[0] + y * f.d[1] + z * f.d[2];
   }
+#pragma unroll
+  for (int k = 0; k < 48; ++k) out[k] = net[k];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double* N = net + 16 * c;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bern_to_pow(N[4 * i], N[4 * i + 1], N[4 * i + 2], N[4 * i + 3]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bern_to_pow(N[j], N[4 + j], N[8 + j], N[12 + j]);
+  }
+  double* pw = powc + 48 * p;
+#pragma unroll
+  for (int k = 0; k < 48; ++k) pw[k] = net[k];
 }
 
 // Adaptive leaf sub-patches of every patch for this direction: depth-first
@@ -694,6 +721,7 @@ void free_round(Round& rd) {
   if (rd.subgc) cudaFree(rd.subgc);
   if (rd.sub_offs) cudaFree(rd.sub_offs);
   if (rd.proj) cudaFree(rd.proj);
+  if (rd.powc) cudaFree(rd.powc);
   if (rd.nodes) cudaFree(rd.nodes);
   if (rd.leafbox) cudaFree(rd.leafbox);
   if (rd.leaves) cudaFree(rd.leaves);
@@ -744,7 +772,8 @@ cudaError_t build_round_dir(gwn_scene* sc, const double d[3], Round& rd, cudaStr
     if (e != cudaSuccess) goto out; \
   } while (0)
       RC(cudaMalloc(&rd.proj, sizeof(double) * 48 * P));
-      k_project<<<pb, 128, 0, st>>>(sc->ctrl, P, rd.f, rd.proj);
+      RC(cudaMalloc(&rd.powc, sizeof(double) * 48 * P));
+      k_project<<<pb, 128, 0, st>>>(sc->ctrl, P, rd.f, rd.proj, rd.powc);
       RC(cudaGetLastError());
       // leaves: count, scan, fill
       RC(cudaMalloc(&lcount, sizeof(int64_t) * (P + 1)));

@@ -170,6 +170,16 @@ __global__ void k_finalize(int32_t m, const int32_t* __restrict__ active,
   publish_scalars(done, blk, host, nblk);
 }
 
+__device__ __forceinline__ void finalize4_group(int32_t s0, int32_t m,
+                            const int32_t* __restrict__ chi,
+                            const int32_t* __restrict__ flags, const double* __restrict__ bpart,
+                            int nchunk, int max_rounds, int max_jitters, uint64_t seed,
+                            int64_t index_base, const int64_t* __restrict__ qidx, double jscale,
+                            const double* __restrict__ q0, double* __restrict__ pos,
+                            int8_t* __restrict__ jit, int8_t* __restrict__ jreason,
+                            double* __restrict__ w_out, int8_t* __restrict__ st_out,
+                            int32_t* __restrict__ next, int32_t* __restrict__ next_n);
+
 // K5, round 0 with the identity slot map (the common case): four queries per
 // thread with 16-byte loads of chi / flags / partials and 16- and 4-byte
 // stores of w / status; flagged queries (rare) take finalize_one and a plain
@@ -185,8 +195,24 @@ __device__ __forceinline__ void finalize4_body(int32_t m, const int32_t* __restr
                             const unsigned long long* __restrict__ pair_count,
                             unsigned long long pair_cap) {
   if (*pair_count > pair_cap) return;  // the round is re-run
-  const int32_t s0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
-  if (s0 >= m) return;
+  // grid-stride over groups of four: a few blocks per SM keep the
+  // publish_scalars completion counter (one atomic per block) short
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 4 * g < m;
+       g += (int64_t)gridDim.x * blockDim.x)
+    finalize4_group((int32_t)(4 * g), m, chi, flags, bpart, nchunk, max_rounds, max_jitters,
+                    seed, index_base, qidx, jscale, q0, pos, jit, jreason, w_out, st_out, next,
+                    next_n);
+}
+
+__device__ __forceinline__ void finalize4_group(int32_t s0, int32_t m,
+                            const int32_t* __restrict__ chi,
+                            const int32_t* __restrict__ flags, const double* __restrict__ bpart,
+                            int nchunk, int max_rounds, int max_jitters, uint64_t seed,
+                            int64_t index_base, const int64_t* __restrict__ qidx, double jscale,
+                            const double* __restrict__ q0, double* __restrict__ pos,
+                            int8_t* __restrict__ jit, int8_t* __restrict__ jreason,
+                            double* __restrict__ w_out, int8_t* __restrict__ st_out,
+                            int32_t* __restrict__ next, int32_t* __restrict__ next_n) {
   if (s0 + 4 > m) {  // ragged tail: scalar
     for (int32_t s = s0; s < m; ++s) {
       double ang = 0.0;
@@ -513,7 +539,8 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
                           ((uintptr_t)(d_st + c0) & 3) == 0;
         if (vec4) {
           const int32_t nth = (m + 3) / 4;
-          k_finalize4<<<(nth + 127) / 128, 128, 0, st>>>(
+          const int nb4 = std::min((nth + 127) / 128, 4 * sc->sm_count);
+          k_finalize4<<<nb4, 128, 0, st>>>(
               m, chi, fl, bterm, nchunk, sc->prm.max_rounds, sc->prm.max_jitters,
               sc->prm.dir_seed, index_base + c0, qidx ? qidx + c0 : nullptr,
               sc->prm.jitter_scale * sc->diag, q0, pos, jit, jreason, d_w + c0, d_st + c0, nxt,

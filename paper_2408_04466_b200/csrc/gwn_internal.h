@@ -85,6 +85,7 @@ struct CellEnt {
 struct Round {
   Frame f;
   double* proj = nullptr;      // (P,48)
+  double* powc = nullptr;      // (P,48) proj in the power basis (K3 Newton, Horner)
   int64_t n_leaves = 0;
   LeafRec* leaves = nullptr;   // (n_leaves) adaptive leaf sub-patches
   double* leafbox = nullptr;   // (n_leaves,5) cull boxes: a lo/hi, b lo/hi, c max

@@ -428,6 +428,14 @@ struct RootResult {
 // Newton on the whole patch from (u, v); residual / domain / t acceptance of
 // surfaces.py:665-670, record fields of surfaces.py:681-697 in the
 // right-handed ray frame (d = (0,0,1)).
+// 16-byte read-only load the compiler may not hoist out of a loop: kReload
+// Newton re-reads the (L1-resident) A/B nets every iteration instead of
+// holding 32 doubles in registers, which buys occupancy.
+__device__ __forceinline__ void ldg2_keep(const double* p, double& x, double& y) {
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "l"(p));
+}
+
+template <bool kReload = false>
 __device__ __forceinline__ RootResult newton_solve(const double* __restrict__ P48, double qa,
                                                    double qb, double qc, double u, double v,
                                                    const DevParams& prm) {
@@ -440,8 +448,16 @@ __device__ __forceinline__ RootResult newton_solve(const double* __restrict__ P4
   for (int it = 0; it < kNewtonMax; ++it) {
     bern3(u, bu, dbu);
     bern3(v, bv, dbv);
-    eval_coord(P48, bu, dbu, bv, dbv, A, Au, Av);
-    eval_coord(P48 + 16, bu, dbu, bv, dbv, B, Bu, Bv);
+    if (kReload) {
+      double X[32];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) ldg2_keep(P48 + 2 * k, X[2 * k], X[2 * k + 1]);
+      eval_coord(X, bu, dbu, bv, dbv, A, Au, Av);
+      eval_coord(X + 16, bu, dbu, bv, dbv, B, Bu, Bv);
+    } else {
+      eval_coord(P48, bu, dbu, bv, dbv, A, Au, Av);
+      eval_coord(P48 + 16, bu, dbu, bv, dbv, B, Bu, Bv);
+    }
     A -= qa;
     B -= qb;
     r.iters++;
@@ -497,6 +513,118 @@ __device__ __forceinline__ RootResult newton_solve(const double* __restrict__ P4
   }
   double C, Cu, Cv;
   eval_coord(P48 + 32, bu, dbu, bv, dbv, C, Cu, Cv);
+  u -= du;
+  v -= dv;
+  r.u = u;
+  r.v = v;
+  const double tol = prm.domain_tol;                                   // surfaces.py:668
+  if (!(u >= -tol && u <= 1.0 + tol && v >= -tol && v <= 1.0 + tol)) {
+    r.status = ROOT_REJECTED;
+    return r;
+  }
+  r.t = C - qc - (Cu * du + Cv * dv);
+  if (r.t < -prm.t_tol) {                                              // surfaces.py:670
+    r.status = ROOT_REJECTED;
+    return r;
+  }
+  const double nx = Bu * Cv - Cu * Bv, ny = Cu * Av - Au * Cv, nz = Au * Bv - Bu * Av;
+  const double nn = sqrt(nx * nx + ny * ny + nz * nz);
+  r.sign = 1; r.tang = 1; r.graze = 1;
+  if (!(nn < prm.degenerate)) {                                        // surfaces.py:684-687
+    const double dd = nz / nn;
+    r.sign = dd > 0.0 ? 1 : -1;                                        // surfaces.py:695
+    r.tang = fabs(dd) <= prm.tangent;                                  // :696 tangency
+    const double bd = fmin(fmin(u, 1.0 - u), fmin(v, 1.0 - v));
+    r.graze = bd < prm.edge_graze;                                     // :697 grazing
+  }
+  r.onsurf = fabs(r.t) <= prm.on_surface_t;
+  r.status = ROOT_ACCEPTED;
+  return r;
+}
+
+// Value and partials of one coordinate net in the tensor power basis (W[4i+j]
+// = coefficient of u^i v^j) by Horner: 33 fp64 ops (61 flops, FMA = 2)
+// against 44 for the Bernstein form plus its two basis evaluations.
+__device__ __forceinline__ void eval_pow(const double* __restrict__ W, double u, double v,
+                                         double u3, double v3, double& f, double& fu,
+                                         double& fv) {
+  double R[4], Rv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double a0 = W[4 * i], a1 = W[4 * i + 1], a2 = W[4 * i + 2], a3 = W[4 * i + 3];
+    R[i] = fma(fma(fma(a3, v, a2), v, a1), v, a0);
+    Rv[i] = fma(fma(v3, a3, a2 + a2), v, a1);
+  }
+  f = fma(fma(fma(R[3], u, R[2]), u, R[1]), u, R[0]);
+  fu = fma(fma(u3, R[3], R[2] + R[2]), u, R[1]);
+  fv = fma(fma(fma(Rv[3], u, Rv[2]), u, Rv[1]), u, Rv[0]);
+}
+
+// newton_solve with the nets in the power basis (K3 Newton pass): identical
+// iteration, stopping rule, acceptance (surfaces.py:665-670) and record
+// fields (surfaces.py:681-697); only the evaluation of the map differs (by
+// rounding).  W48 = (A, B, C) power coefficients of the patch (Round::powc).
+template <bool kReload = false>
+__device__ __forceinline__ RootResult newton_solve_pow(const double* __restrict__ W48, double qa,
+                                                       double qb, double qc, double u, double v,
+                                                       const DevParams& prm) {
+  RootResult r;
+  r.iters = 0;
+  double A = 0, Au = 0, Av = 0, B = 0, Bu = 0, Bv = 0;
+  double du = 0.0, dv = 0.0;
+  bool conv = false;
+  for (int it = 0; it < kNewtonMax; ++it) {
+    const double u3 = 3.0 * u, v3 = 3.0 * v;
+    if (kReload) {
+      double X[32];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) ldg2_keep(W48 + 2 * k, X[2 * k], X[2 * k + 1]);
+      eval_pow(X, u, v, u3, v3, A, Au, Av);
+      eval_pow(X + 16, u, v, u3, v3, B, Bu, Bv);
+    } else {
+      eval_pow(W48, u, v, u3, v3, A, Au, Av);
+      eval_pow(W48 + 16, u, v, u3, v3, B, Bu, Bv);
+    }
+    A -= qa;
+    B -= qb;
+    r.iters++;
+    const double det = Au * Bv - Av * Bu;
+    if (!(fabs(det) > 0.0)) break;
+    const double id = 1.0 / det;
+    const double su = (Bv * A - Av * B) * id, sv = (Au * B - Bu * A) * id;
+    if (!isfinite(su) || !isfinite(sv)) break;
+    if (fabs(su) <= GWN_NEWTON_STOP * fmax(1.0, fabs(u)) &&
+        fabs(sv) <= GWN_NEWTON_STOP * fmax(1.0, fabs(v)) &&
+        (GWN_NEWTON_STOP > 1e-11 || sqrt(A * A + B * B) <= prm.residual)) {
+      du = su;
+      dv = sv;
+      conv = true;
+      if (GWN_NEWTON_STOP > 1e-11) {
+        A = 0.0;
+        B = 0.0;
+      }
+      break;
+    }
+    u -= su;
+    v -= sv;
+    if (fabs(u) > 8.0 || fabs(v) > 8.0) break;
+  }
+  if (!conv) {
+    eval_pow(W48, u, v, 3.0 * u, 3.0 * v, A, Au, Av);
+    eval_pow(W48 + 16, u, v, 3.0 * u, 3.0 * v, B, Bu, Bv);
+    A -= qa;
+    B -= qb;
+  }
+  r.t = 0.0;
+  r.sign = 0; r.tang = 0; r.graze = 0; r.onsurf = 0;
+  if (!(sqrt(A * A + B * B) <= prm.residual)) {                        // surfaces.py:665
+    r.u = u;
+    r.v = v;
+    r.status = ROOT_DIVERGED;
+    return r;
+  }
+  double C, Cu, Cv;
+  eval_pow(W48 + 32, u, v, 3.0 * u, 3.0 * v, C, Cu, Cv);
   u -= du;
   v -= dv;
   r.u = u;

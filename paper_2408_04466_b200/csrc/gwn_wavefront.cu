@@ -24,6 +24,7 @@ struct WaveArgs {
   const LeafRec* leaves;  // round leaves (patch of a fallback item)
   const double* qproj;
   const double* proj;
+  const double* powc;   // proj in the power basis (Newton pass)
   DevParams prm;
   int32_t* chi;
   int32_t* flags;
@@ -47,13 +48,10 @@ struct WaveArgs {
 
 // Newton solve of a certified (leaf or fold sub-leaf) candidate + ownership:
 // adds the owned root's sign to chi and its flags to fl.
-__device__ __forceinline__ void newton_accept(const WaveArgs& w, int32_t slot, int32_t patch,
-                                              uint64_t code, double u, double v, double qa,
-                                              double qb, double qc, int32_t& chi, int32_t& fl,
-                                              unsigned long long& iters,
-                                              unsigned long long& roots) {
-  const double* P48 = w.proj + 48 * (int64_t)patch;
-  RootResult r = newton_solve(P48, qa, qb, qc, u, v, w.prm);
+__device__ __forceinline__ void newton_own(const WaveArgs& w, int32_t slot, uint64_t code,
+                                           const RootResult& r, int32_t& chi, int32_t& fl,
+                                           unsigned long long& iters,
+                                           unsigned long long& roots) {
   iters += r.iters;
   const int level = code_level(code);
   const double wu = code_wu(level), wv = code_wv(level);
@@ -85,6 +83,16 @@ __device__ __forceinline__ void newton_accept(const WaveArgs& w, int32_t slot, i
       }
     }
   }
+}
+
+__device__ __forceinline__ void newton_accept(const WaveArgs& w, int32_t slot, int32_t patch,
+                                              uint64_t code, double u, double v, double qa,
+                                              double qb, double qc, int32_t& chi, int32_t& fl,
+                                              unsigned long long& iters,
+                                              unsigned long long& roots) {
+  const double* P48 = w.proj + 48 * (int64_t)patch;
+  const RootResult r = newton_solve(P48, qa, qb, qc, u, v, w.prm);
+  newton_own(w, slot, code, r, chi, fl, iters, roots);
 }
 
 // K3 pass 0: one thread per (query, leaf) candidate.  The leaf's Krawczyk
@@ -344,28 +352,81 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
 }
 
 // Newton pass over the certified leaves + ownership + K5 part 1.
+//
+// Dynamic fetch, 32 items per warp: blocks that start late (the fallback
+// kernel holds part of every SM) find the queue drained instead of owning a
+// fixed share of it.  The fetch is software-pipelined one batch deep: the
+// atomic that reserves batch b+1 and the loads of its items are issued before
+// batch b is solved, so neither the atomic's round trip nor the item load sits
+// on the critical path (ncu on config 2: the two stalls were 26% of the
+// samples without the pipeline).
 #ifndef GWN_NEWTON_MINB
-#define GWN_NEWTON_MINB 1
+#define GWN_NEWTON_MINB 3
 #endif
+#ifndef GWN_NEWTON_RELOAD
+#define GWN_NEWTON_RELOAD 0
+#endif
+#ifndef GWN_NEWTON_PREFETCH
+#define GWN_NEWTON_PREFETCH 1
+#endif
+#ifndef GWN_NEWTON_BERNSTEIN
+#define GWN_NEWTON_BERNSTEIN 0
+#endif
+__device__ __forceinline__ void newton_item_run(const WaveArgs& w, const NewtonItem& it,
+                                                int32_t& chi, int32_t& fl,
+                                                unsigned long long& iters,
+                                                unsigned long long& roots) {
+#if GWN_NEWTON_BERNSTEIN
+  const double* P48 = w.proj + 48 * (int64_t)it.patch;
+  RootResult r = newton_solve<GWN_NEWTON_RELOAD != 0>(P48, it.qa, it.qb, it.qc, it.u, it.v,
+                                                      w.prm);
+#else
+  const double* W48 = w.powc + 48 * (int64_t)it.patch;
+  RootResult r = newton_solve_pow<GWN_NEWTON_RELOAD != 0>(W48, it.qa, it.qb, it.qc, it.u, it.v,
+                                                          w.prm);
+#endif
+  newton_own(w, it.slot, it.code, r, chi, fl, iters, roots);
+}
+
+// Work-counter reservation.  nvcc/ptxas expand atomicAdd (inline-PTX
+// atom.add too) into a warp-aggregated sequence whose SHFL consumes the
+// result at once, which put the atomic's round trip back on the critical
+// path (13.5% of the stall samples at config 2 with the pipelined fetch).
+// atom.inc with a limit the counter never reaches is left alone (ptxas turns
+// a 0xffffffff limit back into an add), so the counter counts 32-item batches
+// (low word of n_work, zeroed per round) and the result is consumed a batch
+// later.
+__device__ __forceinline__ unsigned long long reserve_batch(unsigned long long* p) {
+  unsigned old;
+  asm volatile("atom.global.inc.u32 %0, [%1], %2;"
+               : "=r"(old) : "l"(p), "r"(0x7fffffffu) : "memory");
+  return 32ull * old;
+}
+
 __global__ void __launch_bounds__(128, GWN_NEWTON_MINB) k3_newton(WaveArgs w) {
   const int64_t n = (int64_t)min(*w.n_count, w.n_cap);
   unsigned long long iters = 0, roots = 0;
   const int lane = threadIdx.x & 31;
-  // dynamic fetch, 32 items per warp: blocks that start late (the fallback
-  // kernel holds part of every SM) find the queue drained instead of owning
-  // a fixed share of it
-  for (;;) {
-    unsigned long long b = 0;
-    if (lane == 0) b = atomicAdd(w.n_work, 32ull);
-    const int64_t base = (int64_t)__shfl_sync(0xffffffffu, b, 0);
-    if (base >= n) break;
-    const int64_t i = base + lane;
+#if GWN_NEWTON_PREFETCH == 1
+  unsigned long long b_cur = 0, b_nxt = 0;
+  if (lane == 0) {
+    b_cur = reserve_batch(w.n_work);
+    b_nxt = reserve_batch(w.n_work);
+  }
+  int64_t base = (int64_t)__shfl_sync(0xffffffffu, b_cur, 0);
+  NewtonItem it{};
+  if (base + lane < n) it = w.nq[base + lane];
+  while (base < n) {
+    // reservations are monotone, so the next batch starts past this one and
+    // every reserved batch below n is solved
+    const int64_t nbase = (int64_t)__shfl_sync(0xffffffffu, b_nxt, 0);
+    NewtonItem nx{};
+    if (nbase + lane < n) nx = w.nq[nbase + lane];
+    if (lane == 0 && nbase < n) b_nxt = reserve_batch(w.n_work);
     int32_t slot = -1, chi = 0, fl = 0;
-    if (i < n) {
-      const NewtonItem it = w.nq[i];
+    if (base + lane < n) {
       slot = it.slot;
-      newton_accept(w, it.slot, it.patch, it.code, it.u, it.v, it.qa, it.qb, it.qc, chi, fl,
-                    iters, roots);
+      newton_item_run(w, it, chi, fl, iters, roots);
     }
     // segmented warp-shuffle reduction keyed by query slot, one atomic per run
     const bool tail = seg_reduce(slot, chi, fl);
@@ -373,7 +434,33 @@ __global__ void __launch_bounds__(128, GWN_NEWTON_MINB) k3_newton(WaveArgs w) {
       if (chi) atomicAdd(&w.chi[slot], chi);
       if (fl) atomicOr(&w.flags[slot], fl);
     }
+    it = nx;
+    base = nbase;
   }
+#else
+  // GWN_NEWTON_PREFETCH=0: no pipelining; 2: only the atomic runs one batch
+  // ahead (2 registers instead of a whole prefetched item)
+  unsigned long long b = 0;
+  if (GWN_NEWTON_PREFETCH == 2 && lane == 0) b = reserve_batch(w.n_work);
+  for (;;) {
+    if (GWN_NEWTON_PREFETCH != 2 && lane == 0) b = reserve_batch(w.n_work);
+    const int64_t base = (int64_t)__shfl_sync(0xffffffffu, b, 0);
+    if (base >= n) break;
+    if (GWN_NEWTON_PREFETCH == 2 && lane == 0) b = reserve_batch(w.n_work);
+    const int64_t i = base + lane;
+    int32_t slot = -1, chi = 0, fl = 0;
+    if (i < n) {
+      const NewtonItem it = w.nq[i];
+      slot = it.slot;
+      newton_item_run(w, it, chi, fl, iters, roots);
+    }
+    const bool tail = seg_reduce(slot, chi, fl);
+    if (slot >= 0 && tail) {
+      if (chi) atomicAdd(&w.chi[slot], chi);
+      if (fl) atomicOr(&w.flags[slot], fl);
+    }
+  }
+#endif
   warp_sum_u64(&w.counters[CNT_NEWTON], iters);
   warp_sum_u64(&w.counters[CNT_ROOTS], roots);
 }
@@ -410,7 +497,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
     g_dev = sc->device;
   }
   cudaError_t e = cudaSuccess;
-  WaveArgs w{rd.leaves, qproj, rd.proj, sc->dprm, chi, flags,
+  WaveArgs w{rd.leaves, qproj, rd.proj, rd.powc, sc->dprm, chi, flags,
              rec ? rec->rec : nullptr, rec ? rec->count : nullptr, rec ? rec->cap : 0ull,
              counters, Q.overflow, Q.nq, Q.n_count, Q.cap, newton_work,
              rd.sub_offs, rd.sub, rd.subbox, rd.subskip, rd.subgc, rd.sub_level};
