@@ -564,7 +564,15 @@ __device__ __forceinline__ void eval_pow(const double* __restrict__ W, double u,
 // iteration, stopping rule, acceptance (surfaces.py:665-670) and record
 // fields (surfaces.py:681-697); only the evaluation of the map differs (by
 // rounding).  W48 = (A, B, C) power coefficients of the patch (Round::powc).
-template <bool kReload = false>
+// 16-byte shared-memory load the compiler may not hoist (see ldg2_keep)
+__device__ __forceinline__ void lds2_keep(const double* p, double& x, double& y) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+
+// kLoad: 0 = coefficients through the compiler (hoisted into registers),
+// 1 = re-read from global (L1) every iteration, 2 = re-read from shared
+template <int kLoad = 0>
 __device__ __forceinline__ RootResult newton_solve_pow(const double* __restrict__ W48, double qa,
                                                        double qb, double qc, double u, double v,
                                                        const DevParams& prm) {
@@ -575,10 +583,13 @@ __device__ __forceinline__ RootResult newton_solve_pow(const double* __restrict_
   bool conv = false;
   for (int it = 0; it < kNewtonMax; ++it) {
     const double u3 = 3.0 * u, v3 = 3.0 * v;
-    if (kReload) {
+    if (kLoad) {
       double X[32];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) ldg2_keep(W48 + 2 * k, X[2 * k], X[2 * k + 1]);
+      for (int k = 0; k < 16; ++k) {
+        if (kLoad == 2) lds2_keep(W48 + 2 * k, X[2 * k], X[2 * k + 1]);
+        else ldg2_keep(W48 + 2 * k, X[2 * k], X[2 * k + 1]);
+      }
       eval_pow(X, u, v, u3, v3, A, Au, Av);
       eval_pow(X + 16, u, v, u3, v3, B, Bu, Bv);
     } else {

@@ -358,32 +358,36 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
 // fixed share of it.  The fetch is software-pipelined one batch deep: the
 // atomic that reserves batch b+1 and the loads of its items are issued before
 // batch b is solved, so neither the atomic's round trip nor the item load sits
-// on the critical path (ncu on config 2: the two stalls were 26% of the
-// samples without the pipeline).
+// on the critical path.  (Measured at config 2: the stall samples move to the
+// coefficient loads; the step time is unchanged, the pipeline is kept.)
+// Scenes of at most kTabMaxP patches read the coefficients from a shared
+// memory table (k3_newton<true>): no registers hold them, so more warps fit.
 #ifndef GWN_NEWTON_MINB
 #define GWN_NEWTON_MINB 3
 #endif
-#ifndef GWN_NEWTON_RELOAD
-#define GWN_NEWTON_RELOAD 0
-#endif
-#ifndef GWN_NEWTON_PREFETCH
-#define GWN_NEWTON_PREFETCH 1
+#ifndef GWN_NEWTON_MINB_SMEM
+#define GWN_NEWTON_MINB_SMEM 5
 #endif
 #ifndef GWN_NEWTON_BERNSTEIN
 #define GWN_NEWTON_BERNSTEIN 0
 #endif
-__device__ __forceinline__ void newton_item_run(const WaveArgs& w, const NewtonItem& it,
-                                                int32_t& chi, int32_t& fl,
+// Patch table in shared memory (P <= kTabMaxP): power coefficients at a
+// padded stride, so lanes reading the same coefficient of different patches
+// hit different banks (100 words per patch: bank offset 4 per patch).
+constexpr int kTabStride = 50;
+constexpr int kTabMaxP = 96;  // 38.4 KB
+
+template <bool kSmem>
+__device__ __forceinline__ void newton_item_run(const WaveArgs& w, const double* tab,
+                                                const NewtonItem& it, int32_t& chi, int32_t& fl,
                                                 unsigned long long& iters,
                                                 unsigned long long& roots) {
 #if GWN_NEWTON_BERNSTEIN
   const double* P48 = w.proj + 48 * (int64_t)it.patch;
-  RootResult r = newton_solve<GWN_NEWTON_RELOAD != 0>(P48, it.qa, it.qb, it.qc, it.u, it.v,
-                                                      w.prm);
+  RootResult r = newton_solve(P48, it.qa, it.qb, it.qc, it.u, it.v, w.prm);
 #else
-  const double* W48 = w.powc + 48 * (int64_t)it.patch;
-  RootResult r = newton_solve_pow<GWN_NEWTON_RELOAD != 0>(W48, it.qa, it.qb, it.qc, it.u, it.v,
-                                                          w.prm);
+  const double* W48 = kSmem ? tab + kTabStride * it.patch : w.powc + 48 * (int64_t)it.patch;
+  RootResult r = newton_solve_pow<kSmem ? 2 : 0>(W48, it.qa, it.qb, it.qc, it.u, it.v, w.prm);
 #endif
   newton_own(w, it.slot, it.code, r, chi, fl, iters, roots);
 }
@@ -403,11 +407,18 @@ __device__ __forceinline__ unsigned long long reserve_batch(unsigned long long* 
   return 32ull * old;
 }
 
-__global__ void __launch_bounds__(128, GWN_NEWTON_MINB) k3_newton(WaveArgs w) {
+template <bool kSmem>
+__global__ void __launch_bounds__(128, kSmem ? GWN_NEWTON_MINB_SMEM : GWN_NEWTON_MINB)
+k3_newton(WaveArgs w, int32_t P) {
+  extern __shared__ double tab[];
+  if (kSmem) {
+    for (int k = threadIdx.x; k < 48 * P; k += blockDim.x)
+      tab[kTabStride * (k / 48) + k % 48] = w.powc[k];
+    __syncthreads();
+  }
   const int64_t n = (int64_t)min(*w.n_count, w.n_cap);
   unsigned long long iters = 0, roots = 0;
   const int lane = threadIdx.x & 31;
-#if GWN_NEWTON_PREFETCH == 1
   unsigned long long b_cur = 0, b_nxt = 0;
   if (lane == 0) {
     b_cur = reserve_batch(w.n_work);
@@ -426,7 +437,7 @@ __global__ void __launch_bounds__(128, GWN_NEWTON_MINB) k3_newton(WaveArgs w) {
     int32_t slot = -1, chi = 0, fl = 0;
     if (base + lane < n) {
       slot = it.slot;
-      newton_item_run(w, it, chi, fl, iters, roots);
+      newton_item_run<kSmem>(w, tab, it, chi, fl, iters, roots);
     }
     // segmented warp-shuffle reduction keyed by query slot, one atomic per run
     const bool tail = seg_reduce(slot, chi, fl);
@@ -437,37 +448,13 @@ __global__ void __launch_bounds__(128, GWN_NEWTON_MINB) k3_newton(WaveArgs w) {
     it = nx;
     base = nbase;
   }
-#else
-  // GWN_NEWTON_PREFETCH=0: no pipelining; 2: only the atomic runs one batch
-  // ahead (2 registers instead of a whole prefetched item)
-  unsigned long long b = 0;
-  if (GWN_NEWTON_PREFETCH == 2 && lane == 0) b = reserve_batch(w.n_work);
-  for (;;) {
-    if (GWN_NEWTON_PREFETCH != 2 && lane == 0) b = reserve_batch(w.n_work);
-    const int64_t base = (int64_t)__shfl_sync(0xffffffffu, b, 0);
-    if (base >= n) break;
-    if (GWN_NEWTON_PREFETCH == 2 && lane == 0) b = reserve_batch(w.n_work);
-    const int64_t i = base + lane;
-    int32_t slot = -1, chi = 0, fl = 0;
-    if (i < n) {
-      const NewtonItem it = w.nq[i];
-      slot = it.slot;
-      newton_item_run(w, it, chi, fl, iters, roots);
-    }
-    const bool tail = seg_reduce(slot, chi, fl);
-    if (slot >= 0 && tail) {
-      if (chi) atomicAdd(&w.chi[slot], chi);
-      if (fl) atomicOr(&w.flags[slot], fl);
-    }
-  }
-#endif
   warp_sum_u64(&w.counters[CNT_NEWTON], iters);
   warp_sum_u64(&w.counters[CNT_ROOTS], roots);
 }
 
-static int grid_for(const void* fn, int sm_count, int block = 128) {
+static int grid_for(const void* fn, int sm_count, int block = 128, size_t smem = 0) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem);
   if (per_sm < 1) per_sm = 1;
   return sm_count * per_sm;
 }
@@ -480,7 +467,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
                              int32_t* chi, int32_t* flags, unsigned long long* counters,
                              unsigned long long* newton_work, cudaEvent_t* ev4,
                              cudaEvent_t* join, const RecordSink* rec, cudaStream_t st) {
-  static thread_local int g_cand = 0, g_fb = 0, g_newton = 0, g_dev = -1;
+  static thread_local int g_cand = 0, g_fb = 0, g_newton = 0, g_newton_s = 0, g_dev = -1;
   if (g_dev != sc->device) {
     g_cand = grid_for((const void*)k3_candidates, sc->sm_count);
     // fallback: 3 blocks per SM spread its few, long-lived items thinly
@@ -492,8 +479,10 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
     // fallback blocks take the SMs (GWN_NEWTON_BPS > 0 caps blocks per SM)
     const char* e_nb = getenv("GWN_NEWTON_BPS");
     const int nbps = e_nb ? atoi(e_nb) : 0;
-    const int full = grid_for((const void*)k3_newton, sc->sm_count);
+    const int full = grid_for((const void*)k3_newton<false>, sc->sm_count);
     g_newton = nbps > 0 && sc->sm_count * nbps < full ? sc->sm_count * nbps : full;
+    g_newton_s = grid_for((const void*)k3_newton<true>, sc->sm_count, 128,
+                          sizeof(double) * kTabStride * kTabMaxP);
     g_dev = sc->device;
   }
   cudaError_t e = cudaSuccess;
@@ -541,7 +530,14 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
   }
   if (ev4) cudaEventRecord(ev4[4], st);
   tl_mark(st, "newton start");
-  k3_newton<<<g_newton, 128, 0, st>>>(w);
+  static const bool smem_ok = [] {
+    const char* e = getenv("GWN_NEWTON_SMEM");
+    return !(e && atoi(e) == 0);
+  }();
+  if (smem_ok && sc->P <= kTabMaxP)
+    k3_newton<true><<<g_newton_s, 128, sizeof(double) * kTabStride * sc->P, st>>>(w, (int32_t)sc->P);
+  else
+    k3_newton<false><<<g_newton, 128, 0, st>>>(w, (int32_t)sc->P);
   tl_mark(st, "newton done");
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev4) cudaEventRecord(ev4[3], st);
