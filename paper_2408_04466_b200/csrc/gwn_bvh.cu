@@ -540,8 +540,13 @@ static cudaError_t build_grid(Round& rd, double amin, double amax, double bmin, 
     // wider than any leaf-box expansion (<= 1e-12 (1 + mag) + 3e-9 patch extent)
     const double margin = 1e-8 * (1.0 + fabs(amin) + fabs(amax) + fabs(bmin) + fabs(bmax));
     const double x0 = amin - margin, x1 = amax + margin, y0 = bmin - margin, y1 = bmax + margin;
-    const double cw = fmax(0.5 * h[0] / (double)n, (x1 - x0) / 4096.0);
-    const double ch = fmax(0.5 * h[1] / (double)n, (y1 - y0) / 4096.0);
+    // cell = kf x the mean leaf-box extent (GWN_GRID_CELL overrides kf)
+    static const double kf = [] {
+      const char* e = getenv("GWN_GRID_CELL");
+      return e ? atof(e) : 0.5;
+    }();
+    const double cw = fmax(kf * h[0] / (double)n, (x1 - x0) / 4096.0);
+    const double ch = fmax(kf * h[1] / (double)n, (y1 - y0) / 4096.0);
     const int ga = (int)fmin(4096.0, fmax(1.0, ceil((x1 - x0) / cw)));
     const int gb = (int)fmin(4096.0, fmax(1.0, ceil((y1 - y0) / ch)));
     const int64_t ncell = (int64_t)ga * gb;

@@ -45,6 +45,57 @@ __device__ __forceinline__ long long warp_push(bool want, unsigned long long* co
   return (long long)idx;
 }
 
+// Block-aggregated reservation in two append queues: one atomic per queue
+// per call instead of one per warp.  Every warp of a kernel hammering the same
+// counter serialises at its L2 slice: the SHFL waiting for that atomic was
+// 30% of k3_candidates' and 15% of the cull's stall samples at config 2.
+// n0 / n1: this thread's item counts; o0 / o1: its first slots.  Every thread
+// of the block must call it (three barriers; the shared block is reusable on
+// return).  A null counter reserves nothing.
+template <int NW>
+struct BlockPush {
+  unsigned long long cnt[2][NW];
+  unsigned long long base[2];
+};
+
+template <int NW>
+__device__ __forceinline__ void block_reserve(BlockPush<NW>& S, int n0, int n1,
+                                              unsigned long long* c0, unsigned long long* c1,
+                                              unsigned long long& o0, unsigned long long& o1) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int i0 = n0, i1 = n1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v0 = __shfl_up_sync(0xffffffffu, i0, o);
+    const int v1 = __shfl_up_sync(0xffffffffu, i1, o);
+    if (lane >= o) {
+      i0 += v0;
+      i1 += v1;
+    }
+  }
+  if (lane == 31) {
+    S.cnt[0][wid] = (unsigned long long)i0;
+    S.cnt[1][wid] = (unsigned long long)i1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {  // thread q reserves queue q
+    const int q = threadIdx.x;
+    unsigned long long run = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      const unsigned long long t = S.cnt[q][k];
+      S.cnt[q][k] = run;
+      run += t;
+    }
+    unsigned long long* c = q ? c1 : c0;
+    S.base[q] = (run && c) ? atomicAdd(c, run) : 0ull;
+  }
+  __syncthreads();
+  o0 = S.base[0] + S.cnt[0][wid] + (unsigned long long)(i0 - n0);
+  o1 = S.base[1] + S.cnt[1][wid] + (unsigned long long)(i1 - n1);
+  __syncthreads();
+}
+
 __device__ __forceinline__ void warp_sum_u64(unsigned long long* dst, unsigned long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);

@@ -98,8 +98,11 @@ __device__ __forceinline__ void newton_accept(const WaveArgs& w, int32_t slot, i
 // K3 pass 0: one thread per (query, leaf) candidate.  The leaf's Krawczyk
 // data are query-independent (K1), so the test is ~40 flops: exclude,
 // certified (-> Newton item) or undecided (-> fallback item).
-__global__ void __launch_bounds__(128)
+constexpr int kCandBlock = 256;
+
+__global__ void __launch_bounds__(kCandBlock)
 k3_candidates(const unsigned long long* __restrict__ npairs_dev, K3Queues Q, WaveArgs w) {
+  __shared__ BlockPush<kCandBlock / 32> S;
   // on capacity overflow the engine discards and re-runs the round; never
   // read past the buffers
   const int64_t npairs = (int64_t)min(*npairs_dev, Q.cap);
@@ -123,10 +126,17 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev, K3Queues Q, Wav
       wantN = kr == 1;
       wantF = kr == 2;
     }
-    long long k = warp_push(wantF, Q.f_count, Q.cap, Q.overflow);
-    if (k >= 0) Q.fq[k] = NodeItem{slot, leaf, code};
-    k = warp_push(wantN, Q.n_count, Q.cap, Q.overflow);
-    if (k >= 0) Q.nq[k] = NewtonItem{slot, patch, code, nu_, nv_, qa, qb, qc, 0.0};
+    // (the loop bound is block-uniform, so every thread reaches the barriers)
+    unsigned long long kf = 0, kn = 0;
+    block_reserve(S, wantF ? 1 : 0, wantN ? 1 : 0, Q.f_count, Q.n_count, kf, kn);
+    if (wantF) {
+      if (kf < Q.cap) Q.fq[kf] = NodeItem{slot, leaf, code};
+      else *Q.overflow = 1;
+    }
+    if (wantN) {
+      if (kn < Q.cap) Q.nq[kn] = NewtonItem{slot, patch, code, nu_, nv_, qa, qb, qc, 0.0};
+      else *Q.overflow = 1;
+    }
   }
   warp_sum_u64(&w.counters[CNT_NODES], tested);
 }
@@ -469,7 +479,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
                              cudaEvent_t* join, const RecordSink* rec, cudaStream_t st) {
   static thread_local int g_cand = 0, g_fb = 0, g_newton = 0, g_newton_s = 0, g_dev = -1;
   if (g_dev != sc->device) {
-    g_cand = grid_for((const void*)k3_candidates, sc->sm_count);
+    g_cand = grid_for((const void*)k3_candidates, sc->sm_count, kCandBlock);
     // fallback: 3 blocks per SM spread its few, long-lived items thinly
     // (measured on config 2 against 1, 2, 4, 6, 8; GWN_FB_BPS overrides)
     const char* e_bps = getenv("GWN_FB_BPS");
@@ -492,7 +502,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
              rd.sub_offs, rd.sub, rd.subbox, rd.subskip, rd.subgc, rd.sub_level};
   if (ev4) cudaEventRecord(ev4[0], st);
   tl_mark(st, "k3 start");
-  k3_candidates<<<g_cand, 128, 0, st>>>(npairs_dev, Q, w);
+  k3_candidates<<<g_cand, kCandBlock, 0, st>>>(npairs_dev, Q, w);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // The fallback (few, latency-bound items) runs on a side stream,
   // concurrently with the Newton pass and K4; the engine joins it (`join`)
