@@ -290,17 +290,66 @@ struct Trace {
   }
 };
 
+// Per-thread, per-device eval workspace: one block carved by a bump
+// allocator and kept across evals.  gwn_eval synchronises its streams before
+// returning, so the next eval on the same thread may reuse the block; evals
+// on other threads have their own.  Requests past the block fall back to
+// stream-ordered allocations for this eval, and the block grows to the
+// high-water mark at the next one.  (One allocation per eval instead of
+// ~14: the host reaches the first kernel launch ~10 us sooner.)
+struct WsCache {
+  char* buf = nullptr;
+  size_t cap = 0, want = 0;
+  void* k3 = nullptr;  // K3 queue scratch, kept the same way
+  size_t k3_cap = 0;
+};
+static thread_local WsCache t_wscache[64];
+
 struct Workspace {
   cudaStream_t st;
   std::vector<void*> ptrs;
   cudaError_t err = cudaSuccess;
+  WsCache* c = nullptr;
+  size_t off = 0;
+  void begin(int device) {
+    c = &t_wscache[device & 63];
+    if (c->want > c->cap) {
+      if (c->buf) cudaFreeAsync(c->buf, st);
+      c->buf = nullptr;
+      c->cap = 0;
+      const size_t want = c->want + c->want / 4;
+      if (cudaMallocAsync((void**)&c->buf, want, st) == cudaSuccess) {
+        c->cap = want;
+      } else {
+        c->buf = nullptr;
+        cudaGetLastError();  // fall back to per-request allocations
+      }
+    }
+  }
   template <class T>
   T* get(size_t n) {
-    void* p = nullptr;
     if (err != cudaSuccess) return nullptr;
-    err = cudaMallocAsync(&p, n * sizeof(T) + 16, st);
+    const size_t bytes = (n * sizeof(T) + 16 + 255) & ~(size_t)255;
+    off += bytes;
+    if (c) c->want = std::max(c->want, off);
+    if (c && c->buf && off <= c->cap) return (T*)(c->buf + off - bytes);
+    void* p = nullptr;
+    err = cudaMallocAsync(&p, bytes, st);
     if (err == cudaSuccess) ptrs.push_back(p);
     return (T*)p;
+  }
+  // K3 scratch of at least `bytes` (cached; grows stream-ordered)
+  cudaError_t k3(size_t bytes, void** out) {
+    if (c->k3_cap < bytes) {
+      if (c->k3) cudaFreeAsync(c->k3, st);
+      c->k3 = nullptr;
+      c->k3_cap = 0;
+      const cudaError_t e = cudaMallocAsync(&c->k3, bytes, st);
+      if (e != cudaSuccess) return e;
+      c->k3_cap = bytes;
+    }
+    *out = c->k3;
+    return cudaSuccess;
   }
   void release() {
     for (void* p : ptrs) cudaFreeAsync(p, st);
@@ -391,6 +440,7 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   g_tl = getenv("GWN_TIMELINE") ? &tl : nullptr;
   tl_mark(st, "start");
   tr.mark("setup");
+  ws.begin(sc->device);
   d_cnt = ws.get<unsigned long long>(kBlk);
   CKE(ws.err);
   if (host) {
@@ -481,10 +531,8 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         // candidate capacity from the scene's running estimate
         int64_t want = (int64_t)(sc->pairs_per_query * 1.25 * m) + 4096;
         if (want > pair_cap) {
-          if (k3_scratch) CKE(cudaFreeAsync(k3_scratch, st));
-          k3_scratch = nullptr;
           pair_cap = want;
-          CKE(cudaMallocAsync(&k3_scratch, intersect_scratch_bytes(pair_cap), st));
+          CKE(ws.k3(intersect_scratch_bytes(pair_cap), &k3_scratch));
         }
         const K3Queues Q = k3_queues(k3_scratch, pair_cap, k3cnt);
         tr.mark("round setup");
@@ -604,7 +652,6 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         CKE(cudaMemcpyAsync(status_out + c0, d_st + c0, mc, cudaMemcpyDeviceToHost, cs_out));
       }
     }
-    if (k3_scratch) cudaFreeAsync(k3_scratch, st);
   }
   if (host && !pipe) {
     CKE(cudaMemcpyAsync(w_out, d_w, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
