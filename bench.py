@@ -56,6 +56,20 @@ CONFIG_DESC = {
 }
 
 
+def _traffic(kname: str, config: int, n: int):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu
+    --set full capture (profiles/roofline_traffic.json, config 2 at 2^20
+    queries), or None for another workload."""
+    if config != 2 or n != (1 << 20):
+        return None
+    try:
+        with open(os.path.join(HERE, "profiles", "roofline_traffic.json")) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None
+    return t.get(kname.split(" ")[0])
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -210,6 +224,8 @@ def boundary_roofline(G, torch, dev, stream, peak_tf, nq=1 << 20, k=3):
                         f"{nq} queries", "kernel": "k_boundary_e (K4 fan term)",
             "bound": "fp64", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
             "frac": ach / peak_tf if peak_tf else None, "kernel_ms": best,
+            "traffic": _traffic("k_boundary_e_config3_2^20", 2, 1 << 20) if nq == 1 << 20
+            else None,
             "segment_pairs": segs}
 
 
@@ -296,28 +312,27 @@ def main():
     w_pin = torch.empty(nq, dtype=torch.float64).pin_memory()
     st_pin = torch.empty(nq, dtype=torch.int8).pin_memory()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
-    w_all = torch.empty(per * world, dtype=torch.float64, device=dev)
-    st_all = torch.empty(per * world, dtype=torch.int8, device=dev)
-    w_pad = torch.zeros(per, dtype=torch.float64, device=dev)
-    st_pad = torch.zeros(per, dtype=torch.int8, device=dev)
+    # N > 1: the engine writes into this rank's packed (w, status) block and
+    # ONE all-gather assembles every rank's results (distributed.py)
+    from paper_2408_04466_b200.distributed import gather_packed, packed_shard
+    pbuf, w_pk, st_pk = packed_shard(per, dev)
+    g_all = torch.empty(world * pbuf.numel(), dtype=torch.uint8, device=dev)
+    if world > 1:
+        w_dev, st_dev = w_pk[:nq], st_pk[:nq]
 
     def step_device():
         G.winding_numbers(sc, q_dev, index_base=s0, out=(w_dev, st_dev),
                           stream=stream.cuda_stream)
         if world > 1:
-            w_pad[:nq].copy_(w_dev)
-            st_pad[:nq].copy_(st_dev)
-            dist.all_gather_into_tensor(w_all, w_pad)
-            dist.all_gather_into_tensor(st_all, st_pad)
+            gather_packed(pbuf, world, n_total, out=g_all)
 
     def step_e2e():
         G.winding_numbers(sc, q_pin, index_base=s0, out=(w_pin, st_pin),
                           stream=stream.cuda_stream)
         if world > 1:
-            w_pad[:nq].copy_(w_pin, non_blocking=True)
-            st_pad[:nq].copy_(st_pin, non_blocking=True)
-            dist.all_gather_into_tensor(w_all, w_pad)
-            dist.all_gather_into_tensor(st_all, st_pad)
+            w_pk[:nq].copy_(w_pin, non_blocking=True)
+            st_pk[:nq].copy_(st_pin, non_blocking=True)
+            gather_packed(pbuf, world, n_total, out=g_all)
 
     def timed(fn, k):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -400,7 +415,8 @@ def main():
             "gpu_launches": launches,
             "roofline": {"bound": "fp64", "kernel": kname, "achieved": achieved,
                          "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf if peak_tf else None, "traffic": None,
+                         "frac": achieved / peak_tf if peak_tf else None,
+                         "traffic": _traffic(kname, args.config, nq),
                          "peak_source": "FP64 DFMA-chain microbenchmark run live on this GPU "
                                         "(MEASURED_PEAKS.json has no FP64 entry)",
                          "kernel_ms": kms, "kernel_share_of_step":

@@ -1,5 +1,5 @@
 """Multi-GPU sharding: queries split across ranks, scene replicated, one
-all-gather of (w, status).  SURVEY.md §8(e): queries are independent, so the
+all-gather of the packed (w, status) block.  SURVEY.md §8(e): queries are independent, so the
 data path has exactly one collective -- NCCL all-gather over NVLink on B200
 boxes, gloo in the CPU tests.
 
@@ -22,6 +22,44 @@ def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int, int]:
     s = min(n, rank * per)
     e = min(n, s + per)
     return s, e, per
+
+
+def packed_shard(per: int, device):
+    """This rank's send buffer for the one all-gather: ``per`` float64 winding
+    numbers followed by ``per`` int8 status codes in one byte buffer
+    (``per`` rounded up to a multiple of 8 so every rank's float64 block stays
+    8-byte aligned in the gathered buffer).  Returns ``(buf, w_view, st_view)``;
+    the engine writes straight into the views (no staging copy)."""
+    import torch
+
+    per8 = (per + 7) // 8 * 8
+    buf = torch.zeros(9 * per8, dtype=torch.uint8, device=device)
+    w_view = buf[: 8 * per8].view(torch.float64)
+    st_view = buf[8 * per8:].view(torch.int8)
+    st_view.fill_(-1)  # padding slots past the rank's slice
+    return buf, w_view, st_view
+
+
+def gather_packed(buf, world: int, n: int, *, group=None, out=None):
+    """ONE all-gather of every rank's packed (w, status) block (SURVEY §8(e));
+    returns full-length ``(w, status)`` in global query order.  ``out`` may
+    pass a preallocated (world * len(buf),) uint8 receive buffer."""
+    import torch
+    import torch.distributed as dist
+
+    if out is None:
+        out = torch.empty(world * buf.numel(), dtype=torch.uint8, device=buf.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    per8 = buf.numel() // 9
+    blocks = out.view(world, 9 * per8)
+    w = blocks[:, : 8 * per8].reshape(-1).view(torch.float64).reshape(world, per8)
+    st = blocks[:, 8 * per8:].view(torch.int8)
+    return w, st
+
+
+def unpad(w, st, per: int, n: int):
+    """(world, per8) gathered blocks -> flat length-n results."""
+    return w[:, :per].reshape(-1)[:n], st[:, :per].reshape(-1)[:n]
 
 
 def sharded_winding_numbers(scene, queries, *, group=None, evaluate=None, device=None):
@@ -47,17 +85,11 @@ def sharded_winding_numbers(scene, queries, *, group=None, evaluate=None, device
     if device is None:
         device = torch.device("cuda", torch.cuda.current_device()) \
             if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    buf, w_view, st_view = packed_shard(per, device)
     w_loc, st_loc = evaluate(scene, queries[s:e], s)
-    w_loc = torch.as_tensor(np.asarray(w_loc) if not torch.is_tensor(w_loc) else w_loc,
-                            dtype=torch.float64).to(device)
-    st_loc = torch.as_tensor(np.asarray(st_loc) if not torch.is_tensor(st_loc) else st_loc,
-                             dtype=torch.int8).to(device)
-    w_pad = torch.zeros(per, dtype=torch.float64, device=device)
-    st_pad = torch.full((per,), -1, dtype=torch.int8, device=device)
-    w_pad[: e - s] = w_loc
-    st_pad[: e - s] = st_loc
-    w_all = torch.empty(per * world, dtype=torch.float64, device=device)
-    st_all = torch.empty(per * world, dtype=torch.int8, device=device)
-    dist.all_gather_into_tensor(w_all, w_pad, group=group)
-    dist.all_gather_into_tensor(st_all, st_pad, group=group)
-    return w_all[:n], st_all[:n]
+    w_view[: e - s] = torch.as_tensor(
+        np.asarray(w_loc) if not torch.is_tensor(w_loc) else w_loc, dtype=torch.float64).to(device)
+    st_view[: e - s] = torch.as_tensor(
+        np.asarray(st_loc) if not torch.is_tensor(st_loc) else st_loc, dtype=torch.int8).to(device)
+    w_all, st_all = gather_packed(buf, world, n, group=group)
+    return unpad(w_all, st_all, per, n)
