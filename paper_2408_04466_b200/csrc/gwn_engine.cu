@@ -587,7 +587,12 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
                           ((uintptr_t)(d_st + c0) & 3) == 0;
         if (vec4) {
           const int32_t nth = (m + 3) / 4;
-          const int nb4 = std::min((nth + 127) / 128, 4 * sc->sm_count);
+          static const int k5_bps = [] {  // K5 blocks per SM cap (GWN_K5_BPS; 0 = one group per thread)
+            const char* e = getenv("GWN_K5_BPS");
+            return e ? atoi(e) : 4;
+          }();
+          const int nb4 = k5_bps > 0 ? std::min((nth + 127) / 128, k5_bps * sc->sm_count)
+                                     : (nth + 127) / 128;
           k_finalize4<<<nb4, 128, 0, st>>>(
               m, chi, fl, bterm, nchunk, sc->prm.max_rounds, sc->prm.max_jitters,
               sc->prm.dir_seed, index_base + c0, qidx ? qidx + c0 : nullptr,
