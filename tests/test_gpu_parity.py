@@ -274,3 +274,33 @@ def test_concurrent_evals_on_distinct_streams():
         t.join()
     for k in range(2):
         assert np.array_equal(out[k][0], ref_w) and np.array_equal(out[k][1], ref_st)
+
+
+_NEWTON_PATH_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2408_04466_b200 as G
+from paper_2408_04466_b200 import scenes
+s = scenes.make(int(sys.argv[2]), 1 << 15)
+sc = G.Scene(s.ctrl)
+w, st = G.winding_numbers(sc, torch.from_numpy(s.queries).cuda())
+np.save(sys.argv[3], np.stack([w.cpu().numpy(), st.cpu().numpy().astype(np.float64)]))
+"""
+
+
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_newton_shared_table_equals_register_path(tmp_path, cfg):
+    """Scenes of <= 96 patches run K3 Newton from the shared-memory patch
+    table; GWN_NEWTON_SMEM=0 forces the register path.  Same arithmetic in the
+    same order, so the results must be bit-identical."""
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("1", "0"):
+        f = str(tmp_path / f"r{mode}.npy")
+        env = dict(os.environ, GWN_NEWTON_SMEM=mode)
+        subprocess.run([sys.executable, "-c", _NEWTON_PATH_SCRIPT, repo, str(cfg), f],
+                       env=env, check=True, timeout=300)
+        out[mode] = np.load(f)
+    assert np.array_equal(out["1"], out["0"])
