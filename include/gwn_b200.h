@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define GWN_ABI_VERSION 1
+#define GWN_ABI_VERSION 2
 
 /* return codes (negative = error) */
 #define GWN_OK 0
@@ -87,6 +87,7 @@ typedef struct gwn_scene_info {
   double diag;
   int32_t device;
   int32_t sm_count;
+  int64_t n_far_cycles;     /* boundary cycles with a far-field expansion    */
 } gwn_scene_info;
 
 /* Device-side counters of the last gwn_eval on a scene (for the roofline
@@ -105,6 +106,8 @@ typedef struct gwn_stats {
   double ms_k3_candidates, ms_k3_fallback, ms_k3_newton;  /* split of ms_intersect */
   int64_t k3_fallback_items;  /* undecided leaf candidates solved by the DFS fallback */
   int64_t k3_newton_items;    /* certified leaf candidates (Newton solves)          */
+  int64_t far_pairs;          /* (query, boundary cycle) pairs taken by the far-field
+                                 expansion instead of the exact fan sum */
 } gwn_stats;
 
 int gwn_abi_version(void);

@@ -62,7 +62,7 @@ class SceneInfo(C.Structure):
     _fields_ = [
         ("n_patches", C.c_int64), ("n_net_edges", C.c_int64), ("n_net_segments", C.c_int64),
         ("bbox_min", C.c_double * 3), ("bbox_max", C.c_double * 3), ("diag", C.c_double),
-        ("device", C.c_int32), ("sm_count", C.c_int32),
+        ("device", C.c_int32), ("sm_count", C.c_int32), ("n_far_cycles", C.c_int64),
     ]
 
 
@@ -75,6 +75,7 @@ class Stats(C.Structure):
         ("ms_other", C.c_double), ("ms_k3_candidates", C.c_double),
         ("ms_k3_fallback", C.c_double), ("ms_k3_newton", C.c_double),
         ("k3_fallback_items", C.c_int64), ("k3_newton_items", C.c_int64),
+        ("far_pairs", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

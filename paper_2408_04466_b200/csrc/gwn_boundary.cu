@@ -23,8 +23,10 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "gwn_fan.cuh"
+#include "gwn_farfield.cuh"
 
 namespace gwn {
 
@@ -245,13 +247,25 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
 #ifndef GWN_K4_MINB
 #define GWN_K4_MINB 2
 #endif
-template <int QPT>
+// kFF: far-field scene (gwn_farfield.cu).  Per edge, each query decides with
+// ff_far() whether the edge's cycle is taken by the far kernel; far queries
+// multiply their running product by (1, 0) (exactly neutral) and a warp whose
+// queries are all far skips the edge.  `order` (nullable) maps threads to
+// slots (3-D Morton order, so warps agree).
+struct FFView {
+  const int32_t* order;
+  const int32_t* edge;   // cycle of each edge, -1 = exact only
+  const double* g;       // cycle centres, round frame
+  const double* r2;      // R_min^2, line radius^2
+};
+
+template <int QPT, bool kFF>
 __global__ void __launch_bounds__(kBlockQ, GWN_K4_MINB)
 k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
              const double* __restrict__ vproj, int64_t V, int S, int64_t n_edges,
              const double* __restrict__ band_h, Frame f, DevParams prm,
              double* __restrict__ bpart, int32_t* __restrict__ flag_acc,
-             unsigned long long* __restrict__ counters) {
+             unsigned long long* __restrict__ counters, FFView ff) {
   const int nchunk = gridDim.y;
   const int64_t e0 = n_edges * blockIdx.y / nchunk, e1 = n_edges * (blockIdx.y + 1) / nchunk;
   const int ept = kTileV / S;  // whole edges per tile
@@ -260,22 +274,34 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
   double qa[QPT], qb[QPT], qc[QPT];
   SegState st[QPT];
   int flags[QPT], minhi[QPT], neg[QPT];
+  bool live[QPT];
 #pragma unroll
   for (int j = 0; j < QPT; ++j) {
-    slot[j] = blockIdx.x * (blockDim.x * QPT) + j * blockDim.x + threadIdx.x;
-    const bool live = slot[j] < m;
-    const int32_t q = live ? (active ? active[slot[j]] : slot[j]) : 0;
-    const double px = live ? pos[3 * (int64_t)q] : 0.0;
-    const double py = live ? pos[3 * (int64_t)q + 1] : 0.0;
-    const double pz = live ? pos[3 * (int64_t)q + 2] : 0.0;
-    qa[j] = px * f.e1[0] + py * f.e1[1] + pz * f.e1[2];
-    qb[j] = px * f.e2[0] + py * f.e2[1] + pz * f.e2[2];
-    qc[j] = px * f.d[0] + py * f.d[1] + pz * f.d[2];
+    // ordered (far-field) launches: a warp's QPT*32 queries are consecutive
+    // in Morton order, so they share one small region
+    const int32_t t = (kFF && ff.order)
+                          ? blockIdx.x * (blockDim.x * QPT) + (threadIdx.x & ~31) * QPT + j * 32 +
+                                (threadIdx.x & 31)
+                          : blockIdx.x * (blockDim.x * QPT) + j * blockDim.x + threadIdx.x;
+    live[j] = t < m;
+    slot[j] = (kFF && ff.order && live[j]) ? ff.order[t] : t;
+    const int32_t q = live[j] ? (active ? active[slot[j]] : slot[j]) : 0;
+    const double px = live[j] ? pos[3 * (int64_t)q] : 0.0;
+    const double py = live[j] ? pos[3 * (int64_t)q + 1] : 0.0;
+    const double pz = live[j] ? pos[3 * (int64_t)q + 2] : 0.0;
+    if (kFF) {
+      frame_q(f, px, py, pz, qa[j], qb[j], qc[j]);
+    } else {
+      qa[j] = px * f.e1[0] + py * f.e1[1] + pz * f.e1[2];
+      qb[j] = px * f.e2[0] + py * f.e2[1] + pz * f.e2[2];
+      qc[j] = px * f.d[0] + py * f.d[1] + pz * f.d[2];
+    }
     st[j] = SegState{1.0, 0.0, 0};
     flags[j] = 0;
     minhi[j] = 0x7fffffff;
     neg[j] = 0;
   }
+  unsigned long long exact_pairs = 0;  // (query, segment) pairs summed exactly
   VtxF va[QPT], vb[QPT];
   for (int64_t te = e0; te < e1; te += ept) {
     const int ne = (int)min((int64_t)ept, e1 - te);
@@ -291,6 +317,24 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
     __syncthreads();
     for (int e = 0; e < ne; ++e) {
       const int b = e * S;
+      // far queries of this edge's cycle: neutral factor (1, 0); skip the
+      // edge when the whole warp is far
+      bool far[QPT];
+#pragma unroll
+      for (int j = 0; j < QPT; ++j) far[j] = false;
+      if (kFF) {
+        const int c = __ldg(ff.edge + te + e);
+        bool all = true;
+        int nnear = 0;
+#pragma unroll
+        for (int j = 0; j < QPT; ++j) {
+          far[j] = c >= 0 && live[j] && ff_far(qa[j], qb[j], qc[j], ff.g + 3 * c, ff.r2 + 2 * c);
+          all &= far[j] || !live[j];
+          nnear += (live[j] && !far[j]) ? 1 : 0;
+        }
+        if (__all_sync(0xffffffffu, all)) continue;
+        exact_pairs += (unsigned long long)nnear * (unsigned long long)(S - 1);
+      }
 #pragma unroll
       for (int j = 0; j < QPT; ++j)
         va[j] = make_vtxf(sx[b], sy[b], sz[b], qa[j], qb[j], qc[j], minhi[j]);
@@ -303,8 +347,9 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
 #pragma unroll
           for (int j = 0; j < QPT; ++j) {
             vb[j] = make_vtxf(sx[k + h], sy[k + h], sz[k + h], qa[j], qb[j], qc[j], minhi[j]);
-            const double num = va[j].uy * vb[j].ux - va[j].ux * vb[j].uy;
-            const double den = va[j].ux * vb[j].ux + va[j].uy * vb[j].uy + va[j].uz * vb[j].uz;
+            double num = va[j].uy * vb[j].ux - va[j].ux * vb[j].uy;
+            double den = va[j].ux * vb[j].ux + va[j].uy * vb[j].uy + va[j].uz * vb[j].uz;
+            if (kFF && far[j]) { den = 1.0; num = 0.0; }
             neg[j] |= __double2hiint(den);
             cmul_track(st[j], den, num);
           }
@@ -312,8 +357,9 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
           for (int j = 0; j < QPT; ++j) {
             va[j] = make_vtxf(sx[k + h + 1], sy[k + h + 1], sz[k + h + 1], qa[j], qb[j], qc[j],
                               minhi[j]);
-            const double num = vb[j].uy * va[j].ux - vb[j].ux * va[j].uy;
-            const double den = vb[j].ux * va[j].ux + vb[j].uy * va[j].uy + vb[j].uz * va[j].uz;
+            double num = vb[j].uy * va[j].ux - vb[j].ux * va[j].uy;
+            double den = vb[j].ux * va[j].ux + vb[j].uy * va[j].uy + vb[j].uz * va[j].uz;
+            if (kFF && far[j]) { den = 1.0; num = 0.0; }
             neg[j] |= __double2hiint(den);
             cmul_track(st[j], den, num);
           }
@@ -325,8 +371,9 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
 #pragma unroll
         for (int j = 0; j < QPT; ++j) {
           vb[j] = make_vtxf(sx[k], sy[k], sz[k], qa[j], qb[j], qc[j], minhi[j]);
-          const double num = va[j].uy * vb[j].ux - va[j].ux * vb[j].uy;
-          const double den = va[j].ux * vb[j].ux + va[j].uy * vb[j].uy + va[j].uz * vb[j].uz;
+          double num = va[j].uy * vb[j].ux - va[j].ux * vb[j].uy;
+          double den = va[j].ux * vb[j].ux + va[j].uy * vb[j].uy + va[j].uz * vb[j].uz;
+          if (kFF && far[j]) { den = 1.0; num = 0.0; }
           neg[j] |= __double2hiint(den);
           cmul_track(st[j], den, num);
           va[j] = vb[j];
@@ -346,6 +393,10 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
         int mh = 0x7fffffff;
         for (int e = 0; e < ne; ++e) {
           const int b = e * S;
+          if (kFF) {  // far cycles: the line misses their sphere, no band
+            const int c = __ldg(ff.edge + te + e);
+            if (c >= 0 && ff_far(qa[j], qb[j], qc[j], ff.g + 3 * c, ff.r2 + 2 * c)) continue;
+          }
           const double h = __ldg(band_h + te + e);
           VtxF A = make_vtxf(sx[b], sy[b], sz[b], qa[j], qb[j], qc[j], mh);
           for (int i = b + 1; i < b + S; ++i) {
@@ -365,12 +416,16 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
     if (minhi[j] < kDegHi) flags[j] |= FLAG_DEGEN;
 #pragma unroll
   for (int j = 0; j < QPT; ++j) {
-    if (slot[j] < m) {
+    if (live[j]) {
       bpart[(int64_t)blockIdx.y * m + slot[j]] = seg_angle(st[j]);
       if (flags[j]) atomicOr(&flag_acc[slot[j]], flags[j]);
     }
   }
-  if (threadIdx.x == 0) {
+  if (kFF) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) exact_pairs += __shfl_down_sync(0xffffffffu, exact_pairs, o);
+    if ((threadIdx.x & 31) == 0 && exact_pairs) atomicAdd(&counters[CNT_SEGMENTS], exact_pairs);
+  } else if (threadIdx.x == 0) {
     int32_t nq = min((int32_t)(blockDim.x * QPT), m - (int32_t)(blockIdx.x * blockDim.x * QPT));
     const int64_t segs = (e1 - e0) * (int64_t)(S - 1);
     atomicAdd(&counters[CNT_SEGMENTS], (unsigned long long)(segs * nq));
@@ -416,6 +471,19 @@ cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st) {
   if (V == 0) return cudaSuccess;
   cudaError_t e = cudaMalloc(&rd.vproj, sizeof(double) * 3 * V);
   if (e != cudaSuccess) return e;
+  if (sc->ff_n > 0) {  // far-field cycle centres in this round's frame
+    std::vector<double> h(3 * (size_t)sc->ff_n);
+    for (int c = 0; c < sc->ff_n; ++c) {
+      const double* g = &sc->ff_g_host[3 * c];
+      h[3 * c] = g[0] * rd.f.e1[0] + g[1] * rd.f.e1[1] + g[2] * rd.f.e1[2];
+      h[3 * c + 1] = g[0] * rd.f.e2[0] + g[1] * rd.f.e2[1] + g[2] * rd.f.e2[2];
+      h[3 * c + 2] = g[0] * rd.f.d[0] + g[1] * rd.f.d[1] + g[2] * rd.f.d[2];
+    }
+    if ((e = cudaMalloc(&rd.ffg, sizeof(double) * h.size())) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(rd.ffg, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice)) !=
+        cudaSuccess)
+      return e;
+  }
   k_vproj<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(sc->verts, V, rd.f, rd.vproj);
   return cudaGetLastError();
 }
@@ -432,26 +500,48 @@ constexpr int kQPT = GWN_K4_QPT;
 int boundary_chunks(const gwn_scene* sc, int32_t m) {
   (void)m;
   if (sc->n_edges <= 0) return 1;
-  return (int)std::min<int64_t>(sc->n_edges, 64);
+  // exact edge chunks, then the far-field row (gwn_farfield.cu) when on
+  return (int)std::min<int64_t>(sc->n_edges, 64) + (sc->ff_n > 0 ? kFFRows : 0);
 }
 
+// nchunk partial rows: the exact kernel fills rows [0, nexact), the far
+// kernel the kFFRows rows after them (far-field scenes); `order` (nullable) is the exact
+// kernel's thread -> slot map (launch_ff_order).
 cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             const int32_t* active, const double* pos, double* bpart, int nchunk,
-                            int32_t* flags, unsigned long long* counters, cudaStream_t st) {
+                            int32_t* flags, unsigned long long* counters, cudaStream_t st,
+                            const int32_t* order) {
   if (m <= 0) return cudaSuccess;
   int64_t V = sc->n_edges * sc->S;
   if (V == 0) return cudaMemsetAsync(bpart, 0, sizeof(double) * m, st);
-  dim3 grid((m + kBlockQ * kQPT - 1) / (kBlockQ * kQPT), nchunk);
   static const bool generic = getenv("GWN_K4_GENERIC") != nullptr;  // A/B switch
-  if (sc->S <= kTileV && !generic)
-    k_boundary_e<kQPT><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S, sc->n_edges,
-                                                 sc->band_h, rd.f, sc->dprm, bpart, flags,
-                                                 counters);
-  else
+  const bool ff = sc->ff_n > 0 && rd.ffg;
+  const int nexact = nchunk - (sc->ff_n > 0 ? kFFRows : 0);
+  dim3 grid((m + kBlockQ * kQPT - 1) / (kBlockQ * kQPT), nexact);
+  cudaError_t e = cudaSuccess;
+  if (sc->S <= kTileV && !generic) {
+    if (ff) {
+      const FFView fv{order, sc->ff_edge, rd.ffg, sc->ff_r};
+      k_boundary_e<kQPT, true><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S,
+                                                         sc->n_edges, sc->band_h, rd.f, sc->dprm,
+                                                         bpart, flags, counters, fv);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      return launch_boundary_far(sc, rd, m, active, pos, bpart + (int64_t)nexact * m, counters,
+                                 st);
+    }
+    k_boundary_e<kQPT, false><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S,
+                                                        sc->n_edges, sc->band_h, rd.f, sc->dprm,
+                                                        bpart, flags, counters,
+                                                        FFView{nullptr, nullptr, nullptr, nullptr});
+  } else {
     k_boundary<kQPT><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S, sc->n_edges,
                                                sc->band_h, rd.f, sc->dprm, bpart, flags,
                                                counters);
-  return cudaGetLastError();
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (sc->ff_n > 0)  // exact path for everything: the far rows are zero
+    return cudaMemsetAsync(bpart + (int64_t)nexact * m, 0, sizeof(double) * m * kFFRows, st);
+  return cudaSuccess;
 }
 
 // _kernels.single_loop_batch (_kernels.py:801-823) on the GPU: one closed loop,

@@ -731,6 +731,7 @@ void free_round(Round& rd) {
   if (rd.leafbox) cudaFree(rd.leafbox);
   if (rd.leaves) cudaFree(rd.leaves);
   if (rd.vproj) cudaFree(rd.vproj);
+  if (rd.ffg) cudaFree(rd.ffg);
   if (rd.cell_offs) cudaFree(rd.cell_offs);
   if (rd.cell_ent) cudaFree(rd.cell_ent);
   rd = Round();

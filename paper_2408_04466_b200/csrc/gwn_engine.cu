@@ -493,6 +493,10 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     // it is opt-in; the grid cull does not need coherent queries)
     const bool sort_q = sc->P > 0 && cm >= 65536 && getenv("GWN_QUERY_ORDER");
     void* order_tmp = sort_q ? ws.get<char>(query_order_scratch_bytes((int32_t)cm)) : nullptr;
+    // far-field scenes: 3-D Morton order of each round's queries for K4
+    const bool ff_sort = sc->ff_n > 0 && cm >= 4096;
+    int32_t* ff_order = ff_sort ? ws.get<int32_t>((size_t)cm) : nullptr;
+    void* ff_tmp = ff_sort ? ws.get<char>(ff_order_scratch_bytes((int32_t)cm)) : nullptr;
     int64_t pair_cap = 0;
     void* k3_scratch = nullptr;  // K3 queues (fallback + Newton items)
     CKE(ws.err);
@@ -574,8 +578,14 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         // (closed scenes: no net boundary, B = 0, nothing to launch)
         const int nchunk = sc->n_edges > 0 ? boundary_chunks(sc, m) : 0;
         if (nchunk > 0) {
-          CKE(launch_boundary(sc, rd, m, active, rpos, bterm, nchunk, fl, d_cnt, st));
-          ++launches;
+          const int32_t* ord = nullptr;
+          if (ff_sort && m >= 4096) {
+            CKE(launch_ff_order(sc, m, active, rpos, ff_tmp, ff_order, st));
+            ord = ff_order;
+            launches += 2;
+          }
+          CKE(launch_boundary(sc, rd, m, active, rpos, bterm, nchunk, fl, d_cnt, st, ord));
+          launches += sc->ff_n > 0 ? 2 : 1;
         }
         if (sc->timed) CKE(cudaEventRecord(ev[3], st));
         // ---- K5: finalize / compact re-shoots (after the K3 side stream)
@@ -670,6 +680,7 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   stats.newton_iters = (int64_t)h_cnt[CNT_NEWTON];
   stats.roots = (int64_t)h_cnt[CNT_ROOTS];
   stats.boundary_segments = (int64_t)h_cnt[CNT_SEGMENTS];
+  stats.far_pairs = (int64_t)h_cnt[CNT_FAR];
   if (getenv("GWN_TRACE"))
     fprintf(stderr, "[gwn] fallback: max nodes/item %llu, slowest batch: %llu cycles tree %llu code %llu items %llu, max levels %llu\n",
             h_cnt[CNT_MAXNODES], h_cnt[CNT_BIGITEMS] >> 24, (h_cnt[CNT_BIGITEMS] >> 16) & 255, (h_cnt[CNT_BIGITEMS] >> 8) & 255, h_cnt[CNT_BIGITEMS] & 255, h_cnt[CNT_MAXLEVELS]);

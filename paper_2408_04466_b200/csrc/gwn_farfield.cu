@@ -1,0 +1,440 @@
+// gwn_farfield.cu -- far field of the boundary term (the
+// math and the error bound are in gwn_farfield.cuh and DESIGN.md §2 K4).
+//
+// Scene build (build_farfield): the net edges are grouped into closed cycles
+// (union-find on their bitwise-shared end points); every cycle gets its
+// centre g, bounding radius rho, unsigned fan area A_abs, the far radius
+// R_min from the truncation bound, and its double-layer moments D_n^m --
+// integrated on the device over the fan triangles (g, v_i, v_i+1) of the same
+// sampled polyline K4 sums (k_ff_moments, Gauss-Legendre on the collapsed
+// square, exact for the degree-(K-1) integrands).
+//
+// Per eval: k_boundary_far adds, for every far (query, cycle) pair,
+// Omega(p) = -sum D_n^m I_n^m(p - g) into one extra partial row; the exact
+// kernel masks (or, warp-uniformly, skips) those pairs' segments.  Queries
+// are put in 3-D Morton order for the exact kernel (launch_ff_order) so the
+// far / near decisions of a warp agree and whole cycles are skipped.
+#include <cub/cub.cuh>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <numeric>
+#include <vector>
+
+#include "gwn_farfield.cuh"
+
+namespace gwn {
+
+constexpr int kFFQ = 9;  // Gauss-Legendre points per direction (exact to degree 17 >= K)
+
+struct FFQuad {
+  double x[kFFQ], w[kFFQ];  // nodes / weights on [0, 1]
+};
+
+// Gauss-Legendre on [0, 1] by Newton on P_n (host)
+static FFQuad ff_quad() {
+  FFQuad q;
+  const int n = kFFQ;
+  for (int i = 0; i < n; ++i) {
+    double x = cos(M_PI * (i + 0.75) / (n + 0.5));
+    double dp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = x;
+      for (int k = 2; k <= n; ++k) {
+        const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      dp = n * (x * p1 - p0) / (x * x - 1.0);
+      const double dx = p1 / dp;
+      x -= dx;
+      if (fabs(dx) < 1e-16) break;
+    }
+    q.x[i] = 0.5 * (x + 1.0);
+    q.w[i] = 1.0 / ((1.0 - x * x) * dp * dp);  // 2 / ((1-x^2) P'^2) on [-1,1], halved
+  }
+  return q;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// D_n^m of one cycle per block: items (segment, quadrature point) over the
+// cycle's edges; the regular solid harmonics and their gradients by the
+// recurrences of gwn_farfield.cuh (dual numbers), one warp reduction and one
+// shared-memory add per term.
+__global__ void __launch_bounds__(256)
+k_ff_moments(const int64_t* __restrict__ coff, const int32_t* __restrict__ cedge,
+             const double* __restrict__ verts, int64_t V, int S, const double* __restrict__ g,
+             FFQuad Q, double* __restrict__ D) {
+  __shared__ double acc[2 * kFFTerms];
+  const int c = blockIdx.x;
+  for (int k = threadIdx.x; k < 2 * kFFTerms; k += blockDim.x) acc[k] = 0.0;
+  __syncthreads();
+  const int64_t e0 = coff[c], e1 = coff[c + 1];
+  const int64_t segs = (e1 - e0) * (S - 1);
+  const int64_t items = segs * kFFQ * kFFQ;
+  const double gx = g[3 * c], gy = g[3 * c + 1], gz = g[3 * c + 2];
+  for (int64_t base = 0; base < items; base += blockDim.x) {
+    const int64_t it = base + threadIdx.x;
+    double wq = 0.0, nx = 0.0, ny = 0.0, nz = 0.0, x = 0.0, y = 0.0, z = 0.0;
+    if (it < items) {
+      const int64_t sg = it / (kFFQ * kFFQ);
+      const int qp = (int)(it % (kFFQ * kFFQ));
+      const int64_t e = cedge[e0 + sg / (S - 1)];
+      const int64_t k = e * S + sg % (S - 1);
+      const double ax = verts[k] - gx, ay = verts[V + k] - gy, az = verts[2 * V + k] - gz;
+      const double bx = verts[k + 1] - gx, by = verts[V + k + 1] - gy,
+                   bz = verts[2 * V + k + 1] - gz;
+      nx = ay * bz - az * by;
+      ny = az * bx - ax * bz;
+      nz = ax * by - ay * bx;
+      const double u = Q.x[qp / kFFQ], v = Q.x[qp % kFFQ];
+      const double s = u, t = (1.0 - u) * v;
+      wq = Q.w[qp / kFFQ] * Q.w[qp % kFFQ] * (1.0 - u);
+      x = s * ax + t * bx;
+      y = s * ay + t * by;
+      z = s * az + t * bz;
+    }
+    const double r2 = x * x + y * y + z * z;
+    // diagonal R_m^m = -(x+iy)/(2m) R_{m-1}^{m-1}: value (re, im) and d/dx,y,z
+    double dR = 1.0, dI = 0.0, dxR = 0.0, dxI = 0.0, dyR = 0.0, dyI = 0.0, dzR = 0.0, dzI = 0.0;
+    for (int m = 0; m <= kFFK; ++m) {
+      if (m > 0) {
+        const double c0 = -1.0 / (2.0 * m);
+        // (x + iy) * (vR + i vI)
+        const double nR = x * dR - y * dI, nI = x * dI + y * dR;
+        const double nxR = dR + x * dxR - y * dxI, nxI = dI + x * dxI + y * dxR;
+        const double nyR = -dI + x * dyR - y * dyI, nyI = dR + x * dyI + y * dyR;
+        const double nzR = x * dzR - y * dzI, nzI = x * dzI + y * dzR;
+        dR = c0 * nR; dI = c0 * nI;
+        dxR = c0 * nxR; dxI = c0 * nxI;
+        dyR = c0 * nyR; dyI = c0 * nyI;
+        dzR = c0 * nzR; dzI = c0 * nzI;
+      }
+      // column n = m, m+1, ...: R_n = ((2n-1) z R_{n-1} - r^2 R_{n-2}) / ((n+m)(n-m))
+      double aR = dR, aI = dI, axR = dxR, axI = dxI, ayR = dyR, ayI = dyI, azR = dzR, azI = dzI;
+      double bR = 0, bI = 0, bxR = 0, bxI = 0, byR = 0, byI = 0, bzR = 0, bzI = 0;
+      for (int n = m; n <= kFFK; ++n) {
+        if (n > m) {
+          const double inv = 1.0 / ((double)(n + m) * (double)(n - m));
+          const double k1 = 2.0 * n - 1.0;
+          const double vR = (k1 * z * aR - r2 * bR) * inv, vI = (k1 * z * aI - r2 * bI) * inv;
+          const double vxR = (k1 * z * axR - (2.0 * x * bR + r2 * bxR)) * inv;
+          const double vxI = (k1 * z * axI - (2.0 * x * bI + r2 * bxI)) * inv;
+          const double vyR = (k1 * z * ayR - (2.0 * y * bR + r2 * byR)) * inv;
+          const double vyI = (k1 * z * ayI - (2.0 * y * bI + r2 * byI)) * inv;
+          const double vzR = (k1 * (aR + z * azR) - (2.0 * z * bR + r2 * bzR)) * inv;
+          const double vzI = (k1 * (aI + z * azI) - (2.0 * z * bI + r2 * bzI)) * inv;
+          bR = aR; bI = aI; bxR = axR; bxI = axI; byR = ayR; byI = ayI; bzR = azR; bzI = azI;
+          aR = vR; aI = vI; axR = vxR; axI = vxI; ayR = vyR; ayI = vyI; azR = vzR; azI = vzI;
+        }
+        if (n == 0) continue;
+        // n . conj(grad R) = (n.gradR_re) - i (n.gradR_im), times the weight
+        const double fr = warp_sum_d(wq * (nx * axR + ny * ayR + nz * azR));
+        const double fi = warp_sum_d(-wq * (nx * axI + ny * ayI + nz * azI));
+        if ((threadIdx.x & 31) == 0) {
+          atomicAdd(&acc[2 * ff_term(n, m)], fr);
+          atomicAdd(&acc[2 * ff_term(n, m) + 1], fi);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 2 * kFFTerms; k += blockDim.x)
+    D[(int64_t)c * 2 * kFFTerms + k] = acc[k];
+}
+
+static int ff_find(std::vector<int>& p, int a) {
+  while (p[a] != a) a = p[a] = p[p[a]];
+  return a;
+}
+
+void free_farfield(gwn_scene* sc) {
+  if (sc->ff_edge) cudaFree(sc->ff_edge);
+  if (sc->ff_g) cudaFree(sc->ff_g);
+  if (sc->ff_r) cudaFree(sc->ff_r);
+  if (sc->ff_D) cudaFree(sc->ff_D);
+  sc->ff_edge = nullptr;
+  sc->ff_g = sc->ff_r = sc->ff_D = nullptr;
+  sc->ff_n = 0;
+  sc->ff_g_host.clear();
+}
+
+// ectrl: (n_edges, 4, 3) cubic edge nets on the host, sc->verts sampled.
+cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
+  const char* env = getenv("GWN_FARFIELD");
+  if (env && atoi(env) == 0) return cudaSuccess;
+  const int64_t ne = sc->n_edges;
+  const int S = sc->S;
+  if (ne <= 0) return cudaSuccess;
+  // cycles: union-find over the edges' end points (bitwise shared lattice points)
+  std::map<std::array<double, 3>, int> pid;
+  std::vector<int> ea(ne), eb(ne);
+  auto point_id = [&](const double* P) {
+    std::array<double, 3> k{P[0], P[1], P[2]};
+    auto it = pid.find(k);
+    if (it != pid.end()) return it->second;
+    const int id = (int)pid.size();
+    pid.emplace(k, id);
+    return id;
+  };
+  for (int64_t e = 0; e < ne; ++e) {
+    ea[e] = point_id(ectrl + 12 * e);
+    eb[e] = point_id(ectrl + 12 * e + 9);
+  }
+  std::vector<int> par(pid.size());
+  std::iota(par.begin(), par.end(), 0);
+  for (int64_t e = 0; e < ne; ++e) {
+    const int a = ff_find(par, ea[e]), b = ff_find(par, eb[e]);
+    if (a != b) par[a] = b;
+  }
+  std::map<int, int> cyc_of_root;
+  std::vector<int> ecyc(ne);
+  for (int64_t e = 0; e < ne; ++e) {
+    const int r = ff_find(par, ea[e]);
+    auto it = cyc_of_root.find(r);
+    if (it == cyc_of_root.end()) it = cyc_of_root.emplace(r, (int)cyc_of_root.size()).first;
+    ecyc[e] = it->second;
+  }
+  const int C = (int)cyc_of_root.size();
+  // per-cycle geometry from the sampled polyline (the vertices K4 sums)
+  const int64_t V = ne * S;
+  std::vector<double> hv((size_t)(3 * V));
+  cudaError_t err = cudaMemcpy(hv.data(), sc->verts, sizeof(double) * 3 * V,
+                               cudaMemcpyDeviceToHost);
+  if (err != cudaSuccess) return err;
+  std::vector<double> g(3 * C, 0.0), cnt(C, 0.0), rho(C, 0.0), aabs(C, 0.0);
+  for (int64_t e = 0; e < ne; ++e)
+    for (int s = 0; s < S; ++s) {
+      const int64_t k = e * S + s;
+      const int c = ecyc[e];
+      g[3 * c] += hv[k];
+      g[3 * c + 1] += hv[V + k];
+      g[3 * c + 2] += hv[2 * V + k];
+      cnt[c] += 1.0;
+    }
+  for (int c = 0; c < C; ++c)
+    for (int k = 0; k < 3; ++k) g[3 * c + k] /= cnt[c];
+  for (int64_t e = 0; e < ne; ++e) {
+    const int c = ecyc[e];
+    for (int s = 0; s < S; ++s) {
+      const int64_t k = e * S + s;
+      const double ax = hv[k] - g[3 * c], ay = hv[V + k] - g[3 * c + 1],
+                   az = hv[2 * V + k] - g[3 * c + 2];
+      rho[c] = fmax(rho[c], sqrt(ax * ax + ay * ay + az * az));
+      if (s + 1 < S) {
+        const double bx = hv[k + 1] - g[3 * c], by = hv[V + k + 1] - g[3 * c + 1],
+                     bz = hv[2 * V + k + 1] - g[3 * c + 2];
+        const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
+        aabs[c] += 0.5 * sqrt(cx * cx + cy * cy + cz * cz);
+      }
+    }
+  }
+  // far radius: A_abs (K+2) rho^(K+1) / (R - rho)^(K+3) <= tau; cycles whose
+  // R_min exceeds twice the scene diagonal keep the exact sum only
+  std::vector<int> keep(C, -1);
+  std::vector<double> r2, gk;
+  int nk = 0;
+  for (int c = 0; c < C; ++c) {
+    const double K = kFFK;
+    const double rmin =
+        rho[c] * (1.0 + 1e-9) +
+        pow(aabs[c] * (K + 2.0) * pow(rho[c], K + 1.0) / kFFTau, 1.0 / (K + 3.0));
+    static const bool all = getenv("GWN_FF_ALL") != nullptr;  // tests: expand every cycle
+    if ((!all && !(rmin < 2.0 * sc->diag)) || !(rho[c] > 0.0)) continue;
+    keep[c] = nk++;
+    const double line = rho[c] * (1.0 + 1e-6) + 1e-9 * (1.0 + sc->diag);
+    r2.push_back(rmin * rmin);
+    r2.push_back(line * line);
+    gk.insert(gk.end(), {g[3 * c], g[3 * c + 1], g[3 * c + 2]});
+  }
+  if (nk == 0) return cudaSuccess;
+  std::vector<int32_t> fe(ne);
+  std::vector<int64_t> coff(nk + 1, 0);
+  for (int64_t e = 0; e < ne; ++e) {
+    fe[e] = keep[ecyc[e]];
+    if (fe[e] >= 0) ++coff[fe[e] + 1];
+  }
+  for (int c = 0; c < nk; ++c) coff[c + 1] += coff[c];
+  std::vector<int32_t> cedge(coff[nk]);
+  {
+    std::vector<int64_t> pos(coff.begin(), coff.end() - 1);
+    for (int64_t e = 0; e < ne; ++e)
+      if (fe[e] >= 0) cedge[pos[fe[e]]++] = (int32_t)e;
+  }
+  int64_t* d_coff = nullptr;
+  int32_t* d_cedge = nullptr;
+#define FF(x)                       \
+  do {                              \
+    err = (x);                      \
+    if (err != cudaSuccess) goto out; \
+  } while (0)
+  FF(cudaMalloc(&sc->ff_edge, sizeof(int32_t) * ne));
+  FF(cudaMalloc(&sc->ff_g, sizeof(double) * 3 * nk));
+  FF(cudaMalloc(&sc->ff_r, sizeof(double) * 2 * nk));
+  FF(cudaMalloc(&sc->ff_D, sizeof(double) * 2 * kFFTerms * nk));
+  FF(cudaMalloc(&d_coff, sizeof(int64_t) * (nk + 1)));
+  FF(cudaMalloc(&d_cedge, sizeof(int32_t) * std::max<int64_t>(1, coff[nk])));
+  FF(cudaMemcpy(sc->ff_edge, fe.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice));
+  FF(cudaMemcpy(sc->ff_g, gk.data(), sizeof(double) * 3 * nk, cudaMemcpyHostToDevice));
+  FF(cudaMemcpy(sc->ff_r, r2.data(), sizeof(double) * 2 * nk, cudaMemcpyHostToDevice));
+  FF(cudaMemcpy(d_coff, coff.data(), sizeof(int64_t) * (nk + 1), cudaMemcpyHostToDevice));
+  FF(cudaMemcpy(d_cedge, cedge.data(), sizeof(int32_t) * coff[nk], cudaMemcpyHostToDevice));
+  k_ff_moments<<<nk, 256>>>(d_coff, d_cedge, sc->verts, V, S, sc->ff_g, ff_quad(), sc->ff_D);
+  FF(cudaGetLastError());
+  FF(cudaDeviceSynchronize());
+  sc->ff_n = nk;
+  sc->ff_g_host = gk;
+out:
+#undef FF
+  if (d_coff) cudaFree(d_coff);
+  if (d_cedge) cudaFree(d_cedge);
+  if (err != cudaSuccess) free_farfield(sc);
+  return err;
+}
+
+// Far kernel: one query per thread, cycle group blockIdx.y (kFFRows rows);
+// far pairs add
+// Omega(p) = -sum_{n>=1} [Re(D_n^0 I_n^0) + 2 sum_{m>=1} Re(D_n^m I_n^m)]
+// (I by upward recurrences, stable for |p - g| > rho) into the far row.
+__global__ void __launch_bounds__(128)
+k_boundary_far(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
+               int32_t C, const double* __restrict__ ffg, const double* __restrict__ ffr,
+               const double* __restrict__ gw, const double* __restrict__ D, Frame f,
+               double* __restrict__ brow, unsigned long long* __restrict__ counters) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = s < m;
+  const int32_t q = live ? (active ? active[s] : s) : 0;
+  const double px = live ? pos[3 * (int64_t)q] : 0.0, py = live ? pos[3 * (int64_t)q + 1] : 0.0,
+               pz = live ? pos[3 * (int64_t)q + 2] : 0.0;
+  double qa, qb, qc;
+  frame_q(f, px, py, pz, qa, qb, qc);
+  double om = 0.0;
+  unsigned long long nfar = 0;
+  const int c0 = (int)((int64_t)C * blockIdx.y / gridDim.y);
+  const int c1 = (int)((int64_t)C * (blockIdx.y + 1) / gridDim.y);
+  for (int c = c0; c < c1; ++c) {
+    if (!live || !ff_far(qa, qb, qc, ffg + 3 * c, ffr + 2 * c)) continue;
+    ++nfar;
+    const double x = px - __ldg(gw + 3 * c), y = py - __ldg(gw + 3 * c + 1),
+                 z = pz - __ldg(gw + 3 * c + 2);
+    const double ir2 = 1.0 / (x * x + y * y + z * z);
+    const double* Dc = D + (int64_t)c * 2 * kFFTerms;
+    double dR = sqrt(ir2), dI = 0.0;  // I_0^0 = 1/r
+    double acc = 0.0;
+    // fully unrolled: every recurrence constant and D offset is an immediate
+#pragma unroll
+    for (int mm = 0; mm <= kFFK; ++mm) {
+      if (mm > 0) {  // I_m^m = -(2m-1)(x+iy)/r^2 I_{m-1}^{m-1}
+        const double c0 = -(2.0 * mm - 1.0) * ir2;
+        const double nR = c0 * (x * dR - y * dI), nI = c0 * (x * dI + y * dR);
+        dR = nR;
+        dI = nI;
+      }
+      double aR = dR, aI = dI, bR = 0.0, bI = 0.0;
+      double col = 0.0;
+#pragma unroll
+      for (int n = mm; n <= kFFK; ++n) {
+        if (n > mm) {  // I_n^m = ((2n-1) z I_{n-1}^m - ((n-1)^2 - m^2) I_{n-2}^m) / r^2
+          const double k1 = 2.0 * n - 1.0, k2 = (double)((n - 1) * (n - 1) - mm * mm);
+          const double vR = (k1 * z * aR - k2 * bR) * ir2, vI = (k1 * z * aI - k2 * bI) * ir2;
+          bR = aR;
+          bI = aI;
+          aR = vR;
+          aI = vI;
+        }
+        if (n == 0) continue;
+        const int t = ff_term(n, mm);
+        col += __ldg(Dc + 2 * t) * aR - __ldg(Dc + 2 * t + 1) * aI;
+      }
+      acc += mm == 0 ? col : 2.0 * col;
+    }
+    om -= acc;
+  }
+  // K4's partials are sums of atan2 (half angles): Omega / 2
+  if (live) brow[(int64_t)blockIdx.y * m + s] = 0.5 * om;
+  // far (query, cycle) pairs, one atomic per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nfar += __shfl_down_sync(0xffffffffu, nfar, o);
+  if ((threadIdx.x & 31) == 0 && nfar) atomicAdd(&counters[CNT_FAR], nfar);
+}
+
+cudaError_t launch_boundary_far(const gwn_scene* sc, const Round& rd, int32_t m,
+                                const int32_t* active, const double* pos, double* brow,
+                                unsigned long long* counters, cudaStream_t st) {
+  if (m <= 0 || sc->ff_n <= 0) return cudaSuccess;
+  const dim3 grid((m + 127) / 128, kFFRows);
+  k_boundary_far<<<grid, 128, 0, st>>>(m, active, pos, sc->ff_n, rd.ffg, sc->ff_r, sc->ff_g,
+                                       sc->ff_D, rd.f, brow, counters);
+  return cudaGetLastError();
+}
+
+// 3-D Morton order of the round's queries (30-bit keys over the scene box
+// widened 2x) for the exact K4 kernel: a warp's queries are neighbours, so
+// its far / near decisions per cycle agree and far cycles are skipped.
+__device__ __forceinline__ unsigned ff_spread10(unsigned v) {
+  v &= 1023u;
+  v = (v | (v << 16)) & 0x030000FFu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+__global__ void k_ff_keys(int32_t m, const int32_t* __restrict__ active,
+                          const double* __restrict__ pos, double x0, double y0, double z0,
+                          double inv, unsigned* __restrict__ keys, int32_t* __restrict__ ids) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  const int32_t q = active ? active[s] : s;
+  auto cell = [&](double v, double o) {
+    const double t = (v - o) * inv;
+    return (unsigned)fmin(1023.0, fmax(0.0, t));
+  };
+  keys[s] = (ff_spread10(cell(pos[3 * (int64_t)q], x0)) << 2) |
+            (ff_spread10(cell(pos[3 * (int64_t)q + 1], y0)) << 1) |
+            ff_spread10(cell(pos[3 * (int64_t)q + 2], z0));
+  ids[s] = s;
+}
+
+size_t ff_order_scratch_bytes(int32_t m) {
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, (unsigned*)nullptr, (unsigned*)nullptr,
+                                  (int32_t*)nullptr, (int32_t*)nullptr, m, 0, 30);
+  return tb + 4 * sizeof(unsigned) * (size_t)m + 1024;
+}
+
+cudaError_t launch_ff_order(const gwn_scene* sc, int32_t m, const int32_t* active,
+                            const double* pos, void* scratch, int32_t* order, cudaStream_t st) {
+  char* p = (char*)scratch;
+  auto take = [&](size_t b) {
+    char* r = p;
+    p += (b + 255) & ~(size_t)255;
+    return r;
+  };
+  unsigned* k0 = (unsigned*)take(sizeof(unsigned) * m);
+  unsigned* k1 = (unsigned*)take(sizeof(unsigned) * m);
+  int32_t* i0 = (int32_t*)take(sizeof(int32_t) * m);
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, i0, order, m, 0, 30, st);
+  void* tmp = take(tb);
+  double ext = 0.0;
+  for (int k = 0; k < 3; ++k) ext = fmax(ext, sc->bbox_max[k] - sc->bbox_min[k]);
+  ext = 2.0 * ext + 1e-30;
+  const double x0 = 0.5 * (sc->bbox_min[0] + sc->bbox_max[0]) - 0.5 * ext;
+  const double y0 = 0.5 * (sc->bbox_min[1] + sc->bbox_max[1]) - 0.5 * ext;
+  const double z0 = 0.5 * (sc->bbox_min[2] + sc->bbox_max[2]) - 0.5 * ext;
+  k_ff_keys<<<(m + 255) / 256, 256, 0, st>>>(m, active, pos, x0, y0, z0, 1024.0 / ext, k0, i0);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, i0, order, m, 0, 30, st);
+}
+
+}  // namespace gwn

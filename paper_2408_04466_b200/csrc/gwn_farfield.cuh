@@ -1,0 +1,55 @@
+// gwn_farfield.cuh -- far field of the boundary term.
+//
+// The net boundary is the boundary of a surface, so every connected component
+// of its edge graph is a closed cycle.  For a closed cycle, K4's fan sum from
+// c = -d equals the cycle's solid angle Omega(p) (the fan-from-centre surface)
+// whenever the line p + t d misses the cycle's bounding sphere: no 4 pi branch
+// and no band re-shoot.  Outside the sphere Omega is harmonic and has the
+// multipole expansion
+//     Omega(p) = -sum_{n>=1} sum_{m=-n..n} D_n^m I_n^m(p - g),
+//     D_n^m = integral over the fan surface of n . conj(grad R_n^m(x - g)) dA,
+// with the regular / irregular solid harmonics R, I of the addition theorem
+// 1/|p - q| = sum_n sum_m conj(R_n^m(q)) I_n^m(p) (recurrences below; checked
+// in tools/farfield/proto.py).  Truncated at n = kFFK the error is at most
+//     A_abs (K+2) rho^(K+1) / (R - rho)^(K+3)
+// (|d^k (1/r)| <= k!/r^(k+1) along any unit direction, the Legendre bound),
+// so a (query, cycle) pair is "far" when R^2 >= R_min^2 with that bound at
+// kFFTau, and the line to the query misses the sphere.  Both K4 kernels take
+// the decision with ff_far() on the same bits, so the exact kernel's masked /
+// skipped segments and the far kernel's terms partition the cycles exactly.
+#pragma once
+
+#include "gwn_internal.h"
+
+namespace gwn {
+
+constexpr int kFFK = 16;                               // expansion order
+constexpr int kFFTerms = (kFFK + 1) * (kFFK + 2) / 2;  // (n, m), 0 <= m <= n <= K
+constexpr double kFFTau = 1e-12;                       // truncation bound per cycle (rad)
+// far-field partial rows: cycle groups summed in fixed order by K5, so the
+// far kernel fills the GPU and w stays bit-identical for any batching
+constexpr int kFFRows = 16;
+
+__device__ __forceinline__ int ff_term(int n, int m) { return n * (n + 1) / 2 + m; }
+
+// query in the round frame (explicit roundings: every kernel that takes a
+// far-field decision computes bit-identical coordinates)
+__device__ __forceinline__ void frame_q(const Frame& f, double px, double py, double pz,
+                                        double& qa, double& qb, double& qc) {
+  qa = __fma_rn(pz, f.e1[2], __fma_rn(py, f.e1[1], __dmul_rn(px, f.e1[0])));
+  qb = __fma_rn(pz, f.e2[2], __fma_rn(py, f.e2[1], __dmul_rn(px, f.e2[0])));
+  qc = __fma_rn(pz, f.d[2], __fma_rn(py, f.d[1], __dmul_rn(px, f.d[0])));
+}
+
+// g3: cycle centre in the round frame (d = z); r2 = (R_min^2, line radius^2)
+__device__ __forceinline__ bool ff_far(double qa, double qb, double qc,
+                                       const double* __restrict__ g3,
+                                       const double* __restrict__ r2) {
+  const double dx = __dsub_rn(__ldg(g3), qa), dy = __dsub_rn(__ldg(g3 + 1), qb);
+  const double dz = __dsub_rn(__ldg(g3 + 2), qc);
+  const double l2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  const double R2 = __dadd_rn(l2, __dmul_rn(dz, dz));
+  return l2 > __ldg(r2 + 1) && R2 > __ldg(r2);
+}
+
+}  // namespace gwn

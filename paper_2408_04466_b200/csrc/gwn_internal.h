@@ -41,7 +41,8 @@ enum : int {
   CNT_MAXNODES = 5,  // max DFS nodes of one fallback item (diagnostic)
   CNT_BIGITEMS = 6,  // slowest fallback warp: cycles<<24 | tree levels<<16 | code levels<<8 | items
   CNT_MAXLEVELS = 7, // deepest fallback BFS, in levels (diagnostic)
-  CNT_N = 8,
+  CNT_FAR = 8,       // (query, cycle) pairs taken by the far-field expansion
+  CNT_N = 9,
 };
 
 struct Frame {
@@ -92,6 +93,7 @@ struct Round {
   Node* nodes = nullptr;       // (n_leaves-1) LBVH over the leaf boxes
   double amin = 0, ainv = 0, bmin = 0, binv = 0;  // projected scene box (Morton keys)
   double* vproj = nullptr;     // (3,V) boundary vertices in the ray frame (K4)
+  double* ffg = nullptr;       // (ff_n,3) far-field cycle centres in the ray frame
   // uniform grid over the leaf boxes (K2 point location); used when its
   // cells stay short, else the LBVH
   bool use_grid = false;
@@ -127,6 +129,14 @@ struct gwn_scene {
   int32_t S = 0;
   double* verts = nullptr;      // (3,V) SoA, V = n_edges*S
   double* band_h = nullptr;     // (n_edges)
+  // far field of the boundary term (gwn_farfield.cu): closed cycles of the
+  // net boundary with a solid-harmonic expansion; ff_n = 0 when off
+  int32_t ff_n = 0;
+  int32_t* ff_edge = nullptr;   // (n_edges) cycle of each edge, -1 = exact only
+  double* ff_g = nullptr;       // (ff_n,3) cycle centre (world)
+  double* ff_r = nullptr;       // (ff_n,2) R_min^2, line radius^2
+  double* ff_D = nullptr;       // (ff_n, kFFTerms, 2) double-layer moments
+  std::vector<double> ff_g_host;
   // per-round caches
   std::mutex mu;
   // deques: push_back never moves existing rounds, so a Round* taken under
@@ -203,9 +213,17 @@ cudaError_t launch_query_order(const Round& rd, int32_t m, const double* pos, vo
 size_t query_order_scratch_bytes(int32_t m);
 cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             const int32_t* active, const double* pos, double* bpart, int nchunk,
-                            int32_t* flags, unsigned long long* counters,
-                            cudaStream_t st);                                 // gwn_boundary.cu
-int boundary_chunks(const gwn_scene* sc, int32_t m);
+                            int32_t* flags, unsigned long long* counters, cudaStream_t st,
+                            const int32_t* order = nullptr);                  // gwn_boundary.cu
+int boundary_chunks(const gwn_scene* sc, int32_t m);  // partial rows (exact chunks + far row)
+cudaError_t build_farfield(gwn_scene* sc, const double* ectrl);     // gwn_farfield.cu
+void free_farfield(gwn_scene* sc);
+cudaError_t launch_boundary_far(const gwn_scene* sc, const Round& rd, int32_t m,
+                                const int32_t* active, const double* pos, double* brow,
+                                unsigned long long* counters, cudaStream_t st);
+cudaError_t launch_ff_order(const gwn_scene* sc, int32_t m, const int32_t* active,
+                            const double* pos, void* scratch, int32_t* order, cudaStream_t st);
+size_t ff_order_scratch_bytes(int32_t m);
 cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st);  // gwn_boundary.cu
 cudaError_t selftest_rsqrt(int64_t n, unsigned long long* max_ulp_host);
 cudaError_t launch_all_hits(const gwn_scene* sc, const Round& rd, int64_t patch,

@@ -365,6 +365,7 @@ extern "C" int gwn_eval_rays(gwn_scene* sc, const double* origins, int64_t R,
       stats.newton_iters = (int64_t)hc[CNT_NEWTON];
       stats.roots = (int64_t)hc[CNT_ROOTS];
       stats.boundary_segments = (int64_t)hc[CNT_SEGMENTS];
+      stats.far_pairs = (int64_t)hc[CNT_FAR];
       {
     std::lock_guard<std::mutex> lk(sc->mu);
     sc->stats = stats;

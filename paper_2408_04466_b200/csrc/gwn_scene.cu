@@ -327,6 +327,8 @@ extern "C" int gwn_scene_create(const double* ctrl, int64_t P, const gwn_params*
     CK(cudaDeviceSynchronize());
     cudaFree(d_ectrl);
     d_ectrl = nullptr;
+    // far field of the boundary term: closed cycles + multipole moments
+    CK(build_farfield(sc, ectrl.data()));
   }
   // round 0 eagerly (projection, LBVH, boundary precompute)
   {
@@ -350,6 +352,7 @@ extern "C" int gwn_scene_destroy(gwn_scene* sc) {
   if (sc->ctrl) cudaFree(sc->ctrl);
   if (sc->verts) cudaFree(sc->verts);
   if (sc->band_h) cudaFree(sc->band_h);
+  free_farfield(sc);
   delete sc;
   return GWN_OK;
 }
@@ -369,6 +372,7 @@ extern "C" int gwn_scene_info_get(const gwn_scene* sc, gwn_scene_info* out) {
   out->diag = sc->diag;
   out->device = sc->device;
   out->sm_count = sc->sm_count;
+  out->n_far_cycles = sc->ff_n;
   return GWN_OK;
 }
 

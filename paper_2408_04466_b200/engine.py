@@ -105,6 +105,11 @@ class Scene:
         return int(self.info.n_net_segments)
 
     @property
+    def n_far_cycles(self) -> int:
+        """Closed net-boundary cycles with a far-field expansion (DESIGN §2 K4)."""
+        return int(self.info.n_far_cycles)
+
+    @property
     def diag(self) -> float:
         return float(self.info.diag)
 

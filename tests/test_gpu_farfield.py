@@ -1,0 +1,87 @@
+"""Far field of the boundary term (DESIGN §2 K4): the
+solid-harmonic expansion of closed net-boundary cycles against the exact fan
+sum (GWN_FARFIELD=0 switches the expansion off at scene creation), in fresh
+processes so the switch is read at library load."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2408_04466_b200 as G
+from paper_2408_04466_b200 import scenes
+cfg, nq, out, mode = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5]
+s = scenes.make(cfg, nq)
+sc = G.Scene(s.ctrl)
+q = s.queries
+if mode == "far":  # single patch, queries 8..40 patch radii away
+    rng = np.random.default_rng(0)
+    c = s.ctrl.reshape(-1, 3).mean(0)
+    u = rng.normal(size=(1024, 3)); u /= np.linalg.norm(u, axis=1)[:, None]
+    q = c + np.repeat([8.0, 12.0, 20.0, 40.0], 256)[:, None] * u
+qd = torch.from_numpy(np.ascontiguousarray(q)).cuda()
+w, st = G.winding_numbers(sc, qd)
+extra = {}
+if mode == "halves":  # the same queries in two calls with global index bases
+    h = len(q) // 2
+    w1, s1 = G.winding_numbers(sc, qd[:h], index_base=0)
+    w2, s2 = G.winding_numbers(sc, qd[h:], index_base=h)
+    extra = dict(wh=torch.cat([w1, w2]).cpu().numpy(), sh=torch.cat([s1, s2]).cpu().numpy())
+np.savez(out, w=w.cpu().numpy(), st=st.cpu().numpy(), far=sc.stats()["far_pairs"],
+         cycles=sc.n_far_cycles, **extra)
+"""
+
+
+def _run(tmp_path, cfg, nq, mode="plain", **env):
+    f = str(tmp_path / f"r{cfg}_{mode}_{len(env)}_{'_'.join(env.values())}.npz")
+    e = dict(os.environ, **env)
+    subprocess.run([sys.executable, "-c", _SCRIPT, REPO, str(cfg), str(nq), f, mode], env=e,
+                   check=True, timeout=600)
+    return np.load(f)
+
+
+def test_farfield_matches_exact_sum_config5(tmp_path):
+    ex = _run(tmp_path, 5, 1 << 13, GWN_FARFIELD="0")
+    ff = _run(tmp_path, 5, 1 << 13)
+    assert int(ex["cycles"]) == 0 and int(ff["cycles"]) > 100
+    assert int(ff["far"]) > 0
+    assert np.array_equal(ex["st"], ff["st"])
+    ok = ex["st"] == 0
+    # truncation bound 1e-12 rad per cycle (DESIGN): |dw| far below the 1e-9 bar
+    assert np.abs(ex["w"] - ff["w"])[ok].max() <= 1e-11
+
+
+def test_farfield_far_queries_single_cycle(tmp_path):
+    ex = _run(tmp_path, 1, 16, mode="far", GWN_FARFIELD="0")
+    ff = _run(tmp_path, 1, 16, mode="far", GWN_FF_ALL="1")
+    assert int(ff["cycles"]) == 1 and int(ff["far"]) == 1024
+    assert np.abs(ex["w"] - ff["w"]).max() <= 1e-14
+
+
+def test_farfield_batching_is_bit_identical(tmp_path):
+    r = _run(tmp_path, 5, 1 << 12, mode="halves")
+    assert int(r["far"]) > 0
+    assert np.array_equal(r["w"], r["wh"]) and np.array_equal(r["st"], r["sh"])
+
+
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_open_sheets_keep_the_exact_sum(tmp_path, cfg):
+    """One border cycle whose far radius exceeds the scene: no expansion, and the
+    results are bit-identical to the switch being off."""
+    ex = _run(tmp_path, cfg, 1 << 12, GWN_FARFIELD="0")
+    ff = _run(tmp_path, cfg, 1 << 12)
+    assert int(ff["cycles"]) == 0
+    assert np.array_equal(ex["w"], ff["w"]) and np.array_equal(ex["st"], ff["st"])
