@@ -527,7 +527,7 @@ cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                                                          bpart, flags, counters, fv);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       return launch_boundary_far(sc, rd, m, active, pos, bpart + (int64_t)nexact * m, counters,
-                                 st);
+                                 st, order);
     }
     k_boundary_e<kQPT, false><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S,
                                                         sc->n_edges, sc->band_h, rd.f, sc->dprm,

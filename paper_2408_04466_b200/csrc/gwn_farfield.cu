@@ -28,7 +28,9 @@
 
 namespace gwn {
 
-constexpr int kFFQ = 9;  // Gauss-Legendre points per direction (exact to degree 17 >= K)
+// Gauss-Legendre points per direction: exact to degree 2Q-1 >= K (the
+// integrands have degree K-1 in (s, t), one more in u after the collapse)
+constexpr int kFFQ = kFFK / 2 + 1;
 
 struct FFQuad {
   double x[kFFQ], w[kFFQ];  // nodes / weights on [0, 1]
@@ -161,6 +163,8 @@ void free_farfield(gwn_scene* sc) {
   if (sc->ff_g) cudaFree(sc->ff_g);
   if (sc->ff_r) cudaFree(sc->ff_r);
   if (sc->ff_D) cudaFree(sc->ff_D);
+  if (sc->ff_lv) cudaFree(sc->ff_lv);
+  sc->ff_lv = nullptr;
   sc->ff_edge = nullptr;
   sc->ff_g = sc->ff_r = sc->ff_D = nullptr;
   sc->ff_n = 0;
@@ -240,7 +244,7 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   // far radius: A_abs (K+2) rho^(K+1) / (R - rho)^(K+3) <= tau; cycles whose
   // R_min exceeds twice the scene diagonal keep the exact sum only
   std::vector<int> keep(C, -1);
-  std::vector<double> r2, gk;
+  std::vector<double> r2, gk, lvr;
   int nk = 0;
   for (int c = 0; c < C; ++c) {
     const double K = kFFK;
@@ -253,6 +257,12 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
     const double line = rho[c] * (1.0 + 1e-6) + 1e-9 * (1.0 + sc->diag);
     r2.push_back(rmin * rmin);
     r2.push_back(line * line);
+    for (int lv = 0; lv < kFFLevels; ++lv) {  // thresholds of the lower orders
+      const double p = ff_order(lv);
+      const double rp = rho[c] * (1.0 + 1e-9) +
+                        pow(aabs[c] * (p + 2.0) * pow(rho[c], p + 1.0) / kFFTau, 1.0 / (p + 3.0));
+      lvr.push_back(lv == kFFLevels - 1 ? rmin * rmin : rp * rp);
+    }
     gk.insert(gk.end(), {g[3 * c], g[3 * c + 1], g[3 * c + 2]});
   }
   if (nk == 0) return cudaSuccess;
@@ -280,6 +290,8 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   FF(cudaMalloc(&sc->ff_g, sizeof(double) * 3 * nk));
   FF(cudaMalloc(&sc->ff_r, sizeof(double) * 2 * nk));
   FF(cudaMalloc(&sc->ff_D, sizeof(double) * 2 * kFFTerms * nk));
+  FF(cudaMalloc(&sc->ff_lv, sizeof(double) * kFFLevels * nk));
+  FF(cudaMemcpy(sc->ff_lv, lvr.data(), sizeof(double) * kFFLevels * nk, cudaMemcpyHostToDevice));
   FF(cudaMalloc(&d_coff, sizeof(int64_t) * (nk + 1)));
   FF(cudaMalloc(&d_cedge, sizeof(int32_t) * std::max<int64_t>(1, coff[nk])));
   FF(cudaMemcpy(sc->ff_edge, fe.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice));
@@ -300,17 +312,56 @@ out:
   return err;
 }
 
-// Far kernel: one query per thread, cycle group blockIdx.y (kFFRows rows);
-// far pairs add
+// Far kernel: one query per thread (Morton order when given), cycle group
+// blockIdx.y (kFFRows rows); far pairs add
 // Omega(p) = -sum_{n>=1} [Re(D_n^0 I_n^0) + 2 sum_{m>=1} Re(D_n^m I_n^m)]
-// (I by upward recurrences, stable for |p - g| > rho) into the far row.
+// to the lowest order P of ff_order() whose bound holds at the pair's
+// distance (I by upward recurrences, stable for |p - g| > rho).
+template <int P>
+__device__ __forceinline__ double ff_eval(double x, double y, double z,
+                                          const double2* __restrict__ Dc) {
+  const double ir2 = 1.0 / (x * x + y * y + z * z);
+  double dR = sqrt(ir2), dI = 0.0;  // I_0^0 = 1/r
+  double acc = 0.0;
+  // fully unrolled: every recurrence constant and D offset is an immediate
+#pragma unroll
+  for (int mm = 0; mm <= P; ++mm) {
+    if (mm > 0) {  // I_m^m = -(2m-1)(x+iy)/r^2 I_{m-1}^{m-1}
+      const double c0 = -(2.0 * mm - 1.0) * ir2;
+      const double nR = c0 * (x * dR - y * dI), nI = c0 * (x * dI + y * dR);
+      dR = nR;
+      dI = nI;
+    }
+    double aR = dR, aI = dI, bR = 0.0, bI = 0.0;
+    double col = 0.0;
+#pragma unroll
+    for (int n = mm; n <= P; ++n) {
+      if (n > mm) {  // I_n^m = ((2n-1) z I_{n-1}^m - ((n-1)^2 - m^2) I_{n-2}^m) / r^2
+        const double k1 = 2.0 * n - 1.0, k2 = (double)((n - 1) * (n - 1) - mm * mm);
+        const double vR = (k1 * z * aR - k2 * bR) * ir2, vI = (k1 * z * aI - k2 * bI) * ir2;
+        bR = aR;
+        bI = aI;
+        aR = vR;
+        aI = vI;
+      }
+      if (n == 0) continue;
+      const double2 d = __ldg(Dc + ff_term(n, mm));
+      col += d.x * aR - d.y * aI;
+    }
+    acc += mm == 0 ? col : 2.0 * col;
+  }
+  return -acc;
+}
+
 __global__ void __launch_bounds__(128)
-k_boundary_far(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
-               int32_t C, const double* __restrict__ ffg, const double* __restrict__ ffr,
+k_boundary_far(int32_t m, const int32_t* __restrict__ order, const int32_t* __restrict__ active,
+               const double* __restrict__ pos, int32_t C, const double* __restrict__ ffg,
+               const double* __restrict__ ffr, const double* __restrict__ fflv,
                const double* __restrict__ gw, const double* __restrict__ D, Frame f,
                double* __restrict__ brow, unsigned long long* __restrict__ counters) {
-  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = s < m;
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = t < m;
+  const int32_t s = live ? (order ? order[t] : t) : 0;
   const int32_t q = live ? (active ? active[s] : s) : 0;
   const double px = live ? pos[3 * (int64_t)q] : 0.0, py = live ? pos[3 * (int64_t)q + 1] : 0.0,
                pz = live ? pos[3 * (int64_t)q + 2] : 0.0;
@@ -325,38 +376,14 @@ k_boundary_far(int32_t m, const int32_t* __restrict__ active, const double* __re
     ++nfar;
     const double x = px - __ldg(gw + 3 * c), y = py - __ldg(gw + 3 * c + 1),
                  z = pz - __ldg(gw + 3 * c + 2);
-    const double ir2 = 1.0 / (x * x + y * y + z * z);
-    const double* Dc = D + (int64_t)c * 2 * kFFTerms;
-    double dR = sqrt(ir2), dI = 0.0;  // I_0^0 = 1/r
-    double acc = 0.0;
-    // fully unrolled: every recurrence constant and D offset is an immediate
-#pragma unroll
-    for (int mm = 0; mm <= kFFK; ++mm) {
-      if (mm > 0) {  // I_m^m = -(2m-1)(x+iy)/r^2 I_{m-1}^{m-1}
-        const double c0 = -(2.0 * mm - 1.0) * ir2;
-        const double nR = c0 * (x * dR - y * dI), nI = c0 * (x * dI + y * dR);
-        dR = nR;
-        dI = nI;
-      }
-      double aR = dR, aI = dI, bR = 0.0, bI = 0.0;
-      double col = 0.0;
-#pragma unroll
-      for (int n = mm; n <= kFFK; ++n) {
-        if (n > mm) {  // I_n^m = ((2n-1) z I_{n-1}^m - ((n-1)^2 - m^2) I_{n-2}^m) / r^2
-          const double k1 = 2.0 * n - 1.0, k2 = (double)((n - 1) * (n - 1) - mm * mm);
-          const double vR = (k1 * z * aR - k2 * bR) * ir2, vI = (k1 * z * aI - k2 * bI) * ir2;
-          bR = aR;
-          bI = aI;
-          aR = vR;
-          aI = vI;
-        }
-        if (n == 0) continue;
-        const int t = ff_term(n, mm);
-        col += __ldg(Dc + 2 * t) * aR - __ldg(Dc + 2 * t + 1) * aI;
-      }
-      acc += mm == 0 ? col : 2.0 * col;
-    }
-    om -= acc;
+    const double R2 = x * x + y * y + z * z;
+    const double* lv = fflv + (int64_t)kFFLevels * c;
+    const double2* Dc = reinterpret_cast<const double2*>(D + (int64_t)c * 2 * kFFTerms);
+    static_assert(kFFLevels == 4, "ff_eval dispatch below covers four orders");
+    if (R2 > __ldg(lv)) om += ff_eval<ff_order(0)>(x, y, z, Dc);
+    else if (R2 > __ldg(lv + 1)) om += ff_eval<ff_order(1)>(x, y, z, Dc);
+    else if (R2 > __ldg(lv + 2)) om += ff_eval<ff_order(2)>(x, y, z, Dc);
+    else om += ff_eval<ff_order(3)>(x, y, z, Dc);
   }
   // K4's partials are sums of atan2 (half angles): Omega / 2
   if (live) brow[(int64_t)blockIdx.y * m + s] = 0.5 * om;
@@ -368,11 +395,12 @@ k_boundary_far(int32_t m, const int32_t* __restrict__ active, const double* __re
 
 cudaError_t launch_boundary_far(const gwn_scene* sc, const Round& rd, int32_t m,
                                 const int32_t* active, const double* pos, double* brow,
-                                unsigned long long* counters, cudaStream_t st) {
+                                unsigned long long* counters, cudaStream_t st,
+                                const int32_t* order) {
   if (m <= 0 || sc->ff_n <= 0) return cudaSuccess;
   const dim3 grid((m + 127) / 128, kFFRows);
-  k_boundary_far<<<grid, 128, 0, st>>>(m, active, pos, sc->ff_n, rd.ffg, sc->ff_r, sc->ff_g,
-                                       sc->ff_D, rd.f, brow, counters);
+  k_boundary_far<<<grid, 128, 0, st>>>(m, order, active, pos, sc->ff_n, rd.ffg, sc->ff_r,
+                                       sc->ff_lv, sc->ff_g, sc->ff_D, rd.f, brow, counters);
   return cudaGetLastError();
 }
 

@@ -23,12 +23,19 @@
 
 namespace gwn {
 
-constexpr int kFFK = 16;                               // expansion order
+#ifndef GWN_FFK
+#define GWN_FFK 20
+#endif
+constexpr int kFFK = GWN_FFK;                          // expansion order
 constexpr int kFFTerms = (kFFK + 1) * (kFFK + 2) / 2;  // (n, m), 0 <= m <= n <= K
 constexpr double kFFTau = 1e-12;                       // truncation bound per cycle (rad)
 // far-field partial rows: cycle groups summed in fixed order by K5, so the
 // far kernel fills the GPU and w stays bit-identical for any batching
 constexpr int kFFRows = 16;
+// adaptive order: a far pair uses the lowest of these orders whose bound
+// holds at its distance (per-cycle thresholds, Scene::ff_lv)
+constexpr int kFFLevels = 4;
+__host__ __device__ constexpr int ff_order(int lv) { return kFFK - 4 * (kFFLevels - 1 - lv); }
 
 __device__ __forceinline__ int ff_term(int n, int m) { return n * (n + 1) / 2 + m; }
 

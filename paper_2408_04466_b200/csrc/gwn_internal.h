@@ -136,6 +136,7 @@ struct gwn_scene {
   double* ff_g = nullptr;       // (ff_n,3) cycle centre (world)
   double* ff_r = nullptr;       // (ff_n,2) R_min^2, line radius^2
   double* ff_D = nullptr;       // (ff_n, kFFTerms, 2) double-layer moments
+  double* ff_lv = nullptr;      // (ff_n, kFFLevels) R^2 thresholds of the adaptive orders
   std::vector<double> ff_g_host;
   // per-round caches
   std::mutex mu;
@@ -220,7 +221,8 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl);     // gwn_farfi
 void free_farfield(gwn_scene* sc);
 cudaError_t launch_boundary_far(const gwn_scene* sc, const Round& rd, int32_t m,
                                 const int32_t* active, const double* pos, double* brow,
-                                unsigned long long* counters, cudaStream_t st);
+                                unsigned long long* counters, cudaStream_t st,
+                                const int32_t* order);
 cudaError_t launch_ff_order(const gwn_scene* sc, int32_t m, const int32_t* active,
                             const double* pos, void* scratch, int32_t* order, cudaStream_t st);
 size_t ff_order_scratch_bytes(int32_t m);
