@@ -83,6 +83,8 @@ def parse():
                          "with N); strong: the config's queries are split over the GPUs")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-far-field", action="store_true",
+                    help="skip the SURVEY §8(f4) far-field side measurement (config 5)")
     ap.add_argument("--no-ray-reuse", action="store_true",
                     help="skip the SURVEY §8(f1) ray-reuse side measurement")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -227,6 +229,48 @@ def boundary_roofline(G, torch, dev, stream, peak_tf, nq=1 << 20, k=3):
             "traffic": _traffic("k_boundary_e_config3_2^20", 2, 1 << 20) if nq == 1 << 20
             else None,
             "segment_pairs": segs}
+
+
+def far_field(G, torch, dev, stream, nq=1 << 18, k=2):
+    """SURVEY §8(f) f4 side measurement: config 5's boundary term (the 64M x 16K
+    north-star scene, 2^18 queries here) with the far-field expansion against
+    the exact fan sum -- both device-timed K4 stages, best of k, and the
+    largest |dw| between the two."""
+    from paper_2408_04466_b200 import scenes
+    s = scenes.make(5, nq)
+    q = torch.from_numpy(s.queries).to(dev)
+    res = {}
+    for mode in ("exact", "far"):
+        old = os.environ.get("GWN_FARFIELD")
+        if mode == "exact":
+            os.environ["GWN_FARFIELD"] = "0"
+        try:
+            sc = G.Scene(s.ctrl)          # the switch is read at scene creation
+        finally:
+            if mode == "exact":
+                if old is None:
+                    os.environ.pop("GWN_FARFIELD", None)
+                else:
+                    os.environ["GWN_FARFIELD"] = old
+        w, st = G.winding_numbers(sc, q, stream=stream.cuda_stream)
+        sc.set_timing(True)
+        best, stt = float("inf"), None
+        for _ in range(k):
+            w, st = G.winding_numbers(sc, q, stream=stream.cuda_stream)
+            t = sc.stats()
+            if t["ms_boundary"] < best:
+                best, stt = t["ms_boundary"], t
+        sc.set_timing(False)
+        res[mode] = (best, w.cpu().numpy(), st.cpu().numpy(), stt, sc.n_far_cycles)
+    ok = (res["exact"][2] == 0) & (res["far"][2] == 0)
+    return {"workload": f"config5 scene ({s.n_patches} patches), {nq} queries, boundary term (K4)",
+            "ms_exact": res["exact"][0], "ms_far_field": res["far"][0],
+            "speedup": res["exact"][0] / res["far"][0],
+            "far_cycles": res["far"][4], "far_pairs": res["far"][3]["far_pairs"],
+            "exact_segment_pairs": res["far"][3]["boundary_segments"],
+            "exact_segment_pairs_without": res["exact"][3]["boundary_segments"],
+            "max_abs_dw": float(np.abs(res["exact"][1] - res["far"][1])[ok].max()),
+            "status_equal": bool(np.array_equal(res["exact"][2], res["far"][2]))}
 
 
 def ray_reuse(G, torch, sc, dev, stream, n=256, k=5):
@@ -433,6 +477,8 @@ def main():
             out["ray_reuse"] = ray_reuse(G, torch, sc, dev, stream)
         if world == 1 and not args.no_ray_reuse:
             out["roofline_open_scene"] = boundary_roofline(G, torch, dev, stream, peak_tf)
+        if world == 1 and not args.no_far_field:
+            out["far_field"] = far_field(G, torch, dev, stream)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(spec, args.cpu_seconds)
         print(json.dumps(out), flush=True)
