@@ -332,7 +332,9 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
           all &= far[j] || !live[j];
           nnear += (live[j] && !far[j]) ? 1 : 0;
         }
+#ifndef GWN_FF_NOSKIP
         if (__all_sync(0xffffffffu, all)) continue;
+#endif
         exact_pairs += (unsigned long long)nnear * (unsigned long long)(S - 1);
       }
 #pragma unroll
@@ -481,6 +483,17 @@ cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st) {
     }
     if ((e = cudaMalloc(&rd.ffg, sizeof(double) * h.size())) != cudaSuccess) return e;
     if ((e = cudaMemcpy(rd.ffg, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice)) !=
+        cudaSuccess)
+      return e;
+    std::vector<double> a(6 * (size_t)sc->ff_n);  // sliver chords in this frame
+    for (size_t k = 0; k < a.size() / 3; ++k) {
+      const double* g = &sc->ff_chord_host[3 * k];
+      a[3 * k] = g[0] * rd.f.e1[0] + g[1] * rd.f.e1[1] + g[2] * rd.f.e1[2];
+      a[3 * k + 1] = g[0] * rd.f.e2[0] + g[1] * rd.f.e2[1] + g[2] * rd.f.e2[2];
+      a[3 * k + 2] = g[0] * rd.f.d[0] + g[1] * rd.f.d[1] + g[2] * rd.f.d[2];
+    }
+    if ((e = cudaMalloc(&rd.ffa, sizeof(double) * a.size())) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(rd.ffa, a.data(), sizeof(double) * a.size(), cudaMemcpyHostToDevice)) !=
         cudaSuccess)
       return e;
   }

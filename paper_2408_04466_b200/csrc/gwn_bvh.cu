@@ -732,6 +732,7 @@ void free_round(Round& rd) {
   if (rd.leaves) cudaFree(rd.leaves);
   if (rd.vproj) cudaFree(rd.vproj);
   if (rd.ffg) cudaFree(rd.ffg);
+  if (rd.ffa) cudaFree(rd.ffa);
   if (rd.cell_offs) cudaFree(rd.cell_offs);
   if (rd.cell_ent) cudaFree(rd.cell_ent);
   rd = Round();

@@ -69,18 +69,21 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 // D_n^m of one cycle per block: items (segment, quadrature point) over the
 // cycle's edges; the regular solid harmonics and their gradients by the
-// recurrences of gwn_farfield.cuh (dual numbers), one warp reduction and one
-// shared-memory add per term.
+// recurrences of gwn_farfield.cuh (dual numbers), one warp reduction per term
+// into the warp's own partial sums (deterministic; 256 threads = 8 warps).
 __global__ void __launch_bounds__(256)
 k_ff_moments(const int64_t* __restrict__ coff, const int32_t* __restrict__ cedge,
-             const double* __restrict__ verts, int64_t V, int S, const double* __restrict__ g,
-             FFQuad Q, double* __restrict__ D) {
-  __shared__ double acc[2 * kFFTerms];
-  const int c = blockIdx.x;
-  for (int k = threadIdx.x; k < 2 * kFFTerms; k += blockDim.x) acc[k] = 0.0;
+             const int32_t* __restrict__ chord, const double* __restrict__ verts, int64_t V,
+             int S, const double* __restrict__ g, FFQuad Q, double* __restrict__ D) {
+  // per-warp partial sums, added in a fixed order: the moments (and every
+  // far-field result) are bit-identical across scene builds
+  __shared__ double acc[8][2 * kFFTerms];
+  const int c = blockIdx.x, wid = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < 8 * 2 * kFFTerms; k += blockDim.x) (&acc[0][0])[k] = 0.0;
   __syncthreads();
   const int64_t e0 = coff[c], e1 = coff[c + 1];
-  const int64_t segs = (e1 - e0) * (S - 1);
+  const int ch = chord[c];  // sliver: one more segment, the closing chord
+  const int64_t segs = (e1 - e0) * (S - 1) + (ch >= 0 ? 1 : 0);
   const int64_t items = segs * kFFQ * kFFQ;
   const double gx = g[3 * c], gy = g[3 * c + 1], gz = g[3 * c + 2];
   for (int64_t base = 0; base < items; base += blockDim.x) {
@@ -89,11 +92,17 @@ k_ff_moments(const int64_t* __restrict__ coff, const int32_t* __restrict__ cedge
     if (it < items) {
       const int64_t sg = it / (kFFQ * kFFQ);
       const int qp = (int)(it % (kFFQ * kFFQ));
-      const int64_t e = cedge[e0 + sg / (S - 1)];
-      const int64_t k = e * S + sg % (S - 1);
-      const double ax = verts[k] - gx, ay = verts[V + k] - gy, az = verts[2 * V + k] - gz;
-      const double bx = verts[k + 1] - gx, by = verts[V + k + 1] - gy,
-                   bz = verts[2 * V + k + 1] - gz;
+      int64_t ka, kb;
+      if (ch >= 0 && sg == segs - 1) {  // chord: last sample -> first
+        ka = (int64_t)ch * S + S - 1;
+        kb = (int64_t)ch * S;
+      } else {
+        const int64_t e = cedge[e0 + sg / (S - 1)];
+        ka = e * S + sg % (S - 1);
+        kb = ka + 1;
+      }
+      const double ax = verts[ka] - gx, ay = verts[V + ka] - gy, az = verts[2 * V + ka] - gz;
+      const double bx = verts[kb] - gx, by = verts[V + kb] - gy, bz = verts[2 * V + kb] - gz;
       nx = ay * bz - az * by;
       ny = az * bx - ax * bz;
       nz = ax * by - ay * bx;
@@ -142,15 +151,19 @@ k_ff_moments(const int64_t* __restrict__ coff, const int32_t* __restrict__ cedge
         const double fr = warp_sum_d(wq * (nx * axR + ny * ayR + nz * azR));
         const double fi = warp_sum_d(-wq * (nx * axI + ny * ayI + nz * azI));
         if ((threadIdx.x & 31) == 0) {
-          atomicAdd(&acc[2 * ff_term(n, m)], fr);
-          atomicAdd(&acc[2 * ff_term(n, m) + 1], fi);
+          acc[wid][2 * ff_term(n, m)] += fr;
+          acc[wid][2 * ff_term(n, m) + 1] += fi;
         }
       }
     }
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < 2 * kFFTerms; k += blockDim.x)
-    D[(int64_t)c * 2 * kFFTerms + k] = acc[k];
+  for (int k = threadIdx.x; k < 2 * kFFTerms; k += blockDim.x) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += acc[w][k];
+    D[(int64_t)c * 2 * kFFTerms + k] = v;
+  }
 }
 
 static int ff_find(std::vector<int>& p, int a) {
@@ -164,7 +177,10 @@ void free_farfield(gwn_scene* sc) {
   if (sc->ff_r) cudaFree(sc->ff_r);
   if (sc->ff_D) cudaFree(sc->ff_D);
   if (sc->ff_lv) cudaFree(sc->ff_lv);
+  if (sc->ff_chord) cudaFree(sc->ff_chord);
   sc->ff_lv = nullptr;
+  sc->ff_chord = nullptr;
+  sc->ff_chord_host.clear();
   sc->ff_edge = nullptr;
   sc->ff_g = sc->ff_r = sc->ff_D = nullptr;
   sc->ff_n = 0;
@@ -214,70 +230,105 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   cudaError_t err = cudaMemcpy(hv.data(), sc->verts, sizeof(double) * 3 * V,
                                cudaMemcpyDeviceToHost);
   if (err != cudaSuccess) return err;
-  std::vector<double> g(3 * C, 0.0), cnt(C, 0.0), rho(C, 0.0), aabs(C, 0.0);
-  for (int64_t e = 0; e < ne; ++e)
-    for (int s = 0; s < S; ++s) {
-      const int64_t k = e * S + s;
-      const int c = ecyc[e];
-      g[3 * c] += hv[k];
-      g[3 * c + 1] += hv[V + k];
-      g[3 * c + 2] += hv[2 * V + k];
-      cnt[c] += 1.0;
-    }
-  for (int c = 0; c < C; ++c)
-    for (int k = 0; k < 3; ++k) g[3 * c + k] /= cnt[c];
-  for (int64_t e = 0; e < ne; ++e) {
-    const int c = ecyc[e];
-    for (int s = 0; s < S; ++s) {
-      const int64_t k = e * S + s;
-      const double ax = hv[k] - g[3 * c], ay = hv[V + k] - g[3 * c + 1],
-                   az = hv[2 * V + k] - g[3 * c + 2];
-      rho[c] = fmax(rho[c], sqrt(ax * ax + ay * ay + az * az));
-      if (s + 1 < S) {
-        const double bx = hv[k + 1] - g[3 * c], by = hv[V + k + 1] - g[3 * c + 1],
-                     bz = hv[2 * V + k + 1] - g[3 * c + 2];
-        const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
-        aabs[c] += 0.5 * sqrt(cx * cx + cy * cy + cz * cz);
+  // expansion entries: whole cycles, and for a cycle too large to be far
+  // from anything (a sheet's border) one sliver per edge -- the edge closed
+  // by its chord, whose exact chord term the far kernel adds back
+  struct Entry {
+    std::vector<int32_t> edges;
+    int32_t chord = -1;  // edge whose end points close the sliver, -1: a cycle
+    double g[3] = {0, 0, 0}, rho = 0, aabs = 0;
+  };
+  std::vector<std::vector<int32_t>> cyc_edges(C);
+  for (int64_t e = 0; e < ne; ++e) cyc_edges[ecyc[e]].push_back((int32_t)e);
+  auto vtx = [&](int64_t k, double* o) {
+    o[0] = hv[k];
+    o[1] = hv[V + k];
+    o[2] = hv[2 * V + k];
+  };
+  auto geometry = [&](Entry& en) {
+    double cntv = 0.0;
+    for (int32_t e : en.edges)
+      for (int s2 = 0; s2 < S; ++s2) {
+        double v[3];
+        vtx((int64_t)e * S + s2, v);
+        for (int k = 0; k < 3; ++k) en.g[k] += v[k];
+        cntv += 1.0;
       }
+    for (int k = 0; k < 3; ++k) en.g[k] /= cntv;
+    auto tri = [&](const double* a0, const double* b0) {
+      const double ax = a0[0] - en.g[0], ay = a0[1] - en.g[1], az = a0[2] - en.g[2];
+      const double bx = b0[0] - en.g[0], by = b0[1] - en.g[1], bz = b0[2] - en.g[2];
+      const double cx = ay * bz - az * by, cy = az * bx - ax * bz, cz = ax * by - ay * bx;
+      en.aabs += 0.5 * sqrt(cx * cx + cy * cy + cz * cz);
+    };
+    for (int32_t e : en.edges)
+      for (int s2 = 0; s2 < S; ++s2) {
+        double v[3], w[3];
+        vtx((int64_t)e * S + s2, v);
+        en.rho = fmax(en.rho, sqrt((v[0] - en.g[0]) * (v[0] - en.g[0]) +
+                                   (v[1] - en.g[1]) * (v[1] - en.g[1]) +
+                                   (v[2] - en.g[2]) * (v[2] - en.g[2])));
+        if (s2 + 1 < S) {
+          vtx((int64_t)e * S + s2 + 1, w);
+          tri(v, w);
+        }
+      }
+    if (en.chord >= 0) {  // closing chord, last sample -> first
+      double a0[3], b0[3];
+      vtx((int64_t)en.chord * S + S - 1, a0);
+      vtx((int64_t)en.chord * S, b0);
+      tri(a0, b0);
+    }
+  };
+  auto rmin_of = [&](const Entry& en, double p) {
+    return en.rho * (1.0 + 1e-9) +
+           pow(en.aabs * (p + 2.0) * pow(en.rho, p + 1.0) / kFFTau, 1.0 / (p + 3.0));
+  };
+  static const bool all = getenv("GWN_FF_ALL") != nullptr;  // tests: expand every cycle
+  std::vector<Entry> ents;
+  for (int c = 0; c < C; ++c) {
+    Entry en;
+    en.edges = cyc_edges[c];
+    geometry(en);
+    if (en.rho > 0.0 && (all || rmin_of(en, kFFK) < 0.5 * sc->diag)) {
+      ents.push_back(en);
+      continue;
+    }
+    for (int32_t e : cyc_edges[c]) {  // too large: per-edge slivers
+      Entry sv;
+      sv.edges = {e};
+      sv.chord = e;
+      geometry(sv);
+      if (sv.rho > 0.0 && rmin_of(sv, kFFK) < 0.5 * sc->diag) ents.push_back(sv);
     }
   }
-  // far radius: A_abs (K+2) rho^(K+1) / (R - rho)^(K+3) <= tau; cycles whose
-  // R_min exceeds twice the scene diagonal keep the exact sum only
-  std::vector<int> keep(C, -1);
-  std::vector<double> r2, gk, lvr;
-  int nk = 0;
-  for (int c = 0; c < C; ++c) {
-    const double K = kFFK;
-    const double rmin =
-        rho[c] * (1.0 + 1e-9) +
-        pow(aabs[c] * (K + 2.0) * pow(rho[c], K + 1.0) / kFFTau, 1.0 / (K + 3.0));
-    static const bool all = getenv("GWN_FF_ALL") != nullptr;  // tests: expand every cycle
-    if ((!all && !(rmin < 2.0 * sc->diag)) || !(rho[c] > 0.0)) continue;
-    keep[c] = nk++;
-    const double line = rho[c] * (1.0 + 1e-6) + 1e-9 * (1.0 + sc->diag);
+  const int nk = (int)ents.size();
+  if (nk == 0) return cudaSuccess;
+  std::vector<double> r2, gk, lvr, chk(6 * (size_t)nk, 0.0);
+  std::vector<int32_t> fe(ne, -1), chord(nk, -1);
+  std::vector<int64_t> coff(nk + 1, 0);
+  std::vector<int32_t> cedge;
+  for (int c = 0; c < nk; ++c) {
+    const Entry& en = ents[c];
+    const double rmin = rmin_of(en, kFFK);
+    const double line = en.rho * (1.0 + 1e-6) + 1e-9 * (1.0 + sc->diag);
     r2.push_back(rmin * rmin);
     r2.push_back(line * line);
     for (int lv = 0; lv < kFFLevels; ++lv) {  // thresholds of the lower orders
-      const double p = ff_order(lv);
-      const double rp = rho[c] * (1.0 + 1e-9) +
-                        pow(aabs[c] * (p + 2.0) * pow(rho[c], p + 1.0) / kFFTau, 1.0 / (p + 3.0));
+      const double rp = rmin_of(en, ff_order(lv));
       lvr.push_back(lv == kFFLevels - 1 ? rmin * rmin : rp * rp);
     }
-    gk.insert(gk.end(), {g[3 * c], g[3 * c + 1], g[3 * c + 2]});
-  }
-  if (nk == 0) return cudaSuccess;
-  std::vector<int32_t> fe(ne);
-  std::vector<int64_t> coff(nk + 1, 0);
-  for (int64_t e = 0; e < ne; ++e) {
-    fe[e] = keep[ecyc[e]];
-    if (fe[e] >= 0) ++coff[fe[e] + 1];
-  }
-  for (int c = 0; c < nk; ++c) coff[c + 1] += coff[c];
-  std::vector<int32_t> cedge(coff[nk]);
-  {
-    std::vector<int64_t> pos(coff.begin(), coff.end() - 1);
-    for (int64_t e = 0; e < ne; ++e)
-      if (fe[e] >= 0) cedge[pos[fe[e]]++] = (int32_t)e;
+    gk.insert(gk.end(), {en.g[0], en.g[1], en.g[2]});
+    for (int32_t e : en.edges) {
+      fe[e] = c;
+      cedge.push_back(e);
+    }
+    coff[c + 1] = (int64_t)cedge.size();
+    chord[c] = en.chord;
+    if (en.chord >= 0) {  // chord end points: first sample (start), last (end)
+      vtx((int64_t)en.chord * S, &chk[6 * c]);
+      vtx((int64_t)en.chord * S + S - 1, &chk[6 * c + 3]);
+    }
   }
   int64_t* d_coff = nullptr;
   int32_t* d_cedge = nullptr;
@@ -294,16 +345,20 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   FF(cudaMemcpy(sc->ff_lv, lvr.data(), sizeof(double) * kFFLevels * nk, cudaMemcpyHostToDevice));
   FF(cudaMalloc(&d_coff, sizeof(int64_t) * (nk + 1)));
   FF(cudaMalloc(&d_cedge, sizeof(int32_t) * std::max<int64_t>(1, coff[nk])));
+  FF(cudaMalloc(&sc->ff_chord, sizeof(int32_t) * nk));
+  FF(cudaMemcpy(sc->ff_chord, chord.data(), sizeof(int32_t) * nk, cudaMemcpyHostToDevice));
   FF(cudaMemcpy(sc->ff_edge, fe.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice));
   FF(cudaMemcpy(sc->ff_g, gk.data(), sizeof(double) * 3 * nk, cudaMemcpyHostToDevice));
   FF(cudaMemcpy(sc->ff_r, r2.data(), sizeof(double) * 2 * nk, cudaMemcpyHostToDevice));
   FF(cudaMemcpy(d_coff, coff.data(), sizeof(int64_t) * (nk + 1), cudaMemcpyHostToDevice));
   FF(cudaMemcpy(d_cedge, cedge.data(), sizeof(int32_t) * coff[nk], cudaMemcpyHostToDevice));
-  k_ff_moments<<<nk, 256>>>(d_coff, d_cedge, sc->verts, V, S, sc->ff_g, ff_quad(), sc->ff_D);
+  k_ff_moments<<<nk, 256>>>(d_coff, d_cedge, sc->ff_chord, sc->verts, V, S, sc->ff_g, ff_quad(),
+                            sc->ff_D);
   FF(cudaGetLastError());
   FF(cudaDeviceSynchronize());
   sc->ff_n = nk;
   sc->ff_g_host = gk;
+  sc->ff_chord_host = chk;
 out:
 #undef FF
   if (d_coff) cudaFree(d_coff);
@@ -357,7 +412,8 @@ __global__ void __launch_bounds__(128)
 k_boundary_far(int32_t m, const int32_t* __restrict__ order, const int32_t* __restrict__ active,
                const double* __restrict__ pos, int32_t C, const double* __restrict__ ffg,
                const double* __restrict__ ffr, const double* __restrict__ fflv,
-               const double* __restrict__ gw, const double* __restrict__ D, Frame f,
+               const double* __restrict__ gw, const double* __restrict__ D,
+               const int32_t* __restrict__ chord, const double* __restrict__ ffa, Frame f,
                double* __restrict__ brow, unsigned long long* __restrict__ counters) {
   const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = t < m;
@@ -384,8 +440,26 @@ k_boundary_far(int32_t m, const int32_t* __restrict__ order, const int32_t* __re
     else if (R2 > __ldg(lv + 1)) om += ff_eval<ff_order(1)>(x, y, z, Dc);
     else if (R2 > __ldg(lv + 2)) om += ff_eval<ff_order(2)>(x, y, z, Dc);
     else om += ff_eval<ff_order(3)>(x, y, z, Dc);
+    if (__ldg(chord + c) >= 0) {
+      // sliver: the edge's fan sum = Omega(edge + chord back) + the chord's
+      // forward fan term, K4's shifted form in the ray frame (den > 0: the
+      // line misses the sliver's sphere)
+      const double* A = ffa + 6 * (int64_t)c;
+      const double rax = __ldg(A) - qa, ray = __ldg(A + 1) - qb, raz = __ldg(A + 2) - qc;
+      const double rbx = __ldg(A + 3) - qa, rby = __ldg(A + 4) - qb, rbz = __ldg(A + 5) - qc;
+      const double ia = 1.0 / sqrt(rax * rax + ray * ray + raz * raz);
+      const double ib = 1.0 / sqrt(rbx * rbx + rby * rby + rbz * rbz);
+      const double uax = rax * ia, uay = ray * ia, uaz = fma(raz, ia, -1.0);
+      const double ubx = rbx * ib, uby = rby * ib, ubz = fma(rbz, ib, -1.0);
+      const double num = uay * ubx - uax * uby;
+      const double den = uax * ubx + uay * uby + uaz * ubz;
+      om += 2.0 * atan2(num, den);
+    }
   }
   // K4's partials are sums of atan2 (half angles): Omega / 2
+#ifdef GWN_FF_NOFAR
+  om = 0.0;
+#endif
   if (live) brow[(int64_t)blockIdx.y * m + s] = 0.5 * om;
   // far (query, cycle) pairs, one atomic per warp
 #pragma unroll
@@ -400,7 +474,8 @@ cudaError_t launch_boundary_far(const gwn_scene* sc, const Round& rd, int32_t m,
   if (m <= 0 || sc->ff_n <= 0) return cudaSuccess;
   const dim3 grid((m + 127) / 128, kFFRows);
   k_boundary_far<<<grid, 128, 0, st>>>(m, order, active, pos, sc->ff_n, rd.ffg, sc->ff_r,
-                                       sc->ff_lv, sc->ff_g, sc->ff_D, rd.f, brow, counters);
+                                       sc->ff_lv, sc->ff_g, sc->ff_D, sc->ff_chord, rd.ffa,
+                                       rd.f, brow, counters);
   return cudaGetLastError();
 }
 

@@ -94,6 +94,7 @@ struct Round {
   double amin = 0, ainv = 0, bmin = 0, binv = 0;  // projected scene box (Morton keys)
   double* vproj = nullptr;     // (3,V) boundary vertices in the ray frame (K4)
   double* ffg = nullptr;       // (ff_n,3) far-field cycle centres in the ray frame
+  double* ffa = nullptr;       // (ff_n,6) sliver chord end points in the ray frame
   // uniform grid over the leaf boxes (K2 point location); used when its
   // cells stay short, else the LBVH
   bool use_grid = false;
@@ -137,6 +138,8 @@ struct gwn_scene {
   double* ff_r = nullptr;       // (ff_n,2) R_min^2, line radius^2
   double* ff_D = nullptr;       // (ff_n, kFFTerms, 2) double-layer moments
   double* ff_lv = nullptr;      // (ff_n, kFFLevels) R^2 thresholds of the adaptive orders
+  int32_t* ff_chord = nullptr;  // (ff_n) sliver entries: edge of the closing chord, else -1
+  std::vector<double> ff_chord_host;  // (ff_n,6) chord start / end (world), zeros for cycles
   std::vector<double> ff_g_host;
   // per-round caches
   std::mutex mu;

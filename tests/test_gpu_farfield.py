@@ -1,6 +1,6 @@
-"""Far field of the boundary term (DESIGN §2 K4): the
-solid-harmonic expansion of closed net-boundary cycles against the exact fan
-sum (GWN_FARFIELD=0 switches the expansion off at scene creation), in fresh
+"""Far field of the boundary term: the
+solid-harmonic expansion of closed net-boundary cycles (and of edge slivers
+closed by their chords) against the exact fan sum (GWN_FARFIELD=0 switches the expansion off at scene creation), in fresh
 processes so the switch is read at library load."""
 
 import os
@@ -77,11 +77,22 @@ def test_farfield_batching_is_bit_identical(tmp_path):
     assert np.array_equal(r["w"], r["wh"]) and np.array_equal(r["st"], r["sh"])
 
 
-@pytest.mark.parametrize("cfg", [1, 3])
-def test_open_sheets_keep_the_exact_sum(tmp_path, cfg):
-    """One border cycle whose far radius exceeds the scene: no expansion, and the
-    results are bit-identical to the switch being off."""
-    ex = _run(tmp_path, cfg, 1 << 12, GWN_FARFIELD="0")
-    ff = _run(tmp_path, cfg, 1 << 12)
+def test_small_patch_keeps_the_exact_sum(tmp_path):
+    """Config 1: the patch's border slivers are never far from its own box, so
+    nothing is expanded and the results are bit-identical to the switch off."""
+    ex = _run(tmp_path, 1, 1 << 12, GWN_FARFIELD="0")
+    ff = _run(tmp_path, 1, 1 << 12)
     assert int(ff["cycles"]) == 0
     assert np.array_equal(ex["w"], ff["w"]) and np.array_equal(ex["st"], ff["st"])
+
+
+def test_open_sheet_edge_slivers(tmp_path):
+    """Config 3: the border cycle is too large to be far, so each of its 32
+    edges is expanded as a sliver closed by its chord (the chord's exact fan
+    term added back)."""
+    ex = _run(tmp_path, 3, 1 << 14, GWN_FARFIELD="0")
+    ff = _run(tmp_path, 3, 1 << 14)
+    assert int(ff["cycles"]) == 32 and int(ff["far"]) > 0
+    assert np.array_equal(ex["st"], ff["st"])
+    ok = ex["st"] == 0
+    assert np.abs(ex["w"] - ff["w"])[ok].max() <= 1e-11
