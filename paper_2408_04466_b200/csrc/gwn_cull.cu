@@ -96,9 +96,7 @@ k_cull_grid(GridView grid, Frame f, int32_t m, const int32_t* __restrict__ activ
     const int32_t me = blockIdx.x * blockDim.x + threadIdx.x;
     int buf[kLBuf];
     int n = 0;
-    for (int j = 0; j < cnt; ++j) {
-      const float2* p = reinterpret_cast<const float2*>(grid.ent + beg + j);
-      const float2 e0 = __ldg(p), e1 = __ldg(p + 1), e2 = __ldg(p + 2);
+    auto take = [&](float2 e0, float2 e1, float2 e2) {
       if (fqa >= e0.x && fqa <= e0.y && fqb >= e1.x && fqb <= e1.y && e2.x >= fqc) {
         const int leaf = __float_as_int(e2.y);
         if (n < kLBuf) {
@@ -108,6 +106,28 @@ k_cull_grid(GridView grid, Frame f, int32_t m, const int32_t* __restrict__ activ
           if (k < cap) pairs[k] = make_int2(me, leaf);
         }
       }
+    };
+    // entries in groups of GWN_CULL_BATCH: every load of a group is issued
+    // before its first test, so one L1/L2 round trip covers the group
+#ifndef GWN_CULL_BATCH
+#define GWN_CULL_BATCH 4
+#endif
+    int j = 0;
+    for (; j + GWN_CULL_BATCH <= cnt; j += GWN_CULL_BATCH) {
+      float2 E[GWN_CULL_BATCH][3];
+#pragma unroll
+      for (int u = 0; u < GWN_CULL_BATCH; ++u) {
+        const float2* p = reinterpret_cast<const float2*>(grid.ent + beg + j + u);
+        E[u][0] = __ldg(p);
+        E[u][1] = __ldg(p + 1);
+        E[u][2] = __ldg(p + 2);
+      }
+#pragma unroll
+      for (int u = 0; u < GWN_CULL_BATCH; ++u) take(E[u][0], E[u][1], E[u][2]);
+    }
+    for (; j < cnt; ++j) {
+      const float2* p = reinterpret_cast<const float2*>(grid.ent + beg + j);
+      take(__ldg(p), __ldg(p + 1), __ldg(p + 2));
     }
     // one warp-aggregated reservation for the buffered candidates
     int hincl = n;
