@@ -70,6 +70,27 @@ def _traffic(kname: str, config: int, n: int):
     return t.get(kname.split(" ")[0])
 
 
+def _cull_roofline(stt, nq):
+    """K2 `k_cull_grid` against HBM: algorithmic DRAM bytes = per query the
+    position read (24 B), its ray-frame projection and chi / flag
+    accumulators written (24 + 8 B), the cell range read (8 B); per candidate
+    the (slot, leaf) pair written (8 B).  Cell entries are L2-resident."""
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            peak, src = json.load(f)["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+    except (OSError, ValueError, KeyError):
+        peak, src = 7700.0, "B200_PROFILING.md fallback"
+    ms = stt["ms_cull"]
+    algo = 64.0 * nq + 8.0 * stt["candidates"]
+    ach = algo / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+    return {"bound": "hbm", "kernel": "k_cull_grid (K2)", "achieved": ach, "peak": peak,
+            "unit": "GB/s", "frac": ach / peak if peak else None,
+            "traffic": _traffic("k_cull_grid", 2, nq), "algorithmic_bytes": algo,
+            "kernel_ms": ms, "peak_source": src,
+            "note": "latency-bound (ncu: long-scoreboard stalls on the dependent "
+                    "position -> cell -> entry loads), not bandwidth-bound"}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -465,6 +486,9 @@ def main():
                                         "(MEASURED_PEAKS.json has no FP64 entry)",
                          "kernel_ms": kms, "kernel_share_of_step":
                              kms / (ms_dev / args.steps) if ms_dev else None},
+            # the longest kernel of the step is the K2 cull: memory-latency bound,
+            # reported against the measured HBM copy bandwidth
+            "roofline_cull": _cull_roofline(stt, nq),
             "stage_ms": {"cull": stt["ms_cull"], "k3_candidates": stt["ms_k3_candidates"],
                          "k3_fallback": stt["ms_k3_fallback"], "k3_newton": stt["ms_k3_newton"],
                          "boundary": stt["ms_boundary"], "finalize": stt["ms_other"]},
