@@ -280,9 +280,16 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
       tri(a0, b0);
     }
   };
+  // smallest R at which the order-p truncation bound (gwn_farfield.cuh,
+  // ff_bound) is <= kFFTau; the bound decreases in R, so bisection
   auto rmin_of = [&](const Entry& en, double p) {
-    return en.rho * (1.0 + 1e-9) +
-           pow(en.aabs * (p + 2.0) * pow(en.rho, p + 1.0) / kFFTau, 1.0 / (p + 3.0));
+    double lo = en.rho * (1.0 + 1e-9), hi = 2.0 * lo;
+    while (ff_bound(en.aabs, en.rho, (int)p, hi) > kFFTau) hi *= 2.0;
+    for (int it = 0; it < 60; ++it) {
+      const double mid = 0.5 * (lo + hi);
+      (ff_bound(en.aabs, en.rho, (int)p, mid) > kFFTau ? lo : hi) = mid;
+    }
+    return hi;
   };
   static const bool all = getenv("GWN_FF_ALL") != nullptr;  // tests: expand every cycle
   std::vector<Entry> ents;

@@ -9,15 +9,22 @@
 //     Omega(p) = -sum_{n>=1} sum_{m=-n..n} D_n^m I_n^m(p - g),
 //     D_n^m = integral over the fan surface of n . conj(grad R_n^m(x - g)) dA,
 // with the regular / irregular solid harmonics R, I of the addition theorem
-// 1/|p - q| = sum_n sum_m conj(R_n^m(q)) I_n^m(p) (recurrences below; checked
-// in tools/farfield/proto.py).  Truncated at n = kFFK the error is at most
-//     A_abs (K+2) rho^(K+1) / (R - rho)^(K+3)
-// (|d^k (1/r)| <= k!/r^(k+1) along any unit direction, the Legendre bound),
-// so a (query, cycle) pair is "far" when R^2 >= R_min^2 with that bound at
-// kFFTau, and the line to the query misses the sphere.  Both K4 kernels take
+// 1/|p - q| = sum_n sum_m conj(R_n^m(q)) I_n^m(p) (recurrences in
+// gwn_farfield.cu; checked in tools/farfield/proto.py).  Keeping n <= K keeps
+// the degree-(K-1) part of grad_q 1/|p-q| in delta = q - g; the dropped part
+// is bounded two ways (ff_bound takes the smaller):
+//   Taylor remainder with |d^k (1/r)| <= k!/r^(k+1) along unit directions:
+//     A_abs (K+1) rho^K / (R - rho)^(K+2);
+//   Legendre tail: grad of |d|^n P_n(cos) is <= sqrt(2) n |d|^(n-1) (|P_n| <= 1
+//   and Bernstein's inequality), summed over n > K:
+//     sqrt(2) A_abs (K+1) rho^K / (R^K (R - rho)^2).
+// A (query, cycle) pair is "far" when R^2 >= R_min^2 with the bound at
+// kFFTau and the line to the query misses the sphere.  Both K4 kernels take
 // the decision with ff_far() on the same bits, so the exact kernel's masked /
 // skipped segments and the far kernel's terms partition the cycles exactly.
 #pragma once
+
+#include <math.h>
 
 #include "gwn_internal.h"
 
@@ -38,6 +45,16 @@ constexpr int kFFLevels = 4;
 __host__ __device__ constexpr int ff_order(int lv) { return kFFK - 4 * (kFFLevels - 1 - lv); }
 
 __device__ __forceinline__ int ff_term(int n, int m) { return n * (n + 1) / 2 + m; }
+
+// truncation bound of the order-K expansion at distance R (see above; host)
+inline double ff_bound(double aabs, double rho, int K, double R) {
+  if (!(R > rho)) return INFINITY;
+  const double x = rho / R;
+  const double taylor = aabs * (K + 1.0) * pow(rho, (double)K) / pow(R - rho, K + 2.0);
+  const double legendre = 1.4142135623730951 * aabs * (K + 1.0) * pow(x, (double)K) /
+                          ((R - rho) * (R - rho));
+  return fmin(taylor, legendre);
+}
 
 // query in the round frame (explicit roundings: every kernel that takes a
 // far-field decision computes bit-identical coordinates)

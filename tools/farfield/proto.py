@@ -147,3 +147,21 @@ def sign_check():
         r = g - p
         line = np.sqrt(max(r @ r - (r @ d) ** 2, 0))
         print(f"line dist {line:.3f}  k4 {k4_fan(p, V, d):+.12f}  exact {omega_exact(p, V, g):+.12f}")
+
+
+def bound_check():
+    """The truncation bounds of gwn_farfield.cuh against measured errors."""
+    V = loop_of_patch()
+    for Kt in (6, 8, 10):
+        g, rho, aabs, D = moments(V, Kt)
+        rng = np.random.default_rng(1)
+        for Rr in (1.5, 2, 3, 5, 10):
+            errs = []
+            for _ in range(40):
+                u = rng.normal(size=3); u /= np.linalg.norm(u)
+                p = g + Rr * rho * u
+                errs.append(abs(omega_mp(p, g, D, Kt) - omega_exact(p, V, g)))
+            R = Rr * rho
+            tay = aabs * (Kt + 1) * rho ** Kt / (R - rho) ** (Kt + 2)
+            leg = 2 ** 0.5 * aabs * (Kt + 1) * (rho / R) ** Kt / (R - rho) ** 2
+            print(f"K {Kt} R/rho {Rr}: max err {max(errs):.2e}  bound {min(tay, leg):.2e}  ok {max(errs) <= min(tay, leg)}")
