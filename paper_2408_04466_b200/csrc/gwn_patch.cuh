@@ -572,60 +572,80 @@ __device__ __forceinline__ void lds2_keep(const double* p, double& x, double& y)
 
 // kLoad: 0 = coefficients through the compiler (hoisted into registers),
 // 1 = re-read from global (L1) every iteration, 2 = re-read from shared
-template <int kLoad = 0>
-__device__ __forceinline__ RootResult newton_solve_pow(const double* __restrict__ W48, double qa,
-                                                       double qb, double qc, double u, double v,
-                                                       const DevParams& prm) {
-  RootResult r;
-  r.iters = 0;
-  double A = 0, Au = 0, Av = 0, B = 0, Bu = 0, Bv = 0;
-  double du = 0.0, dv = 0.0;
-  bool conv = false;
-  for (int it = 0; it < kNewtonMax; ++it) {
-    const double u3 = 3.0 * u, v3 = 3.0 * v;
-    if (kLoad) {
-      double X[32];
+template <int kLoad>
+__device__ __forceinline__ void pow_eval_ab(const double* __restrict__ W48, double u, double v,
+                                            double& A, double& Au, double& Av, double& B,
+                                            double& Bu, double& Bv) {
+  const double u3 = 3.0 * u, v3 = 3.0 * v;
+  if (kLoad) {
+    double X[32];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        if (kLoad == 2) lds2_keep(W48 + 2 * k, X[2 * k], X[2 * k + 1]);
-        else ldg2_keep(W48 + 2 * k, X[2 * k], X[2 * k + 1]);
-      }
-      eval_pow(X, u, v, u3, v3, A, Au, Av);
-      eval_pow(X + 16, u, v, u3, v3, B, Bu, Bv);
-    } else {
-      eval_pow(W48, u, v, u3, v3, A, Au, Av);
-      eval_pow(W48 + 16, u, v, u3, v3, B, Bu, Bv);
+    for (int k = 0; k < 16; ++k) {
+      if (kLoad == 2) lds2_keep(W48 + 2 * k, X[2 * k], X[2 * k + 1]);
+      else ldg2_keep(W48 + 2 * k, X[2 * k], X[2 * k + 1]);
     }
-    A -= qa;
-    B -= qb;
-    r.iters++;
-    const double det = Au * Bv - Av * Bu;
-    if (!(fabs(det) > 0.0)) break;
-    const double id = 1.0 / det;
-    const double su = (Bv * A - Av * B) * id, sv = (Au * B - Bu * A) * id;
-    if (!isfinite(su) || !isfinite(sv)) break;
-    if (fabs(su) <= GWN_NEWTON_STOP * fmax(1.0, fabs(u)) &&
-        fabs(sv) <= GWN_NEWTON_STOP * fmax(1.0, fabs(v)) &&
-        (GWN_NEWTON_STOP > 1e-11 || sqrt(A * A + B * B) <= prm.residual)) {
-      du = su;
-      dv = sv;
-      conv = true;
-      if (GWN_NEWTON_STOP > 1e-11) {
-        A = 0.0;
-        B = 0.0;
-      }
-      break;
+    eval_pow(X, u, v, u3, v3, A, Au, Av);
+    eval_pow(X + 16, u, v, u3, v3, B, Bu, Bv);
+  } else {
+    eval_pow(W48, u, v, u3, v3, A, Au, Av);
+    eval_pow(W48 + 16, u, v, u3, v3, B, Bu, Bv);
+  }
+}
+
+// Newton iteration state (power basis); `act` while iterating
+struct NState {
+  double u, v, du, dv, A, Au, Av, B, Bu, Bv;
+  int iters;
+  bool conv, act;
+};
+
+__device__ __forceinline__ NState nstate(double u, double v, bool act) {
+  NState s;
+  s.u = u; s.v = v; s.du = 0.0; s.dv = 0.0;
+  s.A = s.Au = s.Av = s.B = s.Bu = s.Bv = 0.0;
+  s.iters = 0; s.conv = false; s.act = act;
+  return s;
+}
+
+// one iteration on freshly evaluated A, B, partials (already minus q)
+__device__ __forceinline__ void nstate_update(NState& s, const DevParams& prm) {
+  s.iters++;
+  const double det = s.Au * s.Bv - s.Av * s.Bu;
+  if (!(fabs(det) > 0.0)) { s.act = false; return; }
+  const double id = 1.0 / det;
+  const double su = (s.Bv * s.A - s.Av * s.B) * id, sv = (s.Au * s.B - s.Bu * s.A) * id;
+  if (!isfinite(su) || !isfinite(sv)) { s.act = false; return; }
+  if (fabs(su) <= GWN_NEWTON_STOP * fmax(1.0, fabs(s.u)) &&
+      fabs(sv) <= GWN_NEWTON_STOP * fmax(1.0, fabs(s.v)) &&
+      (GWN_NEWTON_STOP > 1e-11 || sqrt(s.A * s.A + s.B * s.B) <= prm.residual)) {
+    s.du = su;
+    s.dv = sv;
+    s.conv = true;
+    if (GWN_NEWTON_STOP > 1e-11) {
+      s.A = 0.0;
+      s.B = 0.0;
     }
-    u -= su;
-    v -= sv;
-    if (fabs(u) > 8.0 || fabs(v) > 8.0) break;
+    s.act = false;
+    return;
   }
-  if (!conv) {
-    eval_pow(W48, u, v, 3.0 * u, 3.0 * v, A, Au, Av);
-    eval_pow(W48 + 16, u, v, 3.0 * u, 3.0 * v, B, Bu, Bv);
-    A -= qa;
-    B -= qb;
+  s.u -= su;
+  s.v -= sv;
+  if (fabs(s.u) > 8.0 || fabs(s.v) > 8.0) s.act = false;
+}
+
+// acceptance (surfaces.py:665-670) and record fields (surfaces.py:681-697)
+__device__ __forceinline__ RootResult nstate_finish(NState& s, const double* __restrict__ W48,
+                                                    double qa, double qb, double qc,
+                                                    const DevParams& prm) {
+  RootResult r;
+  r.iters = s.iters;
+  double u = s.u, v = s.v;
+  if (!s.conv) {
+    pow_eval_ab<0>(W48, u, v, s.A, s.Au, s.Av, s.B, s.Bu, s.Bv);
+    s.A -= qa;
+    s.B -= qb;
   }
+  const double A = s.A, Au = s.Au, Av = s.Av, B = s.B, Bu = s.Bu, Bv = s.Bv;
   r.t = 0.0;
   r.sign = 0; r.tang = 0; r.graze = 0; r.onsurf = 0;
   if (!(sqrt(A * A + B * B) <= prm.residual)) {                        // surfaces.py:665
@@ -636,8 +656,8 @@ __device__ __forceinline__ RootResult newton_solve_pow(const double* __restrict_
   }
   double C, Cu, Cv;
   eval_pow(W48 + 32, u, v, 3.0 * u, 3.0 * v, C, Cu, Cv);
-  u -= du;
-  v -= dv;
+  u -= s.du;
+  v -= s.dv;
   r.u = u;
   r.v = v;
   const double tol = prm.domain_tol;                                   // surfaces.py:668
@@ -645,7 +665,7 @@ __device__ __forceinline__ RootResult newton_solve_pow(const double* __restrict_
     r.status = ROOT_REJECTED;
     return r;
   }
-  r.t = C - qc - (Cu * du + Cv * dv);
+  r.t = C - qc - (Cu * s.du + Cv * s.dv);
   if (r.t < -prm.t_tol) {                                              // surfaces.py:670
     r.status = ROOT_REJECTED;
     return r;
@@ -663,6 +683,24 @@ __device__ __forceinline__ RootResult newton_solve_pow(const double* __restrict_
   r.onsurf = fabs(r.t) <= prm.on_surface_t;
   r.status = ROOT_ACCEPTED;
   return r;
+}
+
+// newton_solve with the nets in the power basis (K3 Newton pass): identical
+// iteration, stopping rule, acceptance (surfaces.py:665-670) and record
+// fields (surfaces.py:681-697); only the evaluation of the map differs (by
+// rounding).  W48 = (A, B, C) power coefficients of the patch (Round::powc).
+template <int kLoad = 0>
+__device__ __forceinline__ RootResult newton_solve_pow(const double* __restrict__ W48, double qa,
+                                                       double qb, double qc, double u, double v,
+                                                       const DevParams& prm) {
+  NState s = nstate(u, v, true);
+  for (int it = 0; it < kNewtonMax && s.act; ++it) {
+    pow_eval_ab<kLoad>(W48, s.u, s.v, s.A, s.Au, s.Av, s.B, s.Bu, s.Bv);
+    s.A -= qa;
+    s.B -= qb;
+    nstate_update(s, prm);
+  }
+  return nstate_finish(s, W48, qa, qb, qc, prm);
 }
 
 }  // namespace gwn
