@@ -428,14 +428,12 @@ struct RootResult {
 // Newton on the whole patch from (u, v); residual / domain / t acceptance of
 // surfaces.py:665-670, record fields of surfaces.py:681-697 in the
 // right-handed ray frame (d = (0,0,1)).
-// 16-byte read-only load the compiler may not hoist out of a loop: kReload
-// Newton re-reads the (L1-resident) A/B nets every iteration instead of
-// holding 32 doubles in registers, which buys occupancy.
+// 16-byte read-only load the compiler may not hoist out of a loop (the
+// power-basis Newton with kLoad = 1 re-reads its nets every iteration)
 __device__ __forceinline__ void ldg2_keep(const double* p, double& x, double& y) {
   asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "l"(p));
 }
 
-template <bool kReload = false>
 __device__ __forceinline__ RootResult newton_solve(const double* __restrict__ P48, double qa,
                                                    double qb, double qc, double u, double v,
                                                    const DevParams& prm) {
@@ -448,16 +446,8 @@ __device__ __forceinline__ RootResult newton_solve(const double* __restrict__ P4
   for (int it = 0; it < kNewtonMax; ++it) {
     bern3(u, bu, dbu);
     bern3(v, bv, dbv);
-    if (kReload) {
-      double X[32];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) ldg2_keep(P48 + 2 * k, X[2 * k], X[2 * k + 1]);
-      eval_coord(X, bu, dbu, bv, dbv, A, Au, Av);
-      eval_coord(X + 16, bu, dbu, bv, dbv, B, Bu, Bv);
-    } else {
-      eval_coord(P48, bu, dbu, bv, dbv, A, Au, Av);
-      eval_coord(P48 + 16, bu, dbu, bv, dbv, B, Bu, Bv);
-    }
+    eval_coord(P48, bu, dbu, bv, dbv, A, Au, Av);
+    eval_coord(P48 + 16, bu, dbu, bv, dbv, B, Bu, Bv);
     A -= qa;
     B -= qb;
     r.iters++;

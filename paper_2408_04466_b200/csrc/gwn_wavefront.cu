@@ -212,7 +212,7 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
     __syncwarp();
     int cur = 0, ncur = s_n0[wb], levels = 0;
     const long long tclk0 = clock64();
-    int tree_lv = 0, code_lv = 0, newton_calls = 0;
+    int tree_lv = 0, code_lv = 0;
     while (ncur > 0) {
       ++levels;
       {
