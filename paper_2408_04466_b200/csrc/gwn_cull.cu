@@ -53,6 +53,10 @@ k_cull_grid(GridView grid, Frame f, int32_t m, const int32_t* __restrict__ activ
             const double* __restrict__ pos, double* __restrict__ qproj,
             int2* __restrict__ pairs, unsigned long long* __restrict__ pair_count,
             unsigned long long cap, CullZero z) {
+  // programmatic dependent launch: K3's candidate test (which waits for this
+  // grid's completion before reading) may launch once the last wave of cull
+  // blocks is running, filling SMs as they retire
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   int beg = 0, cnt = 0;

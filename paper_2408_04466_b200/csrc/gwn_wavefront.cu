@@ -103,6 +103,8 @@ constexpr int kCandBlock = 256;
 __global__ void __launch_bounds__(kCandBlock)
 k3_candidates(const unsigned long long* __restrict__ npairs_dev, K3Queues Q, WaveArgs w) {
   __shared__ BlockPush<kCandBlock / 32> S;
+  // launched programmatically behind the cull (GWN_PDL): wait for its results
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // on capacity overflow the engine discards and re-runs the round; never
   // read past the buffers
   const int64_t npairs = (int64_t)min(*npairs_dev, Q.cap);
@@ -165,6 +167,10 @@ k3_fallback(const NodeItem* __restrict__ in, const unsigned long long* __restric
   __shared__ int32_t islot[kFbWarps][32], ipatch[kFbWarps][32], imax[kFbWarps][32];
   __shared__ int32_t ichi[kFbWarps][32], ifl[kFbWarps][32], inodes[kFbWarps][32];
   __shared__ int32_t s_n0[kFbWarps];  // initial frontier size
+  // programmatic dependent launch (GWN_PDL): the Newton pass queued behind this
+  // kernel on the same stream may start as soon as every fallback block is
+  // resident -- it does not read the fallback's results
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t n = (int64_t)min(*in_count, w.n_cap);  // pushes past capacity were dropped
   const int lane = threadIdx.x & 31, wb = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -505,7 +511,24 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
              rd.sub_offs, rd.sub, rd.subbox, rd.subskip, rd.subgc, rd.sub_level};
   if (ev4) cudaEventRecord(ev4[0], st);
   tl_mark(st, "k3 start");
-  k3_candidates<<<g_cand, kCandBlock, 0, st>>>(npairs_dev, Q, w);
+  static const bool pdl_cand = [] {
+    const char* e = getenv("GWN_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  if (pdl_cand && !ev4) {  // programmatic dependent launch behind the cull
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g_cand);
+    cfg.blockDim = dim3(kCandBlock);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if ((e = cudaLaunchKernelEx(&cfg, k3_candidates, npairs_dev, Q, w)) != cudaSuccess) return e;
+  } else {
+    k3_candidates<<<g_cand, kCandBlock, 0, st>>>(npairs_dev, Q, w);
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // The fallback (few, latency-bound items) runs on a side stream,
   // concurrently with the Newton pass and K4; the engine joins it (`join`)
@@ -525,9 +548,17 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
     if ((e = cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming)) != cudaSuccess) return e;
   }
   // In timing mode (ev4) everything runs on `st` so each kernel's events
-  // measure it alone.
-  cudaStream_t fs = ev4 ? st : side;
-  if (!ev4) {
+  // measure it alone.  GWN_PDL (default on): the fallback runs on `st` too and
+  // the Newton pass is a programmatic dependent launch behind it, so the
+  // fallback's few long-lived blocks are resident first and Newton fills the
+  // rest of the GPU concurrently (no side stream, no join).
+  static const bool pdl = [] {
+    const char* e = getenv("GWN_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  const bool use_pdl = pdl && !ev4;
+  cudaStream_t fs = (ev4 || use_pdl) ? st : side;
+  if (!ev4 && !use_pdl) {
     if ((e = cudaEventRecord(fork_ev, st)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(side, fork_ev, 0)) != cudaSuccess) return e;
   }
@@ -537,7 +568,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
   tl_mark(fs, "fb done");
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev4) cudaEventRecord(ev4[2], fs);
-  if (!ev4) {
+  if (!ev4 && !use_pdl) {
     if ((e = cudaEventRecord(join_ev, side)) != cudaSuccess) return e;
     *join = join_ev;
   }
@@ -547,10 +578,27 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
     const char* e = getenv("GWN_NEWTON_SMEM");
     return !(e && atoi(e) == 0);
   }();
-  if (smem_ok && sc->P <= kTabMaxP)
+  const bool tabled = smem_ok && sc->P <= kTabMaxP;
+  if (use_pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(tabled ? g_newton_s : g_newton);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = tabled ? sizeof(double) * kTabStride * sc->P : 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int32_t P32 = (int32_t)sc->P;
+    e = tabled ? cudaLaunchKernelEx(&cfg, k3_newton<true>, w, P32)
+               : cudaLaunchKernelEx(&cfg, k3_newton<false>, w, P32);
+    if (e != cudaSuccess) return e;
+  } else if (tabled) {
     k3_newton<true><<<g_newton_s, 128, sizeof(double) * kTabStride * sc->P, st>>>(w, (int32_t)sc->P);
-  else
+  } else {
     k3_newton<false><<<g_newton, 128, 0, st>>>(w, (int32_t)sc->P);
+  }
   tl_mark(st, "newton done");
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev4) cudaEventRecord(ev4[3], st);
