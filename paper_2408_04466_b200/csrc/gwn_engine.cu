@@ -398,9 +398,13 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   Workspace ws;
   ws.st = st;
   const bool host = (flags & GWN_HOST_BUFFERS) != 0;
-  // auto chunk: 4M queries (2M when the boundary partials are wide)
+  // auto chunk: 4M queries (2M when the boundary partials are wide; 8M for
+  // far-field scenes, whose Morton-ordered K4 warps agree more often in larger
+  // chunks -- config 5 at 2^23 queries: 1254 -> 1086 ms)
   const int64_t chunk_max = sc->prm.chunk_queries > 0 ? sc->prm.chunk_queries
-                            : boundary_chunks(sc, 0) > 16 ? (1ll << 21) : (1ll << 22);
+                            : sc->ff_n > 0               ? (1ll << 23)
+                            : boundary_chunks(sc, 0) > 16 ? (1ll << 21)
+                                                          : (1ll << 22);
   // device scalar block, published to mapped pinned memory once per round
   // by K5's last block:
   // [0, CNT_N) eval counters, CNT_N + [0] candidate count, [1] next active
