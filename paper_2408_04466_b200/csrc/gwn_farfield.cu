@@ -415,7 +415,10 @@ __device__ __forceinline__ double ff_eval(double x, double y, double z,
   return -acc;
 }
 
-__global__ void __launch_bounds__(128)
+#ifndef GWN_FF_MINB
+#define GWN_FF_MINB 8
+#endif
+__global__ void __launch_bounds__(128, GWN_FF_MINB)
 k_boundary_far(int32_t m, const int32_t* __restrict__ order, const int32_t* __restrict__ active,
                const double* __restrict__ pos, int32_t C, const double* __restrict__ ffg,
                const double* __restrict__ ffr, const double* __restrict__ fflv,
