@@ -259,8 +259,11 @@ struct FFView {
   const double* r2;      // R_min^2, line radius^2
 };
 
+#ifndef GWN_K4_MINB_FF
+#define GWN_K4_MINB_FF 3  // far-field scenes: occupancy beats the few spills (config 5 -5%)
+#endif
 template <int QPT, bool kFF>
-__global__ void __launch_bounds__(kBlockQ, GWN_K4_MINB)
+__global__ void __launch_bounds__(kBlockQ, kFF ? GWN_K4_MINB_FF : GWN_K4_MINB)
 k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
              const double* __restrict__ vproj, int64_t V, int S, int64_t n_edges,
              const double* __restrict__ band_h, Frame f, DevParams prm,
