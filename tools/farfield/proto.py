@@ -57,8 +57,6 @@ def addition_check():
             s += t if m == 0 else 2 * t.real
     print("addition theorem:", s.real, 1 / np.linalg.norm(p - q))
 
-addition_check()
-
 
 def loop_of_patch(seed=3):
     from paper_2408_04466_b200 import scenes
@@ -112,6 +110,7 @@ def omega_exact(p, V, g):
 
 
 if __name__ == "__main__":
+    addition_check()
     V = loop_of_patch()
     g, rho, aabs, D = moments(V, K)
     print("loop", V.shape, "rho", rho, "A_abs", aabs)
