@@ -225,13 +225,23 @@ def run_reference(args, spec, rank, world):
 
 
 def boundary_roofline(G, torch, dev, stream, peak_tf, nq=1 << 20, k=3):
-    """K4 (the open-scene kernel) on config 3's scene, 2^20 queries: algorithmic
-    FP64 flops (device segment counter x FLOP_SEGMENT) over its CUDA-event
-    time, best of k -- a side measurement: the bench workload (config 2) is
-    closed and has no net boundary."""
+    """K4's exact fan kernel (`k_boundary_e`, far field off) on config 3's scene,
+    2^20 queries: algorithmic FP64 flops (device segment counter x
+    FLOP_SEGMENT) over its CUDA-event time, best of k -- a side measurement:
+    the bench workload (config 2) is closed and has no net boundary."""
     from paper_2408_04466_b200 import scenes
     s = scenes.make(3, nq)
-    sc = G.Scene(s.ctrl)
+    # the exact fan kernel on its own (the f4 far field would take most of
+    # config 3's pairs; it has its own side measurement, `far_field`)
+    old = os.environ.get("GWN_FARFIELD")
+    os.environ["GWN_FARFIELD"] = "0"
+    try:
+        sc = G.Scene(s.ctrl)
+    finally:
+        if old is None:
+            os.environ.pop("GWN_FARFIELD", None)
+        else:
+            os.environ["GWN_FARFIELD"] = old
     q = torch.from_numpy(s.queries).to(dev)
     G.winding_numbers(sc, q, stream=stream.cuda_stream)
     sc.set_timing(True)
