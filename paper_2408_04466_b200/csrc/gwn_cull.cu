@@ -48,7 +48,10 @@ struct GridView {
 // per-lane walk (cheaper without the shuffles).  Measured (threshold 32 of
 // 8/16/24/32/64): config 5 cull 174 -> 82 us, config 3 159 -> 117 us,
 // config 4 3.3 -> 2.95 ms, config 2 unchanged.
-__global__ void __launch_bounds__(128)
+#ifndef GWN_CULL_BS
+#define GWN_CULL_BS 128
+#endif
+__global__ void __launch_bounds__(GWN_CULL_BS)
 k_cull_grid(GridView grid, Frame f, int32_t m, const int32_t* __restrict__ active,
             const double* __restrict__ pos, double* __restrict__ qproj,
             int2* __restrict__ pairs, unsigned long long* __restrict__ pair_count,
@@ -285,7 +288,7 @@ cudaError_t launch_cull(const gwn_scene* sc, const Round& rd, int32_t m, const i
              rd.gx0, rd.gy0, rd.gia, rd.gib};
   static const bool per_lane = getenv("GWN_CULL_PERLANE") != nullptr;  // A/B switch
   if (g.offs && !per_lane) {
-    k_cull_grid<<<(m + 127) / 128, 128, 0, st>>>(g, rd.f, m, active, pos, qproj, Q.pairs,
+    k_cull_grid<<<(m + GWN_CULL_BS - 1) / GWN_CULL_BS, GWN_CULL_BS, 0, st>>>(g, rd.f, m, active, pos, qproj, Q.pairs,
                                                  pair_count, (unsigned long long)cap, z);
     return cudaGetLastError();
   }
