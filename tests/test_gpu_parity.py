@@ -288,6 +288,23 @@ np.save(sys.argv[3], np.stack([w.cpu().numpy(), st.cpu().numpy().astype(np.float
 """
 
 
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_programmatic_launch_equals_two_streams(tmp_path, cfg):
+    """GWN_PDL=0 runs the fallback on a side stream joined by an event instead of
+    the programmatic dependent launches; the results must be bit-identical."""
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("1", "0"):
+        f = str(tmp_path / f"pdl{mode}.npy")
+        env = dict(os.environ, GWN_PDL=mode)
+        subprocess.run([sys.executable, "-c", _NEWTON_PATH_SCRIPT, repo, str(cfg), f],
+                       env=env, check=True, timeout=300)
+        out[mode] = np.load(f)
+    assert np.array_equal(out["1"], out["0"])
+
+
 @pytest.mark.parametrize("cfg", [1, 3])
 def test_newton_shared_table_equals_register_path(tmp_path, cfg):
     """Scenes of <= 96 patches run K3 Newton from the shared-memory patch
