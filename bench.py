@@ -357,6 +357,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: GWN_BENCH_ONE_GPU=1 runs every rank on cuda:0 over gloo, so
+    # the N > 1 code path (sharding, packed all-gather, max over ranks) can be
+    # exercised on a one-GPU box; never used for reported numbers
+    one_gpu = os.environ.get("GWN_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     from paper_2408_04466_b200 import scenes
     base = args.queries or scenes.FULL_QUERIES[args.config]
     # weak scaling: N x the per-GPU count from the same seeded generator
@@ -372,7 +378,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     n_total = len(spec.queries)
     from paper_2408_04466_b200.distributed import shard_bounds
     s0, s1, per = shard_bounds(n_total, rank, world)
@@ -439,6 +448,17 @@ def main():
     mark = clocks.mark()
     ms_dev, launches = timed(step_device, args.steps)
     clock_info = clocks.stop(mark)
+    if one_gpu and world > 1:  # test hook: the gathered results equal one full eval
+        from paper_2408_04466_b200.distributed import unpad
+        torch.cuda.synchronize()
+        wg, sg = unpad(*gather_packed(pbuf, world, n_total, out=g_all), per, n_total)
+        if rank == 0:
+            w1, s1 = G.winding_numbers(sc, torch.from_numpy(spec.queries).to(dev))
+            ok = torch.equal(wg, w1) and torch.equal(sg, s1)
+            print(f"one-gpu gather check: {'identical' if ok else 'MISMATCH'}", file=sys.stderr,
+                  flush=True)
+            if not ok:
+                raise SystemExit("sharded + gathered results differ from one full eval")
     for _ in range(2):
         step_e2e()
     ms_e2e, _ = timed(step_e2e, args.steps)
