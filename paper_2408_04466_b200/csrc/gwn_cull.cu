@@ -51,7 +51,10 @@ struct GridView {
 #ifndef GWN_CULL_BS
 #define GWN_CULL_BS 128
 #endif
-__global__ void __launch_bounds__(GWN_CULL_BS)
+#ifndef GWN_CULL_MINB
+#define GWN_CULL_MINB 1
+#endif
+__global__ void __launch_bounds__(GWN_CULL_BS, GWN_CULL_MINB)
 k_cull_grid(GridView grid, Frame f, int32_t m, const int32_t* __restrict__ active,
             const double* __restrict__ pos, double* __restrict__ qproj,
             int2* __restrict__ pairs, unsigned long long* __restrict__ pair_count,
