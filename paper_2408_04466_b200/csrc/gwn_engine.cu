@@ -614,11 +614,15 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
           const int32_t nth = (m + 3) / 4;
           static const int k5_bps = [] {  // K5 blocks per SM cap (GWN_K5_BPS; 0 = one group per thread)
             const char* e = getenv("GWN_K5_BPS");
-            return e ? atoi(e) : 4;
+            return e ? atoi(e) : 2;
           }();
-          const int nb4 = k5_bps > 0 ? std::min((nth + 127) / 128, k5_bps * sc->sm_count)
-                                     : (nth + 127) / 128;
-          k_finalize4<<<nb4, 128, 0, st>>>(
+          static const int k5_bs = [] {  // K5 block size (GWN_K5_BS); 512 x 2 per SM keeps
+            const char* e = getenv("GWN_K5_BS");  // the publish counter's atomics few
+            return e ? atoi(e) : 512;
+          }();
+          const int nb4 = k5_bps > 0 ? std::min((nth + k5_bs - 1) / k5_bs, k5_bps * sc->sm_count)
+                                     : (nth + k5_bs - 1) / k5_bs;
+          k_finalize4<<<nb4, k5_bs, 0, st>>>(
               m, chi, fl, bterm, nchunk, sc->prm.max_rounds, sc->prm.max_jitters,
               sc->prm.dir_seed, index_base + c0, qidx ? qidx + c0 : nullptr,
               sc->prm.jitter_scale * sc->diag, q0, pos, jit, jreason, d_w + c0, d_st + c0, nxt,
