@@ -257,6 +257,9 @@ extern "C" int gwn_scene_create(const double* ctrl, int64_t P, const gwn_params*
     return GWN_E_NODEVICE;
   }
   sc->sm_count = prop.multiProcessorCount;
+  // tests: initial candidates-per-query estimate (a tiny value forces the
+  // capacity-overflow re-run of the first rounds)
+  if (const char* e = getenv("GWN_PAIRS_INIT")) sc->pairs_per_query = atof(e);
   {
     // keep stream-ordered workspace cached across evals (default threshold 0
     // would unmap it at every synchronisation)

@@ -244,6 +244,37 @@ def test_odd_batch_sizes_equal_full_batch():
         assert np.array_equal(wp, w[a:b]) and np.array_equal(sp, st[a:b])
 
 
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_candidate_capacity_overflow_rerun_is_identical(cfg, monkeypatch):
+    """A round whose candidate pairs overflow the capacity is discarded and re-run at
+    the exact size (gwn_engine.cu, K5 publish): a scene created with a tiny initial
+    estimate (GWN_PAIRS_INIT) overflows its first round and still returns the default
+    scene's results bit for bit -- evals and ray reuse."""
+    s = scenes.make(cfg, {3: 1 << 14, 5: 4096}[cfg])  # > 4096 candidate pairs
+    sc = G.Scene(s.ctrl)
+    w, st = G.winding_numbers(sc, s.queries)
+    assert int(sc.stats()["candidates"]) > 4096
+    monkeypatch.setenv("GWN_PAIRS_INIT", "0")
+    tiny = G.Scene(s.ctrl)
+    monkeypatch.delenv("GWN_PAIRS_INIT")
+    w1, st1 = G.winding_numbers(tiny, s.queries)
+    first = int(tiny.stats()["kernel_launches"])
+    w2, st2 = G.winding_numbers(tiny, s.queries)
+    second = int(tiny.stats()["kernel_launches"])
+    assert np.array_equal(w1, w) and np.array_equal(st1, st)
+    assert np.array_equal(w2, w) and np.array_equal(st2, st)
+    assert first > second, (first, second)  # the overflowed round ran twice
+    o = np.array([-0.4, 0.3, -0.2])
+    d = np.array([1.0, 0.2, 0.3]) / np.linalg.norm([1.0, 0.2, 0.3])
+    ts = np.linspace(0.0, 2.5, 64)
+    monkeypatch.setenv("GWN_PAIRS_INIT", "0")
+    tiny_r = G.Scene(s.ctrl)
+    monkeypatch.delenv("GWN_PAIRS_INIT")
+    wr = np.asarray(G.winding_numbers_along_ray(tiny_r, G.Ray(o, d), ts))
+    wr0 = np.asarray(G.winding_numbers_along_ray(sc, G.Ray(o, d), ts))
+    assert np.array_equal(wr, wr0)
+
+
 def test_samples_per_edge_parity():
     s = scenes.make(1, 1000)
     for S in (2, 50, 1900):
