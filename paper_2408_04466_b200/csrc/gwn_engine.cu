@@ -189,7 +189,7 @@ __device__ __forceinline__ void finalize4_group(int32_t s0, int32_t m,
                             const double* __restrict__ q0, double* __restrict__ pos,
                             int8_t* __restrict__ jit, int8_t* __restrict__ jreason,
                             double* __restrict__ w_out, int8_t* __restrict__ st_out,
-                            int32_t* __restrict__ next, int32_t* __restrict__ next_n);
+                            int32_t* __restrict__ next, int32_t* __restrict__ next_n, bool ovf);
 
 // K5, round 0 with the identity slot map (the common case): four queries per
 // thread with 16-byte loads of chi / flags / partials and 16- and 4-byte
@@ -205,14 +205,16 @@ __device__ __forceinline__ void finalize4_body(int32_t m, const int32_t* __restr
                             int32_t* __restrict__ next, int32_t* __restrict__ next_n,
                             const unsigned long long* __restrict__ pair_count,
                             unsigned long long pair_cap) {
-  if (*pair_count > pair_cap) return;  // the round is re-run
+  // the round is re-run if the candidate buffer overflowed; the flag is tested
+  // after each group's loads are issued, so its round trip overlaps them
+  const bool ovf = *pair_count > pair_cap;
   // grid-stride over groups of four: a few blocks per SM keep the
   // publish_scalars completion counter (one atomic per block) short
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 4 * g < m;
        g += (int64_t)gridDim.x * blockDim.x)
     finalize4_group((int32_t)(4 * g), m, chi, flags, bpart, nchunk, max_rounds, max_jitters,
                     seed, index_base, qidx, jscale, q0, pos, jit, jreason, w_out, st_out, next,
-                    next_n);
+                    next_n, ovf);
 }
 
 __device__ __forceinline__ void finalize4_group(int32_t s0, int32_t m,
@@ -223,8 +225,10 @@ __device__ __forceinline__ void finalize4_group(int32_t s0, int32_t m,
                             const double* __restrict__ q0, double* __restrict__ pos,
                             int8_t* __restrict__ jit, int8_t* __restrict__ jreason,
                             double* __restrict__ w_out, int8_t* __restrict__ st_out,
-                            int32_t* __restrict__ next, int32_t* __restrict__ next_n) {
+                            int32_t* __restrict__ next, int32_t* __restrict__ next_n,
+                            bool ovf) {
   if (s0 + 4 > m) {  // ragged tail: scalar
+    if (ovf) return;
     for (int32_t s = s0; s < m; ++s) {
       double ang = 0.0;
       for (int c = 0; c < nchunk; ++c) ang = __dadd_rn(ang, bpart[(int64_t)c * m + s]);
@@ -235,8 +239,13 @@ __device__ __forceinline__ void finalize4_group(int32_t s0, int32_t m,
     }
     return;
   }
-  const int4 c4 = *reinterpret_cast<const int4*>(chi + s0);
-  const int4 f4 = *reinterpret_cast<const int4*>(flags + s0);
+  // volatile loads: issued here, before the overflow test below
+  int4 c4, f4;
+  asm volatile("ld.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(c4.x), "=r"(c4.y), "=r"(c4.z), "=r"(c4.w) : "l"(chi + s0));
+  asm volatile("ld.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(f4.x), "=r"(f4.y), "=r"(f4.z), "=r"(f4.w) : "l"(flags + s0));
+  if (ovf) return;
   double ang[4] = {0.0, 0.0, 0.0, 0.0};
   for (int c = 0; c < nchunk; ++c) {
     const double* b = bpart + (int64_t)c * m + s0;
