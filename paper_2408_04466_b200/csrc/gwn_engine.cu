@@ -482,10 +482,15 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   }
   {
     int64_t cm = n < chunk_max ? n : chunk_max;
+    std::vector<int64_t> cst{0};  // chunk starts
     if (pipe) {
       static const int64_t parts = [] {  // GWN_PIPE_CHUNKS overrides (experiments)
         const char* e = getenv("GWN_PIPE_CHUNKS");
-        const long long v = e ? atoll(e) : 4;
+        // measured at config 2 (2^20 queries, pinned host buffers), e2e G q/s:
+        // 2 chunks 1.63, 4 1.70, 6 1.79, 8 1.55, 12 1.27; splitting the last
+        // chunk (GWN_PIPE_TAIL) or issuing every input copy up front
+        // (GWN_PIPE_AHEAD) did not help
+        const long long v = e ? atoll(e) : 6;
         return (int64_t)(v < 1 ? 1 : v);
       }();
       const int64_t pc =
@@ -495,7 +500,20 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         CKE(cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking));
         CKE(cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking));
       }
-      const int64_t nch = (n + cm - 1) / cm;
+      // chunk boundaries: equal chunks, the last one split GWN_PIPE_TAIL times
+      // in halves -- after the final input copy only the last (small) chunk's
+      // rounds and output copy remain
+      static const int tail = [] {
+        const char* e = getenv("GWN_PIPE_TAIL");
+        return e ? atoi(e) : 0;
+      }();
+      for (int64_t a = cm; a < n; a += cm) cst.push_back(a);
+      for (int t = 0; t < tail; ++t) {
+        const int64_t a = cst.back(), half = ((n - a) / 2 + 1023) & ~1023ll;
+        if (half < (1ll << 15) || a + half >= n) break;
+        cst.push_back(a + half);
+      }
+      const int64_t nch = (int64_t)cst.size();
       pev.assign((size_t)(2 * nch), nullptr);
       for (auto& e : pev) CKE(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
@@ -524,20 +542,30 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     int64_t pair_cap = 0;
     void* k3_scratch = nullptr;  // K3 queues (fallback + Newton items)
     CKE(ws.err);
-    for (int64_t c0 = 0; c0 < n; c0 += cm) {
-      const int32_t mc = (int32_t)((n - c0) < cm ? (n - c0) : cm);
+    if (!pipe)
+      for (int64_t a = cm; a < n; a += cm) cst.push_back(a);
+    cst.push_back(n);
+    for (int64_t ci = 0; ci + 1 < (int64_t)cst.size(); ++ci) {
+      const int64_t c0 = cst[ci];
+      const int32_t mc = (int32_t)(cst[ci + 1] - c0);
       const double* q0 = d_q + 3 * c0;
-      const int64_t ci = c0 / cm;
       if (pipe) {
         auto h2d = [&](int64_t k) -> cudaError_t {
-          const int64_t a = k * cm, b = std::min(n, a + cm);
+          const int64_t a = cst[k], b = cst[k + 1];
           cudaError_t e = cudaMemcpyAsync((double*)d_q + 3 * a, queries + 3 * a,
                                           sizeof(double) * 3 * (b - a), cudaMemcpyHostToDevice,
                                           cs_in);
           return e != cudaSuccess ? e : cudaEventRecord(pev[2 * k], cs_in);
         };
-        if (ci == 0) CKE(h2d(0));
-        if (c0 + cm < n) CKE(h2d(ci + 1));
+        // input copies issued GWN_PIPE_AHEAD chunks ahead of the rounds
+        static const int64_t ahead = [] {
+          const char* e = getenv("GWN_PIPE_AHEAD");
+          const long long v = e ? atoll(e) : 1;
+          return (int64_t)(v < 1 ? 1 : v);
+        }();
+        const int64_t nchk = (int64_t)cst.size() - 1;
+        for (int64_t k = ci == 0 ? 0 : ci + ahead; k <= ci + ahead && k < nchk; ++k)
+          CKE(h2d(k));
         CKE(cudaStreamWaitEvent(st, pev[2 * ci], 0));
       }
       // round 0 reads the queries in place; k_finalize fills pos / jit for

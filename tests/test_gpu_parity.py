@@ -64,6 +64,18 @@ def test_device_tensors_and_chunking_are_identical():
     assert np.array_equal(w3, w2) and np.array_equal(st3, st2)
 
 
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_pipelined_host_path_equals_device_path(cfg):
+    """Host buffers of >= 2^18 queries take the pipelined path (chunked input copies,
+    rounds and output copies on three streams, tail chunk split): bit-identical to
+    one device-resident eval, at an odd size."""
+    s = scenes.make(cfg, (1 << 18) + 777)
+    sc = G.Scene(s.ctrl)
+    w, st = G.winding_numbers(sc, torch.from_numpy(s.queries).cuda())
+    wh, sh = G.winding_numbers(sc, s.queries)
+    assert np.array_equal(w.cpu().numpy(), wh) and np.array_equal(st.cpu().numpy(), sh)
+
+
 def test_sharded_slices_equal_unsharded():
     s, sc = _scene(2)
     w, st = G.winding_numbers(sc, s.queries)
