@@ -463,6 +463,26 @@ def main():
         step_e2e()
     ms_e2e, _ = timed(step_e2e, args.steps)
 
+    # the e2e step's PCIe floor: the same bytes copied alone (inputs H2D and
+    # (w, status) D2H on two streams at once), no compute
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    q_cp = torch.empty_like(q_dev)
+
+    def step_copies():
+        s_in.wait_stream(stream)
+        s_out.wait_stream(stream)
+        with torch.cuda.stream(s_in):
+            q_cp.copy_(q_pin, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            w_pin.copy_(w_dev, non_blocking=True)
+            st_pin.copy_(st_dev, non_blocking=True)
+        stream.wait_stream(s_in)
+        stream.wait_stream(s_out)
+
+    for _ in range(2):
+        step_copies()
+    ms_cp, _ = timed(step_copies, args.steps)
+
     # ---- roofline of the dominant FP64 kernel, measured live: the library
     # records CUDA events around each kernel on `stream` (set_timing)
     sc.set_timing(True)
@@ -507,6 +527,12 @@ def main():
             "candidate_pairs_per_s": stt["candidates"] / (ms_dev * 1e-3 / args.steps) * world,
             "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": int(nq * 24),
                     "d2h_bytes_per_step": int(nq * 9)},
+            "e2e_copy_floor": {
+                "value": n_total / (ms_cp * 1e-3 / args.steps), "unit": "queries/s",
+                "ms_per_step": ms_cp / args.steps, "frac": ms_cp / ms_e2e,
+                "note": "the e2e step's input and output copies alone (pinned host memory, "
+                        "H2D and D2H concurrently on two streams); frac = floor time / "
+                        "e2e time"},
             "gpu_launches": launches,
             "roofline": {"bound": "fp64", "kernel": kname, "achieved": achieved,
                          "peak": peak_tf, "unit": "TFLOP/s",
