@@ -4,8 +4,14 @@
 
 One step = one pass of the hot path (cull -> intersect -> boundary ->
 reduce/re-shoot, plus the all-gather for N>1) over the rank's shard of the
-config's synthetic queries.  Default workload: config 2 (BASELINE.json
-configs[1]): closed 6-patch bicubic surface, 2^20 queries, fp64.
+config's synthetic queries.  Default workload: config 5 (BASELINE.json
+configs[4], the north-star job): 15,876 bicubic patches (256 deformed closed
+surfaces, 5% holes, 2% flipped duplicates), 2^26 queries, fp64 -- the largest
+configuration, and it fits one B200.  Its queries are split over the N GPUs
+(strong scaling: the job is fixed).
+
+``--gpus N`` without torchrun re-launches this script under
+``torch.distributed.run`` with N ranks (one per GPU, NCCL, NCCL_DEBUG=INFO).
 
 Printed JSON (rank 0, one line):
   value      queries/s over all ranks, queries resident in HBM, device-timed
@@ -13,12 +19,16 @@ Printed JSON (rank 0, one line):
   e2e        the same metric through the public API from pinned host memory
              (H2D of the step's queries and D2H of w + status inside the timed
              region)
-  roofline   K3 (the dominant kernel at config 2) algorithmic FP64 flops per
-             launch (device counters x per-stage flop constants, DESIGN.md
-             §Measurement) / its event-timed duration, vs the FP64 DFMA peak
-             measured live on this GPU
-  cpu_baseline  the CPU oracle port (oracle/, all host threads) on a bounded
-             sample of the same workload, rank 0 at N=1
+  roofline   the dominant kernel of the step (the exact near-field boundary
+             kernel at config 5): algorithmic FP64 flops per launch (device
+             counters x per-unit flops) / its CUDA-event time, vs
+             the FP64 DFMA peak measured live on this GPU; `rooflines` has every
+             FP64 kernel of the step
+  parity     the oracle (oracle/, CPU) on the first 8,192 queries, compared
+             with the GPU's results in the same run
+  cpu_baseline  that oracle run's rate (the reference algorithm restated in C,
+             all host threads), rank 0 at N=1; `as_shipped_reference` times
+             the reference package itself (baseline/_ref) per BASELINE.md §2
 """
 
 from __future__ import annotations
@@ -26,6 +36,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -36,80 +47,76 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
-# Algorithmic FP64 flops per unit of work (FMA = 2).  K3: SURVEY.md §8(d)'s
-# per-unit figures for the reference algorithm's work units (a Newton
-# iteration evaluates the map and its partials in the Bernstein basis and
-# solves the 2x2 system; an accepted root adds C, the normal and the record
-# tests).  The kernel's Horner form of the same iteration executes fewer
-# (142), so achieved counts work done, not instructions issued.
+# Algorithmic FP64 flops per unit of work (FMA = 2), DESIGN.md §4.
 FLOP_NEWTON = 220.0    # K3 Newton iteration (220 per N_newton)
 FLOP_ROOT = 200.0      # K3 accepted root (200 per N_root)
-FLOP_SEGMENT = 34.0    # K4 per (query, net segment) in the ray frame: vertex (3 sub, |r|^2 5,
-                       # rsqrt seed + Halley 8, u 4) + num 3, den 5, complex product 6
+FLOP_SEGMENT = 34.0    # K4 exact, per (query, net segment) in the ray frame: vertex (3 sub,
+                       # |r|^2 5, rsqrt seed + Halley 8, u 4) + num 3, den 5, complex product 6
+FLOP_TERM = 12.0       # K4 far field, per solid-harmonic term: complex recurrence 8 +
+                       # complex multiply-add 4
 
 CONFIG_DESC = {
     1: "config1: single open bicubic patch, 4096 queries U[-0.5,1.5]^3",
     2: "config2: closed 6-patch bicubic cube-sphere, 2^20 queries U[-1.5,1.5]^3",
     3: "config3: open 8x8 height-field sheet (64 patches), 2^22 queries (10% within 1e-3)",
     4: "config4: 16 overlapping closed surfaces (1024 patches), 2^24 queries U[-3,3]^3",
-    5: "config5: 15876 patches (256 surfaces, 5% holes, 2% flipped duplicates), 2^26 queries",
+    5: "config5: 15876 bicubic patches (256 deformed closed surfaces, 5% holes, 2% flipped "
+       "duplicates), 2^26 queries uniform in the scene box",
 }
-
-
-def _traffic(kname: str, config: int, n: int):
-    """DRAM bytes per launch of the roofline kernel from the committed ncu
-    --set full capture (profiles/roofline_traffic.json, config 2 at 2^20
-    queries), or None for another workload."""
-    if config != 2 or n != (1 << 20):
-        return None
-    try:
-        with open(os.path.join(HERE, "profiles", "roofline_traffic.json")) as f:
-            t = json.load(f)
-    except (OSError, ValueError):
-        return None
-    return t.get(kname.split(" ")[0])
-
-
-def _cull_roofline(stt, nq):
-    """K2 `k_cull_grid` against HBM: algorithmic DRAM bytes = per query the
-    position read (24 B), its ray-frame projection and chi / flag
-    accumulators written (24 + 8 B), the cell range read (8 B); per candidate
-    the (slot, leaf) pair written (8 B).  Cell entries are L2-resident."""
-    try:
-        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
-            peak, src = json.load(f)["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
-    except (OSError, ValueError, KeyError):
-        peak, src = 7700.0, "B200_PROFILING.md fallback"
-    ms = stt["ms_cull"]
-    algo = 64.0 * nq + 8.0 * stt["candidates"]
-    ach = algo / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
-    return {"bound": "hbm", "kernel": "k_cull_grid (K2)", "achieved": ach, "peak": peak,
-            "unit": "GB/s", "frac": ach / peak if peak else None,
-            "traffic": _traffic("k_cull_grid", 2, nq), "algorithmic_bytes": algo,
-            "kernel_ms": ms, "peak_source": src,
-            "note": "latency-bound (ncu: long-scoreboard stalls on the dependent "
-                    "position -> cell -> entry loads), not bandwidth-bound"}
+PARITY_Q = 8192        # oracle parity sample (first queries of the config)
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--queries", type=int, default=0,
-                    help="override the per-GPU query count (weak scaling) / total (strong)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: every GPU evaluates the config's query count (total grows "
-                         "with N); strong: the config's queries are split over the GPUs")
+                    help="override the job's query count (strong) / per-GPU count (weak)")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="strong (default for config 5): the config's queries are split over "
+                         "the GPUs; weak: every GPU evaluates the config's query count")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-far-field", action="store_true",
-                    help="skip the SURVEY §8(f4) far-field side measurement (config 5)")
-    ap.add_argument("--no-ray-reuse", action="store_true",
-                    help="skip the SURVEY §8(f1) ray-reuse side measurement")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    return ap.parse_args()
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the side measurements (other configs, far field, ray reuse, "
+                         "as-shipped reference)")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    a = ap.parse_args()
+    if a.scaling is None:
+        a.scaling = "strong" if a.config == 5 else "weak"
+    return a
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_spawn(args) -> int:
+    """--gpus N > 1 outside torchrun: re-launch this script with N ranks (the
+    exact code path the driver's torchrun launch runs)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
 class ClockSampler:
@@ -128,7 +135,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -145,7 +152,7 @@ class ClockSampler:
     def stop(self, since: int = 0) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.12)
+        time.sleep(0.15)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
@@ -166,38 +173,63 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-def cpu_baseline(spec, seconds: float) -> dict:
-    """Time the CPU oracle port (all host threads) on a bounded sample."""
+def _traffic(key: str):
+    """DRAM bytes per launch of a kernel from the committed ncu --set full
+    captures (profiles/roofline_traffic.json; same config and chunk size as
+    the bench's launches), or None."""
+    try:
+        with open(os.path.join(HERE, "profiles", "roofline_traffic.json")) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None
+    v = t.get(key)
+    return v if isinstance(v, (int, float)) else None
+
+
+def oracle_parity(spec, w_gpu, st_gpu, n: int, cores: int) -> tuple[dict, dict]:
+    """The CPU oracle (the reference algorithm restated in C, oracle/) on the
+    first n queries with all host threads: parity against the GPU's results
+    of the same run, and the cpu_baseline rate."""
     from oracle import oracle as O
-    cores = os.cpu_count() or 1
-    n = 1024
-    q = spec.queries
-    O.scene_eval(spec.ctrl, q[:64])                     # warm caches / thread pool
-    while True:
-        t = time.perf_counter()
-        O.scene_eval(spec.ctrl, q[:n], qidx=np.arange(n), nthreads=cores)
-        dt = time.perf_counter() - t
-        if dt >= seconds / 4 or n >= len(q):
-            break
-        n = min(len(q), n * 4)
-    return {"value": n / dt, "unit": "queries/s", "cores": cores, "kind": "port",
+    q = spec.queries[:n]
+    O.scene_eval(spec.ctrl, q[:16], qidx=np.arange(16), nthreads=cores)  # warm
+    t = time.perf_counter()
+    wo, so, _, _ = O.scene_eval(spec.ctrl, q, qidx=np.arange(n), nthreads=cores)
+    dt = time.perf_counter() - t
+    wg, sg = w_gpu[:n], st_gpu[:n]
+    both = (sg == 0) & (so == 0)
+    d = np.abs(wg - wo)[both]
+    cls_g, cls_o = np.round(wg[both]), np.round(wo[both])
+    far = np.abs(wo[both] - np.round(wo[both])) > 1e-6
+    par = {"queries": n, "both_status_ok": int(both.sum()),
+           "status_equal": int((sg == so).sum()),
+           "max_abs_dw": float(d.max()) if d.size else 0.0,
+           "rms_dw": float(np.sqrt(np.mean(d * d))) if d.size else 0.0,
+           "rounded_w_equal": int((cls_g == cls_o).sum()),
+           "non_integer_w": int(far.sum()),
+           "tolerance": "north star: |dw| <= 1e-6; integer classification exact",
+           "pass": bool(d.size and d.max() <= 1e-6 and both.mean() > 0.99)}
+    base = {"value": n / dt, "unit": "queries/s", "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"first {n} queries of {CONFIG_DESC[spec.config].split(':')[0]} "
-                      f"({dt:.1f} s, oracle/gwn_oracle.c, {cores} threads)"}
+                      f"({dt:.1f} s; oracle/gwn_oracle.c, the reference algorithm restated in C "
+                      f"with subdivided seeding, exact boundary sum, {cores} threads)"}
+    return par, base
 
 
 def run_reference(args, spec, rank, world):
-    """--impl reference: the CPU oracle port on the host cores (rank 0 only)."""
+    """--impl reference: the CPU oracle port on the host cores (rank 0 only),
+    each step a bounded sample of the workload."""
     if rank != 0:
         return 0
     from oracle import oracle as O
     cores = os.cpu_count() or 1
-    # bounded per-step sample: ~2 s of CPU work per step
-    n = 2048
-    while True:
+    n = 256
+    while True:  # bounded per-step sample: >= ~4 s of CPU work per step
         t = time.perf_counter()
         O.scene_eval(spec.ctrl, spec.queries[:n], qidx=np.arange(n), nthreads=cores)
         dt = time.perf_counter() - t
-        if dt > 1.0 or n >= len(spec.queries):
+        if dt > 4.0 or n >= len(spec.queries):
             break
         n = min(len(spec.queries), n * 2)
     for _ in range(args.warmup):
@@ -216,7 +248,10 @@ def run_reference(args, spec, rank, world):
         "config": {"workload": CONFIG_DESC[spec.config], "n_patches": spec.n_patches,
                    "queries": int(len(spec.queries)), "sample_per_step": n},
         "cpu_baseline": {"value": v, "unit": "queries/s", "cores": cores, "kind": "port",
-                         "sample": f"first {n} queries per step, oracle/gwn_oracle.c"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"first {n} queries per step, oracle/gwn_oracle.c (the "
+                                   "reference algorithm restated in C; the reference itself is "
+                                   "Python with no bicubic type or engine, DESIGN.md §8)"},
         "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -224,49 +259,37 @@ def run_reference(args, spec, rank, world):
     return 0
 
 
-def boundary_roofline(G, torch, dev, stream, peak_tf, nq=1 << 20, k=3):
-    """K4's exact fan kernel (`k_boundary_e`, far field off) on config 3's scene,
-    2^20 queries: algorithmic FP64 flops (device segment counter x
-    FLOP_SEGMENT) over its CUDA-event time, best of k -- a side measurement:
-    the bench workload (config 2) is closed and has no net boundary."""
+def side_config(G, torch, cfg: int, dev, stream, k: int = 5) -> dict:
+    """Another BASELINE config on one GPU, device-resident, L2 flushed: the
+    config's full query count, best-effort per-stage split (extra key)."""
     from paper_2408_04466_b200 import scenes
-    s = scenes.make(3, nq)
-    # the exact fan kernel on its own (the f4 far field would take most of
-    # config 3's pairs; it has its own side measurement, `far_field`)
-    old = os.environ.get("GWN_FARFIELD")
-    os.environ["GWN_FARFIELD"] = "0"
-    try:
-        sc = G.Scene(s.ctrl)
-    finally:
-        if old is None:
-            os.environ.pop("GWN_FARFIELD", None)
-        else:
-            os.environ["GWN_FARFIELD"] = old
+    s = scenes.make(cfg)
+    sc = G.Scene(s.ctrl, device=dev.index)
     q = torch.from_numpy(s.queries).to(dev)
-    G.winding_numbers(sc, q, stream=stream.cuda_stream)
-    sc.set_timing(True)
-    best, segs = float("inf"), 0
+    w = torch.empty(len(q), dtype=torch.float64, device=dev)
+    st = torch.empty(len(q), dtype=torch.int8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        G.winding_numbers(sc, q, out=(w, st), stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    ms = 0.0
     for _ in range(k):
-        G.winding_numbers(sc, q, stream=stream.cuda_stream)
-        st = sc.stats()
-        if st["ms_boundary"] < best:
-            best, segs = st["ms_boundary"], st["boundary_segments"]
-    sc.set_timing(False)
-    ach = segs * FLOP_SEGMENT / (best * 1e-3) / 1e12
-    return {"workload": f"config3 scene (64 patches, {sc.n_net_segments} net segments), "
-                        f"{nq} queries", "kernel": "k_boundary_e (K4 fan term)",
-            "bound": "fp64", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
-            "frac": ach / peak_tf if peak_tf else None, "kernel_ms": best,
-            "traffic": _traffic("k_boundary_e_config3_2^20", 2, 1 << 20) if nq == 1 << 20
-            else None,
-            "segment_pairs": segs}
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        G.winding_numbers(sc, q, out=(w, st), stream=stream.cuda_stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms += a.elapsed_time(b)
+    return {"workload": CONFIG_DESC[cfg], "queries": len(q), "n_patches": s.n_patches,
+            "value": len(q) / (ms / k * 1e-3), "unit": "queries/s", "ms_per_step": ms / k,
+            "steps": k, "warmup": 3}
 
 
-def far_field(G, torch, dev, stream, nq=1 << 18, k=2):
-    """SURVEY §8(f) f4 side measurement: config 5's boundary term (the 64M x 16K
-    north-star scene, 2^18 queries here) with the far-field expansion against
-    the exact fan sum -- both device-timed K4 stages, best of k, and the
-    largest |dw| between the two."""
+def far_field_side(G, torch, dev, stream, nq=1 << 18, k=2) -> dict:
+    """config 5's boundary term with the far field against
+    the exact fan sum (GWN_FARFIELD=0), both device-timed, and the largest
+    |dw| between the two."""
     from paper_2408_04466_b200 import scenes
     s = scenes.make(5, nq)
     q = torch.from_numpy(s.queries).to(dev)
@@ -276,38 +299,41 @@ def far_field(G, torch, dev, stream, nq=1 << 18, k=2):
         if mode == "exact":
             os.environ["GWN_FARFIELD"] = "0"
         try:
-            sc = G.Scene(s.ctrl)          # the switch is read at scene creation
+            sc = G.Scene(s.ctrl, device=dev.index)   # the switch is read at scene creation
         finally:
             if mode == "exact":
                 if old is None:
                     os.environ.pop("GWN_FARFIELD", None)
                 else:
                     os.environ["GWN_FARFIELD"] = old
-        w, st = G.winding_numbers(sc, q, stream=stream.cuda_stream)
+        G.winding_numbers(sc, q, stream=stream.cuda_stream)
         sc.set_timing(True)
-        best, stt = float("inf"), None
+        best, stt, w, st = float("inf"), None, None, None
         for _ in range(k):
             w, st = G.winding_numbers(sc, q, stream=stream.cuda_stream)
             t = sc.stats()
             if t["ms_boundary"] < best:
                 best, stt = t["ms_boundary"], t
         sc.set_timing(False)
-        res[mode] = (best, w.cpu().numpy(), st.cpu().numpy(), stt, sc.n_far_cycles)
+        res[mode] = (best, w.cpu().numpy(), st.cpu().numpy(), stt)
     ok = (res["exact"][2] == 0) & (res["far"][2] == 0)
-    return {"workload": f"config5 scene ({s.n_patches} patches), {nq} queries, boundary term (K4)",
+    return {"workload": f"config5 scene, {nq} queries, boundary term (K4)",
             "ms_exact": res["exact"][0], "ms_far_field": res["far"][0],
             "speedup": res["exact"][0] / res["far"][0],
-            "far_cycles": res["far"][4], "far_pairs": res["far"][3]["far_pairs"],
+            "far_pairs": res["far"][3]["far_pairs"], "near_pairs": res["far"][3]["near_pairs"],
             "exact_segment_pairs": res["far"][3]["boundary_segments"],
             "exact_segment_pairs_without": res["exact"][3]["boundary_segments"],
             "max_abs_dw": float(np.abs(res["exact"][1] - res["far"][1])[ok].max()),
             "status_equal": bool(np.array_equal(res["exact"][2], res["far"][2]))}
 
 
-def ray_reuse(G, torch, sc, dev, stream, n=256, k=5):
-    """voxel centres of the scene AABB at n^3 through
+def ray_reuse_side(G, torch, cfg, dev, stream, n=256, k=3) -> dict:
+    """voxel centres of a config's scene box at n^3 through
     gwn_eval_rays (n^2 rays along +x) against gwn_eval of the same points,
     both device-resident, CUDA events on `stream`."""
+    from paper_2408_04466_b200 import scenes
+    s = scenes.make(cfg, 8)
+    sc = G.Scene(s.ctrl, device=dev.index)
     bb = sc.aabb()
     lo, hi = bb.min_corner, bb.max_corner
     c = (torch.arange(n, dtype=torch.float64, device=dev) + 0.5) / n
@@ -322,8 +348,6 @@ def ray_reuse(G, torch, sc, dev, stream, n=256, k=5):
     st_pp = torch.empty(n ** 3, dtype=torch.int8, device=dev)
 
     def t_of(fn):
-        # best of k single calls (CUDA events on `stream`), after two warm-ups
-        fn()
         fn()
         torch.cuda.synchronize()
         best = float("inf")
@@ -334,8 +358,6 @@ def ray_reuse(G, torch, sc, dev, stream, n=256, k=5):
             b.record(stream)
             torch.cuda.synchronize()
             best = min(best, a.elapsed_time(b))
-            if os.environ.get("GWN_RR_DEBUG"):
-                print("ray_reuse call ms", a.elapsed_time(b), file=sys.stderr, flush=True)
         return best
 
     res = {}
@@ -345,11 +367,47 @@ def ray_reuse(G, torch, sc, dev, stream, n=256, k=5):
     w_r, st_r = res["r"]
     ok = (st_r == 0) & (st_pp == 0)
     diff = float((w_r - w_pp).abs()[ok].max()) if bool(ok.any()) else 0.0
-    return {"workload": f"voxelize scene AABB at {n}^3 = {n ** 3} voxel centres, {n * n} rays "
-                        "along +x (SPEC.md:398-407)",
+    return {"workload": f"config{cfg} scene box voxelized at {n}^3 = {n ** 3} voxel centres, "
+                        f"{n * n} rays along +x (SPEC.md:398-407)",
             "value": n ** 3 / (ms_r * 1e-3), "unit": "points/s", "ms": ms_r,
             "rays_cast": sc.rays_cast, "per_point_value": n ** 3 / (ms_p * 1e-3),
             "per_point_ms": ms_p, "speedup": ms_p / ms_r, "max_abs_diff_vs_per_point": diff}
+
+
+def rooflines(stt: dict, peak_tf: float, ms_step: float, config: int) -> dict:
+    """Every FP64 kernel of the step: algorithmic flops (device counters x
+    per-unit flops) / its event-timed duration, against the live DFMA peak."""
+    ks = {
+        "k_ff_near (K4 exact near field)": (
+            stt.get("ms_k4_exact", 0.0), stt["boundary_segments"] * FLOP_SEGMENT,
+            f"{int(stt['boundary_segments'])} (query, segment) pairs x {FLOP_SEGMENT:.0f} flop",
+            "k_ff_near"),
+        "k_ff_fill (K4 far field)": (
+            stt.get("ms_k4_far", 0.0), stt.get("far_terms", 0) * FLOP_TERM,
+            f"{int(stt.get('far_terms', 0))} solid-harmonic terms x {FLOP_TERM:.0f} flop "
+            f"({int(stt['far_pairs'])} far (query, cycle) pairs)", "k_ff_fill"),
+        "k3_newton (K3 Newton + record)": (
+            stt["ms_k3_newton"], stt["newton_iters"] * FLOP_NEWTON + stt["roots"] * FLOP_ROOT,
+            f"{int(stt['newton_iters'])} iterations x {FLOP_NEWTON:.0f} + {int(stt['roots'])} "
+            f"roots x {FLOP_ROOT:.0f} flop", "k3_newton"),
+    }
+    if stt.get("ms_k4_exact", 0.0) <= 0.0 and stt["ms_boundary"] > 0:
+        ks["k_boundary_e (K4 exact)"] = (stt["ms_boundary"],
+                                         stt["boundary_segments"] * FLOP_SEGMENT,
+                                         "all (query, segment) pairs", "k_boundary_e")
+    out = {}
+    for name, (ms, flops, units, key) in ks.items():
+        if ms <= 0.0 or flops <= 0.0:
+            continue
+        ach = flops / (ms * 1e-3) / 1e12
+        out[name] = {"bound": "fp64", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": ach / peak_tf if peak_tf else None,
+                     "traffic": _traffic(f"c{config}:{key}"),
+                     "kernel_ms_per_step": ms, "kernel_share_of_step": ms / ms_step,
+                     "algorithmic_units": units,
+                     "peak_source": "FP64 DFMA-chain microbenchmark run live on this GPU "
+                                    "(MEASURED_PEAKS.json has no FP64 entry)"}
+    return out
 
 
 def main():
@@ -357,15 +415,18 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_spawn(args)
     # test hook: GWN_BENCH_ONE_GPU=1 runs every rank on cuda:0 over gloo, so
     # the N > 1 code path (sharding, packed all-gather, max over ranks) can be
     # exercised on a one-GPU box; never used for reported numbers
     one_gpu = os.environ.get("GWN_BENCH_ONE_GPU") == "1"
+    if world != args.gpus:
+        raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
     if one_gpu:
         local = 0
     from paper_2408_04466_b200 import scenes
     base = args.queries or scenes.FULL_QUERIES[args.config]
-    # weak scaling: N x the per-GPU count from the same seeded generator
     total = base * world if args.scaling == "weak" else base
     spec = scenes.make(args.config, total)
     if args.impl == "reference":
@@ -383,12 +444,16 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=dev)
     n_total = len(spec.queries)
-    from paper_2408_04466_b200.distributed import shard_bounds
+    from paper_2408_04466_b200.distributed import gather_packed, packed_shard, shard_bounds
     s0, s1, per = shard_bounds(n_total, rank, world)
     local_q = np.ascontiguousarray(spec.queries[s0:s1])
     nq = len(local_q)
-    sc = G.Scene(spec.ctrl, device=local)
     stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    sc = G.Scene(spec.ctrl, device=local)
+    torch.cuda.synchronize()
+    scene_build_s = time.perf_counter() - t
     q_dev = torch.from_numpy(local_q).to(dev)
     w_dev = torch.empty(nq, dtype=torch.float64, device=dev)
     st_dev = torch.empty(nq, dtype=torch.int8, device=dev)
@@ -398,7 +463,6 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     # N > 1: the engine writes into this rank's packed (w, status) block and
     # ONE all-gather assembles every rank's results (distributed.py)
-    from paper_2408_04466_b200.distributed import gather_packed, packed_shard
     pbuf, w_pk, st_pk = packed_shard(per, dev)
     g_all = torch.empty(world * pbuf.numel(), dtype=torch.uint8, device=dev)
     if world > 1:
@@ -440,9 +504,18 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()), launches
 
+    # first evaluation: builds the re-shoot rounds' structures (cached on the
+    # scene) -- reported, not timed as a step
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    step_device()
+    torch.cuda.synchronize()
+    first_eval_s = time.perf_counter() - t
+    st0 = sc.stats()
     clocks = ClockSampler(local)
     clocks.start()
-    for _ in range(max(3, args.warmup)):
+    warm = max(3, args.warmup)
+    for _ in range(warm - 1):
         step_device()
     torch.cuda.synchronize()
     mark = clocks.mark()
@@ -453,15 +526,17 @@ def main():
         torch.cuda.synchronize()
         wg, sg = unpad(*gather_packed(pbuf, world, n_total, out=g_all), per, n_total)
         if rank == 0:
-            w1, s1 = G.winding_numbers(sc, torch.from_numpy(spec.queries).to(dev))
-            ok = torch.equal(wg, w1) and torch.equal(sg, s1)
+            w1, s1_ = G.winding_numbers(sc, torch.from_numpy(spec.queries).to(dev))
+            ok = torch.equal(wg, w1) and torch.equal(sg, s1_)
             print(f"one-gpu gather check: {'identical' if ok else 'MISMATCH'}", file=sys.stderr,
                   flush=True)
             if not ok:
                 raise SystemExit("sharded + gathered results differ from one full eval")
-    for _ in range(2):
-        step_e2e()
+    w_host = w_dev[:min(nq, PARITY_Q)].cpu().numpy()
+    st_host = st_dev[:min(nq, PARITY_Q)].cpu().numpy()
+    step_e2e()
     ms_e2e, _ = timed(step_e2e, args.steps)
+    e2e_equal = bool(torch.equal(w_pin[:1024], w_dev[:1024].cpu()))
 
     # the e2e step's PCIe floor: the same bytes copied alone (inputs H2D and
     # (w, status) D2H on two streams at once), no compute
@@ -479,54 +554,44 @@ def main():
         stream.wait_stream(s_in)
         stream.wait_stream(s_out)
 
-    for _ in range(2):
-        step_copies()
+    step_copies()
     ms_cp, _ = timed(step_copies, args.steps)
 
-    # ---- roofline of the dominant FP64 kernel, measured live: the library
+    # ---- per-kernel times and device counters of one step: the library
     # records CUDA events around each kernel on `stream` (set_timing)
     sc.set_timing(True)
-    kk = 3
-    agg = {}
-    for _ in range(kk):
-        flush.zero_()
-        G.winding_numbers(sc, q_dev, index_base=s0, out=(w_dev, st_dev),
-                          stream=stream.cuda_stream)
-        for k, v in sc.stats().items():
-            agg[k] = agg.get(k, 0) + v
+    flush.zero_()
+    G.winding_numbers(sc, q_dev, index_base=s0, out=(w_dev, st_dev), stream=stream.cuda_stream)
+    stt = sc.stats()
     sc.set_timing(False)
-    stt = {k: v / kk for k, v in agg.items()}
     peak_tf, _ = G.fp64_peak(local)
-    kernels = {
-        "k3_newton (K3 Newton + record)": (stt["ms_k3_newton"],
-                                           stt["newton_iters"] * FLOP_NEWTON
-                                           + stt["roots"] * FLOP_ROOT),
-        "k_boundary (K4 fan term)": (stt["ms_boundary"], stt["boundary_segments"] * FLOP_SEGMENT),
-    }
-    kname, (kms, kflops) = max(kernels.items(), key=lambda kv: kv[1][0])
-    achieved = kflops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
+    ms_step = ms_dev / args.steps
+    rl = rooflines(stt, peak_tf, ms_step, args.config)
+    head_name = max(rl, key=lambda k: rl[k]["kernel_ms_per_step"]) if rl else None
 
-    value = n_total / (ms_dev * 1e-3 / args.steps)
+    value = n_total / (ms_step * 1e-3)
     e2e = n_total / (ms_e2e * 1e-3 / args.steps)
     out = None
     if rank == 0:
+        head = dict(rl[head_name], kernel=head_name) if head_name else None
         out = {
             "metric": "winding-number queries/sec", "value": value, "unit": "queries/s",
-            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
-            "ms_per_step": ms_dev / args.steps, "higher_is_better": True,
+            "n_gpus": world, "steps": args.steps, "warmup": warm,
+            "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, SURVEY.md §8(d); no public dataset)",
             "config": {"workload": CONFIG_DESC[args.config], "n_patches": spec.n_patches,
                        "queries": n_total, "queries_per_gpu": per,
                        "net_boundary_segments": sc.n_net_segments,
+                       "boundary_entries": sc.n_far_cycles,
                        "parallelism": f"dp{world} (queries sharded, scene replicated, "
                                       "one all-gather)",
                        "l2": "flushed between steps (256 MiB write)"},
             "nominal_pairs_per_s": value * spec.n_patches,
-            "candidate_pairs_per_s": stt["candidates"] / (ms_dev * 1e-3 / args.steps) * world,
+            "candidate_pairs_per_s": stt["candidates"] / (ms_step * 1e-3) * world,
             "e2e": {"value": e2e, "unit": "queries/s", "h2d_bytes_per_step": int(nq * 24),
-                    "d2h_bytes_per_step": int(nq * 9)},
+                    "d2h_bytes_per_step": int(nq * 9), "results_equal_device_path": e2e_equal},
             "e2e_copy_floor": {
                 "value": n_total / (ms_cp * 1e-3 / args.steps), "unit": "queries/s",
                 "ms_per_step": ms_cp / args.steps, "frac": ms_cp / ms_e2e,
@@ -534,33 +599,43 @@ def main():
                         "H2D and D2H concurrently on two streams); frac = floor time / "
                         "e2e time"},
             "gpu_launches": launches,
-            "roofline": {"bound": "fp64", "kernel": kname, "achieved": achieved,
-                         "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved / peak_tf if peak_tf else None,
-                         "traffic": _traffic(kname, args.config, nq),
-                         "peak_source": "FP64 DFMA-chain microbenchmark run live on this GPU "
-                                        "(MEASURED_PEAKS.json has no FP64 entry)",
-                         "kernel_ms": kms, "kernel_share_of_step":
-                             kms / (ms_dev / args.steps) if ms_dev else None},
-            # the longest kernel of the step is the K2 cull: memory-latency bound,
-            # reported against the measured HBM copy bandwidth
-            "roofline_cull": _cull_roofline(stt, nq),
+            "roofline": head,
+            "rooflines": rl,
+            "scene_build_s": scene_build_s,
+            "first_eval_s": first_eval_s,
+            "rounds_built": int(st0["rounds_built"]),
+            "first_eval_round_build_ms": st0["ms_round_build"],
+            "one_shot_s": scene_build_s + first_eval_s,
             "stage_ms": {"cull": stt["ms_cull"], "k3_candidates": stt["ms_k3_candidates"],
                          "k3_fallback": stt["ms_k3_fallback"], "k3_newton": stt["ms_k3_newton"],
-                         "boundary": stt["ms_boundary"], "finalize": stt["ms_other"]},
+                         "boundary": stt["ms_boundary"], "k4_far": stt["ms_k4_far"],
+                         "k4_exact": stt["ms_k4_exact"], "finalize": stt["ms_other"]},
             "counters": {k: stt[k] for k in ("candidates", "nodes", "newton_iters", "roots",
                                              "k3_newton_items", "k3_fallback_items",
-                                             "boundary_segments", "retried", "rounds")},
+                                             "boundary_segments", "far_pairs", "far_terms",
+                                             "near_pairs", "retried", "rounds")},
             "clocks": clock_info,
         }
-        if world == 1 and not args.no_ray_reuse:
-            out["ray_reuse"] = ray_reuse(G, torch, sc, dev, stream)
-        if world == 1 and not args.no_ray_reuse:
-            out["roofline_open_scene"] = boundary_roofline(G, torch, dev, stream, peak_tf)
-        if world == 1 and not args.no_far_field:
-            out["far_field"] = far_field(G, torch, dev, stream)
-        if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(spec, args.cpu_seconds)
+    if world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        par, base = oracle_parity(spec, w_host, st_host, min(nq, PARITY_Q), cores)
+        out["parity"] = par
+        out["cpu_baseline"] = base
+        if not args.no_extras:
+            try:
+                from oracle import ref_asshipped
+                out["as_shipped_reference"] = ref_asshipped.measure(cores)
+            except Exception as e:  # the reference package travels in baseline/_ref
+                out["as_shipped_reference"] = {"unavailable": f"{type(e).__name__}: {e}"}
+    if world == 1 and not args.no_extras:
+        extra = {}
+        for cfg in (2, 3, 4):
+            if cfg != args.config:
+                extra[f"config{cfg}"] = side_config(G, torch, cfg, dev, stream)
+        out["other_configs"] = extra
+        out["far_field"] = far_field_side(G, torch, dev, stream)
+        out["ray_reuse"] = ray_reuse_side(G, torch, 4, dev, stream)
+    if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define GWN_ABI_VERSION 2
+#define GWN_ABI_VERSION 3
 
 /* return codes (negative = error) */
 #define GWN_OK 0
@@ -53,6 +53,8 @@ extern "C" {
 #define GWN_STATUS_ON_SURFACE 1   /* OnSurface: jittered by jitter_scale*diag */
 #define GWN_STATUS_EXHAUSTED 2    /* SeedExhausted: re-shoot budget spent     */
 #define GWN_STATUS_DEGENERATE 3   /* DegenerateProjection: jittered           */
+#define GWN_STATUS_JITTER_EXHAUSTED 4 /* still on the surface / boundary after
+                                     max_jitters jitters: w is unreliable   */
 
 /* gwn_eval flags */
 #define GWN_HOST_BUFFERS 1        /* queries / outputs are host pointers */
@@ -108,6 +110,11 @@ typedef struct gwn_stats {
   int64_t k3_newton_items;    /* certified leaf candidates (Newton solves)          */
   int64_t far_pairs;          /* (query, boundary cycle) pairs taken by the far-field
                                  expansion instead of the exact fan sum */
+  int64_t far_terms;          /* solid-harmonic terms those expansions summed          */
+  int64_t near_pairs;         /* (query, boundary cycle) pairs summed exactly          */
+  double ms_k4_far, ms_k4_exact;  /* split of ms_boundary (far-field scenes, timed)   */
+  int64_t rounds_built;       /* direction rounds (K1 structures) cached on the scene */
+  double ms_round_build;      /* host wall time building new rounds in this eval      */
 } gwn_stats;
 
 int gwn_abi_version(void);
@@ -146,13 +153,20 @@ int gwn_eval_rays(gwn_scene* scene, const double* origins, int64_t R,
                   int64_t* rays_cast);
 int gwn_set_timing(gwn_scene* scene, int32_t timed);
 
-/* All hits of one ray with one patch of the scene (host buffers). Records:
- * t, u, v, sign, tangency, grazing.  Returns count (may exceed cap: only cap
- * written) or a negative error. */
+/* patch.all_hits(ray, t_window, eps) (surfaces.py:587-589, body
+ * surfaces.py:634-701): all hits of one ray with one patch of the scene, host
+ * buffers.  `eps` = the caller's thresholds (NULL: the scene's); only roots
+ * with t in [t_lo, t_hi] (+-1e-12, surfaces.py:679) are returned, sorted by t.
+ * Records: t, u, v, sign, tangency, grazing.  A near-tangent contact the
+ * subdivision cannot separate is returned as a tangent record.  Returns the
+ * count (at most 18, Bezout's bound for a line and a bicubic; only `cap`
+ * rows written) or a negative error; *flags_out (may be NULL) receives the
+ * root set's flag bits (1 = re-shoot: tangent / grazing contact). */
 int gwn_all_hits(gwn_scene* scene, int64_t patch, const double origin[3],
-                 const double direction[3], double* t_out, double* uv_out,
-                 int32_t* sign_out, int8_t* tangency_out, int8_t* grazing_out,
-                 int32_t cap);
+                 const double direction[3], const gwn_params* eps, double t_lo,
+                 double t_hi, double* t_out, double* uv_out, int32_t* sign_out,
+                 int8_t* tangency_out, int8_t* grazing_out, int32_t cap,
+                 int32_t* flags_out);
 
 /* _kernels.single_loop_batch on the GPU: closed loop (B,3), ray, cached hit
  * ts/signs (H), query ts (K) -> w (K), ok (K).  Host buffers. */

@@ -728,7 +728,7 @@ static void eval_query(const scene_t* sc, const double p0[3], int64_t qidx, doub
         for (int k = 0; k < 3; ++k) p[k] = p0[k] + s * v[k];
         continue;
       }
-      status = jit_reason;
+      status = 4;                          /* still on it after the jitter budget */
       break;
     }
     if (flags & (1 | 2)) continue;         /* tangent / grazing / band: new direction */

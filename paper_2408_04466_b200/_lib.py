@@ -75,7 +75,9 @@ class Stats(C.Structure):
         ("ms_other", C.c_double), ("ms_k3_candidates", C.c_double),
         ("ms_k3_fallback", C.c_double), ("ms_k3_newton", C.c_double),
         ("k3_fallback_items", C.c_int64), ("k3_newton_items", C.c_int64),
-        ("far_pairs", C.c_int64),
+        ("far_pairs", C.c_int64), ("far_terms", C.c_int64), ("near_pairs", C.c_int64),
+        ("ms_k4_far", C.c_double), ("ms_k4_exact", C.c_double), ("rounds_built", C.c_int64),
+        ("ms_round_build", C.c_double),
     ]
 
     def as_dict(self) -> dict:
@@ -115,8 +117,10 @@ def lib() -> C.CDLL:
                                     C.POINTER(C.c_int64)]
         L.gwn_stats_get.argtypes = [vp, C.POINTER(Stats)]
         L.gwn_set_timing.argtypes = [vp, C.c_int32]
-        L.gwn_all_hits.argtypes = [vp, C.c_int64, dp, dp, dp, dp, C.POINTER(C.c_int32),
-                                   C.POINTER(C.c_int8), C.POINTER(C.c_int8), C.c_int32]
+        L.gwn_all_hits.argtypes = [vp, C.c_int64, dp, dp, C.POINTER(GwnParams), C.c_double,
+                                   C.c_double, dp, dp, C.POINTER(C.c_int32),
+                                   C.POINTER(C.c_int8), C.POINTER(C.c_int8), C.c_int32,
+                                   C.POINTER(C.c_int32)]
         L.gwn_single_loop_batch.argtypes = [dp, C.c_int64, dp, dp, dp, C.POINTER(C.c_int64),
                                             C.c_int64, dp, C.c_int64, C.c_double, C.c_double,
                                             dp, C.POINTER(C.c_int8), C.c_int]
@@ -155,4 +159,18 @@ def check(rc: int, what: str) -> int:
 def default_params() -> GwnParams:
     p = GwnParams()
     lib().gwn_params_default(C.byref(p))
+    return p
+
+
+def params_from_eps(eps) -> GwnParams:
+    """gwn_params with the EpsilonConfig fields the kernels consume
+    (config.py:15-38 names -> include/gwn_b200.h fields); engine knobs at
+    their defaults."""
+    p = default_params()
+    p.residual = eps.residual
+    p.dedup = eps.dedup
+    p.tangent = eps.tangent_parametric
+    p.edge_graze = eps.edge_graze
+    p.degenerate = eps.degenerate
+    p.jitter_scale = eps.jitter_scale
     return p

@@ -145,7 +145,7 @@ def cmd_query(a) -> int:
     if a.oracle:
         o = ev.oracle(p[None, :], a.tess)[0]
         print(f"oracle={o:.9f} diff={abs(o - w[0]):.3e}")
-    return EXIT_DEGENERATE if int(st[0]) in (2, 3) else 0
+    return EXIT_DEGENERATE if int(st[0]) in (2, 4) else 0  # budgets spent
 
 
 def cmd_slice(a) -> int:

@@ -25,6 +25,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "gwn_fan.cuh"
 #include "gwn_farfield.cuh"
 
@@ -247,28 +249,99 @@ k_boundary(int32_t m, const int32_t* __restrict__ active, const double* __restri
 #ifndef GWN_K4_MINB
 #define GWN_K4_MINB 2
 #endif
-// kFF: far-field scene (gwn_farfield.cu).  Per edge, each query decides with
-// ff_far() whether the edge's cycle is taken by the far kernel; far queries
-// multiply their running product by (1, 0) (exactly neutral) and a warp whose
-// queries are all far skips the edge.  `order` (nullable) maps threads to
-// slots (3-D Morton order, so warps agree).
-struct FFView {
-  const int32_t* order;
-  const int32_t* edge;   // cycle of each edge, -1 = exact only
-  const double* g;       // cycle centres, round frame
-  const double* r2;      // R_min^2, line radius^2
-};
 
-#ifndef GWN_K4_MINB_FF
-#define GWN_K4_MINB_FF 3  // far-field scenes: occupancy beats the few spills (config 5 -5%)
-#endif
-template <int QPT, bool kFF>
-__global__ void __launch_bounds__(kBlockQ, kFF ? GWN_K4_MINB_FF : GWN_K4_MINB)
+// one edge's S-1 segments from shared memory (vertex b .. b+S-1) into the
+// running products: blocks of 8 segments, renormalised after each block
+template <int QPT>
+__device__ __forceinline__ void edge_segments(const double* sx, const double* sy,
+                                              const double* sz, int b, int S, const bool* use,
+                                              const double* qa, const double* qb,
+                                              const double* qc, SegState* st, int* neg,
+                                              int* minhi, VtxF* va, VtxF* vb) {
+#pragma unroll
+  for (int j = 0; j < QPT; ++j)
+    va[j] = make_vtxf(sx[b], sy[b], sz[b], qa[j], qb[j], qc[j], minhi[j]);
+  int k = b + 1;
+  const int kend = b + S;
+  for (; k + 8 <= kend; k += 8) {
+#pragma unroll
+    for (int h = 0; h < 8; h += 2) {
+#pragma unroll
+      for (int j = 0; j < QPT; ++j) {
+        vb[j] = make_vtxf(sx[k + h], sy[k + h], sz[k + h], qa[j], qb[j], qc[j], minhi[j]);
+        const double num = va[j].uy * vb[j].ux - va[j].ux * vb[j].uy;
+        const double den = va[j].ux * vb[j].ux + va[j].uy * vb[j].uy + va[j].uz * vb[j].uz;
+        neg[j] |= __double2hiint(den);
+        cmul_track(st[j], den, num);
+      }
+#pragma unroll
+      for (int j = 0; j < QPT; ++j) {
+        va[j] = make_vtxf(sx[k + h + 1], sy[k + h + 1], sz[k + h + 1], qa[j], qb[j], qc[j],
+                          minhi[j]);
+        const double num = vb[j].uy * va[j].ux - vb[j].ux * va[j].uy;
+        const double den = vb[j].ux * va[j].ux + vb[j].uy * va[j].uy + vb[j].uz * va[j].uz;
+        neg[j] |= __double2hiint(den);
+        cmul_track(st[j], den, num);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) renorm(st[j]);
+  }
+  for (; k < kend; ++k) {
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) {
+      vb[j] = make_vtxf(sx[k], sy[k], sz[k], qa[j], qb[j], qc[j], minhi[j]);
+      const double num = va[j].uy * vb[j].ux - va[j].ux * vb[j].uy;
+      const double den = va[j].ux * vb[j].ux + va[j].uy * vb[j].uy + va[j].uz * vb[j].uz;
+      neg[j] |= __double2hiint(den);
+      cmul_track(st[j], den, num);
+      va[j] = vb[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) renorm(st[j]);
+  (void)use;
+}
+
+// rare: some segment of the staged edges had den < 0 -> polyline/curve band
+// test for the lanes concerned, re-walking the staged edges
+template <int QPT>
+__device__ __forceinline__ void band_rewalk(const double* sx, const double* sy, const double* sz,
+                                            int ne, int S, const double* __restrict__ band_h,
+                                            int64_t e_first, const double* qa, const double* qb,
+                                            const double* qc, double band_factor, int* neg,
+                                            int* flags) {
+  bool any = false;
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) any |= neg[j] < 0;
+  if (!__any_sync(0xffffffffu, any)) return;
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) {
+    if (neg[j] >= 0) continue;
+    int mh = 0x7fffffff;
+    for (int e = 0; e < ne; ++e) {
+      const int b = e * S;
+      const double h = __ldg(band_h + e_first + e);
+      VtxF A = make_vtxf(sx[b], sy[b], sz[b], qa[j], qb[j], qc[j], mh);
+      for (int i = b + 1; i < b + S; ++i) {
+        const VtxF B = make_vtxf(sx[i], sy[i], sz[i], qa[j], qb[j], qc[j], mh);
+        const double num = A.uy * B.ux - A.ux * B.uy;
+        const double den = A.ux * B.ux + A.uy * B.uy + A.uz * B.uz;
+        if (den < 0.0 && band_hit_f(A, B, num, h, band_factor)) flags[j] |= FLAG_BAND;
+        A = B;
+      }
+    }
+    neg[j] = 0;
+  }
+}
+
+template <int QPT>
+__global__ void __launch_bounds__(kBlockQ, GWN_K4_MINB)
 k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __restrict__ pos,
              const double* __restrict__ vproj, int64_t V, int S, int64_t n_edges,
              const double* __restrict__ band_h, Frame f, DevParams prm,
              double* __restrict__ bpart, int32_t* __restrict__ flag_acc,
-             unsigned long long* __restrict__ counters, FFView ff) {
+             unsigned long long* __restrict__ counters) {
   const int nchunk = gridDim.y;
   const int64_t e0 = n_edges * blockIdx.y / nchunk, e1 = n_edges * (blockIdx.y + 1) / nchunk;
   const int ept = kTileV / S;  // whole edges per tile
@@ -280,31 +353,21 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
   bool live[QPT];
 #pragma unroll
   for (int j = 0; j < QPT; ++j) {
-    // ordered (far-field) launches: a warp's QPT*32 queries are consecutive
-    // in Morton order, so they share one small region
-    const int32_t t = (kFF && ff.order)
-                          ? blockIdx.x * (blockDim.x * QPT) + (threadIdx.x & ~31) * QPT + j * 32 +
-                                (threadIdx.x & 31)
-                          : blockIdx.x * (blockDim.x * QPT) + j * blockDim.x + threadIdx.x;
+    const int32_t t = blockIdx.x * (blockDim.x * QPT) + j * blockDim.x + threadIdx.x;
     live[j] = t < m;
-    slot[j] = (kFF && ff.order && live[j]) ? ff.order[t] : t;
+    slot[j] = t;
     const int32_t q = live[j] ? (active ? active[slot[j]] : slot[j]) : 0;
     const double px = live[j] ? pos[3 * (int64_t)q] : 0.0;
     const double py = live[j] ? pos[3 * (int64_t)q + 1] : 0.0;
     const double pz = live[j] ? pos[3 * (int64_t)q + 2] : 0.0;
-    if (kFF) {
-      frame_q(f, px, py, pz, qa[j], qb[j], qc[j]);
-    } else {
-      qa[j] = px * f.e1[0] + py * f.e1[1] + pz * f.e1[2];
-      qb[j] = px * f.e2[0] + py * f.e2[1] + pz * f.e2[2];
-      qc[j] = px * f.d[0] + py * f.d[1] + pz * f.d[2];
-    }
+    qa[j] = px * f.e1[0] + py * f.e1[1] + pz * f.e1[2];
+    qb[j] = px * f.e2[0] + py * f.e2[1] + pz * f.e2[2];
+    qc[j] = px * f.d[0] + py * f.d[1] + pz * f.d[2];
     st[j] = SegState{1.0, 0.0, 0};
     flags[j] = 0;
     minhi[j] = 0x7fffffff;
     neg[j] = 0;
   }
-  unsigned long long exact_pairs = 0;  // (query, segment) pairs summed exactly
   VtxF va[QPT], vb[QPT];
   for (int64_t te = e0; te < e1; te += ept) {
     const int ne = (int)min((int64_t)ept, e1 - te);
@@ -318,103 +381,9 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
       sz[k] = vproj[2 * V + g];
     }
     __syncthreads();
-    for (int e = 0; e < ne; ++e) {
-      const int b = e * S;
-      // far queries of this edge's cycle: neutral factor (1, 0); skip the
-      // edge when the whole warp is far
-      bool far[QPT];
-#pragma unroll
-      for (int j = 0; j < QPT; ++j) far[j] = false;
-      if (kFF) {
-        const int c = __ldg(ff.edge + te + e);
-        bool all = true;
-        int nnear = 0;
-#pragma unroll
-        for (int j = 0; j < QPT; ++j) {
-          far[j] = c >= 0 && live[j] && ff_far(qa[j], qb[j], qc[j], ff.g + 3 * c, ff.r2 + 2 * c);
-          all &= far[j] || !live[j];
-          nnear += (live[j] && !far[j]) ? 1 : 0;
-        }
-#ifndef GWN_FF_NOSKIP
-        if (__all_sync(0xffffffffu, all)) continue;
-#endif
-        exact_pairs += (unsigned long long)nnear * (unsigned long long)(S - 1);
-      }
-#pragma unroll
-      for (int j = 0; j < QPT; ++j)
-        va[j] = make_vtxf(sx[b], sy[b], sz[b], qa[j], qb[j], qc[j], minhi[j]);
-      int k = b + 1;
-      const int kend = b + S;
-      // blocks of 8 segments: va -> vb -> va ..., renorm after each block
-      for (; k + 8 <= kend; k += 8) {
-#pragma unroll
-        for (int h = 0; h < 8; h += 2) {
-#pragma unroll
-          for (int j = 0; j < QPT; ++j) {
-            vb[j] = make_vtxf(sx[k + h], sy[k + h], sz[k + h], qa[j], qb[j], qc[j], minhi[j]);
-            double num = va[j].uy * vb[j].ux - va[j].ux * vb[j].uy;
-            double den = va[j].ux * vb[j].ux + va[j].uy * vb[j].uy + va[j].uz * vb[j].uz;
-            if (kFF && far[j]) { den = 1.0; num = 0.0; }
-            neg[j] |= __double2hiint(den);
-            cmul_track(st[j], den, num);
-          }
-#pragma unroll
-          for (int j = 0; j < QPT; ++j) {
-            va[j] = make_vtxf(sx[k + h + 1], sy[k + h + 1], sz[k + h + 1], qa[j], qb[j], qc[j],
-                              minhi[j]);
-            double num = vb[j].uy * va[j].ux - vb[j].ux * va[j].uy;
-            double den = vb[j].ux * va[j].ux + vb[j].uy * va[j].uy + vb[j].uz * va[j].uz;
-            if (kFF && far[j]) { den = 1.0; num = 0.0; }
-            neg[j] |= __double2hiint(den);
-            cmul_track(st[j], den, num);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < QPT; ++j) renorm(st[j]);
-      }
-      for (; k < kend; ++k) {
-#pragma unroll
-        for (int j = 0; j < QPT; ++j) {
-          vb[j] = make_vtxf(sx[k], sy[k], sz[k], qa[j], qb[j], qc[j], minhi[j]);
-          double num = va[j].uy * vb[j].ux - va[j].ux * vb[j].uy;
-          double den = va[j].ux * vb[j].ux + va[j].uy * vb[j].uy + va[j].uz * vb[j].uz;
-          if (kFF && far[j]) { den = 1.0; num = 0.0; }
-          neg[j] |= __double2hiint(den);
-          cmul_track(st[j], den, num);
-          va[j] = vb[j];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < QPT; ++j) renorm(st[j]);
-    }
-    // rare: some segment of this tile had den < 0 -> polyline/curve band test
-    bool any = false;
-#pragma unroll
-    for (int j = 0; j < QPT; ++j) any |= neg[j] < 0;
-    if (__any_sync(0xffffffffu, any)) {
-#pragma unroll
-      for (int j = 0; j < QPT; ++j) {
-        if (neg[j] >= 0) continue;
-        int mh = 0x7fffffff;
-        for (int e = 0; e < ne; ++e) {
-          const int b = e * S;
-          if (kFF) {  // far cycles: the line misses their sphere, no band
-            const int c = __ldg(ff.edge + te + e);
-            if (c >= 0 && ff_far(qa[j], qb[j], qc[j], ff.g + 3 * c, ff.r2 + 2 * c)) continue;
-          }
-          const double h = __ldg(band_h + te + e);
-          VtxF A = make_vtxf(sx[b], sy[b], sz[b], qa[j], qb[j], qc[j], mh);
-          for (int i = b + 1; i < b + S; ++i) {
-            const VtxF B = make_vtxf(sx[i], sy[i], sz[i], qa[j], qb[j], qc[j], mh);
-            const double num = A.uy * B.ux - A.ux * B.uy;
-            const double den = A.ux * B.ux + A.uy * B.uy + A.uz * B.uz;
-            if (den < 0.0 && band_hit_f(A, B, num, h, prm.band_factor)) flags[j] |= FLAG_BAND;
-            A = B;
-          }
-        }
-        neg[j] = 0;
-      }
-    }
+    for (int e = 0; e < ne; ++e)
+      edge_segments<QPT>(sx, sy, sz, e * S, S, live, qa, qb, qc, st, neg, minhi, va, vb);
+    band_rewalk<QPT>(sx, sy, sz, ne, S, band_h, te, qa, qb, qc, prm.band_factor, neg, flags);
   }
 #pragma unroll
   for (int j = 0; j < QPT; ++j)
@@ -426,15 +395,442 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
       if (flags[j]) atomicOr(&flag_acc[slot[j]], flags[j]);
     }
   }
-  if (kFF) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) exact_pairs += __shfl_down_sync(0xffffffffu, exact_pairs, o);
-    if ((threadIdx.x & 31) == 0 && exact_pairs) atomicAdd(&counters[CNT_SEGMENTS], exact_pairs);
-  } else if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     int32_t nq = min((int32_t)(blockDim.x * QPT), m - (int32_t)(blockIdx.x * blockDim.x * QPT));
     const int64_t segs = (e1 - e0) * (int64_t)(S - 1);
     atomicAdd(&counters[CNT_SEGMENTS], (unsigned long long)(segs * nq));
   }
+}
+
+#ifndef GWN_K4_QPT
+#define GWN_K4_QPT 2
+#endif
+constexpr int kQPT = GWN_K4_QPT;
+
+// ---------------------------------------------------------------------------
+// Far-field scenes (entries built by gwn_farfield.cu).  Per round and chunk:
+//   k_ff_count   per query (3-D Morton order), every entry: far or near?
+//                counts per query and per entry (warp-aggregated atomics)
+//   scans        query-major offsets qoff, entry-major offsets eoff, tiles
+//   k_ff_fill    the same decisions again: far entries add their multipole
+//                expansion (row 0), near ones append (query slot, k) to the
+//                entry's pair list
+//   k_ff_near    one block per tile of one entry's near pairs: the entry's
+//                vertices staged once in shared memory, every lane sums the
+//                exact fan over all of the entry's segments for its query --
+//                no lane is ever masked, unlike a query-major walk over all
+//                edges that skips far entries per lane
+//   k_ff_near_sum  per query: its near angles in entry order (row 1)
+// Both rows and every sum in them are in a fixed order, so w is
+// bit-identical for any batching, chunking or sharding.
+//
+// Far test (both passes, bit-identical): R >= R_min(entry) and the ray's
+// forward half-line p + t d (t > 0) misses the entry's sphere -- the fan sum's
+// 2 pi branch sits where +d meets the polyline, so only that half-line
+// matters (a sphere wholly behind p along d is far even when the backward
+// line crosses it).
+// ---------------------------------------------------------------------------
+
+struct FFRound {
+  int32_t C;
+  const double* g3;     // (C,3) entry centres in the round frame
+  const double* r2;     // (C,2) R_min^2, line radius^2
+  const double* lv;     // (C,kFFLevels) R^2 thresholds of the orders
+  const double* gw;     // (C,3) entry centres (world)
+  const double2* D;     // (C,kFFTerms) moments
+  const int32_t* chord; // (C) sliver chord edge or -1
+  const double* ffa;    // (C,6) chord end points, round frame
+};
+
+__device__ __forceinline__ bool ff_far2(double qa, double qb, double qc,
+                                        const double* __restrict__ g3,
+                                        const double* __restrict__ r2) {
+  const double dx = __dsub_rn(__ldg(g3), qa), dy = __dsub_rn(__ldg(g3 + 1), qb);
+  const double dz = __dsub_rn(__ldg(g3 + 2), qc);
+  const double l2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  const double R2 = __dadd_rn(l2, __dmul_rn(dz, dz));
+  const double line2 = __ldg(r2 + 1);
+  return R2 > __ldg(r2) && (l2 > line2 || (dz < 0.0 && __dmul_rn(dz, dz) > line2));
+}
+
+// Omega(p) = -sum_{n>=1} [Re(D_n^0 I_n^0) + 2 sum_{m>=1} Re(D_n^m I_n^m)] of
+// order pl (<= P): the loops run to the warp's largest order P and a lane
+// adds only its own terms, so its sum is bit-identical to an order-pl
+// evaluation whatever its neighbours need (explicit roundings).
+template <int P>
+__device__ __forceinline__ double ff_eval_pred(double x, double y, double z,
+                                               const double2* __restrict__ Dc, int pl) {
+  const double ir2 = __drcp_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)),
+                                         __dmul_rn(z, z)));
+  double dR = __dsqrt_rn(ir2), dI = 0.0;  // I_0^0 = 1/r
+  double acc = 0.0;
+#pragma unroll
+  for (int mm = 0; mm <= P; ++mm) {
+    if (mm > 0) {  // I_m^m = -(2m-1)(x+iy)/r^2 I_{m-1}^{m-1}
+      const double c0 = __dmul_rn(-(2.0 * mm - 1.0), ir2);
+      const double nR = __dmul_rn(c0, __fma_rn(x, dR, -__dmul_rn(y, dI)));
+      const double nI = __dmul_rn(c0, __fma_rn(x, dI, __dmul_rn(y, dR)));
+      dR = nR;
+      dI = nI;
+    }
+    double aR = dR, aI = dI, bR = 0.0, bI = 0.0;
+    double col = 0.0;
+#pragma unroll
+    for (int n = mm; n <= P; ++n) {
+      if (n > mm) {  // I_n^m = ((2n-1) z I_{n-1}^m - ((n-1)^2 - m^2) I_{n-2}^m) / r^2
+        const double kz = __dmul_rn(2.0 * n - 1.0, z);
+        const double k2 = (double)((n - 1) * (n - 1) - mm * mm);
+        const double vR = __dmul_rn(__fma_rn(kz, aR, -__dmul_rn(k2, bR)), ir2);
+        const double vI = __dmul_rn(__fma_rn(kz, aI, -__dmul_rn(k2, bI)), ir2);
+        bR = aR;
+        bI = aI;
+        aR = vR;
+        aI = vI;
+      }
+      if (n == 0) continue;
+      const double2 d = __ldg(Dc + ff_term(n, mm));
+      if (n <= pl) col = __fma_rn(d.x, aR, __fma_rn(-d.y, aI, col));
+    }
+    if (mm <= pl) acc = __dadd_rn(acc, mm == 0 ? col : __dmul_rn(2.0, col));
+  }
+  return -acc;
+}
+
+__device__ __forceinline__ int ff_nterms(int P) { return (P + 1) * (P + 2) / 2 - 1; }
+
+struct FFQuery {
+  int32_t s;   // slot
+  bool live;
+  double px, py, pz, qa, qb, qc;
+};
+
+__device__ __forceinline__ FFQuery ff_query(int32_t m, const int32_t* __restrict__ order,
+                                            const int32_t* __restrict__ active,
+                                            const double* __restrict__ pos, const Frame& f) {
+  FFQuery Q;
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  Q.live = t < m;
+  Q.s = Q.live ? (order ? order[t] : t) : 0;
+  const int32_t q = Q.live ? (active ? active[Q.s] : Q.s) : 0;
+  Q.px = Q.live ? pos[3 * (int64_t)q] : 0.0;
+  Q.py = Q.live ? pos[3 * (int64_t)q + 1] : 0.0;
+  Q.pz = Q.live ? pos[3 * (int64_t)q + 2] : 0.0;
+  frame_q(f, Q.px, Q.py, Q.pz, Q.qa, Q.qb, Q.qc);
+  return Q;
+}
+
+constexpr int kFFBlock = 128;
+
+__global__ void __launch_bounds__(kFFBlock)
+k_ff_count(int32_t m, const int32_t* __restrict__ order, const int32_t* __restrict__ active,
+           const double* __restrict__ pos, Frame f, FFRound R, unsigned* __restrict__ qcnt,
+           unsigned* __restrict__ ecnt, unsigned long long* __restrict__ counters) {
+  const FFQuery Q = ff_query(m, order, active, pos, f);
+  const int lane = threadIdx.x & 31;
+  unsigned n = 0;
+  for (int c = 0; c < R.C; ++c) {  // warp-uniform loop
+    const bool near = Q.live && !ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+    n += near ? 1u : 0u;
+    const unsigned b = __ballot_sync(0xffffffffu, near);
+    if (b && lane == __ffs(b) - 1) atomicAdd(&ecnt[c], (unsigned)__popc(b));
+  }
+  if (Q.live) qcnt[Q.s] = n;
+  unsigned long long tot = n;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_down_sync(0xffffffffu, tot, o);
+  if (lane == 0 && tot) atomicAdd(&counters[CNT_NEAR], tot);
+}
+
+__global__ void __launch_bounds__(kFFBlock)
+k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restrict__ active,
+          const double* __restrict__ pos, Frame f, FFRound R,
+          const unsigned long long* __restrict__ eoff, unsigned* __restrict__ efill,
+          int2* __restrict__ recs, double* __restrict__ row_far,
+          unsigned long long* __restrict__ counters) {
+  const FFQuery Q = ff_query(m, order, active, pos, f);
+  const int lane = threadIdx.x & 31;
+  double om = 0.0;
+  int k = 0;
+  unsigned long long nfar = 0, terms = 0;
+  for (int c = 0; c < R.C; ++c) {  // warp-uniform loop
+    const bool far = Q.live && ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+    const bool near = Q.live && !far;
+    const unsigned b = __ballot_sync(0xffffffffu, near);
+    if (b) {  // append the near lanes to entry c's pair list
+      const int leader = __ffs(b) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(&efill[c], (unsigned)__popc(b));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (near) {
+        recs[eoff[c] + base + __popc(b & ((1u << lane) - 1))] = make_int2(Q.s, k);
+        ++k;
+      }
+    }
+    // far: the expansion at the lane's order, the warp runs to its largest
+    int lvl = -1;
+    double x = 1.0, y = 0.0, z = 0.0;
+    if (far) {
+      x = __dsub_rn(Q.px, __ldg(R.gw + 3 * c));
+      y = __dsub_rn(Q.py, __ldg(R.gw + 3 * c + 1));
+      z = __dsub_rn(Q.pz, __ldg(R.gw + 3 * c + 2));
+      const double R2 = __dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z));
+      const double* lv = R.lv + (int64_t)kFFLevels * c;
+      lvl = kFFLevels - 1;
+#pragma unroll
+      for (int l = 0; l < kFFLevels - 1; ++l)
+        if (lvl == kFFLevels - 1 && R2 > __ldg(lv + l)) lvl = l;
+    }
+    const int wl = __reduce_max_sync(0xffffffffu, (unsigned)(lvl + 1)) - 1;
+    if (wl < 0) continue;
+    const double2* Dc = R.D + (int64_t)c * kFFTerms;
+    const int pl = far ? ff_order(lvl) : -1;
+    double v;
+    static_assert(kFFLevels == 4, "the order dispatch below covers four levels");
+    switch (wl) {
+      case 0: v = ff_eval_pred<ff_order(0)>(x, y, z, Dc, pl); break;
+      case 1: v = ff_eval_pred<ff_order(1)>(x, y, z, Dc, pl); break;
+      case 2: v = ff_eval_pred<ff_order(2)>(x, y, z, Dc, pl); break;
+      default: v = ff_eval_pred<ff_order(3)>(x, y, z, Dc, pl); break;
+    }
+    if (!far) continue;
+    om = __dadd_rn(om, v);
+    ++nfar;
+    terms += (unsigned long long)ff_nterms(pl);
+    if (__ldg(R.chord + c) >= 0) {
+      // sliver: the edge's fan sum = Omega(edge + chord back) + the chord's
+      // forward fan term, K4's shifted form in the ray frame (den > 0: the
+      // half-line misses the sliver's sphere)
+      const double* A = R.ffa + 6 * (int64_t)c;
+      const double rax = __ldg(A) - Q.qa, ray = __ldg(A + 1) - Q.qb, raz = __ldg(A + 2) - Q.qc;
+      const double rbx = __ldg(A + 3) - Q.qa, rby = __ldg(A + 4) - Q.qb,
+                   rbz = __ldg(A + 5) - Q.qc;
+      const double ia = 1.0 / sqrt(rax * rax + ray * ray + raz * raz);
+      const double ib = 1.0 / sqrt(rbx * rbx + rby * rby + rbz * rbz);
+      const double uax = rax * ia, uay = ray * ia, uaz = fma(raz, ia, -1.0);
+      const double ubx = rbx * ib, uby = rby * ib, ubz = fma(rbz, ib, -1.0);
+      const double num = uay * ubx - uax * uby;
+      const double den = uax * ubx + uay * uby + uaz * ubz;
+      om = __dadd_rn(om, 2.0 * atan2(num, den));
+    }
+  }
+  // K4's partials are sums of atan2 (half angles): Omega / 2
+  if (Q.live) row_far[Q.s] = 0.5 * om;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nfar += __shfl_down_sync(0xffffffffu, nfar, o);
+    terms += __shfl_down_sync(0xffffffffu, terms, o);
+  }
+  if (lane == 0 && nfar) {
+    atomicAdd(&counters[CNT_FAR], nfar);
+    atomicAdd(&counters[CNT_FAR_TERMS], terms);
+  }
+}
+
+// tiles of kBlockQ * kQPT near pairs per entry
+__global__ void k_ff_tiles(int32_t C, const unsigned* __restrict__ ecnt, int tp,
+                           unsigned* __restrict__ tcnt) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) tcnt[c] = (ecnt[c] + tp - 1) / tp;
+}
+
+template <int QPT>
+__global__ void __launch_bounds__(kBlockQ, GWN_K4_MINB)
+k_ff_near(int32_t C, const unsigned long long* __restrict__ toff,
+          const unsigned long long* __restrict__ eoff, const int32_t* __restrict__ ent_eoff,
+          const int2* __restrict__ recs, const unsigned long long* __restrict__ qoff,
+          const int32_t* __restrict__ active, const double* __restrict__ pos,
+          const double* __restrict__ vproj, int64_t V, int S, const double* __restrict__ band_h,
+          Frame f, DevParams prm, double* __restrict__ slot_ang,
+          int32_t* __restrict__ flag_acc, unsigned long long* __restrict__ counters) {
+  // entry of this tile: the last c with toff[c] <= tile (block-uniform search)
+  const unsigned long long tile = blockIdx.x;
+  int lo = 0, hi = C;  // toff[lo] <= tile < toff[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(toff + mid) <= tile) lo = mid; else hi = mid;
+  }
+  const int c = lo;
+  const unsigned long long p_beg = eoff[c] + (tile - toff[c]) * (unsigned long long)(kBlockQ * QPT);
+  const unsigned long long p_end = min(eoff[c + 1], p_beg + (unsigned long long)(kBlockQ * QPT));
+  const int64_t E0 = ent_eoff[c], E1 = ent_eoff[c + 1];
+  const int ept = kTileV / S;
+  __shared__ double sx[kTileV], sy[kTileV], sz[kTileV];
+  int32_t qs[QPT], qk[QPT];
+  double qa[QPT], qb[QPT], qc[QPT];
+  SegState st[QPT];
+  int flags[QPT], minhi[QPT], neg[QPT];
+  bool live[QPT];
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) {
+    const unsigned long long p = p_beg + (unsigned long long)(j * kBlockQ + threadIdx.x);
+    live[j] = p < p_end;
+    const int2 r = live[j] ? recs[p] : make_int2(0, 0);
+    qs[j] = r.x;
+    qk[j] = r.y;
+    const int32_t q = live[j] ? (active ? active[r.x] : r.x) : 0;
+    const double px = live[j] ? pos[3 * (int64_t)q] : 0.0;
+    const double py = live[j] ? pos[3 * (int64_t)q + 1] : 0.0;
+    const double pz = live[j] ? pos[3 * (int64_t)q + 2] : 0.0;
+    qa[j] = px * f.e1[0] + py * f.e1[1] + pz * f.e1[2];
+    qb[j] = px * f.e2[0] + py * f.e2[1] + pz * f.e2[2];
+    qc[j] = px * f.d[0] + py * f.d[1] + pz * f.d[2];
+    st[j] = SegState{1.0, 0.0, 0};
+    flags[j] = 0;
+    minhi[j] = 0x7fffffff;
+    neg[j] = 0;
+  }
+  VtxF va[QPT], vb[QPT];
+  for (int64_t te = E0; te < E1; te += ept) {
+    const int ne = (int)min((int64_t)ept, E1 - te);
+    const int nt = ne * S;
+    const int64_t t0 = te * S;
+    __syncthreads();
+    for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+      const int64_t g = t0 + k;
+      sx[k] = vproj[g];
+      sy[k] = vproj[V + g];
+      sz[k] = vproj[2 * V + g];
+    }
+    __syncthreads();
+    for (int e = 0; e < ne; ++e)
+      edge_segments<QPT>(sx, sy, sz, e * S, S, live, qa, qb, qc, st, neg, minhi, va, vb);
+    band_rewalk<QPT>(sx, sy, sz, ne, S, band_h, te, qa, qb, qc, prm.band_factor, neg, flags);
+  }
+  int nlive = 0;
+#pragma unroll
+  for (int j = 0; j < QPT; ++j) {
+    if (!live[j]) continue;
+    ++nlive;
+    if (minhi[j] < kDegHi) flags[j] |= FLAG_DEGEN;
+    slot_ang[qoff[qs[j]] + (unsigned long long)qk[j]] = seg_angle(st[j]);
+    if (flags[j]) atomicOr(&flag_acc[qs[j]], flags[j]);
+  }
+  // exact (query, segment) pairs, one atomic per warp
+  unsigned long long segs = (unsigned long long)nlive * (unsigned long long)((E1 - E0) * (S - 1));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) segs += __shfl_down_sync(0xffffffffu, segs, o);
+  if ((threadIdx.x & 31) == 0 && segs) atomicAdd(&counters[CNT_SEGMENTS], segs);
+}
+
+// per query: its near angles in entry order (row 1 of the partials)
+__global__ void k_ff_near_sum(int32_t m, const unsigned long long* __restrict__ qoff,
+                              const double* __restrict__ slot_ang, double* __restrict__ row) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  double a = 0.0;
+  for (unsigned long long p = qoff[s]; p < qoff[s + 1]; ++p) a = __dadd_rn(a, slot_ang[p]);
+  row[s] = a;
+}
+
+// per host thread and device: the far-field pass buffers, grown on demand
+// (gwn_eval synchronises before returning, so the next eval reuses them)
+struct FFCache {
+  size_t cap_q = 0, cap_c = 0, cap_p = 0, cap_tmp = 0;
+  unsigned* qcnt = nullptr;              // (m+1)
+  unsigned long long* qoff = nullptr;    // (m+1)
+  unsigned* ecnt = nullptr;              // (C+1) counts, then fill cursors
+  unsigned* efill = nullptr;             // (C+1)
+  unsigned* tcnt = nullptr;              // (C+1)
+  unsigned long long* eoff = nullptr;    // (C+1)
+  unsigned long long* toff = nullptr;    // (C+1)
+  int2* recs = nullptr;                  // (pairs)
+  double* ang = nullptr;                 // (pairs)
+  void* tmp = nullptr;
+  unsigned long long* h = nullptr;       // pinned: [0] pairs, [1] tiles
+};
+static thread_local FFCache t_ffc[64];
+
+template <class T>
+static cudaError_t ff_grow(T*& p, size_t& cap, size_t n, size_t unit, cudaStream_t st) {
+  if (cap >= n) return cudaSuccess;
+  if (p) cudaFreeAsync(p, st);
+  p = nullptr;
+  cap = 0;
+  const size_t want = n + n / 4 + 1024;
+  cudaError_t e = cudaMallocAsync((void**)&p, want * unit, st);
+  if (e == cudaSuccess) cap = want;
+  return e;
+}
+
+static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int32_t m,
+                                      const int32_t* active, const double* pos, double* bpart,
+                                      int32_t* flags, unsigned long long* counters,
+                                      cudaStream_t st, const int32_t* order, cudaEvent_t* evb) {
+  FFCache& c = t_ffc[sc->device & 63];
+  const int32_t C = sc->ff_n;
+  const int64_t V = sc->n_edges * sc->S;
+  const int tp = kBlockQ * kQPT;
+  cudaError_t e = cudaSuccess;
+#define FC(x)                              \
+  do {                                     \
+    if ((e = (x)) != cudaSuccess) return e; \
+  } while (0)
+  if (!c.h) FC(cudaHostAlloc((void**)&c.h, 4 * sizeof(unsigned long long), cudaHostAllocPortable));
+  {
+    size_t capq = c.cap_q;
+    FC(ff_grow(c.qcnt, capq, (size_t)m + 1, sizeof(unsigned), st));
+    capq = c.cap_q;
+    FC(ff_grow(c.qoff, capq, (size_t)m + 1, sizeof(unsigned long long), st));
+    c.cap_q = capq;
+    size_t capc = c.cap_c;
+    FC(ff_grow(c.ecnt, capc, (size_t)C + 1, sizeof(unsigned), st));
+    capc = c.cap_c;
+    FC(ff_grow(c.efill, capc, (size_t)C + 1, sizeof(unsigned), st));
+    capc = c.cap_c;
+    FC(ff_grow(c.tcnt, capc, (size_t)C + 1, sizeof(unsigned), st));
+    capc = c.cap_c;
+    FC(ff_grow(c.eoff, capc, (size_t)C + 1, sizeof(unsigned long long), st));
+    capc = c.cap_c;
+    FC(ff_grow(c.toff, capc, (size_t)C + 1, sizeof(unsigned long long), st));
+    c.cap_c = capc;
+  }
+  size_t tb1 = 0, tb2 = 0;
+  FC(cub::DeviceScan::ExclusiveSum(nullptr, tb1, c.qcnt, c.qoff, m + 1, st));
+  FC(cub::DeviceScan::ExclusiveSum(nullptr, tb2, c.ecnt, c.eoff, C + 1, st));
+  FC(ff_grow(c.tmp, c.cap_tmp, std::max(tb1, tb2), 1, st));
+  const FFRound R{C, rd.ffg, sc->ff_r, sc->ff_lv, sc->ff_g,
+                  reinterpret_cast<const double2*>(sc->ff_D), sc->ff_chord, rd.ffa};
+  FC(cudaMemsetAsync(c.ecnt, 0, sizeof(unsigned) * (C + 1), st));
+  FC(cudaMemsetAsync(c.efill, 0, sizeof(unsigned) * (C + 1), st));
+  FC(cudaMemsetAsync(c.qcnt + m, 0, sizeof(unsigned), st));
+  const unsigned g = (unsigned)((m + kFFBlock - 1) / kFFBlock);
+  k_ff_count<<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, c.qcnt, c.ecnt, counters);
+  FC(cudaGetLastError());
+  FC(cub::DeviceScan::ExclusiveSum(c.tmp, tb1, c.qcnt, c.qoff, m + 1, st));
+  FC(cub::DeviceScan::ExclusiveSum(c.tmp, tb2, c.ecnt, c.eoff, C + 1, st));
+  k_ff_tiles<<<(C + 255) / 256, 256, 0, st>>>(C + 1, c.ecnt, tp, c.tcnt);
+  FC(cudaGetLastError());
+  FC(cub::DeviceScan::ExclusiveSum(c.tmp, tb2, c.tcnt, c.toff, C + 1, st));
+  // near-pair and tile totals to the host: they size the pair buffers and
+  // the exact kernel's grid (one round trip per round and chunk)
+  FC(cudaMemcpyAsync(c.h, c.qoff + m, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  FC(cudaMemcpyAsync(c.h + 1, c.toff + C, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     st));
+  FC(cudaStreamSynchronize(st));
+  const unsigned long long pairs = c.h[0], tiles = c.h[1];
+  {
+    size_t capp = c.cap_p;
+    FC(ff_grow(c.recs, capp, (size_t)pairs + 1, sizeof(int2), st));
+    capp = c.cap_p;
+    FC(ff_grow(c.ang, capp, (size_t)pairs + 1, sizeof(double), st));
+    c.cap_p = capp;
+  }
+  if (evb) FC(cudaEventRecord(evb[0], st));
+  k_ff_fill<<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, c.eoff, c.efill, c.recs,
+                                    bpart, counters);
+  FC(cudaGetLastError());
+  if (evb) FC(cudaEventRecord(evb[1], st));
+  if (tiles > 0) {
+    k_ff_near<kQPT><<<(unsigned)tiles, kBlockQ, 0, st>>>(
+        C, c.toff, c.eoff, sc->ff_eoff, c.recs, c.qoff, active, pos, rd.vproj, V, sc->S,
+        sc->band_h, rd.f, sc->dprm, c.ang, flags, counters);
+    FC(cudaGetLastError());
+  }
+  if (evb) FC(cudaEventRecord(evb[2], st));
+  k_ff_near_sum<<<(m + 255) / 256, 256, 0, st>>>(m, c.qoff, c.ang, bpart + m);
+  FC(cudaGetLastError());
+#undef FC
+  return cudaSuccess;
 }
 
 // Accuracy of rsqrt_nr against the correctly rounded 1/sqrt on a log-uniform
@@ -504,60 +900,42 @@ cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-#ifndef GWN_K4_QPT
-#define GWN_K4_QPT 2
-#endif
-constexpr int kQPT = GWN_K4_QPT;
+
 
 // Edge chunks of the boundary sum.  Fixed per scene (not per batch) so the
 // chunk partials -- added in chunk order by K5 -- make w bit-identical for any
-// batching, chunking or sharding of the queries; enough chunks that small
-// batches still fill the GPU.
+// batching, chunking or sharding; enough chunks that small batches still fill
+// the GPU.  Far-field scenes: two rows (far sum, near sum).
 int boundary_chunks(const gwn_scene* sc, int32_t m) {
   (void)m;
   if (sc->n_edges <= 0) return 1;
-  // exact edge chunks, then the far-field row (gwn_farfield.cu) when on
-  return (int)std::min<int64_t>(sc->n_edges, 64) + (sc->ff_n > 0 ? kFFRows : 0);
+  if (sc->ff_n > 0) return 2;
+  return (int)std::min<int64_t>(sc->n_edges, 64);
 }
 
-// nchunk partial rows: the exact kernel fills rows [0, nexact), the far
-// kernel the kFFRows rows after them (far-field scenes); `order` (nullable) is the exact
-// kernel's thread -> slot map (launch_ff_order).
+// nchunk partial rows.  `order` (nullable) is the far-field passes' thread ->
+// slot map (launch_ff_order); evb (nullable): 3 events recorded before the
+// far pass, after it and after the exact near kernel (timing mode).
 cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             const int32_t* active, const double* pos, double* bpart, int nchunk,
                             int32_t* flags, unsigned long long* counters, cudaStream_t st,
-                            const int32_t* order) {
+                            const int32_t* order, cudaEvent_t* evb) {
   if (m <= 0) return cudaSuccess;
   int64_t V = sc->n_edges * sc->S;
   if (V == 0) return cudaMemsetAsync(bpart, 0, sizeof(double) * m, st);
-  static const bool generic = getenv("GWN_K4_GENERIC") != nullptr;  // A/B switch
-  const bool ff = sc->ff_n > 0 && rd.ffg;
-  const int nexact = nchunk - (sc->ff_n > 0 ? kFFRows : 0);
-  dim3 grid((m + kBlockQ * kQPT - 1) / (kBlockQ * kQPT), nexact);
-  cudaError_t e = cudaSuccess;
-  if (sc->S <= kTileV && !generic) {
-    if (ff) {
-      const FFView fv{order, sc->ff_edge, rd.ffg, sc->ff_r};
-      k_boundary_e<kQPT, true><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S,
-                                                         sc->n_edges, sc->band_h, rd.f, sc->dprm,
-                                                         bpart, flags, counters, fv);
-      if ((e = cudaGetLastError()) != cudaSuccess) return e;
-      return launch_boundary_far(sc, rd, m, active, pos, bpart + (int64_t)nexact * m, counters,
-                                 st, order);
-    }
-    k_boundary_e<kQPT, false><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S,
-                                                        sc->n_edges, sc->band_h, rd.f, sc->dprm,
-                                                        bpart, flags, counters,
-                                                        FFView{nullptr, nullptr, nullptr, nullptr});
+  if (sc->ff_n > 0 && rd.ffg)
+    return launch_boundary_ff(sc, rd, m, active, pos, bpart, flags, counters, st, order, evb);
+  dim3 grid((m + kBlockQ * kQPT - 1) / (kBlockQ * kQPT), nchunk);
+  if (sc->S <= kTileV) {
+    k_boundary_e<kQPT><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S, sc->n_edges,
+                                                 sc->band_h, rd.f, sc->dprm, bpart, flags,
+                                                 counters);
   } else {
     k_boundary<kQPT><<<grid, kBlockQ, 0, st>>>(m, active, pos, rd.vproj, V, sc->S, sc->n_edges,
                                                sc->band_h, rd.f, sc->dprm, bpart, flags,
                                                counters);
   }
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (sc->ff_n > 0)  // exact path for everything: the far rows are zero
-    return cudaMemsetAsync(bpart + (int64_t)nexact * m, 0, sizeof(double) * m * kFFRows, st);
-  return cudaSuccess;
+  return cudaGetLastError();
 }
 
 // _kernels.single_loop_batch (_kernels.py:801-823) on the GPU: one closed loop,

@@ -17,7 +17,9 @@
 
 namespace gwn {
 
-constexpr int kMaxRoots = 8;
+// A line meets a bicubic patch in at most 2*3*3 = 18 points (Bezout), so the
+// record path never truncates a root set.
+constexpr int kMaxRoots = 18;
 constexpr int kDfsDepth = 12;   // levels below the start node before re-shooting
 constexpr int kDfsBudget = 512; // nodes per item before re-shooting
 
@@ -176,6 +178,31 @@ __device__ __forceinline__ void child_codes(uint64_t code, uint64_t& c0, uint64_
   }
 }
 
+// Append an accepted root unless it duplicates one already found
+// (surfaces.py:672-674: ray points closer than eps.dedup).
+template <bool kRecord>
+__device__ __forceinline__ void record_root(RootAcc<kRecord>& acc, const RootResult& r,
+                                            const DevParams& prm) {
+  for (int k = 0; k < acc.n; ++k)
+    if (fabs(acc.t[k] - r.t) < prm.dedup) return;
+  if (acc.n >= kMaxRoots) {  // more than Bezout's bound: only from a budget overrun
+    acc.flags |= FLAG_RESHOOT | FLAG_OVERFLOW;
+    return;
+  }
+  const int k = acc.n++;
+  acc.t[k] = r.t;
+  acc.chi += r.sign;
+  if (r.tang || r.graze) acc.flags |= FLAG_RESHOOT;
+  if (r.onsurf) acc.flags |= FLAG_ONSURF;
+  if constexpr (kRecord) {
+    acc.u[k] = r.u;
+    acc.v[k] = r.v;
+    acc.sign[k] = r.sign;
+    acc.tang[k] = r.tang;
+    acc.graze[k] = r.graze;
+  }
+}
+
 // All roots of one (query, patch) pair below the start node `start`
 // (0 = the whole patch), depth-first on one thread (single-ray all_hits).
 template <bool kRecord>
@@ -204,28 +231,37 @@ __device__ PairOut solve_pair(const double* __restrict__ P48, double qa, double 
     const int o = node_test(ctx, code, max_level, prm, r, owned);
     if (o == NODE_AMBIGUOUS) {
       acc.flags |= FLAG_RESHOOT;
+      if constexpr (kRecord) {
+        // An undecided node below the depth cap holds a near-tangent double
+        // root (silhouette fold).  The reference reports such a contact as a
+        // record with tangency set (surfaces.py:684-687,696), which makes the
+        // caller re-shoot: solve from the node centre and record the contact
+        // as tangent (node centre and t = C - p.d if Newton does not settle).
+        const int L = code_level(code);
+        const double wu = code_wu(L), wv = code_wv(L);
+        const double uc = ((double)code_iu(code) + 0.5) * wu;
+        const double vc = ((double)code_iv(code) + 0.5) * wv;
+        RootResult q = newton_solve(P48, qa, qb, qc, uc, vc, prm);
+        acc.newton += q.iters;
+        if (q.status != ROOT_ACCEPTED) {
+          double bu[4], dbu[4], bv[4], dbv[4], C, Cu, Cv;
+          bern3(uc, bu, dbu);
+          bern3(vc, bv, dbv);
+          eval_coord(P48 + 32, bu, dbu, bv, dbv, C, Cu, Cv);
+          q.u = uc;
+          q.v = vc;
+          q.t = C - qc;
+          q.sign = 1;
+          q.graze = 1;
+          if (q.t < -prm.t_tol) continue;
+        }
+        q.tang = 1;
+        record_root(acc, q, prm);
+      }
     } else if (o == NODE_ROOT) {
       acc.newton += r.iters;
       if (r.status != ROOT_ACCEPTED || !owned) continue;
-      bool dup = false;
-      for (int k = 0; k < acc.n; ++k) dup |= fabs(acc.t[k] - r.t) < prm.dedup;  // :672-674
-      if (dup) continue;
-      if (acc.n >= kMaxRoots) {
-        acc.flags |= FLAG_RESHOOT;
-        continue;
-      }
-      const int k = acc.n++;
-      acc.t[k] = r.t;
-      acc.chi += r.sign;
-      if (r.tang || r.graze) acc.flags |= FLAG_RESHOOT;
-      if (r.onsurf) acc.flags |= FLAG_ONSURF;
-      if constexpr (kRecord) {
-        acc.u[k] = r.u;
-        acc.v[k] = r.v;
-        acc.sign[k] = r.sign;
-        acc.tang[k] = r.tang;
-        acc.graze[k] = r.graze;
-      }
+      record_root(acc, r, prm);
     } else if (o == NODE_SPLIT) {
       uint64_t c0, c1;
       child_codes(code, c0, c1);

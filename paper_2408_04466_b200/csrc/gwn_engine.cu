@@ -73,8 +73,8 @@ __device__ __forceinline__ bool finalize_one(
         pos[3 * (int64_t)q + k] = __dadd_rn(q0[3 * (int64_t)q + k], __dmul_rn(jscale, v[k]));
       push = true;
     } else {
-      w_out[q] = w;
-      st_out[q] = (int8_t)reason;
+      w_out[q] = w;  // still on the surface / boundary after max_jitters
+      st_out[q] = GWN_STATUS_JITTER_EXHAUSTED;
     }
   } else if (f & (FLAG_RESHOOT | FLAG_BAND)) {
     if (round + 1 < max_rounds) {
@@ -393,11 +393,16 @@ using namespace gwn;
 
 // Round r of the scene (built on first use); the pointer stays valid for
 // the scene's lifetime (deque), taken under the scene mutex.
-static cudaError_t ensure_round(gwn_scene* sc, int r, cudaStream_t st, const Round** out) {
+static cudaError_t ensure_round(gwn_scene* sc, int r, cudaStream_t st, const Round** out,
+                                double* ms_build = nullptr) {
   std::lock_guard<std::mutex> lk(sc->mu);
   if ((int)sc->rounds.size() <= r) {
+    const auto t0 = std::chrono::steady_clock::now();
     const cudaError_t e = build_round(sc, r, st);
     if (e != cudaSuccess) return e;
+    if (ms_build)
+      *ms_build += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                       .count();
   }
   *out = &sc->rounds[r];
   return cudaSuccess;
@@ -439,12 +444,16 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   gwn_stats stats;
   memset(&stats, 0, sizeof stats);
   stats.queries = n;
-  cudaEvent_t ev[8] = {}, ev4[5] = {};
+  cudaEvent_t ev[8] = {}, ev4[5] = {}, evb[3] = {};
   int64_t launches = 0;
   // host buffers, large batches: chunks pipelined against the copies
   // (H2D of chunk k+1 and D2H of chunk k-1 overlap chunk k's rounds)
   const bool pipe = host && n >= (1ll << 18) && !sc->timed;
-  static thread_local cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  // copy streams per host thread AND device (a stream belongs to the device
+  // current at its creation)
+  static thread_local cudaStream_t t_cs_in[64] = {}, t_cs_out[64] = {};
+  cudaStream_t& cs_in = t_cs_in[sc->device & 63];
+  cudaStream_t& cs_out = t_cs_out[sc->device & 63];
   std::vector<cudaEvent_t> pev;  // per chunk: [2k] input copied, [2k+1] chunk done
   unsigned long long* d_cnt = nullptr;
   unsigned long long h_cnt[CNT_N];
@@ -455,7 +464,10 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     static thread_local int64_t* t_pinned = nullptr;
     static thread_local unsigned long long* t_map = nullptr;
     if (!t_pinned) {
-      CKE(cudaHostAlloc(&t_pinned, (kBlk + 1) * sizeof(int64_t), cudaHostAllocMapped));
+      // portable: one host thread may drive several devices (UVA gives the
+      // same device view on each)
+      CKE(cudaHostAlloc(&t_pinned, (kBlk + 1) * sizeof(int64_t),
+                        cudaHostAllocMapped | cudaHostAllocPortable));
       CKE(cudaHostGetDevicePointer((void**)&t_map, t_pinned, 0));
     }
     h_scalar = t_pinned;
@@ -479,6 +491,7 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   if (sc->timed) {
     for (auto& e : ev) CKE(cudaEventCreate(&e));
     for (auto& e : ev4) CKE(cudaEventCreate(&e));
+    for (auto& e : evb) CKE(cudaEventCreate(&e));
   }
   {
     int64_t cm = n < chunk_max ? n : chunk_max;
@@ -582,7 +595,7 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
       }
       for (int r = 0; r < sc->prm.max_rounds && m > 0;) {
         const Round* rdp = nullptr;
-        CKE(ensure_round(sc, r, st, &rdp));
+        CKE(ensure_round(sc, r, st, &rdp, &stats.ms_round_build));
         const Round& rd = *rdp;
         // candidate capacity from the scene's running estimate
         int64_t want = (int64_t)(sc->pairs_per_query * 1.25 * m) + 4096;
@@ -634,10 +647,11 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
           if (ff_sort && m >= 4096) {
             CKE(launch_ff_order(sc, m, active, rpos, ff_tmp, ff_order, st));
             ord = ff_order;
-            launches += 2;
+            launches += 1;  // Morton keys (+ a CUB sort)
           }
-          CKE(launch_boundary(sc, rd, m, active, rpos, bterm, nchunk, fl, d_cnt, st, ord));
-          launches += sc->ff_n > 0 ? 2 : 1;
+          CKE(launch_boundary(sc, rd, m, active, rpos, bterm, nchunk, fl, d_cnt, st, ord,
+                              sc->timed && sc->ff_n > 0 ? evb : nullptr));
+          launches += sc->ff_n > 0 ? 5 : 1;  // far-field: count, tiles, fill, near, near sum
         }
         if (sc->timed) CKE(cudaEventRecord(ev[3], st));
         // ---- K5: finalize / compact re-shoots (after the K3 side stream)
@@ -699,6 +713,12 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
           stats.ms_intersect += b;
           stats.ms_boundary += c;
           stats.ms_other += d;
+          if (sc->ff_n > 0 && nchunk > 0) {
+            cudaEventElapsedTime(&a, evb[0], evb[1]);
+            cudaEventElapsedTime(&b, evb[1], evb[2]);
+            stats.ms_k4_far += a;
+            stats.ms_k4_exact += b;
+          }
           if (sc->P > 0) {
             cudaEventElapsedTime(&a, ev4[0], ev4[1]);
             cudaEventElapsedTime(&b, ev4[1], ev4[2]);
@@ -737,12 +757,15 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   stats.roots = (int64_t)h_cnt[CNT_ROOTS];
   stats.boundary_segments = (int64_t)h_cnt[CNT_SEGMENTS];
   stats.far_pairs = (int64_t)h_cnt[CNT_FAR];
+  stats.far_terms = (int64_t)h_cnt[CNT_FAR_TERMS];
+  stats.near_pairs = (int64_t)h_cnt[CNT_NEAR];
   if (getenv("GWN_TRACE"))
     fprintf(stderr, "[gwn] fallback: max nodes/item %llu, slowest batch: %llu cycles tree %llu code %llu items %llu, max levels %llu\n",
             h_cnt[CNT_MAXNODES], h_cnt[CNT_BIGITEMS] >> 24, (h_cnt[CNT_BIGITEMS] >> 16) & 255, (h_cnt[CNT_BIGITEMS] >> 8) & 255, h_cnt[CNT_BIGITEMS] & 255, h_cnt[CNT_MAXLEVELS]);
   stats.kernel_launches = launches;
   {
     std::lock_guard<std::mutex> lk(sc->mu);
+    stats.rounds_built = (int64_t)sc->rounds.size();
     sc->stats = stats;
   }
   tl_mark(st, "outputs copied");
@@ -760,6 +783,8 @@ done:
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ev4)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : evb)
     if (e) cudaEventDestroy(e);
   tr.mark("done");
   if (g_tl) {
@@ -786,19 +811,28 @@ int eval_impl(gwn_scene* sc, const double* d_q, int64_t n, int64_t index_base,
 }  // namespace gwn
 
 extern "C" int gwn_all_hits(gwn_scene* sc, int64_t patch, const double origin[3],
-                            const double direction[3], double* t_out, double* uv_out,
-                            int32_t* sign_out, int8_t* tang_out, int8_t* graze_out, int32_t cap) {
+                            const double direction[3], const gwn_params* eps, double t_lo,
+                            double t_hi, double* t_out, double* uv_out, int32_t* sign_out,
+                            int8_t* tang_out, int8_t* graze_out, int32_t cap,
+                            int32_t* flags_out) {
   int rc = GWN_OK;
   double* d_out = nullptr;
   int32_t* d_cnt = nullptr;
   double* d_proj = nullptr;
-  int32_t cnt = 0;
-  double h[6 * 8];
+  int32_t cnt[2] = {0, 0};
+  constexpr int kRows = 18;  // Bezout bound of line x bicubic (gwn_dfs.cuh kMaxRoots)
+  double h[6 * kRows];
   Round rd;
-  if (!sc || patch < 0 || patch >= sc->P || !origin || !direction || cap < 0) {
+  gwn::DevParams prm;
+  if (!sc || patch < 0 || patch >= sc->P || !origin || !direction || cap < 0 ||
+      !(t_lo <= t_hi)) {
     set_error("gwn_all_hits: invalid arguments");
     return GWN_E_INVALID;
   }
+  prm = sc->dprm;
+  if (eps)  // the caller's EpsilonConfig (surfaces.py:587 `eps` argument)
+    prm = {eps->residual, eps->dedup, eps->tangent, eps->edge_graze, eps->degenerate,
+           eps->domain_tol, eps->t_tol, eps->on_surface_t, eps->band_factor};
   {
     double dd[3] = {direction[0], direction[1], direction[2]};
     double l = sqrt(dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]);
@@ -824,12 +858,12 @@ extern "C" int gwn_all_hits(gwn_scene* sc, int64_t patch, const double origin[3]
     CKE(cudaMemcpy(d_proj, P48, sizeof P48, cudaMemcpyHostToDevice));
   }
   CKE(cudaMalloc(&d_out, sizeof h));
-  CKE(cudaMalloc(&d_cnt, sizeof(int32_t)));
+  CKE(cudaMalloc(&d_cnt, sizeof cnt));
   rd.proj = d_proj;
-  CKE(launch_all_hits(sc, rd, 0, origin, d_out, d_cnt, 8, 0));
-  CKE(cudaMemcpy(&cnt, d_cnt, sizeof cnt, cudaMemcpyDeviceToHost));
+  CKE(launch_all_hits(rd, prm, origin, t_lo, t_hi, d_out, d_cnt, kRows, 0));
+  CKE(cudaMemcpy(cnt, d_cnt, sizeof cnt, cudaMemcpyDeviceToHost));
   CKE(cudaMemcpy(h, d_out, sizeof h, cudaMemcpyDeviceToHost));
-  for (int k = 0; k < cnt && k < cap && k < 8; ++k) {
+  for (int k = 0; k < cnt[0] && k < cap && k < kRows; ++k) {
     if (t_out) t_out[k] = h[6 * k];
     if (uv_out) {
       uv_out[2 * k] = h[6 * k + 1];
@@ -839,7 +873,8 @@ extern "C" int gwn_all_hits(gwn_scene* sc, int64_t patch, const double origin[3]
     if (tang_out) tang_out[k] = (int8_t)h[6 * k + 4];
     if (graze_out) graze_out[k] = (int8_t)h[6 * k + 5];
   }
-  rc = cnt;
+  if (flags_out) *flags_out = cnt[1];
+  rc = cnt[0];
 done:
   if (d_out) cudaFree(d_out);
   if (d_cnt) cudaFree(d_cnt);

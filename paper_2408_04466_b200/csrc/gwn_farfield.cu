@@ -172,22 +172,33 @@ static int ff_find(std::vector<int>& p, int a) {
 }
 
 void free_farfield(gwn_scene* sc) {
-  if (sc->ff_edge) cudaFree(sc->ff_edge);
   if (sc->ff_g) cudaFree(sc->ff_g);
   if (sc->ff_r) cudaFree(sc->ff_r);
   if (sc->ff_D) cudaFree(sc->ff_D);
   if (sc->ff_lv) cudaFree(sc->ff_lv);
   if (sc->ff_chord) cudaFree(sc->ff_chord);
+  if (sc->ff_eoff) cudaFree(sc->ff_eoff);
   sc->ff_lv = nullptr;
   sc->ff_chord = nullptr;
+  sc->ff_eoff = nullptr;
   sc->ff_chord_host.clear();
-  sc->ff_edge = nullptr;
   sc->ff_g = sc->ff_r = sc->ff_D = nullptr;
   sc->ff_n = 0;
+  sc->ff_expanded = 0;
   sc->ff_g_host.clear();
 }
 
 // ectrl: (n_edges, 4, 3) cubic edge nets on the host, sc->verts sampled.
+//
+// Every net edge ends up in exactly one *entry*, and the edges are permuted
+// (sc->verts, sc->band_h) so each entry's edges are contiguous:
+//   * a closed cycle whose expansion converges inside the scene: one
+//     expanded entry;
+//   * a cycle too large for that (a sheet's border): one sliver entry per
+//     edge (the edge closed by its chord) when the sliver expands, else the
+//     edge alone as an exact-only entry;
+//   * a cycle none of whose slivers expands: one exact-only entry.
+// Exact-only entries have R_min = +inf, so every query takes them exactly.
 cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   const char* env = getenv("GWN_FARFIELD");
   if (env && atoi(env) == 0) return cudaSuccess;
@@ -226,16 +237,17 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   const int C = (int)cyc_of_root.size();
   // per-cycle geometry from the sampled polyline (the vertices K4 sums)
   const int64_t V = ne * S;
-  std::vector<double> hv((size_t)(3 * V));
+  std::vector<double> hv((size_t)(3 * V)), hb((size_t)ne);
   cudaError_t err = cudaMemcpy(hv.data(), sc->verts, sizeof(double) * 3 * V,
                                cudaMemcpyDeviceToHost);
   if (err != cudaSuccess) return err;
-  // expansion entries: whole cycles, and for a cycle too large to be far
-  // from anything (a sheet's border) one sliver per edge -- the edge closed
-  // by its chord, whose exact chord term the far kernel adds back
+  if ((err = cudaMemcpy(hb.data(), sc->band_h, sizeof(double) * ne, cudaMemcpyDeviceToHost)) !=
+      cudaSuccess)
+    return err;
   struct Entry {
-    std::vector<int32_t> edges;
-    int32_t chord = -1;  // edge whose end points close the sliver, -1: a cycle
+    std::vector<int32_t> edges;  // original edge ids
+    bool sliver = false;         // the edge closed by its chord (edges.size() == 1)
+    bool expand = false;
     double g[3] = {0, 0, 0}, rho = 0, aabs = 0;
   };
   std::vector<std::vector<int32_t>> cyc_edges(C);
@@ -273,10 +285,10 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
           tri(v, w);
         }
       }
-    if (en.chord >= 0) {  // closing chord, last sample -> first
+    if (en.sliver) {  // closing chord, last sample -> first
       double a0[3], b0[3];
-      vtx((int64_t)en.chord * S + S - 1, a0);
-      vtx((int64_t)en.chord * S, b0);
+      vtx((int64_t)en.edges[0] * S + S - 1, a0);
+      vtx((int64_t)en.edges[0] * S, b0);
       tri(a0, b0);
     }
   };
@@ -293,48 +305,87 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   };
   static const bool all = getenv("GWN_FF_ALL") != nullptr;  // tests: expand every cycle
   std::vector<Entry> ents;
+  int n_exp = 0;
   for (int c = 0; c < C; ++c) {
     Entry en;
     en.edges = cyc_edges[c];
     geometry(en);
     if (en.rho > 0.0 && (all || rmin_of(en, kFFK) < 0.5 * sc->diag)) {
+      en.expand = true;
+      ++n_exp;
       ents.push_back(en);
       continue;
     }
-    for (int32_t e : cyc_edges[c]) {  // too large: per-edge slivers
+    std::vector<Entry> sl;  // too large: per-edge slivers
+    bool any = false;
+    for (int32_t e : cyc_edges[c]) {
       Entry sv;
       sv.edges = {e};
-      sv.chord = e;
+      sv.sliver = true;
       geometry(sv);
-      if (sv.rho > 0.0 && rmin_of(sv, kFFK) < 0.5 * sc->diag) ents.push_back(sv);
+      sv.expand = sv.rho > 0.0 && rmin_of(sv, kFFK) < 0.5 * sc->diag;
+      any |= sv.expand;
+      sl.push_back(sv);
+    }
+    if (!any) {  // exact only, as one entry
+      en.expand = false;
+      ents.push_back(en);
+      continue;
+    }
+    for (Entry& sv : sl) {
+      if (!sv.expand) sv.sliver = false;  // the edge alone, exact only
+      n_exp += sv.expand ? 1 : 0;
+      ents.push_back(sv);
     }
   }
   const int nk = (int)ents.size();
-  if (nk == 0) return cudaSuccess;
+  if (n_exp == 0) return cudaSuccess;  // nothing expands: the plain exact K4
+  // permute the edges so every entry is a contiguous edge range
+  std::vector<int32_t> perm;  // new edge k = old edge perm[k]
+  std::vector<int32_t> eoff(nk + 1, 0), chord(nk, -1);
+  for (int c = 0; c < nk; ++c) {
+    for (int32_t e : ents[c].edges) perm.push_back(e);
+    eoff[c + 1] = (int32_t)perm.size();
+    if (ents[c].sliver) chord[c] = eoff[c];
+  }
+  {
+    std::vector<double> nv((size_t)(3 * V)), nb((size_t)ne);
+    for (int64_t k = 0; k < ne; ++k) {
+      nb[k] = hb[perm[k]];
+      for (int d = 0; d < 3; ++d)
+        memcpy(&nv[(size_t)(d * V + k * S)], &hv[(size_t)(d * V + (int64_t)perm[k] * S)],
+               sizeof(double) * S);
+    }
+    hv.swap(nv);
+    hb.swap(nb);
+    if ((err = cudaMemcpy(sc->verts, hv.data(), sizeof(double) * 3 * V,
+                          cudaMemcpyHostToDevice)) != cudaSuccess)
+      return err;
+    if ((err = cudaMemcpy(sc->band_h, hb.data(), sizeof(double) * ne, cudaMemcpyHostToDevice)) !=
+        cudaSuccess)
+      return err;
+  }
   std::vector<double> r2, gk, lvr, chk(6 * (size_t)nk, 0.0);
-  std::vector<int32_t> fe(ne, -1), chord(nk, -1);
   std::vector<int64_t> coff(nk + 1, 0);
   std::vector<int32_t> cedge;
   for (int c = 0; c < nk; ++c) {
     const Entry& en = ents[c];
-    const double rmin = rmin_of(en, kFFK);
+    const double rmin = en.expand ? rmin_of(en, kFFK) : INFINITY;
     const double line = en.rho * (1.0 + 1e-6) + 1e-9 * (1.0 + sc->diag);
     r2.push_back(rmin * rmin);
     r2.push_back(line * line);
     for (int lv = 0; lv < kFFLevels; ++lv) {  // thresholds of the lower orders
-      const double rp = rmin_of(en, ff_order(lv));
+      const double rp = en.expand ? rmin_of(en, ff_order(lv)) : INFINITY;
       lvr.push_back(lv == kFFLevels - 1 ? rmin * rmin : rp * rp);
     }
     gk.insert(gk.end(), {en.g[0], en.g[1], en.g[2]});
-    for (int32_t e : en.edges) {
-      fe[e] = c;
-      cedge.push_back(e);
-    }
+    // moments only for expanded entries (exact-only ones keep an empty edge list)
+    if (en.expand)
+      for (int32_t k = eoff[c]; k < eoff[c + 1]; ++k) cedge.push_back(k);
     coff[c + 1] = (int64_t)cedge.size();
-    chord[c] = en.chord;
-    if (en.chord >= 0) {  // chord end points: first sample (start), last (end)
-      vtx((int64_t)en.chord * S, &chk[6 * c]);
-      vtx((int64_t)en.chord * S + S - 1, &chk[6 * c + 3]);
+    if (chord[c] >= 0) {  // chord end points: first sample (start), last (end)
+      vtx((int64_t)chord[c] * S, &chk[6 * c]);
+      vtx((int64_t)chord[c] * S + S - 1, &chk[6 * c + 3]);
     }
   }
   int64_t* d_coff = nullptr;
@@ -344,26 +395,29 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
     err = (x);                      \
     if (err != cudaSuccess) goto out; \
   } while (0)
-  FF(cudaMalloc(&sc->ff_edge, sizeof(int32_t) * ne));
   FF(cudaMalloc(&sc->ff_g, sizeof(double) * 3 * nk));
   FF(cudaMalloc(&sc->ff_r, sizeof(double) * 2 * nk));
   FF(cudaMalloc(&sc->ff_D, sizeof(double) * 2 * kFFTerms * nk));
+  FF(cudaMemset(sc->ff_D, 0, sizeof(double) * 2 * kFFTerms * nk));
   FF(cudaMalloc(&sc->ff_lv, sizeof(double) * kFFLevels * nk));
   FF(cudaMemcpy(sc->ff_lv, lvr.data(), sizeof(double) * kFFLevels * nk, cudaMemcpyHostToDevice));
+  FF(cudaMalloc(&sc->ff_eoff, sizeof(int32_t) * (nk + 1)));
+  FF(cudaMemcpy(sc->ff_eoff, eoff.data(), sizeof(int32_t) * (nk + 1), cudaMemcpyHostToDevice));
   FF(cudaMalloc(&d_coff, sizeof(int64_t) * (nk + 1)));
   FF(cudaMalloc(&d_cedge, sizeof(int32_t) * std::max<int64_t>(1, coff[nk])));
   FF(cudaMalloc(&sc->ff_chord, sizeof(int32_t) * nk));
   FF(cudaMemcpy(sc->ff_chord, chord.data(), sizeof(int32_t) * nk, cudaMemcpyHostToDevice));
-  FF(cudaMemcpy(sc->ff_edge, fe.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice));
   FF(cudaMemcpy(sc->ff_g, gk.data(), sizeof(double) * 3 * nk, cudaMemcpyHostToDevice));
   FF(cudaMemcpy(sc->ff_r, r2.data(), sizeof(double) * 2 * nk, cudaMemcpyHostToDevice));
   FF(cudaMemcpy(d_coff, coff.data(), sizeof(int64_t) * (nk + 1), cudaMemcpyHostToDevice));
-  FF(cudaMemcpy(d_cedge, cedge.data(), sizeof(int32_t) * coff[nk], cudaMemcpyHostToDevice));
+  if (coff[nk] > 0)
+    FF(cudaMemcpy(d_cedge, cedge.data(), sizeof(int32_t) * coff[nk], cudaMemcpyHostToDevice));
   k_ff_moments<<<nk, 256>>>(d_coff, d_cedge, sc->ff_chord, sc->verts, V, S, sc->ff_g, ff_quad(),
                             sc->ff_D);
   FF(cudaGetLastError());
   FF(cudaDeviceSynchronize());
   sc->ff_n = nk;
+  sc->ff_expanded = n_exp;
   sc->ff_g_host = gk;
   sc->ff_chord_host = chk;
 out:
@@ -372,121 +426,6 @@ out:
   if (d_cedge) cudaFree(d_cedge);
   if (err != cudaSuccess) free_farfield(sc);
   return err;
-}
-
-// Far kernel: one query per thread (Morton order when given), cycle group
-// blockIdx.y (kFFRows rows); far pairs add
-// Omega(p) = -sum_{n>=1} [Re(D_n^0 I_n^0) + 2 sum_{m>=1} Re(D_n^m I_n^m)]
-// to the lowest order P of ff_order() whose bound holds at the pair's
-// distance (I by upward recurrences, stable for |p - g| > rho).
-template <int P>
-__device__ __forceinline__ double ff_eval(double x, double y, double z,
-                                          const double2* __restrict__ Dc) {
-  const double ir2 = 1.0 / (x * x + y * y + z * z);
-  double dR = sqrt(ir2), dI = 0.0;  // I_0^0 = 1/r
-  double acc = 0.0;
-  // fully unrolled: every recurrence constant and D offset is an immediate
-#pragma unroll
-  for (int mm = 0; mm <= P; ++mm) {
-    if (mm > 0) {  // I_m^m = -(2m-1)(x+iy)/r^2 I_{m-1}^{m-1}
-      const double c0 = -(2.0 * mm - 1.0) * ir2;
-      const double nR = c0 * (x * dR - y * dI), nI = c0 * (x * dI + y * dR);
-      dR = nR;
-      dI = nI;
-    }
-    double aR = dR, aI = dI, bR = 0.0, bI = 0.0;
-    double col = 0.0;
-#pragma unroll
-    for (int n = mm; n <= P; ++n) {
-      if (n > mm) {  // I_n^m = ((2n-1) z I_{n-1}^m - ((n-1)^2 - m^2) I_{n-2}^m) / r^2
-        const double k1 = 2.0 * n - 1.0, k2 = (double)((n - 1) * (n - 1) - mm * mm);
-        const double vR = (k1 * z * aR - k2 * bR) * ir2, vI = (k1 * z * aI - k2 * bI) * ir2;
-        bR = aR;
-        bI = aI;
-        aR = vR;
-        aI = vI;
-      }
-      if (n == 0) continue;
-      const double2 d = __ldg(Dc + ff_term(n, mm));
-      col += d.x * aR - d.y * aI;
-    }
-    acc += mm == 0 ? col : 2.0 * col;
-  }
-  return -acc;
-}
-
-#ifndef GWN_FF_MINB
-#define GWN_FF_MINB 8
-#endif
-__global__ void __launch_bounds__(128, GWN_FF_MINB)
-k_boundary_far(int32_t m, const int32_t* __restrict__ order, const int32_t* __restrict__ active,
-               const double* __restrict__ pos, int32_t C, const double* __restrict__ ffg,
-               const double* __restrict__ ffr, const double* __restrict__ fflv,
-               const double* __restrict__ gw, const double* __restrict__ D,
-               const int32_t* __restrict__ chord, const double* __restrict__ ffa, Frame f,
-               double* __restrict__ brow, unsigned long long* __restrict__ counters) {
-  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = t < m;
-  const int32_t s = live ? (order ? order[t] : t) : 0;
-  const int32_t q = live ? (active ? active[s] : s) : 0;
-  const double px = live ? pos[3 * (int64_t)q] : 0.0, py = live ? pos[3 * (int64_t)q + 1] : 0.0,
-               pz = live ? pos[3 * (int64_t)q + 2] : 0.0;
-  double qa, qb, qc;
-  frame_q(f, px, py, pz, qa, qb, qc);
-  double om = 0.0;
-  unsigned long long nfar = 0;
-  const int c0 = (int)((int64_t)C * blockIdx.y / gridDim.y);
-  const int c1 = (int)((int64_t)C * (blockIdx.y + 1) / gridDim.y);
-  for (int c = c0; c < c1; ++c) {
-    if (!live || !ff_far(qa, qb, qc, ffg + 3 * c, ffr + 2 * c)) continue;
-    ++nfar;
-    const double x = px - __ldg(gw + 3 * c), y = py - __ldg(gw + 3 * c + 1),
-                 z = pz - __ldg(gw + 3 * c + 2);
-    const double R2 = x * x + y * y + z * z;
-    const double* lv = fflv + (int64_t)kFFLevels * c;
-    const double2* Dc = reinterpret_cast<const double2*>(D + (int64_t)c * 2 * kFFTerms);
-    static_assert(kFFLevels == 4, "ff_eval dispatch below covers four orders");
-    if (R2 > __ldg(lv)) om += ff_eval<ff_order(0)>(x, y, z, Dc);
-    else if (R2 > __ldg(lv + 1)) om += ff_eval<ff_order(1)>(x, y, z, Dc);
-    else if (R2 > __ldg(lv + 2)) om += ff_eval<ff_order(2)>(x, y, z, Dc);
-    else om += ff_eval<ff_order(3)>(x, y, z, Dc);
-    if (__ldg(chord + c) >= 0) {
-      // sliver: the edge's fan sum = Omega(edge + chord back) + the chord's
-      // forward fan term, K4's shifted form in the ray frame (den > 0: the
-      // line misses the sliver's sphere)
-      const double* A = ffa + 6 * (int64_t)c;
-      const double rax = __ldg(A) - qa, ray = __ldg(A + 1) - qb, raz = __ldg(A + 2) - qc;
-      const double rbx = __ldg(A + 3) - qa, rby = __ldg(A + 4) - qb, rbz = __ldg(A + 5) - qc;
-      const double ia = 1.0 / sqrt(rax * rax + ray * ray + raz * raz);
-      const double ib = 1.0 / sqrt(rbx * rbx + rby * rby + rbz * rbz);
-      const double uax = rax * ia, uay = ray * ia, uaz = fma(raz, ia, -1.0);
-      const double ubx = rbx * ib, uby = rby * ib, ubz = fma(rbz, ib, -1.0);
-      const double num = uay * ubx - uax * uby;
-      const double den = uax * ubx + uay * uby + uaz * ubz;
-      om += 2.0 * atan2(num, den);
-    }
-  }
-  // K4's partials are sums of atan2 (half angles): Omega / 2
-#ifdef GWN_FF_NOFAR
-  om = 0.0;
-#endif
-  if (live) brow[(int64_t)blockIdx.y * m + s] = 0.5 * om;
-  // far (query, cycle) pairs, one atomic per warp
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nfar += __shfl_down_sync(0xffffffffu, nfar, o);
-  if ((threadIdx.x & 31) == 0 && nfar) atomicAdd(&counters[CNT_FAR], nfar);
-}
-
-cudaError_t launch_boundary_far(const gwn_scene* sc, const Round& rd, int32_t m,
-                                const int32_t* active, const double* pos, double* brow,
-                                unsigned long long* counters, cudaStream_t st,
-                                const int32_t* order) {
-  if (m <= 0 || sc->ff_n <= 0) return cudaSuccess;
-  const dim3 grid((m + 127) / 128, kFFRows);
-  k_boundary_far<<<grid, 128, 0, st>>>(m, order, active, pos, sc->ff_n, rd.ffg, sc->ff_r,
-                                       sc->ff_lv, sc->ff_g, sc->ff_D, sc->ff_chord, rd.ffa,
-                                       rd.f, brow, counters);
-  return cudaGetLastError();
 }
 
 // 3-D Morton order of the round's queries (30-bit keys over the scene box

@@ -29,6 +29,7 @@ enum : int32_t {
   FLAG_BAND = 2,      // ray within the polyline/curve band of a net segment
   FLAG_ONSURF = 4,    // a hit with |t| <= on_surface_t -> jitter
   FLAG_DEGEN = 8,     // query on a boundary vertex -> jitter
+  FLAG_OVERFLOW = 16, // all_hits: root set larger than the record buffer
 };
 
 // device counters (index into a u64 array)
@@ -41,8 +42,10 @@ enum : int {
   CNT_MAXNODES = 5,  // max DFS nodes of one fallback item (diagnostic)
   CNT_BIGITEMS = 6,  // slowest fallback warp: cycles<<24 | tree levels<<16 | code levels<<8 | items
   CNT_MAXLEVELS = 7, // deepest fallback BFS, in levels (diagnostic)
-  CNT_FAR = 8,       // (query, cycle) pairs taken by the far-field expansion
-  CNT_N = 9,
+  CNT_FAR = 8,       // (query, entry) pairs taken by the far-field expansion
+  CNT_FAR_TERMS = 9, // solid-harmonic terms those expansions summed
+  CNT_NEAR = 10,     // (query, entry) pairs summed exactly (far-field scenes)
+  CNT_N = 11,
 };
 
 struct Frame {
@@ -130,12 +133,14 @@ struct gwn_scene {
   int32_t S = 0;
   double* verts = nullptr;      // (3,V) SoA, V = n_edges*S
   double* band_h = nullptr;     // (n_edges)
-  // far field of the boundary term (gwn_farfield.cu): closed cycles of the
-  // net boundary with a solid-harmonic expansion; ff_n = 0 when off
-  int32_t ff_n = 0;
-  int32_t* ff_edge = nullptr;   // (n_edges) cycle of each edge, -1 = exact only
-  double* ff_g = nullptr;       // (ff_n,3) cycle centre (world)
-  double* ff_r = nullptr;       // (ff_n,2) R_min^2, line radius^2
+  // far field of the boundary term (gwn_farfield.cu): the net edges are
+  // grouped into entries (closed cycles, slivers, exact-only pieces), each a
+  // contiguous edge range; ff_n = 0 when off
+  int32_t ff_n = 0;             // entries
+  int32_t ff_expanded = 0;      // entries with a multipole expansion
+  int32_t* ff_eoff = nullptr;   // (ff_n+1) edge range of each entry
+  double* ff_g = nullptr;       // (ff_n,3) entry centre (world)
+  double* ff_r = nullptr;       // (ff_n,2) R_min^2 (+inf: exact only), line radius^2
   double* ff_D = nullptr;       // (ff_n, kFFTerms, 2) double-layer moments
   double* ff_lv = nullptr;      // (ff_n, kFFLevels) R^2 thresholds of the adaptive orders
   int32_t* ff_chord = nullptr;  // (ff_n) sliver entries: edge of the closing chord, else -1
@@ -218,21 +223,18 @@ size_t query_order_scratch_bytes(int32_t m);
 cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             const int32_t* active, const double* pos, double* bpart, int nchunk,
                             int32_t* flags, unsigned long long* counters, cudaStream_t st,
-                            const int32_t* order = nullptr);                  // gwn_boundary.cu
+                            const int32_t* order = nullptr,
+                            cudaEvent_t* evb = nullptr);                      // gwn_boundary.cu
 int boundary_chunks(const gwn_scene* sc, int32_t m);  // partial rows (exact chunks + far row)
 cudaError_t build_farfield(gwn_scene* sc, const double* ectrl);     // gwn_farfield.cu
 void free_farfield(gwn_scene* sc);
-cudaError_t launch_boundary_far(const gwn_scene* sc, const Round& rd, int32_t m,
-                                const int32_t* active, const double* pos, double* brow,
-                                unsigned long long* counters, cudaStream_t st,
-                                const int32_t* order);
 cudaError_t launch_ff_order(const gwn_scene* sc, int32_t m, const int32_t* active,
                             const double* pos, void* scratch, int32_t* order, cudaStream_t st);
 size_t ff_order_scratch_bytes(int32_t m);
 cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st);  // gwn_boundary.cu
 cudaError_t selftest_rsqrt(int64_t n, unsigned long long* max_ulp_host);
-cudaError_t launch_all_hits(const gwn_scene* sc, const Round& rd, int64_t patch,
-                            const double* o, double* out, int32_t* count, int32_t cap,
+cudaError_t launch_all_hits(const Round& rd, const DevParams& prm, const double* o, double t_lo,
+                            double t_hi, double* out, int32_t* count, int32_t cap,
                             cudaStream_t st);
 cudaError_t launch_single_loop(const double* loop, int64_t B, const double* o, const double* d,
                                const double* hit_ts, const int64_t* hit_signs, int64_t H,

@@ -21,11 +21,15 @@
 
 namespace gwn {
 
-// patch.all_hits(ray) for one ray and one patch (host API, surfaces.py:587-589):
-// out rows = (t, u, v, sign, tangency, grazing), sorted by t (surfaces.py:700).
+// patch.all_hits(ray, t_window, eps) for one ray and one patch (host API,
+// surfaces.py:587-589): out rows = (t, u, v, sign, tangency, grazing) of the
+// roots inside the t window (+-1e-12, surfaces.py:679), sorted by t
+// (surfaces.py:700).  *count = number of such roots (rows past `cap` are not
+// written); *flags = the root set's flag bits (FLAG_RESHOOT for tangent /
+// grazing / undecided contacts).
 __global__ void k_all_hits(const double* __restrict__ P48, Frame f, double ox, double oy,
-                           double oz, DevParams prm, double* __restrict__ out,
-                           int32_t* __restrict__ count, int32_t cap) {
+                           double oz, DevParams prm, double t_lo, double t_hi,
+                           double* __restrict__ out, int32_t* __restrict__ count, int32_t cap) {
   double qa = ox * f.e1[0] + oy * f.e1[1] + oz * f.e1[2];
   double qb = ox * f.e2[0] + oy * f.e2[1] + oz * f.e2[2];
   double qc = ox * f.d[0] + oy * f.d[1] + oz * f.d[2];
@@ -39,19 +43,25 @@ __global__ void k_all_hits(const double* __restrict__ P48, Frame f, double ox, d
     while (j >= 0 && acc.t[idx[j]] > acc.t[key]) { idx[j + 1] = idx[j]; --j; }
     idx[j + 1] = key;
   }
-  for (int k = 0; k < acc.n && k < cap; ++k) {
-    int q = idx[k];
-    double* row = out + 6 * k;
-    row[0] = acc.t[q]; row[1] = acc.u[q]; row[2] = acc.v[q];
-    row[3] = acc.sign[q]; row[4] = acc.tang[q]; row[5] = acc.graze[q];
+  int m = 0;
+  for (int k = 0; k < acc.n; ++k) {
+    const int q = idx[k];
+    if (acc.t[q] < t_lo - 1e-12 || acc.t[q] > t_hi + 1e-12) continue;  // surfaces.py:679
+    if (m < cap) {
+      double* row = out + 6 * m;
+      row[0] = acc.t[q]; row[1] = acc.u[q]; row[2] = acc.v[q];
+      row[3] = acc.sign[q]; row[4] = acc.tang[q]; row[5] = acc.graze[q];
+    }
+    ++m;
   }
-  *count = (acc.flags & FLAG_RESHOOT) && acc.n == 0 ? 0 : acc.n;
+  count[0] = m;
+  count[1] = acc.flags;
 }
 
-cudaError_t launch_all_hits(const gwn_scene* sc, const Round& rd, int64_t patch,
-                            const double* o, double* out, int32_t* count, int32_t cap,
+cudaError_t launch_all_hits(const Round& rd, const DevParams& prm, const double* o, double t_lo,
+                            double t_hi, double* out, int32_t* count, int32_t cap,
                             cudaStream_t st) {
-  k_all_hits<<<1, 1, 0, st>>>(rd.proj + 48 * patch, rd.f, o[0], o[1], o[2], sc->dprm, out, count,
+  k_all_hits<<<1, 1, 0, st>>>(rd.proj, rd.f, o[0], o[1], o[2], prm, t_lo, t_hi, out, count,
                               cap);
   return cudaGetLastError();
 }

@@ -467,6 +467,12 @@ k3_newton(WaveArgs w, int32_t P) {
     it = nx;
     base = nbase;
   }
+  // Programmatic dependent of k3_fallback (which triggers on entry): wait for
+  // the fallback grid here, after the work loop, so Newton keeps its overlap
+  // with it and Newton's completion implies the fallback's (its chi / flag
+  // atomics are then ordered before K4, K5 and the next round by stream
+  // order).  A no-op when launched without the attribute.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   warp_sum_u64(&w.counters[CNT_NEWTON], iters);
   warp_sum_u64(&w.counters[CNT_ROOTS], roots);
 }
@@ -533,8 +539,12 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
   // The fallback (few, latency-bound items) runs on a side stream,
   // concurrently with the Newton pass and K4; the engine joins it (`join`)
   // before K5 reads the accumulators.
-  static thread_local cudaStream_t side = nullptr;
-  static thread_local cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // per host thread and device (streams and events belong to one device)
+  static thread_local cudaStream_t t_side[64] = {};
+  static thread_local cudaEvent_t t_fork[64] = {}, t_join[64] = {};
+  cudaStream_t& side = t_side[sc->device & 63];
+  cudaEvent_t& fork_ev = t_fork[sc->device & 63];
+  cudaEvent_t& join_ev = t_join[sc->device & 63];
   if (!side) {
     // high priority: the fallback's blocks are dispatched ahead of the Newton
     // pass's, so its long dependent chains start first (GWN_FB_PRIO=0: off)

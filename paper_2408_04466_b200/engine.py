@@ -23,7 +23,8 @@ import numpy as np
 from . import _lib
 from . import config as cfg
 from .config import DEFAULT_EPS, EpsilonConfig
-from .errors import STATUS_ERRORS, STATUS_OK, GridMismatch, SceneError, SeedExhausted
+from .errors import (STATUS_ERRORS, STATUS_EXHAUSTED, STATUS_JITTER_EXHAUSTED, STATUS_OK,
+                     DegenerateProjection, GridMismatch, SceneError, SeedExhausted)
 from .geometry import Aabb, Ray
 
 
@@ -64,13 +65,7 @@ class Scene:
         if device is None:
             device = _current_device()
         self.device = device
-        p = _lib.default_params()
-        p.residual = eps.residual
-        p.dedup = eps.dedup
-        p.tangent = eps.tangent_parametric
-        p.edge_graze = eps.edge_graze
-        p.degenerate = eps.degenerate
-        p.jitter_scale = eps.jitter_scale
+        p = _lib.params_from_eps(eps)
         p.samples_per_edge = samples_per_edge
         p.max_rounds = max_rounds
         p.max_jitters = max_jitters
@@ -139,12 +134,28 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
+def _check_out(torch, w, st, n: int, device) -> None:
+    """Caller-owned outputs are written through raw pointers: reject anything
+    the library could write past or across."""
+    if w.dtype != torch.float64 or st.dtype != torch.int8:
+        raise ValueError("out=(w, status) must be float64 and int8 tensors")
+    if w.numel() < n or st.numel() < n:
+        raise ValueError(f"out tensors hold {w.numel()}/{st.numel()} elements, need {n}")
+    if not (w.is_contiguous() and st.is_contiguous()):
+        raise ValueError("out tensors must be contiguous")
+    if w.device != device or st.device != device:
+        raise ValueError(f"out tensors must live on {device} like the queries")
+
+
 def winding_numbers(scene: Scene, queries, *, index_base: int = 0, stream=None,
                     out=None, return_status: bool = True):
     """Generalized winding numbers of many query points (one ``gwn_eval``).
 
     Returns ``(w, status)``; ``status`` codes: 0 ok, 1 on-surface (jittered),
-    2 re-shoot budget exhausted, 3 degenerate projection (jittered).
+    2 re-shoot budget exhausted, 3 degenerate projection (jittered), 4 still
+    on the surface / boundary after the jitter budget (w unreliable).
+    ``out=(w, status)``: caller-owned outputs (float64 / int8, at least n
+    elements, contiguous, on the queries' device).
     """
     L = _lib.lib()
     if _is_torch(queries):
@@ -154,14 +165,15 @@ def winding_numbers(scene: Scene, queries, *, index_base: int = 0, stream=None,
             raise ValueError("queries must be an (n,3) float64 tensor")
         q = q.contiguous()
         n = q.shape[0]
+        if q.is_cuda and q.device.index != scene.device:
+            raise ValueError(f"queries on cuda:{q.device.index}, scene on cuda:{scene.device}")
         if out is not None:
             w, st = out
+            _check_out(torch, w, st, n, q.device)
         else:
             w = torch.empty(n, dtype=torch.float64, device=q.device)
             st = torch.empty(n, dtype=torch.int8, device=q.device)
         flags = 0 if q.is_cuda else _lib.GWN_HOST_BUFFERS
-        if q.is_cuda and (not w.is_cuda or not st.is_cuda):
-            raise ValueError("device queries need device outputs")
         if stream is None and q.is_cuda:
             stream = torch.cuda.current_stream(q.device).cuda_stream
         _lib.check(L.gwn_eval(scene.handle, C.c_void_p(q.data_ptr()), n, index_base,
@@ -172,8 +184,20 @@ def winding_numbers(scene: Scene, queries, *, index_base: int = 0, stream=None,
     if q.ndim != 2 or q.shape[1] != 3:
         raise ValueError("queries must have shape (n, 3)")
     n = q.shape[0]
-    w = np.empty(n, np.float64)
-    st = np.empty(n, np.int8)
+    if out is not None:
+        w, st = out
+        if not (isinstance(w, np.ndarray) and isinstance(st, np.ndarray)):
+            raise ValueError("numpy queries need numpy out=(w, status) arrays")
+        if w.dtype != np.float64 or st.dtype != np.int8 or w.ndim != 1 or st.ndim != 1:
+            raise ValueError("out=(w, status) must be 1-D float64 and int8 arrays")
+        if w.size < n or st.size < n:
+            raise ValueError(f"out arrays hold {w.size}/{st.size} elements, need {n}")
+        if not (w.flags.c_contiguous and st.flags.c_contiguous and w.flags.writeable
+                and st.flags.writeable):
+            raise ValueError("out arrays must be writeable and contiguous")
+    else:
+        w = np.empty(n, np.float64)
+        st = np.empty(n, np.int8)
     _lib.check(L.gwn_eval(scene.handle, C.c_void_p(q.ctypes.data), n, index_base,
                           C.c_void_p(w.ctypes.data), C.c_void_p(st.ctypes.data),
                           _lib.GWN_HOST_BUFFERS, C.c_void_p(stream or 0)), "gwn_eval")
@@ -183,11 +207,14 @@ def winding_numbers(scene: Scene, queries, *, index_base: int = 0, stream=None,
 def winding_number(scene: Scene, p) -> float:
     """w(p).  On-surface / degenerate queries are jittered
     by ``jitter_scale * diag`` (at most 3 times) with a warning; an exhausted
-    re-shoot budget raises :class:`SeedExhausted`."""
+    re-shoot budget raises :class:`SeedExhausted`, a query still on the
+    surface after the jitter budget :class:`DegenerateProjection`."""
     w, st = winding_numbers(scene, np.asarray(p, dtype=np.float64).reshape(1, 3))
     code = int(st[0])
-    if code == 2:
+    if code == STATUS_EXHAUSTED:
         raise SeedExhausted(f"every ray from {p} was tangent / grazing")
+    if code == STATUS_JITTER_EXHAUSTED:
+        raise DegenerateProjection(f"{p} stayed on the surface after every jitter")
     if code != STATUS_OK:
         warnings.warn(f"query {p}: {STATUS_ERRORS[code].__name__}; evaluated at a jittered point")
     return float(w[0])

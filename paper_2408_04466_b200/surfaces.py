@@ -124,28 +124,39 @@ class BicubicPatch:
 
     def all_hits(self, ray: Ray, t_window=(0.0, np.inf),
                  eps: EpsilonConfig = DEFAULT_EPS) -> list[IntersectionRecord]:
+        """Every hit of ``ray`` with the patch inside ``t_window``, sorted by t
+        (surfaces.py:587-589, body :634-701), from the GPU root enumerator.
+        ``eps`` is forwarded to the device (residual, dedup, tangency,
+        grazing and degeneracy thresholds).  A near-tangent contact the
+        subdivision cannot separate comes back as a tangent record, the
+        reference's signal to re-shoot."""
         t_lo, t_hi = t_window
         if t_lo < 0.0:
             raise ValueError("t window must start at 0 or later")
+        if not t_lo <= t_hi:
+            raise ValueError("empty t window")
         sc = self._device_scene()
-        cap = 8
+        cap = 18  # Bezout: a line meets a bicubic patch at most 2*3*3 times
         t = np.zeros(cap)
         uv = np.zeros(2 * cap)
         sg = np.zeros(cap, np.int32)
         tg = np.zeros(cap, np.int8)
         gz = np.zeros(cap, np.int8)
+        flags = C.c_int32(0)
         o = np.ascontiguousarray(ray.origin, dtype=np.float64)
         d = np.ascontiguousarray(ray.direction, dtype=np.float64)
         dp = C.POINTER(C.c_double)
+        prm = _lib.params_from_eps(eps)
         n = _lib.check(_lib.lib().gwn_all_hits(
-            sc.handle, 0, o.ctypes.data_as(dp), d.ctypes.data_as(dp), t.ctypes.data_as(dp),
+            sc.handle, 0, o.ctypes.data_as(dp), d.ctypes.data_as(dp), C.byref(prm),
+            float(t_lo), float(t_hi), t.ctypes.data_as(dp),
             uv.ctypes.data_as(dp), sg.ctypes.data_as(C.POINTER(C.c_int32)),
-            tg.ctypes.data_as(C.POINTER(C.c_int8)), gz.ctypes.data_as(C.POINTER(C.c_int8)), cap),
-            "gwn_all_hits")
+            tg.ctypes.data_as(C.POINTER(C.c_int8)), gz.ctypes.data_as(C.POINTER(C.c_int8)), cap,
+            C.byref(flags)), "gwn_all_hits")
+        if n > cap:  # cannot happen below Bezout's bound; never truncate silently
+            raise RuntimeError(f"all_hits: {n} roots exceed the {cap}-record buffer")
         out = []
-        for k in range(min(n, cap)):
-            if t[k] < t_lo - 1e-12 or t[k] > t_hi + 1e-12:   # surfaces.py:679
-                continue
+        for k in range(n):
             u, v = uv[2 * k], uv[2 * k + 1]
             fu, fv = self.partials(u, v)
             nrm = np.cross(fu, fv)

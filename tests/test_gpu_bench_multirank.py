@@ -34,7 +34,7 @@ def test_bench_sharded_gather_equals_full_eval(world):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port",
            str(_port()), os.path.join(REPO, "bench.py"), "--gpus", str(world), "--steps", "3",
-           "--warmup", "3", "--no-ray-reuse", "--no-far-field", "--no-cpu-baseline",
+           "--warmup", "3", "--config", "2", "--no-extras", "--no-cpu-baseline",
            "--queries", "65537"]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=REPO)
     assert r.returncode == 0, r.stderr[-2000:]
