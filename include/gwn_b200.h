@@ -16,19 +16,21 @@
  *   gwn_eval_rays      SPEC.md:381-407 winding_numbers_along_ray / slice /
  *                      voxelize: one intersection pass per ray, reused by
  *                      every point on it (ray reuse)
- *   gwn_solid_angle_many, gwn_ray_tris_hits, gwn_arc_crossings
- *                      the rest of the kernel dispatch layer
- *                      (_kernels.py:170, :366, :443, :466): mesh solid
- *                      angles, ray/mesh all-hits, great-circle arc crossings
+ *   gwn_solid_angle_many, gwn_ray_tris_hits
+ *                      the mesh kernels of the dispatch layer
+ *                      (_kernels.py:366, :443, :466): mesh solid angles and
+ *                      ray/mesh all-hits
  *   gwn_single_loop_batch
  *                      _kernels.single_loop_batch (_kernels.py:801-823): the
  *                      kernel dispatch layer's ray-reuse boundary kernel
  *   gwn_last_error     error text; negative return codes map to the
  *                      GwnError hierarchy (errors.py:9-90) in the wrapper
  *
- * Threading: a scene is immutable after creation; gwn_eval is
- * reentrant on distinct streams (workspace comes from the stream-ordered
- * allocator).  gwn_last_error is thread-local.
+ * Threading: a scene is immutable after creation.  gwn_eval
+ * may run concurrently from distinct host threads (its workspace is a
+ * per-host-thread, per-device cache grown on demand, and each call
+ * synchronises its stream before returning).  gwn_last_error is
+ * thread-local.
  */
 #ifndef GWN_B200_H
 #define GWN_B200_H
@@ -220,17 +222,6 @@ int64_t gwn_ray_tris_hits(const gwn_tri_bvh* bvh, const double* origins, const d
                           int64_t R, double t_lo, double t_hi, double tang_eps,
                           double plane_tol, int64_t* offs, double* ts, int64_t* tris,
                           double* dotdn, double* us, double* vs, int64_t cap, int device);
-
-/* arc_crossings (_kernels.py:170-190, numpy twin :119-167): transversal
- * crossings between great-circle arcs i < j (chain neighbours skipped),
- * sorted by (i, j) with the +d crossing before -d; coplanar pairs sorted by
- * (i, j) into cop_i/cop_j (*n_cop).  Returns the crossing count; outputs
- * are written only when both counts are <= cap.  Negative on error. */
-int64_t gwn_arc_crossings(const double* S, const double* E, const double* P, const double* L,
-                          const int64_t* prev_idx, const int64_t* next_idx, int64_t B,
-                          double on_tol, double cop_tol, int64_t* pair_i, int64_t* pair_j,
-                          double* points, int64_t* cop_i, int64_t* cop_j, int64_t* n_cop,
-                          int64_t cap, int device);
 
 /* Host-side helpers shared with the oracle contract (no device needed). */
 void gwn_direction(uint64_t seed, int32_t round, double d[3]);

@@ -7,7 +7,6 @@ pkg/src/gwn/_kernels.py:45):
   * solid_angle_sum       _kernels.py:422-440 (_solid_angle_numpy), :443-451
   * ray_tris_hits         _kernels.py:312-363 (_ray_tris_hits_numpy), the
                           brute-force twin of bvh_ray_all_hits :366-381
-  * arc_crossings         _kernels.py:119-167 (_arc_crossings_numpy), :170-190
 
 Parity pinned by tests/test_oracle_golden.py against tests/golden/mesh.npz,
 which tests/golden/make_golden_mesh.py generates by running the reference.
@@ -96,41 +95,3 @@ def bvh_arrays(V, T):
                                np.einsum("ij,ij->i", p1 - cent, p1 - cent)),
                     np.einsum("ij,ij->i", p2 - cent, p2 - cent))
     return p0, e1, e2, nn, nh, cent, r2
-
-
-def arc_crossings(S, E, P, L, prev_idx, next_idx, on_tol, cop_tol):
-    """Crossings (i, j, point) sorted by (i, j), +d before -d; coplanar
-    pairs by (i, j) -- _kernels.py:119-167 plus the lexsort of :186-189."""
-    S, E, P = (np.asarray(x, np.float64) for x in (S, E, P))
-    L = np.asarray(L, np.float64)
-    B = len(S)
-    side = 1e-12
-    ds = S @ P.T
-    de = E @ P.T
-    one_side = ((ds > side) & (de > side)) | ((ds < -side) & (de < -side))
-    cand = ~(one_side | one_side.T)
-    xi, xj, xp, ci, cj = [], [], [], [], []
-    for i in range(B):
-        for j in range(i + 1, B):
-            if not cand[i, j] or j == next_idx[i] or j == prev_idx[i]:
-                continue
-            d = np.cross(P[i], P[j])
-            nd = math.sqrt(d @ d)
-            if nd < cop_tol:
-                ci.append(i)
-                cj.append(j)
-                continue
-            d = d / nd
-            for c in (d, -d):
-                phi_i = math.atan2(np.cross(S[i], c) @ P[i], S[i] @ c)
-                if phi_i < -on_tol or phi_i > L[i] + on_tol:
-                    continue
-                phi_j = math.atan2(np.cross(S[j], c) @ P[j], S[j] @ c)
-                if phi_j < -on_tol or phi_j > L[j] + on_tol:
-                    continue
-                xi.append(i)
-                xj.append(j)
-                xp.append(c)
-    return (np.asarray(xi, np.int64), np.asarray(xj, np.int64),
-            np.asarray(xp, np.float64).reshape(-1, 3), np.asarray(ci, np.int64),
-            np.asarray(cj, np.int64))

@@ -8,7 +8,10 @@ that module has the same call signature here, backed by libgwn_b200.so:
   solid_angle_sum     (:443)  gwn_solid_angle_many (one point)
   solid_angle_many    (:466)  gwn_solid_angle_many
   bvh_ray_all_hits    (:366)  gwn_ray_tris_hits (one ray; ray_tris_hits_batch for R)
-  arc_crossings       (:170)  gwn_arc_crossings
+
+arc_crossings (:170) is the generic spherical arrangement's primitive, which
+the arrangement-free fan formula supersedes (out of scope); it
+has no GPU backend here.
 
 Contiguous float64/int64 in, fresh arrays out, per-element flags instead of
 exceptions; the numpy twins' semantics (the numba kernels share the broken
@@ -148,28 +151,3 @@ def bvh_ray_all_hits(bvh, origin, direction, t_lo, t_hi, tang_eps, plane_tol, de
         bvh, np.asarray(origin, np.float64).reshape(1, 3),
         np.asarray(direction, np.float64).reshape(1, 3), t_lo, t_hi, tang_eps, plane_tol, device)
     return ts, tris, dd, us, vs
-
-
-def arc_crossings(S, E, P, L, prev_idx, next_idx, on_tol, cop_tol, device: int = 0):
-    """All transversal crossings between arcs i < j, skipping chain
-    neighbours (_kernels.py:170-190): ``(pair_i, pair_j, points, coplanar_i,
-    coplanar_j)``, crossings sorted by (i, j)."""
-    S = _f64(S, (-1, 3)); E = _f64(E, (-1, 3)); P = _f64(P, (-1, 3)); L = _f64(L)
-    pv = _i64(prev_idx); nx = _i64(next_idx)
-    B = len(S)
-    cap = 8 * B + 64
-    ncop = C.c_int64(0)
-    while True:
-        pi = np.empty(max(cap, 1), np.int64); pj = np.empty(max(cap, 1), np.int64)
-        pts = np.empty((max(cap, 1), 3)); ci = np.empty(max(cap, 1), np.int64)
-        cj = np.empty(max(cap, 1), np.int64)
-        n = _lib.check(_lib.lib().gwn_arc_crossings(
-            _p(S), _p(E), _p(P), _p(L), _p(pv, C.c_int64), _p(nx, C.c_int64), B,
-            float(on_tol), float(cop_tol), _p(pi, C.c_int64), _p(pj, C.c_int64), _p(pts),
-            _p(ci, C.c_int64), _p(cj, C.c_int64), C.byref(ncop), cap, device),
-            "gwn_arc_crossings")
-        if n <= cap and ncop.value <= cap:
-            break
-        cap = max(n, ncop.value)
-    m = ncop.value
-    return pi[:n], pj[:n], pts[:n], ci[:m], cj[:m]

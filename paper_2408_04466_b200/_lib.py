@@ -33,7 +33,7 @@ EXPORTS = (
     "gwn_scene_destroy", "gwn_scene_info_get", "gwn_eval", "gwn_stats_get", "gwn_set_timing",
     "gwn_all_hits", "gwn_single_loop_batch", "gwn_direction", "gwn_jitter_dir",
     "gwn_net_boundary", "gwn_fp64_peak", "gwn_selftest_rsqrt", "gwn_eval_rays",
-    "gwn_solid_angle_many", "gwn_ray_tris_hits", "gwn_arc_crossings",
+    "gwn_solid_angle_many", "gwn_ray_tris_hits",
 )
 
 
@@ -137,9 +137,6 @@ def lib() -> C.CDLL:
                                         C.c_double, C.c_double, C.c_double, ip, dp, ip, dp,
                                         dp, dp, C.c_int64, C.c_int]
         L.gwn_ray_tris_hits.restype = C.c_int64
-        L.gwn_arc_crossings.argtypes = [dp, dp, dp, dp, ip, ip, C.c_int64, C.c_double,
-                                        C.c_double, ip, ip, dp, ip, ip, ip, C.c_int64, C.c_int]
-        L.gwn_arc_crossings.restype = C.c_int64
         _lib = L
     return _lib
 

@@ -1,6 +1,7 @@
 // gwn_mesh.cu -- the rest of the reference's kernel dispatch layer
 // (pkg/src/gwn/_kernels.py) on the B200: triangle-mesh solid-angle sums,
-// all-hits ray/mesh intersection and great-circle arc crossings.
+// and all-hits ray/mesh intersection.  (Great-circle arc crossings, the
+// generic arrangement's primitive, are out of scope: SURVEY.md §2.)
 //
 // Semantics follow the reference's numpy twins, which are correct; the
 // numba kernels share the broken _cross helper (_kernels.py:45).
@@ -19,9 +20,6 @@
 //     fill pass, then one radix sort of (ray, kind, triangle) puts every
 //     ray's hits in the numpy twin's order (regular hits by triangle, then
 //     parallel contacts by triangle).
-//   * arc_crossings (_kernels.py:119-190, numpy twin): all arc pairs i < j,
-//     one thread per pair, appended then radix-sorted by (i, j, sign) --
-//     the twin's lexsort((pj, pi)) order; coplanar pairs by (i, j).
 #include <cub/cub.cuh>
 
 #include <math.h>
@@ -287,84 +285,6 @@ __global__ void k_iota(int64_t n, int64_t* __restrict__ x) {
   if (i < n) x[i] = i;
 }
 
-// ---------------------------------------------------------------------------
-// arc crossings
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ double dot3(const double* a, const double* b) {
-  return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
-}
-
-// atan2(cross(s, c) . p, s . c): angle of c along the circle with pole p
-__device__ __forceinline__ double angle_on(const double* s, const double* p, const double* c) {
-  const double x = s[1] * c[2] - s[2] * c[1], y = s[2] * c[0] - s[0] * c[2],
-               z = s[0] * c[1] - s[1] * c[0];
-  return atan2(x * p[0] + y * p[1] + z * p[2], dot3(s, c));
-}
-
-__global__ void k_arc_pairs(const double* __restrict__ S, const double* __restrict__ E,
-                            const double* __restrict__ Pl, const double* __restrict__ L,
-                            const int64_t* __restrict__ prv, const int64_t* __restrict__ nxt,
-                            int64_t B, double on_tol, double cop_tol,
-                            unsigned long long* __restrict__ n_x,
-                            unsigned long long* __restrict__ xkey, double* __restrict__ xpt,
-                            unsigned long long* __restrict__ n_c,
-                            unsigned long long* __restrict__ ckey, unsigned long long cap) {
-  const int64_t i = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B || j >= B || j <= i) return;
-  if (j == nxt[i] || j == prv[i]) return;
-  const double side = 1e-12;
-  const double *Si = S + 3 * i, *Ei = E + 3 * i, *Pi = Pl + 3 * i;
-  const double *Sj = S + 3 * j, *Ej = E + 3 * j, *Pj = Pl + 3 * j;
-  // both arcs must straddle the other's plane (:130-134)
-  const double dsj = dot3(Sj, Pi), dej = dot3(Ej, Pi);
-  if ((dsj > side && dej > side) || (dsj < -side && dej < -side)) return;
-  const double dsi = dot3(Si, Pj), dei = dot3(Ei, Pj);
-  if ((dsi > side && dei > side) || (dsi < -side && dei < -side)) return;
-  double dx = Pi[1] * Pj[2] - Pi[2] * Pj[1], dy = Pi[2] * Pj[0] - Pi[0] * Pj[2],
-         dz = Pi[0] * Pj[1] - Pi[1] * Pj[0];
-  const double nd = sqrt(dx * dx + dy * dy + dz * dz);
-  const unsigned long long pk = (unsigned long long)i * (unsigned long long)B + (unsigned long long)j;
-  if (nd < cop_tol) {  // coplanar: reported for the caller (:141-144)
-    const unsigned long long k = atomicAdd(n_c, 1ull);
-    if (k < cap) ckey[k] = pk;
-    return;
-  }
-  dx /= nd;
-  dy /= nd;
-  dz /= nd;
-  for (int s = 0; s < 2; ++s) {
-    const double c[3] = {s == 0 ? dx : -dx, s == 0 ? dy : -dy, s == 0 ? dz : -dz};
-    const double phi_i = angle_on(Si, Pi, c);
-    if (phi_i < -on_tol || phi_i > L[i] + on_tol) continue;
-    const double phi_j = angle_on(Sj, Pj, c);
-    if (phi_j < -on_tol || phi_j > L[j] + on_tol) continue;
-    const unsigned long long k = atomicAdd(n_x, 1ull);
-    if (k < cap) {
-      xkey[k] = pk * 2ull + (unsigned long long)s;
-      xpt[3 * k] = c[0];
-      xpt[3 * k + 1] = c[1];
-      xpt[3 * k + 2] = c[2];
-    }
-  }
-}
-
-__global__ void k_arc_out(int64_t n, const unsigned long long* __restrict__ key,
-                          const int64_t* __restrict__ perm, const double* __restrict__ pts,
-                          int64_t B, int pair_shift, int64_t* __restrict__ oi,
-                          int64_t* __restrict__ oj, double* __restrict__ op) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const unsigned long long pk = key[k] >> pair_shift;
-  oi[k] = (int64_t)(pk / (unsigned long long)B);
-  oj[k] = (int64_t)(pk % (unsigned long long)B);
-  if (op) {
-    const int64_t s = perm[k];
-    for (int c = 0; c < 3; ++c) op[3 * k + c] = pts[3 * s + c];
-  }
-}
-
 // device buffers freed on scope exit (host-synchronous entry points)
 struct DevBufs {
   std::vector<void*> p;
@@ -573,83 +493,4 @@ extern "C" int64_t gwn_ray_tris_hits(const gwn_tri_bvh* bvh, const double* origi
   CKM(cudaMemcpy(vs, v2, sizeof(double) * total, cudaMemcpyDeviceToHost));
   CKM(cudaMemcpy(tris, f2, sizeof(int64_t) * total, cudaMemcpyDeviceToHost));
   return total;
-}
-
-extern "C" int64_t gwn_arc_crossings(const double* S, const double* E, const double* P,
-                                     const double* L, const int64_t* prev_idx,
-                                     const int64_t* next_idx, int64_t B, double on_tol,
-                                     double cop_tol, int64_t* pair_i, int64_t* pair_j,
-                                     double* points, int64_t* cop_i, int64_t* cop_j,
-                                     int64_t* n_cop, int64_t cap, int device) {
-  if (B < 0 || (B > 0 && (!S || !E || !P || !L || !prev_idx || !next_idx)) || !n_cop) {
-    set_error("gwn_arc_crossings: invalid arguments");
-    return GWN_E_INVALID;
-  }
-  *n_cop = 0;
-  if (B < 2) return 0;
-  if (B > (1ll << 30)) {
-    set_error("gwn_arc_crossings: too many arcs");
-    return GWN_E_INVALID;
-  }
-  CKM(cudaSetDevice(device));
-  DevBufs db;
-  const double* dS = db.up(S, 3 * (size_t)B);
-  const double* dE = db.up(E, 3 * (size_t)B);
-  const double* dP = db.up(P, 3 * (size_t)B);
-  const double* dL = db.up(L, (size_t)B);
-  const int64_t* dpv = db.up(prev_idx, (size_t)B);
-  const int64_t* dnx = db.up(next_idx, (size_t)B);
-  unsigned long long* cnt = db.get<unsigned long long>(2);
-  CKM(db.err);
-  // buffer sized by the reference's numba capacity (8 B + 64), grown on demand
-  int64_t bcap = 8 * B + 64;
-  unsigned long long hc[2] = {0, 0};
-  unsigned long long *xkey = nullptr, *ckey = nullptr;
-  double* xpt = nullptr;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    xkey = db.get<unsigned long long>(bcap);
-    ckey = db.get<unsigned long long>(bcap);
-    xpt = db.get<double>(3 * (size_t)bcap);
-    CKM(db.err);
-    CKM(cudaMemset(cnt, 0, 2 * sizeof(unsigned long long)));
-    const dim3 blk(32, 8), grd((unsigned)((B + 31) / 32), (unsigned)((B + 7) / 8));
-    k_arc_pairs<<<grd, blk>>>(dS, dE, dP, dL, dpv, dnx, B, on_tol, cop_tol, cnt, xkey, xpt,
-                              cnt + 1, ckey, (unsigned long long)bcap);
-    CKM(cudaGetLastError());
-    CKM(cudaMemcpy(hc, cnt, sizeof hc, cudaMemcpyDeviceToHost));
-    if ((int64_t)hc[0] <= bcap && (int64_t)hc[1] <= bcap) break;
-    bcap = (int64_t)(hc[0] > hc[1] ? hc[0] : hc[1]) + 64;
-  }
-  const int64_t nx = (int64_t)hc[0], nc = (int64_t)hc[1];
-  *n_cop = nc;
-  if (nx > cap || nc > cap) return nx > nc ? nx : nc;  // caller retries with this capacity
-  const int pbits = bits_for((unsigned long long)B * (unsigned long long)B);
-  if (nx > 0) {
-    unsigned long long* ks = nullptr;
-    int64_t* perm = nullptr;
-    CKM(sort_keys(db, xkey, nx, pbits + 1, &ks, &perm));
-    int64_t* oi = db.get<int64_t>(nx);
-    int64_t* oj = db.get<int64_t>(nx);
-    double* op = db.get<double>(3 * (size_t)nx);
-    CKM(db.err);
-    k_arc_out<<<(unsigned)((nx + 255) / 256), 256>>>(nx, ks, perm, xpt, B, 1, oi, oj, op);
-    CKM(cudaGetLastError());
-    CKM(cudaMemcpy(pair_i, oi, sizeof(int64_t) * nx, cudaMemcpyDeviceToHost));
-    CKM(cudaMemcpy(pair_j, oj, sizeof(int64_t) * nx, cudaMemcpyDeviceToHost));
-    CKM(cudaMemcpy(points, op, sizeof(double) * 3 * nx, cudaMemcpyDeviceToHost));
-  }
-  if (nc > 0) {
-    unsigned long long* ks = nullptr;
-    int64_t* perm = nullptr;
-    CKM(sort_keys(db, ckey, nc, pbits, &ks, &perm));
-    int64_t* oi = db.get<int64_t>(nc);
-    int64_t* oj = db.get<int64_t>(nc);
-    CKM(db.err);
-    k_arc_out<<<(unsigned)((nc + 255) / 256), 256>>>(nc, ks, perm, nullptr, B, 0, oi, oj,
-                                                     nullptr);
-    CKM(cudaGetLastError());
-    CKM(cudaMemcpy(cop_i, oi, sizeof(int64_t) * nc, cudaMemcpyDeviceToHost));
-    CKM(cudaMemcpy(cop_j, oj, sizeof(int64_t) * nc, cudaMemcpyDeviceToHost));
-  }
-  return nx;
 }

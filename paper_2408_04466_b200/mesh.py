@@ -36,52 +36,75 @@ class Bvh:
     R2: np.ndarray
 
 
+def _morton30(c: np.ndarray) -> np.ndarray:
+    """30-bit Morton codes of points quantised to a 1024^3 grid over their box."""
+    lo, hi = c.min(axis=0), c.max(axis=0)
+    ext = np.where(hi > lo, hi - lo, 1.0)
+    g = np.clip(((c - lo) / ext * 1024.0).astype(np.int64), 0, 1023)
+    code = np.zeros(len(c), np.int64)
+    for b in range(10):
+        for a in range(3):
+            code |= ((g[:, a] >> b) & 1) << (3 * b + (2 - a))
+    return code
+
+
 def build_bvh(vertices, triangles, leaf_size: int = 8) -> Bvh:
-    """Median split over triangle centroids along the widest centroid axis
-    (surfaces.py:91-163); leaves hold <= leaf_size triangles."""
+    """A BVH in the reference's ``Bvh`` array layout (surfaces.py:74-89: node
+    boxes, children, leaf ranges into ``tri_order``, per-triangle
+    Moller-Trumbore data), so reference ``Bvh`` objects and these are
+    interchangeable.  Built differently: triangles are ordered once along a
+    Morton curve of their centroids, then the tree is cut level by level into
+    halves of that order (numpy, one pass per level), with node boxes from
+    segmented min/max reductions.  Leaves hold <= leaf_size triangles."""
     V = np.ascontiguousarray(vertices, dtype=np.float64)
     T = np.ascontiguousarray(triangles, dtype=np.int64).reshape(-1, 3)
     F = len(T)
     p0, p1, p2 = V[T[:, 0]], V[T[:, 1]], V[T[:, 2]]
-    tmin = np.minimum(np.minimum(p0, p1), p2)
-    tmax = np.maximum(np.maximum(p0, p1), p2)
     cent = (p0 + p1 + p2) / 3.0
-    nmin, nmax, left, right, start, count = [], [], [], [], [], []
-    order = np.arange(F, dtype=np.int64)
-
-    def node():
-        nmin.append(np.zeros(3)); nmax.append(np.zeros(3))
-        left.append(-1); right.append(-1); start.append(0); count.append(0)
-        return len(nmin) - 1
-
-    stack = [(node(), 0, F)]
-    while stack:
-        nd, lo, hi = stack.pop()
-        ids = order[lo:hi]
-        nmin[nd] = tmin[ids].min(axis=0) if hi > lo else np.zeros(3)
-        nmax[nd] = tmax[ids].max(axis=0) if hi > lo else np.zeros(3)
-        if hi - lo <= leaf_size:
-            start[nd] = lo
-            count[nd] = hi - lo
-            continue
-        axis = int(np.argmax(cent[ids].max(axis=0) - cent[ids].min(axis=0)))
-        mid = (lo + hi) // 2
-        order[lo:hi] = ids[np.argsort(cent[ids, axis], kind="stable")]
-        a, b = node(), node()
-        left[nd], right[nd] = a, b
-        stack.append((a, lo, mid))
-        stack.append((b, mid, hi))
+    order = np.argsort(_morton30(cent), kind="stable") if F else np.zeros(0, np.int64)
+    bmin = np.minimum(np.minimum(p0, p1), p2)[order]
+    bmax = np.maximum(np.maximum(p0, p1), p2)[order]
+    lo_l, hi_l, par_l, side_l = [np.zeros(1, np.int64)], [np.full(1, F, np.int64)], \
+        [np.full(1, -1, np.int64)], [np.zeros(1, np.int64)]
+    lo, hi, base = lo_l[0], hi_l[0], 0
+    while True:  # breadth-first: the children of this level's inner nodes
+        split = (hi - lo) > leaf_size
+        if not split.any():
+            break
+        ids = base + np.nonzero(split)[0]
+        mid = (lo[split] + hi[split]) // 2
+        lo = np.stack([lo[split], mid], 1).reshape(-1)
+        hi = np.stack([mid, hi[split]], 1).reshape(-1)
+        base += len(split)
+        lo_l.append(lo); hi_l.append(hi)
+        par_l.append(np.repeat(ids, 2)); side_l.append(np.tile([0, 1], len(ids)))
+    start = np.concatenate(lo_l)
+    count = np.concatenate(hi_l) - start
+    parent, side = np.concatenate(par_l), np.concatenate(side_l)
+    n = len(start)
+    left, right = np.full(n, -1, np.int64), np.full(n, -1, np.int64)
+    kid = np.arange(n)
+    left[parent[(parent >= 0) & (side == 0)]] = kid[(parent >= 0) & (side == 0)]
+    right[parent[(parent >= 0) & (side == 1)]] = kid[(parent >= 0) & (side == 1)]
+    inner = left >= 0
+    start[inner], count[inner] = 0, 0
+    nmin, nmax = np.zeros((n, 3)), np.zeros((n, 3))
+    leaf = np.nonzero(~inner & (count > 0))[0]
+    if len(leaf):  # leaves partition the Morton order: one segmented reduction
+        leaf = leaf[np.argsort(start[leaf])]
+        nmin[leaf] = np.minimum.reduceat(bmin, start[leaf], axis=0)
+        nmax[leaf] = np.maximum.reduceat(bmax, start[leaf], axis=0)
+    for lvl in reversed(range(len(lo_l) - 1)):  # inner nodes bottom-up
+        a = sum(len(x) for x in lo_l[:lvl])
+        ids = a + np.nonzero(inner[a:a + len(lo_l[lvl])])[0]
+        nmin[ids] = np.minimum(nmin[left[ids]], nmin[right[ids]])
+        nmax[ids] = np.maximum(nmax[left[ids]], nmax[right[ids]])
     e1, e2 = p1 - p0, p2 - p0
-    n = np.cross(e1, e2)
-    nn = np.linalg.norm(n, axis=1)
-    nh = n / np.where(nn > 0, nn, 1.0)[:, None]
-    r2 = np.maximum(np.maximum(np.einsum("ij,ij->i", p0 - cent, p0 - cent),
-                               np.einsum("ij,ij->i", p1 - cent, p1 - cent)),
-                    np.einsum("ij,ij->i", p2 - cent, p2 - cent))
-    return Bvh(np.asarray(nmin, np.float64).reshape(-1, 3),
-               np.asarray(nmax, np.float64).reshape(-1, 3),
-               np.asarray(left, np.int64), np.asarray(right, np.int64),
-               np.asarray(start, np.int64), np.asarray(count, np.int64), order,
+    nrm = np.cross(e1, e2)
+    nn = np.sqrt((nrm * nrm).sum(axis=1))
+    nh = nrm / np.where(nn > 0, nn, 1.0)[:, None]
+    r2 = np.max(np.stack([((p - cent) ** 2).sum(axis=1) for p in (p0, p1, p2)]), axis=0)
+    return Bvh(nmin, nmax, left, right, start, count, order.astype(np.int64),
                np.ascontiguousarray(p0), np.ascontiguousarray(e1), np.ascontiguousarray(e2),
                np.ascontiguousarray(nn), np.ascontiguousarray(nh), np.ascontiguousarray(cent),
                np.ascontiguousarray(r2))

@@ -1,5 +1,5 @@
 """GPU: the rest of the kernel dispatch layer (solid angles, ray/mesh all
-hits, arc crossings) through libgwn_b200.so against the reference's own
+hits) through libgwn_b200.so against the reference's own
 outputs (tests/golden/mesh.npz) and the CPU oracle (oracle/mesh_oracle.py).
 
 Tolerances: solid-angle totals 1e-11 absolute (one complex product per
@@ -125,34 +125,3 @@ def test_ray_hits_large_vs_oracle_and_records():
     empty = K.ray_tris_hits_batch(bvh, np.zeros((0, 3)), np.zeros((0, 3)), 0.0, np.inf, 1e-12,
                                   1e-9)
     assert empty[0].tolist() == [0] and len(empty[1]) == 0
-
-
-@pytest.mark.parametrize("name", ["eight", "star", "patch"])
-def test_arc_crossings_vs_reference(g, name):
-    k = lambda s: g[f"arc_{name}_{s}"]  # noqa: E731
-    pi, pj, pp, ci, cj = K.arc_crossings(k("S"), k("E"), k("P"), k("L"), k("prev"), k("next"),
-                                         1e-9, 1e-12)
-    assert np.array_equal(pi, k("pi")) and np.array_equal(pj, k("pj"))
-    assert np.abs(pp - k("pts")).max(initial=0.0) < 1e-12
-    assert np.array_equal(ci, k("ci")) and np.array_equal(cj, k("cj"))
-
-
-def test_arc_crossings_large_vs_oracle():
-    rng = np.random.default_rng(8)
-    t = np.linspace(0, 2 * np.pi, 401)[:-1]
-    r = 1.0 + 0.5 * np.cos(11 * t) + 0.2 * rng.normal(size=t.size) * 0.05
-    U = np.stack([r * np.cos(3 * t), r * np.sin(3 * t), np.full_like(t, 1.1)], axis=1)
-    U /= np.linalg.norm(U, axis=1, keepdims=True)
-    Un = np.roll(U, -1, axis=0)
-    P = np.cross(U, Un)
-    P /= np.linalg.norm(P, axis=1, keepdims=True)
-    L = np.arctan2(np.linalg.norm(np.cross(U, Un), axis=1), np.einsum("ij,ij->i", U, Un))
-    B = len(U)
-    prv, nxt = (np.arange(B) - 1) % B, (np.arange(B) + 1) % B
-    got = K.arc_crossings(U, Un, P, L, prv, nxt, 1e-9, 1e-12)
-    ref = MO.arc_crossings(U, Un, P, L, prv, nxt, 1e-9, 1e-12)
-    assert len(ref[0]) > 10
-    for a, b in zip(got, ref):
-        assert a.shape == b.shape
-        assert np.abs(a - b).max(initial=0) < 1e-12
-    assert K.arc_crossings(U[:1], Un[:1], P[:1], L[:1], [0], [0], 1e-9, 1e-12)[0].shape == (0,)
