@@ -54,6 +54,7 @@ FLOP_SEGMENT = 34.0    # K4 exact, per (query, net segment) in the ray frame: ve
                        # |r|^2 5, rsqrt seed + Halley 8, u 4) + num 3, den 5, complex product 6
 FLOP_TERM = 12.0       # K4 far field, per solid-harmonic term: complex recurrence 8 +
                        # complex multiply-add 4
+L2P_TERMS = 231        # terms of one order-20 local expansion (j <= 20, 0 <= k <= j)
 
 CONFIG_DESC = {
     1: "config1: single open bicubic patch, 4096 queries U[-0.5,1.5]^3",
@@ -383,9 +384,11 @@ def rooflines(stt: dict, peak_tf: float, ms_step: float, config: int) -> dict:
             f"{int(stt['boundary_segments'])} (query, segment) pairs x {FLOP_SEGMENT:.0f} flop",
             "k_ff_near"),
         "k_ff_fill (K4 far field)": (
-            stt.get("ms_k4_far", 0.0), stt.get("far_terms", 0) * FLOP_TERM,
-            f"{int(stt.get('far_terms', 0))} solid-harmonic terms x {FLOP_TERM:.0f} flop "
-            f"({int(stt['far_pairs'])} far (query, cycle) pairs)", "k_ff_fill"),
+            stt.get("ms_k4_far", 0.0),
+            (stt.get("far_terms", 0) + stt.get("local_evals", 0) * L2P_TERMS) * FLOP_TERM,
+            f"{int(stt.get('far_terms', 0))} multipole terms ({int(stt['far_pairs'])} per-pair far "
+            f"(query, cycle) expansions) + {int(stt.get('local_evals', 0))} local expansions x "
+            f"{L2P_TERMS} terms, x {FLOP_TERM:.0f} flop per term", "k_ff_fill"),
         "k3_newton (K3 Newton + record)": (
             stt["ms_k3_newton"], stt["newton_iters"] * FLOP_NEWTON + stt["roots"] * FLOP_ROOT,
             f"{int(stt['newton_iters'])} iterations x {FLOP_NEWTON:.0f} + {int(stt['roots'])} "
@@ -602,6 +605,7 @@ def main():
             "roofline": head,
             "rooflines": rl,
             "scene_build_s": scene_build_s,
+            "local_expansions": sc.local_expansions,
             "first_eval_s": first_eval_s,
             "rounds_built": int(st0["rounds_built"]),
             "first_eval_round_build_ms": st0["ms_round_build"],

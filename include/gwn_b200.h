@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define GWN_ABI_VERSION 3
+#define GWN_ABI_VERSION 4
 
 /* return codes (negative = error) */
 #define GWN_OK 0
@@ -92,6 +92,12 @@ typedef struct gwn_scene_info {
   int32_t device;
   int32_t sm_count;
   int64_t n_far_cycles;     /* boundary cycles with a far-field expansion    */
+  int32_t fmm_levels;       /* leaf level of round 0's local-expansion octree
+                               (0: per-pair far field only)                  */
+  int32_t pad_;
+  int64_t fmm_translations; /* (box, cycle) multipole-to-local translations  */
+  int64_t fmm_leftover;     /* entries left to the per-query path, all leaves */
+  double fmm_build_ms;      /* host wall time of the octree build (scene creation) */
 } gwn_scene_info;
 
 /* Device-side counters of the last gwn_eval on a scene (for the roofline
@@ -117,6 +123,7 @@ typedef struct gwn_stats {
   double ms_k4_far, ms_k4_exact;  /* split of ms_boundary (far-field scenes, timed)   */
   int64_t rounds_built;       /* direction rounds (K1 structures) cached on the scene */
   double ms_round_build;      /* host wall time building new rounds in this eval      */
+  int64_t local_evals;        /* queries whose far field came from a leaf's local expansion */
 } gwn_stats;
 
 int gwn_abi_version(void);

@@ -63,6 +63,8 @@ class SceneInfo(C.Structure):
         ("n_patches", C.c_int64), ("n_net_edges", C.c_int64), ("n_net_segments", C.c_int64),
         ("bbox_min", C.c_double * 3), ("bbox_max", C.c_double * 3), ("diag", C.c_double),
         ("device", C.c_int32), ("sm_count", C.c_int32), ("n_far_cycles", C.c_int64),
+        ("fmm_levels", C.c_int32), ("pad_", C.c_int32), ("fmm_translations", C.c_int64),
+        ("fmm_leftover", C.c_int64), ("fmm_build_ms", C.c_double),
     ]
 
 
@@ -77,7 +79,7 @@ class Stats(C.Structure):
         ("k3_fallback_items", C.c_int64), ("k3_newton_items", C.c_int64),
         ("far_pairs", C.c_int64), ("far_terms", C.c_int64), ("near_pairs", C.c_int64),
         ("ms_k4_far", C.c_double), ("ms_k4_exact", C.c_double), ("rounds_built", C.c_int64),
-        ("ms_round_build", C.c_double),
+        ("ms_round_build", C.c_double), ("local_evals", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

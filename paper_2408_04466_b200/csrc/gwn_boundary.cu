@@ -456,15 +456,16 @@ __device__ __forceinline__ bool ff_far2(double qa, double qb, double qc,
 // Omega(p) = -sum_{n>=1} [Re(D_n^0 I_n^0) + 2 sum_{m>=1} Re(D_n^m I_n^m)] of
 // order pl (<= P): the loops run to the warp's largest order P and a lane
 // adds only its own terms, so its sum is bit-identical to an order-pl
-// evaluation whatever its neighbours need (explicit roundings).
-template <int P>
-__device__ __forceinline__ double ff_eval_pred(double x, double y, double z,
-                                               const double2* __restrict__ Dc, int pl) {
+// evaluation whatever its neighbours need (explicit roundings).  Runtime
+// loops: one copy of the code for every order (fully unrolled per-order
+// instantiations up to order 30 overflowed the instruction cache).
+__device__ __forceinline__ double ff_eval_rt(double x, double y, double z,
+                                             const double2* __restrict__ Dc, int P, int pl) {
   const double ir2 = __drcp_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)),
                                          __dmul_rn(z, z)));
   double dR = __dsqrt_rn(ir2), dI = 0.0;  // I_0^0 = 1/r
   double acc = 0.0;
-#pragma unroll
+#pragma unroll 1
   for (int mm = 0; mm <= P; ++mm) {
     if (mm > 0) {  // I_m^m = -(2m-1)(x+iy)/r^2 I_{m-1}^{m-1}
       const double c0 = __dmul_rn(-(2.0 * mm - 1.0), ir2);
@@ -475,19 +476,22 @@ __device__ __forceinline__ double ff_eval_pred(double x, double y, double z,
     }
     double aR = dR, aI = dI, bR = 0.0, bI = 0.0;
     double col = 0.0;
-#pragma unroll
-    for (int n = mm; n <= P; ++n) {
-      if (n > mm) {  // I_n^m = ((2n-1) z I_{n-1}^m - ((n-1)^2 - m^2) I_{n-2}^m) / r^2
-        const double kz = __dmul_rn(2.0 * n - 1.0, z);
-        const double k2 = (double)((n - 1) * (n - 1) - mm * mm);
-        const double vR = __dmul_rn(__fma_rn(kz, aR, -__dmul_rn(k2, bR)), ir2);
-        const double vI = __dmul_rn(__fma_rn(kz, aI, -__dmul_rn(k2, bI)), ir2);
-        bR = aR;
-        bI = aI;
-        aR = vR;
-        aI = vI;
-      }
-      if (n == 0) continue;
+    if (mm > 0) {
+      const double2 d = __ldg(Dc + ff_term(mm, mm));
+      if (mm <= pl) col = __fma_rn(d.x, aR, __fma_rn(-d.y, aI, col));
+    }
+    const double m2 = (double)(mm * mm);
+#pragma unroll 2
+    for (int n = mm + 1; n <= P; ++n) {
+      // I_n^m = ((2n-1) z I_{n-1}^m - ((n-1)^2 - m^2) I_{n-2}^m) / r^2
+      const double kz = __dmul_rn(2.0 * n - 1.0, z);
+      const double k2 = (double)((n - 1) * (n - 1)) - m2;
+      const double vR = __dmul_rn(__fma_rn(kz, aR, -__dmul_rn(k2, bR)), ir2);
+      const double vI = __dmul_rn(__fma_rn(kz, aI, -__dmul_rn(k2, bI)), ir2);
+      bR = aR;
+      bI = aI;
+      aR = vR;
+      aI = vI;
       const double2 d = __ldg(Dc + ff_term(n, mm));
       if (n <= pl) col = __fma_rn(d.x, aR, __fma_rn(-d.y, aI, col));
     }
@@ -504,11 +508,11 @@ struct FFQuery {
   double px, py, pz, qa, qb, qc;
 };
 
-__device__ __forceinline__ FFQuery ff_query(int32_t m, const int32_t* __restrict__ order,
-                                            const int32_t* __restrict__ active,
-                                            const double* __restrict__ pos, const Frame& f) {
+__device__ __forceinline__ FFQuery ff_query_at(int32_t t, int32_t m,
+                                               const int32_t* __restrict__ order,
+                                               const int32_t* __restrict__ active,
+                                               const double* __restrict__ pos, const Frame& f) {
   FFQuery Q;
-  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   Q.live = t < m;
   Q.s = Q.live ? (order ? order[t] : t) : 0;
   const int32_t q = Q.live ? (active ? active[Q.s] : Q.s) : 0;
@@ -519,20 +523,151 @@ __device__ __forceinline__ FFQuery ff_query(int32_t m, const int32_t* __restrict
   return Q;
 }
 
-constexpr int kFFBlock = 128;
+// one query per thread, or per warp (kWarp: small rounds)
+template <bool kWarp>
+__device__ __forceinline__ FFQuery ff_query(int32_t m, const int32_t* __restrict__ order,
+                                            const int32_t* __restrict__ active,
+                                            const double* __restrict__ pos, const Frame& f) {
+  const int32_t t = (int32_t)((blockIdx.x * blockDim.x + threadIdx.x) / (kWarp ? 32 : 1));
+  return ff_query_at(t, m, order, active, pos, f);
+}
 
+struct FFList {
+  const int32_t* ent;
+  int32_t b, n;
+  int64_t leaf;   // -1: none (outside the cube, or no local expansions)
+};
+
+struct FFLocal {
+  const int32_t* loff = nullptr;  // null: no local expansions this round
+  const int32_t* lent = nullptr;
+  const double2* leafL = nullptr;
+  int n = 0;                      // leaves per axis
+  int64_t n_leaf = 0;
+  double x0 = 0, y0 = 0, z0 = 0, h = 0, side = 0;
+};
+
+__device__ __forceinline__ FFList ff_list(const FFLocal& F, int32_t C, const FFQuery& Q) {
+  FFList l{nullptr, 0, C, -1};
+  if (!F.loff || !Q.live) return l;
+  const double ux = (Q.px - F.x0) / F.side, uy = (Q.py - F.y0) / F.side,
+               uz = (Q.pz - F.z0) / F.side;
+  int64_t li = F.n_leaf;  // the outside list: every entry
+  if (ux >= 0.0 && ux < 1.0 && uy >= 0.0 && uy < 1.0 && uz >= 0.0 && uz < 1.0) {
+    const int64_t ix = min((int64_t)(ux * F.n), (int64_t)F.n - 1);
+    const int64_t iy = min((int64_t)(uy * F.n), (int64_t)F.n - 1);
+    const int64_t iz = min((int64_t)(uz * F.n), (int64_t)F.n - 1);
+    li = (ix * F.n + iy) * F.n + iz;
+    l.leaf = li;
+  }
+  l.ent = F.lent;
+  l.b = __ldg(F.loff + li);
+  l.n = __ldg(F.loff + li + 1) - l.b;
+  return l;
+}
+
+__device__ __forceinline__ int32_t ff_entry(const FFList& l, int j) {
+  return j < l.n ? (l.ent ? __ldg(l.ent + l.b + j) : j) : -1;
+}
+
+constexpr int kFFBlock = 128;
+constexpr int kFFWarpRoundThreads = 148 * 1024;  // rounds up to ~4.7K queries: a warp each
+
+// warp-aggregated atomicAdd of 1 per lane on counter[c] (lanes of `mask`
+// with equal c share one atomic); returns the lane's slot
+__device__ __forceinline__ unsigned ff_append(unsigned mask, int32_t c, unsigned* counter) {
+  const int lane = threadIdx.x & 31;
+  const unsigned grp = __match_any_sync(mask, c);
+  const int leader = __ffs(grp) - 1;
+  unsigned base = 0;
+  if (lane == leader) base = atomicAdd(counter + c, (unsigned)__popc(grp));
+  base = __shfl_sync(grp, base, leader);
+  return base + (unsigned)__popc(grp & ((1u << lane) - 1u));
+}
+
+// far-pair value: the entry's expansion at the lane's order (the warp runs
+// to its largest order P), plus a sliver's exact chord term (the edge's fan
+// sum = Omega(edge + chord back) + the chord's forward fan term, K4's shifted
+// form in the ray frame; den > 0: the half-line misses the sliver's sphere)
+__device__ __forceinline__ double ff_pair_value(const FFRound& R, const FFQuery& Q, int32_t c,
+                                                bool far, int P, unsigned long long& terms) {
+  int lvl = -1;
+  double x = 1.0, y = 0.0, z = 0.0;
+  if (far) {
+    x = __dsub_rn(Q.px, __ldg(R.gw + 3 * c));
+    y = __dsub_rn(Q.py, __ldg(R.gw + 3 * c + 1));
+    z = __dsub_rn(Q.pz, __ldg(R.gw + 3 * c + 2));
+    const double R2 = __dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z));
+    const double* lv = R.lv + (int64_t)kFFLevels * c;
+    lvl = kFFLevels - 1;
+#pragma unroll
+    for (int l = 0; l < kFFLevels - 1; ++l)
+      if (lvl == kFFLevels - 1 && R2 > __ldg(lv + l)) lvl = l;
+  }
+  const int wl = __reduce_max_sync(0xffffffffu, (unsigned)(lvl + 1)) - 1;
+  if (wl < 0) return 0.0;
+  const double2* Dc = R.D + (int64_t)(far ? c : 0) * kFFTerms;
+  const int pl = far ? ff_order(lvl) : -1;
+  double v = ff_eval_rt(x, y, z, Dc, ff_order(wl), pl);
+  (void)P;
+  if (!far) return 0.0;
+  terms += (unsigned long long)ff_nterms(pl);
+  if (__ldg(R.chord + c) >= 0) {
+    const double* A = R.ffa + 6 * (int64_t)c;
+    const double rax = __ldg(A) - Q.qa, ray = __ldg(A + 1) - Q.qb, raz = __ldg(A + 2) - Q.qc;
+    const double rbx = __ldg(A + 3) - Q.qa, rby = __ldg(A + 4) - Q.qb, rbz = __ldg(A + 5) - Q.qc;
+    const double ia = 1.0 / sqrt(rax * rax + ray * ray + raz * raz);
+    const double ib = 1.0 / sqrt(rbx * rbx + rby * rby + rbz * rbz);
+    const double uax = rax * ia, uay = ray * ia, uaz = fma(raz, ia, -1.0);
+    const double ubx = rbx * ib, uby = rby * ib, ubz = fma(rbz, ib, -1.0);
+    const double num = uay * ubx - uax * uby;
+    const double den = uax * ubx + uay * uby + uaz * ubz;
+    v = __dadd_rn(v, 2.0 * atan2(num, den));
+  }
+  return v;
+}
+
+__device__ __forceinline__ double ff_local(const FFLocal& F, const FFList& L, const FFQuery& Q) {
+  const int64_t n = F.n, ix = L.leaf / (n * n), iy = (L.leaf / n) % n, iz = L.leaf % n;
+  const double zx = F.x0 + ((double)ix + 0.5) * F.h, zy = F.y0 + ((double)iy + 0.5) * F.h,
+               zz = F.z0 + ((double)iz + 0.5) * F.h;
+  return fmm_l2p(Q.px - zx, Q.py - zy, Q.pz - zz, F.leafL + L.leaf * kFmmLT);
+}
+
+// Count pass: near pairs per query (qcnt) and per entry (ecnt).
+// kWarp = false: a thread per query, the warp steps through its lanes' lists
+// together (lanes of one leaf share the list); kWarp = true (small rounds):
+// a warp per query, 32 entries at a time.
+template <bool kWarp>
 __global__ void __launch_bounds__(kFFBlock)
 k_ff_count(int32_t m, const int32_t* __restrict__ order, const int32_t* __restrict__ active,
-           const double* __restrict__ pos, Frame f, FFRound R, unsigned* __restrict__ qcnt,
-           unsigned* __restrict__ ecnt, unsigned long long* __restrict__ counters) {
-  const FFQuery Q = ff_query(m, order, active, pos, f);
+           const double* __restrict__ pos, Frame f, FFRound R, FFLocal F,
+           unsigned* __restrict__ qcnt, unsigned* __restrict__ ecnt,
+           unsigned long long* __restrict__ counters) {
+  const FFQuery Q = ff_query<kWarp>(m, order, active, pos, f);
+  const FFList L = ff_list(F, R.C, Q);
   const int lane = threadIdx.x & 31;
   unsigned n = 0;
-  for (int c = 0; c < R.C; ++c) {  // warp-uniform loop
-    const bool near = Q.live && !ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+  if (kWarp) {
+    for (int j0 = 0; Q.live && j0 < L.n; j0 += 32) {  // warp-uniform (one query)
+      const int32_t c = ff_entry(L, j0 + lane);
+      const bool near = c >= 0 && !ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+      if (near) atomicAdd(ecnt + c, 1u);
+      n += (unsigned)__popc(__ballot_sync(0xffffffffu, near));
+    }
+    if (Q.live && lane == 0) {
+      qcnt[Q.s] = n;
+      if (n) atomicAdd(&counters[CNT_NEAR], (unsigned long long)n);
+    }
+    return;
+  }
+  const int jn = (int)__reduce_max_sync(0xffffffffu, Q.live ? (unsigned)L.n : 0u);
+  for (int j = 0; j < jn; ++j) {  // warp-uniform loop
+    const int32_t c = Q.live ? ff_entry(L, j) : -1;
+    const bool near = c >= 0 && !ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
     n += near ? 1u : 0u;
     const unsigned b = __ballot_sync(0xffffffffu, near);
-    if (b && lane == __ffs(b) - 1) atomicAdd(&ecnt[c], (unsigned)__popc(b));
+    if (near) ff_append(b, c, ecnt);
   }
   if (Q.live) qcnt[Q.s] = n;
   unsigned long long tot = n;
@@ -541,89 +676,80 @@ k_ff_count(int32_t m, const int32_t* __restrict__ order, const int32_t* __restri
   if (lane == 0 && tot) atomicAdd(&counters[CNT_NEAR], tot);
 }
 
+// Fill pass: the far row (local expansion + far pairs, added in list order)
+// and the near-pair records (slot, ordinal) of every entry.  Both variants
+// give a query the same bits: its pair values are computed per lane at the
+// lane's own order and folded into one sum in list order.
+template <bool kWarp>
 __global__ void __launch_bounds__(kFFBlock)
 k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restrict__ active,
-          const double* __restrict__ pos, Frame f, FFRound R,
+          const double* __restrict__ pos, Frame f, FFRound R, FFLocal F,
           const unsigned long long* __restrict__ eoff, unsigned* __restrict__ efill,
           int2* __restrict__ recs, double* __restrict__ row_far,
           unsigned long long* __restrict__ counters) {
-  const FFQuery Q = ff_query(m, order, active, pos, f);
+  const FFQuery Q = ff_query<kWarp>(m, order, active, pos, f);
+  const FFList L = ff_list(F, R.C, Q);
   const int lane = threadIdx.x & 31;
   double om = 0.0;
-  int k = 0;
-  unsigned long long nfar = 0, terms = 0;
-  for (int c = 0; c < R.C; ++c) {  // warp-uniform loop
-    const bool far = Q.live && ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
-    const bool near = Q.live && !far;
-    const unsigned b = __ballot_sync(0xffffffffu, near);
-    if (b) {  // append the near lanes to entry c's pair list
-      const int leader = __ffs(b) - 1;
-      unsigned base = 0;
-      if (lane == leader) base = atomicAdd(&efill[c], (unsigned)__popc(b));
-      base = __shfl_sync(0xffffffffu, base, leader);
+  unsigned long long nfar = 0, terms = 0, nloc = 0;
+  if (L.leaf >= 0) {  // the leaf's local expansion: every cycle its ancestors took
+    om = ff_local(F, L, Q);
+    nloc = (!kWarp || lane == 0) ? 1 : 0;
+  }
+  if (kWarp) {
+    int k = 0;
+    for (int j0 = 0; Q.live && j0 < L.n; j0 += 32) {  // warp-uniform (one query)
+      const int32_t c = ff_entry(L, j0 + lane);
+      const bool far = c >= 0 && ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+      const bool near = c >= 0 && !far;
+      const unsigned nb = __ballot_sync(0xffffffffu, near);
       if (near) {
-        recs[eoff[c] + base + __popc(b & ((1u << lane) - 1))] = make_int2(Q.s, k);
-        ++k;
+        const unsigned slot = atomicAdd(efill + c, 1u);
+        recs[eoff[c] + slot] = make_int2(Q.s, k + __popc(nb & ((1u << lane) - 1u)));
+      }
+      k += __popc(nb);
+      const double v = ff_pair_value(R, Q, c, far, 0, terms);
+      const unsigned fb = __ballot_sync(0xffffffffu, far);
+      nfar += far ? 1 : 0;
+      for (int i = 0; i < 32; ++i) {  // fold in list order
+        const double vi = __shfl_sync(0xffffffffu, v, i);
+        if ((fb >> i) & 1u) om = __dadd_rn(om, vi);
       }
     }
-    // far: the expansion at the lane's order, the warp runs to its largest
-    int lvl = -1;
-    double x = 1.0, y = 0.0, z = 0.0;
-    if (far) {
-      x = __dsub_rn(Q.px, __ldg(R.gw + 3 * c));
-      y = __dsub_rn(Q.py, __ldg(R.gw + 3 * c + 1));
-      z = __dsub_rn(Q.pz, __ldg(R.gw + 3 * c + 2));
-      const double R2 = __dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z));
-      const double* lv = R.lv + (int64_t)kFFLevels * c;
-      lvl = kFFLevels - 1;
-#pragma unroll
-      for (int l = 0; l < kFFLevels - 1; ++l)
-        if (lvl == kFFLevels - 1 && R2 > __ldg(lv + l)) lvl = l;
+    if (Q.live && lane == 0) row_far[Q.s] = 0.5 * om;
+  } else {
+    int k = 0;
+    const int jn = (int)__reduce_max_sync(0xffffffffu, Q.live ? (unsigned)L.n : 0u);
+    for (int j = 0; j < jn; ++j) {  // warp-uniform loop
+      const int32_t c = Q.live ? ff_entry(L, j) : -1;
+      const bool far = c >= 0 && ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+      const bool near = c >= 0 && !far;
+      const unsigned b = __ballot_sync(0xffffffffu, near);
+      if (near) {  // append to entry c's near-pair list
+        const unsigned slot = ff_append(b, c, efill);
+        recs[eoff[c] + slot] = make_int2(Q.s, k);
+        ++k;
+      }
+      const double v = ff_pair_value(R, Q, c, far, 0, terms);
+      if (far) {
+        om = __dadd_rn(om, v);
+        ++nfar;
+      }
     }
-    const int wl = __reduce_max_sync(0xffffffffu, (unsigned)(lvl + 1)) - 1;
-    if (wl < 0) continue;
-    const double2* Dc = R.D + (int64_t)c * kFFTerms;
-    const int pl = far ? ff_order(lvl) : -1;
-    double v;
-    static_assert(kFFLevels == 4, "the order dispatch below covers four levels");
-    switch (wl) {
-      case 0: v = ff_eval_pred<ff_order(0)>(x, y, z, Dc, pl); break;
-      case 1: v = ff_eval_pred<ff_order(1)>(x, y, z, Dc, pl); break;
-      case 2: v = ff_eval_pred<ff_order(2)>(x, y, z, Dc, pl); break;
-      default: v = ff_eval_pred<ff_order(3)>(x, y, z, Dc, pl); break;
-    }
-    if (!far) continue;
-    om = __dadd_rn(om, v);
-    ++nfar;
-    terms += (unsigned long long)ff_nterms(pl);
-    if (__ldg(R.chord + c) >= 0) {
-      // sliver: the edge's fan sum = Omega(edge + chord back) + the chord's
-      // forward fan term, K4's shifted form in the ray frame (den > 0: the
-      // half-line misses the sliver's sphere)
-      const double* A = R.ffa + 6 * (int64_t)c;
-      const double rax = __ldg(A) - Q.qa, ray = __ldg(A + 1) - Q.qb, raz = __ldg(A + 2) - Q.qc;
-      const double rbx = __ldg(A + 3) - Q.qa, rby = __ldg(A + 4) - Q.qb,
-                   rbz = __ldg(A + 5) - Q.qc;
-      const double ia = 1.0 / sqrt(rax * rax + ray * ray + raz * raz);
-      const double ib = 1.0 / sqrt(rbx * rbx + rby * rby + rbz * rbz);
-      const double uax = rax * ia, uay = ray * ia, uaz = fma(raz, ia, -1.0);
-      const double ubx = rbx * ib, uby = rby * ib, ubz = fma(rbz, ib, -1.0);
-      const double num = uay * ubx - uax * uby;
-      const double den = uax * ubx + uay * uby + uaz * ubz;
-      om = __dadd_rn(om, 2.0 * atan2(num, den));
-    }
+    // K4's partials are sums of atan2 (half angles): Omega / 2
+    if (Q.live) row_far[Q.s] = 0.5 * om;
   }
-  // K4's partials are sums of atan2 (half angles): Omega / 2
-  if (Q.live) row_far[Q.s] = 0.5 * om;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     nfar += __shfl_down_sync(0xffffffffu, nfar, o);
     terms += __shfl_down_sync(0xffffffffu, terms, o);
+    nloc += __shfl_down_sync(0xffffffffu, nloc, o);
   }
   if (lane == 0 && nfar) {
     atomicAdd(&counters[CNT_FAR], nfar);
     atomicAdd(&counters[CNT_FAR_TERMS], terms);
   }
+  if (lane == 0 && nloc) atomicAdd(&counters[CNT_LOCAL], nloc);
 }
 
 // tiles of kBlockQ * kQPT near pairs per entry
@@ -790,11 +916,33 @@ static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int3
   FC(ff_grow(c.tmp, c.cap_tmp, std::max(tb1, tb2), 1, st));
   const FFRound R{C, rd.ffg, sc->ff_r, sc->ff_lv, sc->ff_g,
                   reinterpret_cast<const double2*>(sc->ff_D), sc->ff_chord, rd.ffa};
+  FFLocal F;
+  if (rd.fmm) {  // round 0 of a scene with local expansions (gwn_fmm.cu)
+    F.loff = rd.fmm->loff;
+    F.lent = rd.fmm->lent;
+    F.leafL = rd.fmm->leafL;
+    F.n = 1 << rd.fmm->L;
+    F.n_leaf = rd.fmm->n_leaf;
+    F.x0 = sc->fmm_x0[0];
+    F.y0 = sc->fmm_x0[1];
+    F.z0 = sc->fmm_x0[2];
+    F.side = sc->fmm_side;
+    F.h = sc->fmm_side / (double)F.n;
+  }
   FC(cudaMemsetAsync(c.ecnt, 0, sizeof(unsigned) * (C + 1), st));
   FC(cudaMemsetAsync(c.efill, 0, sizeof(unsigned) * (C + 1), st));
   FC(cudaMemsetAsync(c.qcnt + m, 0, sizeof(unsigned), st));
-  const unsigned g = (unsigned)((m + kFFBlock - 1) / kFFBlock);
-  k_ff_count<<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, c.qcnt, c.ecnt, counters);
+  // small rounds (re-shoots): a warp per query, so the few queries' pairs
+  // spread over the GPU instead of serialising in one block
+  const bool per_warp = (int64_t)m * 32 <= (int64_t)kFFWarpRoundThreads;
+  const unsigned g = per_warp ? (unsigned)(((int64_t)m * 32 + kFFBlock - 1) / kFFBlock)
+                              : (unsigned)((m + kFFBlock - 1) / kFFBlock);
+  if (per_warp)
+    k_ff_count<true><<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, F, c.qcnt, c.ecnt,
+                                             counters);
+  else
+    k_ff_count<false><<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, F, c.qcnt,
+                                              c.ecnt, counters);
   FC(cudaGetLastError());
   FC(cub::DeviceScan::ExclusiveSum(c.tmp, tb1, c.qcnt, c.qoff, m + 1, st));
   FC(cub::DeviceScan::ExclusiveSum(c.tmp, tb2, c.ecnt, c.eoff, C + 1, st));
@@ -816,8 +964,12 @@ static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int3
     c.cap_p = capp;
   }
   if (evb) FC(cudaEventRecord(evb[0], st));
-  k_ff_fill<<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, c.eoff, c.efill, c.recs,
-                                    bpart, counters);
+  if (per_warp)
+    k_ff_fill<true><<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, F, c.eoff, c.efill,
+                                            c.recs, bpart, counters);
+  else
+    k_ff_fill<false><<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, F, c.eoff, c.efill,
+                                             c.recs, bpart, counters);
   FC(cudaGetLastError());
   if (evb) FC(cudaEventRecord(evb[1], st));
   if (tiles > 0) {

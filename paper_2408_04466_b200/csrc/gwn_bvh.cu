@@ -735,6 +735,7 @@ void free_round(Round& rd) {
   if (rd.ffa) cudaFree(rd.ffa);
   if (rd.cell_offs) cudaFree(rd.cell_offs);
   if (rd.cell_ent) cudaFree(rd.cell_ent);
+  free_fmm_round(rd);
   rd = Round();
 }
 

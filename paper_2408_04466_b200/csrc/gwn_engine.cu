@@ -759,6 +759,7 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   stats.far_pairs = (int64_t)h_cnt[CNT_FAR];
   stats.far_terms = (int64_t)h_cnt[CNT_FAR_TERMS];
   stats.near_pairs = (int64_t)h_cnt[CNT_NEAR];
+  stats.local_evals = (int64_t)h_cnt[CNT_LOCAL];
   if (getenv("GWN_TRACE"))
     fprintf(stderr, "[gwn] fallback: max nodes/item %llu, slowest batch: %llu cycles tree %llu code %llu items %llu, max levels %llu\n",
             h_cnt[CNT_MAXNODES], h_cnt[CNT_BIGITEMS] >> 24, (h_cnt[CNT_BIGITEMS] >> 16) & 255, (h_cnt[CNT_BIGITEMS] >> 8) & 255, h_cnt[CNT_BIGITEMS] & 255, h_cnt[CNT_MAXLEVELS]);

@@ -28,8 +28,8 @@
 
 namespace gwn {
 
-// Gauss-Legendre points per direction: exact to degree 2Q-1 >= K (the
-// integrands have degree K-1 in (s, t), one more in u after the collapse)
+// Gauss-Legendre points on [0, 1]: exact to degree 2Q-1 >= K (the Stokes
+// integrand below has degree n <= K in the segment parameter)
 constexpr int kFFQ = kFFK / 2 + 1;
 
 struct FFQuad {
@@ -67,31 +67,40 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// D_n^m of one cycle per block: items (segment, quadrature point) over the
-// cycle's edges; the regular solid harmonics and their gradients by the
-// recurrences of gwn_farfield.cuh (dual numbers), one warp reduction per term
-// into the warp's own partial sums (deterministic; 256 threads = 8 warps).
-__global__ void __launch_bounds__(256)
+constexpr int kMomThreads = 128;
+
+// D_n^m of one entry per block, as a line integral over its polyline.  R_n^m
+// is a harmonic homogeneous polynomial, so grad R = -curl(x * grad R)/(n+1)
+// (curl(x * v) = x div v - 3 v + v - (x . grad) v with div v = 0 and v
+// homogeneous of degree n-1), and Stokes on the fan surface gives
+//     D_n^m = integral n . conj(grad R) dA = -1/(n+1) loop (d * conj(grad R(d))) . dd,
+// d = x - g.  Per segment the integrand has degree n in the parameter:
+// kFFQ Gauss points are exact.  Items (segment, point) over the entry's
+// edges (+ the closing chord of a sliver); the regular harmonics and their
+// gradients by the recurrences of gwn_farfield.cuh (dual numbers); one warp
+// reduction per term into the warp's own partial sums, added in a fixed
+// order (bit-identical moments across scene builds).  Checked against the
+// area integral in tools/farfield/fmm_proto.py.
+__global__ void __launch_bounds__(kMomThreads)
 k_ff_moments(const int64_t* __restrict__ coff, const int32_t* __restrict__ cedge,
              const int32_t* __restrict__ chord, const double* __restrict__ verts, int64_t V,
              int S, const double* __restrict__ g, FFQuad Q, double* __restrict__ D) {
-  // per-warp partial sums, added in a fixed order: the moments (and every
-  // far-field result) are bit-identical across scene builds
-  __shared__ double acc[8][2 * kFFTerms];
+  constexpr int kW = kMomThreads / 32;
+  __shared__ double acc[kW][2 * kFFTerms];
   const int c = blockIdx.x, wid = threadIdx.x >> 5;
-  for (int k = threadIdx.x; k < 8 * 2 * kFFTerms; k += blockDim.x) (&acc[0][0])[k] = 0.0;
+  for (int k = threadIdx.x; k < kW * 2 * kFFTerms; k += blockDim.x) (&acc[0][0])[k] = 0.0;
   __syncthreads();
   const int64_t e0 = coff[c], e1 = coff[c + 1];
   const int ch = chord[c];  // sliver: one more segment, the closing chord
   const int64_t segs = (e1 - e0) * (S - 1) + (ch >= 0 ? 1 : 0);
-  const int64_t items = segs * kFFQ * kFFQ;
+  const int64_t items = segs * kFFQ;
   const double gx = g[3 * c], gy = g[3 * c + 1], gz = g[3 * c + 2];
   for (int64_t base = 0; base < items; base += blockDim.x) {
     const int64_t it = base + threadIdx.x;
-    double wq = 0.0, nx = 0.0, ny = 0.0, nz = 0.0, x = 0.0, y = 0.0, z = 0.0;
+    double wq = 0.0, lx = 0.0, ly = 0.0, lz = 0.0, x = 0.0, y = 0.0, z = 0.0;
     if (it < items) {
-      const int64_t sg = it / (kFFQ * kFFQ);
-      const int qp = (int)(it % (kFFQ * kFFQ));
+      const int64_t sg = it / kFFQ;
+      const int qp = (int)(it % kFFQ);
       int64_t ka, kb;
       if (ch >= 0 && sg == segs - 1) {  // chord: last sample -> first
         ka = (int64_t)ch * S + S - 1;
@@ -103,15 +112,14 @@ k_ff_moments(const int64_t* __restrict__ coff, const int32_t* __restrict__ cedge
       }
       const double ax = verts[ka] - gx, ay = verts[V + ka] - gy, az = verts[2 * V + ka] - gz;
       const double bx = verts[kb] - gx, by = verts[V + kb] - gy, bz = verts[2 * V + kb] - gz;
-      nx = ay * bz - az * by;
-      ny = az * bx - ax * bz;
-      nz = ax * by - ay * bx;
-      const double u = Q.x[qp / kFFQ], v = Q.x[qp % kFFQ];
-      const double s = u, t = (1.0 - u) * v;
-      wq = Q.w[qp / kFFQ] * Q.w[qp % kFFQ] * (1.0 - u);
-      x = s * ax + t * bx;
-      y = s * ay + t * by;
-      z = s * az + t * bz;
+      lx = bx - ax;
+      ly = by - ay;
+      lz = bz - az;
+      const double s = Q.x[qp];
+      wq = Q.w[qp];
+      x = ax + s * lx;
+      y = ay + s * ly;
+      z = az + s * lz;
     }
     const double r2 = x * x + y * y + z * z;
     // diagonal R_m^m = -(x+iy)/(2m) R_{m-1}^{m-1}: value (re, im) and d/dx,y,z
@@ -147,9 +155,11 @@ k_ff_moments(const int64_t* __restrict__ coff, const int32_t* __restrict__ cedge
           aR = vR; aI = vI; axR = vxR; axI = vxI; ayR = vyR; ayI = vyI; azR = vzR; azI = vzI;
         }
         if (n == 0) continue;
-        // n . conj(grad R) = (n.gradR_re) - i (n.gradR_im), times the weight
-        const double fr = warp_sum_d(wq * (nx * axR + ny * ayR + nz * azR));
-        const double fi = warp_sum_d(-wq * (nx * axI + ny * ayI + nz * azI));
+        // (d x conj(grad R)) . dd = dd . (d x G) = G . (dd x d), G = conj(grad R)
+        const double cx = ly * z - lz * y, cy = lz * x - lx * z, cz = lx * y - ly * x;
+        const double k0 = -wq / (n + 1.0);
+        const double fr = warp_sum_d(k0 * (cx * axR + cy * ayR + cz * azR));
+        const double fi = warp_sum_d(-k0 * (cx * axI + cy * ayI + cz * azI));
         if ((threadIdx.x & 31) == 0) {
           acc[wid][2 * ff_term(n, m)] += fr;
           acc[wid][2 * ff_term(n, m) + 1] += fi;
@@ -161,7 +171,7 @@ k_ff_moments(const int64_t* __restrict__ coff, const int32_t* __restrict__ cedge
   for (int k = threadIdx.x; k < 2 * kFFTerms; k += blockDim.x) {
     double v = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) v += acc[w][k];
+    for (int w = 0; w < kW; ++w) v += acc[w][k];
     D[(int64_t)c * 2 * kFFTerms + k] = v;
   }
 }
@@ -186,6 +196,9 @@ void free_farfield(gwn_scene* sc) {
   sc->ff_n = 0;
   sc->ff_expanded = 0;
   sc->ff_g_host.clear();
+  if (sc->fmm_dmin) cudaFree(sc->fmm_dmin);
+  sc->fmm_dmin = nullptr;
+  sc->fmm_L = 0;
 }
 
 // ectrl: (n_edges, 4, 3) cubic edge nets on the host, sc->verts sampled.
@@ -412,7 +425,7 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   FF(cudaMemcpy(d_coff, coff.data(), sizeof(int64_t) * (nk + 1), cudaMemcpyHostToDevice));
   if (coff[nk] > 0)
     FF(cudaMemcpy(d_cedge, cedge.data(), sizeof(int32_t) * coff[nk], cudaMemcpyHostToDevice));
-  k_ff_moments<<<nk, 256>>>(d_coff, d_cedge, sc->ff_chord, sc->verts, V, S, sc->ff_g, ff_quad(),
+  k_ff_moments<<<nk, kMomThreads>>>(d_coff, d_cedge, sc->ff_chord, sc->verts, V, S, sc->ff_g, ff_quad(),
                             sc->ff_D);
   FF(cudaGetLastError());
   FF(cudaDeviceSynchronize());
@@ -420,6 +433,20 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   sc->ff_expanded = n_exp;
   sc->ff_g_host = gk;
   sc->ff_chord_host = chk;
+  {  // the octree of local expansions (gwn_fmm.cu) over the closed expanded cycles
+    static const bool fmm_off = [] {
+      const char* v = getenv("GWN_FMM");
+      return v && atoi(v) == 0;
+    }();
+    std::vector<double> rho(nk), aabs(nk);
+    std::vector<char> closed(nk);
+    for (int c = 0; c < nk; ++c) {
+      rho[c] = ents[c].rho;
+      aabs[c] = ents[c].aabs;
+      closed[c] = ents[c].expand && !ents[c].sliver;
+    }
+    if (!fmm_off) FF(fmm_setup_scene(sc, rho, aabs, closed));
+  }
 out:
 #undef FF
   if (d_coff) cudaFree(d_coff);
@@ -480,9 +507,15 @@ cudaError_t launch_ff_order(const gwn_scene* sc, int32_t m, const int32_t* activ
   double ext = 0.0;
   for (int k = 0; k < 3; ++k) ext = fmax(ext, sc->bbox_max[k] - sc->bbox_min[k]);
   ext = 2.0 * ext + 1e-30;
-  const double x0 = 0.5 * (sc->bbox_min[0] + sc->bbox_max[0]) - 0.5 * ext;
-  const double y0 = 0.5 * (sc->bbox_min[1] + sc->bbox_max[1]) - 0.5 * ext;
-  const double z0 = 0.5 * (sc->bbox_min[2] + sc->bbox_max[2]) - 0.5 * ext;
+  double x0 = 0.5 * (sc->bbox_min[0] + sc->bbox_max[0]) - 0.5 * ext;
+  double y0 = 0.5 * (sc->bbox_min[1] + sc->bbox_max[1]) - 0.5 * ext;
+  double z0 = 0.5 * (sc->bbox_min[2] + sc->bbox_max[2]) - 0.5 * ext;
+  if (sc->fmm_L > 0) {  // the local expansions' cube: a leaf's queries are contiguous
+    ext = sc->fmm_side;
+    x0 = sc->fmm_x0[0];
+    y0 = sc->fmm_x0[1];
+    z0 = sc->fmm_x0[2];
+  }
   k_ff_keys<<<(m + 255) / 256, 256, 0, st>>>(m, active, pos, x0, y0, z0, 1024.0 / ext, k0, i0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -30,10 +30,10 @@
 
 namespace gwn {
 
-#ifndef GWN_FFK
-#define GWN_FFK 20
-#endif
-constexpr int kFFK = GWN_FFK;                          // expansion order
+// expansion order of the per-pair path: order 30 brings R_min down to ~2.8
+// cycle radii (order 20: ~4.3), so 2.8x fewer (query, cycle) pairs at config
+// 5 need the exact sum
+constexpr int kFFK = 30;
 constexpr int kFFTerms = (kFFK + 1) * (kFFK + 2) / 2;  // (n, m), 0 <= m <= n <= K
 constexpr double kFFTau = 1e-12;                       // truncation bound per cycle (rad)
 // far-field partial rows: cycle groups summed in fixed order by K5, so the
@@ -41,10 +41,58 @@ constexpr double kFFTau = 1e-12;                       // truncation bound per c
 constexpr int kFFRows = 16;
 // adaptive order: a far pair uses the lowest of these orders whose bound
 // holds at its distance (per-cycle thresholds, Scene::ff_lv)
-constexpr int kFFLevels = 4;
+constexpr int kFFLevels = 6;  // orders 10, 14, ..., 30
 __host__ __device__ constexpr int ff_order(int lv) { return kFFK - 4 * (kFFLevels - 1 - lv); }
 
-__device__ __forceinline__ int ff_term(int n, int m) { return n * (n + 1) / 2 + m; }
+__host__ __device__ __forceinline__ constexpr int ff_term(int n, int m) {
+  return n * (n + 1) / 2 + m;
+}
+
+// local expansions (gwn_fmm.cu): order of the leaves' expansions, their
+// (j, k >= 0) coefficient count, the irregular-harmonic degree M2L needs
+constexpr int kFmmP = 20;
+constexpr int kFmmK = 30;  // multipole order translated by M2L (<= kFFK)
+constexpr int kFmmLT = (kFmmP + 1) * (kFmmP + 2) / 2;
+constexpr int kFmmKT = (kFmmK + 1) * (kFmmK + 2) / 2;
+constexpr int kFmmIN = kFmmK + kFmmP;
+constexpr int kFmmIT = (kFmmIN + 1) * (kFmmIN + 2) / 2;
+constexpr double kFmmTau = 0.5 * kFFTau;  // each of the two truncations of a translated pair
+
+// Omega(z + x) = sum_j [Re(conj(R_j^0(x)) L_j^0) + 2 sum_{k>=1} Re(conj(R_j^k(x)) L_j^k)]
+// (L2P), the regular harmonics by the recurrences of gwn_farfield.cu's
+// moment kernel: R_0^0 = 1, R_m^m = -(x+iy)/(2m) R_{m-1}^{m-1},
+// R_n^m = ((2n-1) z R_{n-1}^m - r^2 R_{n-2}^m) / ((n+m)(n-m)).
+__device__ __forceinline__ double fmm_l2p(double x, double y, double z,
+                                          const double2* __restrict__ Lc) {
+  const double r2 = x * x + y * y + z * z;
+  double dR = 1.0, dI = 0.0, acc = 0.0;
+#pragma unroll
+  for (int m = 0; m <= kFmmP; ++m) {
+    if (m > 0) {
+      const double c0 = -1.0 / (2.0 * m);
+      const double nR = c0 * (x * dR - y * dI), nI = c0 * (x * dI + y * dR);
+      dR = nR;
+      dI = nI;
+    }
+    double aR = dR, aI = dI, bR = 0.0, bI = 0.0, col = 0.0;
+#pragma unroll
+    for (int n = m; n <= kFmmP; ++n) {
+      if (n > m) {
+        const double inv = 1.0 / ((double)(n + m) * (double)(n - m));
+        const double k1 = (2.0 * n - 1.0) * z;
+        const double vR = (k1 * aR - r2 * bR) * inv, vI = (k1 * aI - r2 * bI) * inv;
+        bR = aR;
+        bI = aI;
+        aR = vR;
+        aI = vI;
+      }
+      const double2 l = Lc[ff_term(n, m)];
+      col = fma(aR, l.x, fma(aI, l.y, col));  // Re(conj(R) L)
+    }
+    acc += m == 0 ? col : 2.0 * col;
+  }
+  return acc;
+}
 
 // truncation bound of the order-K expansion at distance R (see above; host)
 inline double ff_bound(double aabs, double rho, int K, double R) {

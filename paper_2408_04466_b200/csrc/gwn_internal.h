@@ -45,7 +45,8 @@ enum : int {
   CNT_FAR = 8,       // (query, entry) pairs taken by the far-field expansion
   CNT_FAR_TERMS = 9, // solid-harmonic terms those expansions summed
   CNT_NEAR = 10,     // (query, entry) pairs summed exactly (far-field scenes)
-  CNT_N = 11,
+  CNT_LOCAL = 11,    // queries whose far field came from a leaf's local expansion
+  CNT_N = 12,
 };
 
 struct Frame {
@@ -79,6 +80,23 @@ struct alignas(16) Node {
 };
 
 struct LeafRec;
+
+// Local expansions of the boundary term's far field for one round
+// (gwn_fmm.cu): an octree over the scene cube; every (box, closed cycle)
+// pair accepted at the coarsest level whose error bound and line test hold
+// is translated (M2L) into the box's local expansion, pushed down (L2L) to
+// the leaves.  Per leaf: its local coefficients and the list of entries left
+// to the per-query path (the "leftover" list).
+struct FmmRound {
+  int L = 0;                    // leaf level
+  int64_t n_leaf = 0;           // 8^L leaf boxes, row-major (ix, iy, iz)
+  double2* leafL = nullptr;     // (n_leaf, kFmmLT) local coefficients L_j^k, k >= 0
+  int32_t* loff = nullptr;      // (n_leaf + 2) leftover list offsets; list n_leaf = every entry
+  int32_t* lent = nullptr;      // leftover entries, ascending per list
+  int64_t m2l_pairs = 0;        // (box, cycle) translations
+  int64_t leftover = 0;         // total leftover entries over the leaves
+  double ms_build = 0.0;
+};
 
 // packed uniform-grid entry: a leaf's cull box rounded outward to float
 struct CellEnt {
@@ -116,6 +134,8 @@ struct Round {
   int64_t* sub_offs = nullptr;  // (n_leaves+1), null when no leaf needed it
   int64_t n_sub = 0;
   int sub_level = 0;
+  // far-field local expansions (built on first use by a large eval; null = per-pair path)
+  FmmRound* fmm = nullptr;
 };
 
 }  // namespace gwn
@@ -145,6 +165,13 @@ struct gwn_scene {
   double* ff_lv = nullptr;      // (ff_n, kFFLevels) R^2 thresholds of the adaptive orders
   int32_t* ff_chord = nullptr;  // (ff_n) sliver entries: edge of the closing chord, else -1
   std::vector<double> ff_chord_host;  // (ff_n,6) chord start / end (world), zeros for cycles
+  // octree of the far field's local expansions (gwn_fmm.cu): cube, leaf level
+  // (0 = off) and, per (entry, level), the distance from a box centre beyond
+  // which the entry's translation into that box meets the error budget
+  // (+inf: never -- slivers and exact-only entries)
+  int fmm_L = 0;
+  double fmm_x0[3] = {0, 0, 0}, fmm_side = 0.0;
+  double* fmm_dmin = nullptr;   // (ff_n, fmm_L + 1)
   std::vector<double> ff_g_host;
   // per-round caches
   std::mutex mu;
@@ -232,6 +259,12 @@ cudaError_t launch_ff_order(const gwn_scene* sc, int32_t m, const int32_t* activ
                             const double* pos, void* scratch, int32_t* order, cudaStream_t st);
 size_t ff_order_scratch_bytes(int32_t m);
 cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st);  // gwn_boundary.cu
+// far-field local expansions (gwn_fmm.cu): scene-level acceptance table,
+// per-round octree build (caller holds sc->mu), release
+cudaError_t fmm_setup_scene(gwn_scene* sc, const std::vector<double>& rho,
+                            const std::vector<double>& aabs, const std::vector<char>& closed);
+cudaError_t build_fmm_round(const gwn_scene* sc, Round& rd, cudaStream_t st);
+void free_fmm_round(Round& rd);
 cudaError_t selftest_rsqrt(int64_t n, unsigned long long* max_ulp_host);
 cudaError_t launch_all_hits(const Round& rd, const DevParams& prm, const double* o, double t_lo,
                             double t_hi, double* out, int32_t* count, int32_t cap,

@@ -337,6 +337,10 @@ extern "C" int gwn_scene_create(const double* ctrl, int64_t P, const gwn_params*
   {
     std::lock_guard<std::mutex> lk(sc->mu);
     CK(build_round(sc, 0, 0));
+    // round 0's local expansions of the boundary far field (gwn_fmm.cu).
+    // Round 0 only: re-shoot rounds carry few queries and keep the per-pair
+    // path, so a query's treatment depends on its round, never on the batch.
+    if (sc->fmm_L > 0) CK(build_fmm_round(sc, sc->rounds[0], 0));
     CK(cudaDeviceSynchronize());
   }
   *out = sc;
@@ -376,6 +380,18 @@ extern "C" int gwn_scene_info_get(const gwn_scene* sc, gwn_scene_info* out) {
   out->device = sc->device;
   out->sm_count = sc->sm_count;
   out->n_far_cycles = sc->ff_n;
+  out->fmm_levels = 0;
+  out->pad_ = 0;
+  out->fmm_translations = out->fmm_leftover = 0;
+  out->fmm_build_ms = 0.0;
+  std::lock_guard<std::mutex> lk(const_cast<gwn_scene*>(sc)->mu);
+  if (!sc->rounds.empty() && sc->rounds[0].fmm) {
+    const gwn::FmmRound* F = sc->rounds[0].fmm;
+    out->fmm_levels = F->L;
+    out->fmm_translations = F->m2l_pairs;
+    out->fmm_leftover = F->leftover;
+    out->fmm_build_ms = F->ms_build;
+  }
   return GWN_OK;
 }
 

@@ -105,6 +105,15 @@ class Scene:
         return int(self.info.n_far_cycles)
 
     @property
+    def local_expansions(self) -> dict:
+        """Round 0's octree of far-field local expansions (DESIGN §2 K4): leaf
+        level (0 = none), (box, cycle) translations, entries left to the
+        per-query path over all leaves, build time at scene creation."""
+        i = self.info
+        return {"levels": int(i.fmm_levels), "translations": int(i.fmm_translations),
+                "leftover_entries": int(i.fmm_leftover), "build_ms": float(i.fmm_build_ms)}
+
+    @property
     def diag(self) -> float:
         return float(self.info.diag)
 

@@ -41,16 +41,19 @@ if mode == "halves":  # the same queries in two calls with global index bases
     w2, s2 = G.winding_numbers(sc, qd[h:], index_base=h)
     extra = dict(wh=torch.cat([w1, w2]).cpu().numpy(), sh=torch.cat([s1, s2]).cpu().numpy())
 np.savez(out, w=w.cpu().numpy(), st=st.cpu().numpy(), far=sc.stats()["far_pairs"],
-         cycles=sc.n_far_cycles, **extra)
+         cycles=sc.n_far_cycles, local=sc.stats()["local_evals"],
+         levels=sc.local_expansions["levels"], **extra)
 """
 
 
 def _run(tmp_path, cfg, nq, mode="plain", **env):
-    f = str(tmp_path / f"r{cfg}_{mode}_{len(env)}_{'_'.join(env.values())}.npz")
+    tag = "_".join(f"{k}{v}" for k, v in sorted(env.items()))
+    f = str(tmp_path / f"r{cfg}_{nq}_{mode}_{tag}.npz")
     e = dict(os.environ, **env)
     subprocess.run([sys.executable, "-c", _SCRIPT, REPO, str(cfg), str(nq), f, mode], env=e,
                    check=True, timeout=600)
-    return np.load(f)
+    with np.load(f) as z:
+        return {k: z[k] for k in z.files}
 
 
 def test_farfield_matches_exact_sum_config5(tmp_path):
@@ -62,6 +65,23 @@ def test_farfield_matches_exact_sum_config5(tmp_path):
     ok = ex["st"] == 0
     # truncation bound 1e-12 rad per cycle (DESIGN): |dw| far below the 1e-9 bar
     assert np.abs(ex["w"] - ff["w"])[ok].max() <= 1e-11
+
+
+def test_local_expansions_match_per_pair_far_field_and_exact_config5(tmp_path):
+    """Round 0's octree of local expansions (gwn_fmm.cu) against the per-pair
+    far field (GWN_FMM=0) and the exact sum (GWN_FARFIELD=0): each translated
+    (box, cycle) pair carries the per-pair path's 1e-12 bound."""
+    n = 1 << 14
+    ex = _run(tmp_path, 5, n, GWN_FARFIELD="0")
+    pp = _run(tmp_path, 5, n, GWN_FMM="0")
+    fm = _run(tmp_path, 5, n)
+    assert int(pp["levels"]) == 0 and int(pp["local"]) == 0
+    assert int(fm["levels"]) >= 2 and int(fm["local"]) >= n - 64  # queries inside the cube
+    assert int(fm["far"]) < int(pp["far"]) // 10   # most cycles came from the expansions
+    assert np.array_equal(ex["st"], fm["st"]) and np.array_equal(pp["st"], fm["st"])
+    ok = ex["st"] == 0
+    assert np.abs(fm["w"] - pp["w"])[ok].max() <= 1e-11
+    assert np.abs(fm["w"] - ex["w"])[ok].max() <= 1e-11
 
 
 def test_farfield_far_queries_single_cycle(tmp_path):

@@ -14,7 +14,7 @@ G.Scene(scenes.make(1, 8).ctrl)
 t = time.perf_counter()
 sc = G.Scene(s.ctrl)
 torch.cuda.synchronize()
-print(f"scene create {time.perf_counter()-t:.3f} s", flush=True)
+print(f"scene create {time.perf_counter()-t:.3f} s  local expansions {sc.local_expansions}", flush=True)
 q = torch.from_numpy(s.queries).cuda()
 for it in range(3):
     sc.set_timing(it == 2)
