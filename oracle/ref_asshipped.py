@@ -159,7 +159,8 @@ def _tess_w(ctrl, p, n):
         a = (i * (n + 1) + j).ravel()
         b = ((i + 1) * (n + 1) + j).ravel()
         T = np.concatenate([np.stack([a, b, b + 1], 1), np.stack([a, b + 1, a + 1], 1)])
-        tot += float(K._solid_angle_numpy(P, T.astype(np.int64), np.asarray(p, np.float64)))
+        tot += float(K._solid_angle_numpy(P, T.astype(np.int64), np.asarray(p, np.float64),
+                                          1e-12)[0])
     return tot / (4.0 * np.pi)
 
 

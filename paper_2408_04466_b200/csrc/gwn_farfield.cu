@@ -68,6 +68,7 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 }
 
 constexpr int kMomThreads = 128;
+constexpr size_t kMomSmem = sizeof(double) * (kMomThreads / 32) * 2 * kFFTerms;
 
 // D_n^m of one entry per block, as a line integral over its polyline.  R_n^m
 // is a harmonic homogeneous polynomial, so grad R = -curl(x * grad R)/(n+1)
@@ -86,7 +87,8 @@ k_ff_moments(const int64_t* __restrict__ coff, const int32_t* __restrict__ cedge
              const int32_t* __restrict__ chord, const double* __restrict__ verts, int64_t V,
              int S, const double* __restrict__ g, FFQuad Q, double* __restrict__ D) {
   constexpr int kW = kMomThreads / 32;
-  __shared__ double acc[kW][2 * kFFTerms];
+  extern __shared__ double mom_acc[];
+  double (*acc)[2 * kFFTerms] = reinterpret_cast<double (*)[2 * kFFTerms]>(mom_acc);
   const int c = blockIdx.x, wid = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < kW * 2 * kFFTerms; k += blockDim.x) (&acc[0][0])[k] = 0.0;
   __syncthreads();
@@ -425,7 +427,9 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   FF(cudaMemcpy(d_coff, coff.data(), sizeof(int64_t) * (nk + 1), cudaMemcpyHostToDevice));
   if (coff[nk] > 0)
     FF(cudaMemcpy(d_cedge, cedge.data(), sizeof(int32_t) * coff[nk], cudaMemcpyHostToDevice));
-  k_ff_moments<<<nk, kMomThreads>>>(d_coff, d_cedge, sc->ff_chord, sc->verts, V, S, sc->ff_g, ff_quad(),
+  FF(cudaFuncSetAttribute(k_ff_moments, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)kMomSmem));
+  k_ff_moments<<<nk, kMomThreads, kMomSmem>>>(d_coff, d_cedge, sc->ff_chord, sc->verts, V, S, sc->ff_g, ff_quad(),
                             sc->ff_D);
   FF(cudaGetLastError());
   FF(cudaDeviceSynchronize());
