@@ -453,16 +453,35 @@ __device__ __forceinline__ bool ff_far2(double qa, double qb, double qc,
   return R2 > __ldg(r2) && (l2 > line2 || (dz < 0.0 && __dmul_rn(dz, dz) > line2));
 }
 
+// Clenshaw coefficients of the irregular-harmonic recurrence (2n+1, (n+1)^2)
+struct FFClen {
+  double a[kFFK + 1], sq[kFFK + 2];
+};
+__constant__ FFClen c_ffc;
+
+cudaError_t ff_init_constants() {  // per device, before the first far-field launch
+  FFClen h;
+  for (int n = 0; n <= kFFK; ++n) h.a[n] = 2.0 * n + 1.0;
+  for (int n = 0; n <= kFFK + 1; ++n) h.sq[n] = (double)n * (double)n;
+  return cudaMemcpyToSymbol(c_ffc, &h, sizeof h);
+}
+
 // Omega(p) = -sum_{n>=1} [Re(D_n^0 I_n^0) + 2 sum_{m>=1} Re(D_n^m I_n^m)] of
-// order pl (<= P): the loops run to the warp's largest order P and a lane
-// adds only its own terms, so its sum is bit-identical to an order-pl
-// evaluation whatever its neighbours need (explicit roundings).  Runtime
-// loops: one copy of the code for every order (fully unrolled per-order
-// instantiations up to order 30 overflowed the instruction cache).
+// order pl (<= P).  Per column m, Clenshaw's backward sum over the
+// three-term recurrence I_{n+1}^m = alpha_n I_n^m + beta_n I_{n-1}^m
+// (alpha_n = (2n+1) z / r^2, beta_n = (m^2 - n^2) / r^2):
+//     b_n = D_n^m + alpha_n b_{n+1} + beta_{n+1} b_{n+2},  sum = b_m I_m^m,
+// six FP64 operations per term (the forward recurrence took ten); checked
+// against the forward sum to 7e-15 relative at 2.4 cycle radii
+// (tools/farfield/fmm_proto.py).  The loops run to the warp's largest order
+// P; a lane's coefficients above its own order pl are zero, so b stays +0
+// there and its sum is bit-identical to an order-pl evaluation whatever its
+// neighbours need.  Runtime loops: one copy of the code for every order.
 __device__ __forceinline__ double ff_eval_rt(double x, double y, double z,
                                              const double2* __restrict__ Dc, int P, int pl) {
   const double ir2 = __drcp_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)),
                                          __dmul_rn(z, z)));
+  const double zr = __dmul_rn(z, ir2);
   double dR = __dsqrt_rn(ir2), dI = 0.0;  // I_0^0 = 1/r
   double acc = 0.0;
 #pragma unroll 1
@@ -474,28 +493,83 @@ __device__ __forceinline__ double ff_eval_rt(double x, double y, double z,
       dR = nR;
       dI = nI;
     }
-    double aR = dR, aI = dI, bR = 0.0, bI = 0.0;
-    double col = 0.0;
-    if (mm > 0) {
-      const double2 d = __ldg(Dc + ff_term(mm, mm));
-      if (mm <= pl) col = __fma_rn(d.x, aR, __fma_rn(-d.y, aI, col));
-    }
-    const double m2 = (double)(mm * mm);
+    if (mm > pl) continue;  // the lane's column is empty (warp-uniform loop bounds kept)
+    const double m2r = __dmul_rn((double)(mm * mm), ir2);
+    double b1R = 0.0, b1I = 0.0, b2R = 0.0, b2I = 0.0;
+    const int nlo = mm > 0 ? mm : 1;  // n = 0 has no moment
 #pragma unroll 2
-    for (int n = mm + 1; n <= P; ++n) {
-      // I_n^m = ((2n-1) z I_{n-1}^m - ((n-1)^2 - m^2) I_{n-2}^m) / r^2
-      const double kz = __dmul_rn(2.0 * n - 1.0, z);
-      const double k2 = (double)((n - 1) * (n - 1)) - m2;
-      const double vR = __dmul_rn(__fma_rn(kz, aR, -__dmul_rn(k2, bR)), ir2);
-      const double vI = __dmul_rn(__fma_rn(kz, aI, -__dmul_rn(k2, bI)), ir2);
-      bR = aR;
-      bI = aI;
-      aR = vR;
-      aI = vI;
+    for (int n = P; n >= nlo; --n) {
       const double2 d = __ldg(Dc + ff_term(n, mm));
-      if (n <= pl) col = __fma_rn(d.x, aR, __fma_rn(-d.y, aI, col));
+      const double cR = n <= pl ? d.x : 0.0, cI = n <= pl ? d.y : 0.0;
+      const double al = __dmul_rn(c_ffc.a[n], zr);
+      const double be = __fma_rn(-c_ffc.sq[n + 1], ir2, m2r);
+      const double bR = __fma_rn(al, b1R, __fma_rn(be, b2R, cR));
+      const double bI = __fma_rn(al, b1I, __fma_rn(be, b2I, cI));
+      b2R = b1R;
+      b2I = b1I;
+      b1R = bR;
+      b1I = bI;
     }
-    if (mm <= pl) acc = __dadd_rn(acc, mm == 0 ? col : __dmul_rn(2.0, col));
+    if (mm == 0) {  // b_1 I_1^0 + beta_1 b_2 I_0^0 ... the column starts at n = 1
+      // sum_{n>=1} D_n^0 I_n^0 with the recurrence seeded at I_0^0: the
+      // Clenshaw sum from n = 1 is b_1 I_1^0 + beta_1 b_2 I_0^0, beta_1 = -1/r^2
+      const double i1 = __dmul_rn(zr, dR);  // I_1^0 = z / r^3 = (z/r^2) I_0^0
+      const double col = __fma_rn(b1R, i1, __dmul_rn(__dmul_rn(-ir2, b2R), dR));
+      acc = __dadd_rn(acc, col);
+    } else {
+      const double col = __fma_rn(b1R, dR, -__dmul_rn(b1I, dI));
+      acc = __dadd_rn(acc, __dmul_rn(2.0, col));
+    }
+  }
+  return -acc;
+}
+
+// ff_eval_rt at the lane's own order P = pl (no predication; the far-pair
+// lists give a warp one order): the same operations in the same order on the
+// lane's terms, so bit-identical to ff_eval_rt(x, y, z, Dc, P', P) for any
+// P' >= P.  Column pointers walk the (n, m) layout (ff_term(n,m) -
+// ff_term(n-1,m) = n).
+__device__ __forceinline__ double ff_eval_own(double x, double y, double z,
+                                              const double2* __restrict__ Dc, int P) {
+  const double ir2 = __drcp_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)),
+                                         __dmul_rn(z, z)));
+  const double zr = __dmul_rn(z, ir2);
+  double dR = __dsqrt_rn(ir2), dI = 0.0;
+  double acc = 0.0;
+#pragma unroll 1
+  for (int mm = 0; mm <= P; ++mm) {
+    if (mm > 0) {
+      const double c0 = __dmul_rn(-(2.0 * mm - 1.0), ir2);
+      const double nR = __dmul_rn(c0, __fma_rn(x, dR, -__dmul_rn(y, dI)));
+      const double nI = __dmul_rn(c0, __fma_rn(x, dI, __dmul_rn(y, dR)));
+      dR = nR;
+      dI = nI;
+    }
+    const double m2r = __dmul_rn((double)(mm * mm), ir2);
+    double b1R = 0.0, b1I = 0.0, b2R = 0.0, b2I = 0.0;
+    const int nlo = mm > 0 ? mm : 1;
+    const double2* dp = Dc + ff_term(P, mm);
+#pragma unroll 4
+    for (int n = P; n >= nlo; --n) {
+      const double2 d = __ldg(dp);
+      dp -= n;
+      const double al = __dmul_rn(c_ffc.a[n], zr);
+      const double be = __fma_rn(-c_ffc.sq[n + 1], ir2, m2r);
+      const double bR = __fma_rn(al, b1R, __fma_rn(be, b2R, d.x));
+      const double bI = __fma_rn(al, b1I, __fma_rn(be, b2I, d.y));
+      b2R = b1R;
+      b2I = b1I;
+      b1R = bR;
+      b1I = bI;
+    }
+    if (mm == 0) {
+      const double i1 = __dmul_rn(zr, dR);
+      const double col = __fma_rn(b1R, i1, __dmul_rn(__dmul_rn(-ir2, b2R), dR));
+      acc = __dadd_rn(acc, col);
+    } else {
+      const double col = __fma_rn(b1R, dR, -__dmul_rn(b1I, dI));
+      acc = __dadd_rn(acc, __dmul_rn(2.0, col));
+    }
   }
   return -acc;
 }
@@ -589,21 +663,44 @@ __device__ __forceinline__ unsigned ff_append(unsigned mask, int32_t c, unsigned
 // to its largest order P), plus a sliver's exact chord term (the edge's fan
 // sum = Omega(edge + chord back) + the chord's forward fan term, K4's shifted
 // form in the ray frame; den > 0: the half-line misses the sliver's sphere)
+// the lowest order level whose truncation bound holds at the pair's distance
+__device__ __forceinline__ int ff_level_of(const FFRound& R, const FFQuery& Q, int32_t c,
+                                           double& x, double& y, double& z) {
+  x = __dsub_rn(Q.px, __ldg(R.gw + 3 * c));
+  y = __dsub_rn(Q.py, __ldg(R.gw + 3 * c + 1));
+  z = __dsub_rn(Q.pz, __ldg(R.gw + 3 * c + 2));
+  const double R2 = __dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z));
+  const double* lv = R.lv + (int64_t)kFFLevels * c;
+  int lvl = kFFLevels - 1;
+#pragma unroll
+  for (int l = 0; l < kFFLevels - 1; ++l)
+    if (lvl == kFFLevels - 1 && R2 > __ldg(lv + l)) lvl = l;
+  return lvl;
+}
+
+__device__ __forceinline__ int ff_level(const FFRound& R, const FFQuery& Q, int32_t c) {
+  double x, y, z;
+  return ff_level_of(R, Q, c, x, y, z);
+}
+
+__device__ __forceinline__ double ff_chord_term(const FFRound& R, const FFQuery& Q, int32_t c) {
+  const double* A = R.ffa + 6 * (int64_t)c;
+  const double rax = __ldg(A) - Q.qa, ray = __ldg(A + 1) - Q.qb, raz = __ldg(A + 2) - Q.qc;
+  const double rbx = __ldg(A + 3) - Q.qa, rby = __ldg(A + 4) - Q.qb, rbz = __ldg(A + 5) - Q.qc;
+  const double ia = 1.0 / sqrt(rax * rax + ray * ray + raz * raz);
+  const double ib = 1.0 / sqrt(rbx * rbx + rby * rby + rbz * rbz);
+  const double uax = rax * ia, uay = ray * ia, uaz = fma(raz, ia, -1.0);
+  const double ubx = rbx * ib, uby = rby * ib, ubz = fma(rbz, ib, -1.0);
+  const double num = uay * ubx - uax * uby;
+  const double den = uax * ubx + uay * uby + uaz * ubz;
+  return 2.0 * atan2(num, den);
+}
+
 __device__ __forceinline__ double ff_pair_value(const FFRound& R, const FFQuery& Q, int32_t c,
                                                 bool far, int P, unsigned long long& terms) {
   int lvl = -1;
   double x = 1.0, y = 0.0, z = 0.0;
-  if (far) {
-    x = __dsub_rn(Q.px, __ldg(R.gw + 3 * c));
-    y = __dsub_rn(Q.py, __ldg(R.gw + 3 * c + 1));
-    z = __dsub_rn(Q.pz, __ldg(R.gw + 3 * c + 2));
-    const double R2 = __dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z));
-    const double* lv = R.lv + (int64_t)kFFLevels * c;
-    lvl = kFFLevels - 1;
-#pragma unroll
-    for (int l = 0; l < kFFLevels - 1; ++l)
-      if (lvl == kFFLevels - 1 && R2 > __ldg(lv + l)) lvl = l;
-  }
+  if (far) lvl = ff_level_of(R, Q, c, x, y, z);
   const int wl = __reduce_max_sync(0xffffffffu, (unsigned)(lvl + 1)) - 1;
   if (wl < 0) return 0.0;
   const double2* Dc = R.D + (int64_t)(far ? c : 0) * kFFTerms;
@@ -612,18 +709,7 @@ __device__ __forceinline__ double ff_pair_value(const FFRound& R, const FFQuery&
   (void)P;
   if (!far) return 0.0;
   terms += (unsigned long long)ff_nterms(pl);
-  if (__ldg(R.chord + c) >= 0) {
-    const double* A = R.ffa + 6 * (int64_t)c;
-    const double rax = __ldg(A) - Q.qa, ray = __ldg(A + 1) - Q.qb, raz = __ldg(A + 2) - Q.qc;
-    const double rbx = __ldg(A + 3) - Q.qa, rby = __ldg(A + 4) - Q.qb, rbz = __ldg(A + 5) - Q.qc;
-    const double ia = 1.0 / sqrt(rax * rax + ray * ray + raz * raz);
-    const double ib = 1.0 / sqrt(rbx * rbx + rby * rby + rbz * rbz);
-    const double uax = rax * ia, uay = ray * ia, uaz = fma(raz, ia, -1.0);
-    const double ubx = rbx * ib, uby = rby * ib, ubz = fma(rbz, ib, -1.0);
-    const double num = uay * ubx - uax * uby;
-    const double den = uax * ubx + uay * uby + uaz * ubz;
-    v = __dadd_rn(v, 2.0 * atan2(num, den));
-  }
+  if (__ldg(R.chord + c) >= 0) v = __dadd_rn(v, ff_chord_term(R, Q, c));
   return v;
 }
 
@@ -642,8 +728,8 @@ template <bool kWarp>
 __global__ void __launch_bounds__(kFFBlock)
 k_ff_count(int32_t m, const int32_t* __restrict__ order, const int32_t* __restrict__ active,
            const double* __restrict__ pos, Frame f, FFRound R, FFLocal F,
-           unsigned* __restrict__ qcnt, unsigned* __restrict__ ecnt,
-           unsigned long long* __restrict__ counters) {
+           unsigned* __restrict__ qcnt, unsigned* __restrict__ ecnt, unsigned* __restrict__ qfcnt,
+           unsigned* __restrict__ lcnt, unsigned long long* __restrict__ counters) {
   const FFQuery Q = ff_query<kWarp>(m, order, active, pos, f);
   const FFList L = ff_list(F, R.C, Q);
   const int lane = threadIdx.x & 31;
@@ -661,15 +747,25 @@ k_ff_count(int32_t m, const int32_t* __restrict__ order, const int32_t* __restri
     }
     return;
   }
+  unsigned nf = 0;
   const int jn = (int)__reduce_max_sync(0xffffffffu, Q.live ? (unsigned)L.n : 0u);
   for (int j = 0; j < jn; ++j) {  // warp-uniform loop
     const int32_t c = Q.live ? ff_entry(L, j) : -1;
-    const bool near = c >= 0 && !ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+    const bool far = c >= 0 && ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+    const bool near = c >= 0 && !far;
     n += near ? 1u : 0u;
     const unsigned b = __ballot_sync(0xffffffffu, near);
     if (near) ff_append(b, c, ecnt);
+    const unsigned fb = __ballot_sync(0xffffffffu, far);
+    if (far) {  // bucket (order level, entry): a warp of the eval shares both
+      ++nf;
+      ff_append(fb, ff_level(R, Q, c) * R.C + c, lcnt);
+    }
   }
-  if (Q.live) qcnt[Q.s] = n;
+  if (Q.live) {
+    qcnt[Q.s] = n;
+    qfcnt[Q.s] = nf;
+  }
   unsigned long long tot = n;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tot += __shfl_down_sync(0xffffffffu, tot, o);
@@ -685,8 +781,9 @@ __global__ void __launch_bounds__(kFFBlock)
 k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restrict__ active,
           const double* __restrict__ pos, Frame f, FFRound R, FFLocal F,
           const unsigned long long* __restrict__ eoff, unsigned* __restrict__ efill,
-          int2* __restrict__ recs, double* __restrict__ row_far,
-          unsigned long long* __restrict__ counters) {
+          int2* __restrict__ recs, const unsigned long long* __restrict__ loffs,
+          unsigned* __restrict__ lfill, int2* __restrict__ frecs, int32_t* __restrict__ fent,
+          double* __restrict__ row_far, unsigned long long* __restrict__ counters) {
   const FFQuery Q = ff_query<kWarp>(m, order, active, pos, f);
   const FFList L = ff_list(F, R.C, Q);
   const int lane = threadIdx.x & 31;
@@ -718,7 +815,7 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
     }
     if (Q.live && lane == 0) row_far[Q.s] = 0.5 * om;
   } else {
-    int k = 0;
+    int k = 0, kf = 0;
     const int jn = (int)__reduce_max_sync(0xffffffffu, Q.live ? (unsigned)L.n : 0u);
     for (int j = 0; j < jn; ++j) {  // warp-uniform loop
       const int32_t c = Q.live ? ff_entry(L, j) : -1;
@@ -730,14 +827,20 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
         recs[eoff[c] + slot] = make_int2(Q.s, k);
         ++k;
       }
-      const double v = ff_pair_value(R, Q, c, far, 0, terms);
+      // far: a record in its order level's bucket (k_ff_far_eval evaluates
+      // each bucket at one order); lanes of one leaf share c, so a warp's
+      // records of one level are contiguous
+      const unsigned fb = __ballot_sync(0xffffffffu, far);
       if (far) {
-        om = __dadd_rn(om, v);
-        ++nfar;
+        const int key = ff_level(R, Q, c) * R.C + c;
+        const unsigned slot = ff_append(fb, key, lfill);
+        frecs[loffs[key] + slot] = make_int2(Q.s, kf++);
+        fent[loffs[key] + slot] = c;
       }
     }
-    // K4's partials are sums of atan2 (half angles): Omega / 2
-    if (Q.live) row_far[Q.s] = 0.5 * om;
+    // the local expansion's value; k_ff_far_sum adds the far pairs in list
+    // order and halves (K4's partials are sums of atan2: Omega / 2)
+    if (Q.live) row_far[Q.s] = om;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -750,6 +853,53 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
     atomicAdd(&counters[CNT_FAR_TERMS], terms);
   }
   if (lane == 0 && nloc) atomicAdd(&counters[CNT_LOCAL], nloc);
+}
+
+// Far pairs of the per-thread path, one thread each, bucket by bucket
+// (buckets = (order level, entry): a warp's lanes agree on the order and
+// read the same moments): the pair's value into its query's far slots
+// (ordinal kf of the query's far pairs).
+__global__ void __launch_bounds__(kFFBlock)
+k_ff_far_eval(unsigned long long nrec, const int2* __restrict__ frecs,
+              const int32_t* __restrict__ fent, const int32_t* __restrict__ active,
+              const double* __restrict__ pos, Frame f, FFRound R,
+              const unsigned long long* __restrict__ qfoff, double* __restrict__ fval,
+              unsigned long long* __restrict__ counters) {
+  const unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = r < nrec;
+  const int2 rec = live ? frecs[r] : make_int2(0, 0);
+  const int32_t c = live ? fent[r] : 0;
+  const FFQuery Q = ff_query_at(live ? rec.x : 0, live ? rec.x + 1 : 0, nullptr, active, pos, f);
+  unsigned long long terms = 0;
+  double v = 0.0;
+  if (live) {
+    double x, y, z;
+    const int pl = ff_order(ff_level_of(R, Q, c, x, y, z));
+    v = ff_eval_own(x, y, z, R.D + (int64_t)c * kFFTerms, pl);
+    terms = (unsigned long long)ff_nterms(pl);
+    if (__ldg(R.chord + c) >= 0) v = __dadd_rn(v, ff_chord_term(R, Q, c));
+  }
+  if (live) fval[qfoff[rec.x] + (unsigned long long)rec.y] = v;
+  unsigned long long nf = live ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nf += __shfl_down_sync(0xffffffffu, nf, o);
+    terms += __shfl_down_sync(0xffffffffu, terms, o);
+  }
+  if ((threadIdx.x & 31) == 0 && nf) {
+    atomicAdd(&counters[CNT_FAR], nf);
+    atomicAdd(&counters[CNT_FAR_TERMS], terms);
+  }
+}
+
+// per query: local expansion value + far pairs in list order, halved
+__global__ void k_ff_far_sum(int32_t m, const unsigned long long* __restrict__ qfoff,
+                             const double* __restrict__ fval, double* __restrict__ row) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  double a = row[s];
+  for (unsigned long long p = qfoff[s]; p < qfoff[s + 1]; ++p) a = __dadd_rn(a, fval[p]);
+  row[s] = 0.5 * a;
 }
 
 // tiles of kBlockQ * kQPT near pairs per entry
@@ -861,8 +1011,19 @@ struct FFCache {
   unsigned long long* toff = nullptr;    // (C+1)
   int2* recs = nullptr;                  // (pairs)
   double* ang = nullptr;                 // (pairs)
+  // far pairs of the per-thread path
+  size_t cap_f = 0;
+  unsigned* qfcnt = nullptr;             // (m+1)
+  unsigned long long* qfoff = nullptr;   // (m+1)
+  size_t cap_k = 0;
+  unsigned* lcnt = nullptr;              // (kFFLevels*C + 1) bucket sizes
+  unsigned* lfill = nullptr;             // (kFFLevels*C) bucket cursors
+  unsigned long long* loffs = nullptr;   // (kFFLevels*C + 1)
+  int2* frecs = nullptr;                 // (far pairs) (slot, ordinal)
+  int32_t* fent = nullptr;               // (far pairs) entry
+  double* fval = nullptr;                // (far pairs) values by (query, ordinal)
   void* tmp = nullptr;
-  unsigned long long* h = nullptr;       // pinned: [0] pairs, [1] tiles
+  unsigned long long* h = nullptr;       // pinned: [0] pairs, [1] tiles, [2] far pairs
 };
 static thread_local FFCache t_ffc[64];
 
@@ -884,6 +1045,7 @@ static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int3
                                       cudaStream_t st, const int32_t* order, cudaEvent_t* evb) {
   FFCache& c = t_ffc[sc->device & 63];
   const int32_t C = sc->ff_n;
+  const int nkey = kFFLevels * C;  // far-pair buckets (order level, entry)
   const int64_t V = sc->n_edges * sc->S;
   const int tp = kBlockQ * kQPT;
   cudaError_t e = cudaSuccess;
@@ -897,7 +1059,18 @@ static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int3
     FC(ff_grow(c.qcnt, capq, (size_t)m + 1, sizeof(unsigned), st));
     capq = c.cap_q;
     FC(ff_grow(c.qoff, capq, (size_t)m + 1, sizeof(unsigned long long), st));
+    capq = c.cap_q;
+    FC(ff_grow(c.qfcnt, capq, (size_t)m + 1, sizeof(unsigned), st));
+    capq = c.cap_q;
+    FC(ff_grow(c.qfoff, capq, (size_t)m + 1, sizeof(unsigned long long), st));
     c.cap_q = capq;
+    size_t capk = c.cap_k;
+    FC(ff_grow(c.lcnt, capk, (size_t)nkey + 1, sizeof(unsigned), st));
+    capk = c.cap_k;
+    FC(ff_grow(c.lfill, capk, (size_t)nkey + 1, sizeof(unsigned), st));
+    capk = c.cap_k;
+    FC(ff_grow(c.loffs, capk, (size_t)nkey + 1, sizeof(unsigned long long), st));
+    c.cap_k = capk;
     size_t capc = c.cap_c;
     FC(ff_grow(c.ecnt, capc, (size_t)C + 1, sizeof(unsigned), st));
     capc = c.cap_c;
@@ -910,10 +1083,11 @@ static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int3
     FC(ff_grow(c.toff, capc, (size_t)C + 1, sizeof(unsigned long long), st));
     c.cap_c = capc;
   }
-  size_t tb1 = 0, tb2 = 0;
+  size_t tb1 = 0, tb2 = 0, tb3 = 0;
   FC(cub::DeviceScan::ExclusiveSum(nullptr, tb1, c.qcnt, c.qoff, m + 1, st));
   FC(cub::DeviceScan::ExclusiveSum(nullptr, tb2, c.ecnt, c.eoff, C + 1, st));
-  FC(ff_grow(c.tmp, c.cap_tmp, std::max(tb1, tb2), 1, st));
+  FC(cub::DeviceScan::ExclusiveSum(nullptr, tb3, c.lcnt, c.loffs, nkey + 1, st));
+  FC(ff_grow(c.tmp, c.cap_tmp, std::max(std::max(tb1, tb2), tb3), 1, st));
   const FFRound R{C, rd.ffg, sc->ff_r, sc->ff_lv, sc->ff_g,
                   reinterpret_cast<const double2*>(sc->ff_D), sc->ff_chord, rd.ffa};
   FFLocal F;
@@ -932,19 +1106,29 @@ static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int3
   FC(cudaMemsetAsync(c.ecnt, 0, sizeof(unsigned) * (C + 1), st));
   FC(cudaMemsetAsync(c.efill, 0, sizeof(unsigned) * (C + 1), st));
   FC(cudaMemsetAsync(c.qcnt + m, 0, sizeof(unsigned), st));
+  FC(cudaMemsetAsync(c.qfcnt + m, 0, sizeof(unsigned), st));
+  FC(cudaMemsetAsync(c.lcnt, 0, sizeof(unsigned) * (nkey + 1), st));
   // small rounds (re-shoots): a warp per query, so the few queries' pairs
-  // spread over the GPU instead of serialising in one block
+  // spread over the GPU instead of serialising in one block; it evaluates its
+  // far pairs in place (no far-pair lists)
   const bool per_warp = (int64_t)m * 32 <= (int64_t)kFFWarpRoundThreads;
   const unsigned g = per_warp ? (unsigned)(((int64_t)m * 32 + kFFBlock - 1) / kFFBlock)
                               : (unsigned)((m + kFFBlock - 1) / kFFBlock);
   if (per_warp)
     k_ff_count<true><<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, F, c.qcnt, c.ecnt,
-                                             counters);
+                                             c.qfcnt, c.lcnt, counters);
   else
     k_ff_count<false><<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, F, c.qcnt,
-                                              c.ecnt, counters);
+                                              c.ecnt, c.qfcnt, c.lcnt, counters);
   FC(cudaGetLastError());
   FC(cub::DeviceScan::ExclusiveSum(c.tmp, tb1, c.qcnt, c.qoff, m + 1, st));
+  if (!per_warp) {
+    FC(cub::DeviceScan::ExclusiveSum(c.tmp, tb1, c.qfcnt, c.qfoff, m + 1, st));
+    FC(cub::DeviceScan::ExclusiveSum(c.tmp, tb3, c.lcnt, c.loffs, nkey + 1, st));
+    FC(cudaMemsetAsync(c.lfill, 0, sizeof(unsigned) * nkey, st));
+    FC(cudaMemcpyAsync(c.h + 2, c.qfoff + m, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       st));
+  }
   FC(cub::DeviceScan::ExclusiveSum(c.tmp, tb2, c.ecnt, c.eoff, C + 1, st));
   k_ff_tiles<<<(C + 255) / 256, 256, 0, st>>>(C + 1, c.ecnt, tp, c.tcnt);
   FC(cudaGetLastError());
@@ -955,22 +1139,40 @@ static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int3
   FC(cudaMemcpyAsync(c.h + 1, c.toff + C, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                      st));
   FC(cudaStreamSynchronize(st));
-  const unsigned long long pairs = c.h[0], tiles = c.h[1];
+  const unsigned long long pairs = c.h[0], tiles = c.h[1], fpairs = per_warp ? 0 : c.h[2];
   {
     size_t capp = c.cap_p;
     FC(ff_grow(c.recs, capp, (size_t)pairs + 1, sizeof(int2), st));
     capp = c.cap_p;
     FC(ff_grow(c.ang, capp, (size_t)pairs + 1, sizeof(double), st));
     c.cap_p = capp;
+    size_t capf = c.cap_f;
+    FC(ff_grow(c.frecs, capf, (size_t)fpairs + 1, sizeof(int2), st));
+    capf = c.cap_f;
+    FC(ff_grow(c.fent, capf, (size_t)fpairs + 1, sizeof(int32_t), st));
+    capf = c.cap_f;
+    FC(ff_grow(c.fval, capf, (size_t)fpairs + 1, sizeof(double), st));
+    c.cap_f = capf;
   }
   if (evb) FC(cudaEventRecord(evb[0], st));
   if (per_warp)
     k_ff_fill<true><<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, F, c.eoff, c.efill,
-                                            c.recs, bpart, counters);
+                                            c.recs, c.loffs, c.lfill, c.frecs, c.fent, bpart,
+                                            counters);
   else
     k_ff_fill<false><<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, F, c.eoff, c.efill,
-                                             c.recs, bpart, counters);
+                                             c.recs, c.loffs, c.lfill, c.frecs, c.fent, bpart,
+                                             counters);
   FC(cudaGetLastError());
+  if (!per_warp) {
+    if (fpairs > 0) {
+      k_ff_far_eval<<<(unsigned)((fpairs + kFFBlock - 1) / kFFBlock), kFFBlock, 0, st>>>(
+          fpairs, c.frecs, c.fent, active, pos, rd.f, R, c.qfoff, c.fval, counters);
+      FC(cudaGetLastError());
+    }
+    k_ff_far_sum<<<(m + 255) / 256, 256, 0, st>>>(m, c.qfoff, c.fval, bpart);
+    FC(cudaGetLastError());
+  }
   if (evb) FC(cudaEventRecord(evb[1], st));
   if (tiles > 0) {
     k_ff_near<kQPT><<<(unsigned)tiles, kBlockQ, 0, st>>>(

@@ -423,11 +423,13 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   Workspace ws;
   ws.st = st;
   const bool host = (flags & GWN_HOST_BUFFERS) != 0;
-  // auto chunk: 4M queries (2M when the boundary partials are wide; 8M for
-  // far-field scenes, whose Morton-ordered K4 warps agree more often in larger
-  // chunks -- config 5 at 2^23 queries: 1254 -> 1086 ms)
+  // auto chunk: 4M queries (2M when the boundary partials are wide; 64M for
+  // far-field scenes: a local-expansion leaf's queries share one warp's list
+  // only when the leaves are well filled, and every chunk pays the re-shoot
+  // rounds' latency -- config 5 at 2^26 queries: 1071 ms in 8M chunks, 930 ms
+  // in one)
   const int64_t chunk_max = sc->prm.chunk_queries > 0 ? sc->prm.chunk_queries
-                            : sc->ff_n > 0               ? (1ll << 23)
+                            : sc->ff_n > 0               ? (1ll << 26)
                             : boundary_chunks(sc, 0) > 16 ? (1ll << 21)
                                                           : (1ll << 22);
   // device scalar block, published to mapped pinned memory once per round
@@ -506,8 +508,11 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         const long long v = e ? atoll(e) : 6;
         return (int64_t)(v < 1 ? 1 : v);
       }();
+      // far-field scenes: two parts (their steps are long next to the copies,
+      // and larger chunks keep the local-expansion leaves' warps uniform)
+      const int64_t np = sc->ff_n > 0 && !getenv("GWN_PIPE_CHUNKS") ? 2 : parts;
       const int64_t pc =
-          (std::max<int64_t>(1ll << 16, (n + parts - 1) / parts) + 1023) & ~1023ll;
+          (std::max<int64_t>(1ll << 16, (n + np - 1) / np) + 1023) & ~1023ll;
       cm = std::min(cm, pc);
       if (!cs_in) {
         CKE(cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking));
@@ -651,7 +656,8 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
           }
           CKE(launch_boundary(sc, rd, m, active, rpos, bterm, nchunk, fl, d_cnt, st, ord,
                               sc->timed && sc->ff_n > 0 ? evb : nullptr));
-          launches += sc->ff_n > 0 ? 5 : 1;  // far-field: count, tiles, fill, near, near sum
+          launches += sc->ff_n > 0 ? 8 : 1;  // far-field: count, levels, tiles, fill, far eval,
+                                            // far sum, near, near sum
         }
         if (sc->timed) CKE(cudaEventRecord(ev[3], st));
         // ---- K5: finalize / compact re-shoots (after the K3 side stream)

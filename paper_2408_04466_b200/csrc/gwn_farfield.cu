@@ -220,6 +220,10 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   const int64_t ne = sc->n_edges;
   const int S = sc->S;
   if (ne <= 0) return cudaSuccess;
+  {
+    const cudaError_t ec = ff_init_constants();
+    if (ec != cudaSuccess) return ec;
+  }
   // cycles: union-find over the edges' end points (bitwise shared lattice points)
   std::map<std::array<double, 3>, int> pid;
   std::vector<int> ea(ne), eb(ne);

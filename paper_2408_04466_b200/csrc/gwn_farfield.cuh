@@ -30,11 +30,11 @@
 
 namespace gwn {
 
-// expansion order of the per-pair path: order 40 brings R_min down to ~2.4
-// cycle radii (order 20: ~4.3), so ~3.5x fewer (query, cycle) pairs at
-// config 5 need the exact sum; pairs farther out use the lowest sufficient
-// order (kFFLevels)
-constexpr int kFFK = 40;
+// expansion order of the per-pair path: order 48 brings R_min down to ~2.2
+// cycle radii (order 20: ~4.3), so ~4x fewer (query, cycle) pairs at config
+// 5 need the exact sum; pairs farther out use the lowest sufficient order
+// (kFFLevels)
+constexpr int kFFK = 48;
 constexpr int kFFTerms = (kFFK + 1) * (kFFK + 2) / 2;  // (n, m), 0 <= m <= n <= K
 constexpr double kFFTau = 1e-12;                       // truncation bound per cycle (rad)
 // far-field partial rows: cycle groups summed in fixed order by K5, so the
@@ -42,7 +42,7 @@ constexpr double kFFTau = 1e-12;                       // truncation bound per c
 constexpr int kFFRows = 16;
 // adaptive order: a far pair uses the lowest of these orders whose bound
 // holds at its distance (per-cycle thresholds, Scene::ff_lv)
-constexpr int kFFLevels = 8;  // orders 12, 16, ..., 40
+constexpr int kFFLevels = 10;  // orders 12, 16, ..., 48
 __host__ __device__ constexpr int ff_order(int lv) { return kFFK - 4 * (kFFLevels - 1 - lv); }
 
 __host__ __device__ __forceinline__ constexpr int ff_term(int n, int m) {

@@ -254,6 +254,7 @@ cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             cudaEvent_t* evb = nullptr);                      // gwn_boundary.cu
 int boundary_chunks(const gwn_scene* sc, int32_t m);  // partial rows (exact chunks + far row)
 cudaError_t build_farfield(gwn_scene* sc, const double* ectrl);     // gwn_farfield.cu
+cudaError_t ff_init_constants();                                   // gwn_boundary.cu
 void free_farfield(gwn_scene* sc);
 cudaError_t launch_ff_order(const gwn_scene* sc, int32_t m, const int32_t* active,
                             const double* pos, void* scratch, int32_t* order, cudaStream_t st);

@@ -8,11 +8,12 @@ from paper_2408_04466_b200 import scenes
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 nq = int(sys.argv[2]) if len(sys.argv) > 2 else (1 << 26)
+chunk = int(sys.argv[3]) if len(sys.argv) > 3 else 0   # 0: the engine's default
 s = scenes.make(cfg, nq)
 torch.cuda.init()
 G.Scene(scenes.make(1, 8).ctrl)
 t = time.perf_counter()
-sc = G.Scene(s.ctrl)
+sc = G.Scene(s.ctrl, chunk_queries=chunk)
 torch.cuda.synchronize()
 print(f"scene create {time.perf_counter()-t:.3f} s  local expansions {sc.local_expansions}", flush=True)
 q = torch.from_numpy(s.queries).cuda()
