@@ -525,50 +525,84 @@ __device__ __forceinline__ double ff_eval_rt(double x, double y, double z,
 }
 
 // ff_eval_rt at the lane's own order P = pl (no predication; the far-pair
-// lists give a warp one order): the same operations in the same order on the
-// lane's terms, so bit-identical to ff_eval_rt(x, y, z, Dc, P', P) for any
-// P' >= P.  Column pointers walk the (n, m) layout (ff_term(n,m) -
-// ff_term(n-1,m) = n).
+// lists give a warp one order), four columns m at a time: they share the
+// loop, the loads of the recurrence constants and alpha_n = (2n+1) z / r^2.
+// Each column runs the same operations in the same order as in ff_eval_rt
+// and the columns are added in increasing m, so the value is bit-identical to
+// ff_eval_rt(x, y, z, Dc, P', P) for any P' >= P.
+struct FFCol {
+  double b1R, b1I, b2R, b2I;
+};
+
+__device__ __forceinline__ void ff_col_step(FFCol& c, double2 d, double al, double be) {
+  const double bR = __fma_rn(al, c.b1R, __fma_rn(be, c.b2R, d.x));
+  const double bI = __fma_rn(al, c.b1I, __fma_rn(be, c.b2I, d.y));
+  c.b2R = c.b1R;
+  c.b2I = c.b1I;
+  c.b1R = bR;
+  c.b1I = bI;
+}
+
 __device__ __forceinline__ double ff_eval_own(double x, double y, double z,
-                                              const double2* __restrict__ Dc, int P) {
+                                              const double2* Dc, int P) {
   const double ir2 = __drcp_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)),
                                          __dmul_rn(z, z)));
   const double zr = __dmul_rn(z, ir2);
-  double dR = __dsqrt_rn(ir2), dI = 0.0;
+  double dR = __dsqrt_rn(ir2), dI = 0.0;  // I_m^m of the next column
   double acc = 0.0;
 #pragma unroll 1
-  for (int mm = 0; mm <= P; ++mm) {
-    if (mm > 0) {
-      const double c0 = __dmul_rn(-(2.0 * mm - 1.0), ir2);
-      const double nR = __dmul_rn(c0, __fma_rn(x, dR, -__dmul_rn(y, dI)));
-      const double nI = __dmul_rn(c0, __fma_rn(x, dI, __dmul_rn(y, dR)));
-      dR = nR;
-      dI = nI;
+  for (int m0 = 0; m0 <= P; m0 += 4) {
+    FFCol col[4];
+    double m2r[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      col[i] = FFCol{0.0, 0.0, 0.0, 0.0};
+      m2r[i] = __dmul_rn((double)((m0 + i) * (m0 + i)), ir2);
     }
-    const double m2r = __dmul_rn((double)(mm * mm), ir2);
-    double b1R = 0.0, b1I = 0.0, b2R = 0.0, b2I = 0.0;
-    const int nlo = mm > 0 ? mm : 1;
-    const double2* dp = Dc + ff_term(P, mm);
-#pragma unroll 4
-    for (int n = P; n >= nlo; --n) {
-      const double2 d = __ldg(dp);
-      dp -= n;
+    // n from P down to m0 + 3: all four columns (when they exist)
+    const int nall = m0 + 3;
+    const double2* dp = Dc + ff_term(P, m0);
+#pragma unroll 2
+    for (int n = P; n >= nall; --n) {
       const double al = __dmul_rn(c_ffc.a[n], zr);
-      const double be = __fma_rn(-c_ffc.sq[n + 1], ir2, m2r);
-      const double bR = __fma_rn(al, b1R, __fma_rn(be, b2R, d.x));
-      const double bI = __fma_rn(al, b1I, __fma_rn(be, b2I, d.y));
-      b2R = b1R;
-      b2I = b1I;
-      b1R = bR;
-      b1I = bI;
+      const double sq = c_ffc.sq[n + 1];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        ff_col_step(col[i], dp[i], al, __fma_rn(-sq, ir2, m2r[i]));
+      dp -= n;
     }
-    if (mm == 0) {
-      const double i1 = __dmul_rn(zr, dR);
-      const double col = __fma_rn(b1R, i1, __dmul_rn(__dmul_rn(-ir2, b2R), dR));
-      acc = __dadd_rn(acc, col);
-    } else {
-      const double col = __fma_rn(b1R, dR, -__dmul_rn(b1I, dI));
-      acc = __dadd_rn(acc, __dmul_rn(2.0, col));
+    // the tail: column m0 + i ends at n = m0 + i (n = 0 has no moment)
+#pragma unroll
+    for (int t = 2; t >= 0; --t) {
+      const int n = m0 + t;
+      if (n > P || n < 1) continue;
+      const double al = __dmul_rn(c_ffc.a[n], zr);
+      const double sq = c_ffc.sq[n + 1];
+      const double2* dn = Dc + ff_term(n, m0);
+#pragma unroll
+      for (int i = 0; i <= t; ++i)
+        ff_col_step(col[i], dn[i], al, __fma_rn(-sq, ir2, m2r[i]));
+    }
+    // column sums in increasing m
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int mm = m0 + i;
+      if (mm > P) break;
+      if (mm > 0) {  // I_m^m = -(2m-1)(x+iy)/r^2 I_{m-1}^{m-1}
+        const double c0 = __dmul_rn(-(2.0 * mm - 1.0), ir2);
+        const double nR = __dmul_rn(c0, __fma_rn(x, dR, -__dmul_rn(y, dI)));
+        const double nI = __dmul_rn(c0, __fma_rn(x, dI, __dmul_rn(y, dR)));
+        dR = nR;
+        dI = nI;
+      }
+      if (mm == 0) {
+        const double i1 = __dmul_rn(zr, dR);
+        const double cs = __fma_rn(col[0].b1R, i1, __dmul_rn(__dmul_rn(-ir2, col[0].b2R), dR));
+        acc = __dadd_rn(acc, cs);
+      } else {
+        const double cs = __fma_rn(col[i].b1R, dR, -__dmul_rn(col[i].b1I, dI));
+        acc = __dadd_rn(acc, __dmul_rn(2.0, cs));
+      }
     }
   }
   return -acc;
@@ -865,17 +899,37 @@ k_ff_far_eval(unsigned long long nrec, const int2* __restrict__ frecs,
               const double* __restrict__ pos, Frame f, FFRound R,
               const unsigned long long* __restrict__ qfoff, double* __restrict__ fval,
               unsigned long long* __restrict__ counters) {
-  const unsigned long long r = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // the block's records share one entry almost always (buckets hold
+  // thousands): its moments are staged in shared memory, read as broadcasts
+  __shared__ double2 sD[kFFTerms];
+  __shared__ int32_t s_c[2];
+  const unsigned long long r0 = (unsigned long long)blockIdx.x * blockDim.x;
+  const unsigned long long r = r0 + threadIdx.x;
   const bool live = r < nrec;
   const int2 rec = live ? frecs[r] : make_int2(0, 0);
   const int32_t c = live ? fent[r] : 0;
+  if (threadIdx.x == 0) {
+    const unsigned long long rl = min(nrec, r0 + blockDim.x) - 1;
+    s_c[0] = fent[r0];
+    s_c[1] = fent[rl];
+  }
+  __syncthreads();
+  const bool staged = s_c[0] == s_c[1];
+  if (staged) {
+    const double2* src = R.D + (int64_t)s_c[0] * kFFTerms;
+    for (int q = threadIdx.x; q < kFFTerms; q += blockDim.x) sD[q] = __ldg(src + q);
+  }
+  __syncthreads();
   const FFQuery Q = ff_query_at(live ? rec.x : 0, live ? rec.x + 1 : 0, nullptr, active, pos, f);
   unsigned long long terms = 0;
   double v = 0.0;
   if (live) {
     double x, y, z;
     const int pl = ff_order(ff_level_of(R, Q, c, x, y, z));
-    v = ff_eval_own(x, y, z, R.D + (int64_t)c * kFFTerms, pl);
+    if (staged)  // two inlined copies: shared-memory loads here, global below
+      v = ff_eval_own(x, y, z, sD, pl);
+    else
+      v = ff_eval_own(x, y, z, R.D + (int64_t)c * kFFTerms, pl);
     terms = (unsigned long long)ff_nterms(pl);
     if (__ldg(R.chord + c) >= 0) v = __dadd_rn(v, ff_chord_term(R, Q, c));
   }
