@@ -406,6 +406,11 @@ k_boundary_e(int32_t m, const int32_t* __restrict__ active, const double* __rest
 #define GWN_K4_QPT 2
 #endif
 constexpr int kQPT = GWN_K4_QPT;
+// the far-field scenes' exact kernel (k_ff_near): one pair per thread at four
+// 256-thread blocks per SM (config 5 at 2^24: 111.6 -> 104.1 ms against
+// two pairs per thread at two blocks; tools/k4_variants.py)
+constexpr int kNearQPT = 1;
+constexpr int kNearMinBlocks = 4;
 
 // ---------------------------------------------------------------------------
 // Far-field scenes (entries built by gwn_farfield.cu).  Per round and chunk:
@@ -956,7 +961,7 @@ __global__ void k_ff_far_sum(int32_t m, const unsigned long long* __restrict__ q
   row[s] = 0.5 * a;
 }
 
-// tiles of kBlockQ * kQPT near pairs per entry
+// tiles of kBlockQ * kNearQPT near pairs per entry
 __global__ void k_ff_tiles(int32_t C, const unsigned* __restrict__ ecnt, int tp,
                            unsigned* __restrict__ tcnt) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -964,7 +969,7 @@ __global__ void k_ff_tiles(int32_t C, const unsigned* __restrict__ ecnt, int tp,
 }
 
 template <int QPT>
-__global__ void __launch_bounds__(kBlockQ, GWN_K4_MINB)
+__global__ void __launch_bounds__(kBlockQ, kNearMinBlocks)
 k_ff_near(int32_t C, const unsigned long long* __restrict__ toff,
           const unsigned long long* __restrict__ eoff, const int32_t* __restrict__ ent_eoff,
           const int2* __restrict__ recs, const unsigned long long* __restrict__ qoff,
@@ -1101,7 +1106,7 @@ static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int3
   const int32_t C = sc->ff_n;
   const int nkey = kFFLevels * C;  // far-pair buckets (order level, entry)
   const int64_t V = sc->n_edges * sc->S;
-  const int tp = kBlockQ * kQPT;
+  const int tp = kBlockQ * kNearQPT;
   cudaError_t e = cudaSuccess;
 #define FC(x)                              \
   do {                                     \
@@ -1229,7 +1234,7 @@ static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int3
   }
   if (evb) FC(cudaEventRecord(evb[1], st));
   if (tiles > 0) {
-    k_ff_near<kQPT><<<(unsigned)tiles, kBlockQ, 0, st>>>(
+    k_ff_near<kNearQPT><<<(unsigned)tiles, kBlockQ, 0, st>>>(
         C, c.toff, c.eoff, sc->ff_eoff, c.recs, c.qoff, active, pos, rd.vproj, V, sc->S,
         sc->band_h, rd.f, sc->dprm, c.ang, flags, counters);
     FC(cudaGetLastError());
