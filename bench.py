@@ -52,9 +52,10 @@ FLOP_NEWTON = 220.0    # K3 Newton iteration (220 per N_newton)
 FLOP_ROOT = 200.0      # K3 accepted root (200 per N_root)
 FLOP_SEGMENT = 34.0    # K4 exact, per (query, net segment) in the ray frame: vertex (3 sub,
                        # |r|^2 5, rsqrt seed + Halley 8, u 4) + num 3, den 5, complex product 6
-FLOP_TERM = 12.0       # K4 far field, per solid-harmonic term: complex recurrence 8 +
-                       # complex multiply-add 4
+FLOP_TERM = 10.0       # K4 far field, per multipole term (Clenshaw, gwn_boundary.cu):
+                       # b = D + alpha b1 + beta b2 on a complex b (4 FMA) + beta (1 FMA)
 L2P_TERMS = 231        # terms of one order-20 local expansion (j <= 20, 0 <= k <= j)
+FLOP_L2P = 12.0        # per local-expansion term: complex recurrence 8 + multiply-add 4
 
 CONFIG_DESC = {
     1: "config1: single open bicubic patch, 4096 queries U[-0.5,1.5]^3",
@@ -385,10 +386,11 @@ def rooflines(stt: dict, peak_tf: float, ms_step: float, config: int) -> dict:
             "k_ff_near"),
         "k_ff_fill (K4 far field)": (
             stt.get("ms_k4_far", 0.0),
-            (stt.get("far_terms", 0) + stt.get("local_evals", 0) * L2P_TERMS) * FLOP_TERM,
-            f"{int(stt.get('far_terms', 0))} multipole terms ({int(stt['far_pairs'])} per-pair far "
-            f"(query, cycle) expansions) + {int(stt.get('local_evals', 0))} local expansions x "
-            f"{L2P_TERMS} terms, x {FLOP_TERM:.0f} flop per term", "k_ff_fill"),
+            stt.get("far_terms", 0) * FLOP_TERM + stt.get("local_evals", 0) * L2P_TERMS * FLOP_L2P,
+            f"{int(stt.get('far_terms', 0))} multipole terms x {FLOP_TERM:.0f} flop "
+            f"({int(stt['far_pairs'])} per-pair far (query, cycle) expansions) + "
+            f"{int(stt.get('local_evals', 0))} local expansions x {L2P_TERMS} terms x "
+            f"{FLOP_L2P:.0f} flop", "k_ff_fill"),
         "k3_newton (K3 Newton + record)": (
             stt["ms_k3_newton"], stt["newton_iters"] * FLOP_NEWTON + stt["roots"] * FLOP_ROOT,
             f"{int(stt['newton_iters'])} iterations x {FLOP_NEWTON:.0f} + {int(stt['roots'])} "
@@ -632,6 +634,14 @@ def main():
             except Exception as e:  # the reference package travels in baseline/_ref
                 out["as_shipped_reference"] = {"unavailable": f"{type(e).__name__}: {e}"}
     if world == 1 and not args.no_extras:
+        # the side measurements build their own scenes: release the headline
+        # job's scene and cached 2^26-query workspace first
+        del sc, q_dev, w_dev, st_dev, flush, pbuf, w_pk, st_pk, g_all
+        import gc
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        G.release_caches(local)
         extra = {}
         for cfg in (2, 3, 4):
             if cfg != args.config:

@@ -230,6 +230,10 @@ int64_t gwn_ray_tris_hits(const gwn_tri_bvh* bvh, const double* origins, const d
                           double plane_tol, int64_t* offs, double* ts, int64_t* tris,
                           double* dotdn, double* us, double* vs, int64_t cap, int device);
 
+/* Free this host thread's cached eval workspace on `device` (gwn_eval keeps
+ * its buffers at the largest batch seen, for the next call). */
+int gwn_release_caches(int device);
+
 /* Host-side helpers shared with the oracle contract (no device needed). */
 void gwn_direction(uint64_t seed, int32_t round, double d[3]);
 void gwn_jitter_dir(uint64_t seed, int64_t qidx, int32_t attempt, double v[3]);

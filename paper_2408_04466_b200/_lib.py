@@ -33,7 +33,7 @@ EXPORTS = (
     "gwn_scene_destroy", "gwn_scene_info_get", "gwn_eval", "gwn_stats_get", "gwn_set_timing",
     "gwn_all_hits", "gwn_single_loop_batch", "gwn_direction", "gwn_jitter_dir",
     "gwn_net_boundary", "gwn_fp64_peak", "gwn_selftest_rsqrt", "gwn_eval_rays",
-    "gwn_solid_angle_many", "gwn_ray_tris_hits",
+    "gwn_solid_angle_many", "gwn_ray_tris_hits", "gwn_release_caches",
 )
 
 
@@ -139,6 +139,8 @@ def lib() -> C.CDLL:
                                         C.c_double, C.c_double, C.c_double, ip, dp, ip, dp,
                                         dp, dp, C.c_int64, C.c_int]
         L.gwn_ray_tris_hits.restype = C.c_int64
+        L.gwn_release_caches.argtypes = [C.c_int]
+        L.gwn_release_caches.restype = C.c_int
         _lib = L
     return _lib
 

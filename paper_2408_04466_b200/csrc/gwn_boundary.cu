@@ -1086,6 +1086,17 @@ struct FFCache {
 };
 static thread_local FFCache t_ffc[64];
 
+void release_boundary_caches(int device) {
+  FFCache& c = t_ffc[device & 63];
+  void* ps[] = {c.qcnt, c.qoff, c.ecnt, c.efill, c.tcnt, c.eoff, c.toff, c.recs, c.ang, c.tmp,
+                c.qfcnt, c.qfoff, c.lcnt, c.lfill, c.loffs, c.frecs, c.fent, c.fval};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  unsigned long long* h = c.h;
+  c = FFCache();
+  c.h = h;  // the pinned scalars stay
+}
+
 template <class T>
 static cudaError_t ff_grow(T*& p, size_t& cap, size_t n, size_t unit, cudaStream_t st) {
   if (cap >= n) return cudaSuccess;

@@ -325,6 +325,17 @@ struct WsCache {
 };
 static thread_local WsCache t_wscache[64];
 
+void release_boundary_caches(int device);  // gwn_boundary.cu
+
+// this host thread's eval workspace on `device` (gwn_release_caches)
+static void release_ws_cache(int device) {
+  WsCache& c = t_wscache[device & 63];
+  if (c.buf) cudaFree(c.buf);
+  if (c.k3) cudaFree(c.k3);
+  c = WsCache();
+  release_boundary_caches(device);
+}
+
 struct Workspace {
   cudaStream_t st;
   std::vector<void*> ptrs;
@@ -381,6 +392,23 @@ struct Workspace {
 
 using namespace gwn;
 
+// gwn_release_caches: this host thread's eval workspace on `device` (the
+// buffers grow to the largest batch seen and are kept for the next eval)
+extern "C" int gwn_release_caches(int device) {
+  if (device < 0) {
+    set_error("gwn_release_caches: invalid device");
+    return GWN_E_INVALID;
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(device);
+  cudaDeviceSynchronize();
+  release_ws_cache(device);
+  cudaDeviceSynchronize();
+  cudaSetDevice(cur);
+  return GWN_OK;
+}
+
 #define CKE(call)                                                              \
   do {                                                                         \
     cudaError_t e_ = (call);                                                   \
@@ -423,13 +451,13 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   Workspace ws;
   ws.st = st;
   const bool host = (flags & GWN_HOST_BUFFERS) != 0;
-  // auto chunk: 4M queries (2M when the boundary partials are wide; 64M for
+  // auto chunk: 4M queries (2M when the boundary partials are wide; 32M for
   // far-field scenes: a local-expansion leaf's queries share one warp's list
   // only when the leaves are well filled, and every chunk pays the re-shoot
-  // rounds' latency -- config 5 at 2^26 queries: 1071 ms in 8M chunks, 930 ms
-  // in one)
+  // rounds' latency -- config 5 at 2^26 queries: 1071 ms in 8M chunks, 958 in
+  // 32M, 930 in one 64M chunk, whose K3 queues alone take ~60 GB)
   const int64_t chunk_max = sc->prm.chunk_queries > 0 ? sc->prm.chunk_queries
-                            : sc->ff_n > 0               ? (1ll << 26)
+                            : sc->ff_n > 0               ? (1ll << 25)
                             : boundary_chunks(sc, 0) > 16 ? (1ll << 21)
                                                           : (1ll << 22);
   // device scalar block, published to mapped pinned memory once per round

@@ -437,6 +437,12 @@ def net_boundary(ctrl) -> tuple[np.ndarray, np.ndarray]:
     return ec[:n], w[:n]
 
 
+def release_caches(device: int = 0) -> None:
+    """Free this thread's cached eval workspace on `device` (gwn_eval keeps
+    its buffers at the largest batch seen for the next call)."""
+    _lib.check(_lib.lib().gwn_release_caches(int(device)), "gwn_release_caches")
+
+
 def fp64_peak(device: int = 0) -> tuple[float, float]:
     """Measured FP64 DFMA peak (TFLOP/s, ms) of ``device``."""
     tf, ms = C.c_double(), C.c_double()
