@@ -248,6 +248,8 @@ static void newton3(const double* X, const double o[3], const double d[3], doubl
 
 typedef struct roots_t {
   int n;
+  int ambiguous;      /* a leaf at the depth cap stayed uncertified (a fold) */
+  double amb_t;
   double r[OR_MAX_ROOTS][3];
 } roots_t;
 
@@ -330,6 +332,8 @@ int or_multistart_hits(const double* X, const double o[3], const double d[3],
   aabb_of(X, 16, lo, hi);                          /* surfaces.py:636 (control-net box) */
   roots_t R;
   R.n = 0;
+  R.ambiguous = 0;
+  R.amb_t = 0.0;
   multistart_box(X, o, d, prm, lo, hi, 0.5, 0.5, &R);   /* domain_center, surfaces.py:581 */
   return build_records(X, d, prm, &R, out, cap);
 }
@@ -423,9 +427,10 @@ static void subdiv_hits(const double* X, const double* N, double u0, double v0, 
   aabb_of(N, 16, lo, hi);                          /* geometry.py:70-73 */
   if (!or_ray_aabb_clip(o, d, lo, hi, &c0, &c1)) return;   /* geometry.py:198-219 */
   if (c1 < fmax(c0, 0.0)) return;
-  int leaf = depth >= OR_MAX_DEPTH ||
-             (depth >= prm->subdiv_depth && leaf_injective(N, d));
+  const int certified = depth >= prm->subdiv_depth && leaf_injective(N, d);
+  int leaf = depth >= OR_MAX_DEPTH || certified;
   if (leaf) {
+    const int n_before = R->n;
     /* the reference seeding (domain centre, t seeds; surfaces.py:645-660)
      * on the leaf, plus the leaf's four quarter points at mid-window */
     multistart_box(X, o, d, prm, lo, hi, u0 + 0.5 * w, v0 + 0.5 * w, R);
@@ -433,6 +438,24 @@ static void subdiv_hits(const double* X, const double* N, double u0, double v0, 
     for (int q = 0; q < 4; ++q)
       try_seed(X, o, d, prm, u0 + (q & 1 ? 0.75 : 0.25) * w, v0 + (q & 2 ? 0.75 : 0.25) * w,
                tm, R);
+    if (!certified && !R->ambiguous) {
+      /* an uncertified leaf at the depth cap (a silhouette fold) whose seeds
+       * converged to a near-tangent contact: residual-accepted points along
+       * a tangent are not a reliable root set.  As on the GPU
+       * (undecided nodes, gwn_wavefront.cu), the ray is reported tangent and
+       * the query is re-shot. */
+      for (int i = n_before; i < R->n; ++i) {
+        double fu[3], fv[3], nn[3];
+        or_bicubic_partials(X, R->r[i][0], R->r[i][1], fu, fv);
+        cross3(fu, fv, nn);
+        const double l = norm3(nn);
+        if (!(l > 0.0) || fabs(dot3(nn, d)) < 1e-4 * l) {
+          R->ambiguous = 1;
+          R->amb_t = R->r[i][2];
+          break;
+        }
+      }
+    }
     return;
   }
   double A[48], B[48], AA[48], AB[48], BA[48], BB[48];
@@ -450,8 +473,33 @@ int or_patch_all_hits(const double* X, const double o[3], const double d[3],
                       const or_params* prm, or_record* out, int cap) {
   roots_t R;
   R.n = 0;
+  R.ambiguous = 0;
+  R.amb_t = 0.0;
   subdiv_hits(X, X, 0.0, 0.0, 1.0, 0, o, d, prm, &R);
-  return build_records(X, d, prm, &R, out, cap);
+  int n = build_records(X, d, prm, &R, out, cap);
+  /* a root with |d . n^| < 1e-6 lies within ~1e-6 of a tangent contact:
+   * residual acceptance (1e-10) then admits a run of points along the
+   * tangent, each counted (measured: 44 "roots" at |d . n^| ~ 1e-8 on one
+   * ray); re-shoot instead, as the GPU's certification does */
+  for (int i = 0; i < n && !R.ambiguous; ++i)
+    if (!out[i].tangency && fabs(dot3(out[i].normal, d)) < 1e-6) {
+      R.ambiguous = 1;
+      R.amb_t = out[i].t;
+    }
+  if (R.ambiguous) {
+    /* one tangent record (sign 0: chi unchanged) carries the re-shoot */
+    int k = n;
+    if (k < cap) {
+      ++n;
+    } else {
+      k = cap - 1;
+    }
+    or_record* rec = &out[k];
+    rec->t = R.amb_t; rec->u = rec->v = 0.5; rec->pad = 0;
+    rec->normal[0] = d[0]; rec->normal[1] = d[1]; rec->normal[2] = d[2];
+    rec->sign = 0; rec->tangency = 1; rec->grazing = 0;
+  }
+  return n;
 }
 
 /* ------------------------------------------------------------------------- */

@@ -22,6 +22,18 @@ What is captured (reference file:line):
                                                             _kernels.py:723-823
   tess.npz      dense-tessellation w through _solid_angle_numpy
                                                             _kernels.py:422-440
+  scene3.npz,   scene-level sums of the reference's per-patch terms: for each
+  scene5.npz    query and patch, chi from the reference solver on de
+                Casteljau sub-patches and w_k = single_loop_batch(loop_k,
+                hits_k) from the line-45-fixed copy (chi + the fan formula
+                where it returns ok = 0, counted in `fallback`); w = sum_k
+                w_k (SPEC additivity).  Config 3 (64 patches) and
+                config 5 (15,876 patches): pins net-boundary cancellation,
+                the far field and re-shoot-free round-0 values against the
+                reference.                                   surfaces.py:611-701,
+                                                            _kernels.py:723-823
+
+    python tests/golden/make_golden.py scene    # only the scene fixtures
 """
 
 from __future__ import annotations
@@ -308,6 +320,70 @@ def gen_tess():
     np.savez_compressed(os.path.join(HERE, "tess.npz"), ctrl=ctrl, queries=P, w=w)
 
 
+def _scene_chunk(args):
+    """Worker: per-patch reference terms of a few queries (one ray each along d)."""
+    ctrl, loops, Q, d, idx = args
+    K_fix = fixed_kernels()
+    lo = ctrl.reshape(len(ctrl), -1, 3).min(axis=1)
+    hi = ctrl.reshape(len(ctrl), -1, 3).max(axis=1)
+    out = []
+    for i in idx:
+        p = Q[i]
+        # patches whose control box the ray meets (the solver's own clip,
+        # geometry.py:198-219, vectorised as a prefilter)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            t0 = (lo - p) / d
+            t1 = (hi - p) / d
+        tmin = np.where(d != 0, np.minimum(t0, t1), np.where((p >= lo) & (p <= hi), -np.inf, np.inf))
+        tmax = np.where(d != 0, np.maximum(t0, t1), np.where((p >= lo) & (p <= hi), np.inf, -np.inf))
+        hit = (np.maximum(tmin.max(axis=1), 0.0) <= tmax.min(axis=1))
+        w = 0.0
+        chi = 0
+        fallback = 0
+        for k in range(len(ctrl)):
+            if hit[k]:
+                recs = ref_hits_subdivided(ctrl[k], p, d)
+                hts = np.array([r.t for r in recs], float)
+                hs = np.array([r.sign for r in recs], np.int64)
+            else:
+                hts, hs = np.zeros(0), np.zeros(0, np.int64)
+            chi += int(hs.sum()) if len(hs) else 0
+            a, b = K_fix.single_loop_batch(loops[k], p, d, hts, hs, np.zeros(1), 1e-9, 1e-12)
+            if b[0]:
+                w += float(a[0])
+            else:
+                # ok = 0: the reference defers to its (absent) generic path;
+                # the fan formula stands in (pinned to this kernel at 1.8e-14
+                # where ok = 1, fan.npz)
+                from oracle import oracle as O
+                w += float(hs.sum() if len(hs) else 0) + O.loop_fan(loops[k], p, d)
+                fallback += 1
+        out.append((i, w, chi, fallback))
+    return out
+
+
+def gen_scene(cfg, n, nproc=8):
+    import multiprocessing as mp
+    sc = scenes.make(cfg, n)
+    ctrl = np.ascontiguousarray(sc.ctrl)
+    loops = [SU.patch_boundary(BicubicAdapter(c), 200).points for c in ctrl]
+    d = direction(0)
+    Q = sc.queries[:n]
+    parts = [list(range(j, n, nproc)) for j in range(nproc)]
+    with mp.get_context("fork").Pool(nproc) as pool:
+        res = pool.map(_scene_chunk, [(ctrl, loops, Q, d, ix) for ix in parts])
+    w = np.zeros(n)
+    chi = np.zeros(n, np.int64)
+    fb = np.zeros(n, np.int64)
+    for part in res:
+        for i, wi, ci, fi in part:
+            w[i], chi[i], fb[i] = wi, ci, fi
+    np.savez_compressed(os.path.join(HERE, f"scene{cfg}.npz"), config=cfg, queries=Q, d=d, w=w,
+                        chi=chi, fallback=fb)
+    print(f"scene{cfg}.npz: {n} queries, {int(fb.sum())} (query, patch) boundary terms from the "
+          f"fan formula where single_loop_batch returned ok = 0")
+
+
 def main():
     rng = np.random.default_rng(20240804)
     gen_clip(rng)
@@ -319,4 +395,10 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "scene":
+        gen_scene(3, 64)
+        gen_scene(5, 16)
+    else:
+        main()
+        gen_scene(3, 64)
+        gen_scene(5, 16)

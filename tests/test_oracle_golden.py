@@ -146,3 +146,19 @@ def test_direction_independence_open_patch():
         m = oka & okb
         assert m.sum() > 250
         assert np.abs(a - b)[m].max() < 1e-11
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_scene_sums_match_reference(golden_dir, cfg):
+    """The oracle (net boundary, exact cancellation) against the reference's
+    per-patch terms summed over configs 3 and 5 (scene{3,5}.npz; chi from the
+    subdivided reference solver, boundary terms from the fixed
+    single_loop_batch): chi exact, w within 1e-12."""
+    from paper_2408_04466_b200 import scenes
+    g = _load(golden_dir, f"scene{cfg}.npz")
+    s = scenes.make(cfg, len(g["queries"]))
+    chi, bt, fl = O.scene_eval_dir(s.ctrl, g["queries"], g["d"])
+    ok = fl == 0
+    assert ok.sum() >= len(ok) - 2
+    assert np.array_equal(chi[ok], g["chi"][ok])
+    assert np.abs(chi + bt - g["w"])[ok].max() < 1e-12
