@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define GWN_ABI_VERSION 4
+#define GWN_ABI_VERSION 5
 
 /* return codes (negative = error) */
 #define GWN_OK 0
@@ -78,6 +78,9 @@ typedef struct gwn_params {
   int32_t max_jitters;      /* SPEC.md:375 jitter budget                 3     */
   int32_t chunk_queries;    /* queries per internal chunk (0 = auto)           */
   uint64_t dir_seed;        /* deterministic direction sequence seed           */
+  int32_t cached_rounds;    /* direction rounds kept on the scene (>= 1; later
+                               re-shoot rounds are built per eval and freed) 4 */
+  int32_t reserved_;
 } gwn_params;
 
 typedef struct gwn_scene gwn_scene;

@@ -44,6 +44,7 @@ class GwnParams(C.Structure):
         ("domain_tol", C.c_double), ("t_tol", C.c_double), ("on_surface_t", C.c_double),
         ("band_factor", C.c_double), ("samples_per_edge", C.c_int32), ("max_rounds", C.c_int32),
         ("max_jitters", C.c_int32), ("chunk_queries", C.c_int32), ("dir_seed", C.c_uint64),
+        ("cached_rounds", C.c_int32), ("reserved_", C.c_int32),
     ]
 
 

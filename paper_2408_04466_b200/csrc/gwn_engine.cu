@@ -449,6 +449,14 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   Trace tr;
   GpuTimeline tl;
   Workspace ws;
+  // rounds past the scene's cache (prm.cached_rounds, default 4: round 0
+  // with the far field's local expansions and the first re-shoot rounds,
+  // which every large batch needs): built for this eval in
+  // `spill` (one at a time) and freed at its end, so a batch of stubborn
+  // queries re-shot up to 32 times cannot pile 32 full-scene rounds on the
+  // device (~5 GB each at config 5)
+  Round spill;
+  int spill_r = -1;
   ws.st = st;
   const bool host = (flags & GWN_HOST_BUFFERS) != 0;
   // auto chunk: 4M queries (2M when the boundary partials are wide; 32M for
@@ -628,7 +636,23 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
       }
       for (int r = 0; r < sc->prm.max_rounds && m > 0;) {
         const Round* rdp = nullptr;
-        CKE(ensure_round(sc, r, st, &rdp, &stats.ms_round_build));
+        if (r < std::max(1, sc->prm.cached_rounds)) {
+          CKE(ensure_round(sc, r, st, &rdp, &stats.ms_round_build));
+        } else {
+          if (spill_r != r) {
+            if (spill_r >= 0) free_round(spill);
+            spill_r = -1;
+            double dr[3];
+            gwn_direction(sc->prm.dir_seed, r, dr);
+            const auto t0 = std::chrono::steady_clock::now();
+            CKE(build_round_dir(sc, dr, spill, st));
+            stats.ms_round_build += std::chrono::duration<double, std::milli>(
+                                        std::chrono::steady_clock::now() - t0)
+                                        .count();
+            spill_r = r;
+          }
+          rdp = &spill;
+        }
         const Round& rd = *rdp;
         // candidate capacity from the scene's running estimate
         int64_t want = (int64_t)(sc->pairs_per_query * 1.25 * m) + 4096;
@@ -806,6 +830,10 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   tl_mark(st, "outputs copied");
   tr.mark("outputs copied");
 done:
+  if (spill_r >= 0) {
+    cudaStreamSynchronize(st);
+    free_round(spill);
+  }
   if (pipe && cs_in) {  // no copy may outlive the workspace
     cudaStreamSynchronize(cs_in);
     cudaStreamSynchronize(cs_out);

@@ -136,6 +136,8 @@ extern "C" void gwn_params_default(gwn_params* p) {
   p->max_rounds = 32;
   p->max_jitters = 3;
   p->chunk_queries = 0;
+  p->cached_rounds = 4;
+  p->reserved_ = 0;
   p->dir_seed = 0x2408044660ull;
 }
 
@@ -237,8 +239,9 @@ extern "C" int gwn_scene_create(const double* ctrl, int64_t P, const gwn_params*
   sc = new gwn_scene();
   if (prm_in) sc->prm = *prm_in;
   else gwn_params_default(&sc->prm);
-  if (sc->prm.samples_per_edge < 2 || sc->prm.max_rounds < 1) {
-    set_error("gwn_scene_create: samples_per_edge must be >= 2 and max_rounds >= 1");
+  if (sc->prm.samples_per_edge < 2 || sc->prm.max_rounds < 1 || sc->prm.cached_rounds < 1) {
+    set_error("gwn_scene_create: samples_per_edge must be >= 2, max_rounds and cached_rounds "
+              ">= 1");
     delete sc;
     return GWN_E_INVALID;
   }

@@ -56,7 +56,8 @@ class Scene:
     def __init__(self, patches, eps: EpsilonConfig = DEFAULT_EPS,
                  samples_per_edge: int = 200, device: int | None = None,
                  max_rounds: int = cfg.MAX_ROUNDS, max_jitters: int = cfg.MAX_JITTERS,
-                 dir_seed: int = cfg.DIR_SEED, chunk_queries: int = 0):
+                 dir_seed: int = cfg.DIR_SEED, chunk_queries: int = 0,
+                 cached_rounds: int = 4):
         if samples_per_edge < 2:
             raise ValueError("need at least 2 samples per edge")
         self.ctrl = _as_ctrl(patches)
@@ -71,6 +72,7 @@ class Scene:
         p.max_jitters = max_jitters
         p.dir_seed = dir_seed
         p.chunk_queries = chunk_queries
+        p.cached_rounds = cached_rounds
         self.params = p
         h = C.c_void_p()
         dp = C.POINTER(C.c_double)

@@ -470,3 +470,17 @@ def test_scene_sums_match_reference_fixture(golden_dir, cfg):
     m = (fl == 0) & (st == 0)    # not re-shot: the round-0 direction d
     assert m.sum() >= len(m) - 2
     assert np.abs(w - g["w"])[m].max() <= W_TOL
+
+
+def test_round_cache_cap_is_bit_identical():
+    """Re-shoot rounds past the scene's cache (cached_rounds) are built per
+    eval and freed: same results, and the scene keeps only the cached ones."""
+    s = scenes.make(3, 1 << 14)
+    a = G.Scene(s.ctrl)
+    b = G.Scene(s.ctrl, cached_rounds=1)
+    wa, sa = G.winding_numbers(a, s.queries)
+    wb, sb = G.winding_numbers(b, s.queries)
+    assert np.array_equal(wa, wb) and np.array_equal(sa, sb)
+    ta, tb = a.stats(), b.stats()
+    assert ta["rounds"] == tb["rounds"] and ta["rounds"] >= 2   # re-shoot rounds ran
+    assert tb["rounds_built"] == 1 and ta["rounds_built"] >= 2
