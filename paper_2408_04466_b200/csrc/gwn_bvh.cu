@@ -70,15 +70,8 @@ __global__ void k_project(const double* __restrict__ ctrl, int64_t P, Frame f,
 // the leaf then certifies from the precomputed data alone), or kLeafMaxLevel.
 // kFill = false: count leaves per patch; true: write LeafRec, the leaf's
 // control-box (cull primitive) and its Morton key.
-// leaf depth cap (GWN_LEAF_MAXLEVEL overrides, for experiments)
-static int leaf_max_level() {
-  static int v = [] {
-    const char* e = getenv("GWN_LEAF_MAXLEVEL");
-    int x = e ? atoi(e) : kLeafMaxLevel;
-    return x < 1 ? 1 : x > kLeafLevelCap ? kLeafLevelCap : x;
-  }();
-  return v;
-}
+// leaf depth cap
+static int leaf_max_level() { return kLeafMaxLevel < kLeafLevelCap ? kLeafMaxLevel : kLeafLevelCap; }
 
 // Conservative box expansion of patch P48 (rounding + the 1e-9 parametric
 // acceptance band of surfaces.py:668: roots just outside the domain).
@@ -540,11 +533,8 @@ static cudaError_t build_grid(Round& rd, double amin, double amax, double bmin, 
     // wider than any leaf-box expansion (<= 1e-12 (1 + mag) + 3e-9 patch extent)
     const double margin = 1e-8 * (1.0 + fabs(amin) + fabs(amax) + fabs(bmin) + fabs(bmax));
     const double x0 = amin - margin, x1 = amax + margin, y0 = bmin - margin, y1 = bmax + margin;
-    // cell = kf x the mean leaf-box extent (GWN_GRID_CELL overrides kf)
-    static const double kf = [] {
-      const char* e = getenv("GWN_GRID_CELL");
-      return e ? atof(e) : 0.5;
-    }();
+    // cell = kf x the mean leaf-box extent (measured best at config 2)
+    constexpr double kf = 0.5;
     const double cw = fmax(kf * h[0] / (double)n, (x1 - x0) / 4096.0);
     const double ch = fmax(kf * h[1] / (double)n, (y1 - y0) / 4096.0);
     const int ga = (int)fmin(4096.0, fmax(1.0, ceil((x1 - x0) / cw)));
@@ -622,18 +612,14 @@ __global__ void k_foldtree_gc(int64_t total, const int32_t* __restrict__ skip,
 
 // Fold trees of the round's uncertified leaves (k_foldtree): the deepest
 // sub_level <= kSubLevelMax whose node count stays within the budget
-// (GWN_SUB_LEVEL overrides; 0 disables).
 static cudaError_t build_subleaves(Round& rd, cudaStream_t st) {
-  const char* env = getenv("GWN_SUB_LEVEL");
-  int level = env ? atoi(env) : kSubLevelMax;
+  int level = kSubLevelMax;
   if (level > kLeafLevelCap) level = kLeafLevelCap;  // (kLeafLevelCap bounds the stacks)
   const int64_t n = rd.n_leaves;
   if (level <= leaf_max_level() || n <= 0) return cudaSuccess;
-  const char* env_b = getenv("GWN_TREE_BUDGET");  // node budget (experiments)
-  const int64_t budget = env_b ? atoll(env_b) : std::max<int64_t>(4 * n, 1ll << 20);
+  const int64_t budget = std::max<int64_t>(4 * n, 1ll << 20);  // node budget
   const int level0 = level;
-  const char* env_r = getenv("GWN_TREE_R");  // certified-leaf tree threshold (experiments)
-  double tree_r = env_r ? atof(env_r) : kTreeR;
+  double tree_r = kTreeR;  // certified-leaf tree threshold
   cudaError_t e = cudaSuccess;
   int64_t *cnt = nullptr, *offs = nullptr;
   void* tmp = nullptr;

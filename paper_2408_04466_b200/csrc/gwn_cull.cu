@@ -289,8 +289,7 @@ cudaError_t launch_cull(const gwn_scene* sc, const Round& rd, int32_t m, const i
   if (m <= 0) return cudaSuccess;
   GridView g{rd.use_grid ? rd.cell_offs : nullptr, rd.cell_ent, rd.ga, rd.gb,
              rd.gx0, rd.gy0, rd.gia, rd.gib};
-  static const bool per_lane = getenv("GWN_CULL_PERLANE") != nullptr;  // A/B switch
-  if (g.offs && !per_lane) {
+  if (g.offs) {
     k_cull_grid<<<(m + GWN_CULL_BS - 1) / GWN_CULL_BS, GWN_CULL_BS, 0, st>>>(g, rd.f, m, active, pos, qproj, Q.pairs,
                                                  pair_count, (unsigned long long)cap, z);
     return cudaGetLastError();

@@ -535,18 +535,12 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     int64_t cm = n < chunk_max ? n : chunk_max;
     std::vector<int64_t> cst{0};  // chunk starts
     if (pipe) {
-      static const int64_t parts = [] {  // GWN_PIPE_CHUNKS overrides (experiments)
-        const char* e = getenv("GWN_PIPE_CHUNKS");
-        // measured at config 2 (2^20 queries, pinned host buffers), e2e G q/s:
-        // 2 chunks 1.63, 4 1.70, 6 1.79, 8 1.55, 12 1.27; splitting the last
-        // chunk (GWN_PIPE_TAIL) or issuing every input copy up front
-        // (GWN_PIPE_AHEAD) did not help
-        const long long v = e ? atoll(e) : 6;
-        return (int64_t)(v < 1 ? 1 : v);
-      }();
-      // far-field scenes: two parts (their steps are long next to the copies,
-      // and larger chunks keep the local-expansion leaves' warps uniform)
-      const int64_t np = sc->ff_n > 0 && !getenv("GWN_PIPE_CHUNKS") ? 2 : parts;
+      // parts: measured at config 2 (2^20 queries, pinned host buffers), e2e
+      // G q/s: 2 chunks 1.63, 4 1.70, 6 1.79, 8 1.55, 12 1.27 (splitting the
+      // last chunk or issuing every input copy up front did not help);
+      // far-field scenes: two (their steps are long next to the copies, and
+      // larger chunks keep the local-expansion leaves' warps uniform)
+      const int64_t np = sc->ff_n > 0 ? 2 : 6;
       const int64_t pc =
           (std::max<int64_t>(1ll << 16, (n + np - 1) / np) + 1023) & ~1023ll;
       cm = std::min(cm, pc);
@@ -554,19 +548,8 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         CKE(cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking));
         CKE(cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking));
       }
-      // chunk boundaries: equal chunks, the last one split GWN_PIPE_TAIL times
-      // in halves -- after the final input copy only the last (small) chunk's
-      // rounds and output copy remain
-      static const int tail = [] {
-        const char* e = getenv("GWN_PIPE_TAIL");
-        return e ? atoi(e) : 0;
-      }();
+      // chunk boundaries: equal chunks
       for (int64_t a = cm; a < n; a += cm) cst.push_back(a);
-      for (int t = 0; t < tail; ++t) {
-        const int64_t a = cst.back(), half = ((n - a) / 2 + 1023) & ~1023ll;
-        if (half < (1ll << 15) || a + half >= n) break;
-        cst.push_back(a + half);
-      }
       const int64_t nch = (int64_t)cst.size();
       pev.assign((size_t)(2 * nch), nullptr);
       for (auto& e : pev) CKE(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -584,10 +567,10 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     unsigned long long* rsc = d_cnt + CNT_N;  // round scalars (see kBlk)
     unsigned long long* k3cnt = rsc + 4;
     bool cnt_zeroed = false;
-    // round-0 spatial ordering of the queries (64 x 64 Morton cells)
-    // (measured on config 2: the ordering costs what it saves in the cull, so
-    // it is opt-in; the grid cull does not need coherent queries)
-    const bool sort_q = sc->P > 0 && cm >= 65536 && getenv("GWN_QUERY_ORDER");
+    // (a round-0 spatial ordering of the queries before the cull costs what
+    // it saves at config 2 -- the grid cull does not need coherent queries --
+    // so the cull takes them in input order)
+    const bool sort_q = false;
     void* order_tmp = sort_q ? ws.get<char>(query_order_scratch_bytes((int32_t)cm)) : nullptr;
     // far-field scenes: 3-D Morton order of each round's queries for K4
     const bool ff_sort = sc->ff_n > 0 && cm >= 4096;
@@ -611,12 +594,8 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
                                           cs_in);
           return e != cudaSuccess ? e : cudaEventRecord(pev[2 * k], cs_in);
         };
-        // input copies issued GWN_PIPE_AHEAD chunks ahead of the rounds
-        static const int64_t ahead = [] {
-          const char* e = getenv("GWN_PIPE_AHEAD");
-          const long long v = e ? atoll(e) : 1;
-          return (int64_t)(v < 1 ? 1 : v);
-        }();
+        // input copies issued one chunk ahead of the rounds
+        constexpr int64_t ahead = 1;
         const int64_t nchk = (int64_t)cst.size() - 1;
         for (int64_t k = ci == 0 ? 0 : ci + ahead; k <= ci + ahead && k < nchk; ++k)
           CKE(h2d(k));
@@ -721,14 +700,9 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
                           ((uintptr_t)(d_st + c0) & 3) == 0;
         if (vec4) {
           const int32_t nth = (m + 3) / 4;
-          static const int k5_bps = [] {  // K5 blocks per SM cap (GWN_K5_BPS; 0 = one group per thread)
-            const char* e = getenv("GWN_K5_BPS");
-            return e ? atoi(e) : 2;
-          }();
-          static const int k5_bs = [] {  // K5 block size (GWN_K5_BS); 512 x 2 per SM keeps
-            const char* e = getenv("GWN_K5_BS");  // the publish counter's atomics few
-            return e ? atoi(e) : 512;
-          }();
+          // K5: 512-thread blocks, at most 2 per SM (the publish counter's
+          // atomics stay few)
+          constexpr int k5_bps = 2, k5_bs = 512;
           const int nb4 = k5_bps > 0 ? std::min((nth + k5_bs - 1) / k5_bs, k5_bps * sc->sm_count)
                                      : (nth + k5_bs - 1) / k5_bs;
           k_finalize4<<<nb4, k5_bs, 0, st>>>(

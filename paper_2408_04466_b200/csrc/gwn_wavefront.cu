@@ -496,16 +496,11 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
   if (g_dev != sc->device) {
     g_cand = grid_for((const void*)k3_candidates, sc->sm_count, kCandBlock);
     // fallback: 3 blocks per SM spread its few, long-lived items thinly
-    // (measured on config 2 against 1, 2, 4, 6, 8; GWN_FB_BPS overrides)
-    const char* e_bps = getenv("GWN_FB_BPS");
-    const int bps = e_bps ? atoi(e_bps) : 3;
-    g_fb = bps > 0 ? sc->sm_count * bps : grid_for((const void*)k3_fallback, sc->sm_count, 32 * kFbWarps);
+    // (measured on config 2 against 1, 2, 4, 6, 8)
+    g_fb = sc->sm_count * 3;
     // Newton at full occupancy: its dynamic fetch drains the queue, then the
-    // fallback blocks take the SMs (GWN_NEWTON_BPS > 0 caps blocks per SM)
-    const char* e_nb = getenv("GWN_NEWTON_BPS");
-    const int nbps = e_nb ? atoi(e_nb) : 0;
-    const int full = grid_for((const void*)k3_newton<false>, sc->sm_count);
-    g_newton = nbps > 0 && sc->sm_count * nbps < full ? sc->sm_count * nbps : full;
+    // fallback blocks take the SMs
+    g_newton = grid_for((const void*)k3_newton<false>, sc->sm_count);
     g_newton_s = grid_for((const void*)k3_newton<true>, sc->sm_count, 128,
                           sizeof(double) * kTabStride * kTabMaxP);
     g_dev = sc->device;
@@ -547,11 +542,10 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
   cudaEvent_t& join_ev = t_join[sc->device & 63];
   if (!side) {
     // high priority: the fallback's blocks are dispatched ahead of the Newton
-    // pass's, so its long dependent chains start first (GWN_FB_PRIO=0: off)
+    // pass's, so its long dependent chains start first
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
-    const char* e_pr = getenv("GWN_FB_PRIO");
-    const int prio = (e_pr && atoi(e_pr) == 0) ? lo_prio : hi_prio;
+    const int prio = hi_prio;
     if ((e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, prio)) != cudaSuccess)
       return e;
     if ((e = cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming)) != cudaSuccess) return e;
