@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define GWN_ABI_VERSION 5
+#define GWN_ABI_VERSION 6
 
 /* return codes (negative = error) */
 #define GWN_OK 0
@@ -127,6 +127,8 @@ typedef struct gwn_stats {
   int64_t rounds_built;       /* direction rounds (K1 structures) cached on the scene */
   double ms_round_build;      /* host wall time building new rounds in this eval      */
   int64_t local_evals;        /* queries whose far field came from a leaf's local expansion */
+  int64_t shadow_pairs;       /* far pairs whose forward half-line crosses the cycle's
+                                 sphere (expansion + shadow winding number, DESIGN §9 f4) */
 } gwn_stats;
 
 int gwn_abi_version(void);

@@ -81,6 +81,7 @@ class Stats(C.Structure):
         ("far_pairs", C.c_int64), ("far_terms", C.c_int64), ("near_pairs", C.c_int64),
         ("ms_k4_far", C.c_double), ("ms_k4_exact", C.c_double), ("rounds_built", C.c_int64),
         ("ms_round_build", C.c_double), ("local_evals", C.c_int64),
+        ("shadow_pairs", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

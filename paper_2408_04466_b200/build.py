@@ -35,19 +35,43 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile(out: str, defines: list[str]) -> str:
+    """Each .cu to an object in parallel (one nvcc per file), then one link."""
+    from concurrent.futures import ThreadPoolExecutor
+    odir = out + ".objs"
+    os.makedirs(odir, exist_ok=True)
+    base = [NVCC, *[f for f in FLAGS if f != "-shared"], *[f"-D{d}" for d in defines],
+            "-I", os.path.join(REPO, "include")]
+
+    def one(src):
+        obj = os.path.join(odir, os.path.basename(src) + ".o")
+        return subprocess.run([*base, "-c", "-o", obj, src], capture_output=True, text=True), obj
+
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+        results = list(ex.map(one, sources()))
+    log = "".join(r.stderr for r, _ in results)
+    bad = [r for r, _ in results if r.returncode != 0]
+    if bad:
+        sys.stderr.write("".join(r.stdout + r.stderr for r in bad))
+        raise RuntimeError(f"nvcc failed building {os.path.basename(out)}")
+    link = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                           "-o", out + ".tmp", *[o for _, o in results]],
+                          capture_output=True, text=True)
+    if link.returncode != 0:
+        sys.stderr.write(link.stdout + link.stderr)
+        raise RuntimeError(f"nvcc failed linking {os.path.basename(out)}")
+    os.replace(out + ".tmp", out)
+    return log
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(REPO, "include"), "-o", LIB + ".tmp", *sources()]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libgwn_b200.so")
+    log = _compile(LIB, [])
     with open(os.path.join(HERE, "csrc", "ptxas_report.txt"), "w") as f:
-        f.write(res.stderr)
+        f.write(log)
     if verbose:
-        sys.stderr.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
+        sys.stderr.write(log)
     return LIB
 
 
@@ -56,12 +80,7 @@ def build_variant(name: str, defines: list[str]) -> str:
     (selected at import with GWN_B200_LIB=<path>); not used by the product."""
     out = os.path.join(REPO, "build", "variants", f"libgwn_b200_{name}.so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(REPO, "include"),
-           "-o", out, *sources()]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed building variant {name}")
+    _compile(out, defines)
     return out
 
 

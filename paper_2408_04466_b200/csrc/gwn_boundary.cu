@@ -436,6 +436,19 @@ constexpr int kNearMinBlocks = 4;
 // line crosses it).
 // ---------------------------------------------------------------------------
 
+// Shadow winding grids (per round and closed expanded cycle): a pair whose
+// forward half-line crosses the cycle's sphere, with the sphere wholly in
+// front of the query, is far too when its cell is clean -- its exact fan sum
+// is then the expansion's value plus kShadowJump times the winding number of
+// the cycle's projection along d around the query (k_ff_wind).
+constexpr int kWG = 128;             // cells per side over the sphere's disk
+constexpr int kWDirty = -128;        // a cell some segment may come near
+#ifndef GWN_SHADOW_SIGN
+#define GWN_SHADOW_SIGN -1
+#endif
+// in the units of the far rows (Omega; halved into the partial angle sums)
+constexpr double kShadowJump = GWN_SHADOW_SIGN * 12.566370614359172954;
+
 struct FFRound {
   int32_t C;
   const double* g3;     // (C,3) entry centres in the round frame
@@ -445,17 +458,40 @@ struct FFRound {
   const double2* D;     // (C,kFFTerms) moments
   const int32_t* chord; // (C) sliver chord edge or -1
   const double* ffa;    // (C,6) chord end points, round frame
+  const int8_t* wg;     // (C,kWG,kWG) shadow winding grids (k_ff_wind)
+  const double* wgeo;   // (C,3) grid origin and inverse cell size
 };
 
-__device__ __forceinline__ bool ff_far2(double qa, double qb, double qc,
-                                        const double* __restrict__ g3,
-                                        const double* __restrict__ r2) {
+// Far test of entry c (every pass calls it on the same bits, so the
+// decisions agree): 0 = near (the exact fan sum); 1 = far, R >= R_min and the
+// forward half-line misses the entry's sphere (wind = 0); 2 = far, R >= R_min,
+// the half-line crosses the sphere and the query's cell of the entry's shadow
+// winding grid is clean (wind = the cell's value; see k_ff_wind).
+__device__ __forceinline__ int ff_class(const FFRound& R, int32_t c, double qa, double qb,
+                                        double qc, int& wind) {
+  const double* g3 = R.g3 + 3 * (int64_t)c;
+  const double* r2 = R.r2 + 2 * (int64_t)c;
   const double dx = __dsub_rn(__ldg(g3), qa), dy = __dsub_rn(__ldg(g3 + 1), qb);
   const double dz = __dsub_rn(__ldg(g3 + 2), qc);
   const double l2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
   const double R2 = __dadd_rn(l2, __dmul_rn(dz, dz));
   const double line2 = __ldg(r2 + 1);
-  return R2 > __ldg(r2) && (l2 > line2 || (dz < 0.0 && __dmul_rn(dz, dz) > line2));
+  wind = 0;
+  if (!(R2 > __ldg(r2))) return 0;
+  if (l2 > line2 || (dz < 0.0 && __dmul_rn(dz, dz) > line2)) return 1;
+  // the forward half-line crosses the sphere, which lies wholly in front of
+  // the query (R > R_min > the sphere's radius)
+#ifdef GWN_NO_SHADOW
+  return 0;
+#endif
+  const double* gg = R.wgeo + 3 * (int64_t)c;
+  const double fx = __dmul_rn(__dsub_rn(qa, __ldg(gg)), __ldg(gg + 2));
+  const double fy = __dmul_rn(__dsub_rn(qb, __ldg(gg + 1)), __ldg(gg + 2));
+  if (!(fx >= 0.0 && fx < (double)kWG && fy >= 0.0 && fy < (double)kWG)) return 0;
+  const int v = __ldg(R.wg + ((int64_t)c * kWG + (int)fy) * kWG + (int)fx);
+  if (v == kWDirty) return 0;
+  wind = v;
+  return 2;
 }
 
 // Clenshaw coefficients of the irregular-harmonic recurrence (2n+1, (n+1)^2)
@@ -736,7 +772,7 @@ __device__ __forceinline__ double ff_chord_term(const FFRound& R, const FFQuery&
 }
 
 __device__ __forceinline__ double ff_pair_value(const FFRound& R, const FFQuery& Q, int32_t c,
-                                                bool far, int P, unsigned long long& terms) {
+                                                bool far, int wind, unsigned long long& terms) {
   int lvl = -1;
   double x = 1.0, y = 0.0, z = 0.0;
   if (far) lvl = ff_level_of(R, Q, c, x, y, z);
@@ -745,10 +781,10 @@ __device__ __forceinline__ double ff_pair_value(const FFRound& R, const FFQuery&
   const double2* Dc = R.D + (int64_t)(far ? c : 0) * kFFTerms;
   const int pl = far ? ff_order(lvl) : -1;
   double v = ff_eval_rt(x, y, z, Dc, ff_order(wl), pl);
-  (void)P;
   if (!far) return 0.0;
   terms += (unsigned long long)ff_nterms(pl);
   if (__ldg(R.chord + c) >= 0) v = __dadd_rn(v, ff_chord_term(R, Q, c));
+  if (wind) v = __dadd_rn(v, kShadowJump * (double)wind);
   return v;
 }
 
@@ -776,7 +812,8 @@ k_ff_count(int32_t m, const int32_t* __restrict__ order, const int32_t* __restri
   if (kWarp) {
     for (int j0 = 0; Q.live && j0 < L.n; j0 += 32) {  // warp-uniform (one query)
       const int32_t c = ff_entry(L, j0 + lane);
-      const bool near = c >= 0 && !ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+      int wd;
+      const bool near = c >= 0 && ff_class(R, c, Q.qa, Q.qb, Q.qc, wd) == 0;
       if (near) atomicAdd(ecnt + c, 1u);
       n += (unsigned)__popc(__ballot_sync(0xffffffffu, near));
     }
@@ -790,7 +827,8 @@ k_ff_count(int32_t m, const int32_t* __restrict__ order, const int32_t* __restri
   const int jn = (int)__reduce_max_sync(0xffffffffu, Q.live ? (unsigned)L.n : 0u);
   for (int j = 0; j < jn; ++j) {  // warp-uniform loop
     const int32_t c = Q.live ? ff_entry(L, j) : -1;
-    const bool far = c >= 0 && ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+    int wd;
+    const bool far = c >= 0 && ff_class(R, c, Q.qa, Q.qb, Q.qc, wd) > 0;
     const bool near = c >= 0 && !far;
     n += near ? 1u : 0u;
     const unsigned b = __ballot_sync(0xffffffffu, near);
@@ -827,7 +865,7 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
   const FFList L = ff_list(F, R.C, Q);
   const int lane = threadIdx.x & 31;
   double om = 0.0;
-  unsigned long long nfar = 0, terms = 0, nloc = 0;
+  unsigned long long nfar = 0, terms = 0, nloc = 0, nsh = 0;
   if (L.leaf >= 0) {  // the leaf's local expansion: every cycle its ancestors took
     om = ff_local(F, L, Q);
     nloc = (!kWarp || lane == 0) ? 1 : 0;
@@ -836,7 +874,9 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
     int k = 0;
     for (int j0 = 0; Q.live && j0 < L.n; j0 += 32) {  // warp-uniform (one query)
       const int32_t c = ff_entry(L, j0 + lane);
-      const bool far = c >= 0 && ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+      int wd = 0;
+      const int cls = c >= 0 ? ff_class(R, c, Q.qa, Q.qb, Q.qc, wd) : 0;
+      const bool far = cls > 0;
       const bool near = c >= 0 && !far;
       const unsigned nb = __ballot_sync(0xffffffffu, near);
       if (near) {
@@ -844,9 +884,10 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
         recs[eoff[c] + slot] = make_int2(Q.s, k + __popc(nb & ((1u << lane) - 1u)));
       }
       k += __popc(nb);
-      const double v = ff_pair_value(R, Q, c, far, 0, terms);
+      const double v = ff_pair_value(R, Q, c, far, wd, terms);
       const unsigned fb = __ballot_sync(0xffffffffu, far);
       nfar += far ? 1 : 0;
+      nsh += cls == 2 ? 1 : 0;
       for (int i = 0; i < 32; ++i) {  // fold in list order
         const double vi = __shfl_sync(0xffffffffu, v, i);
         if ((fb >> i) & 1u) om = __dadd_rn(om, vi);
@@ -858,7 +899,9 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
     const int jn = (int)__reduce_max_sync(0xffffffffu, Q.live ? (unsigned)L.n : 0u);
     for (int j = 0; j < jn; ++j) {  // warp-uniform loop
       const int32_t c = Q.live ? ff_entry(L, j) : -1;
-      const bool far = c >= 0 && ff_far2(Q.qa, Q.qb, Q.qc, R.g3 + 3 * c, R.r2 + 2 * c);
+      int wd = 0;
+      const int cls = c >= 0 ? ff_class(R, c, Q.qa, Q.qb, Q.qc, wd) : 0;
+      const bool far = cls > 0;
       const bool near = c >= 0 && !far;
       const unsigned b = __ballot_sync(0xffffffffu, near);
       if (near) {  // append to entry c's near-pair list
@@ -871,6 +914,7 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
       // records of one level are contiguous
       const unsigned fb = __ballot_sync(0xffffffffu, far);
       if (far) {
+        nsh += cls == 2 ? 1 : 0;
         const int key = ff_level(R, Q, c) * R.C + c;
         const unsigned slot = ff_append(fb, key, lfill);
         frecs[loffs[key] + slot] = make_int2(Q.s, kf++);
@@ -886,7 +930,9 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
     nfar += __shfl_down_sync(0xffffffffu, nfar, o);
     terms += __shfl_down_sync(0xffffffffu, terms, o);
     nloc += __shfl_down_sync(0xffffffffu, nloc, o);
+    nsh += __shfl_down_sync(0xffffffffu, nsh, o);
   }
+  if (lane == 0 && nsh) atomicAdd(&counters[CNT_SHADOW], nsh);
   if (lane == 0 && nfar) {
     atomicAdd(&counters[CNT_FAR], nfar);
     atomicAdd(&counters[CNT_FAR_TERMS], terms);
@@ -937,6 +983,9 @@ k_ff_far_eval(unsigned long long nrec, const int2* __restrict__ frecs,
       v = ff_eval_own(x, y, z, R.D + (int64_t)c * kFFTerms, pl);
     terms = (unsigned long long)ff_nterms(pl);
     if (__ldg(R.chord + c) >= 0) v = __dadd_rn(v, ff_chord_term(R, Q, c));
+    int wd;  // the pair's shadow winding number (same decision as the fill pass)
+    ff_class(R, c, Q.qa, Q.qb, Q.qc, wd);
+    if (wd) v = __dadd_rn(v, kShadowJump * (double)wd);
   }
   if (live) fval[qfoff[rec.x] + (unsigned long long)rec.y] = v;
   unsigned long long nf = live ? 1 : 0;
@@ -1158,8 +1207,9 @@ static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int3
   FC(cub::DeviceScan::ExclusiveSum(nullptr, tb2, c.ecnt, c.eoff, C + 1, st));
   FC(cub::DeviceScan::ExclusiveSum(nullptr, tb3, c.lcnt, c.loffs, nkey + 1, st));
   FC(ff_grow(c.tmp, c.cap_tmp, std::max(std::max(tb1, tb2), tb3), 1, st));
-  const FFRound R{C, rd.ffg, sc->ff_r, sc->ff_lv, sc->ff_g,
-                  reinterpret_cast<const double2*>(sc->ff_D), sc->ff_chord, rd.ffa};
+  const FFRound R{C,        rd.ffg,   sc->ff_r, sc->ff_lv, sc->ff_g,
+                  reinterpret_cast<const double2*>(sc->ff_D), sc->ff_chord, rd.ffa,
+                  rd.ffw,   rd.ffwg};
   FFLocal F;
   if (rd.fmm) {  // round 0 of a scene with local expansions (gwn_fmm.cu)
     F.loff = rd.fmm->loff;
@@ -1291,6 +1341,127 @@ __global__ void k_vproj(const double* __restrict__ verts, int64_t V, Frame f,
   vproj[2 * V + i] = x * f.d[0] + y * f.d[1] + z * f.d[2];
 }
 
+// Shadow winding grid of closed expanded entry c (one block): kWG x kWG
+// cells over the square around the disk of the cycle's sphere projected
+// along d (X, Y of the round frame).  A cell holds the winding number of the
+// cycle's projection around the cell centre, or kWDirty when some vertex's
+// projection lies within del = 2.02 Lmax of the cell (Lmax: the entry's
+// longest 3-D segment).
+// Why that makes a clean cell exact: a segment (a, b) of the fan sum has
+// den = (a^ - d).(b^ - d) (a^ = the unit vector from the query to a); den < 0
+// forces |a^ - d| < |a^ - b^| <= 2|a - b| / (|a - q| + |b - q|), so the
+// perpendicular distance of a from the query's line is below 2|a - b|.  In
+// a clean cell no segment has den < 0 (no branch flip, no band test: the
+// exact kernel would raise no flag) and no projected segment passes through
+// the cell (its end points would lie within Lmax of it), so the cell's
+// winding number is the query's.  The fan sum then equals Omega/2 of the
+// cycle's fan surface plus 2 pi times that winding number (the forward
+// half-line crosses the fan surface wind times, all at t > 0).
+__global__ void __launch_bounds__(256)
+k_ff_wind(int32_t C, const int32_t* __restrict__ ent_eoff, const int32_t* __restrict__ chord,
+          const double* __restrict__ r2, const double* __restrict__ g3,
+          const double* __restrict__ vproj, int64_t V, int S, int8_t* __restrict__ wg,
+          double* __restrict__ wgeo) {
+  const int c = blockIdx.x;
+  const int t = threadIdx.x;
+  __shared__ int cr[kWG + 1], dr[kWG + 1];
+  __shared__ double s_red[8];
+  const double rmin2 = r2[2 * c], line2 = r2[2 * c + 1];
+  const double line = sqrt(line2);
+  const double x0 = g3[3 * c] - line, y0 = g3[3 * c + 1] - line;
+  const double h = 2.0 * line / kWG, ih = kWG / (2.0 * line);
+  int8_t* out = wg + (int64_t)c * kWG * kWG;
+  if (t == 0) {
+    wgeo[3 * c] = x0;
+    wgeo[3 * c + 1] = y0;
+    wgeo[3 * c + 2] = ih;
+  }
+  // closed expanded cycles only (slivers keep their chord term exact)
+  if (!(chord[c] < 0 && rmin2 < INFINITY && rmin2 > line2 && line > 0.0)) {
+    for (int k = t; k < kWG * kWG; k += blockDim.x) out[k] = (int8_t)kWDirty;
+    return;
+  }
+  const int64_t v0 = (int64_t)ent_eoff[c] * S, v1 = (int64_t)ent_eoff[c + 1] * S;
+  double lm = 0.0;
+  for (int64_t k = v0 + t; k < v1; k += blockDim.x) {
+    if ((k - v0) % S == S - 1) continue;  // an edge's last sample starts no segment
+    const double ex = vproj[k + 1] - vproj[k], ey = vproj[V + k + 1] - vproj[V + k],
+                 ez = vproj[2 * V + k + 1] - vproj[2 * V + k];
+    lm = fmax(lm, ex * ex + ey * ey + ez * ez);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lm = fmax(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+  if ((t & 31) == 0) s_red[t >> 5] = lm;
+  __syncthreads();
+  lm = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) lm = fmax(lm, s_red[w]);
+  // 1% over the bound, plus the rounding of the coordinates
+  const double del = 2.02 * sqrt(lm) + 1e-6 * h + 1e-12 * (fabs(x0) + fabs(y0) + line);
+  for (int row = 0; row < kWG; ++row) {
+    const double yc = y0 + (row + 0.5) * h;
+    for (int k = t; k <= kWG; k += blockDim.x) {
+      cr[k] = 0;
+      dr[k] = 0;
+    }
+    __syncthreads();
+    for (int64_t k = v0 + t; k < v1; k += blockDim.x) {
+      const double ax = vproj[k], ay = vproj[V + k];
+      if (fabs(ay - yc) <= del + 0.5 * h) {  // cells within del of the vertex
+        const double lo = (ax - del - x0) * ih, hi = (ax + del - x0) * ih;
+        if (hi >= 0.0 && lo < (double)kWG) {
+          const int ka = lo < 0.0 ? 0 : (int)lo;
+          const int kb = hi >= (double)kWG ? kWG - 1 : (int)hi;
+          atomicAdd(&dr[ka], 1);
+          atomicAdd(&dr[kb + 1], -1);
+        }
+      }
+      if ((k - v0) % S == S - 1) continue;
+      const double by = vproj[V + k + 1];
+      if ((ay <= yc) != (by <= yc)) {  // the segment crosses the row's centre line
+        const double bx = vproj[k + 1];
+        const double xc = ax + (yc - ay) * (bx - ax) / (by - ay);
+        // cells whose centre lies left of the crossing count it (+x ray)
+        const double f = (xc - x0) * ih - 0.5;
+        const int kc = f <= 0.0 ? 0 : (f >= (double)kWG ? kWG : (int)ceil(f));
+        const int dir = by > ay ? 1 : -1;
+        if (kc > 0) {
+          atomicAdd(&cr[0], dir);
+          atomicAdd(&cr[kc], -dir);
+        }
+      }
+    }
+    __syncthreads();
+    if (t < 32) {  // prefix sums: lane t owns cells 4t .. 4t+3
+      int a[4], b[4], sa = 0, sb = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        sa += cr[4 * t + i];
+        sb += dr[4 * t + i];
+        a[i] = sa;
+        b[i] = sb;
+      }
+      int pa = sa, pb = sb;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ya = __shfl_up_sync(0xffffffffu, pa, o), yb = __shfl_up_sync(0xffffffffu, pb, o);
+        if (t >= o) {
+          pa += ya;
+          pb += yb;
+        }
+      }
+      pa -= sa;
+      pb -= sb;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int wv = pa + a[i], dv = pb + b[i];
+        out[row * kWG + 4 * t + i] =
+            (int8_t)(dv > 0 || wv <= kWDirty || wv > 127 ? kWDirty : wv);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st) {
   const int64_t V = sc->n_edges * sc->S;
   if (V == 0) return cudaSuccess;
@@ -1321,6 +1492,14 @@ cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st) {
       return e;
   }
   k_vproj<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(sc->verts, V, rd.f, rd.vproj);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (sc->ff_n > 0) {
+    if ((e = cudaMalloc(&rd.ffw, (size_t)sc->ff_n * kWG * kWG)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&rd.ffwg, sizeof(double) * 3 * (size_t)sc->ff_n)) != cudaSuccess)
+      return e;
+    k_ff_wind<<<(unsigned)sc->ff_n, 256, 0, st>>>(sc->ff_n, sc->ff_eoff, sc->ff_chord, sc->ff_r,
+                                                  rd.ffg, rd.vproj, V, sc->S, rd.ffw, rd.ffwg);
+  }
   return cudaGetLastError();
 }
 

@@ -354,103 +354,6 @@ __global__ void k_refit(int n, const int32_t* __restrict__ sorted_ids,
   }
 }
 
-// Round-0 spatial ordering of the queries: a counting sort into the 256
-// cells of a 16 x 16 Morton grid over the projected scene box (~4K queries
-// per cell at 1M queries, so every warp stays inside one cell).  Warps then
-// traverse the LBVH and touch leaf records coherently.  The order inside a
-// cell depends on atomic timing, which no result depends on (all reductions
-// are keyed by query slot).
-constexpr int kBuckets = 256;
-
-__device__ __forceinline__ int query_bucket(const double* __restrict__ pos, int32_t s,
-                                            const Frame& f, double amin, double ainv,
-                                            double bmin, double binv) {
-  const double x = pos[3 * (int64_t)s], y = pos[3 * (int64_t)s + 1], z = pos[3 * (int64_t)s + 2];
-  const double a = x * f.e1[0] + y * f.e1[1] + z * f.e1[2];
-  const double b = x * f.e2[0] + y * f.e2[1] + z * f.e2[2];
-  const uint32_t ia = (uint32_t)fmin(fmax((a - amin) * ainv * 16.0, 0.0), 15.0);
-  const uint32_t ib = (uint32_t)fmin(fmax((b - bmin) * binv * 16.0, 0.0), 15.0);
-  uint32_t key = 0;
-  for (int bit = 0; bit < 4; ++bit)
-    key |= (((ia >> bit) & 1u) << (2 * bit)) | (((ib >> bit) & 1u) << (2 * bit + 1));
-  return (int)key;
-}
-
-__global__ void __launch_bounds__(256)
-k_bucket_count(int32_t m, const double* __restrict__ pos, Frame f, double amin, double ainv,
-               double bmin, double binv, uint16_t* __restrict__ keys,
-               int32_t* __restrict__ hist) {
-  __shared__ int32_t h[kBuckets];
-  for (int k = threadIdx.x; k < kBuckets; k += blockDim.x) h[k] = 0;
-  __syncthreads();
-  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < m) {
-    const int key = query_bucket(pos, s, f, amin, ainv, bmin, binv);
-    keys[s] = (uint16_t)key;
-    atomicAdd(&h[key], 1);
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < kBuckets; k += blockDim.x)
-    if (h[k]) atomicAdd(&hist[k], h[k]);
-}
-
-// exclusive scan of the kBuckets counts (one block), cursors zeroed
-__global__ void __launch_bounds__(kBuckets) k_bucket_scan(int32_t* __restrict__ hist,
-                                                          int32_t* __restrict__ cursor) {
-  __shared__ int32_t part[kBuckets];
-  const int t = threadIdx.x;
-  const int32_t v = hist[t];
-  part[t] = v;
-  __syncthreads();
-  for (int o = 1; o < kBuckets; o <<= 1) {
-    const int32_t add = t >= o ? part[t - o] : 0;
-    __syncthreads();
-    part[t] += add;
-    __syncthreads();
-  }
-  hist[t] = part[t] - v;
-  cursor[t] = 0;
-}
-
-__global__ void __launch_bounds__(256)
-k_bucket_scatter(int32_t m, const uint16_t* __restrict__ keys, const int32_t* __restrict__ offs,
-                 int32_t* __restrict__ cursor, int32_t* __restrict__ perm) {
-  __shared__ int32_t cnt[kBuckets];
-  __shared__ int32_t base[kBuckets];
-  for (int k = threadIdx.x; k < kBuckets; k += blockDim.x) cnt[k] = 0;
-  __syncthreads();
-  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  int key = 0, local = 0;
-  if (s < m) {
-    key = keys[s];
-    local = atomicAdd(&cnt[key], 1);
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < kBuckets; k += blockDim.x)
-    if (cnt[k]) base[k] = atomicAdd(&cursor[k], cnt[k]);
-  __syncthreads();
-  if (s < m) perm[offs[key] + base[key] + local] = s;
-}
-
-cudaError_t launch_query_order(const Round& rd, int32_t m, const double* pos, void* scratch,
-                               int32_t* perm, cudaStream_t st) {
-  if (m <= 0) return cudaSuccess;
-  int32_t* hist = (int32_t*)scratch;
-  int32_t* cursor = hist + kBuckets;
-  uint16_t* keys = (uint16_t*)(cursor + kBuckets);
-  cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(int32_t) * kBuckets, st);
-  if (e != cudaSuccess) return e;
-  const unsigned g = (unsigned)((m + 255) / 256);
-  k_bucket_count<<<g, 256, 0, st>>>(m, pos, rd.f, rd.amin, rd.ainv, rd.bmin, rd.binv, keys, hist);
-  k_bucket_scan<<<1, kBuckets, 0, st>>>(hist, cursor);
-  k_bucket_scatter<<<g, 256, 0, st>>>(m, keys, hist, cursor, perm);
-  return cudaGetLastError();
-}
-
-size_t query_order_scratch_bytes(int32_t m) {
-  return sizeof(int32_t) * 2 * kBuckets + sizeof(uint16_t) * ((size_t)m + 8);
-}
-
 // ---- uniform grid over the leaf boxes ------------------------------------
 
 __global__ void k_leaf_extent_sum(const double* __restrict__ leafbox, int64_t n,
@@ -719,6 +622,8 @@ void free_round(Round& rd) {
   if (rd.vproj) cudaFree(rd.vproj);
   if (rd.ffg) cudaFree(rd.ffg);
   if (rd.ffa) cudaFree(rd.ffa);
+  if (rd.ffw) cudaFree(rd.ffw);
+  if (rd.ffwg) cudaFree(rd.ffwg);
   if (rd.cell_offs) cudaFree(rd.cell_offs);
   if (rd.cell_ent) cudaFree(rd.cell_ent);
   free_fmm_round(rd);

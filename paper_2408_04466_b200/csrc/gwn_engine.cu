@@ -567,15 +567,19 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     unsigned long long* rsc = d_cnt + CNT_N;  // round scalars (see kBlk)
     unsigned long long* k3cnt = rsc + 4;
     bool cnt_zeroed = false;
-    // (a round-0 spatial ordering of the queries before the cull costs what
-    // it saves at config 2 -- the grid cull does not need coherent queries --
-    // so the cull takes them in input order)
-    const bool sort_q = false;
-    void* order_tmp = sort_q ? ws.get<char>(query_order_scratch_bytes((int32_t)cm)) : nullptr;
+    // Scenes beyond the shared-memory patch table: round 0 takes the queries
+    // in 3-D Morton order (the K4 order), so a warp's rays cross the same
+    // leaves and patches -- the cull walks the same cells, and the Newton
+    // pass's coefficient loads hit the same L1 lines instead of 32 patches
+    // per warp.  (Config 2's grid cull gains nothing from it.)
+#ifndef GWN_QSORT
+#define GWN_QSORT 1
+#endif
+    const bool sort_q = GWN_QSORT && sc->P > 96 && cm >= 4096;
     // far-field scenes: 3-D Morton order of each round's queries for K4
     const bool ff_sort = sc->ff_n > 0 && cm >= 4096;
     int32_t* ff_order = ff_sort ? ws.get<int32_t>((size_t)cm) : nullptr;
-    void* ff_tmp = ff_sort ? ws.get<char>(ff_order_scratch_bytes((int32_t)cm)) : nullptr;
+    void* ff_tmp = ff_sort || sort_q ? ws.get<char>(ff_order_scratch_bytes((int32_t)cm)) : nullptr;
     int64_t pair_cap = 0;
     void* k3_scratch = nullptr;  // K3 queues (fallback + Newton items)
     CKE(ws.err);
@@ -606,12 +610,10 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
       int32_t m = mc;
       const int32_t* active = nullptr;
       int cur = 0;
-      if (sort_q) {
-        const Round* r0 = nullptr;
-        CKE(ensure_round(sc, 0, st, &r0));
-        CKE(launch_query_order(*r0, mc, q0, order_tmp, act[1], st));
+      if (sort_q && mc >= 4096) {
+        CKE(launch_ff_order(sc, mc, nullptr, q0, ff_tmp, act[1], st));
         active = act[1];  // round 0 writes its re-shoot list into act[0]
-        launches += 3;
+        launches += 1;  // Morton keys (+ a CUB sort)
       }
       for (int r = 0; r < sc->prm.max_rounds && m > 0;) {
         const Round* rdp = nullptr;
@@ -680,7 +682,7 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         const int nchunk = sc->n_edges > 0 ? boundary_chunks(sc, m) : 0;
         if (nchunk > 0) {
           const int32_t* ord = nullptr;
-          if (ff_sort && m >= 4096) {
+          if (ff_sort && m >= 4096 && !(r == 0 && sort_q)) {  // (round 0: sorted already)
             CKE(launch_ff_order(sc, m, active, rpos, ff_tmp, ff_order, st));
             ord = ff_order;
             launches += 1;  // Morton keys (+ a CUB sort)
@@ -792,6 +794,7 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
   stats.far_terms = (int64_t)h_cnt[CNT_FAR_TERMS];
   stats.near_pairs = (int64_t)h_cnt[CNT_NEAR];
   stats.local_evals = (int64_t)h_cnt[CNT_LOCAL];
+  stats.shadow_pairs = (int64_t)h_cnt[CNT_SHADOW];
   if (getenv("GWN_TRACE"))
     fprintf(stderr, "[gwn] fallback: max nodes/item %llu, slowest batch: %llu cycles tree %llu code %llu items %llu, max levels %llu\n",
             h_cnt[CNT_MAXNODES], h_cnt[CNT_BIGITEMS] >> 24, (h_cnt[CNT_BIGITEMS] >> 16) & 255, (h_cnt[CNT_BIGITEMS] >> 8) & 255, h_cnt[CNT_BIGITEMS] & 255, h_cnt[CNT_MAXLEVELS]);

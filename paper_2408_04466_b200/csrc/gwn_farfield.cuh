@@ -114,15 +114,4 @@ __device__ __forceinline__ void frame_q(const Frame& f, double px, double py, do
   qc = __fma_rn(pz, f.d[2], __fma_rn(py, f.d[1], __dmul_rn(px, f.d[0])));
 }
 
-// g3: cycle centre in the round frame (d = z); r2 = (R_min^2, line radius^2)
-__device__ __forceinline__ bool ff_far(double qa, double qb, double qc,
-                                       const double* __restrict__ g3,
-                                       const double* __restrict__ r2) {
-  const double dx = __dsub_rn(__ldg(g3), qa), dy = __dsub_rn(__ldg(g3 + 1), qb);
-  const double dz = __dsub_rn(__ldg(g3 + 2), qc);
-  const double l2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
-  const double R2 = __dadd_rn(l2, __dmul_rn(dz, dz));
-  return l2 > __ldg(r2 + 1) && R2 > __ldg(r2);
-}
-
 }  // namespace gwn

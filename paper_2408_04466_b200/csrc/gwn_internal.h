@@ -46,7 +46,8 @@ enum : int {
   CNT_FAR_TERMS = 9, // solid-harmonic terms those expansions summed
   CNT_NEAR = 10,     // (query, entry) pairs summed exactly (far-field scenes)
   CNT_LOCAL = 11,    // queries whose far field came from a leaf's local expansion
-  CNT_N = 12,
+  CNT_SHADOW = 12,   // far pairs whose forward half-line crosses the cycle's sphere
+  CNT_N = 13,
 };
 
 struct Frame {
@@ -116,6 +117,8 @@ struct Round {
   double* vproj = nullptr;     // (3,V) boundary vertices in the ray frame (K4)
   double* ffg = nullptr;       // (ff_n,3) far-field cycle centres in the ray frame
   double* ffa = nullptr;       // (ff_n,6) sliver chord end points in the ray frame
+  int8_t* ffw = nullptr;       // (ff_n,kWG,kWG) shadow winding grids (k_ff_wind)
+  double* ffwg = nullptr;      // (ff_n,3) grid origin (X, Y) and inverse cell size
   // uniform grid over the leaf boxes (K2 point location); used when its
   // cells stay short, else the LBVH
   bool use_grid = false;
@@ -244,9 +247,6 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
 // [2] overflow, [3] Newton work)
 K3Queues k3_queues(void* scratch, int64_t cap, unsigned long long* k3cnt);
 size_t intersect_scratch_bytes(int64_t pair_cap);
-cudaError_t launch_query_order(const Round& rd, int32_t m, const double* pos, void* scratch,
-                               int32_t* perm, cudaStream_t st);               // gwn_bvh.cu
-size_t query_order_scratch_bytes(int32_t m);
 cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             const int32_t* active, const double* pos, double* bpart, int nchunk,
                             int32_t* flags, unsigned long long* counters, cudaStream_t st,

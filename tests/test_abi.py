@@ -26,7 +26,7 @@ def test_exports_every_declared_symbol():
     for name in names:
         assert hasattr(L, name), name
     assert set(names) == set(_lib.EXPORTS)
-    assert L.gwn_abi_version() == 5
+    assert L.gwn_abi_version() == 6
 
 
 def test_default_params_mirror_reference_epsilons():

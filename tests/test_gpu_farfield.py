@@ -41,6 +41,7 @@ if mode == "halves":  # the same queries in two calls with global index bases
     w2, s2 = G.winding_numbers(sc, qd[h:], index_base=h)
     extra = dict(wh=torch.cat([w1, w2]).cpu().numpy(), sh=torch.cat([s1, s2]).cpu().numpy())
 np.savez(out, w=w.cpu().numpy(), st=st.cpu().numpy(), far=sc.stats()["far_pairs"],
+         shadow=sc.stats()["shadow_pairs"], near=sc.stats()["near_pairs"],
          cycles=sc.n_far_cycles, local=sc.stats()["local_evals"],
          levels=sc.local_expansions["levels"], **extra)
 """
@@ -64,6 +65,22 @@ def test_farfield_matches_exact_sum_config5(tmp_path):
     assert np.array_equal(ex["st"], ff["st"])
     ok = ex["st"] == 0
     # truncation bound 1e-12 rad per cycle (DESIGN): |dw| far below the 1e-9 bar
+    assert np.abs(ex["w"] - ff["w"])[ok].max() <= 1e-11
+
+
+def test_shadow_pairs_match_exact_sum_config5(tmp_path):
+    """Pairs whose forward half-line crosses a cycle's sphere (the sphere in
+    front of the query, beyond R_min) are far when their cell of the cycle's
+    shadow winding grid is clean: expansion + 2 pi x winding number (DESIGN
+    §9 f4).  A wrong winding number or sign would move w by 1/2 or more; the
+    exact sum's status flags (band, degenerate) must be unchanged."""
+    n = 1 << 15
+    ex = _run(tmp_path, 5, n, GWN_FARFIELD="0")
+    ff = _run(tmp_path, 5, n)
+    assert int(ff["shadow"]) > n // 4          # the path is exercised
+    assert int(ff["near"]) < int(ff["far"]) // 2
+    assert np.array_equal(ex["st"], ff["st"])
+    ok = ex["st"] == 0
     assert np.abs(ex["w"] - ff["w"])[ok].max() <= 1e-11
 
 
