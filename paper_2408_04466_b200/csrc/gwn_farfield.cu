@@ -312,13 +312,16 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
     }
   };
   // smallest R at which the order-p truncation bound (gwn_farfield.cuh,
-  // ff_bound) is <= kFFTau; the bound decreases in R, so bisection
+  // ff_bound) is <= tau; the bound decreases in R, so bisection.  tau: the
+  // per-entry share of the kFFDw budget -- first over the cycles (which
+  // entry to split into slivers), then over the final entries
+  double tau = 2.0 * M_PI * kFFDw / std::max(1, C);
   auto rmin_of = [&](const Entry& en, double p) {
     double lo = en.rho * (1.0 + 1e-9), hi = 2.0 * lo;
-    while (ff_bound(en.aabs, en.rho, (int)p, hi) > kFFTau) hi *= 2.0;
+    while (ff_bound(en.aabs, en.rho, (int)p, hi) > tau) hi *= 2.0;
     for (int it = 0; it < 60; ++it) {
       const double mid = 0.5 * (lo + hi);
-      (ff_bound(en.aabs, en.rho, (int)p, mid) > kFFTau ? lo : hi) = mid;
+      (ff_bound(en.aabs, en.rho, (int)p, mid) > tau ? lo : hi) = mid;
     }
     return hi;
   };
@@ -359,6 +362,8 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
   }
   const int nk = (int)ents.size();
   if (n_exp == 0) return cudaSuccess;  // nothing expands: the plain exact K4
+  tau = std::min(tau, 2.0 * M_PI * kFFDw / nk);
+  sc->ff_tau = tau;
   // permute the edges so every entry is a contiguous edge range
   std::vector<int32_t> perm;  // new edge k = old edge perm[k]
   std::vector<int32_t> eoff(nk + 1, 0), chord(nk, -1);

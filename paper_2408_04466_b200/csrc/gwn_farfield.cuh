@@ -18,10 +18,11 @@
 //   Legendre tail: grad of |d|^n P_n(cos) is <= sqrt(2) n |d|^(n-1) (|P_n| <= 1
 //   and Bernstein's inequality), summed over n > K:
 //     sqrt(2) A_abs (K+1) rho^K / (R^K (R - rho)^2).
-// A (query, cycle) pair is "far" when R^2 >= R_min^2 with the bound at
-// kFFTau and the line to the query misses the sphere.  Both K4 kernels take
-// the decision with ff_far() on the same bits, so the exact kernel's masked /
-// skipped segments and the far kernel's terms partition the cycles exactly.
+// A (query, cycle) pair is "far" when R^2 >= R_min^2 with the bound at the
+// scene's tau and either the forward half-line misses the sphere or its
+// shadow cell is clean (gwn_boundary.cu, ff_class).  Every K4 pass takes the
+// decision with ff_class on the same bits, so the exact and far pairs
+// partition the (query, cycle) pairs exactly.
 #pragma once
 
 #include <math.h>
@@ -36,7 +37,12 @@ namespace gwn {
 // (kFFLevels)
 constexpr int kFFK = 48;
 constexpr int kFFTerms = (kFFK + 1) * (kFFK + 2) / 2;  // (n, m), 0 <= m <= n <= K
-constexpr double kFFTau = 1e-12;                       // truncation bound per cycle (rad)
+// Error budget of the far field: every expanded entry's truncation is bounded
+// by tau = 2 pi kFFDw / (expanded entries) (Omega units, per pair; the FMM
+// splits it into two halves), so the far field moves a query's w by at most
+// kFFDw -- two orders below the north star's 1e-6.  Measured errors stay
+// near 1e-14 (the bound is conservative).
+constexpr double kFFDw = 1e-8;
 // far-field partial rows: cycle groups summed in fixed order by K5, so the
 // far kernel fills the GPU and w stays bit-identical for any batching
 constexpr int kFFRows = 16;
@@ -57,7 +63,6 @@ constexpr int kFmmLT = (kFmmP + 1) * (kFmmP + 2) / 2;
 constexpr int kFmmKT = (kFmmK + 1) * (kFmmK + 2) / 2;
 constexpr int kFmmIN = kFmmK + kFmmP;
 constexpr int kFmmIT = (kFmmIN + 1) * (kFmmIN + 2) / 2;
-constexpr double kFmmTau = 0.5 * kFFTau;  // each of the two truncations of a translated pair
 
 // Omega(z + x) = sum_j [Re(conj(R_j^0(x)) L_j^0) + 2 sum_{k>=1} Re(conj(R_j^k(x)) L_j^k)]
 // (L2P), the regular harmonics by the recurrences of gwn_farfield.cu's

@@ -18,7 +18,8 @@
 //   L2P  fmm_l2p (gwn_farfield.cuh).
 // Negative orders by X_n^{-m} = (-1)^m conj(X_n^m) for X = R, I, D, L.
 //
-// Error budget of a translated (box, cycle) pair, each half kFmmTau:
+// Error budget of a translated (box, cycle) pair, each half tau / 2 (tau:
+// the scene's per-entry share, gwn_farfield.cu):
 //   (1) the cycle's multipole truncated at K = kFmmK (the orders M2L
 //       translates) at the box's nearest point, D - r_B:
 //       ff_bound(A_abs, rho, K, D - r_B);
@@ -29,7 +30,7 @@
 //       M <= A_abs / (D - R0 - rho)^2 + ff_bound(A_abs, rho, K, D - R0).
 // Both decrease in the box-centre distance D, so fmm_setup_scene tabulates per
 // (cycle, level) the smallest D meeting both (bisection, best of several R0):
-// the per-pair guarantee equals the per-pair path's (kFFTau).  The line test
+// the per-pair guarantee equals the per-pair path's (tau).  The line test
 // of the per-pair path (the line through the query misses the cycle's sphere)
 // holds for every query of a box when the line through its centre passes the
 // sphere by more than the box's circumradius.
@@ -68,10 +69,10 @@ static double fmm_tail_bound(double aabs, double rho, double rB, double D) {
   return best;
 }
 
-static bool fmm_ok(double aabs, double rho, double rB, double D) {
+static bool fmm_ok(double aabs, double rho, double rB, double D, double half_tau) {
   if (!(D - rB > rho)) return false;
-  return ff_bound(aabs, rho, kFmmK, D - rB) <= kFmmTau &&
-         fmm_tail_bound(aabs, rho, rB, D) <= kFmmTau;
+  return ff_bound(aabs, rho, kFmmK, D - rB) <= half_tau &&
+         fmm_tail_bound(aabs, rho, rB, D) <= half_tau;
 }
 
 static double fmm_box_radius(const gwn_scene* sc, int l) {
@@ -107,11 +108,11 @@ cudaError_t fmm_setup_scene(gwn_scene* sc, const std::vector<double>& rho,
       const double rB = fmm_box_radius(sc, l);
       double lo = rB + rho[c], hi = 2.0 * lo + 1.0;
       int guard = 0;
-      while (!fmm_ok(aabs[c], rho[c], rB, hi) && guard++ < 200) hi *= 2.0;
+      while (!fmm_ok(aabs[c], rho[c], rB, hi, 0.5 * sc->ff_tau) && guard++ < 200) hi *= 2.0;
       if (guard >= 200) continue;
       for (int it = 0; it < 80; ++it) {
         const double mid = 0.5 * (lo + hi);
-        (fmm_ok(aabs[c], rho[c], rB, mid) ? hi : lo) = mid;
+        (fmm_ok(aabs[c], rho[c], rB, mid, 0.5 * sc->ff_tau) ? hi : lo) = mid;
       }
       dmin[(size_t)c * nl + l] = hi;
     }

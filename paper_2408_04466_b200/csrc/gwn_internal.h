@@ -166,6 +166,7 @@ struct gwn_scene {
   double* ff_r = nullptr;       // (ff_n,2) R_min^2 (+inf: exact only), line radius^2
   double* ff_D = nullptr;       // (ff_n, kFFTerms, 2) double-layer moments
   double* ff_lv = nullptr;      // (ff_n, kFFLevels) R^2 thresholds of the adaptive orders
+  double ff_tau = 0.0;          // per-entry truncation bound (Omega units, kFFDw budget)
   int32_t* ff_chord = nullptr;  // (ff_n) sliver entries: edge of the closing chord, else -1
   std::vector<double> ff_chord_host;  // (ff_n,6) chord start / end (world), zeros for cycles
   // octree of the far field's local expansions (gwn_fmm.cu): cube, leaf level
