@@ -568,10 +568,10 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
     unsigned long long* k3cnt = rsc + 4;
     bool cnt_zeroed = false;
     // Scenes beyond the shared-memory patch table: round 0 takes the queries
-    // in 3-D Morton order (the K4 order), so a warp's rays cross the same
-    // leaves and patches -- the cull walks the same cells, and the Newton
-    // pass's coefficient loads hit the same L1 lines instead of 32 patches
-    // per warp.  (Config 2's grid cull gains nothing from it.)
+    // in ray-column order (launch_column_order), so a warp's rays cross the
+    // same leaves and patches -- the cull reads each cell's entries once, and
+    // the Newton pass's coefficient loads hit the same L1 lines instead of 32
+    // patches per warp.  (Config 2's grid cull gains nothing from it.)
 #ifndef GWN_QSORT
 #define GWN_QSORT 1
 #endif
@@ -611,9 +611,11 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
       const int32_t* active = nullptr;
       int cur = 0;
       if (sort_q && mc >= 4096) {
-        CKE(launch_ff_order(sc, mc, nullptr, q0, ff_tmp, act[1], st));
+        const Round* r0 = nullptr;
+        CKE(ensure_round(sc, 0, st, &r0, &stats.ms_round_build));
+        CKE(launch_column_order(*r0, mc, q0, ff_tmp, act[1], st));
         active = act[1];  // round 0 writes its re-shoot list into act[0]
-        launches += 1;  // Morton keys (+ a CUB sort)
+        launches += 1;  // column keys (+ a CUB sort)
       }
       for (int r = 0; r < sc->prm.max_rounds && m > 0;) {
         const Round* rdp = nullptr;
@@ -682,7 +684,7 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         const int nchunk = sc->n_edges > 0 ? boundary_chunks(sc, m) : 0;
         if (nchunk > 0) {
           const int32_t* ord = nullptr;
-          if (ff_sort && m >= 4096 && !(r == 0 && sort_q)) {  // (round 0: sorted already)
+          if (ff_sort && m >= 4096) {
             CKE(launch_ff_order(sc, m, active, rpos, ff_tmp, ff_order, st));
             ord = ff_order;
             launches += 1;  // Morton keys (+ a CUB sort)

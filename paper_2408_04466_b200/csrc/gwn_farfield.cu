@@ -503,6 +503,54 @@ size_t ff_order_scratch_bytes(int32_t m) {
   return tb + 4 * sizeof(unsigned) * (size_t)m + 1024;
 }
 
+// Round-0 order of the queries for the cull and the intersector: 2-D Morton
+// keys (15 bits per axis) of their projections onto the ray frame's (e1, e2)
+// plane over the projected scene box, so a warp's queries share ray columns
+// -- the same cull cells (read once from DRAM, then from L1/L2) and the same
+// candidate patches (the Newton pass's coefficient lines).
+__device__ __forceinline__ unsigned spread15(unsigned v) {
+  v &= 0x7fffu;
+  v = (v | (v << 8)) & 0x00FF00FFu;
+  v = (v | (v << 4)) & 0x0F0F0F0Fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+
+__global__ void k_col_keys(int32_t m, const double* __restrict__ pos, Frame f, double amin,
+                           double ainv, double bmin, double binv, unsigned* __restrict__ keys,
+                           int32_t* __restrict__ ids) {
+  const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  double qa, qb, qc;
+  frame_q(f, pos[3 * (int64_t)s], pos[3 * (int64_t)s + 1], pos[3 * (int64_t)s + 2], qa, qb, qc);
+  const unsigned ia = (unsigned)fmin(32767.0, fmax(0.0, (qa - amin) * ainv * 32768.0));
+  const unsigned ib = (unsigned)fmin(32767.0, fmax(0.0, (qb - bmin) * binv * 32768.0));
+  keys[s] = (spread15(ia) << 1) | spread15(ib);
+  ids[s] = s;
+}
+
+cudaError_t launch_column_order(const Round& rd, int32_t m, const double* pos, void* scratch,
+                                int32_t* order, cudaStream_t st) {
+  char* p = (char*)scratch;
+  auto take = [&](size_t b) {
+    char* r = p;
+    p += (b + 255) & ~(size_t)255;
+    return r;
+  };
+  unsigned* k0 = (unsigned*)take(sizeof(unsigned) * m);
+  unsigned* k1 = (unsigned*)take(sizeof(unsigned) * m);
+  int32_t* i0 = (int32_t*)take(sizeof(int32_t) * m);
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, i0, order, m, 0, 30, st);
+  void* tmp = take(tb);
+  k_col_keys<<<(m + 255) / 256, 256, 0, st>>>(m, pos, rd.f, rd.amin, rd.ainv, rd.bmin, rd.binv,
+                                              k0, i0);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, i0, order, m, 0, 30, st);
+}
+
 cudaError_t launch_ff_order(const gwn_scene* sc, int32_t m, const int32_t* active,
                             const double* pos, void* scratch, int32_t* order, cudaStream_t st) {
   char* p = (char*)scratch;

@@ -260,6 +260,8 @@ void free_farfield(gwn_scene* sc);
 cudaError_t launch_ff_order(const gwn_scene* sc, int32_t m, const int32_t* active,
                             const double* pos, void* scratch, int32_t* order, cudaStream_t st);
 size_t ff_order_scratch_bytes(int32_t m);
+cudaError_t launch_column_order(const Round& rd, int32_t m, const double* pos, void* scratch,
+                                int32_t* order, cudaStream_t st);  // gwn_farfield.cu
 cudaError_t launch_vproj(const gwn_scene* sc, Round& rd, cudaStream_t st);  // gwn_boundary.cu
 // far-field local expansions (gwn_fmm.cu): scene-level acceptance table,
 // per-round octree build (caller holds sc->mu), release
