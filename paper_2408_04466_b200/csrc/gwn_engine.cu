@@ -641,9 +641,10 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         int64_t want = (int64_t)(sc->pairs_per_query * 1.25 * m) + 4096;
         if (want > pair_cap) {
           pair_cap = want;
-          CKE(ws.k3(intersect_scratch_bytes(pair_cap), &k3_scratch));
+          CKE(ws.k3(intersect_scratch_bytes(pair_cap, sc->P), &k3_scratch));
         }
-        const K3Queues Q = k3_queues(k3_scratch, pair_cap, k3cnt);
+        // (small re-shoot rounds skip the patch bins: a few items per patch)
+        const K3Queues Q = k3_queues(k3_scratch, pair_cap, k3cnt, m >= kBinMinQueries ? sc->P : 0);
         tr.mark("round setup");
         tl_mark(st, "round setup done");
         if (sc->timed) CKE(cudaEventRecord(ev[0], st));
@@ -674,7 +675,7 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
         if (sc->P > 0) {
           CKE(launch_intersect(sc, rd, Q, rsc, qproj, chi, fl, d_cnt, k3cnt + 3,
                                sc->timed ? ev4 : nullptr, &join, nullptr, st));
-          launches += 3;
+          launches += Q.n_bins ? 6 : 3;  // + bin memset, scan, scatter
         }
         tr.mark("k3 launched");
         tl_mark(st, "k3 main done");

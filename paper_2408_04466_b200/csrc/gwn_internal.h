@@ -246,8 +246,11 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
 // K3 queues in `scratch` (intersect_scratch_bytes(cap)); k3cnt: 4 zeroed
 // device counters per round ([0] fallback items, [1] Newton items,
 // [2] overflow, [3] Newton work)
-K3Queues k3_queues(void* scratch, int64_t cap, unsigned long long* k3cnt);
-size_t intersect_scratch_bytes(int64_t pair_cap);
+// P > kTabMaxP adds the patch bins of the Newton pass (K3Queues::nkey ...);
+// rounds of fewer than kBinMinQueries queries pass P = 0 (no bins).
+constexpr int32_t kBinMinQueries = 1 << 16;
+K3Queues k3_queues(void* scratch, int64_t cap, unsigned long long* k3cnt, int64_t P);
+size_t intersect_scratch_bytes(int64_t pair_cap, int64_t P);
 cudaError_t launch_boundary(const gwn_scene* sc, const Round& rd, int32_t m,
                             const int32_t* active, const double* pos, double* bpart, int nchunk,
                             int32_t* flags, unsigned long long* counters, cudaStream_t st,

@@ -191,6 +191,16 @@ struct K3Queues {
   unsigned long long* n_count;
   unsigned long long cap;
   int* overflow;
+  // Patch bins (scenes beyond the shared-memory patch table, n_bins = P, else
+  // 0): k3_candidates counts its Newton items per patch (bin_count, zeroed per
+  // round) and records (patch, rank in bin) per item; k_bin_scan /
+  // k_bin_scatter turn that into `perm`, the item indices in patch order, so a
+  // warp of the Newton pass works on one patch at a time.
+  int2* nkey = nullptr;
+  int32_t* perm = nullptr;
+  int32_t* bin_count = nullptr;
+  int32_t* bin_off = nullptr;
+  int32_t n_bins = 0;
 };
 
 }  // namespace gwn

@@ -257,12 +257,12 @@ extern "C" int gwn_eval_rays(gwn_scene* sc, const double* origins, int64_t R,
       HitRec* rec = nullptr;
       for (;;) {
         std::vector<void*> rb;
-        void* scratch = dalloc<char>(rb, intersect_scratch_bytes(pair_cap), st, ae);
+        void* scratch = dalloc<char>(rb, intersect_scratch_bytes(pair_cap, sc->P), st, ae);
         const int64_t rcap = 2 * pair_cap + 1024;
         rec = dalloc<HitRec>(bufs, rcap, st, ae);
         CKR(ae);
         CKR(cudaMemsetAsync(rsc, 0, sizeof(unsigned long long) * 12, st));
-        const K3Queues Q = k3_queues(scratch, pair_cap, rsc + 8);
+        const K3Queues Q = k3_queues(scratch, pair_cap, rsc + 8, m >= kBinMinQueries ? sc->P : 0);
         CullZero z;
         z.chi = rchi;
         z.flags = rfl;

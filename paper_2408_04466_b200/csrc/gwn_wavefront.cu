@@ -139,6 +139,20 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev, K3Queues Q, Wav
       if (kn < Q.cap) Q.nq[kn] = NewtonItem{slot, patch, code, nu_, nv_, qa, qb, qc, 0.0};
       else *Q.overflow = 1;
     }
+    if (Q.n_bins) {
+      // rank of the item in its patch bin: one atomic per distinct patch of the
+      // warp (neighbouring rays cross the same patches)
+      const bool put = wantN && kn < Q.cap;
+      const int lane = threadIdx.x & 31;
+      const unsigned grp = __match_any_sync(0xffffffffu, put ? patch : -1 - lane);
+      if (put) {
+        const int leader = __ffs(grp) - 1;
+        int32_t rank0 = 0;
+        if (lane == leader) rank0 = atomicAdd(Q.bin_count + patch, __popc(grp));
+        rank0 = __shfl_sync(grp, rank0, leader);
+        Q.nkey[kn] = make_int2(patch, rank0 + __popc(grp & ((1u << lane) - 1u)));
+      }
+    }
   }
   warp_sum_u64(&w.counters[CNT_NODES], tested);
 }
@@ -477,6 +491,158 @@ k3_newton(WaveArgs w, int32_t P) {
   warp_sum_u64(&w.counters[CNT_ROOTS], roots);
 }
 
+// Patch bins, step 2: exclusive scan of the per-patch item counts (one block;
+// P is at most a few 10^4).
+__global__ void __launch_bounds__(1024) k_bin_scan(const int32_t* __restrict__ count,
+                                                   int32_t* __restrict__ off, int32_t P) {
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int32_t b = 0; b < P; b += 1024) {
+    const int32_t i = b + (int32_t)threadIdx.x;
+    const int32_t c = i < P ? count[i] : 0;
+    int32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int32_t t = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += v;
+      }
+      wsum[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const int32_t before = carry + (wid ? wsum[wid - 1] : 0) + incl - c;
+    if (i < P) off[i] = before;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = before + c;
+    __syncthreads();
+  }
+}
+
+// Patch bins, step 3: item i goes to position off[patch] + rank.
+__global__ void __launch_bounds__(256) k_bin_scatter(K3Queues Q) {
+  const int64_t n = (int64_t)min(*Q.n_count, Q.cap);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int2 k = Q.nkey[i];
+    Q.perm[__ldg(Q.bin_off + k.x) + k.y] = (int32_t)i;
+  }
+}
+
+// Newton pass in patch order (scenes beyond the shared-memory patch table).
+// A batch of 32 items taken through `perm` holds one patch (two where a bin
+// ends): the warp stages that patch's 48 power coefficients in its own
+// shared-memory slot and every lane re-reads them as broadcasts each iteration
+// (no per-lane coefficient registers, no 32-line L1 gathers: ncu put
+// k3_newton<false> at 99% L1/LSU and 15% FP64 pipe at config 5).  Items of one
+// query are no longer adjacent, so chi / flags go out as one atomic per root.
+#ifndef GWN_NEWTON_MINB_BIN
+#define GWN_NEWTON_MINB_BIN 5
+#endif
+#ifndef GWN_NB_PREFETCH
+#define GWN_NB_PREFETCH 1
+#endif
+#ifndef GWN_NB_RUN
+#define GWN_NB_RUN 8
+#endif
+// A warp reserves a run of up to GWN_NB_RUN consecutive batches at a time, so
+// its shared-memory table stays valid from batch to batch (the coefficient
+// load that fills it is a full L2 round trip on the batch's critical path:
+// 29% of the stall samples when every batch re-staged its patch).
+__global__ void __launch_bounds__(128, GWN_NEWTON_MINB_BIN)
+k3_newton_binned(WaveArgs w, const int32_t* __restrict__ perm) {
+  __shared__ __align__(16) double wtab[4][48];
+  const int64_t n = (int64_t)min(*w.n_count, w.n_cap);
+  const int64_t nb = (n + 31) >> 5;  // batches
+  const int64_t nwarps = (int64_t)gridDim.x * 4;
+  // run length: long runs for table reuse, short ones when there is little work
+  const int64_t R = max((int64_t)1, min((int64_t)GWN_NB_RUN, nb / (nwarps * 4)));
+  unsigned long long iters = 0, roots = 0;
+  const int lane = threadIdx.x & 31;
+  double* tab = wtab[threadIdx.x >> 5];
+  unsigned r_cur = 0, r_nxt = 0;
+  if (lane == 0) {
+    r_cur = reserve_batch(w.n_work);
+    r_nxt = reserve_batch(w.n_work);
+  }
+  int64_t b = R * (int64_t)__shfl_sync(0xffffffffu, r_cur, 0);  // current batch
+  int64_t run_end = b + R;
+  int32_t cur_p = -1;
+#if GWN_NB_PREFETCH
+  // perm index two batches ahead, item lines prefetched one batch ahead
+  int32_t idx = b * 32 + lane < n ? perm[b * 32 + lane] : -1;
+#else
+  NewtonItem it{};
+  if (b * 32 + lane < n) it = w.nq[perm[b * 32 + lane]];
+#endif
+  while (b < nb) {
+    // the batch after this one: next of the run, else the next run's first
+    int64_t b2 = b + 1, run_end2 = run_end;
+    if (b2 >= run_end) {
+      b2 = R * (int64_t)__shfl_sync(0xffffffffu, r_nxt, 0);
+      run_end2 = b2 + R;
+      if (lane == 0 && b2 < nb) r_nxt = reserve_batch(w.n_work);
+    }
+#if GWN_NB_PREFETCH
+    const int32_t idx2 = b2 * 32 + lane < n ? perm[b2 * 32 + lane] : -1;
+    NewtonItem it{};
+    if (idx >= 0) it = w.nq[idx];
+    const bool have = idx >= 0;
+#else
+    NewtonItem nx{};
+    if (b2 * 32 + lane < n) nx = w.nq[perm[b2 * 32 + lane]];
+    const bool have = b * 32 + lane < n;
+#endif
+    int32_t chi = 0, fl = 0;
+    unsigned rem = __ballot_sync(0xffffffffu, have);
+    while (rem) {
+      const int leader = __ffs(rem) - 1;
+      const int32_t p = __shfl_sync(0xffffffffu, it.patch, leader);
+      const bool mine = have && it.patch == p;
+      rem &= ~__ballot_sync(0xffffffffu, mine);
+      if (p != cur_p) {
+        __syncwarp();
+        if (lane < 24)
+          reinterpret_cast<double2*>(tab)[lane] =
+              __ldg(reinterpret_cast<const double2*>(w.powc + 48 * (int64_t)p) + lane);
+        __syncwarp();
+        cur_p = p;
+      }
+#if GWN_NB_PREFETCH
+      // the next batch's item lines into L1 while this one is solved
+      if (idx2 >= 0 && !rem)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(w.nq + idx2));
+#endif
+      if (mine) {
+        const RootResult r = newton_solve_pow<2>(tab, it.qa, it.qb, it.qc, it.u, it.v, w.prm);
+        newton_own(w, it.slot, it.code, r, chi, fl, iters, roots);
+      }
+    }
+    if (chi) atomicAdd(&w.chi[it.slot], chi);
+    if (fl) atomicOr(&w.flags[it.slot], fl);
+#if GWN_NB_PREFETCH
+    idx = idx2;
+#else
+    it = nx;
+#endif
+    b = b2;
+    run_end = run_end2;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // see k3_newton
+  warp_sum_u64(&w.counters[CNT_NEWTON], iters);
+  warp_sum_u64(&w.counters[CNT_ROOTS], roots);
+}
+
 static int grid_for(const void* fn, int sm_count, int block = 128, size_t smem = 0) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem);
@@ -492,7 +658,8 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
                              int32_t* chi, int32_t* flags, unsigned long long* counters,
                              unsigned long long* newton_work, cudaEvent_t* ev4,
                              cudaEvent_t* join, const RecordSink* rec, cudaStream_t st) {
-  static thread_local int g_cand = 0, g_fb = 0, g_newton = 0, g_newton_s = 0, g_dev = -1;
+  static thread_local int g_cand = 0, g_fb = 0, g_newton = 0, g_newton_s = 0, g_newton_b = 0,
+                          g_dev = -1;
   if (g_dev != sc->device) {
     g_cand = grid_for((const void*)k3_candidates, sc->sm_count, kCandBlock);
     // fallback: 3 blocks per SM spread its few, long-lived items thinly
@@ -503,6 +670,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
     g_newton = grid_for((const void*)k3_newton<false>, sc->sm_count);
     g_newton_s = grid_for((const void*)k3_newton<true>, sc->sm_count, 128,
                           sizeof(double) * kTabStride * kTabMaxP);
+    g_newton_b = grid_for((const void*)k3_newton_binned, sc->sm_count);
     g_dev = sc->device;
   }
   cudaError_t e = cudaSuccess;
@@ -510,6 +678,10 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
              rec ? rec->rec : nullptr, rec ? rec->count : nullptr, rec ? rec->cap : 0ull,
              counters, Q.overflow, Q.nq, Q.n_count, Q.cap, newton_work,
              rd.sub_offs, rd.sub, rd.subbox, rd.subskip, rd.subgc, rd.sub_level};
+  const bool binned = Q.n_bins > 0;
+  if (binned &&
+      (e = cudaMemsetAsync(Q.bin_count, 0, sizeof(int32_t) * Q.n_bins, st)) != cudaSuccess)
+    return e;
   if (ev4) cudaEventRecord(ev4[0], st);
   tl_mark(st, "k3 start");
   static const bool pdl_cand = [] {
@@ -576,14 +748,24 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
     if ((e = cudaEventRecord(join_ev, side)) != cudaSuccess) return e;
     *join = join_ev;
   }
-  if (ev4) cudaEventRecord(ev4[4], st);
   tl_mark(st, "newton start");
   static const bool smem_ok = [] {
     const char* e = getenv("GWN_NEWTON_SMEM");
     return !(e && atoi(e) == 0);
   }();
   const bool tabled = smem_ok && sc->P <= kTabMaxP;
-  if (use_pdl) {
+  // (stage timing: the Newton stage includes its scan and scatter)
+  if (ev4) cudaEventRecord(ev4[4], st);
+  if (binned) {  // items in patch order (the fallback runs meanwhile)
+    k_bin_scan<<<1, 1024, 0, st>>>(Q.bin_count, Q.bin_off, Q.n_bins);
+    k_bin_scatter<<<sc->sm_count * 8, 256, 0, st>>>(Q);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (binned) {
+    // (a plain launch: the scan and scatter above sit between the fallback and
+    // this kernel, so there is no programmatic pair to form)
+    k3_newton_binned<<<g_newton_b, 128, 0, st>>>(w, Q.perm);
+  } else if (use_pdl) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(tabled ? g_newton_s : g_newton);
     cfg.blockDim = dim3(128);
@@ -609,7 +791,7 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
   return e;
 }
 
-K3Queues k3_queues(void* scratch, int64_t cap, unsigned long long* k3cnt) {
+K3Queues k3_queues(void* scratch, int64_t cap, unsigned long long* k3cnt, int64_t P) {
   char* p = (char*)scratch;
   K3Queues q;
   auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };  // keep every queue aligned
@@ -618,6 +800,20 @@ K3Queues k3_queues(void* scratch, int64_t cap, unsigned long long* k3cnt) {
   q.fq = (NodeItem*)p;
   p += up(sizeof(NodeItem) * cap);
   q.nq = (NewtonItem*)p;
+#ifndef GWN_NEWTON_BIN
+#define GWN_NEWTON_BIN 1
+#endif
+  if (GWN_NEWTON_BIN && P > kTabMaxP && cap < (1ll << 31)) {
+    p += up(sizeof(NewtonItem) * cap);
+    q.nkey = (int2*)p;
+    p += up(sizeof(int2) * cap);
+    q.perm = (int32_t*)p;
+    p += up(sizeof(int32_t) * cap);
+    q.bin_count = (int32_t*)p;
+    p += up(sizeof(int32_t) * P);
+    q.bin_off = (int32_t*)p;
+    q.n_bins = (int32_t)P;
+  }
   q.f_count = k3cnt;
   q.n_count = k3cnt + 1;
   q.overflow = (int*)(k3cnt + 2);
@@ -625,8 +821,10 @@ K3Queues k3_queues(void* scratch, int64_t cap, unsigned long long* k3cnt) {
   return q;
 }
 
-size_t intersect_scratch_bytes(int64_t pair_cap) {
-  return (sizeof(int2) + sizeof(NodeItem) + sizeof(NewtonItem)) * pair_cap + 512;
+size_t intersect_scratch_bytes(int64_t pair_cap, int64_t P) {
+  size_t b = (sizeof(int2) + sizeof(NodeItem) + sizeof(NewtonItem)) * pair_cap + 1024;
+  if (P > kTabMaxP) b += (sizeof(int2) + sizeof(int32_t)) * pair_cap + 2 * sizeof(int32_t) * P + 1024;
+  return b;
 }
 
 }  // namespace gwn
