@@ -128,6 +128,18 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev, K3Queues Q, Wav
       wantN = kr == 1;
       wantF = kr == 2;
     }
+    // Patch bins: rank of the item in its patch's bin, one atomic per distinct
+    // patch of the warp (neighbouring rays cross the same patches), issued
+    // before the block reservation so its round trip overlaps the barriers.
+    // (Every tested pair yields at most one item and at most `cap` pairs are
+    // tested, so a Newton item always has a slot: kn < cap below.)
+    unsigned grp = 0;
+    int32_t rank0 = 0;
+    const int lane = threadIdx.x & 31;
+    if (Q.n_bins) {
+      grp = __match_any_sync(0xffffffffu, wantN ? patch : -1 - lane);
+      if (wantN && lane == __ffs(grp) - 1) rank0 = atomicAdd(Q.bin_count + patch, __popc(grp));
+    }
     // (the loop bound is block-uniform, so every thread reaches the barriers)
     unsigned long long kf = 0, kn = 0;
     block_reserve(S, wantF ? 1 : 0, wantN ? 1 : 0, Q.f_count, Q.n_count, kf, kn);
@@ -139,19 +151,10 @@ k3_candidates(const unsigned long long* __restrict__ npairs_dev, K3Queues Q, Wav
       if (kn < Q.cap) Q.nq[kn] = NewtonItem{slot, patch, code, nu_, nv_, qa, qb, qc, 0.0};
       else *Q.overflow = 1;
     }
-    if (Q.n_bins) {
-      // rank of the item in its patch bin: one atomic per distinct patch of the
-      // warp (neighbouring rays cross the same patches)
-      const bool put = wantN && kn < Q.cap;
-      const int lane = threadIdx.x & 31;
-      const unsigned grp = __match_any_sync(0xffffffffu, put ? patch : -1 - lane);
-      if (put) {
-        const int leader = __ffs(grp) - 1;
-        int32_t rank0 = 0;
-        if (lane == leader) rank0 = atomicAdd(Q.bin_count + patch, __popc(grp));
-        rank0 = __shfl_sync(grp, rank0, leader);
+    if (Q.n_bins && wantN) {
+      rank0 = __shfl_sync(grp, rank0, __ffs(grp) - 1);
+      if (kn < Q.cap)
         Q.nkey[kn] = make_int2(patch, rank0 + __popc(grp & ((1u << lane) - 1u)));
-      }
     }
   }
   warp_sum_u64(&w.counters[CNT_NODES], tested);
@@ -535,7 +538,8 @@ __global__ void __launch_bounds__(256) k_bin_scatter(K3Queues Q) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int2 k = Q.nkey[i];
-    Q.perm[__ldg(Q.bin_off + k.x) + k.y] = (int32_t)i;
+    const int64_t pos = (int64_t)__ldg(Q.bin_off + k.x) + k.y;
+    if (pos < n) Q.perm[pos] = (int32_t)i;
   }
 }
 
