@@ -36,15 +36,38 @@ constexpr int kTileV = 2000;   // vertices per shared-memory tile (3 x 2000 x 8 
 constexpr int kBlockQ = 256;   // queries (threads) per block
 
 // Per-vertex quantities of the shifted fan formula in the round's ray frame
-// (e1, e2, d): d = (0,0,1), so u = r/|r| - d = (rx il, ry il, rz il - 1).
+// (e1, e2, d): d = (0,0,1).  The segment factor den + i num is used only
+// through its argument, so it may carry any positive scale: with the raw
+// offsets r_a = a - p, l_a = |r_a| and u_a = r_a - l_a d (= l_a (a^ - d)),
+//     den' = u_a . u_b = l_a l_b (1 + a^.b^ + b^.c + c.a^),
+//     num' = u_a,y u_b,x - u_a,x u_b,y = l_a l_b c.(a^ x b^),
+// the same expressions as for the unit vectors without the three
+// normalising multiplications per vertex (2 of 23 FP64 operations per
+// segment).  The running product is renormalised (exact power of two) every
+// 8 segments; coordinates up to ~1e18 stay far from overflow.
+#ifndef GWN_K4_UNNORM
+#define GWN_K4_UNNORM 1
+#endif
 struct VtxF {
-  double ux, uy, uz;   // a^ - d in frame coordinates
-  double il;           // 1 / |x - p|
+  double ux, uy, uz;   // GWN_K4_UNNORM: r - l d, else a^ - d (frame coordinates)
+  double il;           // GWN_K4_UNNORM: l = |x - p|, else 1 / |x - p|
 };
 
 // degenerate projection |x - p| < 1e-12 (_kernels.py:541-542): the high word
 // of l2 >= 0 is monotone in l2; hi(1e-24) = 0x3AF357C2
 constexpr int kDegHi = 0x3AF357C2;
+
+// sqrt(x) to full precision from the MUFU.RSQ64H seed y (~2^-22): with
+// h = x y and e = 1 - x y^2, sqrt(x) = h (1 - e)^(-1/2) = h (1 + e/2 + 3e^2/8)
+// (the companion of rsqrt_nr; no special-value path, see there)
+__device__ __forceinline__ double sqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = x * y;
+  const double e = fma(-h, y, 1.0);
+  const double p = fma(0.375, e, 0.5);
+  return fma(h * e, p, h);
+}
 
 __device__ __forceinline__ VtxF make_vtxf(double X, double Y, double Zc, double qa, double qb,
                                           double qc, int& minhi) {
@@ -52,21 +75,37 @@ __device__ __forceinline__ VtxF make_vtxf(double X, double Y, double Zc, double 
   const double rx = X - qa, ry = Y - qb, rz = Zc - qc;
   const double l2 = rx * rx + ry * ry + rz * rz;
   minhi = min(minhi, __double2hiint(l2));
+#if GWN_K4_UNNORM
+  v.il = sqrt_nr(l2);
+  v.ux = rx;
+  v.uy = ry;
+  v.uz = rz - v.il;
+#else
   v.il = rsqrt_nr(l2);
   v.ux = rx * v.il;
   v.uy = ry * v.il;
   v.uz = fma(rz, v.il, -1.0);
+#endif
   return v;
 }
 
 // polyline/curve band test (rare path, den < 0): d within band_factor*h/dist
-// of the arc (a, b); raw offsets are (u + d) / il.
+// of the arc (a, b); `num` is the segment's num as computed from a and b (it
+// carries the scale l_a l_b under GWN_K4_UNNORM, and so does the cross
+// product below: the test is the same).
 __device__ __forceinline__ bool band_hit_f(const VtxF& a, const VtxF& b, double num, double h,
                                            double band_factor) {
+#if GWN_K4_UNNORM
+  const double la = a.il, lb = b.il;
+  const double ax = a.ux, ay = a.uy, az = a.uz + la;   // raw offsets
+  const double bx = b.ux, by = b.uy, bz = b.uz + lb;
+  const double sgx = bx - ax, sgy = by - ay, sgz = bz - az;
+#else
   const double la = 1.0 / a.il, lb = 1.0 / b.il;
   const double ax = a.ux, ay = a.uy, az = a.uz + 1.0;
   const double bx = b.ux, by = b.uy, bz = b.uz + 1.0;
   const double sgx = bx * lb - ax * la, sgy = by * lb - ay * la, sgz = bz * lb - az * la;
+#endif
   const double L = sqrt(sgx * sgx + sgy * sgy + sgz * sgz);
   const double dist = fmin(la, lb) - L;
   if (dist <= 0.0) return true;
@@ -303,8 +342,13 @@ __device__ __forceinline__ void edge_segments(const double* sx, const double* sy
   (void)use;
 }
 
-// rare: some segment of the staged edges had den < 0 -> polyline/curve band
-// test for the lanes concerned, re-walking the staged edges
+// Some segment of the staged edges had den < 0 for some lane: polyline/curve
+// band test for the lanes concerned.  Warp-cooperative: a flagged lane's
+// query is broadcast and the 32 lanes share the staged segments (each segment
+// with the same operations a single lane would use, so the flags are the
+// same).  One lane re-walking every staged edge alone while 31 wait was 12% of
+// k_ff_near's issued instructions at config 5 (ncu: 28.3 active threads per
+// warp).  Every lane of the warp must call this.
 template <int QPT>
 __device__ __forceinline__ void band_rewalk(const double* sx, const double* sy, const double* sz,
                                             int ne, int S, const double* __restrict__ band_h,
@@ -315,21 +359,29 @@ __device__ __forceinline__ void band_rewalk(const double* sx, const double* sy, 
 #pragma unroll
   for (int j = 0; j < QPT; ++j) any |= neg[j] < 0;
   if (!__any_sync(0xffffffffu, any)) return;
+  const int lane = threadIdx.x & 31;
+  const int spe = S - 1, nseg = ne * spe;  // segments per edge, staged segments
 #pragma unroll
   for (int j = 0; j < QPT; ++j) {
-    if (neg[j] >= 0) continue;
-    int mh = 0x7fffffff;
-    for (int e = 0; e < ne; ++e) {
-      const int b = e * S;
-      const double h = __ldg(band_h + e_first + e);
-      VtxF A = make_vtxf(sx[b], sy[b], sz[b], qa[j], qb[j], qc[j], mh);
-      for (int i = b + 1; i < b + S; ++i) {
-        const VtxF B = make_vtxf(sx[i], sy[i], sz[i], qa[j], qb[j], qc[j], mh);
+    unsigned need = __ballot_sync(0xffffffffu, neg[j] < 0);
+    while (need) {
+      const int src = __ffs(need) - 1;
+      need &= need - 1;
+      const double a = __shfl_sync(0xffffffffu, qa[j], src);
+      const double b = __shfl_sync(0xffffffffu, qb[j], src);
+      const double c = __shfl_sync(0xffffffffu, qc[j], src);
+      bool hit = false;
+      int mh = 0x7fffffff;
+      for (int t = lane; t < nseg; t += 32) {
+        const int e = t / spe, i = e * S + (t - e * spe);  // segment (i, i + 1) of edge e
+        const VtxF A = make_vtxf(sx[i], sy[i], sz[i], a, b, c, mh);
+        const VtxF B = make_vtxf(sx[i + 1], sy[i + 1], sz[i + 1], a, b, c, mh);
         const double num = A.uy * B.ux - A.ux * B.uy;
         const double den = A.ux * B.ux + A.uy * B.uy + A.uz * B.uz;
-        if (den < 0.0 && band_hit_f(A, B, num, h, band_factor)) flags[j] |= FLAG_BAND;
-        A = B;
+        if (den < 0.0 && band_hit_f(A, B, num, __ldg(band_h + e_first + e), band_factor))
+          hit = true;
       }
+      if (__any_sync(0xffffffffu, hit) && lane == src) flags[j] |= FLAG_BAND;
     }
     neg[j] = 0;
   }
