@@ -560,69 +560,20 @@ cudaError_t ff_init_constants() {  // per device, before the first far-field lau
 }
 
 // Omega(p) = -sum_{n>=1} [Re(D_n^0 I_n^0) + 2 sum_{m>=1} Re(D_n^m I_n^m)] of
-// order pl (<= P).  Per column m, Clenshaw's backward sum over the
-// three-term recurrence I_{n+1}^m = alpha_n I_n^m + beta_n I_{n-1}^m
+// order P.  Per column m, Clenshaw's backward sum over the three-term
+// recurrence I_{n+1}^m = alpha_n I_n^m + beta_n I_{n-1}^m
 // (alpha_n = (2n+1) z / r^2, beta_n = (m^2 - n^2) / r^2):
 //     b_n = D_n^m + alpha_n b_{n+1} + beta_{n+1} b_{n+2},  sum = b_m I_m^m,
 // six FP64 operations per term (the forward recurrence took ten); checked
 // against the forward sum to 7e-15 relative at 2.4 cycle radii
-// (tools/farfield/fmm_proto.py).  The loops run to the warp's largest order
-// P; a lane's coefficients above its own order pl are zero, so b stays +0
-// there and its sum is bit-identical to an order-pl evaluation whatever its
-// neighbours need.  Runtime loops: one copy of the code for every order.
-__device__ __forceinline__ double ff_eval_rt(double x, double y, double z,
-                                             const double2* __restrict__ Dc, int P, int pl) {
-  const double ir2 = __drcp_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)),
-                                         __dmul_rn(z, z)));
-  const double zr = __dmul_rn(z, ir2);
-  double dR = __dsqrt_rn(ir2), dI = 0.0;  // I_0^0 = 1/r
-  double acc = 0.0;
-#pragma unroll 1
-  for (int mm = 0; mm <= P; ++mm) {
-    if (mm > 0) {  // I_m^m = -(2m-1)(x+iy)/r^2 I_{m-1}^{m-1}
-      const double c0 = __dmul_rn(-(2.0 * mm - 1.0), ir2);
-      const double nR = __dmul_rn(c0, __fma_rn(x, dR, -__dmul_rn(y, dI)));
-      const double nI = __dmul_rn(c0, __fma_rn(x, dI, __dmul_rn(y, dR)));
-      dR = nR;
-      dI = nI;
-    }
-    if (mm > pl) continue;  // the lane's column is empty (warp-uniform loop bounds kept)
-    const double m2r = __dmul_rn((double)(mm * mm), ir2);
-    double b1R = 0.0, b1I = 0.0, b2R = 0.0, b2I = 0.0;
-    const int nlo = mm > 0 ? mm : 1;  // n = 0 has no moment
-#pragma unroll 2
-    for (int n = P; n >= nlo; --n) {
-      const double2 d = __ldg(Dc + ff_term(n, mm));
-      const double cR = n <= pl ? d.x : 0.0, cI = n <= pl ? d.y : 0.0;
-      const double al = __dmul_rn(c_ffc.a[n], zr);
-      const double be = __fma_rn(-c_ffc.sq[n + 1], ir2, m2r);
-      const double bR = __fma_rn(al, b1R, __fma_rn(be, b2R, cR));
-      const double bI = __fma_rn(al, b1I, __fma_rn(be, b2I, cI));
-      b2R = b1R;
-      b2I = b1I;
-      b1R = bR;
-      b1I = bI;
-    }
-    if (mm == 0) {  // b_1 I_1^0 + beta_1 b_2 I_0^0 ... the column starts at n = 1
-      // sum_{n>=1} D_n^0 I_n^0 with the recurrence seeded at I_0^0: the
-      // Clenshaw sum from n = 1 is b_1 I_1^0 + beta_1 b_2 I_0^0, beta_1 = -1/r^2
-      const double i1 = __dmul_rn(zr, dR);  // I_1^0 = z / r^3 = (z/r^2) I_0^0
-      const double col = __fma_rn(b1R, i1, __dmul_rn(__dmul_rn(-ir2, b2R), dR));
-      acc = __dadd_rn(acc, col);
-    } else {
-      const double col = __fma_rn(b1R, dR, -__dmul_rn(b1I, dI));
-      acc = __dadd_rn(acc, __dmul_rn(2.0, col));
-    }
-  }
-  return -acc;
-}
-
-// ff_eval_rt at the lane's own order P = pl (no predication; the far-pair
-// lists give a warp one order), four columns m at a time: they share the
-// loop, the loads of the recurrence constants and alpha_n = (2n+1) z / r^2.
-// Each column runs the same operations in the same order as in ff_eval_rt
-// and the columns are added in increasing m, so the value is bit-identical to
-// ff_eval_rt(x, y, z, Dc, P', P) for any P' >= P.
+// (tools/farfield/fmm_proto.py).  Column m = 0 starts at n = 1 (n = 0 has no
+// moment): its sum is b_1 I_1^0 + beta_1 b_2 I_0^0 with beta_1 = -1/r^2.
+// ff_eval_own runs four columns m at a time: they share the loop, the loads
+// of the recurrence constants and alpha_n, and give the FP64 pipe four
+// independent chains.  Every column's operations and their order depend only
+// on (P, m), and the columns are added in increasing m, so a pair's value is
+// the same bits in every kernel that evaluates it (warp-per-query rounds and
+// the bucketed far pairs).
 struct FFCol {
   double b1R, b1I, b2R, b2I;
 };
@@ -825,15 +776,13 @@ __device__ __forceinline__ double ff_chord_term(const FFRound& R, const FFQuery&
 
 __device__ __forceinline__ double ff_pair_value(const FFRound& R, const FFQuery& Q, int32_t c,
                                                 bool far, int wind, unsigned long long& terms) {
-  int lvl = -1;
-  double x = 1.0, y = 0.0, z = 0.0;
-  if (far) lvl = ff_level_of(R, Q, c, x, y, z);
-  const int wl = __reduce_max_sync(0xffffffffu, (unsigned)(lvl + 1)) - 1;
-  if (wl < 0) return 0.0;
-  const double2* Dc = R.D + (int64_t)(far ? c : 0) * kFFTerms;
-  const int pl = far ? ff_order(lvl) : -1;
-  double v = ff_eval_rt(x, y, z, Dc, ff_order(wl), pl);
   if (!far) return 0.0;
+  double x, y, z;
+  const int pl = ff_order(ff_level_of(R, Q, c, x, y, z));
+  // four columns at a time at the lane's own order (bit-identical to the
+  // one-column evaluation at any warp order, see ff_eval_own; its dependent
+  // chain is 4x shorter, which is what bounds a warp-per-query round)
+  double v = ff_eval_own(x, y, z, R.D + (int64_t)c * kFFTerms, pl);
   terms += (unsigned long long)ff_nterms(pl);
   if (__ldg(R.chord + c) >= 0) v = __dadd_rn(v, ff_chord_term(R, Q, c));
   if (wind) v = __dadd_rn(v, kShadowJump * (double)wind);
@@ -912,7 +861,8 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
           const unsigned long long* __restrict__ eoff, unsigned* __restrict__ efill,
           int2* __restrict__ recs, const unsigned long long* __restrict__ loffs,
           unsigned* __restrict__ lfill, int2* __restrict__ frecs, int32_t* __restrict__ fent,
-          double* __restrict__ row_far, unsigned long long* __restrict__ counters) {
+          double* __restrict__ fpos, double* __restrict__ row_far,
+          unsigned long long* __restrict__ counters) {
   const FFQuery Q = ff_query<kWarp>(m, order, active, pos, f);
   const FFList L = ff_list(F, R.C, Q);
   const int lane = threadIdx.x & 31;
@@ -969,8 +919,15 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
         nsh += cls == 2 ? 1 : 0;
         const int key = ff_level(R, Q, c) * R.C + c;
         const unsigned slot = ff_append(fb, key, lfill);
-        frecs[loffs[key] + slot] = make_int2(Q.s, kf++);
-        fent[loffs[key] + slot] = c;
+        const unsigned long long at = loffs[key] + slot;
+        frecs[at] = make_int2(Q.s, kf++);
+        fent[at] = c;
+        // the query's position travels with the record: k_ff_far_eval reads it
+        // in record order instead of gathering it through slot -> active -> pos
+        // (two dependent loads ahead of every pair: 21% of its stall samples)
+        fpos[3 * at] = Q.px;
+        fpos[3 * at + 1] = Q.py;
+        fpos[3 * at + 2] = Q.pz;
       }
     }
     // the local expansion's value; k_ff_far_sum adds the far pairs in list
@@ -998,10 +955,9 @@ k_ff_fill(int32_t m, const int32_t* __restrict__ order, const int32_t* __restric
 // (ordinal kf of the query's far pairs).
 __global__ void __launch_bounds__(kFFBlock)
 k_ff_far_eval(unsigned long long nrec, const int2* __restrict__ frecs,
-              const int32_t* __restrict__ fent, const int32_t* __restrict__ active,
-              const double* __restrict__ pos, Frame f, FFRound R,
-              const unsigned long long* __restrict__ qfoff, double* __restrict__ fval,
-              unsigned long long* __restrict__ counters) {
+              const int32_t* __restrict__ fent, const double* __restrict__ fpos, Frame f,
+              FFRound R, const unsigned long long* __restrict__ qfoff,
+              double* __restrict__ fval, unsigned long long* __restrict__ counters) {
   // the block's records share one entry almost always (buckets hold
   // thousands): its moments are staged in shared memory, read as broadcasts
   __shared__ double2 sD[kFFTerms];
@@ -1011,6 +967,12 @@ k_ff_far_eval(unsigned long long nrec, const int2* __restrict__ frecs,
   const bool live = r < nrec;
   const int2 rec = live ? frecs[r] : make_int2(0, 0);
   const int32_t c = live ? fent[r] : 0;
+  FFQuery Q;
+  Q.live = live;
+  Q.s = rec.x;
+  Q.px = live ? fpos[3 * r] : 0.0;
+  Q.py = live ? fpos[3 * r + 1] : 0.0;
+  Q.pz = live ? fpos[3 * r + 2] : 0.0;
   if (threadIdx.x == 0) {
     const unsigned long long rl = min(nrec, r0 + blockDim.x) - 1;
     s_c[0] = fent[r0];
@@ -1022,8 +984,10 @@ k_ff_far_eval(unsigned long long nrec, const int2* __restrict__ frecs,
     const double2* src = R.D + (int64_t)s_c[0] * kFFTerms;
     for (int q = threadIdx.x; q < kFFTerms; q += blockDim.x) sD[q] = __ldg(src + q);
   }
+  // where the value goes: loaded ahead of the evaluation, which hides it
+  const unsigned long long dst = live ? qfoff[rec.x] + (unsigned long long)rec.y : 0ull;
   __syncthreads();
-  const FFQuery Q = ff_query_at(live ? rec.x : 0, live ? rec.x + 1 : 0, nullptr, active, pos, f);
+  frame_q(f, Q.px, Q.py, Q.pz, Q.qa, Q.qb, Q.qc);
   unsigned long long terms = 0;
   double v = 0.0;
   if (live) {
@@ -1039,7 +1003,7 @@ k_ff_far_eval(unsigned long long nrec, const int2* __restrict__ frecs,
     ff_class(R, c, Q.qa, Q.qb, Q.qc, wd);
     if (wd) v = __dadd_rn(v, kShadowJump * (double)wd);
   }
-  if (live) fval[qfoff[rec.x] + (unsigned long long)rec.y] = v;
+  if (live) fval[dst] = v;
   unsigned long long nf = live ? 1 : 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1181,6 +1145,7 @@ struct FFCache {
   unsigned long long* loffs = nullptr;   // (kFFLevels*C + 1)
   int2* frecs = nullptr;                 // (far pairs) (slot, ordinal)
   int32_t* fent = nullptr;               // (far pairs) entry
+  double* fpos = nullptr;                // (far pairs, 3) query position of the pair
   double* fval = nullptr;                // (far pairs) values by (query, ordinal)
   void* tmp = nullptr;
   unsigned long long* h = nullptr;       // pinned: [0] pairs, [1] tiles, [2] far pairs
@@ -1190,7 +1155,7 @@ static thread_local FFCache t_ffc[64];
 void release_boundary_caches(int device) {
   FFCache& c = t_ffc[device & 63];
   void* ps[] = {c.qcnt, c.qoff, c.ecnt, c.efill, c.tcnt, c.eoff, c.toff, c.recs, c.ang, c.tmp,
-                c.qfcnt, c.qfoff, c.lcnt, c.lfill, c.loffs, c.frecs, c.fent, c.fval};
+                c.qfcnt, c.qfoff, c.lcnt, c.lfill, c.loffs, c.frecs, c.fent, c.fval, c.fpos};
   for (void* p : ps)
     if (p) cudaFree(p);
   unsigned long long* h = c.h;
@@ -1324,22 +1289,24 @@ static cudaError_t launch_boundary_ff(const gwn_scene* sc, const Round& rd, int3
     FC(ff_grow(c.fent, capf, (size_t)fpairs + 1, sizeof(int32_t), st));
     capf = c.cap_f;
     FC(ff_grow(c.fval, capf, (size_t)fpairs + 1, sizeof(double), st));
+    capf = c.cap_f;
+    FC(ff_grow(c.fpos, capf, (size_t)fpairs + 1, 3 * sizeof(double), st));
     c.cap_f = capf;
   }
   if (evb) FC(cudaEventRecord(evb[0], st));
   if (per_warp)
     k_ff_fill<true><<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, F, c.eoff, c.efill,
-                                            c.recs, c.loffs, c.lfill, c.frecs, c.fent, bpart,
-                                            counters);
+                                            c.recs, c.loffs, c.lfill, c.frecs, c.fent, c.fpos,
+                                            bpart, counters);
   else
     k_ff_fill<false><<<g, kFFBlock, 0, st>>>(m, order, active, pos, rd.f, R, F, c.eoff, c.efill,
-                                             c.recs, c.loffs, c.lfill, c.frecs, c.fent, bpart,
-                                             counters);
+                                             c.recs, c.loffs, c.lfill, c.frecs, c.fent, c.fpos,
+                                             bpart, counters);
   FC(cudaGetLastError());
   if (!per_warp) {
     if (fpairs > 0) {
       k_ff_far_eval<<<(unsigned)((fpairs + kFFBlock - 1) / kFFBlock), kFFBlock, 0, st>>>(
-          fpairs, c.frecs, c.fent, active, pos, rd.f, R, c.qfoff, c.fval, counters);
+          fpairs, c.frecs, c.fent, c.fpos, rd.f, R, c.qfoff, c.fval, counters);
       FC(cudaGetLastError());
     }
     k_ff_far_sum<<<(m + 255) / 256, 256, 0, st>>>(m, c.qfoff, c.fval, bpart);
