@@ -961,7 +961,7 @@ k_ff_far_eval(unsigned long long nrec, const int2* __restrict__ frecs,
   // the block's records share one entry almost always (buckets hold
   // thousands): its moments are staged in shared memory, read as broadcasts
   __shared__ double2 sD[kFFTerms];
-  __shared__ int32_t s_c[2];
+  __shared__ int32_t s_c[1];
   const unsigned long long r0 = (unsigned long long)blockIdx.x * blockDim.x;
   const unsigned long long r = r0 + threadIdx.x;
   const bool live = r < nrec;
@@ -973,13 +973,12 @@ k_ff_far_eval(unsigned long long nrec, const int2* __restrict__ frecs,
   Q.px = live ? fpos[3 * r] : 0.0;
   Q.py = live ? fpos[3 * r + 1] : 0.0;
   Q.pz = live ? fpos[3 * r + 2] : 0.0;
-  if (threadIdx.x == 0) {
-    const unsigned long long rl = min(nrec, r0 + blockDim.x) - 1;
-    s_c[0] = fent[r0];
-    s_c[1] = fent[rl];
-  }
+  if (threadIdx.x == 0) s_c[0] = fent[r0];
   __syncthreads();
-  const bool staged = s_c[0] == s_c[1];
+  // staged only when EVERY record of the block has the first one's entry
+  // (records are ordered by (level, entry): a block over several small
+  // buckets can begin and end in the same entry with others in between)
+  const bool staged = __syncthreads_and(!live || c == s_c[0]) != 0;
   if (staged) {
     const double2* src = R.D + (int64_t)s_c[0] * kFFTerms;
     for (int q = threadIdx.x; q < kFFTerms; q += blockDim.x) sD[q] = __ldg(src + q);

@@ -442,6 +442,60 @@ cudaError_t build_farfield(gwn_scene* sc, const double* ectrl) {
                             sc->ff_D);
   FF(cudaGetLastError());
   FF(cudaDeviceSynchronize());
+  {
+    // Order thresholds from the computed moments.  Truncating entry c at order
+    // p < K drops sum_{n=p+1..K} sum_m D_n^m I_n^m and the part beyond K.  With
+    // |I_n^m(x)| <= sqrt((n-m)! (n+m)!) / |x|^(n+1) (from (n-m)!/(n+m)! P_n^m(t)^2
+    // <= 1; checked in tools/farfield/proto.py) the first part is at most
+    //     sum_{n=p+1..K} T_n / R^(n+1),
+    //     T_n = |D_n^0| n! + 2 sum_{m>=1} |D_n^m| sqrt((n-m)! (n+m)!),
+    // and the second part is ff_bound at order K.  This a-posteriori bound is
+    // far tighter than the a-priori ff_bound at order p (which knows only
+    // A_abs and rho), so far pairs run at lower orders for the same tau; the
+    // smaller of the two radii is used.  R_min (order K) is unchanged.
+    // A tight bound is nearly attained, so these thresholds are solved for
+    // tau / kTailMargin: measured differences from the exact sum then stay
+    // near 1e-12 instead of 1e-10 (config 1), for ~3 more orders per pair.
+    static const bool tail_off = [] {
+      const char* v = getenv("GWN_FF_TAIL");
+      return v && atoi(v) == 0;
+    }();
+    std::vector<double> hD((size_t)2 * kFFTerms * nk);
+    FF(cudaMemcpy(hD.data(), sc->ff_D, sizeof(double) * hD.size(), cudaMemcpyDeviceToHost));
+    std::vector<double> lf(2 * kFFK + 2);  // log k!
+    for (int k = 0; k < (int)lf.size(); ++k) lf[k] = lgamma((double)k + 1.0);
+    for (int c = 0; c < nk && !tail_off; ++c) {
+      const Entry& en = ents[c];
+      if (!en.expand) continue;
+      double T[kFFK + 1] = {0.0};
+      for (int n = 1; n <= kFFK; ++n)
+        for (int m = 0; m <= n; ++m) {
+          const double* d = &hD[2 * ((size_t)c * kFFTerms + ff_term(n, m))];
+          T[n] += (m ? 2.0 : 1.0) * hypot(d[0], d[1]) * exp(0.5 * (lf[n - m] + lf[n + m]));
+        }
+      const double rK = sqrt(lvr[(size_t)c * kFFLevels + kFFLevels - 1]);  // R_min at order K
+      for (int lv = 0; lv < kFFLevels - 1; ++lv) {
+        const int p_ord = ff_order(lv);
+        auto tail = [&](double R) {
+          double sum = ff_bound(en.aabs, en.rho, kFFK, R), pw = pow(R, -(double)(p_ord + 2));
+          for (int n = p_ord + 1; n <= kFFK; ++n, pw /= R) sum += T[n] * pw;
+          return sum;
+        };
+        constexpr double kTailMargin = 16.0;
+        const double tt = tau / kTailMargin;
+        const double r_old = sqrt(lvr[(size_t)c * kFFLevels + lv]);
+        if (!(tail(r_old) <= tt)) continue;  // keep the a-priori radius
+        double lo = rK, hi = r_old;           // tail decreases in R
+        if (tail(lo) <= tt) hi = lo;
+        for (int it = 0; it < 60 && hi > lo; ++it) {
+          const double mid = 0.5 * (lo + hi);
+          (tail(mid) > tt ? lo : hi) = mid;
+        }
+        lvr[(size_t)c * kFFLevels + lv] = hi * hi;
+      }
+    }
+    FF(cudaMemcpy(sc->ff_lv, lvr.data(), sizeof(double) * kFFLevels * nk, cudaMemcpyHostToDevice));
+  }
   sc->ff_n = nk;
   sc->ff_expanded = n_exp;
   sc->ff_g_host = gk;
