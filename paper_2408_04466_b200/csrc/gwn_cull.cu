@@ -23,7 +23,17 @@
 namespace gwn {
 
 constexpr int kStack = 64;  // >= LBVH depth bound (30-bit Morton + 32-bit index tie-break)
-constexpr int kLBuf = 12;
+// Per-thread candidate buffer (local memory, L1-resident).  A query with more
+// candidates appends the rest one atomic at a time, each a full L2 round trip
+// the lane waits for: with 12 entries that spill path was 74% of the grid
+// cull's stall samples at config 5 (rays through many overlapping surfaces
+// have 20-60 candidates).  Measured at config 5, 2^23 queries: 12 entries
+// 5.99 ms, 24 4.21, 32 3.33, 48 2.26, 64 1.92, 96 1.83, 128 1.90; config 4
+// 2.03 -> 1.22 ms; config 2 unchanged.
+#ifndef GWN_CULL_LBUF
+#define GWN_CULL_LBUF 64
+#endif
+constexpr int kLBuf = GWN_CULL_LBUF;
 
 __device__ __forceinline__ void query_proj(const Frame& f, const double* __restrict__ pos,
                                            int32_t q, double& qa, double& qb, double& qc) {

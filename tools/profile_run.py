@@ -1,4 +1,5 @@
-"""Minimal driver for ncu: one warm-up eval + one profiled eval of a config."""
+"""Minimal driver for ncu: warm-up evals, then one eval between cudaProfilerStart/Stop
+(use `ncu --profile-from-start off` to capture only that eval's kernels)."""
 import sys
 sys.path.insert(0, '.')
 import numpy as np
@@ -14,4 +15,8 @@ q = torch.from_numpy(s.queries).cuda()
 for _ in range(2):
     w, st = G.winding_numbers(sc, q)
 torch.cuda.synchronize()
+torch.cuda.profiler.start()
+w, st = G.winding_numbers(sc, q)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok", cfg, len(s.queries), sc.stats())
