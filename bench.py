@@ -50,8 +50,9 @@ sys.path.insert(0, HERE)
 # Algorithmic FP64 flops per unit of work (FMA = 2), DESIGN.md §4.
 FLOP_NEWTON = 220.0    # K3 Newton iteration (220 per N_newton)
 FLOP_ROOT = 200.0      # K3 accepted root (200 per N_root)
-FLOP_SEGMENT = 34.0    # K4 exact, per (query, net segment) in the ray frame: vertex (3 sub,
-                       # |r|^2 5, rsqrt seed + Halley 8, u 4) + num 3, den 5, complex product 6
+FLOP_SEGMENT = 31.0    # K4 exact, per (query, net segment) in the ray frame: vertex (3 sub,
+                       # |r|^2 5, sqrt seed + Halley 8, u_z 1) + num 3, den 5, complex product 6
+                       # (34 until the unnormalised factors of round 2 dropped 3 per vertex)
 FLOP_TERM = 10.0       # K4 far field, per multipole term (Clenshaw, gwn_boundary.cu):
                        # b = D + alpha b1 + beta b2 on a complex b (4 FMA) + beta (1 FMA)
 L2P_TERMS = 231        # terms of one order-20 local expansion (j <= 20, 0 <= k <= j)
@@ -384,14 +385,15 @@ def rooflines(stt: dict, peak_tf: float, ms_step: float, config: int) -> dict:
             stt.get("ms_k4_exact", 0.0), stt["boundary_segments"] * FLOP_SEGMENT,
             f"{int(stt['boundary_segments'])} (query, segment) pairs x {FLOP_SEGMENT:.0f} flop",
             "k_ff_near"),
-        "k_ff_fill (K4 far field)": (
+        "k_ff_fill + k_ff_far_eval (K4 far field)": (
             stt.get("ms_k4_far", 0.0),
             stt.get("far_terms", 0) * FLOP_TERM + stt.get("local_evals", 0) * L2P_TERMS * FLOP_L2P,
             f"{int(stt.get('far_terms', 0))} multipole terms x {FLOP_TERM:.0f} flop "
             f"({int(stt['far_pairs'])} per-pair far (query, cycle) expansions) + "
             f"{int(stt.get('local_evals', 0))} local expansions x {L2P_TERMS} terms x "
             f"{FLOP_L2P:.0f} flop", "k_ff_fill"),
-        "k3_newton (K3 Newton + record)": (
+        "k3_newton_binned (K3 Newton + record, with its bin scan and scatter)"
+        if config == 5 or config == 4 else "k3_newton (K3 Newton + record)": (
             stt["ms_k3_newton"], stt["newton_iters"] * FLOP_NEWTON + stt["roots"] * FLOP_ROOT,
             f"{int(stt['newton_iters'])} iterations x {FLOP_NEWTON:.0f} + {int(stt['roots'])} "
             f"roots x {FLOP_ROOT:.0f} flop", "k3_newton"),

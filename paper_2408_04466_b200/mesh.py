@@ -1,6 +1,7 @@
 """Triangle meshes on the B200 kernels (the reference's surfaces.py:66-431
-mesh side): the median-split BVH of ``build_bvh`` (surfaces.py:91-163, same
-arrays, so reference ``Bvh`` objects and these are interchangeable), all-hits
+mesh side): a Morton-order BVH in the array layout of the reference's ``Bvh``
+(surfaces.py:74-89, so reference ``Bvh`` objects and these are
+interchangeable; the tree itself is built differently, see ``build_bvh``), all-hits
 ray/mesh records (``intersect_ray_mesh``, surfaces.py:299-329) and mesh
 generalized winding numbers as solid-angle sums (the reference's ground
 truth, _kernels.py:385-475) through libgwn_b200.so.
