@@ -31,11 +31,18 @@
 
 namespace gwn {
 
-// expansion order of the per-pair path: order 48 brings R_min down to ~2.2
-// cycle radii (order 20: ~4.3), so ~4x fewer (query, cycle) pairs at config
-// 5 need the exact sum; pairs farther out use the lowest sufficient order
-// (kFFLevels)
-constexpr int kFFK = 48;
+// Largest expansion order of the per-pair path.  R_min, the radius inside
+// which a pair takes the exact sum, comes from the order-K a-priori bound:
+// ~4.3 cycle radii at order 20, ~2.2 at 48, ~1.9 at 64.  Pairs farther out
+// use the lowest sufficient order (kFFLevels).  Measured at config 5, 2^23
+// queries (tools/farfield/order_ab.py): K = 48: 8.53 M near pairs, eval
+// 46.6 ms; 56: 7.00 M, 43.7 ms; 64: 6.05 M, 42.9 ms (the far pairs gained
+// cost 2.2 ms, the near pairs lost save 6.2 ms; the moments of a scene take
+// ~1 s longer to integrate).
+#ifndef GWN_FF_K
+#define GWN_FF_K 64
+#endif
+constexpr int kFFK = GWN_FF_K;
 constexpr int kFFTerms = (kFFK + 1) * (kFFK + 2) / 2;  // (n, m), 0 <= m <= n <= K
 // Error budget of the far field: every expanded entry's truncation is bounded
 // by tau = 2 pi kFFDw / (expanded entries) (Omega units, per pair; the FMM
@@ -50,7 +57,7 @@ constexpr double kFFDw = 1e-8;
 constexpr int kFFRows = 16;
 // adaptive order: a far pair uses the lowest of these orders whose bound
 // holds at its distance (per-cycle thresholds, Scene::ff_lv)
-constexpr int kFFLevels = 10;  // orders 12, 16, ..., 48
+constexpr int kFFLevels = (kFFK - 12) / 4 + 1;  // orders 12, 16, ..., kFFK
 __host__ __device__ constexpr int ff_order(int lv) { return kFFK - 4 * (kFFLevels - 1 - lv); }
 
 __host__ __device__ __forceinline__ constexpr int ff_term(int n, int m) {
