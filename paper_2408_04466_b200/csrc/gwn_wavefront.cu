@@ -736,7 +736,10 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
     const char* e = getenv("GWN_PDL");
     return !(e && atoi(e) == 0);
   }();
-  const bool use_pdl = pdl && !ev4;
+  // (patch-bin scenes: the scan and scatter sit between the fallback and the
+  // Newton pass, so there is no programmatic pair to form; the fallback goes
+  // to the high-priority side stream and overlaps the Newton pass and K4)
+  const bool use_pdl = pdl && !ev4 && !binned;
   cudaStream_t fs = (ev4 || use_pdl) ? st : side;
   if (!ev4 && !use_pdl) {
     if ((e = cudaEventRecord(fork_ev, st)) != cudaSuccess) return e;
