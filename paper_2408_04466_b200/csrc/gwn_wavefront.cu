@@ -810,7 +810,12 @@ K3Queues k3_queues(void* scratch, int64_t cap, unsigned long long* k3cnt, int64_
 #ifndef GWN_NEWTON_BIN
 #define GWN_NEWTON_BIN 1
 #endif
-  if (GWN_NEWTON_BIN && P > kTabMaxP && cap < (1ll << 31)) {
+  // GWN_NEWTON_BIN=0 (environment, tests): the unbinned Newton pass
+  static const bool bin_ok = [] {
+    const char* e = getenv("GWN_NEWTON_BIN");
+    return !(e && atoi(e) == 0);
+  }();
+  if (GWN_NEWTON_BIN && bin_ok && P > kTabMaxP && cap < (1ll << 31)) {
     p += up(sizeof(NewtonItem) * cap);
     q.nkey = (int2*)p;
     p += up(sizeof(int2) * cap);
@@ -828,6 +833,7 @@ K3Queues k3_queues(void* scratch, int64_t cap, unsigned long long* k3cnt, int64_
   return q;
 }
 
+// (sized for the bins whether or not this round uses them)
 size_t intersect_scratch_bytes(int64_t pair_cap, int64_t P) {
   size_t b = (sizeof(int2) + sizeof(NodeItem) + sizeof(NewtonItem)) * pair_cap + 1024;
   if (P > kTabMaxP) b += (sizeof(int2) + sizeof(int32_t)) * pair_cap + 2 * sizeof(int32_t) * P + 1024;

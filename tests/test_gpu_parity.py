@@ -328,7 +328,7 @@ import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 import paper_2408_04466_b200 as G
 from paper_2408_04466_b200 import scenes
-s = scenes.make(int(sys.argv[2]), 1 << 15)
+s = scenes.make(int(sys.argv[2]), int(sys.argv[4]) if len(sys.argv) > 4 else 1 << 15)
 sc = G.Scene(s.ctrl)
 w, st = G.winding_numbers(sc, torch.from_numpy(s.queries).cuda())
 np.save(sys.argv[3], np.stack([w.cpu().numpy(), st.cpu().numpy().astype(np.float64)]))
@@ -368,6 +368,28 @@ def test_newton_shared_table_equals_register_path(tmp_path, cfg):
                        env=env, check=True, timeout=300)
         out[mode] = np.load(f)
     assert np.array_equal(out["1"], out["0"])
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_newton_patch_order_equals_queue_order(tmp_path, cfg):
+    """Scenes beyond the shared-memory table run K3 Newton in patch order
+    (per-patch item bins, k3_newton_binned) in rounds of >= 2^16 queries;
+    GWN_NEWTON_BIN=0 keeps the queue order (k3_newton<false>).  The per-item
+    arithmetic is the same and chi / flags are integer sums, so the results
+    must be bit-identical (the small re-shoot rounds take the unbinned pass in
+    both runs)."""
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("1", "0"):
+        f = str(tmp_path / f"bin{mode}.npy")
+        env = dict(os.environ, GWN_NEWTON_BIN=mode)
+        subprocess.run([sys.executable, "-c", _NEWTON_PATH_SCRIPT, repo, str(cfg), f, str(1 << 18)],
+                       env=env, check=True, timeout=600)
+        out[mode] = np.load(f)
+    assert np.array_equal(out["1"], out["0"])
+    assert (out["1"][1] == 0).mean() > 0.99
 
 
 def _silhouette_points(ctrl, d, n_per_patch=8):
