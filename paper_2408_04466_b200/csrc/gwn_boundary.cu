@@ -723,7 +723,10 @@ __device__ __forceinline__ int32_t ff_entry(const FFList& l, int j) {
 }
 
 constexpr int kFFBlock = 128;
-constexpr int kFFWarpRoundThreads = 148 * 1024;  // rounds up to ~4.7K queries: a warp each
+#ifndef GWN_FF_WARP_QUERIES
+#define GWN_FF_WARP_QUERIES 4736
+#endif
+constexpr int kFFWarpRoundThreads = GWN_FF_WARP_QUERIES * 32;  // rounds up to this many queries: a warp each
 
 // warp-aggregated atomicAdd of 1 per lane on counter[c] (lanes of `mask`
 // with equal c share one atomic); returns the lane's slot
