@@ -116,7 +116,10 @@ typedef struct gwn_stats {
   int64_t boundary_segments;/* (query, net segment) pairs evaluated        */
   int64_t kernel_launches;
   double ms_cull, ms_intersect, ms_boundary, ms_other;  /* event timings, 0 if not timed */
-  double ms_k3_candidates, ms_k3_fallback, ms_k3_newton;  /* split of ms_intersect */
+  double ms_k3_candidates, ms_k3_fallback, ms_k3_newton;  /* split of ms_intersect;
+                                 candidates: the candidate test plus, for scenes past the
+                                 shared-memory patch table, the patch-bin scan and scatter
+                                 that order the Newton queue; newton: the Newton kernel */
   int64_t k3_fallback_items;  /* undecided leaf candidates solved by the DFS fallback */
   int64_t k3_newton_items;    /* certified leaf candidates (Newton solves)          */
   int64_t far_pairs;          /* (query, boundary cycle) pairs taken by the far-field

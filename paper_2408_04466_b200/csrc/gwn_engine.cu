@@ -760,7 +760,8 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
             cudaEventElapsedTime(&a, ev4[0], ev4[1]);
             cudaEventElapsedTime(&b, ev4[1], ev4[2]);
             cudaEventElapsedTime(&c, ev4[4], ev4[3]);
-            stats.ms_k3_candidates += a;
+            cudaEventElapsedTime(&d, ev4[2], ev4[4]);  // patch-bin scan + scatter
+            stats.ms_k3_candidates += a + d;
             stats.ms_k3_fallback += b;
             stats.ms_k3_newton += c;
           }

@@ -761,13 +761,15 @@ cudaError_t launch_intersect(const gwn_scene* sc, const Round& rd, const K3Queue
     return !(e && atoi(e) == 0);
   }();
   const bool tabled = smem_ok && sc->P <= kTabMaxP;
-  // (stage timing: the Newton stage includes its scan and scatter)
-  if (ev4) cudaEventRecord(ev4[4], st);
   if (binned) {  // items in patch order (the fallback runs meanwhile)
     k_bin_scan<<<1, 1024, 0, st>>>(Q.bin_count, Q.bin_off, Q.n_bins);
     k_bin_scatter<<<sc->sm_count * 8, 256, 0, st>>>(Q);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
+  // (stage timing: ev4[2] -> ev4[4] is the bin scan and scatter, which the
+  // engine books with the candidate test -- together they build the Newton
+  // queue; ev4[4] -> ev4[3] is the Newton kernel alone)
+  if (ev4) cudaEventRecord(ev4[4], st);
   if (binned) {
     // (a plain launch: the scan and scatter above sit between the fallback and
     // this kernel, so there is no programmatic pair to form)
