@@ -254,6 +254,7 @@ k_cull(const Node* __restrict__ nodes, const double* __restrict__ leafbox, int64
       int stack[kStack];
       int top = 0;
       int node = 0;
+      bool dropped = false;
       for (;;) {
         const Node& nd = nodes[node];
         int next = -1;
@@ -266,11 +267,15 @@ k_cull(const Node* __restrict__ nodes, const double* __restrict__ leafbox, int64
           if (ch < 0) emit(~ch);
           else if (next < 0) next = ch;
           else if (top < kStack) stack[top++] = ch;
+          else dropped = true;  // unreachable (kStack >= the LBVH depth bound); never silent
         }
         if (next >= 0) node = next;
         else if (top > 0) node = stack[--top];
         else break;
       }
+      // a subtree that could not be stacked: the query takes a new direction
+      // (this thread zeroed flags[s] above; K3 / K4 only OR into it later)
+      if (dropped && z.flags) z.flags[s] = FLAG_RESHOOT;
     }
   }
   // warp-aggregated reservation of the buffered candidates
