@@ -66,3 +66,40 @@ def test_fan_sum_equals_solid_angle_when_line_misses_sphere():
         # proto.k4_fan is K4's fan formula in full angles (the kernel stores halves)
         assert abs(proto.k4_fan(p, V, d) - proto.omega_exact(p, V, g)) < 1e-13
         checked += 1
+
+
+def test_irregular_harmonic_bound_and_tail_bound():
+    """The a-posteriori order thresholds (gwn_farfield.cu): |I_n^m(x)| <=
+    sqrt((n-m)! (n+m)!) / |x|^(n+1), so truncating the expansion at order p < K
+    changes it by at most sum_{n=p+1..K} T_n / R^(n+1) with
+    T_n = |D_n^0| n! + 2 sum_{m>=1} |D_n^m| sqrt((n-m)! (n+m)!)."""
+    from math import factorial, sqrt
+    rng = np.random.default_rng(11)
+    K = 24
+    worst = 0.0
+    for _ in range(40):
+        u = rng.normal(size=3)
+        r = rng.uniform(0.5, 3.0)
+        p = r * u / np.linalg.norm(u)
+        I = proto.irregular(p[0], p[1], p[2], K)
+        for n in range(K + 1):
+            for m in range(n + 1):
+                b = sqrt(factorial(n - m) * factorial(n + m)) / r ** (n + 1)
+                worst = max(worst, abs(I[(n, m)]) / b)
+    assert worst <= 1.0 + 1e-12
+    # the tail bound against the actual difference of two truncations
+    V = proto.loop_of_patch()
+    g, rho, aabs, D = proto.moments(V, K)
+    T = np.zeros(K + 1)
+    for n in range(1, K + 1):
+        for m in range(n + 1):
+            T[n] += (2.0 if m else 1.0) * abs(D[(n, m)]) * sqrt(factorial(n - m) * factorial(n + m))
+    for Rr in (1.5, 2.5, 5.0):
+        R = Rr * rho
+        for pl in (8, 12, 16):
+            tail = sum(T[n] / R ** (n + 1) for n in range(pl + 1, K + 1))
+            for _ in range(6):
+                u = rng.normal(size=3)
+                p = g + R * u / np.linalg.norm(u)
+                diff = abs(proto.omega_mp(p, g, D, K) - proto.omega_mp(p, g, D, pl))
+                assert diff <= tail * (1 + 1e-9) + 1e-18, (Rr, pl, diff, tail)
