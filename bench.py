@@ -55,7 +55,7 @@ FLOP_SEGMENT = 31.0    # K4 exact, per (query, net segment) in the ray frame: ve
                        # (34 until the unnormalised factors of round 2 dropped 3 per vertex)
 FLOP_TERM = 10.0       # K4 far field, per multipole term (Clenshaw, gwn_boundary.cu):
                        # b = D + alpha b1 + beta b2 on a complex b (4 FMA) + beta (1 FMA)
-L2P_TERMS = 231        # terms of one order-20 local expansion (j <= 20, 0 <= k <= j)
+L2P_TERMS = 325        # terms of one order-24 local expansion (j <= 24, 0 <= k <= j)
 FLOP_L2P = 12.0        # per local-expansion term: complex recurrence 8 + multiply-add 4
 
 CONFIG_DESC = {

@@ -66,7 +66,14 @@ __host__ __device__ __forceinline__ constexpr int ff_term(int n, int m) {
 
 // local expansions (gwn_fmm.cu): order of the leaves' expansions, their
 // (j, k >= 0) coefficient count, the irregular-harmonic degree M2L needs
-constexpr int kFmmP = 20;
+// order of the leaves' local expansions.  Measured at config 5, 2^23 queries
+// (tools/farfield/order_ab.py): P = 20: 48.8 M per-pair far pairs, eval
+// 42.6 ms; 24: 43.6 M, 41.7 ms; 28: 42.2 M, 46.3 ms (the L2P grows faster than
+// the leftover pairs shrink).
+#ifndef GWN_FMM_P
+#define GWN_FMM_P 24
+#endif
+constexpr int kFmmP = GWN_FMM_P;
 constexpr int kFmmK = 30;  // multipole order translated by M2L (<= kFFK)
 constexpr int kFmmLT = (kFmmP + 1) * (kFmmP + 2) / 2;
 constexpr int kFmmKT = (kFmmK + 1) * (kFmmK + 2) / 2;

@@ -4,7 +4,7 @@
 // query, the multipole expansion of every far closed cycle: ~840 expansions
 // of ~73 terms per query at config 5, 71% of the step.  Here the cycles'
 // multipoles are translated once per direction round into local expansions
-// on an octree over the scene cube, so a query evaluates ONE order-20 local
+// on an octree over the scene cube, so a query evaluates ONE order-kFmmP local
 // expansion (its leaf's) plus the few cycles its leaf could not take.
 //
 // Math (solid harmonics R, I and moments D as in gwn_farfield.cuh; checked in
