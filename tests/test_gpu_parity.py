@@ -106,6 +106,37 @@ def test_closed_cube_full_size_properties():
     assert np.array_equal(wf[m], -w[: 1 << 18][m])
 
 
+def test_north_star_full_size_properties():
+    """BASELINE config 5 at its full size (15,876 patches, 2^26 queries): the
+    8-GPU layout (eight query slices with global index bases, each a single
+    chunk) gives the same bits as one call (two 2^25-query chunks); the far
+    field's statistics are those of the bench; and flipping every patch's
+    orientation negates w on a 2^22-query slice.  Oracle parity
+    on a subsample of the same scene: test_config_parity_vs_oracle[5]."""
+    s = scenes.make(5)
+    n = len(s.queries)
+    assert n == 1 << 26 and s.ctrl.shape[0] == 15876
+    sc = G.Scene(s.ctrl)
+    q = torch.from_numpy(s.queries).cuda()
+    w, st = G.winding_numbers(sc, q)
+    stt = sc.stats()
+    assert stt["rounds"] >= 2 and stt["near_pairs"] < 1.5 * n < stt["far_pairs"]
+    assert float((st == 0).double().mean()) > 0.9999
+    assert bool(torch.isfinite(w).all()) and float(w.abs().max()) < 16.0
+    per = n // 8
+    for r in range(8):
+        wr, sr = G.winding_numbers(sc, q[r * per:(r + 1) * per], index_base=r * per)
+        assert torch.equal(wr, w[r * per:(r + 1) * per]) and torch.equal(sr, st[r * per:(r + 1) * per])
+    del sc
+    G.release_caches()
+    scf = G.Scene(np.ascontiguousarray(np.swapaxes(s.ctrl, 1, 2)))
+    m = 1 << 22
+    wf, stf = G.winding_numbers(scf, q[:m])
+    ok = (st[:m] == 0) & (stf == 0)
+    assert float(ok.double().mean()) > 0.999
+    assert float((wf + w[:m])[ok].abs().max()) <= W_TOL
+
+
 def test_direction_independence_open_patch():
     s, sc = _scene(1)
     sc2 = G.Scene(s.ctrl, dir_seed=777)
