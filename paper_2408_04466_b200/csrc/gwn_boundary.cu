@@ -462,7 +462,10 @@ constexpr int kQPT = GWN_K4_QPT;
 // 256-thread blocks per SM (config 5 at 2^24: 111.6 -> 104.1 ms against
 // two pairs per thread at two blocks; tools/k4_variants.py)
 constexpr int kNearQPT = 1;
-constexpr int kNearMinBlocks = 4;
+#ifndef GWN_NEAR_MINB
+#define GWN_NEAR_MINB 4
+#endif
+constexpr int kNearMinBlocks = GWN_NEAR_MINB;
 
 // ---------------------------------------------------------------------------
 // Far-field scenes (entries built by gwn_farfield.cu).  Per round and chunk:
