@@ -604,7 +604,7 @@ __device__ __forceinline__ double ff_eval_own(double x, double y, double z,
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       col[i] = FFCol{0.0, 0.0, 0.0, 0.0};
-      m2r[i] = __dmul_rn((double)((m0 + i) * (m0 + i)), ir2);
+      m2r[i] = __dmul_rn(c_ffc.sq[min(m0 + i, kFFK + 1)], ir2);  // (m0 + i)^2 from the table
     }
     // n from P down to m0 + 3: all four columns (when they exist)
     const int nall = m0 + 3;
@@ -636,7 +636,7 @@ __device__ __forceinline__ double ff_eval_own(double x, double y, double z,
       const int mm = m0 + i;
       if (mm > P) break;
       if (mm > 0) {  // I_m^m = -(2m-1)(x+iy)/r^2 I_{m-1}^{m-1}
-        const double c0 = __dmul_rn(-(2.0 * mm - 1.0), ir2);
+        const double c0 = __dmul_rn(-c_ffc.a[mm - 1], ir2);  // -(2 mm - 1) from the table
         const double nR = __dmul_rn(c0, __fma_rn(x, dR, -__dmul_rn(y, dI)));
         const double nI = __dmul_rn(c0, __fma_rn(x, dI, __dmul_rn(y, dR)));
         dR = nR;
