@@ -49,7 +49,13 @@
 
 namespace gwn {
 
-constexpr int kFmmMaxL = 6;       // 8^6 = 262,144 leaves, ~1 GB of coefficients
+#ifndef GWN_FMM_MAXL
+#define GWN_FMM_MAXL 6
+#endif
+#ifndef GWN_FMM_LEAF
+#define GWN_FMM_LEAF 0.6
+#endif
+constexpr int kFmmMaxL = GWN_FMM_MAXL;  // 8^6 = 262,144 leaves, ~1.4 GB of coefficients
 constexpr int kFmmMinCycles = 32;  // fewer closed cycles: the per-pair path alone
 
 // ---------------------------------------------------------------------------
@@ -98,7 +104,7 @@ cudaError_t fmm_setup_scene(gwn_scene* sc, const std::vector<double>& rho,
     sc->fmm_x0[k] = 0.5 * (sc->bbox_min[k] + sc->bbox_max[k]) - 0.5 * sc->fmm_side;
   // leaf side ~0.6 of the median cycle radius (measured best trade between
   // translations and leftover pairs at config 5)
-  const int L = (int)ceil(log2(sc->fmm_side / (0.6 * med)));
+  const int L = (int)ceil(log2(sc->fmm_side / (GWN_FMM_LEAF * med)));
   sc->fmm_L = std::max(2, std::min(kFmmMaxL, L));
   const int nl = sc->fmm_L + 1;
   std::vector<double> dmin((size_t)nk * nl, INFINITY);
