@@ -538,9 +538,13 @@ static int eval_core(gwn_scene* sc, const double* queries, int64_t n, int64_t in
       // parts: measured at config 2 (2^20 queries, pinned host buffers), e2e
       // G q/s: 2 chunks 1.63, 4 1.70, 6 1.79, 8 1.55, 12 1.27 (splitting the
       // last chunk or issuing every input copy up front did not help);
-      // far-field scenes: two (their steps are long next to the copies, and
-      // larger chunks keep the local-expansion leaves' warps uniform)
-      const int64_t np = sc->ff_n > 0 ? 2 : 6;
+      // far-field scenes: three (their steps are long next to the copies, and
+      // larger chunks keep the local-expansion leaves' warps uniform; config 5
+      // at 2^26 queries: 2 chunks 323.1 ms, 3 320.0, 4 321.6)
+#ifndef GWN_PIPE_FF
+#define GWN_PIPE_FF 3
+#endif
+      const int64_t np = sc->ff_n > 0 ? GWN_PIPE_FF : 6;
       const int64_t pc =
           (std::max<int64_t>(1ll << 16, (n + np - 1) / np) + 1023) & ~1023ll;
       cm = std::min(cm, pc);
