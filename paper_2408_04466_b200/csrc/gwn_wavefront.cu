@@ -100,7 +100,10 @@ __device__ __forceinline__ void newton_accept(const WaveArgs& w, int32_t slot, i
 // certified (-> Newton item) or undecided (-> fallback item).
 constexpr int kCandBlock = 256;
 
-__global__ void __launch_bounds__(kCandBlock)
+#ifndef GWN_CAND_MINB
+#define GWN_CAND_MINB 3
+#endif
+__global__ void __launch_bounds__(kCandBlock, GWN_CAND_MINB)
 k3_candidates(const unsigned long long* __restrict__ npairs_dev, K3Queues Q, WaveArgs w) {
   __shared__ BlockPush<kCandBlock / 32> S;
   // launched programmatically behind the cull (GWN_PDL): wait for its results
