@@ -731,6 +731,14 @@ cudaError_t build_round_dir(gwn_scene* sc, const double d[3], Round& rd, cudaStr
       }
       RC(cudaStreamSynchronize(st));
       RC(build_grid(rd, amin, amax, bmin, bmax, st));
+      // First guess of the candidates per query from the grid's fill (config 5:
+      // 14.9 entries per cell, 7.9 candidates per query).  With the default of
+      // 4 the first eval of a dense scene overflowed its candidate buffer:
+      // round 0 ran twice and the 30 GB K3 scratch was re-allocated, 0.75 s of
+      // a 1.5 s first eval.  A wrong guess still only costs that, or memory.
+      if (rd.use_grid && sc->pairs_per_query == 4.0 && !getenv("GWN_PAIRS_INIT"))
+        sc->pairs_per_query =
+            fmax(4.0, 0.55 * (double)rd.grid_entries / ((double)rd.ga * (double)rd.gb));
       RC(build_subleaves(rd, st));
     out:
       if (keys) cudaFree(keys);
